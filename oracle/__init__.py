@@ -1,0 +1,263 @@
+"""CPU oracle -- TEST INFRASTRUCTURE ONLY.
+
+ctypes marshalling around liboracle.so (oracle/oracle.c, plain sequential C,
+-ffp-contract=off).  Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / `--impl reference` legs may import this package; the product
+(paper_1812_05540_b200) never does.  See oracle/oracle.h for the citations.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+_P = C.POINTER
+_I32 = _P(C.c_int32)
+_F64 = _P(C.c_double)
+_U32 = _P(C.c_uint32)
+
+
+class Desc(C.Structure):
+    _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int),
+                ("uu_rowptr", _I32), ("uu_col", _I32), ("uu_val", _F64),
+                ("uf_rowptr", _I32), ("uf_col", _I32), ("uf_val", _F64),
+                ("fu_rowptr", _I32), ("fu_col", _I32), ("fu_val", _F64),
+                ("ff_rowptr", _I32), ("ff_col", _I32), ("ff_val", _F64),
+                ("fs", _F64)]
+
+
+class Opts(C.Structure):
+    _fields_ = [("amg_theta", C.c_double), ("amg_coarse_max", C.c_int), ("amg_max_levels", C.c_int),
+                ("zblock", C.c_int), ("tile_x", C.c_int), ("tile_y", C.c_int), ("tile_z", C.c_int),
+                ("mech_mode", C.c_int), ("pres_mode", C.c_int), ("local_mode", C.c_int), ("ff_mode", C.c_int)]
+
+
+class Info(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("restarts", C.c_int), ("status", C.c_int),
+                ("est_relres", C.c_double), ("true_relres", C.c_double),
+                ("t_setup", C.c_double), ("t_solve", C.c_double)]
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        path = os.path.join(_HERE, "liboracle.so")
+        src = [os.path.join(_HERE, f) for f in ("oracle.c", "oracle.h")]
+        if not os.path.exists(path) or any(os.path.getmtime(s) > os.path.getmtime(path) for s in src):
+            subprocess.check_call(["make", "-s", "-C", os.path.dirname(_HERE), "oracle"])
+        L = C.CDLL(path)
+        L.orc_default_opts.argtypes = [_P(Opts)]
+        L.orc_create.argtypes = [_P(Desc), _P(Opts)]
+        L.orc_create.restype = C.c_void_p
+        L.orc_destroy.argtypes = [C.c_void_p]
+        L.orc_setup.argtypes = [C.c_void_p]
+        L.orc_apply.argtypes = [C.c_void_p, _F64, _F64]
+        L.orc_apply_operator.argtypes = [C.c_void_p, _F64, _F64]
+        L.orc_solve.argtypes = [C.c_void_p, _F64, _F64, C.c_double, C.c_int, C.c_int, _P(Info)]
+        L.orc_num_levels.argtypes = [C.c_void_p, C.c_int]
+        L.orc_level_sizes.argtypes = [C.c_void_p, C.c_int, C.c_int, _P(C.c_int64)]
+        L.orc_level_export.argtypes = [C.c_void_p, C.c_int, C.c_int, _I32, _I32, _F64, _I32, _I32, _I32, _F64, _F64]
+        L.orc_counters.argtypes = [C.c_void_p, _P(C.c_int64)]
+        L.orc_get_spp.argtypes = [C.c_void_p, _F64, _I32, _I32, _F64]
+        L.orc_mis2.argtypes = [C.c_int, _I32, _I32, _U32, C.c_int, _I32, _P(C.c_int)]
+        L.orc_amg_build.argtypes = [C.c_int, C.c_int, _I32, _I32, _F64, _I32, _P(Opts)]
+        L.orc_amg_build.restype = C.c_void_p
+        L.orc_amg_vcycle.argtypes = [C.c_void_p, _F64, _F64]
+        L.orc_amg_levels.argtypes = [C.c_void_p]
+        L.orc_amg_level_sizes.argtypes = [C.c_void_p, C.c_int, _P(C.c_int64)]
+        L.orc_amg_level_export.argtypes = [C.c_void_p, C.c_int, _I32, _I32, _F64, _I32, _I32, _I32, _F64, _F64]
+        L.orc_amg_free.argtypes = [C.c_void_p]
+        L.orc_ilu_build.argtypes = [C.c_int] * 6 + [_I32, _I32, _F64]
+        L.orc_ilu_build.restype = C.c_void_p
+        L.orc_ilu_apply.argtypes = [C.c_void_p, _F64, _F64]
+        L.orc_ilu_free.argtypes = [C.c_void_p]
+        _LIB = L
+    return _LIB
+
+
+def _p(a):
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"]
+    if a.dtype == np.int32:
+        return a.ctypes.data_as(_I32)
+    if a.dtype == np.uint32:
+        return a.ctypes.data_as(_U32)
+    assert a.dtype == np.float64, a.dtype
+    return a.ctypes.data_as(_F64)
+
+
+def default_opts(**kw) -> Opts:
+    o = Opts()
+    lib().orc_default_opts(C.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def _export(sizes_fn, export_fn, lvl):
+    out = (C.c_int64 * 6)()
+    sizes_fn(lvl, out)
+    n, nnz, nagg, pnz, nc, coarsest = list(out)
+    d = dict(n=n, nnz=nnz, nagg=nagg, nc=nc, coarsest=bool(coarsest))
+    d["A_rp"] = np.empty(n + 1, np.int32)
+    d["A_ci"] = np.empty(nnz, np.int32)
+    d["A_v"] = np.empty((nnz, nc))
+    d["dl1"] = np.empty((n, nc))
+    if not coarsest:
+        d["agg"] = np.empty(n, np.int32)
+        d["P_rp"] = np.empty(n + 1, np.int32)
+        d["P_ci"] = np.empty(pnz, np.int32)
+        d["P_v"] = np.empty((pnz, nc))
+    export_fn(lvl, _p(d["A_rp"]), _p(d["A_ci"]), _p(d["A_v"]), _p(d.get("agg")), _p(d.get("P_rp")),
+              _p(d.get("P_ci")), _p(d.get("P_v")), _p(d["dl1"]))
+    return d
+
+
+class Oracle:
+    """One coupled problem (synth.Problem) with the oracle's setup products."""
+
+    def __init__(self, pb, **opts):
+        self.pb = pb
+        self._keep = [np.ascontiguousarray(x) for x in (
+            pb.uu_rowptr, pb.uu_col, pb.uu_val, pb.uf_rowptr, pb.uf_col, pb.uf_val,
+            pb.fu_rowptr, pb.fu_col, pb.fu_val, pb.ff_rowptr, pb.ff_col, pb.ff_val, pb.fs)]
+        k = self._keep
+        d = Desc(pb.nx, pb.ny, pb.nz, *[_p(x) for x in k])
+        self.opts = default_opts(**opts)
+        self.h = lib().orc_create(C.byref(d), C.byref(self.opts))
+        self.n = pb.n
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().orc_destroy(self.h)
+            self.h = None
+
+    def setup(self):
+        rc = lib().orc_setup(self.h)
+        if rc != 0:
+            raise RuntimeError(f"orc_setup failed ({rc})")
+        return self
+
+    def apply(self, v):
+        v = np.ascontiguousarray(v, np.float64)
+        z = np.zeros(self.n)
+        rc = lib().orc_apply(self.h, _p(v), _p(z))
+        if rc != 0:
+            raise RuntimeError(f"orc_apply failed ({rc})")
+        return z
+
+    def operator(self, x):
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.zeros(self.n)
+        lib().orc_apply_operator(self.h, _p(x), _p(y))
+        return y
+
+    def solve(self, b, rtol=1e-8, m=64, maxit=1000):
+        b = np.ascontiguousarray(b, np.float64)
+        x = np.zeros(self.n)
+        info = Info()
+        lib().orc_solve(self.h, _p(b), _p(x), rtol, m, maxit, C.byref(info))
+        return x, dict(iterations=info.iterations, restarts=info.restarts, status=info.status,
+                       est_relres=info.est_relres, true_relres=info.true_relres, t_solve=info.t_solve)
+
+    def num_levels(self, which):
+        return lib().orc_num_levels(self.h, which)
+
+    def level(self, which, lvl):
+        L = lib()
+        return _export(lambda l, o: L.orc_level_sizes(self.h, which, l, o),
+                       lambda l, *a: L.orc_level_export(self.h, which, l, *a), lvl)
+
+    def hierarchy(self, which):
+        return [self.level(which, l) for l in range(self.num_levels(which))]
+
+    def counters(self):
+        out = (C.c_int64 * 4)()
+        lib().orc_counters(self.h, out)
+        return dict(skipped_dss=out[0], perturbed=out[1], fallbacks=out[2])
+
+    def spp(self):
+        pb = self.pb
+        nnz = int(pb.ff_rowptr[-1])
+        Dss = np.empty(pb.Nc)
+        rp = np.empty(pb.Nc + 1, np.int32)
+        ci = np.empty(nnz, np.int32)
+        v = np.empty(nnz)
+        lib().orc_get_spp(self.h, _p(Dss), _p(rp), _p(ci), _p(v))
+        return Dss, rp, ci, v
+
+
+def mis2(rp, ci, hashes, rounds=False):
+    n = len(rp) - 1
+    st = np.empty(n, np.int32)
+    nr = C.c_int(0)
+    lib().orc_mis2(n, _p(np.ascontiguousarray(rp, np.int32)), _p(np.ascontiguousarray(ci, np.int32)),
+                   _p(np.ascontiguousarray(hashes, np.uint32)), int(rounds), _p(st), C.byref(nr))
+    return st, nr.value
+
+
+def fmix32(x):
+    x = np.asarray(x, np.uint64) & 0xFFFFFFFF
+    x ^= x >> 16
+    x = (x * 0x85EBCA6B) & 0xFFFFFFFF
+    x ^= x >> 13
+    x = (x * 0xC2B2AE35) & 0xFFFFFFFF
+    x ^= x >> 16
+    return x.astype(np.uint32)
+
+
+class Amg:
+    """Standalone oracle AMG on a (multi-component) CSR matrix, for pins."""
+
+    def __init__(self, rp, ci, v, zb=None, **opts):
+        self.n = len(rp) - 1
+        v = np.ascontiguousarray(v, np.float64)
+        self.nc = 1 if v.ndim == 1 else v.shape[1]
+        zb = np.zeros(self.n, np.int32) if zb is None else np.ascontiguousarray(zb, np.int32)
+        o = default_opts(**opts)
+        self._keep = (np.ascontiguousarray(rp, np.int32), np.ascontiguousarray(ci, np.int32), v, zb)
+        self.h = lib().orc_amg_build(self.n, self.nc, _p(self._keep[0]), _p(self._keep[1]), _p(v), _p(zb), C.byref(o))
+        if not self.h:
+            raise RuntimeError("orc_amg_build failed")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().orc_amg_free(self.h)
+            self.h = None
+
+    def vcycle(self, b):
+        b = np.ascontiguousarray(b, np.float64)
+        x = np.zeros_like(b)
+        lib().orc_amg_vcycle(self.h, _p(b), _p(x))
+        return x
+
+    def levels(self):
+        L = lib()
+        nl = L.orc_amg_levels(self.h)
+        return [_export(lambda l, o: L.orc_amg_level_sizes(self.h, l, o),
+                        lambda l, *a: L.orc_amg_level_export(self.h, l, *a), l) for l in range(nl)]
+
+
+class Ilu:
+    """Standalone oracle tile ILU(0) on an interleaved 2x2 BSR cell matrix, for pins."""
+
+    def __init__(self, nx, ny, nz, tile, rp, ci, v):
+        self._keep = (np.ascontiguousarray(rp, np.int32), np.ascontiguousarray(ci, np.int32),
+                      np.ascontiguousarray(v, np.float64))
+        self.h = lib().orc_ilu_build(nx, ny, nz, tile[0], tile[1], tile[2], *[_p(x) for x in self._keep])
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().orc_ilu_free(self.h)
+            self.h = None
+
+    def apply(self, w):
+        w = np.ascontiguousarray(w, np.float64)
+        dz = np.zeros_like(w)
+        lib().orc_ilu_apply(self.h, _p(w), _p(dz))
+        return dz

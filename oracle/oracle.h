@@ -1,0 +1,75 @@
+/*
+ * oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, sequential CPU C implementation of the two-stage preconditioner
+ * path (fixed-stress Schur complement + CPR inside flexible GMRES) of
+ * White et al., arXiv 1812.05540.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load it.  It shares no
+ * code with the CUDA library (paper_1812_05540_b200/), and the product never
+ * calls it.  Every function cites the PAPER.md line (P:n) or the DESIGN.md
+ * reading (R-xx, mirroring SURVEY.md D1-D25) it follows.
+ */
+#ifndef TSP_ORACLE_H
+#define TSP_ORACLE_H
+#include <stdint.h>
+
+typedef struct {
+    int nx, ny, nz;               /* grid (cells) */
+    const int32_t *uu_rowptr, *uu_col; const double *uu_val;   /* A_uu BSR 3x3 */
+    const int32_t *uf_rowptr, *uf_col; const double *uf_val;   /* A_uf BSR 3x2 */
+    const int32_t *fu_rowptr, *fu_col; const double *fu_val;   /* A_fu BSR 2x3 */
+    const int32_t *ff_rowptr, *ff_col; const double *ff_val;   /* A_ff BSR 2x2 (s,p) interleaved */
+    const double *fs;             /* (D_sp, D_pp) per cell */
+} orc_desc;
+
+typedef struct {
+    double amg_theta;             /* 0.25 (R-strength) */
+    int amg_coarse_max;           /* 64 */
+    int amg_max_levels;           /* 12 */
+    int zblock;                   /* 16 cell planes (R-zblock) */
+    int tile_x, tile_y, tile_z;   /* 16,16,16 (R-ilu-tile) */
+    int mech_mode;                /* 0: amg(A_uu^SDC) P:515; 1: exact dense A_uu^-1 (pins) */
+    int pres_mode;                /* 0: amg(S_pp) P:599;    1: exact dense S_pp^-1 (pins) */
+    int local_mode;               /* 0: tile ILU(0) P:612;  1: exact (S_ff^FS)^-1; 2: none */
+    int ff_mode;                  /* 0: CPR two-stage (Alg.1 steps 3-8); 1: exact dense S_ff^-1 (eq:LU) */
+} orc_opts;
+
+typedef struct {
+    int iterations, restarts, status;   /* status 0 converged, 1 max iters, 2 breakdown */
+    double est_relres, true_relres;
+    double t_setup, t_solve;
+} orc_info;
+
+typedef struct orc orc;
+
+void orc_default_opts(orc_opts *o);
+orc *orc_create(const orc_desc *d, const orc_opts *o);
+void orc_destroy(orc *h);
+int orc_setup(orc *h);                                    /* rows a1-a5 */
+int orc_apply(orc *h, const double *v, double *z);        /* Algorithm 1 */
+void orc_apply_operator(orc *h, const double *x, double *y);   /* eq:jac_system */
+int orc_solve(orc *h, const double *b, double *x, double rtol, int m, int maxit, orc_info *info);
+/* diagnostics / parity hooks */
+int orc_num_levels(orc *h, int which);                    /* which: 0 mechanics SDC, 1 pressure */
+void orc_level_sizes(orc *h, int which, int lvl, int64_t out[6]); /* n, nnz(A), nagg, nnz(P), nc, coarsest */
+void orc_level_export(orc *h, int which, int lvl, int32_t *A_rp, int32_t *A_ci, double *A_v,
+                      int32_t *agg, int32_t *P_rp, int32_t *P_ci, double *P_v, double *dl1);
+void orc_counters(orc *h, int64_t out[4]);                /* skipped D_ss, perturbed pivots, fallbacks, - */
+void orc_get_spp(orc *h, double *Dss, int32_t *rp, int32_t *ci, double *v);   /* quasi-IMPES products */
+
+/* standalone primitives for pins (tests only) */
+int orc_mis2(int n, const int32_t *rp, const int32_t *ci, const uint32_t *hash, int rounds_variant,
+             int32_t *state_out, int *nrounds);
+void *orc_amg_build(int n, int nc, const int32_t *rp, const int32_t *ci, const double *v, const int32_t *zb,
+                    const orc_opts *o);
+void orc_amg_vcycle(void *hier, const double *b, double *x);    /* nc interleaved components */
+int orc_amg_levels(void *hier);
+void orc_amg_level_sizes(void *hier, int lvl, int64_t out[6]);
+void orc_amg_level_export(void *hier, int lvl, int32_t *A_rp, int32_t *A_ci, double *A_v,
+                          int32_t *agg, int32_t *P_rp, int32_t *P_ci, double *P_v, double *dl1);
+void orc_amg_free(void *hier);
+void *orc_ilu_build(int nx, int ny, int nz, int tx, int ty, int tz, const int32_t *rp, const int32_t *ci,
+                    const double *v);
+void orc_ilu_apply(void *ilu, const double *w, double *dz);
+void orc_ilu_free(void *ilu);
+#endif
