@@ -1,0 +1,175 @@
+/*
+ * tsp.h -- C-ABI of the B200-native two-stage preconditioner library (libtsp.so).
+ *
+ * "tsp" = two-stage preconditioner of White, Castelletto, Klevtsov, Bui,
+ * Osei-Kuffuor, Tchelepi, "A Two-Stage Preconditioner for Multiphase
+ * Poromechanics in Reservoir Simulation", arXiv 1812.05540.  P:n below is
+ * /root/reference/PAPER.md line n (the LaTeX source); R-xx is a reading listed
+ * in DESIGN.md.
+ *
+ * The library applies M^-1 of eq:blk_tr_prec by Algorithm 1
+ * (alg:apply_M_inv) inside right-preconditioned flexible GMRES
+ * on the fully coupled Jacobian of eq:jac_system:
+ *   M_uu^-1 = amg(A_uu^SDC)
+ *   M_ff^-1 = M_G^-1 + M_L^-1 (I - S_ff^FS M_G^-1) (eq:mult_prec_op)
+ *   S_ff^FS = A_ff + diag(D_sp, D_pp)             (eq:Schur_1_FS)
+ *   M_G^-1 with quasi-IMPES S_pp and amg(S_pp)
+ *   M_L^-1 = tile-local block ILU(0)              (R-ilu)
+ * Every step runs in sm_100a CUDA kernels; there is no CPU fallback.
+ *
+ * Conventions (all functions):
+ *  - Vectors are fp64 in the layout [ u : 3*N_n, node-major (x,y,z) | f : 2*N_c,
+ *    cell-major interleaved (s, p) ], i.e. the permutation P of P:606 applied.
+ *    Node (i,j,k) = i + (nx+1)(j + (ny+1)k); cell (i,j,k) = i + nx(j + ny k).
+ *  - Matrices are BSR with int32 row pointers / block column indices (sorted,
+ *    unique per row, structurally symmetric patterns for A_uu and A_ff) and fp64
+ *    row-major blocks.  The caller passes the block-row-scaled Jacobian
+ *    with Dirichlet DoF as identity rows (R-dirichlet).
+ *  - Device pointers are CUDA global-memory pointers valid on the handle's
+ *    device; "host" pointers are ordinary (preferably pinned) host memory.
+ *  - The library never keeps a caller pointer beyond the call (tsp_create deep
+ *    copies).  All device work is ordered on the handle's stream.
+ *  - Errors: every call returns tsp_status; on failure tsp_last_error() gives a
+ *    thread-local message.  A handle is not thread safe.
+ */
+#ifndef TSP_H
+#define TSP_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSP_ABI_VERSION 1
+
+typedef int tsp_status;
+enum {
+    TSP_OK = 0,
+    TSP_NOT_CONVERGED = 1,       /* solve: x holds the last iterate, info filled */
+    TSP_ERR_INVALID_ARG = -1,    /* null pointer, bad sizes, unsorted/duplicate columns, negative fs */
+    TSP_ERR_DIM_MISMATCH = -2,
+    TSP_ERR_STATE = -3,          /* apply/solve before setup */
+    TSP_ERR_CUDA = -4,
+    TSP_ERR_NCCL = -5,
+    TSP_ERR_OOM = -6,
+    TSP_ERR_SINGULAR = -7,       /* coarsest AMG level exceeds the dense limit */
+    TSP_ERR_NUMERIC = -8         /* NaN/Inf in an Arnoldi norm */
+};
+
+typedef struct tsp_ctx *tsp_handle;
+
+typedef struct {
+    double amg_theta;            /* strength threshold, 0.25 (R-strength) */
+    int amg_coarse_max;          /* dense solve at <= this many rows, 64 */
+    int amg_max_levels;          /* 12 */
+    int zblock;                  /* cell planes per z-block for aggregation confinement, 16 (R-zblock) */
+    int tile_x, tile_y, tile_z;  /* ILU(0) tile, 16^3 (R-ilu) */
+    int reserved[8];
+} tsp_options;
+
+/* BSR block matrix given to tsp_create (nrows block rows). */
+typedef struct {
+    const int32_t *rowptr;       /* nrows+1 */
+    const int32_t *col;          /* rowptr[nrows] block columns */
+    const double *val;           /* rowptr[nrows] * bm * bn, row-major blocks */
+} tsp_bsr;
+
+typedef struct {
+    int nx, ny, nz;              /* grid in cells: N_n = (nx+1)(ny+1)(nz+1), N_c = nx ny nz */
+    int rank, nranks;            /* this library build: nranks == 1 (multi-GPU) */
+    void *stream;                /* cudaStream_t to order all work on (0 = legacy default) */
+    int inputs_on_device;        /* 0: all pointers below are host; 1: device */
+    tsp_bsr A_uu;                /* 3x3, N_n block rows, N_n block cols */
+    tsp_bsr A_uf;                /* 3x2 [A_us | A_up], N_n x N_c */
+    tsp_bsr A_fu;                /* 2x3 [A_su ; A_pu], N_c x N_n */
+    tsp_bsr A_ff;                /* 2x2 [[A_ss, A_sp],[A_ps, A_pp]], N_c x N_c */
+    const double *fs_diag;       /* 2*N_c: (D_sp, D_pp) per cell, eq:FS_Dps_Dpp P:435-436, row-scaled */
+    tsp_options opts;
+} tsp_desc;
+
+enum { TSP_SETUP_MECH = 1, TSP_SETUP_FLOW = 2 };
+
+typedef struct {
+    double rtol;                 /* ||b - A x|| <= rtol ||b||, default 1e-8 */
+    int restart;                 /* FGMRES(m), default 64 */
+    int max_iters;               /* default 1000 */
+    int x0_zero;                 /* 1: ignore x on input, start from 0 */
+    int host_ptrs;               /* 1: b and x are host pointers (copies are on the stream) */
+} tsp_solve_opts;
+
+typedef struct {
+    int iterations;              /* preconditioner applications inside Arnoldi */
+    int restarts;
+    int status;                  /* TSP_OK, TSP_NOT_CONVERGED or an error */
+    double est_relres;           /* Arnoldi estimate |g_{j+1}| / ||b|| */
+    double true_relres;          /* recomputed ||b - A x|| / ||b|| at exit */
+    double t_solve_s;
+} tsp_solve_info;
+
+typedef struct {
+    int levels[2];               /* [0] mechanics SDC hierarchy, [1] pressure hierarchy */
+    int64_t rows[2][16], nnz[2][16];
+    int64_t launches;            /* kernels launched by this handle since the last reset */
+    int64_t skipped_dss, perturbed_pivots, coarsening_fallbacks;
+    double bytes_apply;          /* algorithmic bytes of one tsp_apply_preconditioner */
+    double bytes_operator;       /* algorithmic bytes of one tsp_apply_operator */
+    double bytes_iter_base;      /* per FGMRES iteration excluding the Krylov-index-dependent part */
+    double bytes_per_krylov_vec; /* CGS2 bytes added per basis vector (x (j+1)) */
+} tsp_stats;
+
+/* per-kernel-class timing (CUDA events on the handle's stream), for roofline */
+#define TSP_PROF_MAX 32
+typedef struct {
+    int nclasses;
+    char name[TSP_PROF_MAX][24];
+    int64_t launches[TSP_PROF_MAX];
+    double ms[TSP_PROF_MAX];       /* summed device time */
+    double bytes[TSP_PROF_MAX];    /* summed algorithmic bytes */
+} tsp_prof;
+
+int tsp_abi_version(void);
+const char *tsp_last_error(void);
+tsp_status tsp_default_options(tsp_options *o);
+
+/* Validates, deep-copies the blocks into library-owned device memory and
+ * repacks them (sliced-ELL, R-layout).  The caller may free its inputs after
+ * return.  Returns TSP_ERR_INVALID_ARG on null/unsorted/inconsistent input. */
+tsp_status tsp_create(tsp_handle *out, const tsp_desc *d);
+
+/* TSP_SETUP_MECH: rows a2 + a4 (SDC extraction, mechanics AMG), once per
+ * simulation.  TSP_SETUP_FLOW: rows a1 + a3 + a4 (pressure) + a5
+ * (fixed stress, quasi-IMPES, pressure AMG, tile ILU(0)), per Newton step
+ * (P:519).  Synchronises the stream. */
+tsp_status tsp_setup(tsp_handle h, unsigned what);
+
+/* z = M^-1 v (Algorithm 1).  Device pointers, length n = 3 N_n + 2 N_c, must
+ * not alias.  Asynchronous on the handle's stream. */
+tsp_status tsp_apply_preconditioner(tsp_handle h, const double *v, double *z);
+
+/* y = A x with the original Jacobian (row a12).  Device pointers, asynchronous. */
+tsp_status tsp_apply_operator(tsp_handle h, const double *x, double *y);
+
+/* Right-preconditioned FGMRES(m) with CGS2 Arnoldi.  Returns TSP_OK,
+ * TSP_NOT_CONVERGED (x = last iterate) or an error.  Synchronises. */
+tsp_status tsp_solve(tsp_handle h, const double *b, double *x, const tsp_solve_opts *o, tsp_solve_info *info);
+void tsp_default_solve_opts(tsp_solve_opts *o);
+
+tsp_status tsp_get_stats(tsp_handle h, tsp_stats *s);
+
+/* Test hook (row c.5 parity): copy level `lvl` of hierarchy `which` (0 mech, 1
+ * pressure) to host buffers.  Sizes: out6 = {n, nnz(A), nagg, nnz(P), nc,
+ * coarsest}.  Any buffer may be NULL; A_v/P_v/dl1 are [entry][nc]. */
+tsp_status tsp_level_sizes(tsp_handle h, int which, int lvl, int64_t out6[6]);
+tsp_status tsp_export_level(tsp_handle h, int which, int lvl, int32_t *A_rp, int32_t *A_ci, double *A_v,
+                            int32_t *agg, int32_t *P_rp, int32_t *P_ci, double *P_v, double *dl1);
+
+tsp_status tsp_prof_enable(tsp_handle h, int on);   /* also resets */
+tsp_status tsp_prof_read(tsp_handle h, tsp_prof *p);  /* synchronises */
+
+void tsp_destroy(tsp_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

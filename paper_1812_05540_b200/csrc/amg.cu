@@ -1,0 +1,760 @@
+// amg.cu -- row a4 (AMG setup on the GPU) and rows a6/a9 (V-cycles).
+//
+// Method (DESIGN.md R-amg, R-strength, R-mis2, R-agg, R-prolong, R-rap,
+// R-cycle): smoothed aggregation with MIS(2) aggregates,
+// Galerkin R = P^T, one V(1,1) l1-Jacobi cycle, dense coarsest solve.  The
+// setup is bit-identical to the oracle: every floating-point sum is a left fold
+// in the oracle's canonical order with IEEE round-to-nearest intrinsics
+// (__dadd_rn/__dmul_rn/__ddiv_rn, no FMA contraction) and no atomics on values.
+// Apply kernels are free (FMA, any order).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "tsp_internal.cuh"
+
+namespace tsp {
+
+__device__ __forceinline__ uint32_t fmix32(uint32_t x)
+{
+    x ^= x >> 16; x *= 0x85ebca6bU; x ^= x >> 13; x *= 0xc2b2ae35U; x ^= x >> 16;
+    return x;
+}
+__device__ __forceinline__ uint64_t prio(int i) { return ((uint64_t)fmix32((uint32_t)i) << 32) | (uint64_t)(uint32_t)i; }
+
+// ------------------------------------------------------------------ l1 norms: d_i = fold_j |a_ij|
+__global__ void k_l1(int n, int nc, const int32_t *__restrict__ rp, const double *__restrict__ v, double *dl1, double *dinv)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int c = 0; c < nc; ++c) {
+        double s = 0.0;
+        for (int64_t q = rp[i]; q < rp[i + 1]; ++q) s = __dadd_rn(s, fabs(v[q * nc + c]));
+        dl1[(int64_t)i * nc + c] = s;
+        dinv[(int64_t)i * nc + c] = s != 0.0 ? 1.0 / s : 0.0;
+    }
+}
+
+__device__ __forceinline__ double meas(const double *__restrict__ v, int64_t q, int nc)
+{
+    double s = 0.0;
+    for (int c = 0; c < nc; ++c) s = __dadd_rn(s, fabs(v[q * nc + c]));
+    return s;
+}
+
+// ------------------------------------------------------------------ strength (R-strength)
+__global__ void k_strength(int n, int nc, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                           const double *__restrict__ v, const int32_t *__restrict__ zb, double theta, uint8_t *S)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double m = 0.0;
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q)
+        if (ci[q] != i) { double t = meas(v, q, nc); if (t > m) m = t; }
+    double thr = __dmul_rn(theta, m);
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+        int j = ci[q];
+        S[q] = (j != i && m > 0.0 && zb[i] == zb[j] && meas(v, q, nc) >= thr) ? 1 : 0;
+    }
+}
+
+__global__ void k_symm(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const uint8_t *__restrict__ S,
+                       uint8_t *E, int *err)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+        int j = ci[q];
+        if (j == i) { E[q] = 0; continue; }
+        int64_t lo = rp[j], hi = rp[j + 1] - 1, qt = -1;
+        while (lo <= hi) {
+            int64_t mid = (lo + hi) >> 1;
+            int cm = ci[mid];
+            if (cm == i) { qt = mid; break; }
+            if (cm < i) lo = mid + 1; else hi = mid - 1;
+        }
+        if (qt < 0) { *err = 1; E[q] = 0; continue; }
+        E[q] = (S[q] || S[qt]) ? 1 : 0;
+    }
+}
+
+// ------------------------------------------------------------------ MIS(2) rounds (R-mis2)
+enum { ST_ISO = -1, ST_UND = 0, ST_ROOT = 1, ST_OUT = 2 };
+
+__global__ void k_mis_init(int n, const int32_t *__restrict__ rp, const uint8_t *__restrict__ E, int8_t *st)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int d = 0;
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) d |= E[q];
+    st[i] = d ? ST_UND : ST_ISO;
+}
+__global__ void k_mis_t1(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const uint8_t *__restrict__ E,
+                         const int8_t *__restrict__ st, uint64_t *t1)
+{
+    int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= n) return;
+    uint64_t m = st[x] == ST_UND ? prio(x) + 1 : 0;
+    for (int64_t q = rp[x]; q < rp[x + 1]; ++q)
+        if (E[q]) { int u = ci[q]; if (st[u] == ST_UND) { uint64_t p = prio(u) + 1; if (p > m) m = p; } }
+    t1[x] = m;
+}
+__global__ void k_mis_root(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const uint8_t *__restrict__ E,
+                           const int8_t *__restrict__ st, const uint64_t *__restrict__ t1, uint8_t *newr)
+{
+    int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    uint8_t r = 0;
+    if (st[v] == ST_UND) {
+        uint64_t m = t1[v];
+        for (int64_t q = rp[v]; q < rp[v + 1]; ++q) if (E[q]) { uint64_t t = t1[ci[q]]; if (t > m) m = t; }
+        r = (m == prio(v) + 1);
+    }
+    newr[v] = r;
+}
+__global__ void k_mis_near(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const uint8_t *__restrict__ E,
+                           const uint8_t *__restrict__ newr, int8_t *st, uint8_t *near1)
+{
+    int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= n) return;
+    uint8_t h = newr[x];
+    for (int64_t q = rp[x]; q < rp[x + 1] && !h; ++q) if (E[q] && newr[ci[q]]) h = 1;
+    near1[x] = h;
+    if (newr[x]) st[x] = ST_ROOT;
+}
+__global__ void k_mis_out(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const uint8_t *__restrict__ E,
+                          const uint8_t *__restrict__ near1, int8_t *st, unsigned long long *undecided)
+{
+    int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    if (st[v] != ST_UND) return;
+    uint8_t h = near1[v];
+    for (int64_t q = rp[v]; q < rp[v + 1] && !h; ++q) if (E[q] && near1[ci[q]]) h = 1;
+    if (h) st[v] = ST_OUT;
+    else atomicAdd(undecided, 1ULL);
+}
+
+// ------------------------------------------------------------------ aggregates (R-agg)
+__global__ void k_rootflag(int n, const int8_t *__restrict__ st, int32_t *flag)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = st[i] == ST_ROOT;
+}
+__global__ void k_phase1(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const uint8_t *__restrict__ E,
+                         const int8_t *__restrict__ st, const int32_t *__restrict__ rid, const int32_t *__restrict__ zb,
+                         int32_t *agg, int32_t *zbc)
+{
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n || st[r] != ST_ROOT) return;
+    int a = rid[r];
+    agg[r] = a;
+    zbc[a] = zb[r];
+    for (int64_t q = rp[r]; q < rp[r + 1]; ++q) if (E[q]) agg[ci[q]] = a;
+}
+__global__ void k_phase2(int n, int nc, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const double *__restrict__ v,
+                         const uint8_t *__restrict__ E, const int8_t *__restrict__ st, const int32_t *__restrict__ ph1, int32_t *agg)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (st[i] == ST_ISO || ph1[i] >= 0) { agg[i] = ph1[i]; return; }
+    int best = -1; double bw = 0.0;
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+        if (!E[q]) continue;
+        int a = ph1[ci[q]];
+        if (a < 0) continue;
+        double w = meas(v, q, nc);
+        if (best < 0 || w > bw || (w == bw && a < best)) { best = a; bw = w; }
+    }
+    agg[i] = best;
+}
+
+// ------------------------------------------------------------------ smoothed prolongator (R-prolong)
+// d_i = a_ii + fold_{weak j} a_ij ; ratio_i = fold_j |a^F_ij| / |d_i|
+__global__ void k_pdiag(int n, int nc, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const double *__restrict__ v,
+                        const uint8_t *__restrict__ E, double *d, unsigned long long *rho_bits)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t qd = -1;
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) if (ci[q] == i) { qd = q; break; }
+    for (int c = 0; c < nc; ++c) {
+        double di = qd >= 0 ? v[qd * nc + c] : 0.0;
+        for (int64_t q = rp[i]; q < rp[i + 1]; ++q)
+            if (ci[q] != i && !E[q]) di = __dadd_rn(di, v[q * nc + c]);
+        d[(int64_t)i * nc + c] = di;
+        if (di == 0.0) continue;
+        double s = 0.0;
+        for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+            double a = (ci[q] == i) ? di : (E[q] ? v[q * nc + c] : 0.0);
+            s = __dadd_rn(s, fabs(a));
+        }
+        double r = __ddiv_rn(s, fabs(di));
+        atomicMax(rho_bits + c, (unsigned long long)__double_as_longlong(r));   // r >= 0: bit order = value order
+    }
+}
+
+#define PMAX 512
+__device__ int collect_aggs(int i, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const uint8_t *__restrict__ E,
+                            const int32_t *__restrict__ agg, int32_t *tmp, int *overflow)
+{
+    int cnt = 0;
+    if (agg[i] < 0) return 0;
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+        int j = ci[q];
+        if ((j == i || E[q]) && agg[j] >= 0) {
+            int a = agg[j];
+            bool dup = false;
+            for (int t = 0; t < cnt; ++t) if (tmp[t] == a) { dup = true; break; }
+            if (dup) continue;
+            if (cnt >= PMAX) { *overflow = 1; break; }
+            int t = cnt++;
+            while (t > 0 && tmp[t - 1] > a) { tmp[t] = tmp[t - 1]; --t; }   // insertion sort
+            tmp[t] = a;
+        }
+    }
+    return cnt;
+}
+__global__ void k_pcount(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const uint8_t *__restrict__ E,
+                         const int32_t *__restrict__ agg, int32_t *cnt, int *overflow)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int32_t tmp[PMAX];
+    cnt[i] = collect_aggs(i, rp, ci, E, agg, tmp, overflow);
+}
+struct Omega { double w[3]; };
+__global__ void k_pfill(int n, int nc, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const double *__restrict__ v,
+                        const uint8_t *__restrict__ E, const int32_t *__restrict__ agg, const double *__restrict__ d, Omega om,
+                        const int32_t *__restrict__ prp, int32_t *pci, double *pv, int *overflow)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int32_t tmp[PMAX];
+    int cnt = collect_aggs(i, rp, ci, E, agg, tmp, overflow);
+    int64_t o = prp[i];
+    for (int t = 0; t < cnt; ++t) {
+        int J = tmp[t];
+        pci[o + t] = J;
+        for (int c = 0; c < nc; ++c) {
+            double di = d[(int64_t)i * nc + c];
+            double w = (di != 0.0) ? __ddiv_rn(om.w[c], di) : 0.0;
+            double s = 0.0;
+            for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+                int j = ci[q];
+                if (!((j == i) || E[q]) || agg[j] != J) continue;
+                double a = (j == i) ? di : v[q * nc + c];
+                s = __dadd_rn(s, a);
+            }
+            double delta = (J == agg[i]) ? 1.0 : 0.0;
+            pv[(o + t) * nc + c] = __dsub_rn(delta, __dmul_rn(w, s));
+        }
+    }
+}
+
+// ------------------------------------------------------------------ transpose helpers
+__global__ void k_expand_rows(int n, const int32_t *__restrict__ rp, int32_t *row)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) row[q] = i;
+}
+__global__ void k_iota(int64_t n, int32_t *a)
+{
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) a[i] = (int32_t)i;
+}
+__global__ void k_col_count(int64_t nnz, const int32_t *__restrict__ ci, int32_t *cnt)
+{
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q < nnz) atomicAdd(cnt + ci[q], 1);
+}
+__global__ void k_transpose_fill(int64_t nnz, int nc, const int32_t *__restrict__ perm, const int32_t *__restrict__ row,
+                                 const double *__restrict__ pv, int32_t *rci, double *rv)
+{
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= nnz) return;
+    int q = perm[t];
+    rci[t] = row[q];
+    for (int c = 0; c < nc; ++c) rv[t * nc + c] = pv[(int64_t)q * nc + c];
+}
+
+// ------------------------------------------------------------------ deterministic SpGEMM (R-rap)
+// C = X Y; C_ik = fold over X's row i (ascending) of x_ij * y_jk, starting at 0.0.
+// One warp per row; the X row is walked sequentially (canonical order), lanes
+// split Y's row j (unique columns, so no two lanes touch one accumulator).
+template <int NC, int HS>
+__global__ void k_spgemm(int n, const int32_t *__restrict__ xrp, const int32_t *__restrict__ xci, const double *__restrict__ xv,
+                         const int32_t *__restrict__ yrp, const int32_t *__restrict__ yci, const double *__restrict__ yv,
+                         int fill, int32_t *cnt, const int32_t *__restrict__ crp, int32_t *cci, double *cv, int *overflow)
+{
+    extern __shared__ unsigned char smraw[];
+    const int wpb = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int *keys = (int *)smraw + w * HS;
+    double *acc = (double *)(smraw + (size_t)wpb * HS * sizeof(int)) + (size_t)w * HS * NC;
+    for (int i = blockIdx.x * wpb + w; i < n; i += gridDim.x * wpb) {
+        for (int t = lane; t < HS; t += 32) keys[t] = -1;
+        __syncwarp();
+        int nfull = 0;
+        for (int64_t q = xrp[i]; q < xrp[i + 1]; ++q) {
+            const int j = xci[q];
+            double xq[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) xq[c] = xv[q * NC + c];
+            for (int64_t p = yrp[j] + lane; p < yrp[j + 1]; p += 32) {
+                const int k = yci[p];
+                unsigned h = ((unsigned)k * 2654435761u) & (HS - 1);
+                int probes = 0;
+                for (;;) {
+                    int old = atomicCAS(&keys[h], -1, k);
+                    if (old == -1) {
+#pragma unroll
+                        for (int c = 0; c < NC; ++c) acc[h * NC + c] = 0.0;
+                        break;
+                    }
+                    if (old == k) break;
+                    h = (h + 1) & (HS - 1);
+                    if (++probes >= HS) { nfull = 1; break; }
+                }
+                if (nfull) break;
+                if (fill) {
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) acc[h * NC + c] = __dadd_rn(acc[h * NC + c], __dmul_rn(xq[c], yv[p * NC + c]));
+                }
+            }
+            __syncwarp();
+        }
+        // count occupied slots
+        int mine = 0;
+        for (int t = lane; t < HS; t += 32) mine += keys[t] >= 0;
+        for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+        if (__any_sync(0xffffffffu, nfull) || mine > (HS * 3) / 4) { if (lane == 0) *overflow = 1; }
+        if (!fill) {
+            if (lane == 0) cnt[i] = mine;
+        } else {
+            const int64_t base = crp[i];
+            for (int t = lane; t < HS; t += 32) {
+                int k = keys[t];
+                if (k < 0) continue;
+                int rank = 0;
+                for (int u = 0; u < HS; ++u) { int kk = keys[u]; rank += (kk >= 0 && kk < k); }
+                cci[base + rank] = k;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) cv[(base + rank) * NC + c] = acc[t * NC + c];
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------ coarsest dense LU -> inverse (one CTA per component)
+// LU with partial pivoting, pivot = first maximal |a| in the column (lowest row on ties),
+// zero pivot -> 1e-12 * max|A| (R-coarse).  Then inverse columns by forward/back substitution.
+__global__ void k_dense_inv(int n, int nc, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const double *__restrict__ v,
+                            double *work, int *piv, double *inv, unsigned long long *npert)
+{
+    const int c = blockIdx.x;
+    double *a = work + (size_t)c * n * n;
+    int *pv = piv + (size_t)c * n;
+    double *out = inv + (size_t)c * n * n;
+    for (int64_t t = threadIdx.x; t < (int64_t)n * n; t += blockDim.x) a[t] = 0.0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        for (int64_t q = rp[i]; q < rp[i + 1]; ++q) a[(int64_t)i * n + ci[q]] = v[q * nc + c];
+    __syncthreads();
+    __shared__ double s_scale;
+    __shared__ int s_p;
+    if (threadIdx.x == 0) {
+        double sc = 0.0;
+        for (int64_t t = 0; t < (int64_t)n * n; ++t) sc = fmax(sc, fabs(a[t]));
+        s_scale = sc == 0.0 ? 1.0 : sc;
+    }
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+        if (threadIdx.x == 0) {
+            int p = k; double best = fabs(a[(int64_t)k * n + k]);
+            for (int i = k + 1; i < n; ++i) { double t = fabs(a[(int64_t)i * n + k]); if (t > best) { best = t; p = i; } }
+            s_p = p; pv[k] = p;
+        }
+        __syncthreads();
+        int p = s_p;
+        if (p != k)
+            for (int j = threadIdx.x; j < n; j += blockDim.x) { double t = a[(int64_t)k * n + j]; a[(int64_t)k * n + j] = a[(int64_t)p * n + j]; a[(int64_t)p * n + j] = t; }
+        __syncthreads();
+        if (threadIdx.x == 0 && a[(int64_t)k * n + k] == 0.0) { a[(int64_t)k * n + k] = 1e-12 * s_scale; atomicAdd(npert, 1ULL); }
+        __syncthreads();
+        double dkk = a[(int64_t)k * n + k];
+        for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) a[(int64_t)i * n + k] /= dkk;
+        __syncthreads();
+        for (int64_t t = threadIdx.x; t < (int64_t)(n - k - 1) * (n - k - 1); t += blockDim.x) {
+            int i = k + 1 + (int)(t / (n - k - 1)), j = k + 1 + (int)(t % (n - k - 1));
+            a[(int64_t)i * n + j] -= a[(int64_t)i * n + k] * a[(int64_t)k * n + j];
+        }
+        __syncthreads();
+    }
+    // inverse: column e of A^-1 solves A x = e_e (row swaps applied in order)
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        double *x = out + (size_t)e;   // column e, stride n: out[i*n + e]
+        for (int i = 0; i < n; ++i) x[(size_t)i * n] = (i == e) ? 1.0 : 0.0;
+        for (int k = 0; k < n; ++k) if (pv[k] != k) { double t = x[(size_t)k * n]; x[(size_t)k * n] = x[(size_t)pv[k] * n]; x[(size_t)pv[k] * n] = t; }
+        for (int i = 0; i < n; ++i) { double s = x[(size_t)i * n]; for (int j = 0; j < i; ++j) s -= a[(int64_t)i * n + j] * x[(size_t)j * n]; x[(size_t)i * n] = s; }
+        for (int i = n - 1; i >= 0; --i) { double s = x[(size_t)i * n]; for (int j = i + 1; j < n; ++j) s -= a[(int64_t)i * n + j] * x[(size_t)j * n]; x[(size_t)i * n] = s / a[(int64_t)i * n + i]; }
+    }
+}
+
+// ------------------------------------------------------------------ host helpers
+template <class T>
+static void exclusive_scan(Ctx &c, const T *in, T *out, int64_t n)
+{
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, c.s);
+    void *t = scratch(c, tb);
+    cub::DeviceScan::ExclusiveSum(t, tb, in, out, n, c.s);
+}
+template <class T>
+static T d2h1(Ctx &c, const T *p)
+{
+    T v;
+    TSP_CUDA(cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, c.s));
+    TSP_CUDA(cudaStreamSynchronize(c.s));
+    return v;
+}
+
+// rp from per-row counts (n+1 entries, counts in [0,n), last = 0)
+static int64_t rowptr_from_counts(Ctx &c, DBuf<int32_t> &cnt, DBuf<int32_t> &rp, int n)
+{
+    TSP_CUDA(cudaMemsetAsync(cnt.p + n, 0, sizeof(int32_t), c.s));
+    rp.alloc(n + 1);
+    exclusive_scan<int32_t>(c, cnt, rp, n + 1);
+    return d2h1(c, rp.p + n);
+}
+
+static void spgemm(Ctx &c, const Csr &X, const Csr &Y, Csr &C, int nc)
+{
+    C.n = X.n; C.m = Y.m; C.nc = nc;
+    DBuf<int32_t> cnt; cnt.alloc(X.n + 1);
+    DBuf<int> ovf; ovf.alloc(1);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        ovf.zero(c.s);
+        const int HS = attempt == 0 ? 512 : 4096;
+        const int wpb = attempt == 0 ? 4 : 1;
+        size_t smem = (size_t)wpb * HS * (sizeof(int) + sizeof(double) * nc);
+        int grid = std::max(1, std::min(grid_for(X.n, wpb), c.sm_count * 32));
+        auto launch = [&](int fill) {
+#define SPG(NCV, HSV)                                                                                                     \
+    do {                                                                                                                  \
+        cudaFuncSetAttribute(k_spgemm<NCV, HSV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                 \
+        k_spgemm<NCV, HSV><<<grid, 32 * wpb, smem, c.s>>>(X.n, X.rp, X.ci, X.v, Y.rp, Y.ci, Y.v, fill, cnt, C.rp, C.ci,   \
+                                                          C.v, ovf);                                                      \
+    } while (0)
+            if (nc == 1 && HS == 512) SPG(1, 512);
+            else if (nc == 1) SPG(1, 4096);
+            else if (HS == 512) SPG(3, 512);
+            else SPG(3, 4096);
+#undef SPG
+            TSP_CUDA(cudaGetLastError());
+            c.launches++;
+        };
+        launch(0);
+        if (d2h1(c, ovf.p)) continue;
+        C.nnz = rowptr_from_counts(c, cnt, C.rp, X.n);
+        C.ci.alloc(C.nnz); C.v.alloc(C.nnz * nc);
+        launch(1);
+        TSP_REQUIRE(!d2h1(c, ovf.p), TSP_ERR_INVALID_ARG, "spgemm: row too dense");
+        return;
+    }
+    throw Error{TSP_ERR_INVALID_ARG, "spgemm: coarse row exceeds 3072 distinct columns"};
+}
+
+static void transpose(Ctx &c, const Csr &P, Csr &R, int nc)
+{
+    R.n = P.m; R.m = P.n; R.nc = nc; R.nnz = P.nnz;
+    DBuf<int32_t> row, keys_out, perm_in, perm_out, cnt;
+    row.alloc(P.nnz + 1); keys_out.alloc(P.nnz + 1); perm_in.alloc(P.nnz + 1); perm_out.alloc(P.nnz + 1);
+    cnt.alloc(R.n + 1); cnt.zero(c.s);
+    if (P.nnz) {
+        k_expand_rows<<<grid_for(P.n, 256), 256, 0, c.s>>>(P.n, P.rp, row);
+        k_iota<<<grid_for(P.nnz, 256), 256, 0, c.s>>>(P.nnz, perm_in);
+        k_col_count<<<grid_for(P.nnz, 256), 256, 0, c.s>>>(P.nnz, P.ci, cnt);
+        size_t tb = 0;
+        int bits = 1; while ((1LL << bits) < (int64_t)R.n + 1) ++bits;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, P.ci.p, keys_out.p, perm_in.p, perm_out.p, (int)P.nnz, 0, bits, c.s);
+        void *t = scratch(c, tb);
+        cub::DeviceRadixSort::SortPairs(t, tb, P.ci.p, keys_out.p, perm_in.p, perm_out.p, (int)P.nnz, 0, bits, c.s);
+        c.launches += 5;
+    }
+    rowptr_from_counts(c, cnt, R.rp, R.n);
+    R.ci.alloc(R.nnz); R.v.alloc(R.nnz * nc);
+    if (P.nnz) k_transpose_fill<<<grid_for(P.nnz, 256), 256, 0, c.s>>>(P.nnz, nc, perm_out, row, P.v, R.ci, R.v);
+    TSP_CUDA(cudaGetLastError());
+}
+
+static void make_coarsest(Ctx &c, Hier &H, Level &L)
+{
+    TSP_REQUIRE(L.n <= 4096, TSP_ERR_SINGULAR, "coarsest AMG level exceeds the dense limit (4096 rows)");
+    L.coarsest = 1;
+    int n = std::max(L.n, 1);
+    DBuf<double> work; work.alloc((size_t)L.nc * n * n);
+    DBuf<int> piv; piv.alloc((size_t)L.nc * n);
+    L.cinv.alloc((size_t)L.nc * n * n);
+    c.dcount.zero(c.s);
+    if (L.n) k_dense_inv<<<L.nc, 256, 0, c.s>>>(L.n, L.nc, L.A.rp, L.A.ci, L.A.v, work, piv, L.cinv, c.dcount);
+    TSP_CUDA(cudaGetLastError());
+    H.perturbed += (int64_t)d2h1(c, c.dcount.p);
+    c.launches++;
+}
+
+void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc)
+{
+    H.L.clear();
+    H.L.reserve(16);
+    H.nc = nc;
+    H.L.emplace_back();
+    {
+        Level &L0 = H.L[0];
+        L0.A = std::move(A0);
+        L0.zb = std::move(zb0);
+    }
+    const int maxl = std::min(std::max(c.o.amg_max_levels, 1), 16);
+    DBuf<int> err; err.alloc(1);
+    for (int lvl = 0;; ++lvl) {
+        Level &L = H.L[lvl];
+        L.n = L.A.n; L.nc = nc;
+        const int n = L.n;
+        L.dl1.alloc((size_t)n * nc); L.dinv.alloc((size_t)n * nc);
+        if (n) k_l1<<<grid_for(n, 256), 256, 0, c.s>>>(n, nc, L.A.rp, L.A.v, L.dl1, L.dinv);
+        c.launches++;
+        if (n <= c.o.amg_coarse_max || lvl == maxl - 1) { make_coarsest(c, H, L); break; }
+        // strength + symmetrisation
+        DBuf<uint8_t> S, E; S.alloc(L.A.nnz + 1); E.alloc(L.A.nnz + 1);
+        err.zero(c.s);
+        k_strength<<<grid_for(n, 256), 256, 0, c.s>>>(n, nc, L.A.rp, L.A.ci, L.A.v, L.zb, c.o.amg_theta, S);
+        k_symm<<<grid_for(n, 256), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, S, E, err);
+        c.launches += 2;
+        TSP_REQUIRE(!d2h1(c, err.p), TSP_ERR_INVALID_ARG, "AMG input pattern is not structurally symmetric");
+        // MIS(2) rounds
+        DBuf<int8_t> st; st.alloc(n);
+        DBuf<uint64_t> t1; t1.alloc(n);
+        DBuf<uint8_t> newr, near1; newr.alloc(n); near1.alloc(n);
+        k_mis_init<<<grid_for(n, 256), 256, 0, c.s>>>(n, L.A.rp, E, st);
+        c.launches++;
+        for (int round = 0; round < 1000; ++round) {
+            k_mis_t1<<<grid_for(n, 256), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, E, st, t1);
+            k_mis_root<<<grid_for(n, 256), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, E, st, t1, newr);
+            k_mis_near<<<grid_for(n, 256), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, E, newr, st, near1);
+            c.dcount.zero(c.s);
+            k_mis_out<<<grid_for(n, 256), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, E, near1, st, c.dcount);
+            c.launches += 4;
+            if (d2h1(c, c.dcount.p) == 0) break;
+        }
+        // aggregates
+        DBuf<int32_t> flag, rid, ph1;
+        flag.alloc(n + 1); rid.alloc(n + 1); ph1.alloc(n);
+        k_rootflag<<<grid_for(n, 256), 256, 0, c.s>>>(n, st, flag);
+        TSP_CUDA(cudaMemsetAsync(flag.p + n, 0, sizeof(int32_t), c.s));
+        exclusive_scan<int32_t>(c, flag, rid, n + 1);
+        const int nagg = d2h1(c, rid.p + n);
+        if (nagg == 0 || (double)nagg > 0.8 * (double)n) {   // stagnation: direct solve here
+            H.fallbacks++;
+            make_coarsest(c, H, L);
+            break;
+        }
+        L.nagg = nagg;
+        L.agg.alloc(n);
+        H.L.emplace_back();
+        Level &Lc = H.L[lvl + 1];
+        Level &Lf = H.L[lvl];   // re-fetch after emplace_back
+        Lc.zb.alloc(nagg);
+        TSP_CUDA(cudaMemsetAsync(ph1, 0xff, sizeof(int32_t) * n, c.s));
+        k_phase1<<<grid_for(n, 256), 256, 0, c.s>>>(n, Lf.A.rp, Lf.A.ci, E, st, rid, Lf.zb, ph1, Lc.zb);
+        k_phase2<<<grid_for(n, 256), 256, 0, c.s>>>(n, nc, Lf.A.rp, Lf.A.ci, Lf.A.v, E, st, ph1, Lf.agg);
+        c.launches += 3;
+        // prolongator
+        DBuf<double> d; d.alloc((size_t)n * nc);
+        DBuf<unsigned long long> rho; rho.alloc(3); rho.zero(c.s);
+        k_pdiag<<<grid_for(n, 256), 256, 0, c.s>>>(n, nc, Lf.A.rp, Lf.A.ci, Lf.A.v, E, d, rho);
+        unsigned long long rb[3] = {0, 0, 0};
+        TSP_CUDA(cudaMemcpyAsync(rb, rho.p, sizeof(rb), cudaMemcpyDeviceToHost, c.s));
+        TSP_CUDA(cudaStreamSynchronize(c.s));
+        Omega om;
+        for (int k = 0; k < 3; ++k) {
+            double r; memcpy(&r, &rb[k], sizeof(double));
+            volatile double three_r = 3.0 * r;   // IEEE: 4 / (3 rho), same expression as the oracle
+            om.w[k] = (k < nc && r > 0.0) ? 4.0 / three_r : 0.0;
+        }
+        DBuf<int32_t> cnt; cnt.alloc(n + 1);
+        err.zero(c.s);
+        k_pcount<<<grid_for(n, 128), 128, 0, c.s>>>(n, Lf.A.rp, Lf.A.ci, E, Lf.agg, cnt, err);
+        Lf.P.n = n; Lf.P.m = nagg; Lf.P.nc = nc;
+        Lf.P.nnz = rowptr_from_counts(c, cnt, Lf.P.rp, n);
+        Lf.P.ci.alloc(Lf.P.nnz); Lf.P.v.alloc(Lf.P.nnz * nc);
+        k_pfill<<<grid_for(n, 128), 128, 0, c.s>>>(n, nc, Lf.A.rp, Lf.A.ci, Lf.A.v, E, Lf.agg, d, om, Lf.P.rp, Lf.P.ci, Lf.P.v, err);
+        c.launches += 3;
+        TSP_REQUIRE(!d2h1(c, err.p), TSP_ERR_INVALID_ARG, "prolongator row exceeds 512 aggregates");
+        transpose(c, Lf.P, Lf.R, nc);
+        Csr AP;
+        spgemm(c, Lf.A, Lf.P, AP, nc);
+        spgemm(c, Lf.R, AP, Lc.A, nc);
+    }
+    // apply-side layouts and work vectors
+    for (size_t l = 0; l < H.L.size(); ++l) {
+        Level &L = H.L[l];
+        sell_from_csr(c, L.A, L.sA, nc);
+        if (!L.coarsest) {
+            sell_from_csr(c, L.P, L.sP, nc);
+            sell_from_csr(c, L.R, L.sR, nc);
+        }
+        size_t m = (size_t)std::max(L.n, 1) * nc;
+        L.b.alloc(m); L.x.alloc(m); L.x2.alloc(m); L.r.alloc(m);
+    }
+    TSP_CUDA(cudaStreamSynchronize(c.s));
+}
+
+// ------------------------------------------------------------------ V-cycle kernels (apply; free arithmetic)
+// pre-smooth from zero + residual: x = D^-1 b ; r = b - A D^-1 b
+template <int NC>
+__global__ void __launch_bounds__(256) k_vc_pre(int n, const int64_t *__restrict__ off, const int32_t *__restrict__ col,
+                                                const double *__restrict__ val, const double *__restrict__ dinv,
+                                                const double *__restrict__ b, double *__restrict__ x, double *__restrict__ r)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int s = i >> 5, lane = i & 31;
+    double acc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+    const int64_t b0 = off[s], b1 = off[s + 1];
+#pragma unroll 2
+    for (int64_t slot = b0; slot < b1; ++slot) {
+        const int j = __ldcs(col + slot * 32 + lane);
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+            acc[c] = fma(__ldcs(val + (slot * NC + c) * 32 + lane), __ldg(b + (int64_t)j * NC + c) * __ldg(dinv + (int64_t)j * NC + c), acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const double bi = b[(int64_t)i * NC + c];
+        x[(int64_t)i * NC + c] = bi * dinv[(int64_t)i * NC + c];
+        r[(int64_t)i * NC + c] = bi - acc[c];
+    }
+}
+// y = S x  (restriction R r)
+template <int NC>
+__global__ void __launch_bounds__(256) k_sell_mv(int n, const int64_t *__restrict__ off, const int32_t *__restrict__ col,
+                                                 const double *__restrict__ val, const double *__restrict__ x, double *__restrict__ y)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int s = i >> 5, lane = i & 31;
+    double acc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+    const int64_t b0 = off[s], b1 = off[s + 1];
+#pragma unroll 2
+    for (int64_t slot = b0; slot < b1; ++slot) {
+        const int j = __ldcs(col + slot * 32 + lane);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c] = fma(__ldcs(val + (slot * NC + c) * 32 + lane), __ldg(x + (int64_t)j * NC + c), acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) y[(int64_t)i * NC + c] = acc[c];
+}
+// x += P xc
+template <int NC>
+__global__ void __launch_bounds__(256) k_prolong(int n, const int64_t *__restrict__ off, const int32_t *__restrict__ col,
+                                                 const double *__restrict__ val, const double *__restrict__ xc, double *__restrict__ x)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int s = i >> 5, lane = i & 31;
+    double acc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = x[(int64_t)i * NC + c];
+    const int64_t b0 = off[s], b1 = off[s + 1];
+    for (int64_t slot = b0; slot < b1; ++slot) {
+        const int j = __ldcs(col + slot * 32 + lane);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c] = fma(__ldcs(val + (slot * NC + c) * 32 + lane), __ldg(xc + (int64_t)j * NC + c), acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) x[(int64_t)i * NC + c] = acc[c];
+}
+// post-smooth: xo = x + D^-1 (b - A x)
+template <int NC>
+__global__ void __launch_bounds__(256) k_vc_post(int n, const int64_t *__restrict__ off, const int32_t *__restrict__ col,
+                                                 const double *__restrict__ val, const double *__restrict__ dinv,
+                                                 const double *__restrict__ b, const double *__restrict__ x, double *__restrict__ xo)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int s = i >> 5, lane = i & 31;
+    double acc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+    const int64_t b0 = off[s], b1 = off[s + 1];
+#pragma unroll 2
+    for (int64_t slot = b0; slot < b1; ++slot) {
+        const int j = __ldcs(col + slot * 32 + lane);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c] = fma(__ldcs(val + (slot * NC + c) * 32 + lane), __ldg(x + (int64_t)j * NC + c), acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const int64_t t = (int64_t)i * NC + c;
+        xo[t] = x[t] + dinv[t] * (b[t] - acc[c]);
+    }
+}
+// coarsest: x = A_c^-1 b per component
+template <int NC>
+__global__ void k_coarse(int n, const double *__restrict__ inv, const double *__restrict__ b, double *__restrict__ x)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int c = blockIdx.y;
+    if (i >= n) return;
+    const double *row = inv + ((size_t)c * n + i) * n;
+    double s = 0.0;
+    for (int j = 0; j < n; ++j) s = fma(row[j], b[(int64_t)j * NC + c], s);
+    x[(int64_t)i * NC + c] = s;
+}
+
+static double sbytes(const Sell &S) { return (double)S.slots * 32 * (4.0 + 8.0 * S.bs); }
+
+template <int NC>
+static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
+{
+    Level &L = H.L[l];
+    const bool mech = NC == 3;
+    if (L.coarsest) {
+        prof_begin(c, PK_COARSE);
+        if (L.n) k_coarse<NC><<<dim3(grid_for(L.n, 128), NC), 128, 0, c.s>>>(L.n, L.cinv, b, xout);
+        prof_end(c, PK_COARSE, 8.0 * L.n * L.n * NC);
+        c.launches++;
+        return;
+    }
+    const int n = L.n;
+    const double vec = 8.0 * NC * n;
+    prof_begin(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P);
+    k_vc_pre<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sA.off, L.sA.col, L.sA.val, L.dinv, b, L.x2, L.r);
+    prof_end(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P, sbytes(L.sA) + 4 * vec);
+    Level &Lc = H.L[l + 1];
+    prof_begin(c, mech ? PK_VC_RESTR_U : PK_VC_RESTR_P);
+    k_sell_mv<NC><<<grid_for(Lc.n, 256), 256, 0, c.s>>>(Lc.n, L.sR.off, L.sR.col, L.sR.val, L.r, Lc.b);
+    prof_end(c, mech ? PK_VC_RESTR_U : PK_VC_RESTR_P, sbytes(L.sR) + vec + 8.0 * NC * Lc.n);
+    vcycle_rec<NC>(c, H, l + 1, Lc.b, Lc.x);
+    prof_begin(c, mech ? PK_VC_PROL_U : PK_VC_PROL_P);
+    k_prolong<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sP.off, L.sP.col, L.sP.val, Lc.x, L.x2);
+    prof_end(c, mech ? PK_VC_PROL_U : PK_VC_PROL_P, sbytes(L.sP) + 2 * vec + 8.0 * NC * Lc.n);
+    prof_begin(c, mech ? PK_VC_POST_U : PK_VC_POST_P);
+    k_vc_post<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sA.off, L.sA.col, L.sA.val, L.dinv, b, L.x2, xout);
+    prof_end(c, mech ? PK_VC_POST_U : PK_VC_POST_P, sbytes(L.sA) + 4 * vec);
+    c.launches += 4;
+}
+
+void amg_vcycle(Ctx &c, Hier &H, const double *b, double *x, bool mech)
+{
+    if (mech) vcycle_rec<3>(c, H, 0, b, x);
+    else vcycle_rec<1>(c, H, 0, b, x);
+    TSP_CUDA(cudaGetLastError());
+}
+
+}  // namespace tsp

@@ -1,0 +1,318 @@
+// capi.cu -- the C-ABI of include/tsp.h: validation, deep copy, phase split
+// (P:519), profiling hooks, parity export.  Host orchestration only;
+// every numerical step is a kernel in apply.cu / amg.cu / ilu.cu / krylov.cu.
+#include <cstdio>
+#include <cstring>
+
+#include "tsp_internal.cuh"
+
+namespace tsp {
+
+static thread_local std::string g_err;
+void set_error(const std::string &m) { g_err = m; }
+
+void *scratch(Ctx &c, size_t bytes)
+{
+    if (bytes > c.scratch_bytes) {
+        c.scratch.alloc(bytes);
+        c.scratch_bytes = bytes;
+    }
+    return c.scratch.p;
+}
+
+static const char *kProfNames[PK_COUNT] = {
+    "op_node", "op_cell", "step2", "step34", "ilu_steps678", "vc_pre_u", "vc_restr_u", "vc_prol_u", "vc_post_u",
+    "vc_pre_p", "vc_restr_p", "vc_prol_p", "vc_post_p", "coarse", "mdot", "maxpy", "norm", "vec", "setup"};
+
+void prof_begin(Ctx &c, int cls)
+{
+    if (!c.prof.on) return;
+    Prof &p = c.prof;
+    if (p.next + 2 > (int)p.pool.size()) return;
+    p.recs.push_back({cls, p.next, p.next + 1, 0.0});
+    cudaEventRecord(p.pool[p.next], c.s);
+    p.next += 2;
+}
+void prof_end(Ctx &c, int cls, double bytes)
+{
+    if (!c.prof.on) return;
+    Prof &p = c.prof;
+    if (p.recs.empty() || p.recs.back().cls != cls || p.recs.back().bytes != 0.0 || p.recs.back().e1 >= p.next) {
+        if (p.recs.empty() || p.recs.back().cls != cls) return;
+    }
+    Prof::Rec &r = p.recs.back();
+    r.bytes = bytes;
+    cudaEventRecord(p.pool[r.e1], c.s);
+}
+
+}  // namespace tsp
+
+using namespace tsp;
+
+struct tsp_ctx : Ctx {};
+
+#define API_BEGIN try {
+#define API_END                                                                                     \
+    }                                                                                               \
+    catch (const tsp::Error &e) {                                                                   \
+        set_error(e.msg);                                                                           \
+        return e.st;                                                                                \
+    }                                                                                               \
+    catch (const std::exception &e) {                                                               \
+        set_error(e.what());                                                                        \
+        return TSP_ERR_CUDA;                                                                        \
+    }                                                                                               \
+    return TSP_OK;
+
+extern "C" {
+
+int tsp_abi_version(void) { return TSP_ABI_VERSION; }
+const char *tsp_last_error(void) { return g_err.c_str(); }
+
+tsp_status tsp_default_options(tsp_options *o)
+{
+    if (!o) { set_error("null options"); return TSP_ERR_INVALID_ARG; }
+    memset(o, 0, sizeof(*o));
+    o->amg_theta = 0.25; o->amg_coarse_max = 64; o->amg_max_levels = 12; o->zblock = 16;
+    o->tile_x = o->tile_y = o->tile_z = 16;
+    return TSP_OK;
+}
+
+void tsp_default_solve_opts(tsp_solve_opts *o)
+{
+    if (!o) return;
+    o->rtol = 1e-8; o->restart = 64; o->max_iters = 1000; o->x0_zero = 1; o->host_ptrs = 0;
+}
+
+tsp_status tsp_create(tsp_handle *out, const tsp_desc *d)
+{
+    if (!out || !d) { set_error("null argument"); return TSP_ERR_INVALID_ARG; }
+    *out = nullptr;
+    tsp_ctx *c = nullptr;
+    API_BEGIN
+    TSP_REQUIRE(d->nx > 0 && d->ny > 0 && d->nz > 0, TSP_ERR_INVALID_ARG, "grid dimensions must be positive");
+    TSP_REQUIRE(d->nranks == 1 && d->rank == 0, TSP_ERR_INVALID_ARG, "this build supports nranks == 1 (see DESIGN.md)");
+    const tsp_bsr *bs[4] = {&d->A_uu, &d->A_uf, &d->A_fu, &d->A_ff};
+    for (int k = 0; k < 4; ++k)
+        TSP_REQUIRE(bs[k]->rowptr && bs[k]->col && bs[k]->val, TSP_ERR_INVALID_ARG, "null matrix pointer");
+    TSP_REQUIRE(d->fs_diag, TSP_ERR_INVALID_ARG, "null fs_diag");
+    c = new tsp_ctx();
+    c->nx = d->nx; c->ny = d->ny; c->nz = d->nz;
+    c->Nn = (d->nx + 1) * (d->ny + 1) * (d->nz + 1);
+    c->Nc = d->nx * d->ny * d->nz;
+    c->n = 3 * (int64_t)c->Nn + 2 * (int64_t)c->Nc;
+    c->s = (cudaStream_t)d->stream;
+    c->o = d->opts;
+    if (c->o.amg_theta <= 0 || c->o.amg_coarse_max <= 0) tsp_default_options(&c->o);
+    if (c->o.zblock <= 0) c->o.zblock = 16;
+    if (c->o.tile_x <= 0 || c->o.tile_y <= 0 || c->o.tile_z <= 0) c->o.tile_x = c->o.tile_y = c->o.tile_z = 16;
+    int dev = 0;
+    TSP_CUDA(cudaGetDevice(&dev));
+    TSP_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, dev));
+    const bool on_dev = d->inputs_on_device != 0;
+    csr_upload(*c, c->uu, c->Nn, c->Nn, 9, d->A_uu.rowptr, d->A_uu.col, d->A_uu.val, on_dev);
+    csr_upload(*c, c->uf, c->Nn, c->Nc, 6, d->A_uf.rowptr, d->A_uf.col, d->A_uf.val, on_dev);
+    csr_upload(*c, c->fu, c->Nc, c->Nn, 6, d->A_fu.rowptr, d->A_fu.col, d->A_fu.val, on_dev);
+    csr_upload(*c, c->ff, c->Nc, c->Nc, 4, d->A_ff.rowptr, d->A_ff.col, d->A_ff.val, on_dev);
+    check_csr(*c, c->uu, "A_uu"); check_csr(*c, c->uf, "A_uf"); check_csr(*c, c->fu, "A_fu"); check_csr(*c, c->ff, "A_ff");
+    c->fs.alloc(2 * (size_t)c->Nc);
+    TSP_CUDA(cudaMemcpyAsync(c->fs, d->fs_diag, sizeof(double) * 2 * c->Nc, on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->s));
+    {
+        std::vector<double> fsh(2 * (size_t)c->Nc);
+        TSP_CUDA(cudaMemcpyAsync(fsh.data(), c->fs, sizeof(double) * fsh.size(), cudaMemcpyDeviceToHost, c->s));
+        TSP_CUDA(cudaStreamSynchronize(c->s));
+        for (double v : fsh) TSP_REQUIRE(v >= 0.0, TSP_ERR_INVALID_ARG, "negative fixed-stress diagonal (S:355)");
+    }
+    sell_from_csr(*c, c->uu, c->s_uu, 9);
+    sell_from_csr(*c, c->uf, c->s_uf, 6);
+    sell_from_csr(*c, c->fu, c->s_fu, 6);
+    sell_from_csr(*c, c->ff, c->s_ff, 4);
+    c->w_yf.alloc(2 * (size_t)c->Nc); c->w_wp.alloc(c->Nc); c->w_zp.alloc(c->Nc); c->w_tmp.alloc(c->Nc);
+    c->kx.alloc(c->n); c->kb.alloc(c->n);
+    c->dcount.alloc(4);
+    TSP_CUDA(cudaStreamSynchronize(c->s));
+    *out = c;
+    return TSP_OK;
+    }
+    catch (const tsp::Error &e) {
+        set_error(e.msg);
+        delete c;
+        return e.st;
+    }
+}
+
+tsp_status tsp_setup(tsp_handle h, unsigned what)
+{
+    if (!h) { set_error("null handle"); return TSP_ERR_INVALID_ARG; }
+    API_BEGIN
+    if (what & TSP_SETUP_MECH) setup_mech(*h);
+    if (what & TSP_SETUP_FLOW) setup_flow(*h);
+    TSP_CUDA(cudaStreamSynchronize(h->s));
+    API_END
+}
+
+tsp_status tsp_apply_preconditioner(tsp_handle h, const double *v, double *z)
+{
+    if (!h || !v || !z) { set_error("null argument"); return TSP_ERR_INVALID_ARG; }
+    if (v == z) { set_error("v and z must not alias"); return TSP_ERR_INVALID_ARG; }
+    API_BEGIN
+    prec_apply(*h, v, z);
+    API_END
+}
+
+tsp_status tsp_apply_operator(tsp_handle h, const double *x, double *y)
+{
+    if (!h || !x || !y) { set_error("null argument"); return TSP_ERR_INVALID_ARG; }
+    if (x == y) { set_error("x and y must not alias"); return TSP_ERR_INVALID_ARG; }
+    API_BEGIN
+    op_apply(*h, x, y);
+    API_END
+}
+
+tsp_status tsp_solve(tsp_handle h, const double *b, double *x, const tsp_solve_opts *o, tsp_solve_info *info)
+{
+    if (!h || !b || !x) { set_error("null argument"); return TSP_ERR_INVALID_ARG; }
+    tsp_solve_opts oo;
+    tsp_default_solve_opts(&oo);
+    if (o) oo = *o;
+    tsp_solve_info inf;
+    memset(&inf, 0, sizeof(inf));
+    API_BEGIN
+    TSP_REQUIRE(h->mech_ready && h->flow_ready, TSP_ERR_STATE, "solve before tsp_setup(MECH|FLOW)");
+    TSP_REQUIRE(oo.rtol > 0 && oo.restart > 0 && oo.max_iters >= 0, TSP_ERR_INVALID_ARG, "bad solve options");
+    const double *db = b;
+    double *dx = x;
+    if (oo.host_ptrs) {
+        TSP_CUDA(cudaMemcpyAsync(h->kb, b, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->s));
+        if (!oo.x0_zero) TSP_CUDA(cudaMemcpyAsync(h->kx, x, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->s));
+        db = h->kb; dx = h->kx;
+    }
+    krylov_solve(*h, db, dx, oo, inf);
+    if (oo.host_ptrs) {
+        TSP_CUDA(cudaMemcpyAsync(x, h->kx, sizeof(double) * h->n, cudaMemcpyDeviceToHost, h->s));
+        TSP_CUDA(cudaStreamSynchronize(h->s));
+    }
+    if (info) *info = inf;
+    return inf.status;
+    }
+    catch (const tsp::Error &e) {
+        set_error(e.msg);
+        inf.status = e.st;
+        if (info) *info = inf;
+        return e.st;
+    }
+}
+
+tsp_status tsp_get_stats(tsp_handle h, tsp_stats *s)
+{
+    if (!h || !s) { set_error("null argument"); return TSP_ERR_INVALID_ARG; }
+    memset(s, 0, sizeof(*s));
+    Hier *H[2] = {&h->mech, &h->pres};
+    double apply_bytes = 0;
+    for (int w = 0; w < 2; ++w) {
+        s->levels[w] = (int)H[w]->L.size();
+        for (size_t l = 0; l < H[w]->L.size() && l < 16; ++l) {
+            const Level &L = H[w]->L[l];
+            s->rows[w][l] = L.n; s->nnz[w][l] = L.A.nnz;
+            const double nc = L.nc, vec = 8.0 * nc * L.n;
+            if (L.coarsest) { apply_bytes += 8.0 * L.n * L.n * nc + 2 * vec; continue; }
+            auto sb = [](const Sell &S) { return (double)S.slots * 32 * (4.0 + 8.0 * S.bs); };
+            apply_bytes += 2 * sb(L.sA) + sb(L.sR) + sb(L.sP) + 11 * vec;
+        }
+        s->skipped_dss = h->skipped_dss;
+        s->perturbed_pivots = h->perturbed + h->mech.perturbed + h->pres.perturbed;
+        s->coarsening_fallbacks = h->mech.fallbacks + h->pres.fallbacks;
+    }
+    auto sb = [](const Sell &S) { return (double)S.slots * 32 * (4.0 + 8.0 * S.bs); };
+    const double Nn = h->Nn, Nc = h->Nc, n = (double)h->n;
+    apply_bytes += sb(h->s_fu) + 24 * Nn + 32 * Nc;            // step 2
+    apply_bytes += sb(h->s_aps) + 40 * Nc;                     // steps 3-4
+    apply_bytes += (28.0 * 8 + 32 + 48) * Nc;                  // steps 6-8
+    s->bytes_apply = apply_bytes;
+    s->bytes_operator = sb(h->s_uu) + sb(h->s_uf) + sb(h->s_fu) + sb(h->s_ff) + 16 * n;
+    s->bytes_iter_base = s->bytes_apply + s->bytes_operator + 8 * n * 6;
+    s->bytes_per_krylov_vec = 8 * n * 4;
+    s->launches = h->launches;
+    return TSP_OK;
+}
+
+tsp_status tsp_level_sizes(tsp_handle h, int which, int lvl, int64_t out6[6])
+{
+    if (!h || !out6) { set_error("null argument"); return TSP_ERR_INVALID_ARG; }
+    Hier &H = which ? h->pres : h->mech;
+    if (lvl < 0 || lvl >= (int)H.L.size()) { set_error("level out of range"); return TSP_ERR_INVALID_ARG; }
+    const Level &L = H.L[lvl];
+    out6[0] = L.n; out6[1] = L.A.nnz; out6[2] = L.nagg; out6[3] = L.coarsest ? 0 : L.P.nnz; out6[4] = L.nc; out6[5] = L.coarsest;
+    return TSP_OK;
+}
+
+tsp_status tsp_export_level(tsp_handle h, int which, int lvl, int32_t *A_rp, int32_t *A_ci, double *A_v, int32_t *agg,
+                            int32_t *P_rp, int32_t *P_ci, double *P_v, double *dl1)
+{
+    if (!h) { set_error("null handle"); return TSP_ERR_INVALID_ARG; }
+    Hier &H = which ? h->pres : h->mech;
+    if (lvl < 0 || lvl >= (int)H.L.size()) { set_error("level out of range"); return TSP_ERR_INVALID_ARG; }
+    API_BEGIN
+    Level &L = H.L[lvl];
+    cudaStream_t s = h->s;
+    auto cp = [&](void *dst, const void *src, size_t bytes) {
+        if (dst && bytes) TSP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    };
+    cp(A_rp, L.A.rp, sizeof(int32_t) * (L.n + 1));
+    cp(A_ci, L.A.ci, sizeof(int32_t) * L.A.nnz);
+    cp(A_v, L.A.v, sizeof(double) * L.A.nnz * L.nc);
+    cp(dl1, L.dl1, sizeof(double) * L.n * L.nc);
+    if (!L.coarsest) {
+        cp(agg, L.agg, sizeof(int32_t) * L.n);
+        cp(P_rp, L.P.rp, sizeof(int32_t) * (L.n + 1));
+        cp(P_ci, L.P.ci, sizeof(int32_t) * L.P.nnz);
+        cp(P_v, L.P.v, sizeof(double) * L.P.nnz * L.nc);
+    }
+    TSP_CUDA(cudaStreamSynchronize(s));
+    API_END
+}
+
+tsp_status tsp_prof_enable(tsp_handle h, int on)
+{
+    if (!h) { set_error("null handle"); return TSP_ERR_INVALID_ARG; }
+    API_BEGIN
+    Prof &p = h->prof;
+    TSP_CUDA(cudaStreamSynchronize(h->s));
+    if (on && p.pool.empty()) {
+        p.pool.resize(1 << 16);
+        for (auto &e : p.pool) TSP_CUDA(cudaEventCreate(&e));
+    }
+    p.recs.clear();
+    p.next = 0;
+    p.on = on != 0;
+    h->launches = 0;
+    API_END
+}
+
+tsp_status tsp_prof_read(tsp_handle h, tsp_prof *out)
+{
+    if (!h || !out) { set_error("null argument"); return TSP_ERR_INVALID_ARG; }
+    API_BEGIN
+    memset(out, 0, sizeof(*out));
+    TSP_CUDA(cudaStreamSynchronize(h->s));
+    out->nclasses = PK_COUNT;
+    for (int k = 0; k < PK_COUNT; ++k) snprintf(out->name[k], sizeof(out->name[k]), "%s", kProfNames[k]);
+    for (auto &r : h->prof.recs) {
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, h->prof.pool[r.e0], h->prof.pool[r.e1]) != cudaSuccess) continue;
+        out->launches[r.cls] += 1;
+        out->ms[r.cls] += ms;
+        out->bytes[r.cls] += r.bytes;
+    }
+    API_END
+}
+
+void tsp_destroy(tsp_handle h)
+{
+    if (!h) return;
+    cudaStreamSynchronize(h->s);
+    for (auto &e : h->prof.pool) cudaEventDestroy(e);
+    delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,98 @@
+// setup.cu -- rows a1-a3 on the GPU and the MECH / FLOW setup phases of P:519,
+// P:638 (mechanics once per simulation, flow per Newton step).
+#include "tsp_internal.cuh"
+
+namespace tsp {
+
+// a2: SDC: keep the (x,x), (y,y), (z,z) entries of every 3x3 block
+__global__ void k_sdc(int64_t nnzb, const double *__restrict__ uu, double *__restrict__ sdc)
+{
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= nnzb) return;
+    sdc[3 * q + 0] = uu[9 * q + 0];
+    sdc[3 * q + 1] = uu[9 * q + 4];
+    sdc[3 * q + 2] = uu[9 * q + 8];
+}
+
+__global__ void k_zb_nodes(int Nn, int nx, int ny, int nz, int zblock, int32_t *zb)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= Nn) return;
+    int k = i / ((nx + 1) * (ny + 1));
+    int kc = k < nz ? k : nz - 1;        // node plane k belongs to cell plane min(k, nz-1) (R-zblock)
+    zb[i] = kc / zblock;
+}
+__global__ void k_zb_cells(int Nc, int nx, int ny, int zblock, int32_t *zb)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < Nc) zb[i] = (i / (nx * ny)) / zblock;
+}
+
+// a1 + a3: fixed stress (eq:Schur_1_FS) and quasi-IMPES:
+//   A_sp^FS = A_sp + D_sp, A_pp^FS = A_pp + D_pp on the diagonal;
+//   D_ss = diagm(A_ss), D_ps = diagm(A_ps);  S_pp = A_pp^FS - (D_ps / D_ss) A_sp^FS  (same pattern).
+// Bit-identical to the oracle (IEEE intrinsics, same expression order).
+__global__ void k_fs_qimpes(int Nc, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const double *__restrict__ v,
+                            const double *__restrict__ fs, double *__restrict__ spp, double *__restrict__ dssinv,
+                            unsigned long long *skipped)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= Nc) return;
+    int64_t qd = -1;
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) if (ci[q] == i) { qd = q; break; }
+    double dss = qd >= 0 ? v[qd * 4 + 0] : 0.0, dps = qd >= 0 ? v[qd * 4 + 2] : 0.0;
+    double cfac = 0.0;
+    if (dss != 0.0) cfac = __ddiv_rn(dps, dss);
+    else atomicAdd(skipped, 1ULL);                         // skip the correction, count it
+    dssinv[i] = dss != 0.0 ? 1.0 / dss : 0.0;
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+        double app = v[q * 4 + 3], asp = v[q * 4 + 1];
+        if (q == qd) { app = __dadd_rn(app, fs[2 * i + 1]); asp = __dadd_rn(asp, fs[2 * i]); }
+        spp[q] = __dsub_rn(app, __dmul_rn(cfac, asp));
+    }
+}
+
+void setup_mech(Ctx &c)
+{
+    c.mech_ready = false;
+    Csr A;
+    A.n = c.Nn; A.m = c.Nn; A.nc = 3; A.nnz = c.uu.nnz;
+    A.rp.alloc(c.Nn + 1); A.ci.alloc(c.uu.nnz); A.v.alloc(3 * c.uu.nnz);
+    TSP_CUDA(cudaMemcpyAsync(A.rp, c.uu.rp, sizeof(int32_t) * (c.Nn + 1), cudaMemcpyDeviceToDevice, c.s));
+    TSP_CUDA(cudaMemcpyAsync(A.ci, c.uu.ci, sizeof(int32_t) * c.uu.nnz, cudaMemcpyDeviceToDevice, c.s));
+    prof_begin(c, PK_SETUP);
+    k_sdc<<<grid_for(c.uu.nnz, 256), 256, 0, c.s>>>(c.uu.nnz, c.uu.v, A.v);
+    DBuf<int32_t> zb; zb.alloc(c.Nn);
+    k_zb_nodes<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(c.Nn, c.nx, c.ny, c.nz, c.o.zblock, zb);
+    prof_end(c, PK_SETUP, 0);
+    c.launches += 2;
+    amg_build(c, c.mech, A, zb, 3);       // a4 (mechanics): M_uu^-1 = amg(A_uu^SDC)
+    c.mech_ready = true;
+}
+
+void setup_flow(Ctx &c)
+{
+    c.flow_ready = false;
+    Csr S;
+    S.n = c.Nc; S.m = c.Nc; S.nc = 1; S.nnz = c.ff.nnz;
+    S.rp.alloc(c.Nc + 1); S.ci.alloc(c.ff.nnz); S.v.alloc(c.ff.nnz);
+    TSP_CUDA(cudaMemcpyAsync(S.rp, c.ff.rp, sizeof(int32_t) * (c.Nc + 1), cudaMemcpyDeviceToDevice, c.s));
+    TSP_CUDA(cudaMemcpyAsync(S.ci, c.ff.ci, sizeof(int32_t) * c.ff.nnz, cudaMemcpyDeviceToDevice, c.s));
+    c.dss_inv.alloc(c.Nc);
+    c.dcount.zero(c.s);
+    k_fs_qimpes<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(c.Nc, c.ff.rp, c.ff.ci, c.ff.v, c.fs, S.v, c.dss_inv, c.dcount);
+    unsigned long long sk = 0;
+    TSP_CUDA(cudaMemcpyAsync(&sk, c.dcount, sizeof(sk), cudaMemcpyDeviceToHost, c.s));
+    TSP_CUDA(cudaStreamSynchronize(c.s));
+    c.skipped_dss = (int64_t)sk;
+    const int map_aps[1] = {2};           // A_ps = entry (1,0) of every 2x2 block (full A_ps)
+    sell_from_csr(c, c.ff, c.s_aps, 1, map_aps);
+    DBuf<int32_t> zb; zb.alloc(c.Nc);
+    k_zb_cells<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(c.Nc, c.nx, c.ny, c.o.zblock, zb);
+    c.launches += 2;
+    amg_build(c, c.pres, S, zb, 1);       // a4 (pressure): M_pp^-1 = amg(S_pp)
+    ilu_setup(c, nullptr);                // a5: tile ILU(0) of P S_ff^FS P^T
+    c.flow_ready = true;
+}
+
+}  // namespace tsp

@@ -1,0 +1,240 @@
+"""Thin ctypes binding of libtsp.so (include/tsp.h).  Argument marshalling only:
+every step of the preconditioner / solver runs in the CUDA kernels of the
+library.  There is no CPU fallback: if libtsp.so is missing or no CUDA device
+is present, the calls raise.
+
+Names follow the C-ABI: tsp_create, tsp_setup, tsp_apply_preconditioner,
+tsp_apply_operator, tsp_solve, tsp_get_stats, tsp_export_level, ...
+`Tsp` bundles them for a synth.Problem-like input.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtsp.so")
+_LIB = None
+_P = C.POINTER
+
+TSP_SETUP_MECH = 1
+TSP_SETUP_FLOW = 2
+STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "INVALID_ARG", -2: "DIM_MISMATCH", -3: "STATE", -4: "CUDA",
+          -5: "NCCL", -6: "OOM", -7: "SINGULAR", -8: "NUMERIC"}
+
+
+class tsp_options(C.Structure):
+    _fields_ = [("amg_theta", C.c_double), ("amg_coarse_max", C.c_int), ("amg_max_levels", C.c_int),
+                ("zblock", C.c_int), ("tile_x", C.c_int), ("tile_y", C.c_int), ("tile_z", C.c_int),
+                ("reserved", C.c_int * 8)]
+
+
+class tsp_bsr(C.Structure):
+    _fields_ = [("rowptr", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p)]
+
+
+class tsp_desc(C.Structure):
+    _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("rank", C.c_int), ("nranks", C.c_int),
+                ("stream", C.c_void_p), ("inputs_on_device", C.c_int),
+                ("A_uu", tsp_bsr), ("A_uf", tsp_bsr), ("A_fu", tsp_bsr), ("A_ff", tsp_bsr),
+                ("fs_diag", C.c_void_p), ("opts", tsp_options)]
+
+
+class tsp_solve_opts(C.Structure):
+    _fields_ = [("rtol", C.c_double), ("restart", C.c_int), ("max_iters", C.c_int), ("x0_zero", C.c_int),
+                ("host_ptrs", C.c_int)]
+
+
+class tsp_solve_info(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("restarts", C.c_int), ("status", C.c_int),
+                ("est_relres", C.c_double), ("true_relres", C.c_double), ("t_solve_s", C.c_double)]
+
+
+class tsp_stats(C.Structure):
+    _fields_ = [("levels", C.c_int * 2), ("rows", (C.c_int64 * 16) * 2), ("nnz", (C.c_int64 * 16) * 2),
+                ("launches", C.c_int64), ("skipped_dss", C.c_int64), ("perturbed_pivots", C.c_int64),
+                ("coarsening_fallbacks", C.c_int64), ("bytes_apply", C.c_double), ("bytes_operator", C.c_double),
+                ("bytes_iter_base", C.c_double), ("bytes_per_krylov_vec", C.c_double)]
+
+
+TSP_PROF_MAX = 32
+
+
+class tsp_prof(C.Structure):
+    _fields_ = [("nclasses", C.c_int), ("name", (C.c_char * 24) * TSP_PROF_MAX),
+                ("launches", C.c_int64 * TSP_PROF_MAX), ("ms", C.c_double * TSP_PROF_MAX),
+                ("bytes", C.c_double * TSP_PROF_MAX)]
+
+
+def lib():
+    """Load libtsp.so; raise loudly if it is missing (no fallback)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libtsp.so not built ({LIB_PATH}); run `make tsp` or __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        L.tsp_abi_version.restype = C.c_int
+        L.tsp_last_error.restype = C.c_char_p
+        L.tsp_default_options.argtypes = [_P(tsp_options)]
+        L.tsp_create.argtypes = [_P(C.c_void_p), _P(tsp_desc)]
+        L.tsp_setup.argtypes = [C.c_void_p, C.c_uint]
+        L.tsp_apply_preconditioner.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.tsp_apply_operator.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.tsp_solve.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, _P(tsp_solve_opts), _P(tsp_solve_info)]
+        L.tsp_default_solve_opts.argtypes = [_P(tsp_solve_opts)]
+        L.tsp_default_solve_opts.restype = None
+        L.tsp_get_stats.argtypes = [C.c_void_p, _P(tsp_stats)]
+        L.tsp_level_sizes.argtypes = [C.c_void_p, C.c_int, C.c_int, _P(C.c_int64)]
+        L.tsp_export_level.argtypes = [C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 8
+        L.tsp_prof_enable.argtypes = [C.c_void_p, C.c_int]
+        L.tsp_prof_read.argtypes = [C.c_void_p, _P(tsp_prof)]
+        L.tsp_destroy.argtypes = [C.c_void_p]
+        L.tsp_destroy.restype = None
+        if L.tsp_abi_version() != 1:
+            raise RuntimeError("libtsp ABI version mismatch")
+        _LIB = L
+    return _LIB
+
+
+EXPORTED = ["tsp_abi_version", "tsp_last_error", "tsp_default_options", "tsp_create", "tsp_setup",
+            "tsp_apply_preconditioner", "tsp_apply_operator", "tsp_solve", "tsp_default_solve_opts",
+            "tsp_get_stats", "tsp_level_sizes", "tsp_export_level", "tsp_prof_enable", "tsp_prof_read",
+            "tsp_destroy"]
+
+
+class TspError(RuntimeError):
+    def __init__(self, status, where):
+        self.status = status
+        msg = lib().tsp_last_error().decode(errors="replace")
+        super().__init__(f"{where}: {STATUS.get(status, status)}: {msg}")
+
+
+def _check(rc, where, ok=(0,)):
+    if rc not in ok:
+        raise TspError(rc, where)
+    return rc
+
+
+def _ptr(a):
+    """Device pointer of a torch CUDA tensor, or host pointer of a numpy array."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        assert a.is_contiguous()
+        return C.c_void_p(a.data_ptr())
+    assert isinstance(a, np.ndarray) and a.flags["C_CONTIGUOUS"]
+    return C.c_void_p(a.ctypes.data)
+
+
+def default_options(**kw) -> tsp_options:
+    o = tsp_options()
+    lib().tsp_default_options(C.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+class Tsp:
+    """One handle.  `arrays` is a synth.Problem (numpy, host) -- or any object
+    with the same attribute names holding CUDA torch tensors (device=True)."""
+
+    def __init__(self, pb, stream=None, device_inputs=False, **opts):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("libtsp needs a CUDA device (no CPU fallback)")
+        L = lib()
+        self.pb = pb
+        self.n = pb.n
+        self.torch = torch
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        keep = []
+
+        def arr(x):
+            if device_inputs:
+                keep.append(x)
+                return _ptr(x)
+            y = np.ascontiguousarray(x)
+            keep.append(y)
+            return _ptr(y)
+
+        d = tsp_desc()
+        d.nx, d.ny, d.nz, d.rank, d.nranks = pb.nx, pb.ny, pb.nz, 0, 1
+        d.stream = C.c_void_p(self.stream.cuda_stream)
+        d.inputs_on_device = int(device_inputs)
+        for name in ("uu", "uf", "fu", "ff"):
+            b = tsp_bsr(arr(getattr(pb, name + "_rowptr")), arr(getattr(pb, name + "_col")), arr(getattr(pb, name + "_val")))
+            setattr(d, "A_" + name, b)
+        d.fs_diag = arr(pb.fs)
+        d.opts = default_options(**opts)
+        h = C.c_void_p()
+        _check(L.tsp_create(C.byref(h), C.byref(d)), "tsp_create")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().tsp_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def setup(self, what=TSP_SETUP_MECH | TSP_SETUP_FLOW):
+        _check(lib().tsp_setup(self.h, what), "tsp_setup")
+        return self
+
+    def apply_preconditioner(self, v, z):
+        _check(lib().tsp_apply_preconditioner(self.h, _ptr(v), _ptr(z)), "tsp_apply_preconditioner")
+        return z
+
+    def apply_operator(self, x, y):
+        _check(lib().tsp_apply_operator(self.h, _ptr(x), _ptr(y)), "tsp_apply_operator")
+        return y
+
+    def solve(self, b, x, rtol=1e-8, restart=64, max_iters=1000, x0_zero=True):
+        """b, x: CUDA tensors (device) or numpy arrays (host; copies on the stream)."""
+        host = isinstance(b, np.ndarray)
+        o = tsp_solve_opts(rtol, restart, max_iters, int(x0_zero), int(host))
+        info = tsp_solve_info()
+        rc = lib().tsp_solve(self.h, _ptr(b), _ptr(x), C.byref(o), C.byref(info))
+        _check(rc, "tsp_solve", ok=(0, 1))
+        return dict(iterations=info.iterations, restarts=info.restarts, status=STATUS.get(info.status, info.status),
+                    est_relres=info.est_relres, true_relres=info.true_relres, t_solve_s=info.t_solve_s)
+
+    def stats(self):
+        s = tsp_stats()
+        _check(lib().tsp_get_stats(self.h, C.byref(s)), "tsp_get_stats")
+        out = {f: getattr(s, f) for f, _ in tsp_stats._fields_ if f not in ("levels", "rows", "nnz")}
+        out["levels"] = list(s.levels)
+        out["rows"] = [list(s.rows[w])[: s.levels[w]] for w in range(2)]
+        out["nnz"] = [list(s.nnz[w])[: s.levels[w]] for w in range(2)]
+        return out
+
+    def num_levels(self, which):
+        return self.stats()["levels"][which]
+
+    def level(self, which, lvl):
+        o = (C.c_int64 * 6)()
+        _check(lib().tsp_level_sizes(self.h, which, lvl, o), "tsp_level_sizes")
+        n, nnz, nagg, pnz, nc, coarsest = list(o)
+        d = dict(n=n, nnz=nnz, nagg=nagg, nc=nc, coarsest=bool(coarsest))
+        d["A_rp"] = np.empty(n + 1, np.int32); d["A_ci"] = np.empty(nnz, np.int32)
+        d["A_v"] = np.empty((nnz, nc)); d["dl1"] = np.empty((n, nc))
+        if not coarsest:
+            d["agg"] = np.empty(n, np.int32); d["P_rp"] = np.empty(n + 1, np.int32)
+            d["P_ci"] = np.empty(pnz, np.int32); d["P_v"] = np.empty((pnz, nc))
+        _check(lib().tsp_export_level(self.h, which, lvl, *[_ptr(d.get(k)) for k in
+                                      ("A_rp", "A_ci", "A_v", "agg", "P_rp", "P_ci", "P_v", "dl1")]), "tsp_export_level")
+        return d
+
+    def hierarchy(self, which):
+        return [self.level(which, l) for l in range(self.num_levels(which))]
+
+    def prof_enable(self, on=True):
+        _check(lib().tsp_prof_enable(self.h, int(on)), "tsp_prof_enable")
+
+    def prof_read(self):
+        p = tsp_prof()
+        _check(lib().tsp_prof_read(self.h, C.byref(p)), "tsp_prof_read")
+        return {p.name[k].value.decode(): dict(launches=p.launches[k], ms=p.ms[k], bytes=p.bytes[k])
+                for k in range(p.nclasses) if p.launches[k]}
