@@ -1,0 +1,323 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: one "step" = one linear solve of the coupled
+poromechanics Jacobian exactly as the paper's phase split runs it (P:519,
+P:638): tsp_setup(MECH|FLOW) (rows a1-a5) followed by tsp_solve, i.e.
+right-preconditioned FGMRES(64) to a 1e-8 relative residual with Algorithm 1
+as the preconditioner (rows a6-a14).  Metric (BASELINE.json): preconditioned
+FGMRES iterations/s; also GDoF/s and the HBM-roofline fraction.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
+
+Prints ONE JSON line on rank 0.  See DESIGN.md "Measurement" for the byte model.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+DEFAULT_CONFIG = "C4"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        return float(mp["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def oracle_sample(pb, gpu_iters, sample_iters=3):
+    """The CPU oracle (as it stands, single thread) on the same workload: full
+    setup (timed) + `sample_iters` FGMRES iterations (timed); the oracle's time
+    for a whole step is setup + gpu_iters * t_iter (iteration counts match +-1)."""
+    import oracle
+    t0 = time.perf_counter()
+    o = oracle.Oracle(pb).setup()
+    t_setup = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    _, info = o.solve(pb.b, rtol=1e-30, m=64, maxit=sample_iters)
+    t_sample = time.perf_counter() - t0
+    t_iter = t_sample / max(info["iterations"], 1)
+    step = t_setup + gpu_iters * t_iter
+    return dict(value=gpu_iters / step, unit="iter/s", cores=1, kind="oracle",
+                t_setup_s=t_setup, t_iter_s=t_iter,
+                sample=f"oracle/ (plain C, 1 thread) on the same {pb.nx}x{pb.ny}x{pb.nz} problem: full setup + "
+                       f"{info['iterations']} FGMRES iterations timed; step = setup + {gpu_iters} x t_iter")
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the CPU oracle timed on the host cores (rank 0 only)."""
+    if rank != 0:
+        return 0
+    pb = synth.generate(args.config)
+    import oracle
+    t0 = time.perf_counter()
+    o = oracle.Oracle(pb).setup()
+    t_setup = time.perf_counter() - t0
+    its = args.ref_sample_iters
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        o.solve(pb.b, rtol=1e-30, m=64, maxit=1)
+    t0 = time.perf_counter()
+    total = 0
+    for _ in range(args.steps):
+        _, info = o.solve(pb.b, rtol=1e-30, m=64, maxit=its)
+        total += info["iterations"]
+    t_iter = (time.perf_counter() - t0) / max(total, 1)
+    full_iters = args.ref_iters
+    step_s = t_setup + full_iters * t_iter
+    value = full_iters / step_s
+    line = {"impl": "reference", "metric": "preconditioned FGMRES iters/s", "value": value, "unit": "iter/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "dof": pb.n, "grid": [pb.nx, pb.ny, pb.nz]},
+            "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": "oracle",
+                             "sample": f"setup once ({t_setup:.2f}s) + {args.steps} samples of {its} FGMRES iterations; "
+                                       f"step = setup + {full_iters} x t_iter"},
+            "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=list(synth.CONFIGS))
+    ap.add_argument("--impl", default="tsp", choices=["tsp", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-sample-iters", type=int, default=2)
+    ap.add_argument("--ref-iters", type=int, default=100, help="iteration count a full reference step is scaled to")
+    args = ap.parse_args()
+    ws, rank, local = dist_init()
+
+    if args.impl == "reference":
+        return run_reference(args, ws, rank)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1812_05540_b200 import Tsp
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    pb = synth.generate(args.config)
+    n = pb.n
+    g = Tsp(pb)
+    b = torch.from_numpy(pb.b).to(dev)
+    x = torch.zeros(n, dtype=torch.float64, device=dev)
+
+    def step():
+        g.setup()
+        return g.solve(b, x, rtol=1e-8, restart=64, max_iters=1000)
+
+    for _ in range(max(args.warmup, 0)):
+        info = step()
+    torch.cuda.synchronize()
+
+    clocks = Clocks(local)
+    clocks.start()
+    g.prof_enable(True)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.current_stream()
+    e0.record(stream)
+    iters, infos = 0, []
+    for _ in range(args.steps):
+        info = step()
+        infos.append(info)
+        iters += info["iterations"]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    prof = g.prof_read()
+    st = g.stats()
+    g.prof_enable(False)
+
+    t_ms = torch.tensor([ms], dtype=torch.float64, device=dev)
+    tot_iters = torch.tensor([float(iters)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot_iters, op=dist.ReduceOp.SUM)
+    ms_max = float(t_ms.item())
+    value = float(tot_iters.item()) / (ms_max * 1e-3)
+
+    # ---- roofline of the dominant kernel (bytes per launch / average launch time, live CUDA events)
+    hbm, peak_src = peaks()
+    dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    dname, d = dom
+    achieved = (d["bytes"] / d["launches"]) / (d["ms"] / d["launches"] * 1e-3) / 1e9
+    solve_ms = sum(i["t_solve_s"] for i in infos) * 1e3
+    mean_j = None
+    # ---- whole-iteration roofline (algorithmic bytes per FGMRES iteration, DESIGN.md byte model)
+    m = 64
+    jsum = 0.0
+    for i in infos:
+        k = i["iterations"]
+        jsum += sum((j % m) for j in range(k))
+    mean_j = jsum / max(iters, 1)
+    bytes_iter = st["bytes_iter_base"] + st["bytes_per_krylov_vec"] * (mean_j + 1)
+    iter_gbs = bytes_iter * iters / (solve_ms * 1e-3) / 1e9
+    kernel_table = {k: dict(launches=v["launches"], ms=round(v["ms"], 4), gbs=round(v["bytes"] / max(v["ms"], 1e-12) / 1e6, 1),
+                            share=round(v["ms"] / sum(p["ms"] for p in prof.values()), 4)) for k, v in prof.items()}
+
+    # ---- end to end through the public API with HOST buffers (pinned)
+    e2e = None
+    if not args.no_e2e:
+        pin = {}
+        for k in ("uu", "uf", "fu", "ff"):
+            for s in ("_rowptr", "_col", "_val"):
+                pin[k + s] = torch.from_numpy(getattr(pb, k + s)).pin_memory()
+        pin["fs"] = torch.from_numpy(pb.fs).pin_memory()
+
+        class Pinned:
+            pass
+        pp = Pinned()
+        for k2, v2 in pin.items():
+            setattr(pp, k2, v2)
+        pp.nx, pp.ny, pp.nz, pp.n = pb.nx, pb.ny, pb.nz, pb.n
+        bh = torch.from_numpy(pb.b).pin_memory()
+        xh = torch.zeros(n, dtype=torch.float64).pin_memory()
+        h2d = sum(v.numel() * v.element_size() for v in pin.values()) + bh.numel() * 8
+        d2h = xh.numel() * 8
+
+        def e2e_step():
+            h = Tsp(pp)
+            h.setup()
+            inf = h.solve(bh.numpy(), xh.numpy())
+            h.close()
+            return inf
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        e_iters = 0
+        for _ in range(args.steps):
+            e_iters += e2e_step()["iterations"]
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ems = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+        eit = torch.tensor([float(e_iters)], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+            dist.all_reduce(eit, op=dist.ReduceOp.SUM)
+        e2e = {"value": float(eit.item()) / (float(ems.item()) * 1e-3), "unit": "iter/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "what": "tsp_create from pinned host blocks + tsp_setup(MECH|FLOW) + tsp_solve(host b -> host x) + tsp_destroy"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and args.config in ("C1", "C2", "C3", "C4"):
+        cpu = oracle_sample(pb, gpu_iters=infos[-1]["iterations"])
+        cpu["cores"] = 1
+
+    if rank == 0:
+        mean_it = iters / max(args.steps, 1)
+        line = {
+            "metric": "preconditioned FGMRES iters/s", "value": value, "unit": "iter/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "grid": [pb.nx, pb.ny, pb.nz], "dof": n,
+                       "step": "tsp_setup(MECH|FLOW) + FGMRES(64) to rtol 1e-8",
+                       "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas (z-slab sharding not in this build)",
+                       "l2": "inputs larger than L2 (matrices >> 126 MB), no flush"},
+            "iterations_per_step": mean_it,
+            "gdof_per_s": value * n / 1e9,
+            "solve_only": {"iters_per_s": iters / (solve_ms * 1e-3), "ms_per_iter": solve_ms / max(iters, 1),
+                           "setup_ms_per_step": (ms_max - solve_ms) / args.steps,
+                           "apply_gdof_per_s": None},
+            "iteration_roofline": {"bytes_per_iter": bytes_iter, "achieved_gbs": iter_gbs, "peak_gbs": hbm,
+                                   "frac": iter_gbs / hbm, "mean_krylov_index": mean_j},
+            "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+                         "bytes_per_launch": d["bytes"] / d["launches"], "ms_per_launch": d["ms"] / d["launches"]},
+            "kernels": kernel_table,
+            "gpu_launches": int(st["launches"]),
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "true_relres": infos[-1]["true_relres"],
+            "hierarchy_rows": st["rows"],
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

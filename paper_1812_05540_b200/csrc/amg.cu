@@ -11,6 +11,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <ctime>
 
 #include "tsp_internal.cuh"
 
@@ -504,8 +507,22 @@ static void make_coarsest(Ctx &c, Hier &H, Level &L)
     c.launches++;
 }
 
+// TSP_DEBUG=1: synchronise and print the wall time of each setup phase
+static void dbg_mark(Ctx &c, const char *what, int lvl)
+{
+    static const bool on = getenv("TSP_DEBUG") != nullptr;
+    static double last = 0;
+    if (!on) return;
+    cudaStreamSynchronize(c.s);
+    timespec t; clock_gettime(CLOCK_MONOTONIC, &t);
+    double now = t.tv_sec + 1e-9 * t.tv_nsec;
+    if (lvl >= 0) fprintf(stderr, "[tsp setup] level %d %-12s %8.3f ms\n", lvl, what, (now - last) * 1e3);
+    last = now;
+}
+
 void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc)
 {
+    dbg_mark(c, "start", -1);
     H.L.clear();
     H.L.reserve(16);
     H.nc = nc;
@@ -547,6 +564,7 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc)
             c.launches += 4;
             if (d2h1(c, c.dcount.p) == 0) break;
         }
+        dbg_mark(c, "strength+mis", lvl);
         // aggregates
         DBuf<int32_t> flag, rid, ph1;
         flag.alloc(n + 1); rid.alloc(n + 1); ph1.alloc(n);
@@ -591,10 +609,14 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc)
         k_pfill<<<grid_for(n, 128), 128, 0, c.s>>>(n, nc, Lf.A.rp, Lf.A.ci, Lf.A.v, E, Lf.agg, d, om, Lf.P.rp, Lf.P.ci, Lf.P.v, err);
         c.launches += 3;
         TSP_REQUIRE(!d2h1(c, err.p), TSP_ERR_INVALID_ARG, "prolongator row exceeds 512 aggregates");
+        dbg_mark(c, "agg+P", lvl);
         transpose(c, Lf.P, Lf.R, nc);
+        dbg_mark(c, "transpose", lvl);
         Csr AP;
         spgemm(c, Lf.A, Lf.P, AP, nc);
+        dbg_mark(c, "AP", lvl);
         spgemm(c, Lf.R, AP, Lc.A, nc);
+        dbg_mark(c, "RAP", lvl);
     }
     // apply-side layouts and work vectors
     for (size_t l = 0; l < H.L.size(); ++l) {
@@ -607,6 +629,7 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc)
         size_t m = (size_t)std::max(L.n, 1) * nc;
         L.b.alloc(m); L.x.alloc(m); L.x2.alloc(m); L.r.alloc(m);
     }
+    dbg_mark(c, "sell+vectors", 99);
     TSP_CUDA(cudaStreamSynchronize(c.s));
 }
 
@@ -717,7 +740,47 @@ __global__ void k_coarse(int n, const double *__restrict__ inv, const double *__
     x[(int64_t)i * NC + c] = s;
 }
 
+// ---- warp-per-row CSR variants for operators with long rows (coarse levels,
+// restriction): lanes stride a row's entries (coalesced [q][c] values), shuffle reduce.
+// MODE 0: y = A x ; MODE 1: pre (x = D^-1 b, r = b - A D^-1 b) ; MODE 2: post (xo = x + D^-1 (b - A x))
+template <int NC, int MODE>
+__global__ void __launch_bounds__(256) k_csr_warp(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                                                  const double *__restrict__ v, const double *__restrict__ dinv,
+                                                  const double *__restrict__ b, const double *__restrict__ x,
+                                                  double *__restrict__ out1, double *__restrict__ out2)
+{
+    const int lane = threadIdx.x & 31;
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= n) return;
+    double acc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+    const int64_t q1 = rp[i + 1];
+    for (int64_t q = rp[i] + lane; q < q1; q += 32) {
+        const int j = ci[q];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            const double xv = MODE == 1 ? __ldg(b + (int64_t)j * NC + c) * __ldg(dinv + (int64_t)j * NC + c) : __ldg(x + (int64_t)j * NC + c);
+            acc[c] = fma(__ldcs(v + q * NC + c), xv, acc[c]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+        for (int o = 16; o; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+    if (lane < NC) {
+        double a = acc[0];
+#pragma unroll
+        for (int c = 1; c < NC; ++c) if (lane == c) a = acc[c];
+        const int64_t t = (int64_t)i * NC + lane;
+        if (MODE == 0) out1[t] = a;
+        else if (MODE == 1) { out1[t] = b[t] * dinv[t]; out2[t] = b[t] - a; }
+        else out1[t] = x[t] + dinv[t] * (b[t] - a);
+    }
+}
+
 static double sbytes(const Sell &S) { return (double)S.slots * 32 * (4.0 + 8.0 * S.bs); }
+static double cbytes(const Csr &A) { return (double)A.nnz * (4.0 + 8.0 * A.nc); }
+static bool use_warp(const Csr &A) { return A.n > 0 && A.nnz >= 12 * (int64_t)A.n; }
 
 template <int NC>
 static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
@@ -733,20 +796,25 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     }
     const int n = L.n;
     const double vec = 8.0 * NC * n;
+    const bool wA = l > 0 && use_warp(L.A), wR = use_warp(L.R);
+    const double bA = wA ? cbytes(L.A) : sbytes(L.sA), bR = wR ? cbytes(L.R) : sbytes(L.sR);
     prof_begin(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P);
-    k_vc_pre<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sA.off, L.sA.col, L.sA.val, L.dinv, b, L.x2, L.r);
-    prof_end(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P, sbytes(L.sA) + 4 * vec);
+    if (wA) k_csr_warp<NC, 1><<<grid_for(n, 8), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, L.A.v, L.dinv, b, nullptr, L.x2, L.r);
+    else k_vc_pre<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sA.off, L.sA.col, L.sA.val, L.dinv, b, L.x2, L.r);
+    prof_end(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P, bA + 4 * vec);
     Level &Lc = H.L[l + 1];
     prof_begin(c, mech ? PK_VC_RESTR_U : PK_VC_RESTR_P);
-    k_sell_mv<NC><<<grid_for(Lc.n, 256), 256, 0, c.s>>>(Lc.n, L.sR.off, L.sR.col, L.sR.val, L.r, Lc.b);
-    prof_end(c, mech ? PK_VC_RESTR_U : PK_VC_RESTR_P, sbytes(L.sR) + vec + 8.0 * NC * Lc.n);
+    if (wR) k_csr_warp<NC, 0><<<grid_for(Lc.n, 8), 256, 0, c.s>>>(Lc.n, L.R.rp, L.R.ci, L.R.v, nullptr, nullptr, L.r, Lc.b, nullptr);
+    else k_sell_mv<NC><<<grid_for(Lc.n, 256), 256, 0, c.s>>>(Lc.n, L.sR.off, L.sR.col, L.sR.val, L.r, Lc.b);
+    prof_end(c, mech ? PK_VC_RESTR_U : PK_VC_RESTR_P, bR + vec + 8.0 * NC * Lc.n);
     vcycle_rec<NC>(c, H, l + 1, Lc.b, Lc.x);
     prof_begin(c, mech ? PK_VC_PROL_U : PK_VC_PROL_P);
     k_prolong<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sP.off, L.sP.col, L.sP.val, Lc.x, L.x2);
     prof_end(c, mech ? PK_VC_PROL_U : PK_VC_PROL_P, sbytes(L.sP) + 2 * vec + 8.0 * NC * Lc.n);
     prof_begin(c, mech ? PK_VC_POST_U : PK_VC_POST_P);
-    k_vc_post<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sA.off, L.sA.col, L.sA.val, L.dinv, b, L.x2, xout);
-    prof_end(c, mech ? PK_VC_POST_U : PK_VC_POST_P, sbytes(L.sA) + 4 * vec);
+    if (wA) k_csr_warp<NC, 2><<<grid_for(n, 8), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, L.A.v, L.dinv, b, L.x2, xout, nullptr);
+    else k_vc_post<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sA.off, L.sA.col, L.sA.val, L.dinv, b, L.x2, xout);
+    prof_end(c, mech ? PK_VC_POST_U : PK_VC_POST_P, bA + 4 * vec);
     c.launches += 4;
 }
 

@@ -9,7 +9,25 @@
 namespace tsp {
 
 static thread_local std::string g_err;
+thread_local cudaStream_t g_alloc_stream = 0;
 void set_error(const std::string &m) { g_err = m; }
+
+// bind the allocation stream of this API call; keep the default pool resident
+struct StreamScope {
+    explicit StreamScope(cudaStream_t s) {
+        g_alloc_stream = s;
+        static bool pool_set = false;
+        if (!pool_set) {
+            int dev = 0;
+            cudaMemPool_t pool;
+            if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            pool_set = true;
+        }
+    }
+};
 
 void *scratch(Ctx &c, size_t bytes)
 {
@@ -24,23 +42,34 @@ static const char *kProfNames[PK_COUNT] = {
     "op_node", "op_cell", "step2", "step34", "ilu_steps678", "vc_pre_u", "vc_restr_u", "vc_prol_u", "vc_post_u",
     "vc_pre_p", "vc_restr_p", "vc_prol_p", "vc_post_p", "coarse", "mdot", "maxpy", "norm", "vec", "setup"};
 
+// Every launch of a profiled class is bracketed by two events from a pool that
+// grows on demand (up to 4M events); prof_end only closes a record that the
+// matching prof_begin opened.
 void prof_begin(Ctx &c, int cls)
 {
-    if (!c.prof.on) return;
     Prof &p = c.prof;
-    if (p.next + 2 > (int)p.pool.size()) return;
+    p.open = false;
+    if (!p.on) return;
+    if (p.next + 2 > (int)p.pool.size()) {
+        if (p.pool.size() >= (1u << 22)) return;
+        size_t old = p.pool.size();
+        p.pool.resize(old ? 2 * old : 4096);
+        for (size_t k = old; k < p.pool.size(); ++k)
+            if (cudaEventCreate(&p.pool[k]) != cudaSuccess) { p.pool.resize(k); return; }
+        if (p.next + 2 > (int)p.pool.size()) return;
+    }
     p.recs.push_back({cls, p.next, p.next + 1, 0.0});
     cudaEventRecord(p.pool[p.next], c.s);
     p.next += 2;
+    p.open = true;
 }
 void prof_end(Ctx &c, int cls, double bytes)
 {
-    if (!c.prof.on) return;
     Prof &p = c.prof;
-    if (p.recs.empty() || p.recs.back().cls != cls || p.recs.back().bytes != 0.0 || p.recs.back().e1 >= p.next) {
-        if (p.recs.empty() || p.recs.back().cls != cls) return;
-    }
+    if (!p.on || !p.open) return;
+    p.open = false;
     Prof::Rec &r = p.recs.back();
+    if (r.cls != cls) return;
     r.bytes = bytes;
     cudaEventRecord(p.pool[r.e1], c.s);
 }
@@ -51,7 +80,7 @@ using namespace tsp;
 
 struct tsp_ctx : Ctx {};
 
-#define API_BEGIN try {
+#define API_BEGIN try { StreamScope ss_(h ? h->s : (cudaStream_t)0);
 #define API_END                                                                                     \
     }                                                                                               \
     catch (const tsp::Error &e) {                                                                   \
@@ -89,6 +118,7 @@ tsp_status tsp_create(tsp_handle *out, const tsp_desc *d)
     if (!out || !d) { set_error("null argument"); return TSP_ERR_INVALID_ARG; }
     *out = nullptr;
     tsp_ctx *c = nullptr;
+    tsp_handle h = nullptr;
     API_BEGIN
     TSP_REQUIRE(d->nx > 0 && d->ny > 0 && d->nz > 0, TSP_ERR_INVALID_ARG, "grid dimensions must be positive");
     TSP_REQUIRE(d->nranks == 1 && d->rank == 0, TSP_ERR_INVALID_ARG, "this build supports nranks == 1 (see DESIGN.md)");
@@ -102,6 +132,7 @@ tsp_status tsp_create(tsp_handle *out, const tsp_desc *d)
     c->Nc = d->nx * d->ny * d->nz;
     c->n = 3 * (int64_t)c->Nn + 2 * (int64_t)c->Nc;
     c->s = (cudaStream_t)d->stream;
+    StreamScope ss2_(c->s);
     c->o = d->opts;
     if (c->o.amg_theta <= 0 || c->o.amg_coarse_max <= 0) tsp_default_options(&c->o);
     if (c->o.zblock <= 0) c->o.zblock = 16;
@@ -136,6 +167,7 @@ tsp_status tsp_create(tsp_handle *out, const tsp_desc *d)
     }
     catch (const tsp::Error &e) {
         set_error(e.msg);
+        (void)h;
         delete c;
         return e.st;
     }
@@ -278,10 +310,6 @@ tsp_status tsp_prof_enable(tsp_handle h, int on)
     API_BEGIN
     Prof &p = h->prof;
     TSP_CUDA(cudaStreamSynchronize(h->s));
-    if (on && p.pool.empty()) {
-        p.pool.resize(1 << 16);
-        for (auto &e : p.pool) TSP_CUDA(cudaEventCreate(&e));
-    }
     p.recs.clear();
     p.next = 0;
     p.on = on != 0;
@@ -310,6 +338,7 @@ tsp_status tsp_prof_read(tsp_handle h, tsp_prof *out)
 void tsp_destroy(tsp_handle h)
 {
     if (!h) return;
+    StreamScope ss_(h->s);
     cudaStreamSynchronize(h->s);
     for (auto &e : h->prof.pool) cudaEventDestroy(e);
     delete h;

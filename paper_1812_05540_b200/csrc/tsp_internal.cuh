@@ -29,6 +29,9 @@ struct Error {
     } while (0)
 
 // ------------------------------------------------------------------ device buffers
+// Stream-ordered allocation (cudaMallocAsync on the stream of the API call in
+// progress, pool kept resident): setup allocates per level without device syncs.
+extern thread_local cudaStream_t g_alloc_stream;
 template <class T>
 struct DBuf {
     T *p = nullptr;
@@ -42,10 +45,10 @@ struct DBuf {
     void alloc(size_t count) {
         release();
         n = count;
-        if (count) TSP_CUDA(cudaMalloc((void **)&p, sizeof(T) * count));
+        if (count) TSP_CUDA(cudaMallocAsync((void **)&p, sizeof(T) * count, g_alloc_stream));
     }
     void zero(cudaStream_t s) { if (n) TSP_CUDA(cudaMemsetAsync(p, 0, sizeof(T) * n, s)); }
-    void release() { if (p) cudaFree(p); p = nullptr; n = 0; }
+    void release() { if (p) cudaFreeAsync(p, g_alloc_stream); p = nullptr; n = 0; }
     operator T *() const { return p; }
 };
 
@@ -105,6 +108,7 @@ struct Prof {
     struct Rec { int cls; int e0, e1; double bytes; };
     std::vector<Rec> recs;
     int next = 0;
+    bool open = false;
 };
 
 // ------------------------------------------------------------------ the handle

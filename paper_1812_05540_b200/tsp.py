@@ -152,7 +152,7 @@ class Tsp:
         keep = []
 
         def arr(x):
-            if device_inputs:
+            if device_inputs or hasattr(x, "data_ptr"):   # CUDA tensors, or pinned host tensors
                 keep.append(x)
                 return _ptr(x)
             y = np.ascontiguousarray(x)

@@ -73,7 +73,7 @@ DEFAULTS = dict(
     nu=0.25, biot=1.0, gravity=9.81, dt=86400.0,
     rho_w0=1035.0, rho_nw0=863.0, c_w=4.34e-10, c_nw=1.98e-10,
     mu_w=1e-3, mu_nw=5e-3, rho_s=2650.0, p0=1e7, swr=0.2, snwr=0.2,
-    well_dbhp=5e6, rw_over_h=0.1, state_dp=0.0, p_unit=1e6, length=100.0, wells=1, dirichlet_bottom=1, row_scale=1,
+    well_dbhp=5e6, rw_over_h=0.1, state_dp=0.0, p_unit=1e6, length=10000.0, wells=1, dirichlet_bottom=1, row_scale=1,
     seed=0, recipe=1,
 )
 
