@@ -94,6 +94,43 @@ __global__ void __launch_bounds__(KB) k_maxpy(int64_t n, int nv, const double *_
     }
 }
 
+// CGS2 pass 1 axpy fused with pass 2 dots: w -= V h ; part[t][blk] = sum_r V_t[r] w[r]
+// (V is read once for both; the second read hits L1/L2).  Per-warp shuffle
+// reductions accumulated in a fixed order: deterministic.
+__global__ void __launch_bounds__(KB) k_maxpy_mdot(int64_t n, int nv, const double *__restrict__ V, int64_t ldv,
+                                                   const double *__restrict__ h, double *__restrict__ w,
+                                                   double *__restrict__ part, int nblk)
+{
+    __shared__ double hs[128];
+    __shared__ double sacc[KB / 32][128];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int t = threadIdx.x; t < nv; t += KB) hs[t] = h[t];
+    for (int t = lane; t < nv; t += 32) sacc[wid][t] = 0.0;
+    __syncthreads();
+    const int64_t stride = (int64_t)nblk * KB;
+    const int64_t nround = (n + stride - 1) / stride;
+    for (int64_t k = 0; k < nround; ++k) {
+        const int64_t r = k * stride + blockIdx.x * (int64_t)KB + threadIdx.x;
+        const bool ok = r < n;
+        double acc = ok ? w[r] : 0.0;
+        if (ok) {
+            for (int t = 0; t < nv; ++t) acc = fma(-hs[t], V[t * ldv + r], acc);
+            w[r] = acc;
+        }
+        for (int t = 0; t < nv; ++t) {
+            double d = ok ? V[t * ldv + r] * acc : 0.0;
+            for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            if (lane == 0) sacc[wid][t] += d;
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < nv; t += KB) {
+        double s = 0.0;
+        for (int u = 0; u < KB / 32; ++u) s += sacc[u][t];
+        part[(int64_t)t * nblk + blockIdx.x] = s;
+    }
+}
+
 // x += Z y
 __global__ void __launch_bounds__(KB) k_update(int64_t n, int k, const double *__restrict__ Z, int64_t ldz,
                                                const double *__restrict__ y, double *__restrict__ x)
@@ -140,6 +177,14 @@ struct Kr {
         k_maxpy<false><<<nblk, KB, 0, c.s>>>(n, nv, V, n, h, w, nullptr, nblk);
         prof_end(c, PK_AXPY, 8.0 * n * (nv + 2));
         c.launches++;
+    }
+    // w -= V h1 ; h2 = V^T w  (CGS2 pass-1 update fused with pass-2 projections)
+    void maxpy_mdot(const double *V, int nv, const double *h1, double *w, double *h2) {
+        prof_begin(c, PK_AXPY);
+        k_maxpy_mdot<<<nblk, KB, 0, c.s>>>(n, nv, V, n, h1, w, c.kpart, nblk);
+        k_reduce<<<nv, 256, 0, c.s>>>(nv, c.kpart, nblk, h2, 0);
+        prof_end(c, PK_AXPY, 8.0 * n * (nv + 2));
+        c.launches += 2;
     }
     // w -= V h and ||w|| -> *nrm
     void maxpy_norm(const double *V, int nv, const double *h, double *w, double *nrm) {
@@ -225,8 +270,7 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
                 op_apply(c, zj, w);                    // w = A z_j
                 // CGS2
                 K.mdot(V, j + 1, w, dh, 0);
-                K.maxpy(V, j + 1, dh, w);
-                K.mdot(V, j + 1, w, dh2, 0);
+                K.maxpy_mdot(V, j + 1, dh, w, dh2);
                 K.maxpy_norm(V, j + 1, dh2, w, dh + j + 1);
                 k_add_into<<<1, 128, 0, c.s>>>(j + 1, dh2, dh);
                 c.launches++;
