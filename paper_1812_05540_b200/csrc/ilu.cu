@@ -3,196 +3,395 @@
 // P:606-612 read as tile-local 2x2-block ILU(0) of the interleaved S_ff^FS
 // (DESIGN.md R-ilu: block Jacobi over fixed 16^3 tiles, natural order inside).
 //
-// On the 7-point TPFA pattern ILU(0) produces no update of off-diagonal blocks
-// (a lower neighbour's upper neighbours are never neighbours of the row), so
-//   U_KJ = A_KJ (J > K),  L_KJ = A_KJ U_JJ^-1 (J < K),
-//   U_KK = A_KK - sum_{J < K, same tile} A_KJ U_JJ^-1 A_JK,
-// and the solve needs only A and D^-1 = U_KK^-1:
-//   forward   yhat_K = D_K^-1 (w_K - sum_{J<K} A_KJ yhat_J)
-//   backward  x_K    = yhat_K - D_K^-1 sum_{J>K} A_KJ x_J
-// One CTA per tile walks the i+j+k wavefronts (46 levels for 16^3) with the tile
-// vector in shared memory.  The oracle instead runs textbook IKJ block ILU(0).
+// On the 7-point pattern ILU(0) only updates diagonal blocks (a lower
+// neighbour's upper neighbours are never neighbours of the row), so with
+// D_K = U_KK^-1:
+//   U_KK = A_KK - sum_{J<K, same tile} A_KJ D_J A_JK
+//   forward   yhat_K = D_K (w_K - sum_{J<K} A_KJ yhat_J)
+//   backward  x_K    = yhat_K - D_K sum_{J>K} A_KJ x_J
+// B200 mapping: one CTA per tile; the tile is swept by x-LINES in (j+k)
+// wavefront order (31 levels for 16^3 instead of 46 cell levels), each line
+// held by a W-lane warp segment.  Inside a line the x-recurrence is affine,
+//   yhat_i = M_i yhat_{i-1} + c_i,  M_i = -D_i A_{i,-x},  c_i = D_i (w_i - y/z terms),
+// and is solved by a log2(W)-step segmented shuffle scan of (M, c) pairs (same
+// ILU(0) operator, different association of the products).  Every global access
+// is along x: coalesced.  The tile vector lives in shared memory.  The oracle
+// runs textbook IKJ block ILU(0) cell by cell.
 #include <algorithm>
 
 #include "tsp_internal.cuh"
 
 namespace tsp {
 
-// slot order: 0 -z, 1 -y, 2 -x, 3 self, 4 +x, 5 +y, 6 +z  (lower = 0..2, upper = 4..6)
-__constant__ int c_dx[7] = {0, 0, -1, 0, 1, 0, 0};
-__constant__ int c_dy[7] = {0, -1, 0, 0, 0, 1, 0};
-__constant__ int c_dz[7] = {-1, 0, 0, 0, 0, 0, 1};
-
+// slot order: 0 -z, 1 -y, 2 -x, 3 self, 4 +x, 5 +y, 6 +z
 struct TileGeo {
-    int nx, ny, nz, tx, ty, tz, ntx, nty, ntz, T, Tpad;
+    int nx, ny, nz, tx, ty, tz, ntx, nty, ntz, W, nlev;
 };
 
-__device__ __forceinline__ int64_t ival_idx(const TileGeo &g, int64_t t, int p, int k, int e)
+__device__ __forceinline__ int64_t vidx(const TileGeo &g, int64_t t, int lk, int lj, int s, int e, int li)
 {
-    return ((((t * (g.Tpad >> 5) + (p >> 5)) * 7 + k) * 4 + e) << 5) + (p & 31);
+    return (((((t * g.tz + lk) * g.ty + lj) * 7 + s) * 4 + e) * g.W) + li;
 }
-__device__ __forceinline__ int64_t idinv_idx(const TileGeo &g, int64_t t, int p, int e)
+__device__ __forceinline__ int64_t didx(const TileGeo &g, int64_t t, int lk, int lj, int e, int li)
 {
-    return (((t * (g.Tpad >> 5) + (p >> 5)) * 4 + e) << 5) + (p & 31);
+    return ((((t * g.tz + lk) * g.ty + lj) * 4 + e) * g.W) + li;
 }
+__device__ __forceinline__ int sidx(const TileGeo &g, int lk, int lj, int li) { return ((lk * g.ty + lj) * g.tx + li) * 2; }
 
 // fill the tile-ordered S_ff^FS = A_ff + diag(D_sp, D_pp) blocks (a1 folded in)
 __global__ void k_ilu_fill(TileGeo g, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
-                           const double *__restrict__ v, const double *__restrict__ fs, const int32_t *__restrict__ posmap,
-                           double *__restrict__ ival)
+                           const double *__restrict__ v, const double *__restrict__ fs, double *__restrict__ ival)
 {
     int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= (int64_t)g.nx * g.ny * g.nz) return;
-    int i = c % g.nx, j = (c / g.nx) % g.ny, k = c / ((int64_t)g.nx * g.ny);
-    int TI = i / g.tx, TJ = j / g.ty, TK = k / g.tz;
-    int64_t t = ((int64_t)TK * g.nty + TJ) * g.ntx + TI;
-    int li = i - TI * g.tx, lj = j - TJ * g.ty, lk = k - TK * g.tz;
-    int p = posmap[(lk * g.ty + lj) * g.tx + li];
+    const int i = c % g.nx, j = (c / g.nx) % g.ny, k = c / ((int64_t)g.nx * g.ny);
+    const int TI = i / g.tx, TJ = j / g.ty, TK = k / g.tz;
+    const int64_t t = ((int64_t)TK * g.nty + TJ) * g.ntx + TI;
+    const int li = i - TI * g.tx, lj = j - TJ * g.ty, lk = k - TK * g.tz;
     for (int s = 0; s < 7; ++s)
-        for (int e = 0; e < 4; ++e) ival[ival_idx(g, t, p, s, e)] = 0.0;
+        for (int e = 0; e < 4; ++e) ival[vidx(g, t, lk, lj, s, e, li)] = 0.0;
+    const int dxs[7] = {0, 0, -1, 0, 1, 0, 0}, dys[7] = {0, -1, 0, 0, 0, 1, 0}, dzs[7] = {-1, 0, 0, 0, 0, 0, 1};
     for (int64_t q = rp[c]; q < rp[c + 1]; ++q) {
-        int64_t d = ci[q];
-        int di = (int)(d % g.nx) - i, dj = (int)((d / g.nx) % g.ny) - j, dk = (int)(d / ((int64_t)g.nx * g.ny)) - k;
+        const int64_t d = ci[q];
+        const int di = (int)(d % g.nx) - i, dj = (int)((d / g.nx) % g.ny) - j, dk = (int)(d / ((int64_t)g.nx * g.ny)) - k;
         int s = -1;
-        for (int u = 0; u < 7; ++u) if (c_dx[u] == di && c_dy[u] == dj && c_dz[u] == dk) s = u;
-        if (s < 0) continue;   // not a 7-point neighbour (never happens for TPFA input)
+        for (int u = 0; u < 7; ++u) if (dxs[u] == di && dys[u] == dj && dzs[u] == dk) s = u;
+        if (s < 0) continue;
         for (int e = 0; e < 4; ++e) {
             double a = v[q * 4 + e];
             if (s == 3 && e == 1) a += fs[2 * c];      // A_sp^FS = A_sp + D_sp
             if (s == 3 && e == 3) a += fs[2 * c + 1];  // A_pp^FS = A_pp + D_pp
-            ival[ival_idx(g, t, p, s, e)] = a;
+            ival[vidx(g, t, lk, lj, s, e, li)] = a;
         }
     }
 }
 
-__device__ __forceinline__ void ld4(const double *__restrict__ a, const TileGeo &g, int64_t t, int p, int s, double r[4])
+__device__ __forceinline__ void ld2x2(const double *__restrict__ a, const TileGeo &g, int64_t t, int lk, int lj, int s, int li, double r[4])
 {
-    for (int e = 0; e < 4; ++e) r[e] = a[ival_idx(g, t, p, s, e)];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) r[e] = a[vidx(g, t, lk, lj, s, e, li)];
+}
+__device__ __forceinline__ void mm2(const double a[4], const double b[4], double r[4])
+{
+    r[0] = a[0] * b[0] + a[1] * b[2]; r[1] = a[0] * b[1] + a[1] * b[3];
+    r[2] = a[2] * b[0] + a[3] * b[2]; r[3] = a[2] * b[1] + a[3] * b[3];
 }
 
-// a5: U_KK = A_KK - sum_{J<K in tile} A_KJ U_JJ^-1 A_JK ; store U_KK^-1 (perturbed if singular)
-__global__ void __launch_bounds__(256) k_ilu_factor(TileGeo g, const int32_t *__restrict__ lvlptr, int nlev,
-                                                    const int32_t *__restrict__ cells, const int32_t *__restrict__ posmap,
-                                                    const double *__restrict__ ival, double *__restrict__ dinv,
-                                                    unsigned long long *__restrict__ npert)
+// a5: one thread per x-line, lines in (j+k) order, cells along x sequential
+__global__ void k_ilu_factor(TileGeo g, const int32_t *__restrict__ lines, const int32_t *__restrict__ lvlptr,
+                             const double *__restrict__ ival, double *__restrict__ dinv, unsigned long long *__restrict__ npert)
 {
     const int64_t t = blockIdx.x;
     const int TI = t % g.ntx, TJ = (t / g.ntx) % g.nty, TK = t / ((int64_t)g.ntx * g.nty);
-    for (int l = 0; l < nlev; ++l) {
+    for (int l = 0; l < g.nlev; ++l) {
         for (int idx = lvlptr[l] + threadIdx.x; idx < lvlptr[l + 1]; idx += blockDim.x) {
-            int pk = cells[idx];
-            int li = pk & 255, lj = (pk >> 8) & 255, lk = pk >> 16;
-            if (TI * g.tx + li >= g.nx || TJ * g.ty + lj >= g.ny || TK * g.tz + lk >= g.nz) continue;
-            int p = idx;
-            double U[4];
-            ld4(ival, g, t, p, 3, U);
-            for (int s = 0; s < 3; ++s) {
-                int ni = li + c_dx[s], nj = lj + c_dy[s], nk = lk + c_dz[s];
-                if (ni < 0 || nj < 0 || nk < 0) continue;   // outside the tile (or domain): dropped
-                int pn = posmap[(nk * g.ty + nj) * g.tx + ni];
-                double A[4], B[4], D[4];
-                ld4(ival, g, t, p, s, A);          // A_KJ
-                ld4(ival, g, t, pn, 6 - s, B);     // A_JK (J's block toward K)
-                for (int e = 0; e < 4; ++e) D[e] = dinv[idinv_idx(g, t, pn, e)];
-                double L0 = A[0] * D[0] + A[1] * D[2], L1 = A[0] * D[1] + A[1] * D[3];
-                double L2 = A[2] * D[0] + A[3] * D[2], L3 = A[2] * D[1] + A[3] * D[3];
-                U[0] -= L0 * B[0] + L1 * B[2]; U[1] -= L0 * B[1] + L1 * B[3];
-                U[2] -= L2 * B[0] + L3 * B[2]; U[3] -= L2 * B[1] + L3 * B[3];
+            const int lj = lines[idx] & 0xffff, lk = lines[idx] >> 16;
+            if (TJ * g.ty + lj >= g.ny || TK * g.tz + lk >= g.nz) continue;
+            const int len = min(g.tx, g.nx - TI * g.tx);
+            for (int li = 0; li < len; ++li) {
+                double U[4];
+                ld2x2(ival, g, t, lk, lj, 3, li, U);
+                for (int s = 0; s < 3; ++s) {
+                    int nlk = lk, nlj = lj, nli = li;
+                    if (s == 0) nlk--; else if (s == 1) nlj--; else nli--;
+                    if (nlk < 0 || nlj < 0 || nli < 0) continue;   // outside the tile: dropped (block Jacobi)
+                    double A[4], B[4], D[4], L[4], T[4];
+                    ld2x2(ival, g, t, lk, lj, s, li, A);          // A_KJ
+                    ld2x2(ival, g, t, nlk, nlj, 6 - s, nli, B);   // A_JK
+                    for (int e = 0; e < 4; ++e) D[e] = dinv[didx(g, t, nlk, nlj, e, nli)];
+                    mm2(A, D, L); mm2(L, B, T);
+                    for (int e = 0; e < 4; ++e) U[e] -= T[e];
+                }
+                const double sc = fmax(fmax(fabs(U[0]), fabs(U[1])), fmax(fabs(U[2]), fabs(U[3])));
+                double det = U[0] * U[3] - U[1] * U[2];
+                if (sc == 0.0 || fabs(det) <= 1e-14 * sc * sc) {   // singular pivot: perturb
+                    const double dl = 1e-12 * (sc > 0.0 ? sc : 1.0);
+                    U[0] += dl; U[3] += dl;
+                    det = U[0] * U[3] - U[1] * U[2];
+                    atomicAdd(npert, 1ULL);
+                }
+                dinv[didx(g, t, lk, lj, 0, li)] = U[3] / det;
+                dinv[didx(g, t, lk, lj, 1, li)] = -U[1] / det;
+                dinv[didx(g, t, lk, lj, 2, li)] = -U[2] / det;
+                dinv[didx(g, t, lk, lj, 3, li)] = U[0] / det;
             }
-            double sc = fmax(fmax(fabs(U[0]), fabs(U[1])), fmax(fabs(U[2]), fabs(U[3])));
-            double det = U[0] * U[3] - U[1] * U[2];
-            if (sc == 0.0 || fabs(det) <= 1e-14 * sc * sc) {
-                double dl = 1e-12 * (sc > 0.0 ? sc : 1.0);
-                U[0] += dl; U[3] += dl;
-                det = U[0] * U[3] - U[1] * U[2];
-                atomicAdd(npert, 1ULL);
-            }
-            dinv[idinv_idx(g, t, p, 0)] = U[3] / det;
-            dinv[idinv_idx(g, t, p, 1)] = -U[1] / det;
-            dinv[idinv_idx(g, t, p, 2)] = -U[2] / det;
-            dinv[idinv_idx(g, t, p, 3)] = U[0] / det;
         }
         __syncthreads();
     }
 }
 
-// steps 6-8 fused: w = y - S^FS z (all neighbours, global z), forward/backward
-// tile solve, z_out = z + dz (interleaved)
-__global__ void __launch_bounds__(256) k_ilu_apply(TileGeo g, const int32_t *__restrict__ lvlptr, int nlev,
-                                                   const int32_t *__restrict__ cells, const int32_t *__restrict__ posmap,
+// segmented affine scan over lanes of width W: x_i = M_i x_{i-dir} + c_i
+template <bool FORWARD>
+__device__ __forceinline__ void affine_scan(double M[4], double c[2], int lseg, int W)
+{
+    for (int off = 1; off < W; off <<= 1) {
+        double Mp[4], cp[2];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) Mp[e] = FORWARD ? __shfl_up_sync(0xffffffffu, M[e], off, W) : __shfl_down_sync(0xffffffffu, M[e], off, W);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) cp[e] = FORWARD ? __shfl_up_sync(0xffffffffu, c[e], off, W) : __shfl_down_sync(0xffffffffu, c[e], off, W);
+        const bool take = FORWARD ? (lseg >= off) : (lseg + off < W);
+        if (take) {
+            const double c0 = M[0] * cp[0] + M[1] * cp[1] + c[0];
+            const double c1 = M[2] * cp[0] + M[3] * cp[1] + c[1];
+            double R[4];
+            mm2(M, Mp, R);
+            c[0] = c0; c[1] = c1;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) M[e] = R[e];
+        }
+    }
+}
+
+// steps 6-8 fused, pipelined form:
+//  phase 0 (fully parallel, coalesced): w = y - S^FS z for every cell of the tile -> shared memory
+//  forward / backward line wavefronts: per level only 4 blocks per cell are read from global
+//  memory, and they are prefetched into registers one level ahead (before the barrier).
+// One line per W-lane segment; requires (lines per level) <= segments per CTA.
+__device__ __forceinline__ void pf_load(const double *__restrict__ ival, const double *__restrict__ dinv, const TileGeo &g,
+                                        int64_t t, int lk, int lj, int li, bool ok, const int s3[3], double P[16])
+{
+    if (!ok) return;
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) P[4 * q + e] = ival[vidx(g, t, lk, lj, s3[q], e, li)];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) P[12 + e] = dinv[didx(g, t, lk, lj, e, li)];
+}
+
+__global__ void __launch_bounds__(256) k_ilu_apply2(TileGeo g, const int32_t *__restrict__ lines, const int32_t *__restrict__ lvlptr,
+                                                    const double *__restrict__ ival, const double *__restrict__ dinv,
+                                                    const double *__restrict__ yf, const double *__restrict__ zs,
+                                                    const double *__restrict__ zp, double *__restrict__ zout)
+{
+    extern __shared__ double sm[];   // [lk][lj][li][2]: w, then yhat, then x
+    const int64_t t = blockIdx.x;
+    const int TI = t % g.ntx, TJ = (t / g.ntx) % g.nty, TK = t / ((int64_t)g.ntx * g.nty);
+    const int64_t sy = g.nx, sz = (int64_t)g.nx * g.ny;
+    const int W = g.W, lane = threadIdx.x & 31, lseg = lane & (W - 1);
+    const int slot0 = (threadIdx.x >> 5) * (32 / W) + lane / W, nslots = (blockDim.x >> 5) * (32 / W);
+    const int li = lseg, gi = TI * g.tx + li;
+    const bool xin = li < g.tx && gi < g.nx;
+    // ---------------- phase 0: w = y - S^FS z (step 6)
+    for (int line = slot0; line < g.ty * g.tz; line += nslots) {
+        const int lj = line % g.ty, lk = line / g.ty;
+        const int gj = TJ * g.ty + lj, gk = TK * g.tz + lk;
+        if (!(xin && gj < g.ny && gk < g.nz)) continue;
+        const int64_t gc = gi + sy * gj + sz * gk;
+        double r0 = yf[2 * gc], r1 = yf[2 * gc + 1];
+        const int dxs[7] = {0, 0, -1, 0, 1, 0, 0}, dys[7] = {0, -1, 0, 0, 0, 1, 0}, dzs[7] = {-1, 0, 0, 0, 0, 0, 1};
+#pragma unroll
+        for (int s = 0; s < 7; ++s) {
+            const int ni = gi + dxs[s], nj = gj + dys[s], nk = gk + dzs[s];
+            if (ni < 0 || nj < 0 || nk < 0 || ni >= g.nx || nj >= g.ny || nk >= g.nz) continue;
+            const int64_t gn = gc + dxs[s] + dys[s] * sy + dzs[s] * sz;
+            double A[4];
+            ld2x2(ival, g, t, lk, lj, s, li, A);
+            const double z0 = zs[gn], z1 = zp[gn];
+            r0 -= A[0] * z0 + A[1] * z1;
+            r1 -= A[2] * z0 + A[3] * z1;
+        }
+        sm[sidx(g, lk, lj, li)] = r0;
+        sm[sidx(g, lk, lj, li) + 1] = r1;
+    }
+    // ---------------- forward
+    const int fw[3] = {1, 0, 2}, bw[3] = {5, 6, 4};   // (-y, -z, -x) and (+y, +z, +x)
+    double P[16];
+    {
+        const int idx = lvlptr[0] + slot0;
+        const bool lv = idx < lvlptr[1];
+        const int lj = lv ? (lines[idx] & 0xffff) : 0, lk = lv ? (lines[idx] >> 16) : 0;
+        pf_load(ival, dinv, g, t, lk, lj, li, lv && xin && TJ * g.ty + lj < g.ny && TK * g.tz + lk < g.nz, fw, P);
+    }
+    __syncthreads();
+    for (int l = 0; l < g.nlev; ++l) {
+        const int idx = lvlptr[l] + slot0;
+        const bool lv = idx < lvlptr[l + 1];
+        const int lj = lv ? (lines[idx] & 0xffff) : 0, lk = lv ? (lines[idx] >> 16) : 0;
+        const bool ok = lv && xin && TJ * g.ty + lj < g.ny && TK * g.tz + lk < g.nz;
+        double M[4] = {0, 0, 0, 0}, c[2] = {0, 0};
+        if (ok) {
+            double r0 = sm[sidx(g, lk, lj, li)], r1 = sm[sidx(g, lk, lj, li) + 1];
+            if (lj > 0) {
+                const double y0 = sm[sidx(g, lk, lj - 1, li)], y1 = sm[sidx(g, lk, lj - 1, li) + 1];
+                r0 -= P[0] * y0 + P[1] * y1; r1 -= P[2] * y0 + P[3] * y1;
+            }
+            if (lk > 0) {
+                const double y0 = sm[sidx(g, lk - 1, lj, li)], y1 = sm[sidx(g, lk - 1, lj, li) + 1];
+                r0 -= P[4] * y0 + P[5] * y1; r1 -= P[6] * y0 + P[7] * y1;
+            }
+            const double *D = P + 12;
+            c[0] = D[0] * r0 + D[1] * r1;
+            c[1] = D[2] * r0 + D[3] * r1;
+            if (li > 0) {
+                double T[4]; mm2(D, P + 8, T);
+                M[0] = -T[0]; M[1] = -T[1]; M[2] = -T[2]; M[3] = -T[3];
+            }
+        }
+        affine_scan<true>(M, c, lseg, W);
+        if (ok) { sm[sidx(g, lk, lj, li)] = c[0]; sm[sidx(g, lk, lj, li) + 1] = c[1]; }
+        // prefetch the next level's blocks (or the backward sweep's first level)
+        {
+            const int ln = l + 1 < g.nlev ? l + 1 : g.nlev - 1;
+            const int idn = lvlptr[ln] + slot0;
+            const bool lvn = idn < lvlptr[ln + 1];
+            const int ljn = lvn ? (lines[idn] & 0xffff) : 0, lkn = lvn ? (lines[idn] >> 16) : 0;
+            pf_load(ival, dinv, g, t, lkn, ljn, li, lvn && xin && TJ * g.ty + ljn < g.ny && TK * g.tz + lkn < g.nz,
+                    l + 1 < g.nlev ? fw : bw, P);
+        }
+        __syncthreads();
+    }
+    // ---------------- backward
+    for (int l = g.nlev - 1; l >= 0; --l) {
+        const int idx = lvlptr[l] + slot0;
+        const bool lv = idx < lvlptr[l + 1];
+        const int lj = lv ? (lines[idx] & 0xffff) : 0, lk = lv ? (lines[idx] >> 16) : 0;
+        const int gj = TJ * g.ty + lj, gk = TK * g.tz + lk;
+        const bool ok = lv && xin && gj < g.ny && gk < g.nz;
+        double M[4] = {0, 0, 0, 0}, c[2] = {0, 0};
+        if (ok) {
+            double t0 = 0, t1 = 0;
+            if (lj + 1 < g.ty && gj + 1 < g.ny) {
+                const double x0 = sm[sidx(g, lk, lj + 1, li)], x1 = sm[sidx(g, lk, lj + 1, li) + 1];
+                t0 += P[0] * x0 + P[1] * x1; t1 += P[2] * x0 + P[3] * x1;
+            }
+            if (lk + 1 < g.tz && gk + 1 < g.nz) {
+                const double x0 = sm[sidx(g, lk + 1, lj, li)], x1 = sm[sidx(g, lk + 1, lj, li) + 1];
+                t0 += P[4] * x0 + P[5] * x1; t1 += P[6] * x0 + P[7] * x1;
+            }
+            const double *D = P + 12;
+            c[0] = sm[sidx(g, lk, lj, li)] - (D[0] * t0 + D[1] * t1);
+            c[1] = sm[sidx(g, lk, lj, li) + 1] - (D[2] * t0 + D[3] * t1);
+            if (li + 1 < g.tx && gi + 1 < g.nx) {
+                double T[4]; mm2(D, P + 8, T);
+                M[0] = -T[0]; M[1] = -T[1]; M[2] = -T[2]; M[3] = -T[3];
+            }
+        }
+        affine_scan<false>(M, c, lseg, W);
+        if (ok) {
+            sm[sidx(g, lk, lj, li)] = c[0]; sm[sidx(g, lk, lj, li) + 1] = c[1];
+            const int64_t gc = gi + sy * gj + sz * gk;
+            zout[2 * gc] = zs[gc] + c[0];        // step 8
+            zout[2 * gc + 1] = zp[gc] + c[1];
+        }
+        if (l > 0) {
+            const int idn = lvlptr[l - 1] + slot0;
+            const bool lvn = idn < lvlptr[l];
+            const int ljn = lvn ? (lines[idn] & 0xffff) : 0, lkn = lvn ? (lines[idn] >> 16) : 0;
+            pf_load(ival, dinv, g, t, lkn, ljn, li, lvn && xin && TJ * g.ty + ljn < g.ny && TK * g.tz + lkn < g.nz, bw, P);
+        }
+        __syncthreads();
+    }
+}
+
+// (first version, kept for reference/validation: w computed inside the forward sweep)
+__global__ void __launch_bounds__(256) k_ilu_apply(TileGeo g, const int32_t *__restrict__ lines, const int32_t *__restrict__ lvlptr,
                                                    const double *__restrict__ ival, const double *__restrict__ dinv,
                                                    const double *__restrict__ yf, const double *__restrict__ zs,
                                                    const double *__restrict__ zp, double *__restrict__ zout)
 {
-    extern __shared__ double sm[];   // [Tpad][2]
+    extern __shared__ double sm[];   // [lk][lj][li][2]
     const int64_t t = blockIdx.x;
     const int TI = t % g.ntx, TJ = (t / g.ntx) % g.nty, TK = t / ((int64_t)g.ntx * g.nty);
-    const int64_t sx = 1, sy = g.nx, sz = (int64_t)g.nx * g.ny;
-    for (int l = 0; l < nlev; ++l) {
-        for (int idx = lvlptr[l] + threadIdx.x; idx < lvlptr[l + 1]; idx += blockDim.x) {
-            int pk = cells[idx];
-            int li = pk & 255, lj = (pk >> 8) & 255, lk = pk >> 16;
-            int gi = TI * g.tx + li, gj = TJ * g.ty + lj, gk = TK * g.tz + lk;
-            if (gi >= g.nx || gj >= g.ny || gk >= g.nz) continue;
-            int64_t gc = gi + sy * gj + sz * gk;
-            double r0 = yf[2 * gc], r1 = yf[2 * gc + 1];
-            // step 6: w = y - S^FS z over all 7 neighbours
+    const int64_t sy = g.nx, sz = (int64_t)g.nx * g.ny;
+    const int W = g.W, lane = threadIdx.x & 31, lseg = lane & (W - 1);
+    const int slot0 = (threadIdx.x >> 5) * (32 / W) + lane / W, nslots = (blockDim.x >> 5) * (32 / W);
+    const int li = lseg, gi = TI * g.tx + li;
+    const bool xin = li < g.tx && gi < g.nx;
+    // ---------------- forward
+    for (int l = 0; l < g.nlev; ++l) {
+        for (int base = lvlptr[l]; base < lvlptr[l + 1]; base += nslots) {
+            const int idx = base + slot0;
+            const bool lv = idx < lvlptr[l + 1];
+            const int lj = lv ? (lines[idx] & 0xffff) : 0, lk = lv ? (lines[idx] >> 16) : 0;
+            const int gj = TJ * g.ty + lj, gk = TK * g.tz + lk;
+            const bool ok = lv && xin && gj < g.ny && gk < g.nz;
+            double M[4] = {0, 0, 0, 0}, c[2] = {0, 0};
+            if (ok) {
+                const int64_t gc = gi + sy * gj + sz * gk;
+                double r0 = yf[2 * gc], r1 = yf[2 * gc + 1];
+                // step 6: w = y - S^FS z over the 7-point stencil (z from global, neighbours across tiles included)
+                const int dxs[7] = {0, 0, -1, 0, 1, 0, 0}, dys[7] = {0, -1, 0, 0, 0, 1, 0}, dzs[7] = {-1, 0, 0, 0, 0, 0, 1};
 #pragma unroll
-            for (int s = 0; s < 7; ++s) {
-                int ni = gi + c_dx[s], nj = gj + c_dy[s], nk = gk + c_dz[s];
-                if (ni < 0 || nj < 0 || nk < 0 || ni >= g.nx || nj >= g.ny || nk >= g.nz) continue;
-                int64_t gn = gc + c_dx[s] * sx + c_dy[s] * sy + c_dz[s] * sz;
-                double a0 = ival[ival_idx(g, t, idx, s, 0)], a1 = ival[ival_idx(g, t, idx, s, 1)];
-                double a2 = ival[ival_idx(g, t, idx, s, 2)], a3 = ival[ival_idx(g, t, idx, s, 3)];
-                double z0 = zs[gn], z1 = zp[gn];
-                r0 -= a0 * z0 + a1 * z1;
-                r1 -= a2 * z0 + a3 * z1;
-            }
-            // forward: r -= sum_{lower in tile} A_KJ yhat_J
+                for (int s = 0; s < 7; ++s) {
+                    const int ni = gi + dxs[s], nj = gj + dys[s], nk = gk + dzs[s];
+                    if (ni < 0 || nj < 0 || nk < 0 || ni >= g.nx || nj >= g.ny || nk >= g.nz) continue;
+                    const int64_t gn = gc + dxs[s] + dys[s] * sy + dzs[s] * sz;
+                    double A[4];
+                    ld2x2(ival, g, t, lk, lj, s, li, A);
+                    const double z0 = zs[gn], z1 = zp[gn];
+                    r0 -= A[0] * z0 + A[1] * z1;
+                    r1 -= A[2] * z0 + A[3] * z1;
+                }
+                // lower neighbours of other lines (previous wavefront levels, shared memory)
+                if (lj > 0) {
+                    double A[4]; ld2x2(ival, g, t, lk, lj, 1, li, A);
+                    const double y0 = sm[sidx(g, lk, lj - 1, li)], y1 = sm[sidx(g, lk, lj - 1, li) + 1];
+                    r0 -= A[0] * y0 + A[1] * y1; r1 -= A[2] * y0 + A[3] * y1;
+                }
+                if (lk > 0) {
+                    double A[4]; ld2x2(ival, g, t, lk, lj, 0, li, A);
+                    const double y0 = sm[sidx(g, lk - 1, lj, li)], y1 = sm[sidx(g, lk - 1, lj, li) + 1];
+                    r0 -= A[0] * y0 + A[1] * y1; r1 -= A[2] * y0 + A[3] * y1;
+                }
+                double D[4];
 #pragma unroll
-            for (int s = 0; s < 3; ++s) {
-                int ni = li + c_dx[s], nj = lj + c_dy[s], nk = lk + c_dz[s];
-                if (ni < 0 || nj < 0 || nk < 0) continue;
-                int pn = posmap[(nk * g.ty + nj) * g.tx + ni];
-                double a0 = ival[ival_idx(g, t, idx, s, 0)], a1 = ival[ival_idx(g, t, idx, s, 1)];
-                double a2 = ival[ival_idx(g, t, idx, s, 2)], a3 = ival[ival_idx(g, t, idx, s, 3)];
-                double y0 = sm[2 * pn], y1 = sm[2 * pn + 1];
-                r0 -= a0 * y0 + a1 * y1;
-                r1 -= a2 * y0 + a3 * y1;
+                for (int e = 0; e < 4; ++e) D[e] = dinv[didx(g, t, lk, lj, e, li)];
+                c[0] = D[0] * r0 + D[1] * r1;
+                c[1] = D[2] * r0 + D[3] * r1;
+                if (li > 0) {
+                    double A[4], T[4];
+                    ld2x2(ival, g, t, lk, lj, 2, li, A);
+                    mm2(D, A, T);
+                    M[0] = -T[0]; M[1] = -T[1]; M[2] = -T[2]; M[3] = -T[3];
+                }
             }
-            double d0 = dinv[idinv_idx(g, t, idx, 0)], d1 = dinv[idinv_idx(g, t, idx, 1)];
-            double d2 = dinv[idinv_idx(g, t, idx, 2)], d3 = dinv[idinv_idx(g, t, idx, 3)];
-            sm[2 * idx] = d0 * r0 + d1 * r1;
-            sm[2 * idx + 1] = d2 * r0 + d3 * r1;
+            affine_scan<true>(M, c, lseg, W);
+            if (ok) { sm[sidx(g, lk, lj, li)] = c[0]; sm[sidx(g, lk, lj, li) + 1] = c[1]; }
         }
         __syncthreads();
     }
-    for (int l = nlev - 1; l >= 0; --l) {
-        for (int idx = lvlptr[l] + threadIdx.x; idx < lvlptr[l + 1]; idx += blockDim.x) {
-            int pk = cells[idx];
-            int li = pk & 255, lj = (pk >> 8) & 255, lk = pk >> 16;
-            int gi = TI * g.tx + li, gj = TJ * g.ty + lj, gk = TK * g.tz + lk;
-            if (gi >= g.nx || gj >= g.ny || gk >= g.nz) continue;
-            double t0 = 0, t1 = 0;
+    // ---------------- backward
+    for (int l = g.nlev - 1; l >= 0; --l) {
+        for (int base = lvlptr[l]; base < lvlptr[l + 1]; base += nslots) {
+            const int idx = base + slot0;
+            const bool lv = idx < lvlptr[l + 1];
+            const int lj = lv ? (lines[idx] & 0xffff) : 0, lk = lv ? (lines[idx] >> 16) : 0;
+            const int gj = TJ * g.ty + lj, gk = TK * g.tz + lk;
+            const bool ok = lv && xin && gj < g.ny && gk < g.nz;
+            double M[4] = {0, 0, 0, 0}, c[2] = {0, 0};
+            if (ok) {
+                double t0 = 0, t1 = 0;
+                if (lj + 1 < g.ty && gj + 1 < g.ny) {
+                    double A[4]; ld2x2(ival, g, t, lk, lj, 5, li, A);
+                    const double x0 = sm[sidx(g, lk, lj + 1, li)], x1 = sm[sidx(g, lk, lj + 1, li) + 1];
+                    t0 += A[0] * x0 + A[1] * x1; t1 += A[2] * x0 + A[3] * x1;
+                }
+                if (lk + 1 < g.tz && gk + 1 < g.nz) {
+                    double A[4]; ld2x2(ival, g, t, lk, lj, 6, li, A);
+                    const double x0 = sm[sidx(g, lk + 1, lj, li)], x1 = sm[sidx(g, lk + 1, lj, li) + 1];
+                    t0 += A[0] * x0 + A[1] * x1; t1 += A[2] * x0 + A[3] * x1;
+                }
+                double D[4];
 #pragma unroll
-            for (int s = 4; s < 7; ++s) {
-                int ni = li + c_dx[s], nj = lj + c_dy[s], nk = lk + c_dz[s];
-                if (ni >= g.tx || nj >= g.ty || nk >= g.tz || gi + c_dx[s] >= g.nx || gj + c_dy[s] >= g.ny || gk + c_dz[s] >= g.nz) continue;
-                int pn = posmap[(nk * g.ty + nj) * g.tx + ni];
-                double a0 = ival[ival_idx(g, t, idx, s, 0)], a1 = ival[ival_idx(g, t, idx, s, 1)];
-                double a2 = ival[ival_idx(g, t, idx, s, 2)], a3 = ival[ival_idx(g, t, idx, s, 3)];
-                double x0 = sm[2 * pn], x1 = sm[2 * pn + 1];
-                t0 += a0 * x0 + a1 * x1;
-                t1 += a2 * x0 + a3 * x1;
+                for (int e = 0; e < 4; ++e) D[e] = dinv[didx(g, t, lk, lj, e, li)];
+                c[0] = sm[sidx(g, lk, lj, li)] - (D[0] * t0 + D[1] * t1);
+                c[1] = sm[sidx(g, lk, lj, li) + 1] - (D[2] * t0 + D[3] * t1);
+                if (li + 1 < g.tx && gi + 1 < g.nx) {
+                    double A[4], T[4];
+                    ld2x2(ival, g, t, lk, lj, 4, li, A);
+                    mm2(D, A, T);
+                    M[0] = -T[0]; M[1] = -T[1]; M[2] = -T[2]; M[3] = -T[3];
+                }
             }
-            double d0 = dinv[idinv_idx(g, t, idx, 0)], d1 = dinv[idinv_idx(g, t, idx, 1)];
-            double d2 = dinv[idinv_idx(g, t, idx, 2)], d3 = dinv[idinv_idx(g, t, idx, 3)];
-            double x0 = sm[2 * idx] - (d0 * t0 + d1 * t1);
-            double x1 = sm[2 * idx + 1] - (d2 * t0 + d3 * t1);
-            sm[2 * idx] = x0; sm[2 * idx + 1] = x1;
-            int64_t gc = gi + sy * gj + sz * gk;
-            zout[2 * gc] = zs[gc] + x0;        // step 8
-            zout[2 * gc + 1] = zp[gc] + x1;
+            affine_scan<false>(M, c, lseg, W);
+            if (ok) {
+                sm[sidx(g, lk, lj, li)] = c[0]; sm[sidx(g, lk, lj, li) + 1] = c[1];
+                const int64_t gc = gi + sy * gj + sz * gk;
+                zout[2 * gc] = zs[gc] + c[0];        // step 8
+                zout[2 * gc + 1] = zp[gc] + c[1];
+            }
         }
         __syncthreads();
     }
@@ -204,48 +403,40 @@ static TileGeo geo(const Ctx &c)
     g.nx = c.nx; g.ny = c.ny; g.nz = c.nz;
     g.tx = std::min(c.o.tile_x, c.nx); g.ty = std::min(c.o.tile_y, c.ny); g.tz = std::min(c.o.tile_z, c.nz);
     g.ntx = (c.nx + g.tx - 1) / g.tx; g.nty = (c.ny + g.ty - 1) / g.ty; g.ntz = (c.nz + g.tz - 1) / g.tz;
-    g.T = g.tx * g.ty * g.tz; g.Tpad = (g.T + 31) / 32 * 32;
+    g.W = 1; while (g.W < g.tx) g.W <<= 1;
+    g.nlev = g.ty + g.tz - 1;
     return g;
 }
 
 void ilu_setup(Ctx &c, const double *)
 {
     TileGeo g = geo(c);
-    TSP_REQUIRE(g.tx <= 255 && g.ty <= 255 && g.tz <= 255, TSP_ERR_INVALID_ARG, "ILU tile edge must be <= 255");
-    // level-major table of the full tile (same for every tile; clipped tiles skip cells)
-    if (c.ilu_tsize != g.T) {
-        std::vector<int32_t> cells, lvlptr, posmap(g.T);
-        int nlev = g.tx + g.ty + g.tz - 2;
-        for (int l = 0; l < nlev; ++l) {
-            lvlptr.push_back((int32_t)cells.size());
-            for (int k = 0; k < g.tz; ++k)
-                for (int j = 0; j < g.ty; ++j)
-                    for (int i = 0; i < g.tx; ++i)
-                        if (i + j + k == l) {
-                            posmap[(k * g.ty + j) * g.tx + i] = (int32_t)cells.size();
-                            cells.push_back(i | (j << 8) | (k << 16));
-                        }
+    TSP_REQUIRE(g.tx <= 32 && g.ty <= 0xffff && g.tz <= 0x7fff, TSP_ERR_INVALID_ARG, "ILU tile_x must be <= 32");
+    if (c.ilu_tsize != g.tx * g.ty * g.tz) {
+        std::vector<int32_t> lines, lvlptr;
+        for (int l = 0; l < g.nlev; ++l) {
+            lvlptr.push_back((int32_t)lines.size());
+            for (int lk = 0; lk < g.tz; ++lk)
+                for (int lj = 0; lj < g.ty; ++lj)
+                    if (lj + lk == l) lines.push_back(lj | (lk << 16));
         }
-        lvlptr.push_back((int32_t)cells.size());
-        c.ilu_nlev = nlev; c.ilu_tsize = g.T;
-        c.ilu_cells.alloc(cells.size()); c.ilu_lvlptr.alloc(lvlptr.size());
-        DBuf<int32_t> pm; pm.alloc(posmap.size());
-        TSP_CUDA(cudaMemcpyAsync(c.ilu_cells, cells.data(), sizeof(int32_t) * cells.size(), cudaMemcpyHostToDevice, c.s));
+        lvlptr.push_back((int32_t)lines.size());
+        c.ilu_nlev = g.nlev; c.ilu_tsize = g.tx * g.ty * g.tz;
+        c.ilu_cells.alloc(lines.size()); c.ilu_lvlptr.alloc(lvlptr.size());
+        TSP_CUDA(cudaMemcpyAsync(c.ilu_cells, lines.data(), sizeof(int32_t) * lines.size(), cudaMemcpyHostToDevice, c.s));
         TSP_CUDA(cudaMemcpyAsync(c.ilu_lvlptr, lvlptr.data(), sizeof(int32_t) * lvlptr.size(), cudaMemcpyHostToDevice, c.s));
-        TSP_CUDA(cudaMemcpyAsync(pm, posmap.data(), sizeof(int32_t) * posmap.size(), cudaMemcpyHostToDevice, c.s));
         TSP_CUDA(cudaStreamSynchronize(c.s));
-        c.ilu_posmap = std::move(pm);
     }
     c.ntx = g.ntx; c.nty = g.nty; c.ntz = g.ntz;
     c.ntiles = g.ntx * g.nty * g.ntz;
-    c.ilu_val.alloc((size_t)c.ntiles * g.Tpad * 28);
-    c.ilu_dinv.alloc((size_t)c.ntiles * g.Tpad * 4);
+    const size_t per_tile = (size_t)g.tz * g.ty * g.W;
+    c.ilu_val.alloc((size_t)c.ntiles * per_tile * 28);
+    c.ilu_dinv.alloc((size_t)c.ntiles * per_tile * 4);
     c.ilu_val.zero(c.s);
     c.ilu_dinv.zero(c.s);
-    k_ilu_fill<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(g, c.ff.rp, c.ff.ci, c.ff.v, c.fs, c.ilu_posmap, c.ilu_val);
+    k_ilu_fill<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(g, c.ff.rp, c.ff.ci, c.ff.v, c.fs, c.ilu_val);
     c.dcount.zero(c.s);
-    k_ilu_factor<<<c.ntiles, 256, 0, c.s>>>(g, c.ilu_lvlptr, c.ilu_nlev, c.ilu_cells, c.ilu_posmap, c.ilu_val, c.ilu_dinv,
-                                            c.dcount);
+    k_ilu_factor<<<c.ntiles, 32, 0, c.s>>>(g, c.ilu_cells, c.ilu_lvlptr, c.ilu_val, c.ilu_dinv, c.dcount);
     TSP_CUDA(cudaGetLastError());
     unsigned long long np = 0;
     TSP_CUDA(cudaMemcpyAsync(&np, c.dcount, sizeof(np), cudaMemcpyDeviceToHost, c.s));
@@ -257,15 +448,20 @@ void ilu_setup(Ctx &c, const double *)
 void ilu_apply_fused(Ctx &c, const double *yf, const double *zs, const double *zp, double *zf_out)
 {
     TileGeo g = geo(c);
-    size_t smem = sizeof(double) * 2 * g.Tpad;
+    const size_t smem = sizeof(double) * 2 * (size_t)g.tx * g.ty * g.tz;
     static bool attr_set = false;
     if (!attr_set) {
-        TSP_CUDA(cudaFuncSetAttribute(k_ilu_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        TSP_CUDA(cudaFuncSetAttribute(k_ilu_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        TSP_CUDA(cudaFuncSetAttribute(k_ilu_apply2, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr_set = true;
     }
+    TSP_REQUIRE(smem <= 227 * 1024, TSP_ERR_INVALID_ARG, "ILU tile too large for shared memory");
+    const int nslots = 8 * (32 / g.W);
     prof_begin(c, PK_ILU);
-    k_ilu_apply<<<c.ntiles, 256, smem, c.s>>>(g, c.ilu_lvlptr, c.ilu_nlev, c.ilu_cells, c.ilu_posmap, c.ilu_val,
-                                              c.ilu_dinv, yf, zs, zp, zf_out);
+    if (std::min(g.ty, g.tz) <= nslots)
+        k_ilu_apply2<<<c.ntiles, 256, smem, c.s>>>(g, c.ilu_cells, c.ilu_lvlptr, c.ilu_val, c.ilu_dinv, yf, zs, zp, zf_out);
+    else
+        k_ilu_apply<<<c.ntiles, 256, smem, c.s>>>(g, c.ilu_cells, c.ilu_lvlptr, c.ilu_val, c.ilu_dinv, yf, zs, zp, zf_out);
     prof_end(c, PK_ILU, (28.0 * 8 + 32 + 16 + 16 + 16) * c.Nc);
     c.launches += 1;
     TSP_CUDA(cudaGetLastError());
