@@ -65,7 +65,9 @@ typedef struct {
     int amg_max_levels;          /* 12 */
     int zblock;                  /* cell planes per z-block for aggregation confinement, 16 (R-zblock) */
     int tile_x, tile_y, tile_z;  /* ILU(0) tile, 16^3 (R-ilu) */
-    int reserved[8];
+    int replicate_rows;          /* multi-GPU: coarse levels with <= this many global rows are gathered on
+                                    every rank (default 32768); no effect on the result */
+    int reserved[7];
 } tsp_options;
 
 /* BSR block matrix given to tsp_create (nrows block rows). */
@@ -75,9 +77,23 @@ typedef struct {
     const double *val;           /* rowptr[nrows] * bm * bn, row-major blocks */
 } tsp_bsr;
 
+/* Multi-GPU (row e): z-slab decomposition.  The grid's cell planes are grouped
+ * into z-blocks of opts.zblock planes (nzb = ceil(nz/zblock)); rank r owns the
+ * z-blocks [floor(r nzb / P), floor((r+1) nzb / P)), i.e. cell planes [k0, k1),
+ * node planes [k0, k1) plus plane nz on the last rank.  Each rank passes ONLY its
+ * owned block rows (in global natural order) with GLOBAL column indices; vectors
+ * are the rank's owned part [u_own | f_own].  Results are bitwise identical for
+ * every P (aggregation and ILU tiles never cross z-blocks, reductions are summed
+ * per fixed chunk in global order).  Requires 1 <= P <= nzb. */
+enum { TSP_COMM_NONE = 0, TSP_COMM_NCCL = 1, TSP_COMM_LOCAL = 2 };
+
 typedef struct {
-    int nx, ny, nz;              /* grid in cells: N_n = (nx+1)(ny+1)(nz+1), N_c = nx ny nz */
-    int rank, nranks;            /* this library build: nranks == 1 (multi-GPU) */
+    int nx, ny, nz;              /* GLOBAL grid in cells: N_n = (nx+1)(ny+1)(nz+1), N_c = nx ny nz */
+    int rank, nranks;            /* this rank and the number of ranks (one per GPU) */
+    int comm_kind;               /* TSP_COMM_NCCL: comm_arg = 128-byte ncclUniqueId (tsp_nccl_unique_id on rank 0,
+                                    broadcast by the caller); TSP_COMM_LOCAL: comm_arg = tsp_local_world_create()
+                                    (test backend: P handles in one process, one host thread each) */
+    const void *comm_arg;
     void *stream;                /* cudaStream_t to order all work on (0 = legacy default) */
     int inputs_on_device;        /* 0: all pointers below are host; 1: device */
     tsp_bsr A_uu;                /* 3x3, N_n block rows, N_n block cols */
@@ -132,6 +148,17 @@ int tsp_abi_version(void);
 const char *tsp_last_error(void);
 tsp_status tsp_default_options(tsp_options *o);
 
+/* NCCL bootstrap: rank 0 creates the id, the caller broadcasts it (e.g. through
+ * torch.distributed) and every rank passes it in tsp_desc.comm_arg. */
+tsp_status tsp_nccl_unique_id(char out[128]);
+/* Test backend: a world of `nranks` handles inside one process (each rank's calls
+ * must come from its own host thread; every collective call is matched). */
+void *tsp_local_world_create(int nranks);
+void tsp_local_world_destroy(void *world);
+/* Owned ranges of `rank` (for callers slicing a global problem): out6 =
+ * {k0, k1, first owned node, owned nodes, first owned cell, owned cells}. */
+tsp_status tsp_partition(int nx, int ny, int nz, int zblock, int rank, int nranks, int64_t out6[6]);
+
 /* Validates, deep-copies the blocks into library-owned device memory and
  * repacks them (sliced-ELL, R-layout).  The caller may free its inputs after
  * return.  Returns TSP_ERR_INVALID_ARG on null/unsorted/inconsistent input. */
@@ -163,6 +190,10 @@ tsp_status tsp_get_stats(tsp_handle h, tsp_stats *s);
 tsp_status tsp_level_sizes(tsp_handle h, int which, int lvl, int64_t out6[6]);
 tsp_status tsp_export_level(tsp_handle h, int which, int lvl, int32_t *A_rp, int32_t *A_ci, double *A_v,
                             int32_t *agg, int32_t *P_rp, int32_t *P_ci, double *P_v, double *dl1);
+
+/* multi-GPU layout of a level: out3 = {distributed (rows split over ranks), global rows,
+ * first global row of this rank}.  Replicated levels are complete on every rank. */
+tsp_status tsp_level_dist(tsp_handle h, int which, int lvl, int64_t out3[3]);
 
 tsp_status tsp_prof_enable(tsp_handle h, int on);   /* also resets */
 tsp_status tsp_prof_read(tsp_handle h, tsp_prof *p);  /* synchronises */

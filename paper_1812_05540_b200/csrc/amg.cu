@@ -47,7 +47,7 @@ __device__ __forceinline__ double meas(const double *__restrict__ v, int64_t q, 
 }
 
 // ------------------------------------------------------------------ strength (R-strength)
-__global__ void k_strength(int n, int nc, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+__global__ void k_strength(int n, int nc, int nown, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
                            const double *__restrict__ v, const int32_t *__restrict__ zb, double theta, uint8_t *S)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -58,19 +58,24 @@ __global__ void k_strength(int n, int nc, const int32_t *__restrict__ rp, const 
     double thr = __dmul_rn(theta, m);
     for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
         int j = ci[q];
-        S[q] = (j != i && m > 0.0 && zb[i] == zb[j] && meas(v, q, nc) >= thr) ? 1 : 0;
+        // columns of other ranks (j >= nown) lie in other z-blocks by construction
+        S[q] = (j != i && m > 0.0 && j < nown && zb[i] == zb[j] && meas(v, q, nc) >= thr) ? 1 : 0;
     }
 }
 
-__global__ void k_symm(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const uint8_t *__restrict__ S,
-                       uint8_t *E, int *err)
+__global__ void k_symm(int n, int nown, int linear, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                       const uint8_t *__restrict__ S, uint8_t *E, int *err)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
         int j = ci[q];
-        if (j == i) { E[q] = 0; continue; }
+        if (j == i || j >= nown) { E[q] = 0; continue; }
         int64_t lo = rp[j], hi = rp[j + 1] - 1, qt = -1;
+        if (linear) {   // distributed level: local ids in a row are not monotone (ghosts first/last)
+            for (int64_t u = lo; u <= hi; ++u) if (ci[u] == i) { qt = u; break; }
+            lo = 1; hi = 0;
+        }
         while (lo <= hi) {
             int64_t mid = (lo + hi) >> 1;
             int cm = ci[mid];
@@ -93,17 +98,17 @@ __global__ void k_mis_init(int n, const int32_t *__restrict__ rp, const uint8_t 
     for (int64_t q = rp[i]; q < rp[i + 1]; ++q) d |= E[q];
     st[i] = d ? ST_UND : ST_ISO;
 }
-__global__ void k_mis_t1(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const uint8_t *__restrict__ E,
+__global__ void k_mis_t1(int n, int off, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const uint8_t *__restrict__ E,
                          const int8_t *__restrict__ st, uint64_t *t1)
 {
     int x = blockIdx.x * blockDim.x + threadIdx.x;
     if (x >= n) return;
-    uint64_t m = st[x] == ST_UND ? prio(x) + 1 : 0;
+    uint64_t m = st[x] == ST_UND ? prio(off + x) + 1 : 0;   // priorities of GLOBAL row ids
     for (int64_t q = rp[x]; q < rp[x + 1]; ++q)
-        if (E[q]) { int u = ci[q]; if (st[u] == ST_UND) { uint64_t p = prio(u) + 1; if (p > m) m = p; } }
+        if (E[q]) { int u = ci[q]; if (st[u] == ST_UND) { uint64_t p = prio(off + u) + 1; if (p > m) m = p; } }
     t1[x] = m;
 }
-__global__ void k_mis_root(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const uint8_t *__restrict__ E,
+__global__ void k_mis_root(int n, int off, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const uint8_t *__restrict__ E,
                            const int8_t *__restrict__ st, const uint64_t *__restrict__ t1, uint8_t *newr)
 {
     int v = blockIdx.x * blockDim.x + threadIdx.x;
@@ -112,7 +117,7 @@ __global__ void k_mis_root(int n, const int32_t *__restrict__ rp, const int32_t 
     if (st[v] == ST_UND) {
         uint64_t m = t1[v];
         for (int64_t q = rp[v]; q < rp[v + 1]; ++q) if (E[q]) { uint64_t t = t1[ci[q]]; if (t > m) m = t; }
-        r = (m == prio(v) + 1);
+        r = (m == prio(off + v) + 1);
     }
     newr[v] = r;
 }
@@ -520,7 +525,141 @@ static void dbg_mark(Ctx &c, const char *what, int lvl)
     last = now;
 }
 
-void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc)
+
+// ------------------------------------------------------------------ distributed-setup helpers
+__global__ void k_add_off(int64_t nnz, const int32_t *__restrict__ a, int64_t off, int32_t *__restrict__ b)
+{
+    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q < nnz) b[q] = (int32_t)(a[q] + off);
+}
+__global__ void k_row_lens(int n, const int32_t *__restrict__ idx, const int32_t *__restrict__ rp, int32_t *__restrict__ len)
+{
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) { const int r = idx ? idx[k] : k; len[k] = rp[r + 1] - rp[r]; }
+}
+// copy rows idx[k] of (rp, ci, v) to a packed buffer at offsets o[k]
+__global__ void k_pack_rows(int n, int nc, const int32_t *__restrict__ idx, const int32_t *__restrict__ rp,
+                            const int32_t *__restrict__ ci, const double *__restrict__ v, const int32_t *__restrict__ o,
+                            int32_t *__restrict__ pci, double *__restrict__ pv)
+{
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int r = idx ? idx[k] : k;
+    int64_t d = o[k];
+    for (int64_t q = rp[r]; q < rp[r + 1]; ++q, ++d) {
+        pci[d] = ci[q];
+        for (int e = 0; e < nc; ++e) pv[d * nc + e] = v[q * nc + e];
+    }
+}
+
+static std::vector<int32_t> d2h_vec(Ctx &c, const int32_t *p, size_t n)
+{
+    std::vector<int32_t> h(n);
+    if (n) TSP_CUDA(cudaMemcpyAsync(h.data(), p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c.s));
+    TSP_CUDA(cudaStreamSynchronize(c.s));
+    return h;
+}
+
+// P rows of the ghost rows of a distributed level: the owners send the rows listed in the
+// halo plan; result = P_ext with rows [own rows | ghost rows] and GLOBAL coarse columns.
+static void ghost_rows(Ctx &c, Halo &H, const Csr &Pg, Csr &Pext, int nc)
+{
+    const int ns = H.nsend[0] + H.nsend[1], ng = H.nghost();
+    DBuf<int32_t> slen, rlen;
+    slen.alloc(std::max(ns, 1)); rlen.alloc(std::max(ng, 1));
+    if (ns) k_row_lens<<<grid_for(ns, 256), 256, 0, c.s>>>(ns, H.sidx, Pg.rp, slen);
+    c.comm->neighbor_exchange(slen.p, 4 * H.nsend[0], rlen.p, 4 * H.nrecv[0], slen.p + H.nsend[0], 4 * H.nsend[1],
+                              rlen.p + H.nrecv[0], 4 * H.nrecv[1], c.s);
+    std::vector<int32_t> sl = d2h_vec(c, slen, ns), rl = d2h_vec(c, rlen, ng);
+    std::vector<int32_t> so(ns + 1, 0), ro(ng + 1, 0);
+    for (int k = 0; k < ns; ++k) so[k + 1] = so[k] + sl[k];
+    for (int k = 0; k < ng; ++k) ro[k + 1] = ro[k] + rl[k];
+    const int64_t sn_lo = so[H.nsend[0]], sn = so[ns], rn_lo = ro[H.nrecv[0]], rn = ro[ng];
+    DBuf<int32_t> sof, sci, rci;
+    DBuf<double> sv, rv;
+    sof.alloc(ns + 1); sci.alloc(std::max<int64_t>(sn, 1)); sv.alloc(std::max<int64_t>(sn, 1) * nc);
+    rci.alloc(std::max<int64_t>(rn, 1)); rv.alloc(std::max<int64_t>(rn, 1) * nc);
+    TSP_CUDA(cudaMemcpyAsync(sof, so.data(), sizeof(int32_t) * (ns + 1), cudaMemcpyHostToDevice, c.s));
+    if (ns) k_pack_rows<<<grid_for(ns, 128), 128, 0, c.s>>>(ns, nc, H.sidx, Pg.rp, Pg.ci, Pg.v, sof, sci, sv);
+    c.comm->neighbor_exchange(sci.p, 4 * sn_lo, rci.p, 4 * rn_lo, sci.p + sn_lo, 4 * (sn - sn_lo), rci.p + rn_lo, 4 * (rn - rn_lo), c.s);
+    c.comm->neighbor_exchange(sv.p, 8 * nc * sn_lo, rv.p, 8 * nc * rn_lo, sv.p + sn_lo * nc, 8 * nc * (sn - sn_lo),
+                              rv.p + rn_lo * nc, 8 * nc * (rn - rn_lo), c.s);
+    // assemble P_ext
+    Pext.n = Pg.n + ng; Pext.m = Pg.m; Pext.nc = nc; Pext.nnz = Pg.nnz + rn;
+    Pext.rp.alloc(Pext.n + 1); Pext.ci.alloc(std::max<int64_t>(Pext.nnz, 1)); Pext.v.alloc(std::max<int64_t>(Pext.nnz, 1) * nc);
+    std::vector<int32_t> prp = d2h_vec(c, Pg.rp, Pg.n + 1);
+    for (int k = 0; k < ng; ++k) prp.push_back((int32_t)(Pg.nnz + ro[k + 1]));
+    TSP_CUDA(cudaMemcpyAsync(Pext.rp, prp.data(), sizeof(int32_t) * prp.size(), cudaMemcpyHostToDevice, c.s));
+    if (Pg.nnz) {
+        TSP_CUDA(cudaMemcpyAsync(Pext.ci, Pg.ci, 4 * Pg.nnz, cudaMemcpyDeviceToDevice, c.s));
+        TSP_CUDA(cudaMemcpyAsync(Pext.v, Pg.v, 8 * nc * Pg.nnz, cudaMemcpyDeviceToDevice, c.s));
+    }
+    if (rn) {
+        TSP_CUDA(cudaMemcpyAsync(Pext.ci.p + Pg.nnz, rci, 4 * rn, cudaMemcpyDeviceToDevice, c.s));
+        TSP_CUDA(cudaMemcpyAsync(Pext.v.p + Pg.nnz * nc, rv, 8 * nc * rn, cudaMemcpyDeviceToDevice, c.s));
+    }
+    TSP_CUDA(cudaStreamSynchronize(c.s));
+    c.launches += 2;
+}
+
+// allgather the rows of a distributed matrix (global columns) into one full copy per rank
+static void gather_rows(Ctx &c, const Csr &A, const DBuf<int32_t> &zb, Csr &F, DBuf<int32_t> &zbF, int nc,
+                        std::vector<int64_t> &counts)
+{
+    std::vector<int64_t> me = {(int64_t)A.n, A.nnz};
+    std::vector<int64_t> all = host_allgather<int64_t>(c, me);
+    const int P = c.nranks;
+    int64_t mxn = 1, mxz = 1, N = 0, Z = 0;
+    counts.assign(P, 0);
+    for (int r = 0; r < P; ++r) {
+        counts[r] = all[2 * r];
+        mxn = std::max(mxn, all[2 * r]); mxz = std::max(mxz, all[2 * r + 1]);
+        N += all[2 * r]; Z += all[2 * r + 1];
+    }
+    DBuf<int32_t> slen, rlen, sci, rci, szb, rzb;
+    DBuf<double> sv, rv;
+    slen.alloc(mxn); rlen.alloc(mxn * P); sci.alloc(mxz); rci.alloc(mxz * P); szb.alloc(mxn); rzb.alloc(mxn * P);
+    sv.alloc(mxz * nc); rv.alloc(mxz * nc * P);
+    if (A.n) {
+        k_row_lens<<<grid_for(A.n, 256), 256, 0, c.s>>>(A.n, nullptr, A.rp, slen);
+        TSP_CUDA(cudaMemcpyAsync(szb, zb, 4 * A.n, cudaMemcpyDeviceToDevice, c.s));
+    }
+    if (A.nnz) {
+        TSP_CUDA(cudaMemcpyAsync(sci, A.ci, 4 * A.nnz, cudaMemcpyDeviceToDevice, c.s));
+        TSP_CUDA(cudaMemcpyAsync(sv, A.v, 8 * nc * A.nnz, cudaMemcpyDeviceToDevice, c.s));
+    }
+    c.comm->allgather(slen.p, rlen.p, 4 * mxn, c.s);
+    c.comm->allgather(szb.p, rzb.p, 4 * mxn, c.s);
+    c.comm->allgather(sci.p, rci.p, 4 * mxz, c.s);
+    c.comm->allgather(sv.p, rv.p, 8 * nc * mxz, c.s);
+    F.n = (int)N; F.m = (int)N; F.nc = nc; F.nnz = Z;
+    F.rp.alloc(N + 1); F.ci.alloc(std::max<int64_t>(Z, 1)); F.v.alloc(std::max<int64_t>(Z, 1) * nc);
+    zbF.alloc(std::max<int64_t>(N, 1));
+    std::vector<int32_t> lens((size_t)mxn * P);
+    TSP_CUDA(cudaMemcpyAsync(lens.data(), rlen, 4 * lens.size(), cudaMemcpyDeviceToHost, c.s));
+    TSP_CUDA(cudaStreamSynchronize(c.s));
+    std::vector<int32_t> rp(1, 0);
+    int64_t rowo = 0, nzo = 0;
+    for (int r = 0; r < P; ++r) {
+        for (int64_t k = 0; k < all[2 * r]; ++k) rp.push_back(rp.back() + lens[(size_t)r * mxn + k]);
+        if (all[2 * r]) TSP_CUDA(cudaMemcpyAsync(zbF.p + rowo, rzb.p + r * mxn, 4 * all[2 * r], cudaMemcpyDeviceToDevice, c.s));
+        if (all[2 * r + 1]) {
+            TSP_CUDA(cudaMemcpyAsync(F.ci.p + nzo, rci.p + r * mxz, 4 * all[2 * r + 1], cudaMemcpyDeviceToDevice, c.s));
+            TSP_CUDA(cudaMemcpyAsync(F.v.p + nzo * nc, rv.p + r * mxz * nc, 8 * nc * all[2 * r + 1], cudaMemcpyDeviceToDevice, c.s));
+        }
+        rowo += all[2 * r]; nzo += all[2 * r + 1];
+    }
+    TSP_CUDA(cudaMemcpyAsync(F.rp, rp.data(), 4 * rp.size(), cudaMemcpyHostToDevice, c.s));
+    TSP_CUDA(cudaStreamSynchronize(c.s));
+    c.launches++;
+}
+
+// ------------------------------------------------------------------ hierarchy build (row a4)
+// Level 0 arrives distributed when nranks > 1 (halo plan `fine_halo`, global row offset
+// `row_off0`).  A coarse level stays distributed while its global size exceeds
+// opts.replicate_rows; below that it is gathered onto every rank and the rest of the
+// hierarchy is built redundantly (identical data => identical results on all ranks).
+void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_halo, int64_t row_off0, int64_t nglob0)
 {
     dbg_mark(c, "start", -1);
     H.L.clear();
@@ -531,33 +670,51 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc)
         Level &L0 = H.L[0];
         L0.A = std::move(A0);
         L0.zb = std::move(zb0);
+        L0.dist = c.comm != nullptr;
+        L0.row_off = row_off0;
+        L0.nglob = nglob0;
+        L0.hp = fine_halo;
     }
     const int maxl = std::min(std::max(c.o.amg_max_levels, 1), 16);
+    const int64_t rep_rows = c.o.replicate_rows > 0 ? c.o.replicate_rows : 32768;
     DBuf<int> err; err.alloc(1);
     for (int lvl = 0;; ++lvl) {
         Level &L = H.L[lvl];
         L.n = L.A.n; L.nc = nc;
+        if (!L.dist) { L.nglob = L.n; L.row_off = 0; }
         const int n = L.n;
-        L.dl1.alloc((size_t)n * nc); L.dinv.alloc((size_t)n * nc);
+        const int nown = n;   // rows of this rank; columns >= nown are ghosts
+        L.dl1.alloc((size_t)std::max(n, 1) * nc); L.dinv.alloc((size_t)std::max(n, 1) * nc);
         if (n) k_l1<<<grid_for(n, 256), 256, 0, c.s>>>(n, nc, L.A.rp, L.A.v, L.dl1, L.dinv);
         c.launches++;
-        if (n <= c.o.amg_coarse_max || lvl == maxl - 1) { make_coarsest(c, H, L); break; }
+        if (L.dist && L.hp->any()) {
+            L.dinv_gh.alloc((size_t)std::max(L.hp->nghost(), 1) * nc);
+            halo_exchange(c, *L.hp, nc, L.dinv, L.dinv_gh);
+        }
+        if (L.nglob <= c.o.amg_coarse_max || lvl == maxl - 1) {
+            TSP_REQUIRE(!L.dist, TSP_ERR_INVALID_ARG, "the distributed fine level is too small for this many ranks");
+            make_coarsest(c, H, L);
+            break;
+        }
         // strength + symmetrisation
         DBuf<uint8_t> S, E; S.alloc(L.A.nnz + 1); E.alloc(L.A.nnz + 1);
         err.zero(c.s);
-        k_strength<<<grid_for(n, 256), 256, 0, c.s>>>(n, nc, L.A.rp, L.A.ci, L.A.v, L.zb, c.o.amg_theta, S);
-        k_symm<<<grid_for(n, 256), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, S, E, err);
+        if (n) {
+            k_strength<<<grid_for(n, 256), 256, 0, c.s>>>(n, nc, nown, L.A.rp, L.A.ci, L.A.v, L.zb, c.o.amg_theta, S);
+            k_symm<<<grid_for(n, 256), 256, 0, c.s>>>(n, nown, L.dist ? 1 : 0, L.A.rp, L.A.ci, S, E, err);
+        }
         c.launches += 2;
         TSP_REQUIRE(!d2h1(c, err.p), TSP_ERR_INVALID_ARG, "AMG input pattern is not structurally symmetric");
-        // MIS(2) rounds
-        DBuf<int8_t> st; st.alloc(n);
-        DBuf<uint64_t> t1; t1.alloc(n);
-        DBuf<uint8_t> newr, near1; newr.alloc(n); near1.alloc(n);
-        k_mis_init<<<grid_for(n, 256), 256, 0, c.s>>>(n, L.A.rp, E, st);
+        // MIS(2) rounds: the strength graph never leaves a z-block, so each rank runs its own rounds
+        DBuf<int8_t> st; st.alloc(std::max(n, 1));
+        DBuf<uint64_t> t1; t1.alloc(std::max(n, 1));
+        DBuf<uint8_t> newr, near1; newr.alloc(std::max(n, 1)); near1.alloc(std::max(n, 1));
+        if (n) k_mis_init<<<grid_for(n, 256), 256, 0, c.s>>>(n, L.A.rp, E, st);
         c.launches++;
-        for (int round = 0; round < 1000; ++round) {
-            k_mis_t1<<<grid_for(n, 256), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, E, st, t1);
-            k_mis_root<<<grid_for(n, 256), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, E, st, t1, newr);
+        const int off = (int)L.row_off;
+        for (int round = 0; round < 1000 && n; ++round) {
+            k_mis_t1<<<grid_for(n, 256), 256, 0, c.s>>>(n, off, L.A.rp, L.A.ci, E, st, t1);
+            k_mis_root<<<grid_for(n, 256), 256, 0, c.s>>>(n, off, L.A.rp, L.A.ci, E, st, t1, newr);
             k_mis_near<<<grid_for(n, 256), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, E, newr, st, near1);
             c.dcount.zero(c.s);
             k_mis_out<<<grid_for(n, 256), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, E, near1, st, c.dcount);
@@ -565,58 +722,120 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc)
             if (d2h1(c, c.dcount.p) == 0) break;
         }
         dbg_mark(c, "strength+mis", lvl);
-        // aggregates
+        // aggregates: local numbering by ascending root, global = coarse_off + local
         DBuf<int32_t> flag, rid, ph1;
-        flag.alloc(n + 1); rid.alloc(n + 1); ph1.alloc(n);
-        k_rootflag<<<grid_for(n, 256), 256, 0, c.s>>>(n, st, flag);
+        flag.alloc(n + 1); rid.alloc(n + 1); ph1.alloc(std::max(n, 1));
+        if (n) k_rootflag<<<grid_for(n, 256), 256, 0, c.s>>>(n, st, flag);
         TSP_CUDA(cudaMemsetAsync(flag.p + n, 0, sizeof(int32_t), c.s));
         exclusive_scan<int32_t>(c, flag, rid, n + 1);
         const int nagg = d2h1(c, rid.p + n);
-        if (nagg == 0 || (double)nagg > 0.8 * (double)n) {   // stagnation: direct solve here
+        int64_t nagg_glob = nagg, coarse_off = 0;
+        if (L.dist) {
+            std::vector<int64_t> all = host_allgather<int64_t>(c, std::vector<int64_t>{(int64_t)nagg});
+            nagg_glob = 0;
+            for (int r = 0; r < c.nranks; ++r) { if (r < c.rank) coarse_off += all[r]; nagg_glob += all[r]; }
+        }
+        if (nagg_glob == 0 || (double)nagg_glob > 0.8 * (double)L.nglob) {   // stagnation: direct solve here
+            TSP_REQUIRE(!L.dist, TSP_ERR_SINGULAR, "coarsening stagnated on a distributed level");
             H.fallbacks++;
             make_coarsest(c, H, L);
             break;
         }
         L.nagg = nagg;
-        L.agg.alloc(n);
+        L.coarse_off = coarse_off;
+        L.agg.alloc(std::max(n, 1));
         H.L.emplace_back();
         Level &Lc = H.L[lvl + 1];
         Level &Lf = H.L[lvl];   // re-fetch after emplace_back
-        Lc.zb.alloc(nagg);
-        TSP_CUDA(cudaMemsetAsync(ph1, 0xff, sizeof(int32_t) * n, c.s));
-        k_phase1<<<grid_for(n, 256), 256, 0, c.s>>>(n, Lf.A.rp, Lf.A.ci, E, st, rid, Lf.zb, ph1, Lc.zb);
-        k_phase2<<<grid_for(n, 256), 256, 0, c.s>>>(n, nc, Lf.A.rp, Lf.A.ci, Lf.A.v, E, st, ph1, Lf.agg);
+        Lc.zb.alloc(std::max(nagg, 1));
+        TSP_CUDA(cudaMemsetAsync(ph1, 0xff, sizeof(int32_t) * std::max(n, 1), c.s));
+        if (n) {
+            k_phase1<<<grid_for(n, 256), 256, 0, c.s>>>(n, Lf.A.rp, Lf.A.ci, E, st, rid, Lf.zb, ph1, Lc.zb);
+            k_phase2<<<grid_for(n, 256), 256, 0, c.s>>>(n, nc, Lf.A.rp, Lf.A.ci, Lf.A.v, E, st, ph1, Lf.agg);
+        }
         c.launches += 3;
         // prolongator
-        DBuf<double> d; d.alloc((size_t)n * nc);
+        DBuf<double> d; d.alloc((size_t)std::max(n, 1) * nc);
         DBuf<unsigned long long> rho; rho.alloc(3); rho.zero(c.s);
-        k_pdiag<<<grid_for(n, 256), 256, 0, c.s>>>(n, nc, Lf.A.rp, Lf.A.ci, Lf.A.v, E, d, rho);
+        if (n) k_pdiag<<<grid_for(n, 256), 256, 0, c.s>>>(n, nc, Lf.A.rp, Lf.A.ci, Lf.A.v, E, d, rho);
         unsigned long long rb[3] = {0, 0, 0};
         TSP_CUDA(cudaMemcpyAsync(rb, rho.p, sizeof(rb), cudaMemcpyDeviceToHost, c.s));
         TSP_CUDA(cudaStreamSynchronize(c.s));
+        std::vector<double> rhos(3);
+        for (int k = 0; k < 3; ++k) memcpy(&rhos[k], &rb[k], sizeof(double));
+        if (Lf.dist) {   // global max (exact, order independent)
+            std::vector<double> all = host_allgather<double>(c, rhos);
+            for (int r = 0; r < c.nranks; ++r)
+                for (int k = 0; k < 3; ++k) rhos[k] = std::max(rhos[k], all[3 * r + k]);
+        }
         Omega om;
         for (int k = 0; k < 3; ++k) {
-            double r; memcpy(&r, &rb[k], sizeof(double));
+            const double r = rhos[k];
             volatile double three_r = 3.0 * r;   // IEEE: 4 / (3 rho), same expression as the oracle
             om.w[k] = (k < nc && r > 0.0) ? 4.0 / three_r : 0.0;
         }
         DBuf<int32_t> cnt; cnt.alloc(n + 1);
         err.zero(c.s);
-        k_pcount<<<grid_for(n, 128), 128, 0, c.s>>>(n, Lf.A.rp, Lf.A.ci, E, Lf.agg, cnt, err);
+        if (n) k_pcount<<<grid_for(n, 128), 128, 0, c.s>>>(n, Lf.A.rp, Lf.A.ci, E, Lf.agg, cnt, err);
         Lf.P.n = n; Lf.P.m = nagg; Lf.P.nc = nc;
         Lf.P.nnz = rowptr_from_counts(c, cnt, Lf.P.rp, n);
-        Lf.P.ci.alloc(Lf.P.nnz); Lf.P.v.alloc(Lf.P.nnz * nc);
-        k_pfill<<<grid_for(n, 128), 128, 0, c.s>>>(n, nc, Lf.A.rp, Lf.A.ci, Lf.A.v, E, Lf.agg, d, om, Lf.P.rp, Lf.P.ci, Lf.P.v, err);
+        Lf.P.ci.alloc(std::max<int64_t>(Lf.P.nnz, 1)); Lf.P.v.alloc(std::max<int64_t>(Lf.P.nnz, 1) * nc);
+        if (n) k_pfill<<<grid_for(n, 128), 128, 0, c.s>>>(n, nc, Lf.A.rp, Lf.A.ci, Lf.A.v, E, Lf.agg, d, om, Lf.P.rp, Lf.P.ci, Lf.P.v, err);
         c.launches += 3;
         TSP_REQUIRE(!d2h1(c, err.p), TSP_ERR_INVALID_ARG, "prolongator row exceeds 512 aggregates");
         dbg_mark(c, "agg+P", lvl);
-        transpose(c, Lf.P, Lf.R, nc);
+        transpose(c, Lf.P, Lf.R, nc);     // local coarse rows x local fine columns
         dbg_mark(c, "transpose", lvl);
+        // P with GLOBAL coarse columns (and the ghost rows on a distributed level)
+        Csr Pg;
+        Pg.n = Lf.P.n; Pg.m = (int)nagg_glob; Pg.nc = nc; Pg.nnz = Lf.P.nnz;
+        Pg.rp.alloc(n + 1); Pg.ci.alloc(std::max<int64_t>(Pg.nnz, 1)); Pg.v.alloc(std::max<int64_t>(Pg.nnz, 1) * nc);
+        TSP_CUDA(cudaMemcpyAsync(Pg.rp, Lf.P.rp, 4 * (n + 1), cudaMemcpyDeviceToDevice, c.s));
+        if (Pg.nnz) {
+            k_add_off<<<grid_for(Pg.nnz, 256), 256, 0, c.s>>>(Pg.nnz, Lf.P.ci, coarse_off, Pg.ci);
+            TSP_CUDA(cudaMemcpyAsync(Pg.v, Lf.P.v, 8 * nc * Pg.nnz, cudaMemcpyDeviceToDevice, c.s));
+        }
         Csr AP;
-        spgemm(c, Lf.A, Lf.P, AP, nc);
+        if (Lf.dist && Lf.hp->any()) {
+            Csr Pext;
+            ghost_rows(c, *Lf.hp, Pg, Pext, nc);
+            spgemm(c, Lf.A, Pext, AP, nc);
+        } else {
+            spgemm(c, Lf.A, Pg, AP, nc);
+        }
+        AP.m = (int)nagg_glob;
         dbg_mark(c, "AP", lvl);
-        spgemm(c, Lf.R, AP, Lc.A, nc);
+        Csr Ac;
+        spgemm(c, Lf.R, AP, Ac, nc);       // local coarse rows, global coarse columns
+        Ac.m = (int)nagg_glob;
         dbg_mark(c, "RAP", lvl);
+        if (Lf.dist && nagg_glob > rep_rows) {
+            // next level stays distributed: remap its columns to local + ghosts
+            Lc.dist = true; Lc.nglob = nagg_glob; Lc.row_off = coarse_off;
+            Lc.A = std::move(Ac);
+            DBuf<int32_t> gcol; gcol.alloc(std::max<int64_t>(Lc.A.nnz, 1));
+            if (Lc.A.nnz) TSP_CUDA(cudaMemcpyAsync(gcol, Lc.A.ci, 4 * Lc.A.nnz, cudaMemcpyDeviceToDevice, c.s));
+            halo_build(c, Lc.halo, nagg, coarse_off, gcol, Lc.A.nnz, Lc.A.ci);
+            Lc.A.gci = std::move(gcol);
+            Lc.A.m = nagg + Lc.halo.nghost();
+            Lc.hp = &Lc.halo;
+            Lf.next_dist = true;
+        } else if (Lf.dist) {
+            // gather the coarse level onto every rank; the prolongator then addresses the full vector
+            DBuf<int32_t> zbF;
+            gather_rows(c, Ac, Lc.zb, Lc.A, zbF, nc, Lf.rep_counts);
+            Lc.zb = std::move(zbF);
+            Lc.dist = false;
+            Lf.rep_offs.assign(c.nranks + 1, 0);
+            for (int r = 0; r < c.nranks; ++r) Lf.rep_offs[r + 1] = Lf.rep_offs[r] + Lf.rep_counts[r];
+            int64_t mx = 1;
+            for (auto v : Lf.rep_counts) mx = std::max(mx, v);
+            Lf.rep_buf.alloc((size_t)mx * nc * (c.nranks + 1));
+            Lf.P.m = (int)nagg_glob;
+            if (Lf.P.nnz) TSP_CUDA(cudaMemcpyAsync(Lf.P.ci, Pg.ci, 4 * Lf.P.nnz, cudaMemcpyDeviceToDevice, c.s));
+        } else {
+            Lc.A = std::move(Ac);
+        }
     }
     // apply-side layouts and work vectors
     for (size_t l = 0; l < H.L.size(); ++l) {
@@ -628,17 +847,31 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc)
         }
         size_t m = (size_t)std::max(L.n, 1) * nc;
         L.b.alloc(m); L.x.alloc(m); L.x2.alloc(m); L.r.alloc(m);
+        {   // kernel choice from global mean row lengths, so every rank computes a row exactly like P = 1
+            std::vector<int64_t> st = {L.A.nnz, (int64_t)L.n, L.coarsest ? 0 : L.R.nnz, L.coarsest ? 0 : (int64_t)L.R.n};
+            if (L.dist) {
+                std::vector<int64_t> all = host_allgather<int64_t>(c, st);
+                st.assign(4, 0);
+                for (int r = 0; r < c.nranks; ++r) for (int k = 0; k < 4; ++k) st[k] += all[4 * r + k];
+            }
+            L.warpA = l > 0 && st[1] > 0 && st[0] >= 12 * st[1];
+            L.warpR = st[3] > 0 && st[2] >= 12 * st[3];
+        }
+        if (L.dist) {
+            const size_t g = (size_t)std::max(L.hp->nghost(), 1) * nc;
+            L.gh_b.alloc(g); L.gh_x.alloc(g);
+        }
     }
     dbg_mark(c, "sell+vectors", 99);
     TSP_CUDA(cudaStreamSynchronize(c.s));
 }
 
 // ------------------------------------------------------------------ V-cycle kernels (apply; free arithmetic)
-// pre-smooth from zero + residual: x = D^-1 b ; r = b - A D^-1 b
+// pre-smooth from zero + residual: x = D^-1 b ; r = b - A D^-1 b   (b, D^-1 ghost-aware)
 template <int NC>
 __global__ void __launch_bounds__(256) k_vc_pre(int n, const int64_t *__restrict__ off, const int32_t *__restrict__ col,
-                                                const double *__restrict__ val, const double *__restrict__ dinv,
-                                                const double *__restrict__ b, double *__restrict__ x, double *__restrict__ r)
+                                                const double *__restrict__ val, GV dinv, GV b, double *__restrict__ x,
+                                                double *__restrict__ r)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -652,16 +885,16 @@ __global__ void __launch_bounds__(256) k_vc_pre(int n, const int64_t *__restrict
         const int j = __ldcs(col + slot * 32 + lane);
 #pragma unroll
         for (int c = 0; c < NC; ++c)
-            acc[c] = fma(__ldcs(val + (slot * NC + c) * 32 + lane), __ldg(b + (int64_t)j * NC + c) * __ldg(dinv + (int64_t)j * NC + c), acc[c]);
+            acc[c] = fma(__ldcs(val + (slot * NC + c) * 32 + lane), GVLD(b, j, c, NC) * GVLD(dinv, j, c, NC), acc[c]);
     }
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-        const double bi = b[(int64_t)i * NC + c];
-        x[(int64_t)i * NC + c] = bi * dinv[(int64_t)i * NC + c];
+        const double bi = b.own[(int64_t)i * NC + c];
+        x[(int64_t)i * NC + c] = bi * dinv.own[(int64_t)i * NC + c];
         r[(int64_t)i * NC + c] = bi - acc[c];
     }
 }
-// y = S x  (restriction R r)
+// y = S x  (restriction R r; rows and columns local)
 template <int NC>
 __global__ void __launch_bounds__(256) k_sell_mv(int n, const int64_t *__restrict__ off, const int32_t *__restrict__ col,
                                                  const double *__restrict__ val, const double *__restrict__ x, double *__restrict__ y)
@@ -702,11 +935,11 @@ __global__ void __launch_bounds__(256) k_prolong(int n, const int64_t *__restric
 #pragma unroll
     for (int c = 0; c < NC; ++c) x[(int64_t)i * NC + c] = acc[c];
 }
-// post-smooth: xo = x + D^-1 (b - A x)
+// post-smooth: xo = x + D^-1 (b - A x)   (x ghost-aware)
 template <int NC>
 __global__ void __launch_bounds__(256) k_vc_post(int n, const int64_t *__restrict__ off, const int32_t *__restrict__ col,
                                                  const double *__restrict__ val, const double *__restrict__ dinv,
-                                                 const double *__restrict__ b, const double *__restrict__ x, double *__restrict__ xo)
+                                                 const double *__restrict__ b, GV x, double *__restrict__ xo)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -719,12 +952,12 @@ __global__ void __launch_bounds__(256) k_vc_post(int n, const int64_t *__restric
     for (int64_t slot = b0; slot < b1; ++slot) {
         const int j = __ldcs(col + slot * 32 + lane);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) acc[c] = fma(__ldcs(val + (slot * NC + c) * 32 + lane), __ldg(x + (int64_t)j * NC + c), acc[c]);
+        for (int c = 0; c < NC; ++c) acc[c] = fma(__ldcs(val + (slot * NC + c) * 32 + lane), GVLD(x, j, c, NC), acc[c]);
     }
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
         const int64_t t = (int64_t)i * NC + c;
-        xo[t] = x[t] + dinv[t] * (b[t] - acc[c]);
+        xo[t] = x.own[t] + dinv[t] * (b[t] - acc[c]);
     }
 }
 // coarsest: x = A_c^-1 b per component
@@ -745,8 +978,7 @@ __global__ void k_coarse(int n, const double *__restrict__ inv, const double *__
 // MODE 0: y = A x ; MODE 1: pre (x = D^-1 b, r = b - A D^-1 b) ; MODE 2: post (xo = x + D^-1 (b - A x))
 template <int NC, int MODE>
 __global__ void __launch_bounds__(256) k_csr_warp(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
-                                                  const double *__restrict__ v, const double *__restrict__ dinv,
-                                                  const double *__restrict__ b, const double *__restrict__ x,
+                                                  const double *__restrict__ v, GV dinv, GV b, GV x,
                                                   double *__restrict__ out1, double *__restrict__ out2)
 {
     const int lane = threadIdx.x & 31;
@@ -760,7 +992,7 @@ __global__ void __launch_bounds__(256) k_csr_warp(int n, const int32_t *__restri
         const int j = ci[q];
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-            const double xv = MODE == 1 ? __ldg(b + (int64_t)j * NC + c) * __ldg(dinv + (int64_t)j * NC + c) : __ldg(x + (int64_t)j * NC + c);
+            const double xv = MODE == 1 ? GVLD(b, j, c, NC) * GVLD(dinv, j, c, NC) : GVLD(x, j, c, NC);
             acc[c] = fma(__ldcs(v + q * NC + c), xv, acc[c]);
         }
     }
@@ -773,14 +1005,23 @@ __global__ void __launch_bounds__(256) k_csr_warp(int n, const int32_t *__restri
         for (int c = 1; c < NC; ++c) if (lane == c) a = acc[c];
         const int64_t t = (int64_t)i * NC + lane;
         if (MODE == 0) out1[t] = a;
-        else if (MODE == 1) { out1[t] = b[t] * dinv[t]; out2[t] = b[t] - a; }
-        else out1[t] = x[t] + dinv[t] * (b[t] - a);
+        else if (MODE == 1) { out1[t] = b.own[t] * dinv.own[t]; out2[t] = b.own[t] - a; }
+        else out1[t] = x.own[t] + dinv.own[t] * (b.own[t] - a);
     }
+}
+
+// compact the padded allgather [rank][mx*nc] into the full replicated vector
+__global__ void k_rep_compact(int nranks, int nc, int64_t mx, const int64_t *__restrict__ offs, const double *__restrict__ buf,
+                              double *__restrict__ out)
+{
+    const int r = blockIdx.y;
+    const int64_t cnt = (offs[r + 1] - offs[r]) * nc;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < cnt; k += (int64_t)gridDim.x * blockDim.x)
+        out[offs[r] * nc + k] = buf[r * mx * nc + k];
 }
 
 static double sbytes(const Sell &S) { return (double)S.slots * 32 * (4.0 + 8.0 * S.bs); }
 static double cbytes(const Csr &A) { return (double)A.nnz * (4.0 + 8.0 * A.nc); }
-static bool use_warp(const Csr &A) { return A.n > 0 && A.nnz >= 12 * (int64_t)A.n; }
 
 template <int NC>
 static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
@@ -796,24 +1037,46 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     }
     const int n = L.n;
     const double vec = 8.0 * NC * n;
-    const bool wA = l > 0 && use_warp(L.A), wR = use_warp(L.R);
+    const bool wA = L.warpA, wR = L.warpR;
     const double bA = wA ? cbytes(L.A) : sbytes(L.sA), bR = wR ? cbytes(L.R) : sbytes(L.sR);
+    const double *ghd = L.dist ? L.dinv_gh.p : nullptr;
+    // pre-smooth + residual (needs b and D^-1 of the ghost rows)
+    if (L.dist) halo_exchange(c, *L.hp, NC, b, L.gh_b);
+    const GV gb = gv(b, n, L.dist ? L.gh_b.p : nullptr), gd = gv(L.dinv, n, ghd);
     prof_begin(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P);
-    if (wA) k_csr_warp<NC, 1><<<grid_for(n, 8), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, L.A.v, L.dinv, b, nullptr, L.x2, L.r);
-    else k_vc_pre<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sA.off, L.sA.col, L.sA.val, L.dinv, b, L.x2, L.r);
+    if (wA) k_csr_warp<NC, 1><<<grid_for(n, 8), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, L.A.v, gd, gb, gv(nullptr, 0), L.x2, L.r);
+    else if (n) k_vc_pre<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sA.off, L.sA.col, L.sA.val, gd, gb, L.x2, L.r);
     prof_end(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P, bA + 4 * vec);
+    // restriction (local rows of R); a replicated next level is gathered on every rank
     Level &Lc = H.L[l + 1];
+    const bool gather = L.dist && !L.next_dist;
+    const int nr = L.sR.nrows;
+    double *rdst = gather ? L.rep_buf.p + (size_t)c.nranks * 0 : Lc.b.p;
     prof_begin(c, mech ? PK_VC_RESTR_U : PK_VC_RESTR_P);
-    if (wR) k_csr_warp<NC, 0><<<grid_for(Lc.n, 8), 256, 0, c.s>>>(Lc.n, L.R.rp, L.R.ci, L.R.v, nullptr, nullptr, L.r, Lc.b, nullptr);
-    else k_sell_mv<NC><<<grid_for(Lc.n, 256), 256, 0, c.s>>>(Lc.n, L.sR.off, L.sR.col, L.sR.val, L.r, Lc.b);
-    prof_end(c, mech ? PK_VC_RESTR_U : PK_VC_RESTR_P, bR + vec + 8.0 * NC * Lc.n);
+    if (wR) k_csr_warp<NC, 0><<<grid_for(nr, 8), 256, 0, c.s>>>(nr, L.R.rp, L.R.ci, L.R.v, gv(nullptr, 0), gv(nullptr, 0),
+                                                             gv(L.r, n), rdst, nullptr);
+    else if (nr) k_sell_mv<NC><<<grid_for(nr, 256), 256, 0, c.s>>>(nr, L.sR.off, L.sR.col, L.sR.val, L.r, rdst);
+    prof_end(c, mech ? PK_VC_RESTR_U : PK_VC_RESTR_P, bR + vec + 8.0 * NC * nr);
+    if (gather) {
+        int64_t mx = 1;
+        for (auto v : L.rep_counts) mx = std::max(mx, v);
+        double *recv = L.rep_buf.p + (size_t)mx * NC;
+        c.comm->allgather(L.rep_buf.p, recv, sizeof(double) * mx * NC, c.s);
+        DBuf<int64_t> offs; offs.alloc(c.nranks + 1);
+        TSP_CUDA(cudaMemcpyAsync(offs, L.rep_offs.data(), sizeof(int64_t) * (c.nranks + 1), cudaMemcpyHostToDevice, c.s));
+        k_rep_compact<<<dim3(grid_for(mx * NC, 256), c.nranks), 256, 0, c.s>>>(c.nranks, NC, mx, offs, recv, Lc.b);
+        c.launches++;
+    }
     vcycle_rec<NC>(c, H, l + 1, Lc.b, Lc.x);
     prof_begin(c, mech ? PK_VC_PROL_U : PK_VC_PROL_P);
-    k_prolong<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sP.off, L.sP.col, L.sP.val, Lc.x, L.x2);
+    if (n) k_prolong<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sP.off, L.sP.col, L.sP.val, Lc.x, L.x2);
     prof_end(c, mech ? PK_VC_PROL_U : PK_VC_PROL_P, sbytes(L.sP) + 2 * vec + 8.0 * NC * Lc.n);
+    // post-smooth (needs x of the ghost rows)
+    if (L.dist) halo_exchange(c, *L.hp, NC, L.x2, L.gh_x);
+    const GV gx = gv(L.x2, n, L.dist ? L.gh_x.p : nullptr);
     prof_begin(c, mech ? PK_VC_POST_U : PK_VC_POST_P);
-    if (wA) k_csr_warp<NC, 2><<<grid_for(n, 8), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, L.A.v, L.dinv, b, L.x2, xout, nullptr);
-    else k_vc_post<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sA.off, L.sA.col, L.sA.val, L.dinv, b, L.x2, xout);
+    if (wA) k_csr_warp<NC, 2><<<grid_for(n, 8), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, L.A.v, gv(L.dinv, n), gv(b, n), gx, xout, nullptr);
+    else if (n) k_vc_post<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sA.off, L.sA.col, L.sA.val, L.dinv, b, gx, xout);
     prof_end(c, mech ? PK_VC_POST_U : PK_VC_POST_P, bA + 4 * vec);
     c.launches += 4;
 }

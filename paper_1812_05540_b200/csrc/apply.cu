@@ -3,6 +3,8 @@
 // 3-4, 5 (pressure V-cycle), 6-8 fused with the tile ILU
 // (P:629-634).  All matrices are SELL-32 (thread per block row, coalesced
 // slot-major values, streaming loads for the matrix, cached loads for x).
+// On a z-slab (multi-GPU) every x-gather is ghost-aware (GV): columns >= the
+// owned count read the halo received from rank-1 / rank+1 just before.
 #include "tsp_internal.cuh"
 
 namespace tsp {
@@ -12,8 +14,7 @@ namespace tsp {
 __global__ void __launch_bounds__(256) k_op_node(int Nn, const int64_t *__restrict__ off_uu, const int32_t *__restrict__ col_uu,
                                                  const double *__restrict__ val_uu, const int64_t *__restrict__ off_uf,
                                                  const int32_t *__restrict__ col_uf, const double *__restrict__ val_uf,
-                                                 const double *__restrict__ xu, const double *__restrict__ xf,
-                                                 double *__restrict__ yu)
+                                                 GV xu, GV xf, double *__restrict__ yu)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= Nn) return;
@@ -25,7 +26,7 @@ __global__ void __launch_bounds__(256) k_op_node(int Nn, const int64_t *__restri
         for (int64_t slot = b0; slot < b1; ++slot) {
             const int cidx = __ldcs(col_uu + slot * 32 + lane);
             const double *v = val_uu + slot * (9 * 32) + lane;
-            const double x0 = __ldg(xu + 3 * (int64_t)cidx), x1 = __ldg(xu + 3 * (int64_t)cidx + 1), x2 = __ldg(xu + 3 * (int64_t)cidx + 2);
+            const double x0 = GVLD(xu, cidx, 0, 3), x1 = GVLD(xu, cidx, 1, 3), x2 = GVLD(xu, cidx, 2, 3);
             a0 = fma(__ldcs(v + 0 * 32), x0, a0); a0 = fma(__ldcs(v + 1 * 32), x1, a0); a0 = fma(__ldcs(v + 2 * 32), x2, a0);
             a1 = fma(__ldcs(v + 3 * 32), x0, a1); a1 = fma(__ldcs(v + 4 * 32), x1, a1); a1 = fma(__ldcs(v + 5 * 32), x2, a1);
             a2 = fma(__ldcs(v + 6 * 32), x0, a2); a2 = fma(__ldcs(v + 7 * 32), x1, a2); a2 = fma(__ldcs(v + 8 * 32), x2, a2);
@@ -37,7 +38,7 @@ __global__ void __launch_bounds__(256) k_op_node(int Nn, const int64_t *__restri
         for (int64_t slot = b0; slot < b1; ++slot) {
             const int cidx = __ldcs(col_uf + slot * 32 + lane);
             const double *v = val_uf + slot * (6 * 32) + lane;
-            const double x0 = __ldg(xf + 2 * (int64_t)cidx), x1 = __ldg(xf + 2 * (int64_t)cidx + 1);
+            const double x0 = GVLD(xf, cidx, 0, 2), x1 = GVLD(xf, cidx, 1, 2);
             a0 = fma(__ldcs(v + 0 * 32), x0, a0); a0 = fma(__ldcs(v + 1 * 32), x1, a0);
             a1 = fma(__ldcs(v + 2 * 32), x0, a1); a1 = fma(__ldcs(v + 3 * 32), x1, a1);
             a2 = fma(__ldcs(v + 4 * 32), x0, a2); a2 = fma(__ldcs(v + 5 * 32), x1, a2);
@@ -51,8 +52,7 @@ template <int MODE>
 __global__ void __launch_bounds__(256) k_op_cell(int Nc, const int64_t *__restrict__ off_fu, const int32_t *__restrict__ col_fu,
                                                  const double *__restrict__ val_fu, const int64_t *__restrict__ off_ff,
                                                  const int32_t *__restrict__ col_ff, const double *__restrict__ val_ff,
-                                                 const double *__restrict__ xu, const double *__restrict__ xf,
-                                                 const double *__restrict__ vf, double *__restrict__ yf)
+                                                 GV xu, GV xf, const double *__restrict__ vf, double *__restrict__ yf)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= Nc) return;
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(256) k_op_cell(int Nc, const int64_t *__restri
         for (int64_t slot = b0; slot < b1; ++slot) {
             const int cidx = __ldcs(col_fu + slot * 32 + lane);
             const double *v = val_fu + slot * (6 * 32) + lane;
-            const double x0 = __ldg(xu + 3 * (int64_t)cidx), x1 = __ldg(xu + 3 * (int64_t)cidx + 1), x2 = __ldg(xu + 3 * (int64_t)cidx + 2);
+            const double x0 = GVLD(xu, cidx, 0, 3), x1 = GVLD(xu, cidx, 1, 3), x2 = GVLD(xu, cidx, 2, 3);
             a0 = fma(__ldcs(v + 0 * 32), x0, a0); a0 = fma(__ldcs(v + 1 * 32), x1, a0); a0 = fma(__ldcs(v + 2 * 32), x2, a0);
             a1 = fma(__ldcs(v + 3 * 32), x0, a1); a1 = fma(__ldcs(v + 4 * 32), x1, a1); a1 = fma(__ldcs(v + 5 * 32), x2, a1);
         }
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(256) k_op_cell(int Nc, const int64_t *__restri
         for (int64_t slot = b0; slot < b1; ++slot) {
             const int cidx = __ldcs(col_ff + slot * 32 + lane);
             const double *v = val_ff + slot * (4 * 32) + lane;
-            const double x0 = __ldg(xf + 2 * (int64_t)cidx), x1 = __ldg(xf + 2 * (int64_t)cidx + 1);
+            const double x0 = GVLD(xf, cidx, 0, 2), x1 = GVLD(xf, cidx, 1, 2);
             a0 = fma(__ldcs(v + 0 * 32), x0, a0); a0 = fma(__ldcs(v + 1 * 32), x1, a0);
             a1 = fma(__ldcs(v + 2 * 32), x0, a1); a1 = fma(__ldcs(v + 3 * 32), x1, a1);
         }
@@ -89,8 +89,8 @@ __global__ void __launch_bounds__(256) k_op_cell(int Nc, const int64_t *__restri
 // steps 3-4: z_s = D_ss^-1 y_s ; w_p = y_p - A_ps z_s with the full A_ps;
 // z_s of the neighbours is recomputed from y_s instead of re-read.
 __global__ void __launch_bounds__(256) k_step34(int Nc, const int64_t *__restrict__ off, const int32_t *__restrict__ col,
-                                                const double *__restrict__ aps, const double *__restrict__ dssinv,
-                                                const double *__restrict__ yf, double *__restrict__ zs, double *__restrict__ wp)
+                                                const double *__restrict__ aps, GV dssinv, GV yf, double *__restrict__ zs,
+                                                double *__restrict__ wp)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= Nc) return;
@@ -100,10 +100,10 @@ __global__ void __launch_bounds__(256) k_step34(int Nc, const int64_t *__restric
 #pragma unroll 4
     for (int64_t slot = b0; slot < b1; ++slot) {
         const int j = __ldcs(col + slot * 32 + lane);
-        acc = fma(__ldcs(aps + slot * 32 + lane), __ldg(yf + 2 * (int64_t)j) * __ldg(dssinv + j), acc);
+        acc = fma(__ldcs(aps + slot * 32 + lane), GVLD(yf, j, 0, 2) * GVLD(dssinv, j, 0, 1), acc);
     }
-    zs[i] = yf[2 * (int64_t)i] * dssinv[i];
-    wp[i] = yf[2 * (int64_t)i + 1] - acc;
+    zs[i] = yf.own[2 * (int64_t)i] * dssinv.own[i];
+    wp[i] = yf.own[2 * (int64_t)i + 1] - acc;
 }
 
 static double sell_bytes(const Sell &S) { return (double)S.slots * 32 * (4.0 + 8.0 * S.bs); }
@@ -112,13 +112,16 @@ void op_apply(Ctx &c, const double *x, double *y)
 {
     const double *xu = x, *xf = x + 3 * (int64_t)c.Nn;
     double *yu = y, *yf = y + 3 * (int64_t)c.Nn;
+    halo_exchange(c, c.hu, 3, xu, c.gh_u);
+    halo_exchange(c, c.hf, 2, xf, c.gh_f);
+    const GV gu = gv(xu, c.Nn, c.gh_u.p), gf = gv(xf, c.Nc, c.gh_f.p);
     prof_begin(c, PK_OP_NODE);
-    k_op_node<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(c.Nn, c.s_uu.off, c.s_uu.col, c.s_uu.val, c.s_uf.off, c.s_uf.col,
-                                                    c.s_uf.val, xu, xf, yu);
+    if (c.Nn) k_op_node<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(c.Nn, c.s_uu.off, c.s_uu.col, c.s_uu.val, c.s_uf.off, c.s_uf.col,
+                                                              c.s_uf.val, gu, gf, yu);
     prof_end(c, PK_OP_NODE, sell_bytes(c.s_uu) + sell_bytes(c.s_uf) + 48.0 * c.Nn + 16.0 * c.Nc);
     prof_begin(c, PK_OP_CELL);
-    k_op_cell<0><<<grid_for(c.Nc, 256), 256, 0, c.s>>>(c.Nc, c.s_fu.off, c.s_fu.col, c.s_fu.val, c.s_ff.off, c.s_ff.col,
-                                                       c.s_ff.val, xu, xf, nullptr, yf);
+    if (c.Nc) k_op_cell<0><<<grid_for(c.Nc, 256), 256, 0, c.s>>>(c.Nc, c.s_fu.off, c.s_fu.col, c.s_fu.val, c.s_ff.off, c.s_ff.col,
+                                                                 c.s_ff.val, gu, gf, nullptr, yf);
     prof_end(c, PK_OP_CELL, sell_bytes(c.s_fu) + sell_bytes(c.s_ff) + 24.0 * c.Nn + 32.0 * c.Nc);
     c.launches += 2;
     TSP_CUDA(cudaGetLastError());
@@ -133,18 +136,23 @@ void prec_apply(Ctx &c, const double *v, double *z)
     // step 1: z_u = M_uu^-1 v_u
     amg_vcycle(c, c.mech, vu, zu, true);
     // step 2: y_f = v_f - A_fu z_u
+    halo_exchange(c, c.hu, 3, zu, c.gh_u);
     prof_begin(c, PK_STEP2);
-    k_op_cell<1><<<grid_for(c.Nc, 256), 256, 0, c.s>>>(c.Nc, c.s_fu.off, c.s_fu.col, c.s_fu.val, nullptr, nullptr, nullptr,
-                                                       zu, nullptr, vf, c.w_yf);
+    if (c.Nc) k_op_cell<1><<<grid_for(c.Nc, 256), 256, 0, c.s>>>(c.Nc, c.s_fu.off, c.s_fu.col, c.s_fu.val, nullptr, nullptr, nullptr,
+                                                                 gv(zu, c.Nn, c.gh_u.p), gv(nullptr, 0), vf, c.w_yf);
     prof_end(c, PK_STEP2, sell_bytes(c.s_fu) + 24.0 * c.Nn + 32.0 * c.Nc);
     // steps 3-4
+    halo_exchange(c, c.hf, 2, c.w_yf, c.gh_f);
     prof_begin(c, PK_STEP34);
-    k_step34<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(c.Nc, c.s_aps.off, c.s_aps.col, c.s_aps.val, c.dss_inv, c.w_yf, c.w_tmp,
-                                                   c.w_wp);
+    if (c.Nc) k_step34<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(c.Nc, c.s_aps.off, c.s_aps.col, c.s_aps.val, gv(c.dss_inv, c.Nc, c.gh_dss.p),
+                                                             gv(c.w_yf, c.Nc, c.gh_f.p), c.w_tmp, c.w_wp);
     prof_end(c, PK_STEP34, sell_bytes(c.s_aps) + 40.0 * c.Nc);
     // step 5: z_p = M_pp^-1 w_p
     amg_vcycle(c, c.pres, c.w_wp, c.w_zp, false);
     // steps 6-8: w_f = y_f - S_ff^FS z_f ; z_f += P^T M_L^-1 P w_f
+    const int ng = c.hf.nghost();
+    halo_exchange(c, c.hf, 1, c.w_tmp, c.gh_f2);
+    halo_exchange(c, c.hf, 1, c.w_zp, c.gh_f2.p + ng);
     ilu_apply_fused(c, c.w_yf, c.w_tmp, c.w_zp, zf);
     c.launches += 2;
     TSP_CUDA(cudaGetLastError());

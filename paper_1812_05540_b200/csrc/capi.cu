@@ -121,36 +121,71 @@ tsp_status tsp_create(tsp_handle *out, const tsp_desc *d)
     tsp_handle h = nullptr;
     API_BEGIN
     TSP_REQUIRE(d->nx > 0 && d->ny > 0 && d->nz > 0, TSP_ERR_INVALID_ARG, "grid dimensions must be positive");
-    TSP_REQUIRE(d->nranks == 1 && d->rank == 0, TSP_ERR_INVALID_ARG, "this build supports nranks == 1 (see DESIGN.md)");
+    TSP_REQUIRE(d->nranks >= 1 && d->rank >= 0 && d->rank < d->nranks, TSP_ERR_INVALID_ARG, "bad rank / nranks");
     const tsp_bsr *bs[4] = {&d->A_uu, &d->A_uf, &d->A_fu, &d->A_ff};
     for (int k = 0; k < 4; ++k)
         TSP_REQUIRE(bs[k]->rowptr && bs[k]->col && bs[k]->val, TSP_ERR_INVALID_ARG, "null matrix pointer");
     TSP_REQUIRE(d->fs_diag, TSP_ERR_INVALID_ARG, "null fs_diag");
     c = new tsp_ctx();
-    c->nx = d->nx; c->ny = d->ny; c->nz = d->nz;
-    c->Nn = (d->nx + 1) * (d->ny + 1) * (d->nz + 1);
-    c->Nc = d->nx * d->ny * d->nz;
-    c->n = 3 * (int64_t)c->Nn + 2 * (int64_t)c->Nc;
     c->s = (cudaStream_t)d->stream;
     StreamScope ss2_(c->s);
     c->o = d->opts;
-    if (c->o.amg_theta <= 0 || c->o.amg_coarse_max <= 0) tsp_default_options(&c->o);
+    if (c->o.amg_theta <= 0 || c->o.amg_coarse_max <= 0) { int rr = c->o.replicate_rows; tsp_default_options(&c->o); c->o.replicate_rows = rr; }
     if (c->o.zblock <= 0) c->o.zblock = 16;
     if (c->o.tile_x <= 0 || c->o.tile_y <= 0 || c->o.tile_z <= 0) c->o.tile_x = c->o.tile_y = c->o.tile_z = 16;
+    if (c->o.replicate_rows <= 0) c->o.replicate_rows = 32768;
+    // z-slab partition (include/tsp.h): local sizes in Nn, Nc, n, nz
+    c->rank = d->rank; c->nranks = d->nranks;
+    c->nx = d->nx; c->ny = d->ny; c->nz_glob = d->nz;
+    const int nzb = (d->nz + c->o.zblock - 1) / c->o.zblock;
+    TSP_REQUIRE(d->nranks <= nzb, TSP_ERR_INVALID_ARG, "more ranks than z-blocks");
+    int64_t part[6];
+    partition(d->nx, d->ny, d->nz, c->o.zblock, d->rank, d->nranks, part);
+    c->k0 = (int)part[0]; c->k1 = (int)part[1];
+    c->node_off = part[2]; c->Nn = (int)part[3]; c->cell_off = part[4]; c->Nc = (int)part[5];
+    c->nz = c->k1 - c->k0;
+    c->Nn_glob = (int64_t)(d->nx + 1) * (d->ny + 1) * (d->nz + 1);
+    c->Nc_glob = (int64_t)d->nx * d->ny * d->nz;
+    c->n = 3 * (int64_t)c->Nn + 2 * (int64_t)c->Nc;
+    c->n_glob = 3 * c->Nn_glob + 2 * c->Nc_glob;
+    if (d->nranks > 1) {
+        TSP_REQUIRE(d->comm_kind == TSP_COMM_NCCL || d->comm_kind == TSP_COMM_LOCAL, TSP_ERR_INVALID_ARG,
+                    "nranks > 1 needs a communicator (comm_kind)");
+        c->comm = make_comm(d->comm_kind, (void *)d->comm_arg, d->rank, d->nranks);
+    }
     int dev = 0;
     TSP_CUDA(cudaGetDevice(&dev));
     TSP_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, dev));
     const bool on_dev = d->inputs_on_device != 0;
-    csr_upload(*c, c->uu, c->Nn, c->Nn, 9, d->A_uu.rowptr, d->A_uu.col, d->A_uu.val, on_dev);
-    csr_upload(*c, c->uf, c->Nn, c->Nc, 6, d->A_uf.rowptr, d->A_uf.col, d->A_uf.val, on_dev);
-    csr_upload(*c, c->fu, c->Nc, c->Nn, 6, d->A_fu.rowptr, d->A_fu.col, d->A_fu.val, on_dev);
-    csr_upload(*c, c->ff, c->Nc, c->Nc, 4, d->A_ff.rowptr, d->A_ff.col, d->A_ff.val, on_dev);
+    csr_upload(*c, c->uu, c->Nn, (int)c->Nn_glob, 9, d->A_uu.rowptr, d->A_uu.col, d->A_uu.val, on_dev);
+    csr_upload(*c, c->uf, c->Nn, (int)c->Nc_glob, 6, d->A_uf.rowptr, d->A_uf.col, d->A_uf.val, on_dev);
+    csr_upload(*c, c->fu, c->Nc, (int)c->Nn_glob, 6, d->A_fu.rowptr, d->A_fu.col, d->A_fu.val, on_dev);
+    csr_upload(*c, c->ff, c->Nc, (int)c->Nc_glob, 4, d->A_ff.rowptr, d->A_ff.col, d->A_ff.val, on_dev);
     check_csr(*c, c->uu, "A_uu"); check_csr(*c, c->uf, "A_uf"); check_csr(*c, c->fu, "A_fu"); check_csr(*c, c->ff, "A_ff");
-    c->fs.alloc(2 * (size_t)c->Nc);
-    TSP_CUDA(cudaMemcpyAsync(c->fs, d->fs_diag, sizeof(double) * 2 * c->Nc, on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->s));
+    // global -> local column ids; halo plans of the node (u) and cell (f) spaces
+    if (c->comm) {
+        Csr *ms[4] = {&c->uu, &c->uf, &c->fu, &c->ff};
+        for (Csr *A : ms) {
+            A->gci.alloc(std::max<int64_t>(A->nnz, 1));
+            if (A->nnz) TSP_CUDA(cudaMemcpyAsync(A->gci, A->ci, 4 * A->nnz, cudaMemcpyDeviceToDevice, c->s));
+        }
+        halo_build(*c, c->hu, c->Nn, c->node_off, c->uu.gci, c->uu.nnz, c->uu.ci);
+        halo_remap(*c, c->hu, c->node_off, c->fu.gci, c->fu.nnz, c->fu.ci);
+        halo_build(*c, c->hf, c->Nc, c->cell_off, c->ff.gci, c->ff.nnz, c->ff.ci);
+        halo_remap(*c, c->hf, c->cell_off, c->uf.gci, c->uf.nnz, c->uf.ci);
+        c->gh_u.alloc((size_t)std::max(c->hu.nghost(), 1) * 3);
+        c->gh_f.alloc((size_t)std::max(c->hf.nghost(), 1) * 2);
+        c->gh_f2.alloc((size_t)std::max(c->hf.nghost(), 1) * 2);
+        c->gh_dss.alloc((size_t)std::max(c->hf.nghost(), 1));
+    } else {
+        c->hu.nown = c->Nn; c->hf.nown = c->Nc;
+    }
+    reduce_setup(*c);
+    c->fs.alloc(2 * (size_t)std::max(c->Nc, 1));
+    if (c->Nc) TSP_CUDA(cudaMemcpyAsync(c->fs, d->fs_diag, sizeof(double) * 2 * c->Nc, on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->s));
     {
         std::vector<double> fsh(2 * (size_t)c->Nc);
-        TSP_CUDA(cudaMemcpyAsync(fsh.data(), c->fs, sizeof(double) * fsh.size(), cudaMemcpyDeviceToHost, c->s));
+        if (c->Nc) TSP_CUDA(cudaMemcpyAsync(fsh.data(), c->fs, sizeof(double) * fsh.size(), cudaMemcpyDeviceToHost, c->s));
         TSP_CUDA(cudaStreamSynchronize(c->s));
         for (double v : fsh) TSP_REQUIRE(v >= 0.0, TSP_ERR_INVALID_ARG, "negative fixed-stress diagonal (S:355)");
     }
@@ -168,7 +203,7 @@ tsp_status tsp_create(tsp_handle *out, const tsp_desc *d)
     catch (const tsp::Error &e) {
         set_error(e.msg);
         (void)h;
-        delete c;
+        if (c) { Comm *cm = c->comm; delete c; delete cm; }
         return e.st;
     }
 }
@@ -293,7 +328,7 @@ tsp_status tsp_export_level(tsp_handle h, int which, int lvl, int32_t *A_rp, int
         if (dst && bytes) TSP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
     };
     cp(A_rp, L.A.rp, sizeof(int32_t) * (L.n + 1));
-    cp(A_ci, L.A.ci, sizeof(int32_t) * L.A.nnz);
+    cp(A_ci, L.A.gci.p ? L.A.gci.p : L.A.ci.p, sizeof(int32_t) * L.A.nnz);   // global column ids
     cp(A_v, L.A.v, sizeof(double) * L.A.nnz * L.nc);
     cp(dl1, L.dl1, sizeof(double) * L.n * L.nc);
     if (!L.coarsest) {
@@ -303,7 +338,21 @@ tsp_status tsp_export_level(tsp_handle h, int which, int lvl, int32_t *A_rp, int
         cp(P_v, L.P.v, sizeof(double) * L.P.nnz * L.nc);
     }
     TSP_CUDA(cudaStreamSynchronize(s));
+    if (!L.coarsest && L.coarse_off) {     // aggregate / coarse ids exported in global numbering
+        if (agg) for (int i = 0; i < L.n; ++i) if (agg[i] >= 0) agg[i] += (int32_t)L.coarse_off;
+        if (P_ci && L.next_dist) for (int64_t q = 0; q < L.P.nnz; ++q) P_ci[q] += (int32_t)L.coarse_off;
+    }
     API_END
+}
+
+tsp_status tsp_level_dist(tsp_handle h, int which, int lvl, int64_t out3[3])
+{
+    if (!h || !out3) { set_error("null argument"); return TSP_ERR_INVALID_ARG; }
+    Hier &H = which ? h->pres : h->mech;
+    if (lvl < 0 || lvl >= (int)H.L.size()) { set_error("level out of range"); return TSP_ERR_INVALID_ARG; }
+    const Level &L = H.L[lvl];
+    out3[0] = L.dist; out3[1] = L.dist ? L.nglob : L.n; out3[2] = L.dist ? L.row_off : 0;
+    return TSP_OK;
 }
 
 tsp_status tsp_prof_enable(tsp_handle h, int on)
@@ -343,7 +392,9 @@ void tsp_destroy(tsp_handle h)
     StreamScope ss_(h->s);
     cudaStreamSynchronize(h->s);
     for (auto &e : h->prof.pool) cudaEventDestroy(e);
+    Comm *cm = h->comm;
     delete h;
+    delete cm;
 }
 
 }  // extern "C"

@@ -24,8 +24,9 @@
 namespace tsp {
 
 // slot order: 0 -z, 1 -y, 2 -x, 3 self, 4 +x, 5 +y, 6 +z
+// nx, ny, nz: LOCAL slab grid (nz = owned cell planes); k0: first owned global plane
 struct TileGeo {
-    int nx, ny, nz, tx, ty, tz, ntx, nty, ntz, W, nlev;
+    int nx, ny, nz, tx, ty, tz, ntx, nty, ntz, W, nlev, k0, nlo, nhi;
 };
 
 __device__ __forceinline__ int64_t vidx(const TileGeo &g, int64_t t, int lk, int lj, int s, int e, int li)
@@ -39,7 +40,8 @@ __device__ __forceinline__ int64_t didx(const TileGeo &g, int64_t t, int lk, int
 __device__ __forceinline__ int sidx(const TileGeo &g, int lk, int lj, int li) { return ((lk * g.ty + lj) * g.tx + li) * 2; }
 
 // fill the tile-ordered S_ff^FS = A_ff + diag(D_sp, D_pp) blocks (a1 folded in)
-__global__ void k_ilu_fill(TileGeo g, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+// (column ids are GLOBAL cell ids: neighbours in the ranks below/above keep their stencil slot)
+__global__ void k_ilu_fill(TileGeo g, int nyg, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
                            const double *__restrict__ v, const double *__restrict__ fs, double *__restrict__ ival)
 {
     int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -53,7 +55,7 @@ __global__ void k_ilu_fill(TileGeo g, const int32_t *__restrict__ rp, const int3
     const int dxs[7] = {0, 0, -1, 0, 1, 0, 0}, dys[7] = {0, -1, 0, 0, 0, 1, 0}, dzs[7] = {-1, 0, 0, 0, 0, 0, 1};
     for (int64_t q = rp[c]; q < rp[c + 1]; ++q) {
         const int64_t d = ci[q];
-        const int di = (int)(d % g.nx) - i, dj = (int)((d / g.nx) % g.ny) - j, dk = (int)(d / ((int64_t)g.nx * g.ny)) - k;
+        const int di = (int)(d % g.nx) - i, dj = (int)((d / g.nx) % nyg) - j, dk = (int)(d / ((int64_t)g.nx * nyg)) - (k + g.k0);
         int s = -1;
         for (int u = 0; u < 7; ++u) if (dxs[u] == di && dys[u] == dj && dzs[u] == dk) s = u;
         if (s < 0) continue;
@@ -163,7 +165,8 @@ __device__ __forceinline__ void pf_load(const double *__restrict__ ival, const d
 __global__ void __launch_bounds__(256) k_ilu_apply2(TileGeo g, const int32_t *__restrict__ lines, const int32_t *__restrict__ lvlptr,
                                                     const double *__restrict__ ival, const double *__restrict__ dinv,
                                                     const double *__restrict__ yf, const double *__restrict__ zs,
-                                                    const double *__restrict__ zp, double *__restrict__ zout)
+                                                    const double *__restrict__ zp, const double *__restrict__ zs_gh,
+                                                    const double *__restrict__ zp_gh, double *__restrict__ zout)
 {
     extern __shared__ double sm[];   // [lk][lj][li][2]: w, then yhat, then x
     const int64_t t = blockIdx.x;
@@ -184,11 +187,20 @@ __global__ void __launch_bounds__(256) k_ilu_apply2(TileGeo g, const int32_t *__
 #pragma unroll
         for (int s = 0; s < 7; ++s) {
             const int ni = gi + dxs[s], nj = gj + dys[s], nk = gk + dzs[s];
-            if (ni < 0 || nj < 0 || nk < 0 || ni >= g.nx || nj >= g.ny || nk >= g.nz) continue;
-            const int64_t gn = gc + dxs[s] + dys[s] * sy + dzs[s] * sz;
+            if (ni < 0 || nj < 0 || ni >= g.nx || nj >= g.ny) continue;
+            double z0, z1;
+            if (nk < 0) {                       // plane below the slab: halo from rank-1
+                if (!g.nlo) continue;
+                z0 = zs_gh[nj * g.nx + ni]; z1 = zp_gh[nj * g.nx + ni];
+            } else if (nk >= g.nz) {            // plane above the slab: halo from rank+1
+                if (!g.nhi) continue;
+                z0 = zs_gh[g.nlo + nj * g.nx + ni]; z1 = zp_gh[g.nlo + nj * g.nx + ni];
+            } else {
+                const int64_t gn = gc + dxs[s] + dys[s] * sy + dzs[s] * sz;
+                z0 = zs[gn]; z1 = zp[gn];
+            }
             double A[4];
             ld2x2(ival, g, t, lk, lj, s, li, A);
-            const double z0 = zs[gn], z1 = zp[gn];
             r0 -= A[0] * z0 + A[1] * z1;
             r1 -= A[2] * z0 + A[3] * z1;
         }
@@ -285,126 +297,16 @@ __global__ void __launch_bounds__(256) k_ilu_apply2(TileGeo g, const int32_t *__
     }
 }
 
-// (first version, kept for reference/validation: w computed inside the forward sweep)
-__global__ void __launch_bounds__(256) k_ilu_apply(TileGeo g, const int32_t *__restrict__ lines, const int32_t *__restrict__ lvlptr,
-                                                   const double *__restrict__ ival, const double *__restrict__ dinv,
-                                                   const double *__restrict__ yf, const double *__restrict__ zs,
-                                                   const double *__restrict__ zp, double *__restrict__ zout)
-{
-    extern __shared__ double sm[];   // [lk][lj][li][2]
-    const int64_t t = blockIdx.x;
-    const int TI = t % g.ntx, TJ = (t / g.ntx) % g.nty, TK = t / ((int64_t)g.ntx * g.nty);
-    const int64_t sy = g.nx, sz = (int64_t)g.nx * g.ny;
-    const int W = g.W, lane = threadIdx.x & 31, lseg = lane & (W - 1);
-    const int slot0 = (threadIdx.x >> 5) * (32 / W) + lane / W, nslots = (blockDim.x >> 5) * (32 / W);
-    const int li = lseg, gi = TI * g.tx + li;
-    const bool xin = li < g.tx && gi < g.nx;
-    // ---------------- forward
-    for (int l = 0; l < g.nlev; ++l) {
-        for (int base = lvlptr[l]; base < lvlptr[l + 1]; base += nslots) {
-            const int idx = base + slot0;
-            const bool lv = idx < lvlptr[l + 1];
-            const int lj = lv ? (lines[idx] & 0xffff) : 0, lk = lv ? (lines[idx] >> 16) : 0;
-            const int gj = TJ * g.ty + lj, gk = TK * g.tz + lk;
-            const bool ok = lv && xin && gj < g.ny && gk < g.nz;
-            double M[4] = {0, 0, 0, 0}, c[2] = {0, 0};
-            if (ok) {
-                const int64_t gc = gi + sy * gj + sz * gk;
-                double r0 = yf[2 * gc], r1 = yf[2 * gc + 1];
-                // step 6: w = y - S^FS z over the 7-point stencil (z from global, neighbours across tiles included)
-                const int dxs[7] = {0, 0, -1, 0, 1, 0, 0}, dys[7] = {0, -1, 0, 0, 0, 1, 0}, dzs[7] = {-1, 0, 0, 0, 0, 0, 1};
-#pragma unroll
-                for (int s = 0; s < 7; ++s) {
-                    const int ni = gi + dxs[s], nj = gj + dys[s], nk = gk + dzs[s];
-                    if (ni < 0 || nj < 0 || nk < 0 || ni >= g.nx || nj >= g.ny || nk >= g.nz) continue;
-                    const int64_t gn = gc + dxs[s] + dys[s] * sy + dzs[s] * sz;
-                    double A[4];
-                    ld2x2(ival, g, t, lk, lj, s, li, A);
-                    const double z0 = zs[gn], z1 = zp[gn];
-                    r0 -= A[0] * z0 + A[1] * z1;
-                    r1 -= A[2] * z0 + A[3] * z1;
-                }
-                // lower neighbours of other lines (previous wavefront levels, shared memory)
-                if (lj > 0) {
-                    double A[4]; ld2x2(ival, g, t, lk, lj, 1, li, A);
-                    const double y0 = sm[sidx(g, lk, lj - 1, li)], y1 = sm[sidx(g, lk, lj - 1, li) + 1];
-                    r0 -= A[0] * y0 + A[1] * y1; r1 -= A[2] * y0 + A[3] * y1;
-                }
-                if (lk > 0) {
-                    double A[4]; ld2x2(ival, g, t, lk, lj, 0, li, A);
-                    const double y0 = sm[sidx(g, lk - 1, lj, li)], y1 = sm[sidx(g, lk - 1, lj, li) + 1];
-                    r0 -= A[0] * y0 + A[1] * y1; r1 -= A[2] * y0 + A[3] * y1;
-                }
-                double D[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) D[e] = dinv[didx(g, t, lk, lj, e, li)];
-                c[0] = D[0] * r0 + D[1] * r1;
-                c[1] = D[2] * r0 + D[3] * r1;
-                if (li > 0) {
-                    double A[4], T[4];
-                    ld2x2(ival, g, t, lk, lj, 2, li, A);
-                    mm2(D, A, T);
-                    M[0] = -T[0]; M[1] = -T[1]; M[2] = -T[2]; M[3] = -T[3];
-                }
-            }
-            affine_scan<true>(M, c, lseg, W);
-            if (ok) { sm[sidx(g, lk, lj, li)] = c[0]; sm[sidx(g, lk, lj, li) + 1] = c[1]; }
-        }
-        __syncthreads();
-    }
-    // ---------------- backward
-    for (int l = g.nlev - 1; l >= 0; --l) {
-        for (int base = lvlptr[l]; base < lvlptr[l + 1]; base += nslots) {
-            const int idx = base + slot0;
-            const bool lv = idx < lvlptr[l + 1];
-            const int lj = lv ? (lines[idx] & 0xffff) : 0, lk = lv ? (lines[idx] >> 16) : 0;
-            const int gj = TJ * g.ty + lj, gk = TK * g.tz + lk;
-            const bool ok = lv && xin && gj < g.ny && gk < g.nz;
-            double M[4] = {0, 0, 0, 0}, c[2] = {0, 0};
-            if (ok) {
-                double t0 = 0, t1 = 0;
-                if (lj + 1 < g.ty && gj + 1 < g.ny) {
-                    double A[4]; ld2x2(ival, g, t, lk, lj, 5, li, A);
-                    const double x0 = sm[sidx(g, lk, lj + 1, li)], x1 = sm[sidx(g, lk, lj + 1, li) + 1];
-                    t0 += A[0] * x0 + A[1] * x1; t1 += A[2] * x0 + A[3] * x1;
-                }
-                if (lk + 1 < g.tz && gk + 1 < g.nz) {
-                    double A[4]; ld2x2(ival, g, t, lk, lj, 6, li, A);
-                    const double x0 = sm[sidx(g, lk + 1, lj, li)], x1 = sm[sidx(g, lk + 1, lj, li) + 1];
-                    t0 += A[0] * x0 + A[1] * x1; t1 += A[2] * x0 + A[3] * x1;
-                }
-                double D[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) D[e] = dinv[didx(g, t, lk, lj, e, li)];
-                c[0] = sm[sidx(g, lk, lj, li)] - (D[0] * t0 + D[1] * t1);
-                c[1] = sm[sidx(g, lk, lj, li) + 1] - (D[2] * t0 + D[3] * t1);
-                if (li + 1 < g.tx && gi + 1 < g.nx) {
-                    double A[4], T[4];
-                    ld2x2(ival, g, t, lk, lj, 4, li, A);
-                    mm2(D, A, T);
-                    M[0] = -T[0]; M[1] = -T[1]; M[2] = -T[2]; M[3] = -T[3];
-                }
-            }
-            affine_scan<false>(M, c, lseg, W);
-            if (ok) {
-                sm[sidx(g, lk, lj, li)] = c[0]; sm[sidx(g, lk, lj, li) + 1] = c[1];
-                const int64_t gc = gi + sy * gj + sz * gk;
-                zout[2 * gc] = zs[gc] + c[0];        // step 8
-                zout[2 * gc + 1] = zp[gc] + c[1];
-            }
-        }
-        __syncthreads();
-    }
-}
-
 static TileGeo geo(const Ctx &c)
 {
     TileGeo g;
-    g.nx = c.nx; g.ny = c.ny; g.nz = c.nz;
-    g.tx = std::min(c.o.tile_x, c.nx); g.ty = std::min(c.o.tile_y, c.ny); g.tz = std::min(c.o.tile_z, c.nz);
+    g.nx = c.nx; g.ny = c.ny; g.nz = c.nz;   // local slab
+    g.tx = std::min(c.o.tile_x, c.nx); g.ty = std::min(c.o.tile_y, c.ny); g.tz = std::min(c.o.tile_z, std::max(c.nz, 1));
     g.ntx = (c.nx + g.tx - 1) / g.tx; g.nty = (c.ny + g.ty - 1) / g.ty; g.ntz = (c.nz + g.tz - 1) / g.tz;
     g.W = 1; while (g.W < g.tx) g.W <<= 1;
     g.nlev = g.ty + g.tz - 1;
+    g.k0 = c.k0;
+    g.nlo = c.hf.nrecv[0]; g.nhi = c.hf.nrecv[1];
     return g;
 }
 
@@ -412,6 +314,9 @@ void ilu_setup(Ctx &c, const double *)
 {
     TileGeo g = geo(c);
     TSP_REQUIRE(g.tx <= 32 && g.ty <= 0xffff && g.tz <= 0x7fff, TSP_ERR_INVALID_ARG, "ILU tile_x must be <= 32");
+    TSP_REQUIRE(std::min(g.ty, g.tz) <= 8 * (32 / g.W), TSP_ERR_INVALID_ARG, "ILU tile: too many lines per wavefront level");
+    TSP_REQUIRE(c.nranks == 1 || (c.o.zblock % c.o.tile_z == 0 && c.o.tile_z <= c.o.zblock), TSP_ERR_INVALID_ARG,
+                "multi-GPU: tile_z must divide zblock (tiles may not cross slabs)");
     if (c.ilu_tsize != g.tx * g.ty * g.tz) {
         std::vector<int32_t> lines, lvlptr;
         for (int l = 0; l < g.nlev; ++l) {
@@ -434,7 +339,8 @@ void ilu_setup(Ctx &c, const double *)
     c.ilu_dinv.alloc((size_t)c.ntiles * per_tile * 4);
     c.ilu_val.zero(c.s);
     c.ilu_dinv.zero(c.s);
-    k_ilu_fill<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(g, c.ff.rp, c.ff.ci, c.ff.v, c.fs, c.ilu_val);
+    if (c.Nc) k_ilu_fill<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(g, c.ny, c.ff.rp, c.ff.gci.p ? c.ff.gci.p : c.ff.ci.p, c.ff.v, c.fs,
+                                                             c.ilu_val);
     c.dcount.zero(c.s);
     k_ilu_factor<<<c.ntiles, 32, 0, c.s>>>(g, c.ilu_cells, c.ilu_lvlptr, c.ilu_val, c.ilu_dinv, c.dcount);
     TSP_CUDA(cudaGetLastError());
@@ -451,17 +357,14 @@ void ilu_apply_fused(Ctx &c, const double *yf, const double *zs, const double *z
     const size_t smem = sizeof(double) * 2 * (size_t)g.tx * g.ty * g.tz;
     static bool attr_set = false;
     if (!attr_set) {
-        TSP_CUDA(cudaFuncSetAttribute(k_ilu_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         TSP_CUDA(cudaFuncSetAttribute(k_ilu_apply2, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr_set = true;
     }
     TSP_REQUIRE(smem <= 227 * 1024, TSP_ERR_INVALID_ARG, "ILU tile too large for shared memory");
-    const int nslots = 8 * (32 / g.W);
+    const double *zs_gh = c.gh_f2.p, *zp_gh = c.gh_f2.p ? c.gh_f2.p + c.hf.nghost() : nullptr;
     prof_begin(c, PK_ILU);
-    if (std::min(g.ty, g.tz) <= nslots)
-        k_ilu_apply2<<<c.ntiles, 256, smem, c.s>>>(g, c.ilu_cells, c.ilu_lvlptr, c.ilu_val, c.ilu_dinv, yf, zs, zp, zf_out);
-    else
-        k_ilu_apply<<<c.ntiles, 256, smem, c.s>>>(g, c.ilu_cells, c.ilu_lvlptr, c.ilu_val, c.ilu_dinv, yf, zs, zp, zf_out);
+    if (c.ntiles) k_ilu_apply2<<<c.ntiles, 256, smem, c.s>>>(g, c.ilu_cells, c.ilu_lvlptr, c.ilu_val, c.ilu_dinv, yf, zs, zp, zs_gh,
+                                                           zp_gh, zf_out);
     prof_end(c, PK_ILU, (28.0 * 8 + 32 + 16 + 16 + 16) * c.Nc);
     c.launches += 1;
     TSP_CUDA(cudaGetLastError());

@@ -59,6 +59,7 @@ struct Csr {
     int64_t nnz = 0;
     DBuf<int32_t> rp, ci;
     DBuf<double> v;
+    DBuf<int32_t> gci;            // global column ids (distributed matrices only)
 };
 
 // Sliced ELL, slice height 32, column-major inside a slice (R-layout):
@@ -74,10 +75,66 @@ struct Sell {
     DBuf<double> val;             // slots * 32 * bs
 };
 
+// ------------------------------------------------------------------ multi-GPU (row e)
+struct Ctx;
+// Communicator of the z-slab decomposition: halos with rank-1 / rank+1, allgather.
+struct Comm {
+    int rank = 0, nranks = 1;
+    virtual ~Comm() {}
+    virtual void neighbor_exchange(const void *send_lo, size_t bytes_send_lo, void *recv_lo, size_t bytes_recv_lo,
+                                   const void *send_hi, size_t bytes_send_hi, void *recv_hi, size_t bytes_recv_hi,
+                                   cudaStream_t s) = 0;
+    virtual void allgather(const void *send, void *recv, size_t bytes, cudaStream_t s) = 0;
+};
+Comm *make_comm(int kind, void *arg, int rank, int nranks);
+template <class T> std::vector<T> host_allgather(Ctx &c, const std::vector<T> &mine);
+
+// Halo plan of a row-distributed vector (rows owned by this rank are [0, nown) locally,
+// ghosts are appended: [lo neighbour's rows | hi neighbour's rows], each list ascending
+// in global numbering).  nsend/nrecv index 0 = lo neighbour, 1 = hi neighbour.
+struct Halo {
+    int nown = 0;
+    int nsend[2] = {0, 0}, nrecv[2] = {0, 0};
+    DBuf<int32_t> sidx;           // owned rows to send, [lo list | hi list]
+    DBuf<double> sbuf;            // pack buffer (3 values per row max)
+    DBuf<int32_t> glo, ghi;       // global ids of the ghost rows (ascending), to remap other matrices
+    int nghost() const { return nrecv[0] + nrecv[1]; }
+    bool any() const { return nsend[0] + nsend[1] + nrecv[0] + nrecv[1] > 0; }
+};
+// ghost-aware vector for kernels: row j < nown is own[j*nc..], else gh[(j-nown)*nc..]
+struct GV {
+    const double *own;
+    const double *gh;
+    int nown;
+};
+#define GVLD(g, j, c, nc) ((j) < (g).nown ? __ldg((g).own + (int64_t)(j) * (nc) + (c)) : __ldg((g).gh + (int64_t)((j) - (g).nown) * (nc) + (c)))
+inline GV gv(const double *own, int nown, const double *gh = nullptr) { return GV{own, gh, nown}; }
+
+// builds the plan from the GLOBAL column ids of a row-distributed CSR (own rows =
+// global [own_off, own_off + nown)) and rewrites `lcols` with local ids
+void halo_build(Ctx &c, Halo &H, int nown, int64_t own_off, const int32_t *gcols, int64_t nnz, int32_t *lcols);
+// remap another matrix whose columns live in the same row space with an existing plan
+void halo_remap(Ctx &c, const Halo &H, int64_t own_off, const int32_t *gcols, int64_t nnz, int32_t *lcols);
+// exchange: ghost[(nrecv0+nrecv1)*nc] <- neighbours' rows of x_own (nc values per row)
+void halo_exchange(Ctx &c, Halo &H, int nc, const double *x_own, double *ghost);
+
 // One AMG level (setup products in CSR, apply operators in SELL).
 struct Level {
     int n = 0, nc = 1, coarsest = 0, nagg = 0;
-    Csr A;                        // level operator
+    // distribution: a level is either DISTRIBUTED (rows split over ranks like the fine
+    // grid, halos with the neighbours) or REPLICATED (every rank holds all rows)
+    bool dist = false;
+    int64_t nglob = 0, row_off = 0;    // global rows and this rank's first row (dist)
+    int64_t coarse_off = 0;            // first global id of this rank's aggregates
+    bool next_dist = false;            // is level+1 distributed?
+    bool warpA = false, warpR = false; // warp-per-row kernels (chosen from GLOBAL row lengths: same on every rank)
+    Halo halo;                         // of A's columns (dist, coarse levels)
+    Halo *hp = nullptr;                // plan in use: &halo, or the fine-grid plan on level 0
+    DBuf<double> dinv_gh;              // ghost copy of dinv (dist)
+    DBuf<double> gh_b, gh_x;           // ghost buffers for b and x (dist)
+    std::vector<int64_t> rep_counts, rep_offs;  // next level replicated: rows per rank (allgather)
+    DBuf<double> rep_buf;              // padded allgather buffer
+    Csr A;                        // level operator (local column ids if dist)
     DBuf<int32_t> zb;             // z-block per row
     DBuf<double> dl1;             // l1 row norms [n][nc]
     DBuf<double> dinv;            // 1 / dl1
@@ -113,8 +170,23 @@ struct Prof {
 
 // ------------------------------------------------------------------ the handle
 struct Ctx {
+    // Nn, Nc, n and nz are this rank's LOCAL (owned) sizes; *_glob the global ones
     int nx, ny, nz, Nn, Nc;
     int64_t n;
+    int nz_glob = 0;
+    int64_t Nn_glob = 0, Nc_glob = 0, n_glob = 0;
+    int rank = 0, nranks = 1;
+    Comm *comm = nullptr;
+    int k0 = 0, k1 = 0;                // owned cell planes [k0, k1)
+    int64_t node_off = 0, cell_off = 0;
+    Halo hu, hf;                       // fine node / cell halos
+    DBuf<int32_t> ff_gcol;             // A_ff global column ids (ILU fill geometry)
+    DBuf<double> gh_u, gh_f, gh_f2, gh_dss;   // fine ghost buffers
+    // deterministic reductions: fixed chunks of the global vector (DESIGN.md R-reduce)
+    int nchunk_loc = 0, nchunk_glob = 0, nchunk_max = 0;
+    DBuf<int64_t> chunk_beg;           // local start of each local chunk (+ end sentinel)
+    std::vector<int64_t> chunk_gidx;   // global index of each local chunk
+    DBuf<int32_t> chunk_perm;          // allgathered [rank][local] slot -> global chunk position
     cudaStream_t s;
     tsp_options o;
     int sm_count = 148;
@@ -163,10 +235,14 @@ void prec_apply(Ctx &c, const double *v, double *z);
 // setup (setup_flow.cu, amg_setup.cu, ilu.cu)
 void setup_mech(Ctx &c);
 void setup_flow(Ctx &c);
-void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc);
+void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_halo, int64_t row_off0, int64_t nglob0);
 void amg_vcycle(Ctx &c, Hier &H, const double *b, double *x, bool mech);
 void ilu_setup(Ctx &c, const double *sff_vals);
 void ilu_apply_fused(Ctx &c, const double *yf, const double *zs, const double *zp, double *zf_out);
+
+// partition of the z-slab decomposition (include/tsp.h)
+void partition(int nx, int ny, int nz, int zblock, int rank, int nranks, int64_t out6[6]);
+void reduce_setup(Ctx &c);
 
 // Krylov (krylov.cu)
 void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, tsp_solve_info &info);

@@ -28,7 +28,7 @@ STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "INVALID_ARG", -2: "DIM_MISMATCH", -3
 class tsp_options(C.Structure):
     _fields_ = [("amg_theta", C.c_double), ("amg_coarse_max", C.c_int), ("amg_max_levels", C.c_int),
                 ("zblock", C.c_int), ("tile_x", C.c_int), ("tile_y", C.c_int), ("tile_z", C.c_int),
-                ("reserved", C.c_int * 8)]
+                ("replicate_rows", C.c_int), ("reserved", C.c_int * 7)]
 
 
 class tsp_bsr(C.Structure):
@@ -37,6 +37,7 @@ class tsp_bsr(C.Structure):
 
 class tsp_desc(C.Structure):
     _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("rank", C.c_int), ("nranks", C.c_int),
+                ("comm_kind", C.c_int), ("comm_arg", C.c_void_p),
                 ("stream", C.c_void_p), ("inputs_on_device", C.c_int),
                 ("A_uu", tsp_bsr), ("A_uf", tsp_bsr), ("A_fu", tsp_bsr), ("A_ff", tsp_bsr),
                 ("fs_diag", C.c_void_p), ("opts", tsp_options)]
@@ -92,6 +93,13 @@ def lib():
         L.tsp_prof_read.argtypes = [C.c_void_p, _P(tsp_prof)]
         L.tsp_destroy.argtypes = [C.c_void_p]
         L.tsp_destroy.restype = None
+        L.tsp_nccl_unique_id.argtypes = [C.c_char_p]
+        L.tsp_local_world_create.argtypes = [C.c_int]
+        L.tsp_local_world_create.restype = C.c_void_p
+        L.tsp_local_world_destroy.argtypes = [C.c_void_p]
+        L.tsp_local_world_destroy.restype = None
+        L.tsp_partition.argtypes = [C.c_int] * 6 + [_P(C.c_int64)]
+        L.tsp_level_dist.argtypes = [C.c_void_p, C.c_int, C.c_int, _P(C.c_int64)]
         if L.tsp_abi_version() != 1:
             raise RuntimeError("libtsp ABI version mismatch")
         _LIB = L
@@ -101,7 +109,38 @@ def lib():
 EXPORTED = ["tsp_abi_version", "tsp_last_error", "tsp_default_options", "tsp_create", "tsp_setup",
             "tsp_apply_preconditioner", "tsp_apply_operator", "tsp_solve", "tsp_default_solve_opts",
             "tsp_get_stats", "tsp_level_sizes", "tsp_export_level", "tsp_prof_enable", "tsp_prof_read",
-            "tsp_destroy"]
+            "tsp_destroy", "tsp_nccl_unique_id", "tsp_local_world_create", "tsp_local_world_destroy",
+            "tsp_partition", "tsp_level_dist"]
+
+TSP_COMM_NONE, TSP_COMM_NCCL, TSP_COMM_LOCAL = 0, 1, 2
+
+
+def partition(nx, ny, nz, zblock, rank, nranks):
+    """Owned ranges of a rank (include/tsp.h): k0, k1, first node, nodes, first cell, cells."""
+    out = (C.c_int64 * 6)()
+    _check(lib().tsp_partition(nx, ny, nz, zblock, rank, nranks, out), "tsp_partition")
+    return tuple(out)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().tsp_nccl_unique_id(buf), "tsp_nccl_unique_id")
+    return buf.raw
+
+
+class LocalWorld:
+    """Test backend: `n` ranks inside this process (one host thread per rank)."""
+
+    def __init__(self, n):
+        self.n = n
+        self.h = lib().tsp_local_world_create(n)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().tsp_local_world_destroy(self.h)
+            self.h = None
+
+    __del__ = close
 
 
 class TspError(RuntimeError):
@@ -140,7 +179,7 @@ class Tsp:
     """One handle.  `arrays` is a synth.Problem (numpy, host) -- or any object
     with the same attribute names holding CUDA torch tensors (device=True)."""
 
-    def __init__(self, pb, stream=None, device_inputs=False, **opts):
+    def __init__(self, pb, stream=None, device_inputs=False, rank=0, nranks=1, comm_kind=0, comm_arg=None, **opts):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("libtsp needs a CUDA device (no CPU fallback)")
@@ -160,7 +199,13 @@ class Tsp:
             return _ptr(y)
 
         d = tsp_desc()
-        d.nx, d.ny, d.nz, d.rank, d.nranks = pb.nx, pb.ny, pb.nz, 0, 1
+        d.nx, d.ny, d.nz, d.rank, d.nranks = pb.nx, pb.ny, pb.nz, rank, nranks
+        d.comm_kind = comm_kind
+        if isinstance(comm_arg, (bytes, bytearray)):
+            self._uid = C.create_string_buffer(bytes(comm_arg), 128)
+            d.comm_arg = C.cast(self._uid, C.c_void_p)
+        else:
+            d.comm_arg = comm_arg
         d.stream = C.c_void_p(self.stream.cuda_stream)
         d.inputs_on_device = int(device_inputs)
         for name in ("uu", "uf", "fu", "ff"):
@@ -229,6 +274,11 @@ class Tsp:
 
     def hierarchy(self, which):
         return [self.level(which, l) for l in range(self.num_levels(which))]
+
+    def level_dist(self, which, lvl):
+        o = (C.c_int64 * 3)()
+        _check(lib().tsp_level_dist(self.h, which, lvl, o), "tsp_level_dist")
+        return dict(dist=bool(o[0]), nglob=o[1], row_off=o[2])
 
     def prof_enable(self, on=True):
         _check(lib().tsp_prof_enable(self.h, int(on)), "tsp_prof_enable")

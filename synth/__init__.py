@@ -171,3 +171,66 @@ def to_scipy(pb: Problem):
     A_fu = sp.bsr_matrix((pb.fu_val, pb.fu_col, pb.fu_rowptr), shape=(2 * pb.Nc, 3 * pb.Nn))
     A_ff = sp.bsr_matrix((pb.ff_val, pb.ff_col, pb.ff_rowptr), shape=(2 * pb.Nc, 2 * pb.Nc))
     return sp.bmat([[A_uu, A_uf], [A_fu, A_ff]]).tocsr(), (A_uu, A_uf, A_fu, A_ff)
+
+
+def slab_partition(nx, ny, nz, zblock, rank, nranks):
+    """The z-slab partition of include/tsp.h (rank r owns z-blocks
+    [floor(r nzb / P), floor((r+1) nzb / P))): returns (k0, k1, node0, nnodes,
+    cell0, ncells).  tests/test_multirank_cpu.py pins it against tsp_partition."""
+    nzb = (nz + zblock - 1) // zblock
+    zlo, zhi = rank * nzb // nranks, (rank + 1) * nzb // nranks
+    k0, k1 = zlo * zblock, min(zhi * zblock, nz)
+    NP, CP = (nx + 1) * (ny + 1), nx * ny
+    last = int(rank == nranks - 1)
+    return k0, k1, k0 * NP, (k1 - k0 + last) * NP, k0 * CP, (k1 - k0) * CP
+
+
+@dataclass
+class LocalProblem:
+    """The rows one rank owns (GLOBAL column ids) -- what a rank passes to tsp_create."""
+    nx: int
+    ny: int
+    nz: int
+    rank: int
+    nranks: int
+    node0: int
+    cell0: int
+    uu_rowptr: np.ndarray
+    uu_col: np.ndarray
+    uu_val: np.ndarray
+    uf_rowptr: np.ndarray
+    uf_col: np.ndarray
+    uf_val: np.ndarray
+    fu_rowptr: np.ndarray
+    fu_col: np.ndarray
+    fu_val: np.ndarray
+    ff_rowptr: np.ndarray
+    ff_col: np.ndarray
+    ff_val: np.ndarray
+    fs: np.ndarray
+    Nn: int
+    Nc: int
+
+    @property
+    def n(self):
+        return 3 * self.Nn + 2 * self.Nc
+
+    def local(self, v, nn_glob):
+        """This rank's part [u_own | f_own] of a global vector [u | f]."""
+        return np.concatenate([v[3 * self.node0:3 * (self.node0 + self.Nn)],
+                               v[3 * nn_glob + 2 * self.cell0:3 * nn_glob + 2 * (self.cell0 + self.Nc)]])
+
+
+def _rows(rp, ci, v, r0, nr):
+    a, b = rp[r0], rp[r0 + nr]
+    return (rp[r0:r0 + nr + 1] - a).astype(np.int32), np.ascontiguousarray(ci[a:b]), np.ascontiguousarray(v[a:b])
+
+
+def local_problem(pb: Problem, rank: int, nranks: int, zblock: int = 16) -> LocalProblem:
+    k0, k1, n0, nn, c0, ncl = slab_partition(pb.nx, pb.ny, pb.nz, zblock, rank, nranks)
+    d = {}
+    for name, r0, nr in (("uu", n0, nn), ("uf", n0, nn), ("fu", c0, ncl), ("ff", c0, ncl)):
+        rp, ci, v = _rows(getattr(pb, name + "_rowptr"), getattr(pb, name + "_col"), getattr(pb, name + "_val"), r0, nr)
+        d[name + "_rowptr"], d[name + "_col"], d[name + "_val"] = rp, ci, v
+    return LocalProblem(nx=pb.nx, ny=pb.ny, nz=pb.nz, rank=rank, nranks=nranks, node0=n0, cell0=c0,
+                        fs=np.ascontiguousarray(pb.fs[c0:c0 + ncl]), Nn=nn, Nc=ncl, **d)
