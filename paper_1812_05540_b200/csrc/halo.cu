@@ -129,80 +129,59 @@ void halo_exchange(Ctx &c, Halo &H, int nc, const double *x_own, double *ghost)
                               b * H.nsend[1], ghost + (size_t)H.nrecv[0] * nc, b * H.nrecv[1], c.s);
 }
 
-// ------------------------------------------------------------------ reduction chunks (R-reduce)
-// The global vector [u | f] is cut into segments per z-block (u rows of its node
-// planes, f rows of its cell planes) and every segment into chunks of CH values from
-// its start.  A rank owns whole z-blocks, hence whole chunks; chunk partials are
-// reduced by a fixed tree and summed over all chunks in global order.
-constexpr int64_t CH = 32768;
+// ------------------------------------------------------------------ reduction layout (R-reduce)
+// The global vector [u | f] is cut into SEGMENTS: the u rows of each z-block's node
+// planes, then the f rows of each z-block's cell planes (global order: u of z-block
+// 0..nzb-1, then f of z-block 0..nzb-1).  A rank owns whole z-blocks, hence whole
+// segments.  Each segment is cut into chunks of CH values from its start (one CTA
+// each, fixed tree), the chunks of a segment are summed by a fixed tree, and the
+// segment sums of all ranks are added in global segment order: the result does not
+// depend on the number of ranks.
+constexpr int64_t CH = 2048;
 
 void reduce_setup(Ctx &c)
 {
     const int zb = c.o.zblock, nzb = (c.nz_glob + zb - 1) / zb;
     const int64_t NP = (int64_t)(c.nx + 1) * (c.ny + 1), CP = (int64_t)c.nx * c.ny;
-    std::vector<int64_t> gstart_u, gstart_f;   // global chunk index where each z-block's segments start
-    int64_t g = 0;
-    struct Seg { int64_t len; int64_t gfirst; };
-    std::vector<Seg> useg(nzb), fseg(nzb);
-    for (int b = 0; b < nzb; ++b) {
-        const int p0 = b * zb, p1 = std::min((b + 1) * zb, c.nz_glob) + (b == nzb - 1 ? 1 : 0);
-        useg[b].len = 3 * NP * (p1 - p0);
-        useg[b].gfirst = g;
-        g += (useg[b].len + CH - 1) / CH;
-    }
-    for (int b = 0; b < nzb; ++b) {
-        const int p0 = b * zb, p1 = std::min((b + 1) * zb, c.nz_glob);
-        fseg[b].len = 2 * CP * (p1 - p0);
-        fseg[b].gfirst = g;
-        g += (fseg[b].len + CH - 1) / CH;
-    }
-    c.nchunk_glob = (int)g;
+    auto ulen = [&](int b) { const int p0 = b * zb, p1 = std::min((b + 1) * zb, c.nz_glob) + (b == nzb - 1 ? 1 : 0); return 3 * NP * (p1 - p0); };
+    auto flen = [&](int b) { const int p0 = b * zb, p1 = std::min((b + 1) * zb, c.nz_glob); return 2 * CP * (p1 - p0); };
     const int zlo = c.k0 / zb, zhi = (c.k1 + zb - 1) / zb;
-    std::vector<int64_t> beg;
-    c.chunk_gidx.clear();
+    std::vector<int64_t> be;            // [beg, end) per local chunk
+    std::vector<int32_t> segc(1, 0);    // first chunk of each local segment
+    std::vector<int64_t> gseg;          // global index of each local segment
     int64_t off = 0;
-    for (int b = zlo; b < zhi; ++b)
-        for (int64_t k = 0; k * CH < useg[b].len; ++k) { beg.push_back(off + k * CH); c.chunk_gidx.push_back(useg[b].gfirst + k); }
-    for (int b = zlo; b < zhi; ++b) off += useg[b].len;
-    TSP_REQUIRE(off == 3 * (int64_t)c.Nn, TSP_ERR_INVALID_ARG, "reduction segments do not cover the owned u rows");
-    for (int b = zlo; b < zhi; ++b) {
-        for (int64_t k = 0; k * CH < fseg[b].len; ++k) { beg.push_back(off + k * CH); c.chunk_gidx.push_back(fseg[b].gfirst + k); }
-        off += fseg[b].len;
-    }
+    for (int part = 0; part < 2; ++part)
+        for (int b = zlo; b < zhi; ++b) {
+            const int64_t len = part == 0 ? ulen(b) : flen(b);
+            for (int64_t k = 0; k * CH < len; ++k) { be.push_back(off + k * CH); be.push_back(off + std::min((k + 1) * CH, len)); }
+            off += len;
+            segc.push_back((int32_t)(be.size() / 2));
+            gseg.push_back(part == 0 ? b : nzb + b);
+        }
     TSP_REQUIRE(off == c.n, TSP_ERR_INVALID_ARG, "reduction segments do not cover the owned rows");
-    // chunk ends: next chunk start, but never across a segment end
-    std::vector<int64_t> be;   // [beg, end) pairs
-    {
-        int64_t o2 = 0;
-        for (int b = zlo; b < zhi; ++b) {
-            for (int64_t k = 0; k * CH < useg[b].len; ++k) { be.push_back(o2 + k * CH); be.push_back(o2 + std::min((k + 1) * CH, useg[b].len)); }
-            o2 += useg[b].len;
-        }
-        for (int b = zlo; b < zhi; ++b) {
-            for (int64_t k = 0; k * CH < fseg[b].len; ++k) { be.push_back(o2 + k * CH); be.push_back(o2 + std::min((k + 1) * CH, fseg[b].len)); }
-            o2 += fseg[b].len;
-        }
-    }
-    c.nchunk_loc = (int)c.chunk_gidx.size();
-    c.chunk_beg.alloc(be.size());
-    TSP_CUDA(cudaMemcpyAsync(c.chunk_beg, be.data(), sizeof(int64_t) * be.size(), cudaMemcpyHostToDevice, c.s));
-    // slot of every global chunk in the allgathered [rank][nchunk_max] layout
-    std::vector<int64_t> cnt = host_allgather<int64_t>(c, std::vector<int64_t>{(int64_t)c.nchunk_loc});
+    c.nchunk_loc = (int)(be.size() / 2);
+    c.nseg_loc = (int)gseg.size();
+    c.nseg_glob = 2 * nzb;
+    c.chunk_beg.alloc(std::max<size_t>(be.size(), 2));
+    if (!be.empty()) TSP_CUDA(cudaMemcpyAsync(c.chunk_beg, be.data(), sizeof(int64_t) * be.size(), cudaMemcpyHostToDevice, c.s));
+    c.seg_chunk.alloc(segc.size());
+    TSP_CUDA(cudaMemcpyAsync(c.seg_chunk, segc.data(), sizeof(int32_t) * segc.size(), cudaMemcpyHostToDevice, c.s));
+    std::vector<int64_t> cnt = host_allgather<int64_t>(c, std::vector<int64_t>{(int64_t)c.nseg_loc});
     int64_t mx = 0;
     for (auto v : cnt) mx = std::max(mx, v);
-    c.nchunk_max = (int)mx;
-    std::vector<int64_t> mine(c.nchunk_max, -1);
-    for (int k = 0; k < c.nchunk_loc; ++k) mine[k] = c.chunk_gidx[k];
+    c.nseg_max = (int)mx;
+    std::vector<int64_t> mine(c.nseg_max, -1);
+    for (int k = 0; k < c.nseg_loc; ++k) mine[k] = gseg[k];
     std::vector<int64_t> all = host_allgather<int64_t>(c, mine);
-    std::vector<int32_t> perm(c.nchunk_glob, -1);
+    std::vector<int32_t> perm(c.nseg_glob, -1);
     for (int r = 0; r < (c.comm ? c.nranks : 1); ++r)
-        for (int k = 0; k < c.nchunk_max; ++k) {
-            const int64_t gi = all[(size_t)r * c.nchunk_max + k];
-            if (gi >= 0) perm[gi] = r * c.nchunk_max + k;
+        for (int k = 0; k < c.nseg_max; ++k) {
+            const int64_t g = all[(size_t)r * c.nseg_max + k];
+            if (g >= 0) perm[g] = r * c.nseg_max + k;
         }
-    for (auto p : perm) TSP_REQUIRE(p >= 0, TSP_ERR_INVALID_ARG, "reduction chunks not covered by the ranks");
-    c.chunk_perm.alloc(perm.size());
-    TSP_CUDA(cudaMemcpyAsync(c.chunk_perm, perm.data(), sizeof(int32_t) * perm.size(), cudaMemcpyHostToDevice, c.s));
+    for (auto p : perm) TSP_REQUIRE(p >= 0, TSP_ERR_INVALID_ARG, "reduction segments not covered by the ranks");
+    c.seg_perm.alloc(perm.size());
+    TSP_CUDA(cudaMemcpyAsync(c.seg_perm, perm.data(), sizeof(int32_t) * perm.size(), cudaMemcpyHostToDevice, c.s));
     TSP_CUDA(cudaStreamSynchronize(c.s));
 }
 

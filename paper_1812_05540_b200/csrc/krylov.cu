@@ -119,17 +119,30 @@ __global__ void __launch_bounds__(KB) k_maxpy_norm(int nv, const double *__restr
     if (threadIdx.x == 0) part[k] = s;
 }
 
-// out[t] = (sqrt of) sum over the global chunks, in global order, of the allgathered partials
-// part_all layout: [rank][nv][cmax]; perm[g] = rank * cmax + local chunk
-__global__ void k_final(int nv, const double *__restrict__ part_all, int cmax, const int32_t *__restrict__ perm, int nglob,
+// per-segment sums of the chunk partials, fixed tree: segp[t*smax + s] = sum_{k in seg s} part[t*cmax + k]
+__global__ void __launch_bounds__(KB) k_seg_reduce(const double *__restrict__ part, int cmax, const int32_t *__restrict__ segc,
+                                                   double *__restrict__ segp, int smax)
+{
+    const int sg = blockIdx.x, t = blockIdx.y;
+    const int k0 = segc[sg], k1 = segc[sg + 1];
+    double x = 0.0;
+    for (int k = k0 + threadIdx.x; k < k1; k += KB) x += part[(int64_t)t * cmax + k];
+    __shared__ double red[KB / 32];
+    const double s = block_sum(x, red);
+    if (threadIdx.x == 0) segp[(int64_t)t * smax + sg] = s;
+}
+
+// out[t] = (sqrt of) the sum over the global segments, in global order, of the allgathered
+// segment sums; seg_all layout [rank][nv][smax], perm[g] = rank * smax + local segment
+__global__ void k_final(int nv, const double *__restrict__ seg_all, int smax, const int32_t *__restrict__ perm, int nglob,
                         double *__restrict__ out, int mode)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nv) return;
     double s = 0.0;
     for (int g = 0; g < nglob; ++g) {
-        const int slot = perm[g], r = slot / cmax, k = slot - r * cmax;
-        s += part_all[((int64_t)r * nv + t) * cmax + k];
+        const int slot = perm[g], r = slot / smax, k = slot - r * smax;
+        s += seg_all[((int64_t)r * nv + t) * smax + k];
     }
     if (mode == 0) out[t] = s;
     else out[t] = sqrt(s);
@@ -169,24 +182,28 @@ struct Kr {
     Kr(Ctx &c_, int maxv) : c(c_), n(c_.n)
     {
         nblk = (int)std::max<int64_t>(1, std::min<int64_t>((n + KB - 1) / KB, (int64_t)c.sm_count * 4));
-        pall.alloc((size_t)std::max(c.nranks, 1) * maxv * std::max(c.nchunk_max, 1) + 16);
+        pall.alloc((size_t)std::max(c.nranks, 1) * maxv * std::max(c.nseg_max, 1) + 16);
     }
-    // reduce the local partials `part` ([nv][cmax]) to out[nv]
+    // chunk partials `kpart` ([nv][nchunk_loc]) -> segment sums -> (allgather) -> out[nv]
     void finish(int nv, double *out, int mode)
     {
-        const double *src = c.kpart;
+        if (c.nseg_loc) {
+            dim3 g(c.nseg_loc, nv);
+            k_seg_reduce<<<g, KB, 0, c.s>>>(c.kpart, c.nchunk_loc, c.seg_chunk, c.seg_part, c.nseg_max);
+        }
+        const double *src = c.seg_part;
         if (c.comm) {
-            c.comm->allgather(c.kpart.p, pall.p, sizeof(double) * nv * c.nchunk_max, c.s);
+            c.comm->allgather(c.seg_part.p, pall.p, sizeof(double) * nv * c.nseg_max, c.s);
             src = pall;
         }
-        k_final<<<(nv + 63) / 64, 64, 0, c.s>>>(nv, src, c.nchunk_max, c.chunk_perm, c.nchunk_glob, out, mode);
-        c.launches++;
+        k_final<<<(nv + 63) / 64, 64, 0, c.s>>>(nv, src, c.nseg_max, c.seg_perm, c.nseg_glob, out, mode);
+        c.launches += 2;
     }
     void mdot(const double *V, int nv, const double *w, double *h)
     {
         prof_begin(c, PK_DOT);
         dim3 g(c.nchunk_loc, (nv + KG - 1) / KG);
-        k_mdot<<<g, KB, 0, c.s>>>(nv, V, n, w, c.chunk_beg, c.kpart, c.nchunk_max);
+        k_mdot<<<g, KB, 0, c.s>>>(nv, V, n, w, c.chunk_beg, c.kpart, c.nchunk_loc);
         finish(nv, h, 0);
         prof_end(c, PK_DOT, 8.0 * n * (nv + (nv + KG - 1) / KG));
         c.launches++;
@@ -194,7 +211,7 @@ struct Kr {
     void maxpy_mdot(const double *V, int nv, const double *h1, double *w, double *h2)
     {
         prof_begin(c, PK_AXPY);
-        k_maxpy_mdot<<<c.nchunk_loc, KB, 0, c.s>>>(nv, V, n, h1, w, c.chunk_beg, c.kpart, c.nchunk_max);
+        k_maxpy_mdot<<<c.nchunk_loc, KB, 0, c.s>>>(nv, V, n, h1, w, c.chunk_beg, c.kpart, c.nchunk_loc);
         finish(nv, h2, 0);
         prof_end(c, PK_AXPY, 8.0 * n * (nv + 2));
         c.launches++;
@@ -211,7 +228,7 @@ struct Kr {
     {
         prof_begin(c, PK_NORM);
         dim3 g(c.nchunk_loc, 1);
-        k_mdot<<<g, KB, 0, c.s>>>(1, w, n, w, c.chunk_beg, c.kpart, c.nchunk_max);
+        k_mdot<<<g, KB, 0, c.s>>>(1, w, n, w, c.chunk_beg, c.kpart, c.nchunk_loc);
         finish(1, nrm, 2);
         prof_end(c, PK_NORM, 8.0 * n);
         c.launches++;
@@ -234,7 +251,8 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
         c.Z.alloc((size_t)m * n);
         c.kr.alloc(std::max<int64_t>(n, 1));
         c.kh.alloc(4 * (m + 2));
-        c.kpart.alloc((size_t)(m + 2) * std::max(c.nchunk_max, 1) + 64);
+        c.kpart.alloc((size_t)(m + 2) * std::max(c.nchunk_loc, 1) + 64);
+        c.seg_part.alloc((size_t)(m + 2) * std::max(c.nseg_max, 1) + 64);
         c.kcap = m;
     }
     Kr K(c, m + 2);

@@ -182,11 +182,15 @@ struct Ctx {
     Halo hu, hf;                       // fine node / cell halos
     DBuf<int32_t> ff_gcol;             // A_ff global column ids (ILU fill geometry)
     DBuf<double> gh_u, gh_f, gh_f2, gh_dss;   // fine ghost buffers
-    // deterministic reductions: fixed chunks of the global vector (DESIGN.md R-reduce)
-    int nchunk_loc = 0, nchunk_glob = 0, nchunk_max = 0;
-    DBuf<int64_t> chunk_beg;           // local start of each local chunk (+ end sentinel)
-    std::vector<int64_t> chunk_gidx;   // global index of each local chunk
-    DBuf<int32_t> chunk_perm;          // allgathered [rank][local] slot -> global chunk position
+    // deterministic reductions (DESIGN.md R-reduce): the global vector is cut into
+    // segments (u and f rows of each z-block) and each segment into fixed chunks;
+    // chunk partials -> per-segment fixed-tree sums -> allgather -> sum in global order
+    int nchunk_loc = 0;
+    DBuf<int64_t> chunk_beg;           // [beg, end) of each local chunk (local offsets)
+    int nseg_loc = 0, nseg_max = 0, nseg_glob = 0;
+    DBuf<int32_t> seg_chunk;           // first local chunk of each local segment (+ end)
+    DBuf<int32_t> seg_perm;            // global segment g -> slot (rank * nseg_max + local segment)
+    DBuf<double> seg_part;             // [nv][nseg_max] per-rank segment sums
     cudaStream_t s;
     tsp_options o;
     int sm_count = 148;
