@@ -246,7 +246,9 @@ def main():
         k = i["iterations"]
         jsum += sum((j % m) for j in range(k))
     mean_j = jsum / max(iters, 1)
-    bytes_iter = st["bytes_iter_base"] + st["bytes_per_krylov_vec"] * (mean_j + 1)
+    reorth_frac = sum(i.get("reorth", 0) for i in infos) / max(iters, 1)
+    # CGS2: three passes over the j+1 basis vectors (projection, fused update+projection, update+norm)
+    bytes_iter = st["bytes_iter_base"] + st["bytes_per_krylov_vec"] * (mean_j + 1) * (2 + reorth_frac)
     iter_gbs = bytes_iter * iters / (solve_ms * 1e-3) / 1e9
     kernel_table = {k: dict(launches=v["launches"], ms=round(v["ms"], 4), gbs=round(v["bytes"] / max(v["ms"], 1e-12) / 1e6, 1),
                             share=round(v["ms"] / sum(p["ms"] for p in prof.values()), 4)) for k, v in prof.items()}
@@ -321,7 +323,8 @@ def main():
                            "setup_ms_per_step": (ms_max - solve_ms) / args.steps,
                            "apply_gdof_per_s": None},
             "iteration_roofline": {"bytes_per_iter": bytes_iter, "achieved_gbs": iter_gbs, "peak_gbs": hbm,
-                                   "frac": iter_gbs / hbm, "mean_krylov_index": mean_j},
+                                   "frac": iter_gbs / hbm, "mean_krylov_index": mean_j,
+                                   "reorth_fraction": reorth_frac},
             "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
                          "bytes_per_launch": d["bytes"] / d["launches"], "ms_per_launch": d["ms"] / d["launches"]},

@@ -121,6 +121,7 @@ typedef struct {
     double est_relres;           /* Arnoldi estimate |g_{j+1}| / ||b|| */
     double true_relres;          /* recomputed ||b - A x|| / ||b|| at exit */
     double t_solve_s;
+    int reorth;                  /* iterations that needed the second Gram-Schmidt pass */
 } tsp_solve_info;
 
 typedef struct {
@@ -131,7 +132,7 @@ typedef struct {
     double bytes_apply;          /* algorithmic bytes of one tsp_apply_preconditioner */
     double bytes_operator;       /* algorithmic bytes of one tsp_apply_operator */
     double bytes_iter_base;      /* per FGMRES iteration excluding the Krylov-index-dependent part */
-    double bytes_per_krylov_vec; /* CGS2 bytes added per basis vector (x (j+1)) */
+    double bytes_per_krylov_vec; /* Gram-Schmidt bytes per basis vector and pass (x (j+1) x passes) */
 } tsp_stats;
 
 /* per-kernel-class timing (CUDA events on the handle's stream), for roofline */

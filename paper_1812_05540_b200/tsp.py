@@ -50,7 +50,8 @@ class tsp_solve_opts(C.Structure):
 
 class tsp_solve_info(C.Structure):
     _fields_ = [("iterations", C.c_int), ("restarts", C.c_int), ("status", C.c_int),
-                ("est_relres", C.c_double), ("true_relres", C.c_double), ("t_solve_s", C.c_double)]
+                ("est_relres", C.c_double), ("true_relres", C.c_double), ("t_solve_s", C.c_double),
+                ("reorth", C.c_int)]
 
 
 class tsp_stats(C.Structure):
@@ -244,7 +245,8 @@ class Tsp:
         rc = lib().tsp_solve(self.h, _ptr(b), _ptr(x), C.byref(o), C.byref(info))
         _check(rc, "tsp_solve", ok=(0, 1))
         return dict(iterations=info.iterations, restarts=info.restarts, status=STATUS.get(info.status, info.status),
-                    est_relres=info.est_relres, true_relres=info.true_relres, t_solve_s=info.t_solve_s)
+                    est_relres=info.est_relres, true_relres=info.true_relres, t_solve_s=info.t_solve_s,
+                    reorth=info.reorth)
 
     def stats(self):
         s = tsp_stats()
