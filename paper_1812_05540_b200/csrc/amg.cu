@@ -868,7 +868,7 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
 
 // ------------------------------------------------------------------ V-cycle kernels (apply; free arithmetic)
 // pre-smooth from zero + residual: x = D^-1 b ; r = b - A D^-1 b   (b, D^-1 ghost-aware)
-template <int NC>
+template <int NC, bool D>
 __global__ void __launch_bounds__(256) k_vc_pre(int n, const int64_t *__restrict__ off, const int32_t *__restrict__ col,
                                                 const double *__restrict__ val, GV dinv, GV b, double *__restrict__ x,
                                                 double *__restrict__ r)
@@ -885,7 +885,7 @@ __global__ void __launch_bounds__(256) k_vc_pre(int n, const int64_t *__restrict
         const int j = __ldcs(col + slot * 32 + lane);
 #pragma unroll
         for (int c = 0; c < NC; ++c)
-            acc[c] = fma(__ldcs(val + (slot * NC + c) * 32 + lane), GVLD(b, j, c, NC) * GVLD(dinv, j, c, NC), acc[c]);
+            acc[c] = fma(__ldcs(val + (slot * NC + c) * 32 + lane), gvld<D>(b, j, c, NC) * gvld<D>(dinv, j, c, NC), acc[c]);
     }
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
@@ -936,7 +936,7 @@ __global__ void __launch_bounds__(256) k_prolong(int n, const int64_t *__restric
     for (int c = 0; c < NC; ++c) x[(int64_t)i * NC + c] = acc[c];
 }
 // post-smooth: xo = x + D^-1 (b - A x)   (x ghost-aware)
-template <int NC>
+template <int NC, bool D>
 __global__ void __launch_bounds__(256) k_vc_post(int n, const int64_t *__restrict__ off, const int32_t *__restrict__ col,
                                                  const double *__restrict__ val, const double *__restrict__ dinv,
                                                  const double *__restrict__ b, GV x, double *__restrict__ xo)
@@ -952,7 +952,7 @@ __global__ void __launch_bounds__(256) k_vc_post(int n, const int64_t *__restric
     for (int64_t slot = b0; slot < b1; ++slot) {
         const int j = __ldcs(col + slot * 32 + lane);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) acc[c] = fma(__ldcs(val + (slot * NC + c) * 32 + lane), GVLD(x, j, c, NC), acc[c]);
+        for (int c = 0; c < NC; ++c) acc[c] = fma(__ldcs(val + (slot * NC + c) * 32 + lane), gvld<D>(x, j, c, NC), acc[c]);
     }
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
@@ -976,7 +976,7 @@ __global__ void k_coarse(int n, const double *__restrict__ inv, const double *__
 // ---- warp-per-row CSR variants for operators with long rows (coarse levels,
 // restriction): lanes stride a row's entries (coalesced [q][c] values), shuffle reduce.
 // MODE 0: y = A x ; MODE 1: pre (x = D^-1 b, r = b - A D^-1 b) ; MODE 2: post (xo = x + D^-1 (b - A x))
-template <int NC, int MODE>
+template <int NC, int MODE, bool D>
 __global__ void __launch_bounds__(256) k_csr_warp(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
                                                   const double *__restrict__ v, GV dinv, GV b, GV x,
                                                   double *__restrict__ out1, double *__restrict__ out2)
@@ -992,7 +992,7 @@ __global__ void __launch_bounds__(256) k_csr_warp(int n, const int32_t *__restri
         const int j = ci[q];
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-            const double xv = MODE == 1 ? GVLD(b, j, c, NC) * GVLD(dinv, j, c, NC) : GVLD(x, j, c, NC);
+            const double xv = MODE == 1 ? gvld<D>(b, j, c, NC) * gvld<D>(dinv, j, c, NC) : gvld<D>(x, j, c, NC);
             acc[c] = fma(__ldcs(v + q * NC + c), xv, acc[c]);
         }
     }
@@ -1044,8 +1044,10 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     if (L.dist) halo_exchange(c, *L.hp, NC, b, L.gh_b);
     const GV gb = gv(b, n, L.dist ? L.gh_b.p : nullptr), gd = gv(L.dinv, n, ghd);
     prof_begin(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P);
-    if (wA) k_csr_warp<NC, 1><<<grid_for(n, 8), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, L.A.v, gd, gb, gv(nullptr, 0), L.x2, L.r);
-    else if (n) k_vc_pre<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sA.off, L.sA.col, L.sA.val, gd, gb, L.x2, L.r);
+    if (wA) (L.dist ? k_csr_warp<NC, 1, true> : k_csr_warp<NC, 1, false>)<<<grid_for(n, 8), 256, 0, c.s>>>(
+        n, L.A.rp, L.A.ci, L.A.v, gd, gb, gv(nullptr, 0), L.x2, L.r);
+    else if (n) (L.dist ? k_vc_pre<NC, true> : k_vc_pre<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
+        n, L.sA.off, L.sA.col, L.sA.val, gd, gb, L.x2, L.r);
     prof_end(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P, bA + 4 * vec);
     // restriction (local rows of R); a replicated next level is gathered on every rank
     Level &Lc = H.L[l + 1];
@@ -1053,8 +1055,8 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     const int nr = L.sR.nrows;
     double *rdst = gather ? L.rep_buf.p + (size_t)c.nranks * 0 : Lc.b.p;
     prof_begin(c, mech ? PK_VC_RESTR_U : PK_VC_RESTR_P);
-    if (wR) k_csr_warp<NC, 0><<<grid_for(nr, 8), 256, 0, c.s>>>(nr, L.R.rp, L.R.ci, L.R.v, gv(nullptr, 0), gv(nullptr, 0),
-                                                             gv(L.r, n), rdst, nullptr);
+    if (wR) k_csr_warp<NC, 0, false><<<grid_for(nr, 8), 256, 0, c.s>>>(nr, L.R.rp, L.R.ci, L.R.v, gv(nullptr, 0), gv(nullptr, 0),
+                                                                    gv(L.r, n), rdst, nullptr);
     else if (nr) k_sell_mv<NC><<<grid_for(nr, 256), 256, 0, c.s>>>(nr, L.sR.off, L.sR.col, L.sR.val, L.r, rdst);
     prof_end(c, mech ? PK_VC_RESTR_U : PK_VC_RESTR_P, bR + vec + 8.0 * NC * nr);
     if (gather) {
@@ -1075,8 +1077,10 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     if (L.dist) halo_exchange(c, *L.hp, NC, L.x2, L.gh_x);
     const GV gx = gv(L.x2, n, L.dist ? L.gh_x.p : nullptr);
     prof_begin(c, mech ? PK_VC_POST_U : PK_VC_POST_P);
-    if (wA) k_csr_warp<NC, 2><<<grid_for(n, 8), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, L.A.v, gv(L.dinv, n), gv(b, n), gx, xout, nullptr);
-    else if (n) k_vc_post<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sA.off, L.sA.col, L.sA.val, L.dinv, b, gx, xout);
+    if (wA) (L.dist ? k_csr_warp<NC, 2, true> : k_csr_warp<NC, 2, false>)<<<grid_for(n, 8), 256, 0, c.s>>>(
+        n, L.A.rp, L.A.ci, L.A.v, gv(L.dinv, n), gv(b, n), gx, xout, nullptr);
+    else if (n) (L.dist ? k_vc_post<NC, true> : k_vc_post<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
+        n, L.sA.off, L.sA.col, L.sA.val, L.dinv, b, gx, xout);
     prof_end(c, mech ? PK_VC_POST_U : PK_VC_POST_P, bA + 4 * vec);
     c.launches += 4;
 }

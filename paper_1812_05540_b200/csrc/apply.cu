@@ -11,6 +11,7 @@ namespace tsp {
 
 // ------------------------------------------------------------------ operator, node rows:
 // y_u = A_uu x_u + A_uf x_f
+template <bool D>
 __global__ void __launch_bounds__(256) k_op_node(int Nn, const int64_t *__restrict__ off_uu, const int32_t *__restrict__ col_uu,
                                                  const double *__restrict__ val_uu, const int64_t *__restrict__ off_uf,
                                                  const int32_t *__restrict__ col_uf, const double *__restrict__ val_uf,
@@ -26,7 +27,7 @@ __global__ void __launch_bounds__(256) k_op_node(int Nn, const int64_t *__restri
         for (int64_t slot = b0; slot < b1; ++slot) {
             const int cidx = __ldcs(col_uu + slot * 32 + lane);
             const double *v = val_uu + slot * (9 * 32) + lane;
-            const double x0 = GVLD(xu, cidx, 0, 3), x1 = GVLD(xu, cidx, 1, 3), x2 = GVLD(xu, cidx, 2, 3);
+            const double x0 = gvld<D>(xu, cidx, 0, 3), x1 = gvld<D>(xu, cidx, 1, 3), x2 = gvld<D>(xu, cidx, 2, 3);
             a0 = fma(__ldcs(v + 0 * 32), x0, a0); a0 = fma(__ldcs(v + 1 * 32), x1, a0); a0 = fma(__ldcs(v + 2 * 32), x2, a0);
             a1 = fma(__ldcs(v + 3 * 32), x0, a1); a1 = fma(__ldcs(v + 4 * 32), x1, a1); a1 = fma(__ldcs(v + 5 * 32), x2, a1);
             a2 = fma(__ldcs(v + 6 * 32), x0, a2); a2 = fma(__ldcs(v + 7 * 32), x1, a2); a2 = fma(__ldcs(v + 8 * 32), x2, a2);
@@ -38,7 +39,7 @@ __global__ void __launch_bounds__(256) k_op_node(int Nn, const int64_t *__restri
         for (int64_t slot = b0; slot < b1; ++slot) {
             const int cidx = __ldcs(col_uf + slot * 32 + lane);
             const double *v = val_uf + slot * (6 * 32) + lane;
-            const double x0 = GVLD(xf, cidx, 0, 2), x1 = GVLD(xf, cidx, 1, 2);
+            const double x0 = gvld<D>(xf, cidx, 0, 2), x1 = gvld<D>(xf, cidx, 1, 2);
             a0 = fma(__ldcs(v + 0 * 32), x0, a0); a0 = fma(__ldcs(v + 1 * 32), x1, a0);
             a1 = fma(__ldcs(v + 2 * 32), x0, a1); a1 = fma(__ldcs(v + 3 * 32), x1, a1);
             a2 = fma(__ldcs(v + 4 * 32), x0, a2); a2 = fma(__ldcs(v + 5 * 32), x1, a2);
@@ -48,7 +49,7 @@ __global__ void __launch_bounds__(256) k_op_node(int Nn, const int64_t *__restri
 }
 
 // cell rows: y_f = [vf -] (A_fu x_u [+ A_ff x_f]);  mode 0: operator; mode 1: step 2, y_f = v_f - A_fu z_u
-template <int MODE>
+template <int MODE, bool D>
 __global__ void __launch_bounds__(256) k_op_cell(int Nc, const int64_t *__restrict__ off_fu, const int32_t *__restrict__ col_fu,
                                                  const double *__restrict__ val_fu, const int64_t *__restrict__ off_ff,
                                                  const int32_t *__restrict__ col_ff, const double *__restrict__ val_ff,
@@ -64,7 +65,7 @@ __global__ void __launch_bounds__(256) k_op_cell(int Nc, const int64_t *__restri
         for (int64_t slot = b0; slot < b1; ++slot) {
             const int cidx = __ldcs(col_fu + slot * 32 + lane);
             const double *v = val_fu + slot * (6 * 32) + lane;
-            const double x0 = GVLD(xu, cidx, 0, 3), x1 = GVLD(xu, cidx, 1, 3), x2 = GVLD(xu, cidx, 2, 3);
+            const double x0 = gvld<D>(xu, cidx, 0, 3), x1 = gvld<D>(xu, cidx, 1, 3), x2 = gvld<D>(xu, cidx, 2, 3);
             a0 = fma(__ldcs(v + 0 * 32), x0, a0); a0 = fma(__ldcs(v + 1 * 32), x1, a0); a0 = fma(__ldcs(v + 2 * 32), x2, a0);
             a1 = fma(__ldcs(v + 3 * 32), x0, a1); a1 = fma(__ldcs(v + 4 * 32), x1, a1); a1 = fma(__ldcs(v + 5 * 32), x2, a1);
         }
@@ -75,7 +76,7 @@ __global__ void __launch_bounds__(256) k_op_cell(int Nc, const int64_t *__restri
         for (int64_t slot = b0; slot < b1; ++slot) {
             const int cidx = __ldcs(col_ff + slot * 32 + lane);
             const double *v = val_ff + slot * (4 * 32) + lane;
-            const double x0 = GVLD(xf, cidx, 0, 2), x1 = GVLD(xf, cidx, 1, 2);
+            const double x0 = gvld<D>(xf, cidx, 0, 2), x1 = gvld<D>(xf, cidx, 1, 2);
             a0 = fma(__ldcs(v + 0 * 32), x0, a0); a0 = fma(__ldcs(v + 1 * 32), x1, a0);
             a1 = fma(__ldcs(v + 2 * 32), x0, a1); a1 = fma(__ldcs(v + 3 * 32), x1, a1);
         }
@@ -88,6 +89,7 @@ __global__ void __launch_bounds__(256) k_op_cell(int Nc, const int64_t *__restri
 
 // steps 3-4: z_s = D_ss^-1 y_s ; w_p = y_p - A_ps z_s with the full A_ps;
 // z_s of the neighbours is recomputed from y_s instead of re-read.
+template <bool D>
 __global__ void __launch_bounds__(256) k_step34(int Nc, const int64_t *__restrict__ off, const int32_t *__restrict__ col,
                                                 const double *__restrict__ aps, GV dssinv, GV yf, double *__restrict__ zs,
                                                 double *__restrict__ wp)
@@ -100,7 +102,7 @@ __global__ void __launch_bounds__(256) k_step34(int Nc, const int64_t *__restric
 #pragma unroll 4
     for (int64_t slot = b0; slot < b1; ++slot) {
         const int j = __ldcs(col + slot * 32 + lane);
-        acc = fma(__ldcs(aps + slot * 32 + lane), GVLD(yf, j, 0, 2) * GVLD(dssinv, j, 0, 1), acc);
+        acc = fma(__ldcs(aps + slot * 32 + lane), gvld<D>(yf, j, 0, 2) * gvld<D>(dssinv, j, 0, 1), acc);
     }
     zs[i] = yf.own[2 * (int64_t)i] * dssinv.own[i];
     wp[i] = yf.own[2 * (int64_t)i + 1] - acc;
@@ -116,12 +118,12 @@ void op_apply(Ctx &c, const double *x, double *y)
     halo_exchange(c, c.hf, 2, xf, c.gh_f);
     const GV gu = gv(xu, c.Nn, c.gh_u.p), gf = gv(xf, c.Nc, c.gh_f.p);
     prof_begin(c, PK_OP_NODE);
-    if (c.Nn) k_op_node<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(c.Nn, c.s_uu.off, c.s_uu.col, c.s_uu.val, c.s_uf.off, c.s_uf.col,
-                                                              c.s_uf.val, gu, gf, yu);
+    if (c.Nn) (c.comm ? k_op_node<true> : k_op_node<false>)<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(
+        c.Nn, c.s_uu.off, c.s_uu.col, c.s_uu.val, c.s_uf.off, c.s_uf.col, c.s_uf.val, gu, gf, yu);
     prof_end(c, PK_OP_NODE, sell_bytes(c.s_uu) + sell_bytes(c.s_uf) + 48.0 * c.Nn + 16.0 * c.Nc);
     prof_begin(c, PK_OP_CELL);
-    if (c.Nc) k_op_cell<0><<<grid_for(c.Nc, 256), 256, 0, c.s>>>(c.Nc, c.s_fu.off, c.s_fu.col, c.s_fu.val, c.s_ff.off, c.s_ff.col,
-                                                                 c.s_ff.val, gu, gf, nullptr, yf);
+    if (c.Nc) (c.comm ? k_op_cell<0, true> : k_op_cell<0, false>)<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(
+        c.Nc, c.s_fu.off, c.s_fu.col, c.s_fu.val, c.s_ff.off, c.s_ff.col, c.s_ff.val, gu, gf, nullptr, yf);
     prof_end(c, PK_OP_CELL, sell_bytes(c.s_fu) + sell_bytes(c.s_ff) + 24.0 * c.Nn + 32.0 * c.Nc);
     c.launches += 2;
     TSP_CUDA(cudaGetLastError());
@@ -138,14 +140,14 @@ void prec_apply(Ctx &c, const double *v, double *z)
     // step 2: y_f = v_f - A_fu z_u
     halo_exchange(c, c.hu, 3, zu, c.gh_u);
     prof_begin(c, PK_STEP2);
-    if (c.Nc) k_op_cell<1><<<grid_for(c.Nc, 256), 256, 0, c.s>>>(c.Nc, c.s_fu.off, c.s_fu.col, c.s_fu.val, nullptr, nullptr, nullptr,
-                                                                 gv(zu, c.Nn, c.gh_u.p), gv(nullptr, 0), vf, c.w_yf);
+    if (c.Nc) (c.comm ? k_op_cell<1, true> : k_op_cell<1, false>)<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(
+        c.Nc, c.s_fu.off, c.s_fu.col, c.s_fu.val, nullptr, nullptr, nullptr, gv(zu, c.Nn, c.gh_u.p), gv(nullptr, 0), vf, c.w_yf);
     prof_end(c, PK_STEP2, sell_bytes(c.s_fu) + 24.0 * c.Nn + 32.0 * c.Nc);
     // steps 3-4
     halo_exchange(c, c.hf, 2, c.w_yf, c.gh_f);
     prof_begin(c, PK_STEP34);
-    if (c.Nc) k_step34<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(c.Nc, c.s_aps.off, c.s_aps.col, c.s_aps.val, gv(c.dss_inv, c.Nc, c.gh_dss.p),
-                                                             gv(c.w_yf, c.Nc, c.gh_f.p), c.w_tmp, c.w_wp);
+    if (c.Nc) (c.comm ? k_step34<true> : k_step34<false>)<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(
+        c.Nc, c.s_aps.off, c.s_aps.col, c.s_aps.val, gv(c.dss_inv, c.Nc, c.gh_dss.p), gv(c.w_yf, c.Nc, c.gh_f.p), c.w_tmp, c.w_wp);
     prof_end(c, PK_STEP34, sell_bytes(c.s_aps) + 40.0 * c.Nc);
     // step 5: z_p = M_pp^-1 w_p
     amg_vcycle(c, c.pres, c.w_wp, c.w_zp, false);

@@ -109,6 +109,13 @@ struct GV {
 };
 #define GVLD(g, j, c, nc) ((j) < (g).nown ? __ldg((g).own + (int64_t)(j) * (nc) + (c)) : __ldg((g).gh + (int64_t)((j) - (g).nown) * (nc) + (c)))
 inline GV gv(const double *own, int nown, const double *gh = nullptr) { return GV{own, gh, nown}; }
+// D = false (single rank / replicated level): no ghost test at all
+template <bool D>
+__device__ __forceinline__ double gvld(const GV &g, int64_t j, int c, int nc)
+{
+    if (D) return GVLD(g, j, c, nc);
+    return __ldg(g.own + j * nc + c);
+}
 
 // builds the plan from the GLOBAL column ids of a row-distributed CSR (own rows =
 // global [own_off, own_off + nown)) and rewrites `lcols` with local ids
