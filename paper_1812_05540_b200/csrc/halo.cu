@@ -137,7 +137,7 @@ void halo_exchange(Ctx &c, Halo &H, int nc, const double *x_own, double *ghost)
 // each, fixed tree), the chunks of a segment are summed by a fixed tree, and the
 // segment sums of all ranks are added in global segment order: the result does not
 // depend on the number of ranks.
-constexpr int64_t CH = 2048;
+constexpr int64_t CH = kRedChunk;
 
 void reduce_setup(Ctx &c)
 {

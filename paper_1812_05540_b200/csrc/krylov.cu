@@ -30,78 +30,118 @@ __device__ __forceinline__ double block_sum(double x, double *red)   // fixed tr
     return s;
 }
 
-// part[(v0+t)*cmax + chunk] = sum_{r in chunk} V_{v0+t}[r] w[r]
+
+// part[t*cmax + chunk] = sum_{r in chunk} V_t[r] w[r].  One block per chunk does every vector: the w
+// chunk is staged once in shared memory, the vectors are streamed in groups of KG with the row loop
+// unrolled by 2 (16 independent loads in flight per thread), then one fixed-tree block sum per vector.
 __global__ void __launch_bounds__(KB) k_mdot(int nv, const double *__restrict__ V, int64_t ldv, const double *__restrict__ w,
                                              const int64_t *__restrict__ be, double *__restrict__ part, int cmax)
 {
-    const int k = blockIdx.x, v0 = blockIdx.y * KG, cnt = min(KG, nv - v0);
-    const int64_t beg = be[2 * k], end = be[2 * k + 1];
-    double acc[KG];
+    __shared__ double ws[kRedChunk];
+    __shared__ double red[KB / 32];
+    const int k = blockIdx.x;
+    const int64_t beg = be[2 * k];
+    const int len = (int)(be[2 * k + 1] - beg);
+    for (int i = threadIdx.x; i < len; i += KB) ws[i] = __ldcs(w + beg + i);
+    __syncthreads();
+    for (int v0 = 0; v0 < nv; v0 += KG) {
+        const int cnt = min(KG, nv - v0);
+        const double *Vg = V + v0 * ldv + beg;
+        double acc[KG];
 #pragma unroll
-    for (int t = 0; t < KG; ++t) acc[t] = 0.0;
-    for (int64_t r = beg + threadIdx.x; r < end; r += KB) {
-        const double wr = __ldg(w + r);
+        for (int t = 0; t < KG; ++t) acc[t] = 0.0;
+        int i = threadIdx.x;
+        for (; i + KB < len; i += 2 * KB) {
+#pragma unroll
+            for (int t = 0; t < KG; ++t)
+                if (t < cnt) {
+                    acc[t] = fma(__ldcs(Vg + t * ldv + i), ws[i], acc[t]);
+                    acc[t] = fma(__ldcs(Vg + t * ldv + i + KB), ws[i + KB], acc[t]);
+                }
+        }
+        for (; i < len; i += KB) {
+#pragma unroll
+            for (int t = 0; t < KG; ++t) if (t < cnt) acc[t] = fma(__ldcs(Vg + t * ldv + i), ws[i], acc[t]);
+        }
 #pragma unroll
         for (int t = 0; t < KG; ++t)
-            if (t < cnt) acc[t] = fma(__ldcs(V + (v0 + t) * ldv + r), wr, acc[t]);
-    }
-    __shared__ double red[KB / 32];
-#pragma unroll
-    for (int t = 0; t < KG; ++t) {
-        const double s = block_sum(acc[t], red);
-        if (threadIdx.x == 0 && t < cnt) part[(int64_t)(v0 + t) * cmax + k] = s;
+            if (t < cnt) {
+                const double s = block_sum(acc[t], red);
+                if (threadIdx.x == 0) part[(int64_t)(v0 + t) * cmax + k] = s;
+            }
     }
 }
 
-// CGS2 pass-1 update fused with the pass-2 projections: w -= V h ; part[t] = V_t . w (per chunk)
+// CGS2 pass-1 update fused with the pass-2 projections: w -= V h ; part[t] = V_t . w (per chunk).
+// Per 256-row slab: thread-per-row update (UL independent loads in flight), the updated slab staged in
+// shared memory, then warp `wid` takes vectors t = wid + 8q and re-reads its slab rows (L1/L2-resident,
+// just streamed by the update) into per-lane partials; one warp tree per vector at the end of the chunk.
+template <int MAXQ>
 __global__ void __launch_bounds__(KB) k_maxpy_mdot(int nv, const double *__restrict__ V, int64_t ldv, const double *__restrict__ h,
                                                    double *__restrict__ w, const int64_t *__restrict__ be,
                                                    double *__restrict__ part, int cmax)
 {
+    constexpr int UL = 4;
     __shared__ double hs[128];
-    __shared__ double sacc[KB / 32][128];
+    __shared__ double ws[KB];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, k = blockIdx.x;
     const int64_t beg = be[2 * k], end = be[2 * k + 1];
     for (int t = threadIdx.x; t < nv; t += KB) hs[t] = h[t];
-    for (int t = lane; t < nv; t += 32) sacc[wid][t] = 0.0;
     __syncthreads();
+    double p[MAXQ];
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q) p[q] = 0.0;
     for (int64_t r0 = beg; r0 < end; r0 += KB) {
         const int64_t r = r0 + threadIdx.x;
-        const bool ok = r < end;
-        double acc = ok ? w[r] : 0.0;
-        if (ok) {
-            for (int t = 0; t < nv; ++t) acc = fma(-hs[t], V[t * ldv + r], acc);
+        double acc = 0.0;
+        if (r < end) {
+            acc = w[r];
+            int t = 0;
+            for (; t + UL <= nv; t += UL) {
+                double vv[UL];
+#pragma unroll
+                for (int u = 0; u < UL; ++u) vv[u] = V[(t + u) * ldv + r];
+#pragma unroll
+                for (int u = 0; u < UL; ++u) acc = fma(-hs[t + u], vv[u], acc);
+            }
+            for (; t < nv; ++t) acc = fma(-hs[t], V[t * ldv + r], acc);
             w[r] = acc;
         }
-        int t = 0;
-        for (; t + 4 <= nv; t += 4) {       // 4 independent shuffle chains
-            double d0 = ok ? V[(t + 0) * ldv + r] * acc : 0.0, d1 = ok ? V[(t + 1) * ldv + r] * acc : 0.0;
-            double d2 = ok ? V[(t + 2) * ldv + r] * acc : 0.0, d3 = ok ? V[(t + 3) * ldv + r] * acc : 0.0;
-            for (int o = 16; o; o >>= 1) {
-                d0 += __shfl_xor_sync(0xffffffffu, d0, o); d1 += __shfl_xor_sync(0xffffffffu, d1, o);
-                d2 += __shfl_xor_sync(0xffffffffu, d2, o); d3 += __shfl_xor_sync(0xffffffffu, d3, o);
+        ws[threadIdx.x] = acc;
+        __syncthreads();
+        const int m = (int)min((int64_t)KB, end - r0);
+#pragma unroll
+        for (int q = 0; q < MAXQ; ++q) {
+            const int t = wid + 8 * q;
+            if (t < nv) {
+                const double *vt = V + t * ldv + r0;
+                if (m == KB) {
+#pragma unroll
+                    for (int e = 0; e < KB / 32; ++e) p[q] = fma(vt[lane + 32 * e], ws[lane + 32 * e], p[q]);
+                } else {
+                    for (int e = lane; e < m; e += 32) p[q] = fma(vt[e], ws[e], p[q]);
+                }
             }
-            if (lane == 0) { sacc[wid][t] += d0; sacc[wid][t + 1] += d1; sacc[wid][t + 2] += d2; sacc[wid][t + 3] += d3; }
         }
-        for (; t < nv; ++t) {
-            double d = ok ? V[t * ldv + r] * acc : 0.0;
-            for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-            if (lane == 0) sacc[wid][t] += d;
-        }
+        __syncthreads();
     }
-    __syncthreads();
-    for (int t = threadIdx.x; t < nv; t += KB) {
-        double s = 0.0;
-        for (int u = 0; u < KB / 32; ++u) s += sacc[u][t];
-        part[(int64_t)t * cmax + k] = s;
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q) {
+        const int t = wid + 8 * q;
+        if (t < nv) {
+            double x = p[q];
+            for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            if (lane == 0) part[(int64_t)t * cmax + k] = x;
+        }
     }
 }
 
-// w -= V h and the per-chunk partial of ||w||^2
+// w -= V h and the per-chunk partial of ||w||^2 (8 independent loads in flight per row)
 __global__ void __launch_bounds__(KB) k_maxpy_norm(int nv, const double *__restrict__ V, int64_t ldv, const double *__restrict__ h,
                                                    double *__restrict__ w, const int64_t *__restrict__ be,
                                                    double *__restrict__ part)
 {
+    constexpr int UL = 8;
     __shared__ double hs[128];
     __shared__ double red[KB / 32];
     const int k = blockIdx.x;
@@ -111,7 +151,15 @@ __global__ void __launch_bounds__(KB) k_maxpy_norm(int nv, const double *__restr
     double nrm = 0.0;
     for (int64_t r = beg + threadIdx.x; r < end; r += KB) {
         double acc = w[r];
-        for (int t = 0; t < nv; ++t) acc = fma(-hs[t], __ldcs(V + t * ldv + r), acc);
+        int t = 0;
+        for (; t + UL <= nv; t += UL) {
+            double vv[UL];
+#pragma unroll
+            for (int u = 0; u < UL; ++u) vv[u] = __ldcs(V + (t + u) * ldv + r);
+#pragma unroll
+            for (int u = 0; u < UL; ++u) acc = fma(-hs[t + u], vv[u], acc);
+        }
+        for (; t < nv; ++t) acc = fma(-hs[t], __ldcs(V + t * ldv + r), acc);
         w[r] = acc;
         nrm = fma(acc, acc, nrm);
     }
@@ -157,7 +205,15 @@ __global__ void __launch_bounds__(KB) k_update(int64_t n, int k, const double *_
     __syncthreads();
     for (int64_t r = blockIdx.x * (int64_t)KB + threadIdx.x; r < n; r += (int64_t)gridDim.x * KB) {
         double acc = x[r];
-        for (int t = 0; t < k; ++t) acc = fma(ys[t], Z[t * ldz + r], acc);
+        int t = 0;
+        for (; t + 8 <= k; t += 8) {
+            double zz[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) zz[u] = __ldcs(Z + (t + u) * ldz + r);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = fma(ys[t + u], zz[u], acc);
+        }
+        for (; t < k; ++t) acc = fma(ys[t], __ldcs(Z + t * ldz + r), acc);
         x[r] = acc;
     }
 }
@@ -176,10 +232,10 @@ __global__ void k_add_into(int nv, const double *__restrict__ a, double *__restr
 
 struct Kr {
     Ctx &c;
-    int64_t n;
+    int64_t n, ld;                    // basis vectors are ld = n rounded up to 32 apart (256-B aligned)
     int nblk;
     DBuf<double> pall;
-    Kr(Ctx &c_, int maxv) : c(c_), n(c_.n)
+    Kr(Ctx &c_, int maxv) : c(c_), n(c_.n), ld((c_.n + 31) & ~(int64_t)31)
     {
         nblk = (int)std::max<int64_t>(1, std::min<int64_t>((n + KB - 1) / KB, (int64_t)c.sm_count * 4));
         pall.alloc((size_t)std::max(c.nranks, 1) * maxv * std::max(c.nseg_max, 1) + 16);
@@ -202,16 +258,16 @@ struct Kr {
     void mdot(const double *V, int nv, const double *w, double *h)
     {
         prof_begin(c, PK_DOT);
-        dim3 g(c.nchunk_loc, (nv + KG - 1) / KG);
-        k_mdot<<<g, KB, 0, c.s>>>(nv, V, n, w, c.chunk_beg, c.kpart, c.nchunk_loc);
+        k_mdot<<<c.nchunk_loc, KB, 0, c.s>>>(nv, V, ld, w, c.chunk_beg, c.kpart, c.nchunk_loc);
         finish(nv, h, 0);
-        prof_end(c, PK_DOT, 8.0 * n * (nv + (nv + KG - 1) / KG));
+        prof_end(c, PK_DOT, 8.0 * n * (nv + 1));
         c.launches++;
     }
     void maxpy_mdot(const double *V, int nv, const double *h1, double *w, double *h2)
     {
         prof_begin(c, PK_AXPY);
-        k_maxpy_mdot<<<c.nchunk_loc, KB, 0, c.s>>>(nv, V, n, h1, w, c.chunk_beg, c.kpart, c.nchunk_loc);
+        (nv <= 64 ? k_maxpy_mdot<8> : k_maxpy_mdot<16>)<<<c.nchunk_loc, KB, 0, c.s>>>(nv, V, ld, h1, w, c.chunk_beg, c.kpart,
+                                                                                        c.nchunk_loc);
         finish(nv, h2, 0);
         prof_end(c, PK_AXPY, 8.0 * n * (nv + 2));
         c.launches++;
@@ -219,7 +275,7 @@ struct Kr {
     void maxpy_norm(const double *V, int nv, const double *h, double *w, double *nrm)
     {
         prof_begin(c, PK_AXPY);
-        k_maxpy_norm<<<c.nchunk_loc, KB, 0, c.s>>>(nv, V, n, h, w, c.chunk_beg, c.kpart);
+        k_maxpy_norm<<<c.nchunk_loc, KB, 0, c.s>>>(nv, V, ld, h, w, c.chunk_beg, c.kpart);
         finish(1, nrm, 2);
         prof_end(c, PK_AXPY, 8.0 * n * (nv + 2));
         c.launches++;
@@ -227,8 +283,7 @@ struct Kr {
     void norm(const double *w, double *nrm)
     {
         prof_begin(c, PK_NORM);
-        dim3 g(c.nchunk_loc, 1);
-        k_mdot<<<g, KB, 0, c.s>>>(1, w, n, w, c.chunk_beg, c.kpart, c.nchunk_loc);
+        k_mdot<<<c.nchunk_loc, KB, 0, c.s>>>(1, w, ld, w, c.chunk_beg, c.kpart, c.nchunk_loc);
         finish(1, nrm, 2);
         prof_end(c, PK_NORM, 8.0 * n);
         c.launches++;
@@ -245,10 +300,10 @@ struct Kr {
 void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, tsp_solve_info &info)
 {
     const int m = std::max(1, std::min(o.restart, 120));
-    const int64_t n = c.n;
-    if (c.kcap != m || c.V.n != (size_t)(m + 1) * n) {
-        c.V.alloc((size_t)(m + 1) * n);
-        c.Z.alloc((size_t)m * n);
+    const int64_t n = c.n, ld = (n + 31) & ~(int64_t)31;
+    if (c.kcap != m || c.V.n != (size_t)(m + 1) * ld) {
+        c.V.alloc((size_t)(m + 1) * ld);
+        c.Z.alloc((size_t)m * ld);
         c.kr.alloc(std::max<int64_t>(n, 1));
         c.kh.alloc(4 * (m + 2));
         c.kpart.alloc((size_t)(m + 2) * std::max(c.nchunk_loc, 1) + 64);
@@ -294,7 +349,7 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
             g[0] = beta;
             int k = 0;
             for (int j = 0; j < m; ++j) {
-                double *vj = V + (size_t)j * n, *zj = Z + (size_t)j * n, *w = V + (size_t)(j + 1) * n;
+                double *vj = V + (size_t)j * ld, *zj = Z + (size_t)j * ld, *w = V + (size_t)(j + 1) * ld;
                 prec_apply(c, vj, zj);                 // z_j = M^-1 v_j (Algorithm 1)
                 op_apply(c, zj, w);                    // w = A z_j
                 // CGS2 (DESIGN.md R-krylov).  A DGKS-selective second pass was measured to be needed
@@ -333,7 +388,7 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
             }
             TSP_CUDA(cudaMemcpyAsync(dh2, yv.data(), sizeof(double) * k, cudaMemcpyHostToDevice, c.s));
             prof_begin(c, PK_AXPY);
-            k_update<<<K.nblk, KB, 0, c.s>>>(n, k, Z, n, dh2, x);
+            k_update<<<K.nblk, KB, 0, c.s>>>(n, k, Z, ld, dh2, x);
             prof_end(c, PK_AXPY, 8.0 * n * (k + 2));
             c.launches++;
         }

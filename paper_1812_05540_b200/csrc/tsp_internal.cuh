@@ -10,6 +10,9 @@
 
 namespace tsp {
 
+// rows per deterministic-reduction chunk (halo.cu reduce_setup; krylov.cu stages one chunk in shared memory)
+constexpr int kRedChunk = 2048;
+
 // ------------------------------------------------------------------ errors
 void set_error(const std::string &msg);
 struct Error {
