@@ -19,6 +19,15 @@
 
 namespace tsp {
 
+// lanes per row from the GLOBAL mean row length (0: sliced-ELL thread per row); measured at C5:
+// 8/16 lanes beat a full warp by 20-35 % on the pressure levels 1-2 and the level-0 restriction
+static int lanes_for(int64_t nnz, int64_t rows)
+{
+    if (rows <= 0 || nnz < 12 * rows) return 0;
+    return nnz < 40 * rows ? 8 : nnz < 96 * rows ? 16 : 32;
+}
+
+
 __device__ __forceinline__ uint32_t fmix32(uint32_t x)
 {
     x ^= x >> 16; x *= 0x85ebca6bU; x ^= x >> 13; x *= 0xc2b2ae35U; x ^= x >> 16;
@@ -854,8 +863,8 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
                 st.assign(4, 0);
                 for (int r = 0; r < c.nranks; ++r) for (int k = 0; k < 4; ++k) st[k] += all[4 * r + k];
             }
-            L.warpA = l > 0 && st[1] > 0 && st[0] >= 12 * st[1];
-            L.warpR = st[3] > 0 && st[2] >= 12 * st[3];
+            L.warpA = l > 0 ? lanes_for(st[0], st[1]) : 0;
+            L.warpR = lanes_for(st[2], st[3]);
         }
         if (L.dist) {
             const size_t g = (size_t)std::max(L.hp->nghost(), 1) * nc;
@@ -973,43 +982,58 @@ __global__ void k_coarse(int n, const double *__restrict__ inv, const double *__
     x[(int64_t)i * NC + c] = s;
 }
 
-// ---- warp-per-row CSR variants for operators with long rows (coarse levels,
-// restriction): lanes stride a row's entries (coalesced [q][c] values), shuffle reduce.
+// ---- vector-CSR variants for operators with long rows (coarse levels, restriction): a
+// group of G lanes (G | 32) per row strides the row's entries (coalesced [q][c] values),
+// then a fixed shuffle tree inside the group.  32/G rows per warp keep several dependent
+// load chains in flight.
 // MODE 0: y = A x ; MODE 1: pre (x = D^-1 b, r = b - A D^-1 b) ; MODE 2: post (xo = x + D^-1 (b - A x))
-template <int NC, int MODE, bool D>
-__global__ void __launch_bounds__(256) k_csr_warp(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
-                                                  const double *__restrict__ v, GV dinv, GV b, GV x,
-                                                  double *__restrict__ out1, double *__restrict__ out2)
+template <int NC, int MODE, bool D, int G>
+__global__ void __launch_bounds__(256) k_csr_vec(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                                                 const double *__restrict__ v, GV dinv, GV b, GV x,
+                                                 double *__restrict__ out1, double *__restrict__ out2)
 {
-    const int lane = threadIdx.x & 31;
-    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (i >= n) return;
+    const int sub = threadIdx.x & (G - 1);
+    const int i = blockIdx.x * (blockDim.x / G) + (threadIdx.x / G);
+    const bool ok = i < n;
     double acc[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) acc[c] = 0.0;
-    const int64_t q1 = rp[i + 1];
-    for (int64_t q = rp[i] + lane; q < q1; q += 32) {
-        const int j = ci[q];
+    if (ok) {
+        const int64_t q1 = rp[i + 1];
+#pragma unroll 2
+        for (int64_t q = rp[i] + sub; q < q1; q += G) {
+            const int j = ci[q];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            const double xv = MODE == 1 ? gvld<D>(b, j, c, NC) * gvld<D>(dinv, j, c, NC) : gvld<D>(x, j, c, NC);
-            acc[c] = fma(__ldcs(v + q * NC + c), xv, acc[c]);
+            for (int c = 0; c < NC; ++c) {
+                const double xv = MODE == 1 ? gvld<D>(b, j, c, NC) * gvld<D>(dinv, j, c, NC) : gvld<D>(x, j, c, NC);
+                acc[c] = fma(__ldcs(v + q * NC + c), xv, acc[c]);
+            }
         }
     }
 #pragma unroll
     for (int c = 0; c < NC; ++c)
-        for (int o = 16; o; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
-    if (lane < NC) {
+#pragma unroll
+        for (int o = G / 2; o; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+    if (ok && sub < NC) {
         double a = acc[0];
 #pragma unroll
-        for (int c = 1; c < NC; ++c) if (lane == c) a = acc[c];
-        const int64_t t = (int64_t)i * NC + lane;
+        for (int c = 1; c < NC; ++c) if (sub == c) a = acc[c];
+        const int64_t t = (int64_t)i * NC + sub;
         if (MODE == 0) out1[t] = a;
         else if (MODE == 1) { out1[t] = b.own[t] * dinv.own[t]; out2[t] = b.own[t] - a; }
         else out1[t] = x.own[t] + dinv.own[t] * (b.own[t] - a);
     }
 }
-
+template <int NC, int MODE, bool D>
+static void csr_vec(int G, cudaStream_t s, int n, const Csr &A, GV dinv, GV b, GV x, double *o1, double *o2)
+{
+    if (!n) return;
+    const int rows = 256 / G;
+    const dim3 grid((unsigned)((n + rows - 1) / rows));
+    if (G == 8) k_csr_vec<NC, MODE, D, 8><<<grid, 256, 0, s>>>(n, A.rp, A.ci, A.v, dinv, b, x, o1, o2);
+    else if (G == 16) k_csr_vec<NC, MODE, D, 16><<<grid, 256, 0, s>>>(n, A.rp, A.ci, A.v, dinv, b, x, o1, o2);
+    else k_csr_vec<NC, MODE, D, 32><<<grid, 256, 0, s>>>(n, A.rp, A.ci, A.v, dinv, b, x, o1, o2);
+}
 // compact the padded allgather [rank][mx*nc] into the full replicated vector
 __global__ void k_rep_compact(int nranks, int nc, int64_t mx, const int64_t *__restrict__ offs, const double *__restrict__ buf,
                               double *__restrict__ out)
@@ -1037,15 +1061,14 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     }
     const int n = L.n;
     const double vec = 8.0 * NC * n;
-    const bool wA = L.warpA, wR = L.warpR;
+    const int wA = L.warpA, wR = L.warpR;
     const double bA = wA ? cbytes(L.A) : sbytes(L.sA), bR = wR ? cbytes(L.R) : sbytes(L.sR);
     const double *ghd = L.dist ? L.dinv_gh.p : nullptr;
     // pre-smooth + residual (needs b and D^-1 of the ghost rows)
     if (L.dist) halo_exchange(c, *L.hp, NC, b, L.gh_b);
     const GV gb = gv(b, n, L.dist ? L.gh_b.p : nullptr), gd = gv(L.dinv, n, ghd);
     prof_begin(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P);
-    if (wA) (L.dist ? k_csr_warp<NC, 1, true> : k_csr_warp<NC, 1, false>)<<<grid_for(n, 8), 256, 0, c.s>>>(
-        n, L.A.rp, L.A.ci, L.A.v, gd, gb, gv(nullptr, 0), L.x2, L.r);
+    if (wA) (L.dist ? csr_vec<NC, 1, true> : csr_vec<NC, 1, false>)(wA, c.s, n, L.A, gd, gb, gv(nullptr, 0), L.x2, L.r);
     else if (n) (L.dist ? k_vc_pre<NC, true> : k_vc_pre<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
         n, L.sA.off, L.sA.col, L.sA.val, gd, gb, L.x2, L.r);
     prof_end(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P, bA + 4 * vec);
@@ -1055,8 +1078,7 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     const int nr = L.sR.nrows;
     double *rdst = gather ? L.rep_buf.p + (size_t)c.nranks * 0 : Lc.b.p;
     prof_begin(c, mech ? PK_VC_RESTR_U : PK_VC_RESTR_P);
-    if (wR) k_csr_warp<NC, 0, false><<<grid_for(nr, 8), 256, 0, c.s>>>(nr, L.R.rp, L.R.ci, L.R.v, gv(nullptr, 0), gv(nullptr, 0),
-                                                                    gv(L.r, n), rdst, nullptr);
+    if (wR) csr_vec<NC, 0, false>(wR, c.s, nr, L.R, gv(nullptr, 0), gv(nullptr, 0), gv(L.r, n), rdst, nullptr);
     else if (nr) k_sell_mv<NC><<<grid_for(nr, 256), 256, 0, c.s>>>(nr, L.sR.off, L.sR.col, L.sR.val, L.r, rdst);
     prof_end(c, mech ? PK_VC_RESTR_U : PK_VC_RESTR_P, bR + vec + 8.0 * NC * nr);
     if (gather) {
@@ -1077,8 +1099,7 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     if (L.dist) halo_exchange(c, *L.hp, NC, L.x2, L.gh_x);
     const GV gx = gv(L.x2, n, L.dist ? L.gh_x.p : nullptr);
     prof_begin(c, mech ? PK_VC_POST_U : PK_VC_POST_P);
-    if (wA) (L.dist ? k_csr_warp<NC, 2, true> : k_csr_warp<NC, 2, false>)<<<grid_for(n, 8), 256, 0, c.s>>>(
-        n, L.A.rp, L.A.ci, L.A.v, gv(L.dinv, n), gv(b, n), gx, xout, nullptr);
+    if (wA) (L.dist ? csr_vec<NC, 2, true> : csr_vec<NC, 2, false>)(wA, c.s, n, L.A, gv(L.dinv, n), gv(b, n), gx, xout, nullptr);
     else if (n) (L.dist ? k_vc_post<NC, true> : k_vc_post<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
         n, L.sA.off, L.sA.col, L.sA.val, L.dinv, b, gx, xout);
     prof_end(c, mech ? PK_VC_POST_U : PK_VC_POST_P, bA + 4 * vec);

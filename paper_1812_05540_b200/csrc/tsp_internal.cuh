@@ -137,7 +137,8 @@ struct Level {
     int64_t nglob = 0, row_off = 0;    // global rows and this rank's first row (dist)
     int64_t coarse_off = 0;            // first global id of this rank's aggregates
     bool next_dist = false;            // is level+1 distributed?
-    bool warpA = false, warpR = false; // warp-per-row kernels (chosen from GLOBAL row lengths: same on every rank)
+    int warpA = 0, warpR = 0;          // lanes per row of the vector-CSR kernels, 0 = sliced-ELL (chosen from
+                                       // GLOBAL row lengths: the same on every rank)
     Halo halo;                         // of A's columns (dist, coarse levels)
     Halo *hp = nullptr;                // plan in use: &halo, or the fine-grid plan on level 0
     DBuf<double> dinv_gh;              // ghost copy of dinv (dist)
