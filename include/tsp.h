@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define TSP_ABI_VERSION 1
+#define TSP_ABI_VERSION 2
 
 typedef int tsp_status;
 enum {
@@ -121,7 +121,8 @@ typedef struct {
     double est_relres;           /* Arnoldi estimate |g_{j+1}| / ||b|| */
     double true_relres;          /* recomputed ||b - A x|| / ||b|| at exit */
     double t_solve_s;
-    int reorth;                  /* iterations that needed the second Gram-Schmidt pass */
+    int reorth;                  /* basis vectors re-orthogonalised (DCGS2: every one, one step late) */
+    double bytes_krylov;         /* algorithmic bytes of the Gram-Schmidt / normalisation / x-update kernels */
 } tsp_solve_info;
 
 typedef struct {
@@ -131,8 +132,8 @@ typedef struct {
     int64_t skipped_dss, perturbed_pivots, coarsening_fallbacks;
     double bytes_apply;          /* algorithmic bytes of one tsp_apply_preconditioner */
     double bytes_operator;       /* algorithmic bytes of one tsp_apply_operator */
-    double bytes_iter_base;      /* per FGMRES iteration excluding the Krylov-index-dependent part */
-    double bytes_per_krylov_vec; /* Gram-Schmidt bytes per basis vector and pass (x (j+1) x passes) */
+    double bytes_iter_base;      /* per FGMRES iteration excluding Gram-Schmidt: apply + operator */
+    double bytes_per_krylov_vec; /* bytes of one basis-vector pass (8 n); exact Krylov bytes: tsp_solve_info */
 } tsp_stats;
 
 /* per-kernel-class timing (CUDA events on the handle's stream), for roofline */

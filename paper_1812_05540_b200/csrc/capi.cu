@@ -297,9 +297,8 @@ tsp_status tsp_get_stats(tsp_handle h, tsp_stats *s)
     apply_bytes += (28.0 * 8 + 32 + 48) * Nc;                  // steps 6-8
     s->bytes_apply = apply_bytes;
     s->bytes_operator = sb(h->s_uu) + sb(h->s_uf) + sb(h->s_fu) + sb(h->s_ff) + 16 * n;
-    // CGS2 as fused here: V is read by the projection pass, the fused update + second
-    // projection pass and the update + norm pass; w read 1, r/w 2, r/w 2, normalisation 2 -> 7
-    s->bytes_iter_base = s->bytes_apply + s->bytes_operator + 8 * n * 7;
+    // Gram-Schmidt depends on the Krylov index: counted exactly per solve (tsp_solve_info.bytes_krylov)
+    s->bytes_iter_base = s->bytes_apply + s->bytes_operator;
     s->bytes_per_krylov_vec = 8 * n;
     s->launches = h->launches;
     return TSP_OK;

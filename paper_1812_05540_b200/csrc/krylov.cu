@@ -1,5 +1,13 @@
 // krylov.cu -- rows a13/a14: right-preconditioned flexible GMRES(m)
-// with classical Gram-Schmidt applied twice (CGS2, DESIGN.md R-krylov).
+// with classical Gram-Schmidt applied twice, the second pass DELAYED by one
+// iteration (DCGS2, DESIGN.md R-krylov): iteration j holds v_0..v_{j-1} final and
+// u_j once-orthogonalised; ONE pass over the basis computes [V_{j-1} u_j]^T [u_j w]
+// (w = A M^-1 u_j), which both re-orthogonalises u_j into v_j (Pythagorean norm)
+// and projects w; ONE fused pass then updates u_j -> v_j and w -> u_{j+1} (+ its
+// norm).  Two basis passes per iteration instead of CGS2's three.  FGMRES keeps
+// z_j = M^-1 u_j, so A Z = V H holds exactly with the Hessenberg column of step j-1
+// completed at step j (H[:, j-1] += rho_{j-1} [s_j; alpha_j - 1 at row j]) and the
+// last column completed by one extra projection of u_{k} at the end of the cycle.
 //
 // Deterministic reductions (R-reduce): every dot product is a sum of per-chunk
 // partials (fixed chunks of the GLOBAL vector, halo.cu), each reduced by a fixed
@@ -30,6 +38,36 @@ __device__ __forceinline__ double block_sum(double x, double *red)   // fixed tr
     return s;
 }
 
+// NV values per thread (NV a power of two <= 32) -> thread t < NV returns the block total of value t.
+// Warp stage: transpose-reduce (log2 NV halving exchanges, NV-1 shuffles instead of 5 NV), after which
+// lane L holds the warp total of value bitrev(L mod NV); then a fixed sum over the warps.
+template <int NV>
+__device__ __forceinline__ double block_sum_multi(double (&d)[NV], double (*red)[NV])
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int h = NV / 2, m = 1; h >= 1; h >>= 1, m <<= 1) {
+        const bool up = lane & m;
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+            const double snd = up ? d[i] : d[i + h], kp = up ? d[i + h] : d[i];
+            d[i] = kp + __shfl_xor_sync(0xffffffffu, snd, m);
+        }
+    }
+    double x = d[0];
+#pragma unroll
+    for (int o = NV; o < 32; o <<= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    int idx = 0;
+#pragma unroll
+    for (int bit = 1, t = NV / 2; bit < NV; bit <<= 1, t >>= 1) if (lane & bit) idx |= t;
+    if (lane < NV) red[wid][idx] = x;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x < NV)
+        for (int u = 0; u < KB / 32; ++u) s += red[u][threadIdx.x];
+    __syncthreads();
+    return s;
+}
 
 // part[t*cmax + chunk] = sum_{r in chunk} V_t[r] w[r].  One block per chunk does every vector: the w
 // chunk is staged once in shared memory, the vectors are streamed in groups of KG with the row loop
@@ -72,96 +110,104 @@ __global__ void __launch_bounds__(KB) k_mdot(int nv, const double *__restrict__ 
     }
 }
 
-// CGS2 pass-1 update fused with the pass-2 projections: w -= V h ; part[t] = V_t . w (per chunk).
-// Per 256-row slab: thread-per-row update (UL independent loads in flight), the updated slab staged in
-// shared memory, then warp `wid` takes vectors t = wid + 8q and re-reads its slab rows (L1/L2-resident,
-// just streamed by the update) into per-lane partials; one warp tree per vector at the end of the chunk.
-template <int MAXQ>
-__global__ void __launch_bounds__(KB) k_maxpy_mdot(int nv, const double *__restrict__ V, int64_t ldv, const double *__restrict__ h,
-                                                   double *__restrict__ w, const int64_t *__restrict__ be,
-                                                   double *__restrict__ part, int cmax)
+// DCGS2 pass 1: part[t] = V_t . u, part[nv + t] = V_t . w for t < nv (V_{nv-1} is u itself), per chunk.
+// u and w chunks staged interleaved in shared memory (one 16-B load per row); KG2 vectors per group,
+// rows unrolled by 2, both products share each V load.
+constexpr int KG2 = 4;
+__global__ void __launch_bounds__(KB) k_mdot2(int nv, const double *__restrict__ V, int64_t ldv, const double *__restrict__ u,
+                                              const double *__restrict__ w, const int64_t *__restrict__ be,
+                                              double *__restrict__ part, int cmax)
 {
-    constexpr int UL = 4;
-    __shared__ double hs[128];
-    __shared__ double ws[KB];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, k = blockIdx.x;
-    const int64_t beg = be[2 * k], end = be[2 * k + 1];
-    for (int t = threadIdx.x; t < nv; t += KB) hs[t] = h[t];
+    __shared__ double2 uw[kRedChunk];
+    __shared__ double red[KB / 32][2 * KG2];
+    const int k = blockIdx.x;
+    const int64_t beg = be[2 * k];
+    const int len = (int)(be[2 * k + 1] - beg);
+    for (int i = threadIdx.x; i < len; i += KB) uw[i] = make_double2(__ldcs(u + beg + i), __ldcs(w + beg + i));
     __syncthreads();
-    double p[MAXQ];
+    for (int v0 = 0; v0 < nv; v0 += KG2) {
+        const int cnt = min(KG2, nv - v0);
+        const double *Vg = V + v0 * ldv + beg;
+        double acc[2 * KG2];
 #pragma unroll
-    for (int q = 0; q < MAXQ; ++q) p[q] = 0.0;
-    for (int64_t r0 = beg; r0 < end; r0 += KB) {
-        const int64_t r = r0 + threadIdx.x;
-        double acc = 0.0;
-        if (r < end) {
-            acc = w[r];
-            int t = 0;
-            for (; t + UL <= nv; t += UL) {
-                double vv[UL];
+        for (int t = 0; t < 2 * KG2; ++t) acc[t] = 0.0;
+        int i = threadIdx.x;
+        for (; i + KB < len; i += 2 * KB) {
+            const double2 x0 = uw[i], x1 = uw[i + KB];
 #pragma unroll
-                for (int u = 0; u < UL; ++u) vv[u] = V[(t + u) * ldv + r];
-#pragma unroll
-                for (int u = 0; u < UL; ++u) acc = fma(-hs[t + u], vv[u], acc);
-            }
-            for (; t < nv; ++t) acc = fma(-hs[t], V[t * ldv + r], acc);
-            w[r] = acc;
-        }
-        ws[threadIdx.x] = acc;
-        __syncthreads();
-        const int m = (int)min((int64_t)KB, end - r0);
-#pragma unroll
-        for (int q = 0; q < MAXQ; ++q) {
-            const int t = wid + 8 * q;
-            if (t < nv) {
-                const double *vt = V + t * ldv + r0;
-                if (m == KB) {
-#pragma unroll
-                    for (int e = 0; e < KB / 32; ++e) p[q] = fma(vt[lane + 32 * e], ws[lane + 32 * e], p[q]);
-                } else {
-                    for (int e = lane; e < m; e += 32) p[q] = fma(vt[e], ws[e], p[q]);
+            for (int t = 0; t < KG2; ++t)
+                if (t < cnt) {
+                    const double va = __ldcs(Vg + t * ldv + i), vb = __ldcs(Vg + t * ldv + i + KB);
+                    acc[t] = fma(va, x0.x, acc[t]); acc[t] = fma(vb, x1.x, acc[t]);
+                    acc[KG2 + t] = fma(va, x0.y, acc[KG2 + t]); acc[KG2 + t] = fma(vb, x1.y, acc[KG2 + t]);
                 }
-            }
         }
-        __syncthreads();
-    }
+        for (; i < len; i += KB) {
+            const double2 x0 = uw[i];
 #pragma unroll
-    for (int q = 0; q < MAXQ; ++q) {
-        const int t = wid + 8 * q;
-        if (t < nv) {
-            double x = p[q];
-            for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-            if (lane == 0) part[(int64_t)t * cmax + k] = x;
+            for (int t = 0; t < KG2; ++t)
+                if (t < cnt) {
+                    const double va = __ldcs(Vg + t * ldv + i);
+                    acc[t] = fma(va, x0.x, acc[t]);
+                    acc[KG2 + t] = fma(va, x0.y, acc[KG2 + t]);
+                }
         }
+        const double s = block_sum_multi<2 * KG2>(acc, red);
+        const int q = threadIdx.x;
+        if (q < 2 * KG2 && (q % KG2) < cnt) part[(int64_t)((q < KG2 ? 0 : nv) + v0 + q % KG2) * cmax + k] = s;
     }
 }
 
-// w -= V h and the per-chunk partial of ||w||^2 (8 independent loads in flight per row)
-__global__ void __launch_bounds__(KB) k_maxpy_norm(int nv, const double *__restrict__ V, int64_t ldv, const double *__restrict__ h,
-                                                   double *__restrict__ w, const int64_t *__restrict__ be,
-                                                   double *__restrict__ part)
+// DCGS2 scalars from the pass-1 dots d = [V_{j-1} u ; u.u | V_{j-1} w ; u.w] (2(j+1) values):
+// s = d[0..j), gamma = d[j], a = d[j+1..2j+1), b = d[2j+1];
+// alpha = sqrt(gamma - s.s) (norm of the re-orthogonalised u), h_j = (b - s.a) / alpha (= v_j . w).
+// sc[0] = alpha, sc[1] = h_j; alpha <= 0 (u numerically inside span V) is reported as NaN.
+__global__ void k_dcgs_coef(int j, const double *__restrict__ d, double *__restrict__ sc)
+{
+    if (threadIdx.x) return;
+    double ss = 0.0, sa = 0.0;
+    for (int t = 0; t < j; ++t) { ss = fma(d[t], d[t], ss); sa = fma(d[t], d[j + 1 + t], sa); }
+    const double a2 = d[j] - ss;
+    const double alpha = a2 > 0.0 ? sqrt(a2) : nan("");
+    sc[0] = alpha;
+    sc[1] = (d[2 * j + 1] - sa) / alpha;
+}
+
+// DCGS2 pass 2 (fused): v_j = (u - V_{j-1} s) / alpha (in place of u); w <- w - V_{j-1} a - h_j v_j;
+// part[chunk] = sum w^2.  8 independent basis loads in flight per row, both sums share them.
+__global__ void __launch_bounds__(KB) k_dcgs_update(int j, const double *__restrict__ V, int64_t ldv,
+                                                    const double *__restrict__ d, const double *__restrict__ sc,
+                                                    double *__restrict__ u, double *__restrict__ w,
+                                                    const int64_t *__restrict__ be, double *__restrict__ part)
 {
     constexpr int UL = 8;
-    __shared__ double hs[128];
+    __shared__ double ss[128], as[128];
     __shared__ double red[KB / 32];
     const int k = blockIdx.x;
     const int64_t beg = be[2 * k], end = be[2 * k + 1];
-    for (int t = threadIdx.x; t < nv; t += KB) hs[t] = h[t];
+    for (int t = threadIdx.x; t < j; t += KB) { ss[t] = d[t]; as[t] = d[j + 1 + t]; }
+    const double alpha = sc[0], hj = sc[1];
     __syncthreads();
     double nrm = 0.0;
     for (int64_t r = beg + threadIdx.x; r < end; r += KB) {
-        double acc = w[r];
+        double su = 0.0, sa = 0.0;
         int t = 0;
-        for (; t + UL <= nv; t += UL) {
+        for (; t + UL <= j; t += UL) {
             double vv[UL];
 #pragma unroll
-            for (int u = 0; u < UL; ++u) vv[u] = __ldcs(V + (t + u) * ldv + r);
+            for (int q = 0; q < UL; ++q) vv[q] = __ldcs(V + (t + q) * ldv + r);
 #pragma unroll
-            for (int u = 0; u < UL; ++u) acc = fma(-hs[t + u], vv[u], acc);
+            for (int q = 0; q < UL; ++q) { su = fma(ss[t + q], vv[q], su); sa = fma(as[t + q], vv[q], sa); }
         }
-        for (; t < nv; ++t) acc = fma(-hs[t], __ldcs(V + t * ldv + r), acc);
-        w[r] = acc;
-        nrm = fma(acc, acc, nrm);
+        for (; t < j; ++t) {
+            const double vv = __ldcs(V + t * ldv + r);
+            su = fma(ss[t], vv, su); sa = fma(as[t], vv, sa);
+        }
+        const double v = (u[r] - su) / alpha;
+        const double wn = (w[r] - sa) - hj * v;
+        u[r] = v;
+        w[r] = wn;
+        nrm = fma(wn, wn, nrm);
     }
     const double s = block_sum(nrm, red);
     if (threadIdx.x == 0) part[k] = s;
@@ -228,12 +274,12 @@ __global__ void k_bminus(int64_t n, const double *__restrict__ b, double *__rest
 {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) r[i] = b[i] - r[i];
 }
-__global__ void k_add_into(int nv, const double *__restrict__ a, double *__restrict__ b) { int i = threadIdx.x; if (i < nv) b[i] += a[i]; }
 
 struct Kr {
     Ctx &c;
     int64_t n, ld;                    // basis vectors are ld = n rounded up to 32 apart (256-B aligned)
     int nblk;
+    double bytes = 0;                 // algorithmic bytes of the Krylov kernels (tsp_solve_info.bytes_krylov)
     DBuf<double> pall;
     Kr(Ctx &c_, int maxv) : c(c_), n(c_.n), ld((c_.n + 31) & ~(int64_t)31)
     {
@@ -261,23 +307,28 @@ struct Kr {
         k_mdot<<<c.nchunk_loc, KB, 0, c.s>>>(nv, V, ld, w, c.chunk_beg, c.kpart, c.nchunk_loc);
         finish(nv, h, 0);
         prof_end(c, PK_DOT, 8.0 * n * (nv + 1));
+        bytes += 8.0 * n * (nv + 1);
         c.launches++;
     }
-    void maxpy_mdot(const double *V, int nv, const double *h1, double *w, double *h2)
+    // pass 1: d = [V_0..V_j]^T [u_j, w] (V_j = u_j), then alpha / h_j into sc
+    void mdot2(const double *V, int j, const double *w, double *d, double *sc)
     {
-        prof_begin(c, PK_AXPY);
-        (nv <= 64 ? k_maxpy_mdot<8> : k_maxpy_mdot<16>)<<<c.nchunk_loc, KB, 0, c.s>>>(nv, V, ld, h1, w, c.chunk_beg, c.kpart,
-                                                                                        c.nchunk_loc);
-        finish(nv, h2, 0);
-        prof_end(c, PK_AXPY, 8.0 * n * (nv + 2));
-        c.launches++;
+        prof_begin(c, PK_DOT);
+        k_mdot2<<<c.nchunk_loc, KB, 0, c.s>>>(j + 1, V, ld, V + (size_t)j * ld, w, c.chunk_beg, c.kpart, c.nchunk_loc);
+        finish(2 * (j + 1), d, 0);
+        k_dcgs_coef<<<1, 32, 0, c.s>>>(j, d, sc);
+        prof_end(c, PK_DOT, 8.0 * n * (j + 2));
+        bytes += 8.0 * n * (j + 2);
+        c.launches += 2;
     }
-    void maxpy_norm(const double *V, int nv, const double *h, double *w, double *nrm)
+    // pass 2: v_j = (u_j - V s)/alpha, w -= V a + h_j v_j, rho = ||w||
+    void dcgs_update(const double *V, int j, const double *d, const double *sc, double *w, double *rho)
     {
         prof_begin(c, PK_AXPY);
-        k_maxpy_norm<<<c.nchunk_loc, KB, 0, c.s>>>(nv, V, ld, h, w, c.chunk_beg, c.kpart);
-        finish(1, nrm, 2);
-        prof_end(c, PK_AXPY, 8.0 * n * (nv + 2));
+        k_dcgs_update<<<c.nchunk_loc, KB, 0, c.s>>>(j, V, ld, d, sc, (double *)V + (size_t)j * ld, w, c.chunk_beg, c.kpart);
+        finish(1, rho, 2);
+        prof_end(c, PK_AXPY, 8.0 * n * (j + 4));
+        bytes += 8.0 * n * (j + 4);
         c.launches++;
     }
     void norm(const double *w, double *nrm)
@@ -286,6 +337,7 @@ struct Kr {
         k_mdot<<<c.nchunk_loc, KB, 0, c.s>>>(1, w, ld, w, c.chunk_beg, c.kpart, c.nchunk_loc);
         finish(1, nrm, 2);
         prof_end(c, PK_NORM, 8.0 * n);
+        bytes += 8.0 * n;
         c.launches++;
     }
     void scale_inv(const double *s, const double *x, double *y)
@@ -293,7 +345,47 @@ struct Kr {
         prof_begin(c, PK_VEC);
         k_scale_inv<<<nblk, KB, 0, c.s>>>(n, s, x, y);
         prof_end(c, PK_VEC, 16.0 * n);
+        bytes += 16.0 * n;
         c.launches++;
+    }
+};
+
+// Hessenberg bookkeeping on the host: raw columns (completed one step late, see the header),
+// their Givens-rotated copies and the rotated right-hand side g.  gin[i] is g[i] before
+// rotation i, so a column whose rotation changes can be re-rotated exactly.
+struct Hess {
+    int m;
+    std::vector<std::vector<double>> raw, rot;
+    std::vector<double> cs, sn, g, gin;
+    explicit Hess(int m_) : m(m_), raw(m_), rot(m_), cs(m_), sn(m_), g(m_ + 1), gin(m_ + 1) {}
+    void reset(double beta)
+    {
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = gin[0] = beta;
+    }
+    // (re)compute the rotation of column i from its raw entries and rotations 0..i-1
+    void rotate(int i)
+    {
+        std::vector<double> R = raw[i];
+        for (int t = 0; t < i; ++t) {
+            const double a = R[t], b = R[t + 1];
+            R[t] = cs[t] * a + sn[t] * b;
+            R[t + 1] = -sn[t] * a + cs[t] * b;
+        }
+        const double rho = std::hypot(R[i], R[i + 1]);
+        cs[i] = R[i] / rho; sn[i] = R[i + 1] / rho;
+        R[i] = rho; R[i + 1] = 0.0;
+        rot[i] = R;
+        g[i] = cs[i] * gin[i];
+        g[i + 1] = -sn[i] * gin[i];
+        gin[i + 1] = g[i + 1];
+    }
+    // complete column i with the delayed re-orthogonalisation of u_{i+1}: u_{i+1} = alpha v_{i+1} + V s
+    void complete(int i, double rho, const double *s, double alpha)
+    {
+        for (int t = 0; t <= i; ++t) raw[i][t] += rho * s[t];
+        raw[i][i + 1] = rho * alpha;
+        rotate(i);
     }
 };
 
@@ -305,23 +397,24 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
         c.V.alloc((size_t)(m + 1) * ld);
         c.Z.alloc((size_t)m * ld);
         c.kr.alloc(std::max<int64_t>(n, 1));
-        c.kh.alloc(4 * (m + 2));
-        c.kpart.alloc((size_t)(m + 2) * std::max(c.nchunk_loc, 1) + 64);
-        c.seg_part.alloc((size_t)(m + 2) * std::max(c.nseg_max, 1) + 64);
+        c.kh.alloc(4 * (m + 2) + 8);
+        c.kpart.alloc((size_t)2 * (m + 2) * std::max(c.nchunk_loc, 1) + 64);
+        c.seg_part.alloc((size_t)2 * (m + 2) * std::max(c.nseg_max, 1) + 64);
         c.kcap = m;
     }
-    Kr K(c, m + 2);
+    Kr K(c, 2 * (m + 2));
     double *V = c.V, *Z = c.Z, *r = c.kr;
-    double *dh = c.kh;                // [0, m+2): h column; [m+2, 2m+4): second pass; then scalars
-    double *dh2 = dh + (m + 2), *dsc = dh + 2 * (m + 2);
+    // device scalars: d = pass-1 dots [0, 2(j+1)), then alpha, h_j, rho right behind them
+    double *dh = c.kh;
     cudaEvent_t e0, e1;
     TSP_CUDA(cudaEventCreate(&e0)); TSP_CUDA(cudaEventCreate(&e1));
     TSP_CUDA(cudaEventRecord(e0, c.s));
 
-    std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), yv(m), col(m + 2);
+    Hess H(m);
+    std::vector<double> yv(m), col(2 * (m + 2) + 8);
     double bn;
-    K.norm(b, dsc);
-    TSP_CUDA(cudaMemcpyAsync(&bn, dsc, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+    K.norm(b, dh);
+    TSP_CUDA(cudaMemcpyAsync(&bn, dh, sizeof(double), cudaMemcpyDeviceToHost, c.s));
     TSP_CUDA(cudaStreamSynchronize(c.s));
     TSP_REQUIRE(std::isfinite(bn), TSP_ERR_NUMERIC, "non-finite ||b||");
     if (o.x0_zero && n) TSP_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, c.s));
@@ -335,61 +428,72 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
             op_apply(c, x, r);                         // r = b - A x ; beta = ||r||
             k_bminus<<<K.nblk, KB, 0, c.s>>>(n, b, r);
             c.launches++;
-            K.norm(r, dsc);
+            K.norm(r, dh);
             double beta;
-            TSP_CUDA(cudaMemcpyAsync(&beta, dsc, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+            TSP_CUDA(cudaMemcpyAsync(&beta, dh, sizeof(double), cudaMemcpyDeviceToHost, c.s));
             TSP_CUDA(cudaStreamSynchronize(c.s));
             TSP_REQUIRE(std::isfinite(beta), TSP_ERR_NUMERIC, "non-finite residual norm");
             info.true_relres = beta / bn;
             if (beta <= o.rtol * bn) { status = TSP_OK; break; }
             if (it >= o.max_iters) { status = TSP_NOT_CONVERGED; break; }
             if (it > 0) info.restarts++;
-            K.scale_inv(dsc, r, V);
-            std::fill(g.begin(), g.end(), 0.0);
-            g[0] = beta;
+            K.scale_inv(dh, r, V);                     // u_0 = r / beta
+            H.reset(beta);
             int k = 0;
+            double rho_prev = 0.0;
+            bool lucky = false;
             for (int j = 0; j < m; ++j) {
-                double *vj = V + (size_t)j * ld, *zj = Z + (size_t)j * ld, *w = V + (size_t)(j + 1) * ld;
-                prec_apply(c, vj, zj);                 // z_j = M^-1 v_j (Algorithm 1)
+                double *uj = V + (size_t)j * ld, *zj = Z + (size_t)j * ld, *w = V + (size_t)(j + 1) * ld;
+                double *d = dh, *sc = dh + 2 * (j + 1), *rho = sc + 2;
+                prec_apply(c, uj, zj);                 // z_j = M^-1 u_j (Algorithm 1)
                 op_apply(c, zj, w);                    // w = A z_j
-                // CGS2 (DESIGN.md R-krylov).  A DGKS-selective second pass was measured to be needed
-                // in 99% of the iterations here (the new direction is nearly in the Krylov space), so the
-                // projection is always repeated; the first update is fused with the second projection.
-                K.mdot(V, j + 1, w, dh);
-                K.maxpy_mdot(V, j + 1, dh, w, dh2);
-                K.maxpy_norm(V, j + 1, dh2, w, dh + j + 1);
-                k_add_into<<<1, 128, 0, c.s>>>(j + 1, dh2, dh);
-                c.launches++;
-                info.reorth++;
-                TSP_CUDA(cudaMemcpyAsync(col.data(), dh, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, c.s));
+                K.mdot2(V, j, w, d, sc);               // [V_{j-1} u_j]^T [u_j w], alpha_j, h_j
+                K.dcgs_update(V, j, d, sc, w, rho);    // v_j, w -> w - V_j h, rho = ||w||
+                TSP_CUDA(cudaMemcpyAsync(col.data(), dh, sizeof(double) * (2 * (j + 1) + 3), cudaMemcpyDeviceToHost, c.s));
                 TSP_CUDA(cudaStreamSynchronize(c.s));
-                const double hn = col[j + 1];
-                TSP_REQUIRE(std::isfinite(hn), TSP_ERR_NUMERIC, "non-finite Arnoldi norm");
-                if (hn != 0.0) K.scale_inv(dh + j + 1, w, w);
-                for (int i = 0; i <= j + 1; ++i) H[(size_t)j * (m + 1) + i] = col[i];
-                for (int i = 0; i < j; ++i) {
-                    double a = H[(size_t)j * (m + 1) + i], cc = H[(size_t)j * (m + 1) + i + 1];
-                    H[(size_t)j * (m + 1) + i] = cs[i] * a + sn[i] * cc;
-                    H[(size_t)j * (m + 1) + i + 1] = -sn[i] * a + cs[i] * cc;
+                const double *dd = col.data(), alpha = dd[2 * (j + 1)], hj = dd[2 * (j + 1) + 1], rj = dd[2 * (j + 1) + 2];
+                TSP_REQUIRE(std::isfinite(alpha) && std::isfinite(hj) && std::isfinite(rj), TSP_ERR_NUMERIC,
+                            "non-finite Arnoldi coefficients (loss of orthogonality)");
+                info.reorth++;
+                if (j > 0) H.complete(j - 1, rho_prev, dd, alpha);   // column j-1 now exact
+                else {                                                  // u_0 = r/beta: v_0 = u_0/alpha
+                    H.g[0] = H.gin[0] = beta * alpha;
                 }
-                double a = H[(size_t)j * (m + 1) + j], cc = H[(size_t)j * (m + 1) + j + 1];
-                double rho = std::hypot(a, cc);
-                cs[j] = a / rho; sn[j] = cc / rho;
-                H[(size_t)j * (m + 1) + j] = rho; H[(size_t)j * (m + 1) + j + 1] = 0.0;
-                g[j + 1] = -sn[j] * g[j]; g[j] = cs[j] * g[j];
+                H.raw[j].assign(j + 2, 0.0);
+                for (int t = 0; t < j; ++t) H.raw[j][t] = dd[j + 1 + t];
+                H.raw[j][j] = hj;
+                H.raw[j][j + 1] = rj;                  // provisional: u_{j+1} taken as v_{j+1}
+                H.rotate(j);
+                rho_prev = rj;
+                if (rj != 0.0) K.scale_inv(rho, w, w); // u_{j+1} = w / rho
                 ++it; k = j + 1;
-                info.est_relres = std::fabs(g[j + 1]) / bn;
-                if (std::fabs(g[j + 1]) <= o.rtol * bn || it >= o.max_iters || hn == 0.0) break;
+                info.est_relres = std::fabs(H.g[j + 1]) / bn;
+                if (rj == 0.0) { lucky = true; break; }
+                if (std::fabs(H.g[j + 1]) <= o.rtol * bn || it >= o.max_iters) break;
+            }
+            // complete the last column: one projection of u_k against V_0..V_{k-1} (+ u_k . u_k)
+            if (!lucky) {
+                K.mdot(V, k + 1, V + (size_t)k * ld, dh);
+                TSP_CUDA(cudaMemcpyAsync(col.data(), dh, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, c.s));
+                TSP_CUDA(cudaStreamSynchronize(c.s));
+                double ss = 0.0;
+                for (int t = 0; t < k; ++t) ss = std::fma(col[t], col[t], ss);
+                const double a2 = col[k] - ss;
+                TSP_REQUIRE(a2 > 0.0 && std::isfinite(a2), TSP_ERR_NUMERIC, "loss of orthogonality in the last Arnoldi vector");
+                H.complete(k - 1, rho_prev, col.data(), std::sqrt(a2));
+                info.est_relres = std::fabs(H.g[k]) / bn;
             }
             for (int i = k - 1; i >= 0; --i) {
-                double s = g[i];
-                for (int t = i + 1; t < k; ++t) s -= H[(size_t)t * (m + 1) + i] * yv[t];
-                yv[i] = s / H[(size_t)i * (m + 1) + i];
+                double sacc = H.g[i];
+                for (int t = i + 1; t < k; ++t) sacc -= H.rot[t][i] * yv[t];
+                yv[i] = sacc / H.rot[i][i];
             }
-            TSP_CUDA(cudaMemcpyAsync(dh2, yv.data(), sizeof(double) * k, cudaMemcpyHostToDevice, c.s));
+            double *dy = dh + 2 * (m + 2) + 4;
+            TSP_CUDA(cudaMemcpyAsync(dy, yv.data(), sizeof(double) * k, cudaMemcpyHostToDevice, c.s));
             prof_begin(c, PK_AXPY);
-            k_update<<<K.nblk, KB, 0, c.s>>>(n, k, Z, ld, dh2, x);
+            k_update<<<K.nblk, KB, 0, c.s>>>(n, k, Z, ld, dy, x);
             prof_end(c, PK_AXPY, 8.0 * n * (k + 2));
+            K.bytes += 8.0 * n * (k + 2);
             c.launches++;
         }
     }
@@ -401,6 +505,7 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
     info.iterations = it;
     info.status = status;
     info.t_solve_s = ms * 1e-3;
+    info.bytes_krylov = K.bytes;
 }
 
 }  // namespace tsp

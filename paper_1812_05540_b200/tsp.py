@@ -51,7 +51,7 @@ class tsp_solve_opts(C.Structure):
 class tsp_solve_info(C.Structure):
     _fields_ = [("iterations", C.c_int), ("restarts", C.c_int), ("status", C.c_int),
                 ("est_relres", C.c_double), ("true_relres", C.c_double), ("t_solve_s", C.c_double),
-                ("reorth", C.c_int)]
+                ("reorth", C.c_int), ("bytes_krylov", C.c_double)]
 
 
 class tsp_stats(C.Structure):
@@ -101,7 +101,7 @@ def lib():
         L.tsp_local_world_destroy.restype = None
         L.tsp_partition.argtypes = [C.c_int] * 6 + [_P(C.c_int64)]
         L.tsp_level_dist.argtypes = [C.c_void_p, C.c_int, C.c_int, _P(C.c_int64)]
-        if L.tsp_abi_version() != 1:
+        if L.tsp_abi_version() != 2:
             raise RuntimeError("libtsp ABI version mismatch")
         _LIB = L
     return _LIB
@@ -246,7 +246,7 @@ class Tsp:
         _check(rc, "tsp_solve", ok=(0, 1))
         return dict(iterations=info.iterations, restarts=info.restarts, status=STATUS.get(info.status, info.status),
                     est_relres=info.est_relres, true_relres=info.true_relres, t_solve_s=info.t_solve_s,
-                    reorth=info.reorth)
+                    reorth=info.reorth, bytes_krylov=info.bytes_krylov)
 
     def stats(self):
         s = tsp_stats()

@@ -304,6 +304,174 @@ __global__ void __launch_bounds__(KB) maxpy_mdot2(int nv, const double *__restri
     }
 }
 
+template <int NV>
+__device__ __forceinline__ double block_sum_multi(double (&d)[NV], double (*red)[NV])
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int h = NV / 2, m = 1; h >= 1; h >>= 1, m <<= 1) {
+        const bool up = lane & m;
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+            const double snd = up ? d[i] : d[i + h], kp = up ? d[i + h] : d[i];
+            d[i] = kp + __shfl_xor_sync(0xffffffffu, snd, m);
+        }
+    }
+    double x = d[0];
+#pragma unroll
+    for (int o = NV; o < 32; o <<= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    int idx = 0;
+#pragma unroll
+    for (int b = 1, t = NV / 2; b < NV; b <<= 1, t >>= 1) if (lane & b) idx |= t;
+    if (lane < NV) red[wid][idx] = x;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x < NV)
+        for (int u = 0; u < KB / 32; ++u) s += red[u][threadIdx.x];
+    __syncthreads();
+    return s;
+}
+template <int G, int U>
+__global__ void __launch_bounds__(KB) mdot2(int nv, const double *__restrict__ V, long ldv, const double *__restrict__ u,
+                                            const double *__restrict__ w, long CH, long n, double *__restrict__ part, int cmax)
+{
+    __shared__ double us[2048], ws[2048];
+    __shared__ double red[KB / 32][2 * G];
+    const int k = blockIdx.x;
+    const long beg = k * CH;
+    const int len = (int)(min(n, beg + CH) - beg);
+    for (int i = threadIdx.x; i < len; i += KB) { us[i] = __ldcs(u + beg + i); ws[i] = __ldcs(w + beg + i); }
+    __syncthreads();
+    for (int v0 = 0; v0 < nv; v0 += G) {
+        const int cnt = min(G, nv - v0);
+        const double *Vg = V + v0 * ldv + beg;
+        double acc[2 * G];
+#pragma unroll
+        for (int t = 0; t < 2 * G; ++t) acc[t] = 0.0;
+        int i = threadIdx.x;
+        for (; i + (U - 1) * KB < len; i += U * KB) {
+#pragma unroll
+            for (int t = 0; t < G; ++t)
+                if (t < cnt) {
+#pragma unroll
+                    for (int q = 0; q < U; ++q) {
+                        const double vv = __ldcs(Vg + t * ldv + i + q * KB);
+                        acc[t] = fma(vv, us[i + q * KB], acc[t]);
+                        acc[G + t] = fma(vv, ws[i + q * KB], acc[G + t]);
+                    }
+                }
+        }
+        for (; i < len; i += KB) {
+#pragma unroll
+            for (int t = 0; t < G; ++t)
+                if (t < cnt) {
+                    const double vv = __ldcs(Vg + t * ldv + i);
+                    acc[t] = fma(vv, us[i], acc[t]);
+                    acc[G + t] = fma(vv, ws[i], acc[G + t]);
+                }
+        }
+        const double s = block_sum_multi<2 * G>(acc, red);
+        const int q = threadIdx.x;
+        if (q < 2 * G && (q % G) < cnt) part[(long)((q < G ? 0 : nv) + v0 + q % G) * cmax + k] = s;
+    }
+}
+
+// interleaved staging {u_i, w_i}
+template <int G, int U>
+__global__ void __launch_bounds__(KB) mdot2i(int nv, const double *__restrict__ V, long ldv, const double *__restrict__ u,
+                                             const double *__restrict__ w, long CH, long n, double *__restrict__ part, int cmax)
+{
+    __shared__ double2 uw[2048];
+    __shared__ double red[KB / 32][2 * G];
+    const int k = blockIdx.x;
+    const long beg = k * CH;
+    const int len = (int)(min(n, beg + CH) - beg);
+    for (int i = threadIdx.x; i < len; i += KB) uw[i] = make_double2(__ldcs(u + beg + i), __ldcs(w + beg + i));
+    __syncthreads();
+    for (int v0 = 0; v0 < nv; v0 += G) {
+        const int cnt = min(G, nv - v0);
+        const double *Vg = V + v0 * ldv + beg;
+        double acc[2 * G];
+#pragma unroll
+        for (int t = 0; t < 2 * G; ++t) acc[t] = 0.0;
+        int i = threadIdx.x;
+        for (; i + (U - 1) * KB < len; i += U * KB) {
+            double2 x[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) x[q] = uw[i + q * KB];
+#pragma unroll
+            for (int t = 0; t < G; ++t)
+                if (t < cnt) {
+#pragma unroll
+                    for (int q = 0; q < U; ++q) {
+                        const double vv = __ldcs(Vg + t * ldv + i + q * KB);
+                        acc[t] = fma(vv, x[q].x, acc[t]);
+                        acc[G + t] = fma(vv, x[q].y, acc[G + t]);
+                    }
+                }
+        }
+        for (; i < len; i += KB) {
+            const double2 x = uw[i];
+#pragma unroll
+            for (int t = 0; t < G; ++t)
+                if (t < cnt) {
+                    const double vv = __ldcs(Vg + t * ldv + i);
+                    acc[t] = fma(vv, x.x, acc[t]);
+                    acc[G + t] = fma(vv, x.y, acc[G + t]);
+                }
+        }
+        const double s = block_sum_multi<2 * G>(acc, red);
+        const int q = threadIdx.x;
+        if (q < 2 * G && (q % G) < cnt) part[(long)((q < G ? 0 : nv) + v0 + q % G) * cmax + k] = s;
+    }
+}
+// no staging: u, w through L1
+template <int G, int U>
+__global__ void __launch_bounds__(KB) mdot2n(int nv, const double *__restrict__ V, long ldv, const double *__restrict__ u,
+                                             const double *__restrict__ w, long CH, long n, double *__restrict__ part, int cmax)
+{
+    __shared__ double red[KB / 32][2 * G];
+    const int k = blockIdx.x;
+    const long beg = k * CH;
+    const int len = (int)(min(n, beg + CH) - beg);
+    for (int v0 = 0; v0 < nv; v0 += G) {
+        const int cnt = min(G, nv - v0);
+        const double *Vg = V + v0 * ldv + beg;
+        double acc[2 * G];
+#pragma unroll
+        for (int t = 0; t < 2 * G; ++t) acc[t] = 0.0;
+        int i = threadIdx.x;
+        for (; i + (U - 1) * KB < len; i += U * KB) {
+            double xu[U], xw[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) { xu[q] = __ldg(u + beg + i + q * KB); xw[q] = __ldg(w + beg + i + q * KB); }
+#pragma unroll
+            for (int t = 0; t < G; ++t)
+                if (t < cnt) {
+#pragma unroll
+                    for (int q = 0; q < U; ++q) {
+                        const double vv = __ldcs(Vg + t * ldv + i + q * KB);
+                        acc[t] = fma(vv, xu[q], acc[t]);
+                        acc[G + t] = fma(vv, xw[q], acc[G + t]);
+                    }
+                }
+        }
+        for (; i < len; i += KB) {
+            const double xu = __ldg(u + beg + i), xw = __ldg(w + beg + i);
+#pragma unroll
+            for (int t = 0; t < G; ++t)
+                if (t < cnt) {
+                    const double vv = __ldcs(Vg + t * ldv + i);
+                    acc[t] = fma(vv, xu, acc[t]);
+                    acc[G + t] = fma(vv, xw, acc[G + t]);
+                }
+        }
+        const double s = block_sum_multi<2 * G>(acc, red);
+        const int q = threadIdx.x;
+        if (q < 2 * G && (q % G) < cnt) part[(long)((q < G ? 0 : nv) + v0 + q % G) * cmax + k] = s;
+    }
+}
+
 __global__ void fillk(double *a, long n, double s)
 {
     for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
@@ -365,6 +533,14 @@ int main(int argc, char **argv)
         mdot_s<4, 2><<<nch, KB>>>(nv, V, n, w, CH, n, part, nch);
         cudaMemcpy(p1.data(), part, 8 * p1.size(), cudaMemcpyDeviceToHost);
         cmp("mdot_s");
+        mdot2<8, 1><<<nch, KB>>>(nv, V, n, V + (nv - 1) * n, w, CH, n, part, nch);
+        {
+            std::vector<double> p2((size_t)2 * nv * nch);
+            cudaMemcpy(p2.data(), part, 8 * p2.size(), cudaMemcpyDeviceToHost);
+            double mx = 0;
+            for (size_t i = 0; i < p0.size(); ++i) mx = fmax(mx, fabs(p2[(size_t)nv * nch + i] - p0[i]) / (fabs(p0[i]) + 1e-300));
+            printf("check mdot2 (w part) max rel diff %.3e\n", mx);
+        }
         cudaFree(w2);
     }
     timeit("copy (r+w)", 2 * vb, [&] { copyk<<<148 * 8, 256>>>(V, w, n); });
@@ -385,6 +561,24 @@ int main(int argc, char **argv)
         timeit(nm, vb * (nv + (nv + 7) / 8), [&] { mdot_s<4, 2><<<nch, KB>>>(nv, V, n, w, CH, n, part, nch); });
         snprintf(nm, 64, "mdot_s G8 U2 CH%ld", CH);
         timeit(nm, vb * (nv + (nv + 7) / 8), [&] { mdot_s<8, 2><<<nch, KB>>>(nv, V, n, w, CH, n, part, nch); });
+        snprintf(nm, 64, "mdot2 G8 U1");
+        timeit(nm, vb * (nv + 1), [&] { mdot2<8, 1><<<nch, KB>>>(nv, V, n, V + (nv - 1) * n, w, CH, n, part, nch); });
+        snprintf(nm, 64, "mdot2 G8 U2");
+        timeit(nm, vb * (nv + 1), [&] { mdot2<8, 2><<<nch, KB>>>(nv, V, n, V + (nv - 1) * n, w, CH, n, part, nch); });
+        snprintf(nm, 64, "mdot2 G4 U2");
+        timeit(nm, vb * (nv + 1), [&] { mdot2<4, 2><<<nch, KB>>>(nv, V, n, V + (nv - 1) * n, w, CH, n, part, nch); });
+        snprintf(nm, 64, "mdot2 G4 U4");
+        timeit(nm, vb * (nv + 1), [&] { mdot2<4, 4><<<nch, KB>>>(nv, V, n, V + (nv - 1) * n, w, CH, n, part, nch); });
+        snprintf(nm, 64, "mdot2i G4 U2");
+        timeit(nm, vb * (nv + 1), [&] { mdot2i<4, 2><<<nch, KB>>>(nv, V, n, V + (nv - 1) * n, w, CH, n, part, nch); });
+        snprintf(nm, 64, "mdot2i G8 U2");
+        timeit(nm, vb * (nv + 1), [&] { mdot2i<8, 2><<<nch, KB>>>(nv, V, n, V + (nv - 1) * n, w, CH, n, part, nch); });
+        snprintf(nm, 64, "mdot2n G4 U2");
+        timeit(nm, vb * (nv + 1), [&] { mdot2n<4, 2><<<nch, KB>>>(nv, V, n, V + (nv - 1) * n, w, CH, n, part, nch); });
+        snprintf(nm, 64, "mdot2n G8 U1");
+        timeit(nm, vb * (nv + 1), [&] { mdot2n<8, 1><<<nch, KB>>>(nv, V, n, V + (nv - 1) * n, w, CH, n, part, nch); });
+        snprintf(nm, 64, "mdot2 G2 U4");
+        timeit(nm, vb * (nv + 1), [&] { mdot2<2, 4><<<nch, KB>>>(nv, V, n, V + (nv - 1) * n, w, CH, n, part, nch); });
         snprintf(nm, 64, "maxpy_mdot0 CH%ld", CH);
         timeit(nm, vb * (nv + 2), [&] { maxpy_mdot0<<<nch, KB>>>(nv, V, n, h, w, CH, n, part, nch); });
         snprintf(nm, 64, "maxpy_mdot1 UL4 CH%ld", CH);
