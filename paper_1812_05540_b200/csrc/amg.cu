@@ -300,6 +300,32 @@ __global__ void k_transpose_fill(int64_t nnz, int nc, const int32_t *__restrict_
 // C = X Y; C_ik = fold over X's row i (ascending) of x_ij * y_jk, starting at 0.0.
 // One warp per row; the X row is walked sequentially (canonical order), lanes
 // split Y's row j (unique columns, so no two lanes touch one accumulator).
+// Latency: the X row's (j, x_ij, Y-row bounds) are fetched lane-parallel 32 entries at
+// a time and broadcast by shuffles, and the first 32 entries of the next Y row are
+// loaded while the current one is merged into the warp's shared-memory hash table.
+template <int NC>
+__device__ __forceinline__ void spg_insert(int k, const double *yq, const double *x, int *keys, double *acc, int HS, bool fill,
+                                           int &nfull)
+{
+    unsigned h = ((unsigned)k * 2654435761u) & (HS - 1);
+    int probes = 0;
+    for (;;) {
+        const int old = atomicCAS(&keys[h], -1, k);
+        if (old == -1) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) acc[h * NC + c] = 0.0;
+            break;
+        }
+        if (old == k) break;
+        h = (h + 1) & (HS - 1);
+        if (++probes >= HS) { nfull = 1; return; }
+    }
+    if (fill) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[h * NC + c] = __dadd_rn(acc[h * NC + c], __dmul_rn(x[c], yq[c]));
+    }
+}
+
 template <int NC, int HS>
 __global__ void k_spgemm(int n, const int32_t *__restrict__ xrp, const int32_t *__restrict__ xci, const double *__restrict__ xv,
                          const int32_t *__restrict__ yrp, const int32_t *__restrict__ yci, const double *__restrict__ yv,
@@ -313,33 +339,61 @@ __global__ void k_spgemm(int n, const int32_t *__restrict__ xrp, const int32_t *
         for (int t = lane; t < HS; t += 32) keys[t] = -1;
         __syncwarp();
         int nfull = 0;
-        for (int64_t q = xrp[i]; q < xrp[i + 1]; ++q) {
-            const int j = xci[q];
-            double xq[NC];
+        const int q0 = xrp[i], q1 = xrp[i + 1];
+        for (int qb = q0; qb < q1 && !nfull; qb += 32) {
+            const int nb = min(32, q1 - qb);
+            int ysl = 0, yel = 0;
+            double xl[NC];
 #pragma unroll
-            for (int c = 0; c < NC; ++c) xq[c] = xv[q * NC + c];
-            for (int64_t p = yrp[j] + lane; p < yrp[j + 1]; p += 32) {
-                const int k = yci[p];
-                unsigned h = ((unsigned)k * 2654435761u) & (HS - 1);
-                int probes = 0;
-                for (;;) {
-                    int old = atomicCAS(&keys[h], -1, k);
-                    if (old == -1) {
+            for (int c = 0; c < NC; ++c) xl[c] = 0.0;
+            if (lane < nb) {
+                const int j = xci[qb + lane];
+                ysl = yrp[j]; yel = yrp[j + 1];
+                if (fill)
 #pragma unroll
-                        for (int c = 0; c < NC; ++c) acc[h * NC + c] = 0.0;
-                        break;
-                    }
-                    if (old == k) break;
-                    h = (h + 1) & (HS - 1);
-                    if (++probes >= HS) { nfull = 1; break; }
-                }
-                if (nfull) break;
-                if (fill) {
-#pragma unroll
-                    for (int c = 0; c < NC; ++c) acc[h * NC + c] = __dadd_rn(acc[h * NC + c], __dmul_rn(xq[c], yv[p * NC + c]));
-                }
+                    for (int c = 0; c < NC; ++c) xl[c] = xv[(int64_t)(qb + lane) * NC + c];
             }
-            __syncwarp();
+            // first chunk of Y row t (prefetched one step ahead)
+            int ys = __shfl_sync(0xffffffffu, ysl, 0), ye = __shfl_sync(0xffffffffu, yel, 0);
+            int ck = -1;
+            double cy[NC];
+            if (ys + lane < ye) {
+                ck = yci[ys + lane];
+                if (fill)
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) cy[c] = yv[(int64_t)(ys + lane) * NC + c];
+            }
+            for (int t = 0; t < nb; ++t) {
+                double x[NC];
+#pragma unroll
+                for (int c = 0; c < NC; ++c) x[c] = __shfl_sync(0xffffffffu, xl[c], t);
+                const int cys = ys, cye = ye;
+                // prefetch row t+1
+                int nk = -1;
+                double ny[NC];
+                if (t + 1 < nb) {
+                    ys = __shfl_sync(0xffffffffu, ysl, t + 1); ye = __shfl_sync(0xffffffffu, yel, t + 1);
+                    if (ys + lane < ye) {
+                        nk = yci[ys + lane];
+                        if (fill)
+#pragma unroll
+                            for (int c = 0; c < NC; ++c) ny[c] = yv[(int64_t)(ys + lane) * NC + c];
+                    }
+                }
+                if (ck >= 0) spg_insert<NC>(ck, cy, x, keys, acc, HS, fill, nfull);
+                for (int p = cys + 32 + lane; p < cye && !nfull; p += 32) {
+                    double yq[NC];
+                    if (fill)
+#pragma unroll
+                        for (int c = 0; c < NC; ++c) yq[c] = yv[(int64_t)p * NC + c];
+                    spg_insert<NC>(yci[p], yq, x, keys, acc, HS, fill, nfull);
+                }
+                __syncwarp();
+                ck = nk;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) cy[c] = ny[c];
+            }
+            nfull = __any_sync(0xffffffffu, nfull);
         }
         // count occupied slots
         int mine = 0;
@@ -451,12 +505,12 @@ static void spgemm(Ctx &c, const Csr &X, const Csr &Y, Csr &C, int nc)
     C.n = X.n; C.m = Y.m; C.nc = nc;
     DBuf<int32_t> cnt; cnt.alloc(X.n + 1);
     DBuf<int> ovf; ovf.alloc(1);
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    for (int attempt = 0; attempt < 3; ++attempt) {
         ovf.zero(c.s);
-        const int HS = attempt == 0 ? 512 : 4096;
-        const int wpb = attempt == 0 ? 4 : 1;
+        const int HS = attempt == 0 ? 128 : attempt == 1 ? 512 : 4096;
+        const int wpb = attempt == 0 ? 8 : attempt == 1 ? 4 : 1;
         size_t smem = (size_t)wpb * HS * (sizeof(int) + sizeof(double) * nc);
-        int grid = std::max(1, std::min(grid_for(X.n, wpb), c.sm_count * 32));
+        int grid = std::max(1, std::min(grid_for(X.n, wpb), c.sm_count * 64));
         auto launch = [&](int fill) {
 #define SPG(NCV, HSV)                                                                                                     \
     do {                                                                                                                  \
@@ -464,8 +518,10 @@ static void spgemm(Ctx &c, const Csr &X, const Csr &Y, Csr &C, int nc)
         k_spgemm<NCV, HSV><<<grid, 32 * wpb, smem, c.s>>>(X.n, X.rp, X.ci, X.v, Y.rp, Y.ci, Y.v, fill, cnt, C.rp, C.ci,   \
                                                           C.v, ovf);                                                      \
     } while (0)
-            if (nc == 1 && HS == 512) SPG(1, 512);
+            if (nc == 1 && HS == 128) SPG(1, 128);
+            else if (nc == 1 && HS == 512) SPG(1, 512);
             else if (nc == 1) SPG(1, 4096);
+            else if (HS == 128) SPG(3, 128);
             else if (HS == 512) SPG(3, 512);
             else SPG(3, 4096);
 #undef SPG
