@@ -199,6 +199,10 @@ tsp_status tsp_level_dist(tsp_handle h, int which, int lvl, int64_t out3[3]);
 
 tsp_status tsp_prof_enable(tsp_handle h, int on);   /* also resets */
 tsp_status tsp_prof_read(tsp_handle h, tsp_prof *p);  /* synchronises */
+/* restrict recording to the classes in `mask` (bit k = class k of tsp_prof.name; default all):
+ * two timing events per recorded launch cost ~2 % of an FGMRES iteration, so a timed run records
+ * only the class whose roofline it reports */
+tsp_status tsp_prof_classes(tsp_handle h, unsigned mask);
 
 void tsp_destroy(tsp_handle h);
 

@@ -326,85 +326,92 @@ __device__ __forceinline__ void spg_insert(int k, const double *yq, const double
     }
 }
 
-template <int NC, int HS>
+// G lanes per row (G | 32): a group walks its X row in order, its lanes split each Y row.
+// G < 32 when Y's rows are short (A P: P has ~4 entries per row), so several rows share a warp.
+template <int NC, int G, int HS>
 __global__ void k_spgemm(int n, const int32_t *__restrict__ xrp, const int32_t *__restrict__ xci, const double *__restrict__ xv,
                          const int32_t *__restrict__ yrp, const int32_t *__restrict__ yci, const double *__restrict__ yv,
                          int fill, int32_t *cnt, const int32_t *__restrict__ crp, int32_t *cci, double *cv, int *overflow)
 {
     extern __shared__ unsigned char smraw[];
-    const int wpb = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int *keys = (int *)smraw + w * HS;
-    double *acc = (double *)(smraw + (size_t)wpb * HS * sizeof(int)) + (size_t)w * HS * NC;
-    for (int i = blockIdx.x * wpb + w; i < n; i += gridDim.x * wpb) {
-        for (int t = lane; t < HS; t += 32) keys[t] = -1;
-        __syncwarp();
+    constexpr int GPW = 32 / G;                     // groups (rows) per warp
+    const int lane = threadIdx.x & 31, sub = lane & (G - 1), gid = lane / G;
+    const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1) << (gid * G));
+    const int ngroups = blockDim.x / G, grp = threadIdx.x / G;
+    // per-group tables padded by one word / one double so the groups of a warp hit different banks
+    int *keys = (int *)smraw + grp * (HS + 1);
+    double *acc = (double *)(smraw + (((size_t)ngroups * (HS + 1) * sizeof(int) + 15) & ~(size_t)15)) + (size_t)grp * (HS * NC + 1);
+    (void)GPW;
+    for (int i = blockIdx.x * ngroups + grp; i < n; i += gridDim.x * ngroups) {
+        for (int t = sub; t < HS; t += G) keys[t] = -1;
+        __syncwarp(gmask);
         int nfull = 0;
         const int q0 = xrp[i], q1 = xrp[i + 1];
-        for (int qb = q0; qb < q1 && !nfull; qb += 32) {
-            const int nb = min(32, q1 - qb);
+        for (int qb = q0; qb < q1 && !nfull; qb += G) {
+            const int nb = min(G, q1 - qb);
             int ysl = 0, yel = 0;
             double xl[NC];
 #pragma unroll
             for (int c = 0; c < NC; ++c) xl[c] = 0.0;
-            if (lane < nb) {
-                const int j = xci[qb + lane];
+            if (sub < nb) {
+                const int j = xci[qb + sub];
                 ysl = yrp[j]; yel = yrp[j + 1];
                 if (fill)
 #pragma unroll
-                    for (int c = 0; c < NC; ++c) xl[c] = xv[(int64_t)(qb + lane) * NC + c];
+                    for (int c = 0; c < NC; ++c) xl[c] = xv[(int64_t)(qb + sub) * NC + c];
             }
             // first chunk of Y row t (prefetched one step ahead)
-            int ys = __shfl_sync(0xffffffffu, ysl, 0), ye = __shfl_sync(0xffffffffu, yel, 0);
+            int ys = __shfl_sync(gmask, ysl, 0, G), ye = __shfl_sync(gmask, yel, 0, G);
             int ck = -1;
             double cy[NC];
-            if (ys + lane < ye) {
-                ck = yci[ys + lane];
+            if (ys + sub < ye) {
+                ck = yci[ys + sub];
                 if (fill)
 #pragma unroll
-                    for (int c = 0; c < NC; ++c) cy[c] = yv[(int64_t)(ys + lane) * NC + c];
+                    for (int c = 0; c < NC; ++c) cy[c] = yv[(int64_t)(ys + sub) * NC + c];
             }
             for (int t = 0; t < nb; ++t) {
                 double x[NC];
 #pragma unroll
-                for (int c = 0; c < NC; ++c) x[c] = __shfl_sync(0xffffffffu, xl[c], t);
+                for (int c = 0; c < NC; ++c) x[c] = __shfl_sync(gmask, xl[c], t, G);
                 const int cys = ys, cye = ye;
-                // prefetch row t+1
                 int nk = -1;
                 double ny[NC];
                 if (t + 1 < nb) {
-                    ys = __shfl_sync(0xffffffffu, ysl, t + 1); ye = __shfl_sync(0xffffffffu, yel, t + 1);
-                    if (ys + lane < ye) {
-                        nk = yci[ys + lane];
+                    ys = __shfl_sync(gmask, ysl, t + 1, G); ye = __shfl_sync(gmask, yel, t + 1, G);
+                    if (ys + sub < ye) {
+                        nk = yci[ys + sub];
                         if (fill)
 #pragma unroll
-                            for (int c = 0; c < NC; ++c) ny[c] = yv[(int64_t)(ys + lane) * NC + c];
+                            for (int c = 0; c < NC; ++c) ny[c] = yv[(int64_t)(ys + sub) * NC + c];
                     }
                 }
                 if (ck >= 0) spg_insert<NC>(ck, cy, x, keys, acc, HS, fill, nfull);
-                for (int p = cys + 32 + lane; p < cye && !nfull; p += 32) {
+                for (int p = cys + G + sub; p < cye && !nfull; p += G) {
                     double yq[NC];
                     if (fill)
 #pragma unroll
                         for (int c = 0; c < NC; ++c) yq[c] = yv[(int64_t)p * NC + c];
                     spg_insert<NC>(yci[p], yq, x, keys, acc, HS, fill, nfull);
                 }
-                __syncwarp();
+                __syncwarp(gmask);
                 ck = nk;
 #pragma unroll
                 for (int c = 0; c < NC; ++c) cy[c] = ny[c];
             }
-            nfull = __any_sync(0xffffffffu, nfull);
+            nfull = __any_sync(gmask, nfull);
         }
         // count occupied slots
         int mine = 0;
-        for (int t = lane; t < HS; t += 32) mine += keys[t] >= 0;
-        for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-        if (__any_sync(0xffffffffu, nfull) || mine > (HS * 3) / 4) { if (lane == 0) *overflow = 1; }
+        for (int t = sub; t < HS; t += G) mine += keys[t] >= 0;
+#pragma unroll
+        for (int o = G / 2; o; o >>= 1) mine += __shfl_xor_sync(gmask, mine, o, G);
+        if (__any_sync(gmask, nfull) || mine > (HS * 3) / 4) { if (sub == 0) *overflow = 1; }
         if (!fill) {
-            if (lane == 0) cnt[i] = mine;
+            if (sub == 0) cnt[i] = mine;
         } else {
             const int64_t base = crp[i];
-            for (int t = lane; t < HS; t += 32) {
+            for (int t = sub; t < HS; t += G) {
                 int k = keys[t];
                 if (k < 0) continue;
                 int rank = 0;
@@ -414,7 +421,7 @@ __global__ void k_spgemm(int n, const int32_t *__restrict__ xrp, const int32_t *
                 for (int c = 0; c < NC; ++c) cv[(base + rank) * NC + c] = acc[t * NC + c];
             }
         }
-        __syncwarp();
+        __syncwarp(gmask);
     }
 }
 
@@ -505,25 +512,37 @@ static void spgemm(Ctx &c, const Csr &X, const Csr &Y, Csr &C, int nc)
     C.n = X.n; C.m = Y.m; C.nc = nc;
     DBuf<int32_t> cnt; cnt.alloc(X.n + 1);
     DBuf<int> ovf; ovf.alloc(1);
+    // lanes per row from Y's mean row length; attempts grow the per-row hash table on overflow
+    const double ymean = Y.n ? (double)Y.nnz / Y.n : 0.0;
+    // (measured at C5: 4 lanes per row halve the scalar A P; with 3 value sets the per-row tables limit
+    //  occupancy and a full warp per row is faster)
+    const int G0 = nc == 3 ? 32 : ymean <= 4.0 ? 4 : ymean <= 8.0 ? 8 : 32;
     for (int attempt = 0; attempt < 3; ++attempt) {
         ovf.zero(c.s);
-        const int HS = attempt == 0 ? 128 : attempt == 1 ? 512 : 4096;
-        const int wpb = attempt == 0 ? 8 : attempt == 1 ? 4 : 1;
-        size_t smem = (size_t)wpb * HS * (sizeof(int) + sizeof(double) * nc);
-        int grid = std::max(1, std::min(grid_for(X.n, wpb), c.sm_count * 64));
+        const int G = attempt == 0 ? G0 : 32;
+        const int HS = attempt == 0 ? (G0 < 32 ? 64 : 128) : attempt == 1 ? 512 : 4096;
+        const int threads = attempt == 2 ? 32 : attempt == 1 ? 128 : 256;
+        const int groups = threads / G;
+        size_t smem = (((size_t)groups * (HS + 1) * sizeof(int) + 15) & ~(size_t)15) + (size_t)groups * (HS * nc + 1) * sizeof(double);
+        int grid = std::max(1, std::min((int)((X.n + groups - 1) / groups), c.sm_count * 64));
         auto launch = [&](int fill) {
-#define SPG(NCV, HSV)                                                                                                     \
+#define SPG(NCV, GV_, HSV)                                                                                                \
     do {                                                                                                                  \
-        cudaFuncSetAttribute(k_spgemm<NCV, HSV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                 \
-        k_spgemm<NCV, HSV><<<grid, 32 * wpb, smem, c.s>>>(X.n, X.rp, X.ci, X.v, Y.rp, Y.ci, Y.v, fill, cnt, C.rp, C.ci,   \
-                                                          C.v, ovf);                                                      \
+        cudaFuncSetAttribute(k_spgemm<NCV, GV_, HSV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
+        k_spgemm<NCV, GV_, HSV><<<grid, threads, smem, c.s>>>(X.n, X.rp, X.ci, X.v, Y.rp, Y.ci, Y.v, fill, cnt, C.rp,     \
+                                                              C.ci, C.v, ovf);                                            \
     } while (0)
-            if (nc == 1 && HS == 128) SPG(1, 128);
-            else if (nc == 1 && HS == 512) SPG(1, 512);
-            else if (nc == 1) SPG(1, 4096);
-            else if (HS == 128) SPG(3, 128);
-            else if (HS == 512) SPG(3, 512);
-            else SPG(3, 4096);
+#define SPG_NC(NCV)                                                                                                       \
+    do {                                                                                                                  \
+        if (attempt == 0 && G == 4) SPG(NCV, 4, 64);                                                                      \
+        else if (attempt == 0 && G == 8) SPG(NCV, 8, 64);                                                                 \
+        else if (attempt == 0) SPG(NCV, 32, 128);                                                                         \
+        else if (attempt == 1) SPG(NCV, 32, 512);                                                                         \
+        else SPG(NCV, 32, 4096);                                                                                          \
+    } while (0)
+            if (nc == 1) SPG_NC(1);
+            else SPG_NC(3);
+#undef SPG_NC
 #undef SPG
             TSP_CUDA(cudaGetLastError());
             c.launches++;

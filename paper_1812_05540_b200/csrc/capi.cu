@@ -49,7 +49,7 @@ void prof_begin(Ctx &c, int cls)
 {
     Prof &p = c.prof;
     p.open = false;
-    if (!p.on) return;
+    if (!p.on || !((p.mask >> cls) & 1u)) return;
     if (p.next + 2 > (int)p.pool.size()) {
         if (p.pool.size() >= (1u << 22)) return;
         size_t old = p.pool.size();
@@ -365,6 +365,13 @@ tsp_status tsp_prof_enable(tsp_handle h, int on)
     p.on = on != 0;
     h->launches = 0;
     API_END
+}
+
+tsp_status tsp_prof_classes(tsp_handle h, unsigned mask)
+{
+    if (!h) { set_error("null handle"); return TSP_ERR_INVALID_ARG; }
+    h->prof.mask = mask;
+    return TSP_OK;
 }
 
 tsp_status tsp_prof_read(tsp_handle h, tsp_prof *out)

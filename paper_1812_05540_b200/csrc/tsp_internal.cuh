@@ -172,6 +172,7 @@ enum ProfClass {
 
 struct Prof {
     bool on = false;
+    unsigned mask = ~0u;             // classes recorded while on (tsp_prof_classes)
     std::vector<cudaEvent_t> pool;
     struct Rec { int cls; int e0, e1; double bytes; };
     std::vector<Rec> recs;

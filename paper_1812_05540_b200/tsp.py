@@ -91,6 +91,7 @@ def lib():
         L.tsp_level_sizes.argtypes = [C.c_void_p, C.c_int, C.c_int, _P(C.c_int64)]
         L.tsp_export_level.argtypes = [C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 8
         L.tsp_prof_enable.argtypes = [C.c_void_p, C.c_int]
+        L.tsp_prof_classes.argtypes = [C.c_void_p, C.c_uint]
         L.tsp_prof_read.argtypes = [C.c_void_p, _P(tsp_prof)]
         L.tsp_destroy.argtypes = [C.c_void_p]
         L.tsp_destroy.restype = None
@@ -110,7 +111,7 @@ def lib():
 EXPORTED = ["tsp_abi_version", "tsp_last_error", "tsp_default_options", "tsp_create", "tsp_setup",
             "tsp_apply_preconditioner", "tsp_apply_operator", "tsp_solve", "tsp_default_solve_opts",
             "tsp_get_stats", "tsp_level_sizes", "tsp_export_level", "tsp_prof_enable", "tsp_prof_read",
-            "tsp_destroy", "tsp_nccl_unique_id", "tsp_local_world_create", "tsp_local_world_destroy",
+            "tsp_prof_classes", "tsp_destroy", "tsp_nccl_unique_id", "tsp_local_world_create", "tsp_local_world_destroy",
             "tsp_partition", "tsp_level_dist"]
 
 TSP_COMM_NONE, TSP_COMM_NCCL, TSP_COMM_LOCAL = 0, 1, 2
@@ -284,6 +285,18 @@ class Tsp:
 
     def prof_enable(self, on=True):
         _check(lib().tsp_prof_enable(self.h, int(on)), "tsp_prof_enable")
+
+    def prof_classes(self, names=None):
+        """Record only the named kernel classes (None: all)."""
+        mask = 0xFFFFFFFF
+        if names is not None:
+            p = tsp_prof()
+            _check(lib().tsp_prof_read(self.h, C.byref(p)), "tsp_prof_read")
+            idx = {p.name[k].value.decode(): k for k in range(p.nclasses)}
+            mask = 0
+            for nm in names:
+                mask |= 1 << idx[nm]
+        _check(lib().tsp_prof_classes(self.h, mask), "tsp_prof_classes")
 
     def prof_read(self):
         p = tsp_prof()
