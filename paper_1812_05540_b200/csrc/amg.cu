@@ -597,7 +597,7 @@ static void make_coarsest(Ctx &c, Hier &H, Level &L)
 }
 
 // TSP_DEBUG=1: synchronise and print the wall time of each setup phase
-static void dbg_mark(Ctx &c, const char *what, int lvl)
+void dbg_mark(Ctx &c, const char *what, int lvl)
 {
     static const bool on = getenv("TSP_DEBUG") != nullptr;
     static double last = 0;
@@ -605,7 +605,18 @@ static void dbg_mark(Ctx &c, const char *what, int lvl)
     cudaStreamSynchronize(c.s);
     timespec t; clock_gettime(CLOCK_MONOTONIC, &t);
     double now = t.tv_sec + 1e-9 * t.tv_nsec;
-    if (lvl >= 0) fprintf(stderr, "[tsp setup] level %d %-12s %8.3f ms\n", lvl, what, (now - last) * 1e3);
+    if (lvl >= 0 || lvl == -2) {
+        cudaMemPool_t pool;
+        uint64_t res = 0, used = 0;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+        }
+        fprintf(stderr, "[tsp setup] level %d %-12s %8.3f ms  pool reserved %.2f GB used %.2f GB\n", lvl, what,
+                (now - last) * 1e3, res / 1e9, used / 1e9);
+    }
     last = now;
 }
 
@@ -747,6 +758,7 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
 {
     dbg_mark(c, "start", -1);
     H.L.clear();
+    dbg_mark(c, "free old", -2);
     H.L.reserve(16);
     H.nc = nc;
     H.L.emplace_back();

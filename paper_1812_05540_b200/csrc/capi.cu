@@ -193,6 +193,10 @@ tsp_status tsp_create(tsp_handle *out, const tsp_desc *d)
     sell_from_csr(*c, c->uf, c->s_uf, 6);
     sell_from_csr(*c, c->fu, c->s_fu, 6);
     sell_from_csr(*c, c->ff, c->s_ff, 4);
+    // keep only what the setup phases read: A_uu's pattern + SDC values (a2), A_ff in full (a1, a3, a5)
+    extract_sdc(*c);
+    c->uu.v.release();
+    for (Csr *A : {&c->uf, &c->fu}) { A->v.release(); A->ci.release(); A->gci.release(); A->rp.release(); }
     c->w_yf.alloc(2 * (size_t)c->Nc); c->w_wp.alloc(c->Nc); c->w_zp.alloc(c->Nc); c->w_tmp.alloc(c->Nc);
     c->kx.alloc(c->n); c->kb.alloc(c->n);
     c->dcount.alloc(4);

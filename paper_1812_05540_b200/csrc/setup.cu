@@ -4,7 +4,7 @@
 
 namespace tsp {
 
-// a2: SDC: keep the (x,x), (y,y), (z,z) entries of every 3x3 block
+// a2: SDC: keep the (x,x), (y,y), (z,z) entries of every 3x3 block (run by tsp_create)
 __global__ void k_sdc(int64_t nnzb, const double *__restrict__ uu, double *__restrict__ sdc)
 {
     int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -67,17 +67,27 @@ static void copy_pattern(Ctx &c, const Csr &src, Csr &dst, int nc)
     }
 }
 
+void extract_sdc(Ctx &c)
+{
+    c.uu_sdc.alloc(3 * (size_t)std::max<int64_t>(c.uu.nnz, 1));
+    if (c.uu.nnz) k_sdc<<<grid_for(c.uu.nnz, 256), 256, 0, c.s>>>(c.uu.nnz, c.uu.v, c.uu_sdc);
+    c.launches++;
+}
+
 void setup_mech(Ctx &c)
 {
     c.mech_ready = false;
+    dbg_mark(c, "mech begin", -1);
+    c.mech.L.clear();                     // free the previous hierarchy first: its memory is reused below
     Csr A;
     copy_pattern(c, c.uu, A, 3);
     prof_begin(c, PK_SETUP);
-    if (c.uu.nnz) k_sdc<<<grid_for(c.uu.nnz, 256), 256, 0, c.s>>>(c.uu.nnz, c.uu.v, A.v);
+    if (c.uu.nnz) TSP_CUDA(cudaMemcpyAsync(A.v, c.uu_sdc, sizeof(double) * 3 * c.uu.nnz, cudaMemcpyDeviceToDevice, c.s));
     DBuf<int32_t> zb; zb.alloc(std::max(c.Nn, 1));
     if (c.Nn) k_zb_nodes<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(c.Nn, c.nx, c.ny, c.nz_glob, c.k0, c.o.zblock, zb);
     prof_end(c, PK_SETUP, 0);
     c.launches += 2;
+    dbg_mark(c, "mech sdc", -2);
     amg_build(c, c.mech, A, zb, 3, &c.hu, c.node_off, c.Nn_glob);   // a4 (mechanics): M_uu^-1 = amg(A_uu^SDC)
     c.mech_ready = true;
 }
@@ -85,6 +95,8 @@ void setup_mech(Ctx &c)
 void setup_flow(Ctx &c)
 {
     c.flow_ready = false;
+    dbg_mark(c, "flow begin", -1);
+    c.pres.L.clear();
     Csr S;
     copy_pattern(c, c.ff, S, 1);
     c.dss_inv.alloc(std::max(c.Nc, 1));
@@ -100,8 +112,10 @@ void setup_flow(Ctx &c)
     DBuf<int32_t> zb; zb.alloc(std::max(c.Nc, 1));
     if (c.Nc) k_zb_cells<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(c.Nc, c.nx, c.ny, c.k0, c.o.zblock, zb);
     c.launches += 2;
+    dbg_mark(c, "flow qimpes", -2);
     amg_build(c, c.pres, S, zb, 1, &c.hf, c.cell_off, c.Nc_glob);   // a4 (pressure): M_pp^-1 = amg(S_pp)
     ilu_setup(c, nullptr);                // a5: tile ILU(0) of P S_ff^FS P^T
+    dbg_mark(c, "ilu", -2);
     c.flow_ready = true;
 }
 

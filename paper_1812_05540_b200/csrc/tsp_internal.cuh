@@ -207,7 +207,9 @@ struct Ctx {
     tsp_options o;
     int sm_count = 148;
     // original blocks (CSR on device) for setup + SELL for apply
-    Csr uu, uf, fu, ff;           // nc = values per block entry (9, 6, 6, 4)
+    Csr uu, uf, fu, ff;           // nc = values per block entry (9, 6, 6, 4); after create only the patterns of
+                                  // uu and the full ff stay (A_uf, A_fu and A_uu's values live in the SELL copies)
+    DBuf<double> uu_sdc;          // a2: SDC values of A_uu (3 per block), extracted at create
     Sell s_uu, s_uf, s_fu, s_ff;  // SELL copies (operator rows)
     DBuf<double> fs;              // 2 per cell
     // flow setup products
@@ -236,6 +238,7 @@ struct Ctx {
 // ------------------------------------------------------------------ launch helpers
 inline int grid_for(int64_t threads, int block) { return (int)((threads + block - 1) / block); }
 void prof_begin(Ctx &c, int cls);
+void dbg_mark(Ctx &c, const char *what, int lvl);   // TSP_DEBUG=1: phase wall times of the setup
 void prof_end(Ctx &c, int cls, double bytes);
 void *scratch(Ctx &c, size_t bytes);
 
@@ -249,6 +252,7 @@ void op_apply(Ctx &c, const double *x, double *y);
 void prec_apply(Ctx &c, const double *v, double *z);
 
 // setup (setup_flow.cu, amg_setup.cu, ilu.cu)
+void extract_sdc(Ctx &c);
 void setup_mech(Ctx &c);
 void setup_flow(Ctx &c);
 void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_halo, int64_t row_off0, int64_t nglob0);
