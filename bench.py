@@ -39,6 +39,17 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(kernel_class):
+    """(DRAM bytes per launch, ncu DRAM % of peak) of a kernel class from the committed ncu --set full
+    capture, or (None, None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            k = json.load(f)["kernels"][kernel_class]
+        return float(k["dram_bytes_per_launch"]), k.get("ncu_dram_pct_of_peak")
+    except Exception:
+        return None, None
+
+
 def dist_init():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -361,7 +372,8 @@ def main():
                                    "frac": iter_gbs / hbm, "mean_krylov_index": mean_j,
                                    "reorth_fraction": reorth_frac},
             "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+                         "frac": achieved / hbm, "traffic": ncu_traffic(dname)[0], "ncu_dram_pct": ncu_traffic(dname)[1],
+                         "peak_source": peak_src,
                          "bytes_per_launch": d["bytes"] / d["launches"], "ms_per_launch": d["ms"] / d["launches"]},
             "kernels": kernel_table,
             "gpu_launches": int(st["launches"]),

@@ -10,7 +10,7 @@ for r in data:
     d[r[mi]] = float(r[vi].replace(',', ''))
 launches = list(L.values())
 names = [l['k'].split('(')[0] for l in launches]
-idx = [i for i, n in enumerate(names) if 'k_maxpy_norm' in n]
+idx = [i for i, n in enumerate(names) if 'k_dcgs_update' in n]
 a, b = idx[-2] + 1, idx[-1] + 1
 tot = sum(l['gpu__time_duration.sum'] for l in launches[a:b])
 for l in launches[a:b]:
