@@ -67,7 +67,15 @@ typedef struct {
     int tile_x, tile_y, tile_z;  /* ILU(0) tile, 16^3 (R-ilu) */
     int replicate_rows;          /* multi-GPU: coarse levels with <= this many global rows are gathered on
                                     every rank (default 32768); no effect on the result */
-    int reserved[7];
+    /* setup variants of the paper; the defaults are the paper's choices */
+    int cpr_mode;                /* 0 quasi-IMPES: D_ss = diagm(A_ss), D_ps = diagm(A_ps);
+                                    1 true-IMPES: column-sum lumping D = diag(A^T e) (eq:CPR_CSL) */
+    int aps_mode;                /* 0 full A_ps in step 4; 1 its diagonal approximation D_ps^(CPR) */
+    int fs_mode;                 /* 0 D_fs = tsp_desc.fs_diag / fs_modulus_scale (eq:FS_Dps_Dpp, remark P:443);
+                                    1 algebraic row-sum lumping (eq:FS_RSL): needs TSP_SETUP_MECH first */
+    int rsl_iters;               /* fs_mode 1: A_uu^-1 ~ this many M_uu-preconditioned Richardson steps, 2 */
+    double fs_modulus_scale;     /* fs_mode 0: K_dr -> scale * K_dr, i.e. D_fs / scale (default 1) */
+    int reserved[4];
 } tsp_options;
 
 /* BSR block matrix given to tsp_create (nrows block rows). */
@@ -203,6 +211,9 @@ tsp_status tsp_prof_read(tsp_handle h, tsp_prof *p);  /* synchronises */
  * two timing events per recorded launch cost ~2 % of an FGMRES iteration, so a timed run records
  * only the class whose roofline it reports */
 tsp_status tsp_prof_classes(tsp_handle h, unsigned mask);
+/* Test hook (after TSP_SETUP_FLOW): this rank's D_ss^(CPR), D_ps^(CPR) (N_c,local each) and the fixed-stress
+ * diagonal actually used by a1, (D_sp, D_pp) per cell (2 N_c,local); host buffers, any may be NULL. */
+tsp_status tsp_export_cpr(tsp_handle h, double *dss, double *dps, double *fs_eff);
 
 void tsp_destroy(tsp_handle h);
 

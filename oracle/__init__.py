@@ -33,7 +33,9 @@ class Desc(C.Structure):
 class Opts(C.Structure):
     _fields_ = [("amg_theta", C.c_double), ("amg_coarse_max", C.c_int), ("amg_max_levels", C.c_int),
                 ("zblock", C.c_int), ("tile_x", C.c_int), ("tile_y", C.c_int), ("tile_z", C.c_int),
-                ("mech_mode", C.c_int), ("pres_mode", C.c_int), ("local_mode", C.c_int), ("ff_mode", C.c_int)]
+                ("mech_mode", C.c_int), ("pres_mode", C.c_int), ("local_mode", C.c_int), ("ff_mode", C.c_int),
+                ("cpr_mode", C.c_int), ("aps_mode", C.c_int), ("fs_mode", C.c_int), ("rsl_iters", C.c_int),
+                ("fs_modulus_scale", C.c_double)]
 
 
 class Info(C.Structure):
@@ -63,6 +65,7 @@ def lib():
         L.orc_level_export.argtypes = [C.c_void_p, C.c_int, C.c_int, _I32, _I32, _F64, _I32, _I32, _I32, _F64, _F64]
         L.orc_counters.argtypes = [C.c_void_p, _P(C.c_int64)]
         L.orc_get_spp.argtypes = [C.c_void_p, _F64, _I32, _I32, _F64]
+        L.orc_get_cpr.argtypes = [C.c_void_p, _F64, _F64, _F64]
         L.orc_mis2.argtypes = [C.c_int, _I32, _I32, _U32, C.c_int, _I32, _P(C.c_int)]
         L.orc_amg_build.argtypes = [C.c_int, C.c_int, _I32, _I32, _F64, _I32, _P(Opts)]
         L.orc_amg_build.restype = C.c_void_p
@@ -190,6 +193,13 @@ class Oracle:
         v = np.empty(nnz)
         lib().orc_get_spp(self.h, _p(Dss), _p(rp), _p(ci), _p(v))
         return Dss, rp, ci, v
+
+    def cpr(self):
+        """(D_ss^(CPR), D_ps^(CPR), D_fs used by a1 as (Nc, 2))."""
+        Nc = self.pb.Nc
+        Dss, Dps, fs = np.empty(Nc), np.empty(Nc), np.empty(2 * Nc)
+        lib().orc_get_cpr(self.h, _p(Dss), _p(Dps), _p(fs))
+        return Dss, Dps, fs.reshape(Nc, 2)
 
 
 def mis2(rp, ci, hashes, rounds=False):

@@ -679,7 +679,8 @@ struct orc {
     obsr uu, uf, fu, ff; double *fs;
     /* a1/a3 products (partitioned scalar blocks) */
     mcsr Ass, Asp, Aps, App, Asp_fs, App_fs, Asu, Apu, Spp;
-    double *Dss;
+    double *Dss, *Dps;            /* D_ss^(CPR), D_ps^(CPR) (P:568-575 / eq:CPR_CSL) */
+    double *fs_eff;               /* (D_sp, D_pp) used by a1: given / scale, or RSL */
     obsr Sff;                     /* interleaved S_ff^FS for M_L */
     ohier *mech, *pres;
     oilu *ilu;
@@ -725,6 +726,7 @@ void orc_default_opts(orc_opts *o)
     memset(o, 0, sizeof(*o));
     o->amg_theta = 0.25; o->amg_coarse_max = 64; o->amg_max_levels = 12;
     o->zblock = 16; o->tile_x = 16; o->tile_y = 16; o->tile_z = 16;
+    o->rsl_iters = 2; o->fs_modulus_scale = 1.0;
 }
 
 orc *orc_create(const orc_desc *d, const orc_opts *o)
@@ -753,44 +755,72 @@ static void dense_from_bsr(const obsr *B, double *D, int ld)
                     D[(int64_t)(i * B->bm + r) * ld + B->ci[q] * B->bn + s] = B->v[(int64_t)B->bm * B->bn * q + r * B->bn + s];
 }
 
+/* step 1 of Algorithm 1: z_u = M_uu^-1 v_u, one SDC V-cycle per displacement component
+ * (P:513-517), or the exact dense solve (pins) */
+static void mech_apply(orc *h, const double *vu, double *zu)
+{
+    int Nn = h->Nn;
+    if (h->o.mech_mode == 0) {
+        double *bc = (double *)xmalloc(sizeof(double) * Nn), *xc = (double *)xmalloc(sizeof(double) * Nn);
+        for (int c = 0; c < 3; ++c) {
+            for (int i = 0; i < Nn; ++i) bc[i] = vu[3 * i + c];
+            vcycle(h->mech, 0, c, bc, xc);
+            for (int i = 0; i < Nn; ++i) zu[3 * i + c] = xc[i];
+        }
+        free(bc); free(xc);
+    } else {
+        dense_lu_solve(3 * Nn, h->dense_uu, h->piv_uu, vu, zu);
+    }
+}
+
+/* y = A_uu x, 3x3 blocks (eq:jac_system) */
+static void uu_matvec(const orc *h, const double *x, double *y)
+{
+    for (int i = 0; i < h->Nn; ++i)
+        for (int r = 0; r < 3; ++r) {
+            double s = 0.0;
+            for (int64_t q = h->uu.rp[i]; q < h->uu.rp[i + 1]; ++q)
+                for (int c = 0; c < 3; ++c) s = s + h->uu.v[9 * q + 3 * r + c] * x[3 * (int64_t)h->uu.ci[q] + c];
+            y[3 * (int64_t)i + r] = s;
+        }
+}
+
+/* eq:FS_RSL: D_sp = -diag(A_su A_uu^-1 A_up e), D_pp = -diag(A_pu A_uu^-1 A_up e).  A_uu^-1 is
+ * approximated with the available preconditioner: rsl_iters steps of Richardson iteration
+ * y_{t+1} = y_t + M_uu^-1 (g - A_uu y_t), y_0 = 0, g = A_up e.  out = (D_sp, D_pp) per cell. */
+static void rsl_diag(orc *h, double *out)
+{
+    int Nn = h->Nn, Nc = h->Nc, N = 3 * Nn;
+    double *g = (double *)xcalloc(N, sizeof(double)), *y = (double *)xcalloc(N, sizeof(double));
+    double *r = (double *)xmalloc(sizeof(double) * N), *t = (double *)xmalloc(sizeof(double) * N);
+    double *dy = (double *)xmalloc(sizeof(double) * N);
+    for (int i = 0; i < Nn; ++i)                         /* g = A_up e: the p column of every 3x2 block of A_uf */
+        for (int64_t q = h->uf.rp[i]; q < h->uf.rp[i + 1]; ++q)
+            for (int rr = 0; rr < 3; ++rr) g[3 * (int64_t)i + rr] = g[3 * (int64_t)i + rr] + h->uf.v[6 * q + 2 * rr + 1];
+    int iters = h->o.rsl_iters > 0 ? h->o.rsl_iters : 1;
+    for (int it = 0; it < iters; ++it) {
+        uu_matvec(h, y, t);
+        for (int k = 0; k < N; ++k) r[k] = g[k] - t[k];
+        mech_apply(h, r, dy);
+        for (int k = 0; k < N; ++k) y[k] = y[k] + dy[k];
+    }
+    for (int K = 0; K < Nc; ++K) {                       /* A_su y, A_pu y: rows s and p of the 2x3 blocks */
+        double ss = 0.0, sp = 0.0;
+        for (int64_t q = h->fu.rp[K]; q < h->fu.rp[K + 1]; ++q)
+            for (int c = 0; c < 3; ++c) {
+                ss = ss + h->fu.v[6 * q + c] * y[3 * (int64_t)h->fu.ci[q] + c];
+                sp = sp + h->fu.v[6 * q + 3 + c] * y[3 * (int64_t)h->fu.ci[q] + c];
+            }
+        out[2 * K] = -ss;
+        out[2 * K + 1] = -sp;
+    }
+    free(g); free(y); free(r); free(t); free(dy);
+}
+
 int orc_setup(orc *h)
 {
     double t0 = now_s();
     int Nc = h->Nc, Nn = h->Nn;
-    /* ---- a1: fixed-stress augmentation, eq:Schur_1_FS (P:406-417):
-     *      A_sp^FS = A_sp + D_sp, A_pp^FS = A_pp + D_pp, D diagonal (P:432-437); A_us ~ 0 (P:397) */
-    bsr_entry(&h->ff, 0, 0, &h->Ass); bsr_entry(&h->ff, 0, 1, &h->Asp);
-    bsr_entry(&h->ff, 1, 0, &h->Aps); bsr_entry(&h->ff, 1, 1, &h->App);
-    bsr_entry(&h->ff, 0, 1, &h->Asp_fs); bsr_entry(&h->ff, 1, 1, &h->App_fs);
-    for (int i = 0; i < Nc; ++i) {
-        int64_t q = find_col(&h->Asp_fs, i, i);
-        if (q < 0) return -1;
-        h->Asp_fs.v[0][q] = h->Asp_fs.v[0][q] + h->fs[2 * i];
-        h->App_fs.v[0][q] = h->App_fs.v[0][q] + h->fs[2 * i + 1];
-    }
-    bsr_rowslice(&h->fu, 0, &h->Asu); bsr_rowslice(&h->fu, 1, &h->Apu);
-    /* interleaved S_ff^FS for the local stage (P:606) */
-    bsr_copy(&h->Sff, Nc, Nc, 2, 2, h->ff.rp, h->ff.ci, h->ff.v);
-    for (int i = 0; i < Nc; ++i)
-        for (int64_t q = h->Sff.rp[i]; q < h->Sff.rp[i + 1]; ++q)
-            if (h->Sff.ci[q] == i) { h->Sff.v[4 * q + 1] = h->Sff.v[4 * q + 1] + h->fs[2 * i]; h->Sff.v[4 * q + 3] = h->Sff.v[4 * q + 3] + h->fs[2 * i + 1]; }
-
-    /* ---- a3: quasi-IMPES: D_ss = diagm(A_ss), D_ps = diagm(A_ps);
-     *      S_pp = A_pp^FS - D_ps D_ss^-1 A_sp^FS (P:577-583), same pattern */
-    h->Dss = (double *)xmalloc(sizeof(double) * Nc);
-    mcsr_alloc(&h->Spp, Nc, Nc, 1, mnnz(&h->App_fs));
-    memcpy(h->Spp.rp, h->App_fs.rp, sizeof(int32_t) * (Nc + 1));
-    memcpy(h->Spp.ci, h->App_fs.ci, sizeof(int32_t) * mnnz(&h->App_fs));
-    for (int i = 0; i < Nc; ++i) {
-        int64_t qd = find_col(&h->Ass, i, i);
-        double dss = h->Ass.v[0][qd], dps = h->Aps.v[0][qd];
-        h->Dss[i] = dss;
-        double ci = 0.0;
-        if (dss != 0.0) ci = dps / dss; else h->skipped_dss++;   /* S:403 */
-        for (int64_t q = h->Spp.rp[i]; q < h->Spp.rp[i + 1]; ++q)
-            h->Spp.v[0][q] = h->App_fs.v[0][q] - ci * h->Asp_fs.v[0][q];
-    }
-
     /* ---- a2 + a4 (mechanics): M_uu^-1 = amg(A_uu^SDC), three components on one
      *      node graph */
     if (h->o.mech_mode == 0) {
@@ -817,6 +847,62 @@ int orc_setup(orc *h)
         dense_from_bsr(&h->uu, h->dense_uu, N);
         dense_lu(N, h->dense_uu, h->piv_uu, &h->perturbed);
     }
+    /* ---- a1 input: the fixed-stress diagonal D_fs -- given (eq:FS_Dps_Dpp), divided by
+     *      fs_modulus_scale (remark P:443), or by row-sum lumping (eq:FS_RSL) */
+    bsr_rowslice(&h->fu, 0, &h->Asu); bsr_rowslice(&h->fu, 1, &h->Apu);
+    h->fs_eff = (double *)xmalloc(sizeof(double) * 2 * Nc);
+    if (h->o.fs_mode == 1) rsl_diag(h, h->fs_eff);
+    else for (int k = 0; k < 2 * Nc; ++k) h->fs_eff[k] = h->fs[k] / h->o.fs_modulus_scale;
+    /* ---- a1: fixed-stress augmentation, eq:Schur_1_FS (P:406-417):
+     *      A_sp^FS = A_sp + D_sp, A_pp^FS = A_pp + D_pp, D diagonal (P:432-437); A_us ~ 0 (P:397) */
+    bsr_entry(&h->ff, 0, 0, &h->Ass); bsr_entry(&h->ff, 0, 1, &h->Asp);
+    bsr_entry(&h->ff, 1, 0, &h->Aps); bsr_entry(&h->ff, 1, 1, &h->App);
+    bsr_entry(&h->ff, 0, 1, &h->Asp_fs); bsr_entry(&h->ff, 1, 1, &h->App_fs);
+    for (int i = 0; i < Nc; ++i) {
+        int64_t q = find_col(&h->Asp_fs, i, i);
+        if (q < 0) return -1;
+        h->Asp_fs.v[0][q] = h->Asp_fs.v[0][q] + h->fs_eff[2 * i];
+        h->App_fs.v[0][q] = h->App_fs.v[0][q] + h->fs_eff[2 * i + 1];
+    }
+    /* interleaved S_ff^FS for the local stage (P:606) */
+    bsr_copy(&h->Sff, Nc, Nc, 2, 2, h->ff.rp, h->ff.ci, h->ff.v);
+    for (int i = 0; i < Nc; ++i)
+        for (int64_t q = h->Sff.rp[i]; q < h->Sff.rp[i + 1]; ++q)
+            if (h->Sff.ci[q] == i) { h->Sff.v[4 * q + 1] = h->Sff.v[4 * q + 1] + h->fs_eff[2 * i]; h->Sff.v[4 * q + 3] = h->Sff.v[4 * q + 3] + h->fs_eff[2 * i + 1]; }
+
+    /* ---- a3: CPR reduction.  quasi-IMPES: D_ss = diagm(A_ss), D_ps = diagm(A_ps);
+     *      true-IMPES (eq:CPR_CSL): D_ss = diag(A_ss^T e), D_ps = diag(A_ps^T e), the column
+     *      sums taken over the rows k of column i in ascending order.
+     *      S_pp = A_pp^FS - D_ps D_ss^-1 A_sp^FS (P:577-583), same pattern */
+    h->Dss = (double *)xmalloc(sizeof(double) * Nc);
+    h->Dps = (double *)xmalloc(sizeof(double) * Nc);
+    for (int i = 0; i < Nc; ++i) {
+        if (h->o.cpr_mode == 1) {
+            double dss = 0.0, dps = 0.0;
+            for (int64_t q = h->Ass.rp[i]; q < h->Ass.rp[i + 1]; ++q) {   /* symmetric pattern: rows k of column i */
+                int k = h->Ass.ci[q];
+                int64_t qk = find_col(&h->Ass, k, i);
+                if (qk < 0) return -1;
+                dss = dss + h->Ass.v[0][qk];
+                dps = dps + h->Aps.v[0][qk];
+            }
+            h->Dss[i] = dss; h->Dps[i] = dps;
+        } else {
+            int64_t qd = find_col(&h->Ass, i, i);
+            h->Dss[i] = h->Ass.v[0][qd]; h->Dps[i] = h->Aps.v[0][qd];
+        }
+    }
+    mcsr_alloc(&h->Spp, Nc, Nc, 1, mnnz(&h->App_fs));
+    memcpy(h->Spp.rp, h->App_fs.rp, sizeof(int32_t) * (Nc + 1));
+    memcpy(h->Spp.ci, h->App_fs.ci, sizeof(int32_t) * mnnz(&h->App_fs));
+    for (int i = 0; i < Nc; ++i) {
+        double dss = h->Dss[i], dps = h->Dps[i];
+        double ci = 0.0;
+        if (dss != 0.0) ci = dps / dss; else h->skipped_dss++;   /* S:403 */
+        for (int64_t q = h->Spp.rp[i]; q < h->Spp.rp[i + 1]; ++q)
+            h->Spp.v[0][q] = h->App_fs.v[0][q] - ci * h->Asp_fs.v[0][q];
+    }
+
     /* ---- a4 (pressure): M_pp^-1 = amg(S_pp^(CPR-FS)) */
     if (h->o.pres_mode == 0) {
         int32_t *zb = (int32_t *)xmalloc(sizeof(int32_t) * Nc);
@@ -877,17 +963,7 @@ int orc_apply(orc *h, const double *v, double *z)
     double *vs = (double *)xmalloc(sizeof(double) * Nc), *vp = (double *)xmalloc(sizeof(double) * Nc);
     for (int K = 0; K < Nc; ++K) { vs[K] = vf[2 * K]; vp[K] = vf[2 * K + 1]; }   /* P^T */
     /* step 1: z_u = M_uu^-1 v_u */
-    if (h->o.mech_mode == 0) {
-        double *bc = (double *)xmalloc(sizeof(double) * Nn), *xc = (double *)xmalloc(sizeof(double) * Nn);
-        for (int c = 0; c < 3; ++c) {
-            for (int i = 0; i < Nn; ++i) bc[i] = vu[3 * i + c];
-            vcycle(h->mech, 0, c, bc, xc);
-            for (int i = 0; i < Nn; ++i) zu[3 * i + c] = xc[i];
-        }
-        free(bc); free(xc);
-    } else {
-        dense_lu_solve(3 * Nn, h->dense_uu, h->piv_uu, vu, zu);
-    }
+    mech_apply(h, vu, zu);
     /* step 2: [y_s; y_p] = [v_s; v_p] - [A_su; A_pu] z_u */
     double *ys = (double *)xmalloc(sizeof(double) * Nc), *yp = (double *)xmalloc(sizeof(double) * Nc);
     memcpy(ys, vs, sizeof(double) * Nc); memcpy(yp, vp, sizeof(double) * Nc);
@@ -903,10 +979,11 @@ int orc_apply(orc *h, const double *v, double *z)
     /* step 3: z_s = (D_ss^(CPR))^-1 y_s */
     double *zs = (double *)xmalloc(sizeof(double) * Nc), *zp = (double *)xmalloc(sizeof(double) * Nc);
     for (int K = 0; K < Nc; ++K) zs[K] = h->Dss[K] != 0.0 ? ys[K] / h->Dss[K] : 0.0;
-    /* step 4: w_p = y_p - A_ps z_s, full A_ps */
+    /* step 4: w_p = y_p - A_ps z_s, full A_ps, or its diagonal D_ps^(CPR) */
     double *wp = (double *)xmalloc(sizeof(double) * Nc);
     memcpy(wp, yp, sizeof(double) * Nc);
-    spmv_sub(&h->Aps, 0, zs, wp);
+    if (h->o.aps_mode == 1) for (int K = 0; K < Nc; ++K) wp[K] = wp[K] - h->Dps[K] * zs[K];
+    else spmv_sub(&h->Aps, 0, zs, wp);
     /* step 5: z_p = M_pp^-1 w_p */
     if (h->o.pres_mode == 0) vcycle(h->pres, 0, 0, wp, zp);
     else dense_lu_solve(Nc, h->dense_pp, h->piv_pp, wp, zp);
@@ -1070,6 +1147,13 @@ void orc_get_spp(orc *h, double *Dss, int32_t *rp, int32_t *ci, double *v)
     if (v) memcpy(v, h->Spp.v[0], sizeof(double) * mnnz(&h->Spp));
 }
 
+void orc_get_cpr(orc *h, double *Dss, double *Dps, double *fs_eff)
+{
+    if (Dss) memcpy(Dss, h->Dss, sizeof(double) * h->Nc);
+    if (Dps) memcpy(Dps, h->Dps, sizeof(double) * h->Nc);
+    if (fs_eff) memcpy(fs_eff, h->fs_eff, sizeof(double) * 2 * h->Nc);
+}
+
 void orc_destroy(orc *h)
 {
     if (!h) return;
@@ -1077,7 +1161,7 @@ void orc_destroy(orc *h)
     free(h->fs);
     mcsr *m[] = {&h->Ass, &h->Asp, &h->Aps, &h->App, &h->Asp_fs, &h->App_fs, &h->Asu, &h->Apu, &h->Spp};
     for (size_t i = 0; i < sizeof(m) / sizeof(m[0]); ++i) mcsr_free(m[i]);
-    free(h->Dss);
+    free(h->Dss); free(h->Dps); free(h->fs_eff);
     amg_free(h->mech); amg_free(h->pres); orc_ilu_free(h->ilu);
     free(h->dense_uu); free(h->dense_pp); free(h->dense_ff); free(h->dense_schur);
     free(h->piv_uu); free(h->piv_pp); free(h->piv_ff); free(h->piv_schur);

@@ -32,6 +32,12 @@ typedef struct {
     int pres_mode;                /* 0: amg(S_pp) P:599;    1: exact dense S_pp^-1 (pins) */
     int local_mode;               /* 0: tile ILU(0) P:612;  1: exact (S_ff^FS)^-1; 2: none */
     int ff_mode;                  /* 0: CPR two-stage (Alg.1 steps 3-8); 1: exact dense S_ff^-1 (eq:LU) */
+    /* NEXT-f3 variants (setup only; defaults reproduce the paper's choices) */
+    int cpr_mode;                 /* 0: quasi-IMPES diagm; 1: true-IMPES column sums (eq:CPR_CSL) */
+    int aps_mode;                 /* 0: full A_ps in step 4; 1: its diagonal approximation D_ps^(CPR) */
+    int fs_mode;                  /* 0: D_fs given (eq:FS_Dps_Dpp); 1: row-sum lumping RSL (eq:FS_RSL) */
+    int rsl_iters;                /* RSL: A_uu^-1 ~ this many M_uu-preconditioned Richardson steps, default 2 */
+    double fs_modulus_scale;      /* fs_mode 0: modulus K_dr -> scale K_dr, i.e. D_fs / scale (remark P:443), default 1 */
 } orc_opts;
 
 typedef struct {
@@ -55,7 +61,8 @@ void orc_level_sizes(orc *h, int which, int lvl, int64_t out[6]); /* n, nnz(A), 
 void orc_level_export(orc *h, int which, int lvl, int32_t *A_rp, int32_t *A_ci, double *A_v,
                       int32_t *agg, int32_t *P_rp, int32_t *P_ci, double *P_v, double *dl1);
 void orc_counters(orc *h, int64_t out[4]);                /* skipped D_ss, perturbed pivots, fallbacks, - */
-void orc_get_spp(orc *h, double *Dss, int32_t *rp, int32_t *ci, double *v);   /* quasi-IMPES products */
+void orc_get_spp(orc *h, double *Dss, int32_t *rp, int32_t *ci, double *v);   /* CPR products (a3) */
+void orc_get_cpr(orc *h, double *Dss, double *Dps, double *fs_eff);  /* D^(CPR) and the D_fs actually used (a1) */
 
 /* standalone primitives for pins (tests only) */
 int orc_mis2(int n, const int32_t *rp, const int32_t *ci, const uint32_t *hash, int rounds_variant,

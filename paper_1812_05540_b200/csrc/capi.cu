@@ -104,6 +104,7 @@ tsp_status tsp_default_options(tsp_options *o)
     memset(o, 0, sizeof(*o));
     o->amg_theta = 0.25; o->amg_coarse_max = 64; o->amg_max_levels = 12; o->zblock = 16;
     o->tile_x = o->tile_y = o->tile_z = 16;
+    o->rsl_iters = 2; o->fs_modulus_scale = 1.0;
     return TSP_OK;
 }
 
@@ -134,6 +135,11 @@ tsp_status tsp_create(tsp_handle *out, const tsp_desc *d)
     if (c->o.zblock <= 0) c->o.zblock = 16;
     if (c->o.tile_x <= 0 || c->o.tile_y <= 0 || c->o.tile_z <= 0) c->o.tile_x = c->o.tile_y = c->o.tile_z = 16;
     if (c->o.replicate_rows <= 0) c->o.replicate_rows = 32768;
+    if (c->o.rsl_iters <= 0) c->o.rsl_iters = 2;
+    if (!(c->o.fs_modulus_scale > 0)) c->o.fs_modulus_scale = 1.0;
+    TSP_REQUIRE(c->o.cpr_mode == 0 || c->o.cpr_mode == 1, TSP_ERR_INVALID_ARG, "cpr_mode must be 0 (quasi) or 1 (true IMPES)");
+    TSP_REQUIRE(c->o.aps_mode == 0 || c->o.aps_mode == 1, TSP_ERR_INVALID_ARG, "aps_mode must be 0 (full) or 1 (diagonal)");
+    TSP_REQUIRE(c->o.fs_mode == 0 || c->o.fs_mode == 1, TSP_ERR_INVALID_ARG, "fs_mode must be 0 (given) or 1 (RSL)");
     // z-slab partition (include/tsp.h): local sizes in Nn, Nc, n, nz
     c->rank = d->rank; c->nranks = d->nranks;
     c->nx = d->nx; c->ny = d->ny; c->nz_glob = d->nz;
@@ -368,6 +374,18 @@ tsp_status tsp_prof_enable(tsp_handle h, int on)
     p.next = 0;
     p.on = on != 0;
     h->launches = 0;
+    API_END
+}
+
+tsp_status tsp_export_cpr(tsp_handle h, double *dss, double *dps, double *fs_eff)
+{
+    if (!h) { set_error("null handle"); return TSP_ERR_INVALID_ARG; }
+    API_BEGIN
+    TSP_REQUIRE(h->flow_ready, TSP_ERR_STATE, "export_cpr before tsp_setup(FLOW)");
+    if (dss && h->Nc) TSP_CUDA(cudaMemcpyAsync(dss, h->cpr_dss, sizeof(double) * h->Nc, cudaMemcpyDeviceToHost, h->s));
+    if (dps && h->Nc) TSP_CUDA(cudaMemcpyAsync(dps, h->cpr_dps, sizeof(double) * h->Nc, cudaMemcpyDeviceToHost, h->s));
+    if (fs_eff && h->Nc) TSP_CUDA(cudaMemcpyAsync(fs_eff, h->fs_eff, sizeof(double) * 2 * h->Nc, cudaMemcpyDeviceToHost, h->s));
+    TSP_CUDA(cudaStreamSynchronize(h->s));
     API_END
 }
 

@@ -339,7 +339,7 @@ void ilu_setup(Ctx &c, const double *)
     c.ilu_dinv.alloc((size_t)c.ntiles * per_tile * 4);
     c.ilu_val.zero(c.s);
     c.ilu_dinv.zero(c.s);
-    if (c.Nc) k_ilu_fill<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(g, c.ny, c.ff.rp, c.ff.gci.p ? c.ff.gci.p : c.ff.ci.p, c.ff.v, c.fs,
+    if (c.Nc) k_ilu_fill<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(g, c.ny, c.ff.rp, c.ff.gci.p ? c.ff.gci.p : c.ff.ci.p, c.ff.v, c.fs_eff,
                                                              c.ilu_val);
     c.dcount.zero(c.s);
     k_ilu_factor<<<c.ntiles, 32, 0, c.s>>>(g, c.ilu_cells, c.ilu_lvlptr, c.ilu_val, c.ilu_dinv, c.dcount);

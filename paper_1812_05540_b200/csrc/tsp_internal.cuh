@@ -211,7 +211,9 @@ struct Ctx {
                                   // uu and the full ff stay (A_uf, A_fu and A_uu's values live in the SELL copies)
     DBuf<double> uu_sdc;          // a2: SDC values of A_uu (3 per block), extracted at create
     Sell s_uu, s_uf, s_fu, s_ff;  // SELL copies (operator rows)
-    DBuf<double> fs;              // 2 per cell
+    DBuf<double> fs;              // 2 per cell, as given (tsp_desc.fs_diag)
+    DBuf<double> fs_eff;          // 2 per cell: the D_fs a1 uses (given / fs_modulus_scale, or RSL)
+    DBuf<double> cpr_dss, cpr_dps; // D_ss^(CPR), D_ps^(CPR) (a3)
     // flow setup products
     DBuf<double> dss_inv;         // 1/D_ss (0 if D_ss == 0)
     Sell s_aps;                   // A_ps values on A_ff's pattern (bs 1)

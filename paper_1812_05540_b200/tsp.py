@@ -28,7 +28,8 @@ STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "INVALID_ARG", -2: "DIM_MISMATCH", -3
 class tsp_options(C.Structure):
     _fields_ = [("amg_theta", C.c_double), ("amg_coarse_max", C.c_int), ("amg_max_levels", C.c_int),
                 ("zblock", C.c_int), ("tile_x", C.c_int), ("tile_y", C.c_int), ("tile_z", C.c_int),
-                ("replicate_rows", C.c_int), ("reserved", C.c_int * 7)]
+                ("replicate_rows", C.c_int), ("cpr_mode", C.c_int), ("aps_mode", C.c_int), ("fs_mode", C.c_int),
+                ("rsl_iters", C.c_int), ("fs_modulus_scale", C.c_double), ("reserved", C.c_int * 4)]
 
 
 class tsp_bsr(C.Structure):
@@ -92,6 +93,7 @@ def lib():
         L.tsp_export_level.argtypes = [C.c_void_p, C.c_int, C.c_int] + [C.c_void_p] * 8
         L.tsp_prof_enable.argtypes = [C.c_void_p, C.c_int]
         L.tsp_prof_classes.argtypes = [C.c_void_p, C.c_uint]
+        L.tsp_export_cpr.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.tsp_prof_read.argtypes = [C.c_void_p, _P(tsp_prof)]
         L.tsp_destroy.argtypes = [C.c_void_p]
         L.tsp_destroy.restype = None
@@ -111,7 +113,7 @@ def lib():
 EXPORTED = ["tsp_abi_version", "tsp_last_error", "tsp_default_options", "tsp_create", "tsp_setup",
             "tsp_apply_preconditioner", "tsp_apply_operator", "tsp_solve", "tsp_default_solve_opts",
             "tsp_get_stats", "tsp_level_sizes", "tsp_export_level", "tsp_prof_enable", "tsp_prof_read",
-            "tsp_prof_classes", "tsp_destroy", "tsp_nccl_unique_id", "tsp_local_world_create", "tsp_local_world_destroy",
+            "tsp_prof_classes", "tsp_export_cpr", "tsp_destroy", "tsp_nccl_unique_id", "tsp_local_world_create", "tsp_local_world_destroy",
             "tsp_partition", "tsp_level_dist"]
 
 TSP_COMM_NONE, TSP_COMM_NCCL, TSP_COMM_LOCAL = 0, 1, 2
@@ -285,6 +287,13 @@ class Tsp:
 
     def prof_enable(self, on=True):
         _check(lib().tsp_prof_enable(self.h, int(on)), "tsp_prof_enable")
+
+    def cpr(self):
+        """Test hook: (D_ss^(CPR), D_ps^(CPR), D_fs used by a1 as (N_c, 2)) of this rank."""
+        Nc = self.pb.Nc if not hasattr(self, "nc_local") else self.nc_local
+        dss, dps, fs = np.empty(Nc), np.empty(Nc), np.empty(2 * Nc)
+        _check(lib().tsp_export_cpr(self.h, dss.ctypes.data, dps.ctypes.data, fs.ctypes.data), "tsp_export_cpr")
+        return dss, dps, fs.reshape(Nc, 2)
 
     def prof_classes(self, names=None):
         """Record only the named kernel classes (None: all)."""
