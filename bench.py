@@ -104,7 +104,7 @@ def cpu_cores():
 SAMPLE_GRID = {"C5": (128, 128, 64)}   # oracle sample grid when the full config is too large for a bounded run
 
 
-def oracle_sample(config, gpu_iters, sample_iters=3, reps=1):
+def oracle_sample(config, gpu_iters, sample_iters=3, reps=1, opts=None):
     """The CPU oracle (as it stands, single thread) on a bounded sample of the
     workload: its full setup (timed) + `sample_iters` FGMRES iterations (timed,
     `reps` times).  Up to C4 the sample is the workload itself; for C5 it is the
@@ -118,7 +118,7 @@ def oracle_sample(config, gpu_iters, sample_iters=3, reps=1):
     pb = synth.generate(config, **kw)
     scale = full / pb.n
     t0 = time.perf_counter()
-    o = oracle.Oracle(pb).setup()
+    o = oracle.Oracle(pb, **(opts or {})).setup()
     t_setup = time.perf_counter() - t0
     its, t_s = 0, 0.0
     for _ in range(reps):
@@ -145,12 +145,12 @@ def run_reference(args, ws, rank):
     if rank != 0:
         return 0
     iters = args.ref_iters or GPU_ITERS[args.config]
-    cpu = oracle_sample(args.config, iters, sample_iters=args.ref_sample_iters, reps=max(args.steps, 1))
+    cpu = oracle_sample(args.config, iters, sample_iters=args.ref_sample_iters, reps=max(args.steps, 1), opts=args.lib_opts)
     value = cpu["value"]
     g = synth.CONFIGS[args.config]
     line = {"impl": "reference", "metric": "preconditioned FGMRES iters/s", "value": value, "unit": "iter/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": cpu["step_s"] * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "grid": [g["nx"], g["ny"], g["nz"]],
                        "dof": synth.sizes(g["nx"], g["ny"], g["nz"])["n"]},
             "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": "oracle", "sample": cpu["sample"]},
@@ -166,11 +166,18 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=list(synth.CONFIGS))
     ap.add_argument("--impl", default="tsp", choices=["tsp", "reference"])
+    ap.add_argument("--opts", default="", help="library options key=value[,key=value] (tsp_options), e.g. "
+                    "cpr_mode=1,aps_mode=1 -- the setup variants of SURVEY NEXT-f3; default: the paper's choices")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-sample-iters", type=int, default=2)
     ap.add_argument("--ref-iters", type=int, default=None, help="iterations a full reference step is scaled to (default: the GPU count measured for the config; parity holds them within +-1)")
     args = ap.parse_args()
+    lib_opts = {}
+    for kv in filter(None, args.opts.split(",")):
+        k, v = kv.split("=")
+        lib_opts[k.strip()] = float(v) if "." in v or "e" in v else int(v)
+    args.lib_opts = lib_opts
     ws, rank, local = dist_init()
 
     if args.impl == "reference":
@@ -200,7 +207,7 @@ def main():
     else:
         src, b_host = pb, pb.b
     n = src.n
-    g = Tsp(src, **topo)
+    g = Tsp(src, **topo, **lib_opts)
     b = torch.from_numpy(np.ascontiguousarray(b_host)).to(dev)
     x = torch.zeros(n, dtype=torch.float64, device=dev)
 
@@ -322,7 +329,7 @@ def main():
         d2h = xh.numel() * 8
 
         def e2e_step():
-            h = Tsp(pp, **topo)
+            h = Tsp(pp, **topo, **lib_opts)
             h.setup()
             inf = h.solve(bh.numpy(), xh.numpy())
             h.close()
@@ -349,7 +356,7 @@ def main():
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu = oracle_sample(args.config, gpu_iters=infos[-1]["iterations"])
+        cpu = oracle_sample(args.config, gpu_iters=infos[-1]["iterations"], opts=lib_opts)
         cpu["cores"] = 1
 
     if rank == 0:
@@ -359,6 +366,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "grid": [pb.nx, pb.ny, pb.nz], "dof": n_glob,
+                       **({"options": lib_opts} if lib_opts else {}),
                        "step": "tsp_setup(MECH|FLOW) + FGMRES(64) to rtol 1e-8",
                        "parallelism": "single GPU" if ws == 1 else f"z-slab decomposition over {ws} GPUs (NCCL)",
                        "l2": "inputs larger than L2 (matrices >> 126 MB), no flush"},
