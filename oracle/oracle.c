@@ -442,16 +442,20 @@ static void spgemm(const mcsr *A, const mcsr *B, mcsr *Cm)
     free(mark); free(rp);
 }
 
-/* l1 row norms d_i = sum_j |a_ij| (R-smoother: l1-Jacobi) */
+/* l1 row norms d_i = sign(a_ii) sum_j |a_ij| (R-smoother: l1-Jacobi; R-l1: a row whose diagonal
+ * is negative keeps that sign, so the smoother's correction points the way Jacobi's would) */
 static void l1_diag(olevel *L)
 {
     const mcsr *A = &L->A;
     for (int c = 0; c < A->nc; ++c) {
         L->dl1[c] = (double *)xmalloc(sizeof(double) * (A->n + 1));
         for (int i = 0; i < A->n; ++i) {
-            double s = 0.0;
-            for (int64_t q = A->rp[i]; q < A->rp[i + 1]; ++q) s = s + fabs(A->v[c][q]);
-            L->dl1[c][i] = s;
+            double s = 0.0, aii = 0.0;
+            for (int64_t q = A->rp[i]; q < A->rp[i + 1]; ++q) {
+                s = s + fabs(A->v[c][q]);
+                if (A->ci[q] == i) aii = A->v[c][q];
+            }
+            L->dl1[c][i] = aii < 0.0 ? -s : s;
         }
     }
 }

@@ -36,13 +36,19 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t x)
 __device__ __forceinline__ uint64_t prio(int i) { return ((uint64_t)fmix32((uint32_t)i) << 32) | (uint64_t)(uint32_t)i; }
 
 // ------------------------------------------------------------------ l1 norms: d_i = fold_j |a_ij|
-__global__ void k_l1(int n, int nc, const int32_t *__restrict__ rp, const double *__restrict__ v, double *dl1, double *dinv)
+__global__ void k_l1(int n, int nc, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const double *__restrict__ v,
+                     double *dl1, double *dinv)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     for (int c = 0; c < nc; ++c) {
-        double s = 0.0;
-        for (int64_t q = rp[i]; q < rp[i + 1]; ++q) s = __dadd_rn(s, fabs(v[q * nc + c]));
+        double s = 0.0, aii = 0.0;
+        for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+            s = __dadd_rn(s, fabs(v[q * nc + c]));
+            if (ci[q] == i) aii = v[q * nc + c];
+        }
+        if (aii < 0.0) s = -s;                             // R-l1: the sign of the diagonal
+
         dl1[(int64_t)i * nc + c] = s;
         dinv[(int64_t)i * nc + c] = s != 0.0 ? 1.0 / s : 0.0;
     }
@@ -781,7 +787,7 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
         const int n = L.n;
         const int nown = n;   // rows of this rank; columns >= nown are ghosts
         L.dl1.alloc((size_t)std::max(n, 1) * nc); L.dinv.alloc((size_t)std::max(n, 1) * nc);
-        if (n) k_l1<<<grid_for(n, 256), 256, 0, c.s>>>(n, nc, L.A.rp, L.A.v, L.dl1, L.dinv);
+        if (n) k_l1<<<grid_for(n, 256), 256, 0, c.s>>>(n, nc, L.A.rp, L.A.ci, L.A.v, L.dl1, L.dinv);
         c.launches++;
         if (L.dist && L.hp->any()) {
             L.dinv_gh.alloc((size_t)std::max(L.hp->nghost(), 1) * nc);

@@ -394,3 +394,15 @@ def test_fgmres_reports_non_convergence():
     o = oracle.Oracle(pb).setup()
     x, info = o.solve(pb.b, rtol=1e-14, m=4, maxit=6)
     assert info["status"] == 1 and info["iterations"] == 6
+
+
+def test_vcycle_is_sign_equivariant():
+    """R-l1: d_i = sign(a_ii) sum_j |a_ij|.  Strength, aggregation and the prolongator depend on |a_ij| and
+    D^-1 A only, so the V-cycle of -A must be exactly minus the V-cycle of A (the unsigned l1 scaling breaks
+    this: a negative-diagonal row would be 'smoothed' uphill).  Exact in IEEE arithmetic (negation)."""
+    A = _laplacian7(7, 6, 5, neumann=False)
+    b = np.random.default_rng(4).uniform(-1, 1, A.shape[0])
+    xa = oracle.Amg(A.indptr, A.indices, A.data, None, amg_coarse_max=20).vcycle(b)
+    xn = oracle.Amg(A.indptr, A.indices, -A.data, None, amg_coarse_max=20).vcycle(b)
+    assert len(oracle.Amg(A.indptr, A.indices, A.data, None, amg_coarse_max=20).levels()) >= 3
+    assert np.array_equal(xn, -xa)
