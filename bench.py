@@ -58,13 +58,15 @@ def dist_init():
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+    """nvidia-smi sampler (B200_PROFILING.md).  It is started before the last warm-up step (its start-up
+    briefly contends with the driver) and only the samples stamped inside the timed region are kept."""
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu):
         self.gpu = gpu
         self.p = None
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
@@ -73,25 +75,40 @@ class Clocks:
         except Exception:
             self.p = None
 
+    def begin(self):
+        import datetime
+        self.t0 = datetime.datetime.now()
+
+    def end(self):
+        import datetime
+        self.t1 = datetime.datetime.now()
+
     def stop(self):
+        import datetime
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.p.terminate()
         out, _ = self.p.communicate(timeout=10)
-        sm, smax, reasons = [], [], set()
+        rows = []
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
+            if len(f) < 10:
                 continue
             try:
-                sm.append(float(f[1])); smax.append(float(f[2]))
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f")
+                rows.append((ts, float(f[2]), float(f[3]), f[6:10]))
             except ValueError:
                 continue
-            for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), f[5:9]):
+        inside = [r for r in rows if self.t0 and self.t1 and self.t0 <= r[0] <= self.t1]
+        use = inside or rows
+        reasons = set()
+        for r in use:
+            for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), r[3]):
                 if val.lower() == "active":
                     reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [r[1] for r in use]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(r[2] for r in use) if use else None,
+                "reasons": sorted(reasons), "samples": len(use), "window": "timed region" if inside else "whole run"}
 
 
 def cpu_cores():
@@ -217,22 +234,25 @@ def main():
         t = time.perf_counter()
         g.setup()                                  # tsp_setup synchronises its stream
         setup_s.append(time.perf_counter() - t)
+        print(f"[bench] setup {1e3 * setup_s[-1]:.1f} ms", file=sys.stderr, flush=True)
         return g.solve(b, x, rtol=1e-8, restart=64, max_iters=1000)
 
     # warm-up; the last warm-up step records every kernel class (the per-class table and the choice of
     # the dominant class); the timed steps then record only the dominant class, whose live CUDA-event
     # times give the roofline (two events per recorded launch; recording all classes costs ~2 %)
+    clocks = Clocks(local)
     for w in range(max(args.warmup, 0)):
         if w == args.warmup - 1:
             g.prof_enable(True)
+            clocks.start()
         info = step()
     torch.cuda.synchronize()
     prof_all = g.prof_read() if args.warmup > 0 else {}
     g.prof_enable(False)
     dom_name = max(prof_all.items(), key=lambda kv: kv[1]["ms"])[0] if prof_all else None
 
-    clocks = Clocks(local)
-    clocks.start()
+    if clocks.p is None:
+        clocks.start()
     g.prof_enable(True)
     if dom_name:
         g.prof_classes([dom_name])
@@ -241,6 +261,7 @@ def main():
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stream = torch.cuda.current_stream()
+    clocks.begin()
     e0.record(stream)
     iters, infos = 0, []
     setup_s.clear()
@@ -253,6 +274,7 @@ def main():
     if ws > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
+    clocks.end()
     clk = clocks.stop()
     prof = g.prof_read()
     st = g.stats()

@@ -75,7 +75,11 @@ typedef struct {
                                     1 algebraic row-sum lumping (eq:FS_RSL): needs TSP_SETUP_MECH first */
     int rsl_iters;               /* fs_mode 1: A_uu^-1 ~ this many M_uu-preconditioned Richardson steps, 2 */
     double fs_modulus_scale;     /* fs_mode 0: K_dr -> scale * K_dr, i.e. D_fs / scale (default 1) */
-    int reserved[4];
+    /* second stage M_L */
+    int second_stage;            /* 0 tile ILU(0) (the paper's option 2, SPE10); 1 hybrid block Gauss-Seidel with the
+                                    16^3 tile as the "processor" (option 1, the staircase) */
+    int local_sweeps;            /* Algorithm 1 steps 6-8 repeated this many times (default 1; the staircase used 3) */
+    int reserved[2];
 } tsp_options;
 
 /* BSR block matrix given to tsp_create (nrows block rows). */

@@ -35,7 +35,7 @@ class Opts(C.Structure):
                 ("zblock", C.c_int), ("tile_x", C.c_int), ("tile_y", C.c_int), ("tile_z", C.c_int),
                 ("mech_mode", C.c_int), ("pres_mode", C.c_int), ("local_mode", C.c_int), ("ff_mode", C.c_int),
                 ("cpr_mode", C.c_int), ("aps_mode", C.c_int), ("fs_mode", C.c_int), ("rsl_iters", C.c_int),
-                ("fs_modulus_scale", C.c_double)]
+                ("fs_modulus_scale", C.c_double), ("second_stage", C.c_int), ("local_sweeps", C.c_int)]
 
 
 class Info(C.Structure):
@@ -78,6 +78,9 @@ def lib():
         L.orc_ilu_build.restype = C.c_void_p
         L.orc_ilu_apply.argtypes = [C.c_void_p, _F64, _F64]
         L.orc_ilu_free.argtypes = [C.c_void_p]
+        L.orc_bgs_build.argtypes = [C.c_int] * 6 + [_I32, _I32, _F64]
+        L.orc_bgs_build.restype = C.c_void_p
+        L.orc_bgs_apply.argtypes = [C.c_void_p, _F64, _F64]
         _LIB = L
     return _LIB
 
@@ -270,4 +273,19 @@ class Ilu:
         w = np.ascontiguousarray(w, np.float64)
         dz = np.zeros_like(w)
         lib().orc_ilu_apply(self.h, _p(w), _p(dz))
+        return dz
+
+
+class Bgs(Ilu):
+    """Standalone oracle hybrid block Gauss-Seidel sweep (tile = processor), for pins."""
+
+    def __init__(self, nx, ny, nz, tile, rp, ci, v):
+        self._keep = (np.ascontiguousarray(rp, np.int32), np.ascontiguousarray(ci, np.int32),
+                      np.ascontiguousarray(v, np.float64))
+        self.h = lib().orc_bgs_build(nx, ny, nz, tile[0], tile[1], tile[2], *[_p(x) for x in self._keep])
+
+    def apply(self, w):
+        w = np.ascontiguousarray(w, np.float64)
+        dz = np.zeros_like(w)
+        lib().orc_bgs_apply(self.h, _p(w), _p(dz))
         return dz

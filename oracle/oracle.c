@@ -672,6 +672,54 @@ void orc_ilu_apply(void *ilu, const double *w, double *dz)
 }
 void orc_ilu_free(void *ilu) { oilu *I = (oilu *)ilu; if (!I) return; free(I->rp); free(I->ci); free(I->F); free(I->Uinv); free(I); }
 
+/* ---------------- option 1 of the second stage: hybrid block Gauss-Seidel (hbgs) ----------------
+ * One sweep from zero = the block forward substitution (L + D)^-1 of the tile-local lower triangle of
+ * P S_ff^FS P^T in natural order (x fastest), D = the 2x2 diagonal blocks (inverted exactly; singular ones
+ * perturbed as the ILU's); couplings leaving the tile are the "hybrid" (Jacobi) part and enter
+ * only through the residual of the next sweep (R-hbgs). */
+void *orc_bgs_build(int nx, int ny, int nz, int tx, int ty, int tz, const int32_t *rp, const int32_t *ci, const double *v)
+{
+    oilu *I = (oilu *)xcalloc(1, sizeof(oilu));
+    int nc = nx * ny * nz;
+    I->nc = nc; I->nx = nx; I->ny = ny; I->nz = nz; I->tx = tx; I->ty = ty; I->tz = tz;
+    I->rp = (int32_t *)xcalloc(nc + 1, sizeof(int32_t));
+    for (int i = 0; i < nc; ++i) { int c = 0; for (int64_t q = rp[i]; q < rp[i + 1]; ++q) c += same_tile(I, i, ci[q]); I->rp[i + 1] = I->rp[i] + c; }
+    I->ci = (int32_t *)xmalloc(sizeof(int32_t) * (I->rp[nc] + 1));
+    I->F = (double *)xmalloc(sizeof(double) * 4 * (I->rp[nc] + 1));
+    I->Uinv = (double *)xmalloc(sizeof(double) * 4 * (nc + 1));
+    for (int i = 0; i < nc; ++i) {
+        int64_t t = I->rp[i];
+        for (int64_t q = rp[i]; q < rp[i + 1]; ++q)
+            if (same_tile(I, i, ci[q])) { I->ci[t] = ci[q]; memcpy(&I->F[4 * t], &v[4 * q], 4 * sizeof(double)); ++t; }
+        double D[4] = {0, 0, 0, 0};
+        for (int64_t q = I->rp[i]; q < I->rp[i + 1]; ++q) if (I->ci[q] == i) memcpy(D, &I->F[4 * q], sizeof(D));
+        double sc = fmax(fmax(fabs(D[0]), fabs(D[1])), fmax(fabs(D[2]), fabs(D[3])));
+        double det = D[0] * D[3] - D[1] * D[2];
+        if (sc == 0.0 || fabs(det) <= 1e-14 * sc * sc) {
+            double dl = 1e-12 * (sc > 0.0 ? sc : 1.0);
+            D[0] += dl; D[3] += dl; I->perturbed++;
+        }
+        inv2(D, &I->Uinv[4 * i]);
+    }
+    return I;
+}
+void orc_bgs_apply(void *bgs, const double *w, double *dz)
+{
+    oilu *I = (oilu *)bgs;
+    for (int i = 0; i < I->nc; ++i) {
+        double a = w[2 * i], b = w[2 * i + 1];
+        for (int64_t q = I->rp[i]; q < I->rp[i + 1]; ++q) {
+            int k = I->ci[q]; if (k >= i) continue;
+            const double *A = &I->F[4 * q];
+            a -= A[0] * dz[2 * k] + A[1] * dz[2 * k + 1];
+            b -= A[2] * dz[2 * k] + A[3] * dz[2 * k + 1];
+        }
+        const double *Di = &I->Uinv[4 * i];
+        dz[2 * i] = Di[0] * a + Di[1] * b;
+        dz[2 * i + 1] = Di[2] * a + Di[3] * b;
+    }
+}
+
 /* ======================================================================
  * the handle: inputs, setup products (a1-a5), Algorithm 1, operator, FGMRES
  * ==================================================================== */
@@ -731,6 +779,7 @@ void orc_default_opts(orc_opts *o)
     o->amg_theta = 0.25; o->amg_coarse_max = 64; o->amg_max_levels = 12;
     o->zblock = 16; o->tile_x = 16; o->tile_y = 16; o->tile_z = 16;
     o->rsl_iters = 2; o->fs_modulus_scale = 1.0;
+    o->second_stage = 0; o->local_sweeps = 1;
 }
 
 orc *orc_create(const orc_desc *d, const orc_opts *o)
@@ -922,7 +971,8 @@ int orc_setup(orc *h)
     }
     /* ---- a5: local stage M_L on P S_ff^FS P^T */
     if (h->o.local_mode == 0) {
-        h->ilu = (oilu *)orc_ilu_build(h->nx, h->ny, h->nz, h->o.tile_x, h->o.tile_y, h->o.tile_z, h->Sff.rp, h->Sff.ci, h->Sff.v);
+        h->ilu = (oilu *)(h->o.second_stage == 1 ? orc_bgs_build : orc_ilu_build)(h->nx, h->ny, h->nz, h->o.tile_x, h->o.tile_y,
+                                                                                h->o.tile_z, h->Sff.rp, h->Sff.ci, h->Sff.v);
     } else if (h->o.local_mode == 1) {
         int N = 2 * Nc;
         h->dense_ff = (double *)xcalloc((int64_t)N * N, sizeof(double));
@@ -992,18 +1042,22 @@ int orc_apply(orc *h, const double *v, double *z)
     if (h->o.pres_mode == 0) vcycle(h->pres, 0, 0, wp, zp);
     else dense_lu_solve(Nc, h->dense_pp, h->piv_pp, wp, zp);
     if (h->o.local_mode != 2) {
-        /* step 6: [w_s; w_p] = [y_s; y_p] - [[A_ss, A_sp^FS],[A_ps, A_pp^FS]] [z_s; z_p] */
+        /* steps 6-8, repeated local_sweeps times (R-sweeps: "several sweeps") */
         double *ws = (double *)xmalloc(sizeof(double) * Nc), *wp2 = (double *)xmalloc(sizeof(double) * Nc);
-        memcpy(ws, ys, sizeof(double) * Nc); memcpy(wp2, yp, sizeof(double) * Nc);
-        spmv_sub(&h->Ass, 0, zs, ws); spmv_sub(&h->Asp_fs, 0, zp, ws);
-        spmv_sub(&h->Aps, 0, zs, wp2); spmv_sub(&h->App_fs, 0, zp, wp2);
-        /* step 7: [dz_s; dz_p] = P^T M_L^-1 P [w_s; w_p] */
         double *wf = (double *)xmalloc(sizeof(double) * 2 * Nc), *dzf = (double *)xmalloc(sizeof(double) * 2 * Nc);
-        for (int K = 0; K < Nc; ++K) { wf[2 * K] = ws[K]; wf[2 * K + 1] = wp2[K]; }
-        if (h->o.local_mode == 0) orc_ilu_apply(h->ilu, wf, dzf);
-        else dense_lu_solve(2 * Nc, h->dense_ff, h->piv_ff, wf, dzf);
-        /* step 8: z += dz */
-        for (int K = 0; K < Nc; ++K) { zs[K] += dzf[2 * K]; zp[K] += dzf[2 * K + 1]; }
+        int sweeps = h->o.local_sweeps > 0 ? h->o.local_sweeps : 1;
+        for (int sw = 0; sw < sweeps; ++sw) {
+            /* step 6: [w_s; w_p] = [y_s; y_p] - [[A_ss, A_sp^FS],[A_ps, A_pp^FS]] [z_s; z_p] */
+            memcpy(ws, ys, sizeof(double) * Nc); memcpy(wp2, yp, sizeof(double) * Nc);
+            spmv_sub(&h->Ass, 0, zs, ws); spmv_sub(&h->Asp_fs, 0, zp, ws);
+            spmv_sub(&h->Aps, 0, zs, wp2); spmv_sub(&h->App_fs, 0, zp, wp2);
+            /* step 7: [dz_s; dz_p] = P^T M_L^-1 P [w_s; w_p]; M_L = ILU(0) or hbgs */
+            for (int K = 0; K < Nc; ++K) { wf[2 * K] = ws[K]; wf[2 * K + 1] = wp2[K]; }
+            if (h->o.local_mode == 0) (h->o.second_stage == 1 ? orc_bgs_apply : orc_ilu_apply)(h->ilu, wf, dzf);
+            else dense_lu_solve(2 * Nc, h->dense_ff, h->piv_ff, wf, dzf);
+            /* step 8: z += dz */
+            for (int K = 0; K < Nc; ++K) { zs[K] += dzf[2 * K]; zp[K] += dzf[2 * K + 1]; }
+        }
         free(ws); free(wp2); free(wf); free(dzf);
     }
     for (int K = 0; K < Nc; ++K) { zf[2 * K] = zs[K]; zf[2 * K + 1] = zp[K]; }   /* P */

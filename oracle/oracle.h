@@ -38,6 +38,9 @@ typedef struct {
     int fs_mode;                  /* 0: D_fs given (eq:FS_Dps_Dpp); 1: row-sum lumping RSL (eq:FS_RSL) */
     int rsl_iters;                /* RSL: A_uu^-1 ~ this many M_uu-preconditioned Richardson steps, default 2 */
     double fs_modulus_scale;      /* fs_mode 0: modulus K_dr -> scale K_dr, i.e. D_fs / scale (remark P:443), default 1 */
+    /* NEXT-f2: the second stage M_L */
+    int second_stage;             /* 0: tile ILU(0) (option 2); 1: hybrid block Gauss-Seidel, tile = processor (option 1) */
+    int local_sweeps;             /* steps 6-8 repeated this many times ("several sweeps"; 3 for the staircase) */
 } orc_opts;
 
 typedef struct {
@@ -79,4 +82,6 @@ void *orc_ilu_build(int nx, int ny, int nz, int tx, int ty, int tz, const int32_
                     const double *v);
 void orc_ilu_apply(void *ilu, const double *w, double *dz);
 void orc_ilu_free(void *ilu);
+void *orc_bgs_build(int nx, int ny, int nz, int tx, int ty, int tz, const int32_t *rp, const int32_t *ci, const double *v);
+void orc_bgs_apply(void *bgs, const double *w, double *dz);     /* one hbgs sweep from zero: tile (L+D)^-1 w */
 #endif

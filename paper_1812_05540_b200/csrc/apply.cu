@@ -108,6 +108,13 @@ __global__ void __launch_bounds__(256) k_step34(int Nc, const int64_t *__restric
     wp[i] = yf.own[2 * (int64_t)i + 1] - acc;
 }
 
+// z_f (interleaved) -> (z_s, z_p) for the next second-stage sweep
+__global__ void k_split_f(int Nc, const double *__restrict__ zf, double *__restrict__ zs, double *__restrict__ zp)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < Nc) { zs[i] = zf[2 * (int64_t)i]; zp[i] = zf[2 * (int64_t)i + 1]; }
+}
+
 static double sell_bytes(const Sell &S) { return (double)S.slots * 32 * (4.0 + 8.0 * S.bs); }
 
 void op_apply(Ctx &c, const double *x, double *y)
@@ -152,10 +159,17 @@ void prec_apply(Ctx &c, const double *v, double *z)
     // step 5: z_p = M_pp^-1 w_p
     amg_vcycle(c, c.pres, c.w_wp, c.w_zp, false);
     // steps 6-8: w_f = y_f - S_ff^FS z_f ; z_f += P^T M_L^-1 P w_f
+    // repeated local_sweeps times ("several sweeps"): the next sweep's z = this sweep's z_f
     const int ng = c.hf.nghost();
-    halo_exchange(c, c.hf, 1, c.w_tmp, c.gh_f2);
-    halo_exchange(c, c.hf, 1, c.w_zp, c.gh_f2.p + ng);
-    ilu_apply_fused(c, c.w_yf, c.w_tmp, c.w_zp, zf);
+    for (int sw = 0; sw < c.o.local_sweeps; ++sw) {
+        if (sw > 0) {
+            if (c.Nc) k_split_f<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(c.Nc, zf, c.w_tmp, c.w_zp);
+            c.launches++;
+        }
+        halo_exchange(c, c.hf, 1, c.w_tmp, c.gh_f2);
+        halo_exchange(c, c.hf, 1, c.w_zp, c.gh_f2.p + ng);
+        ilu_apply_fused(c, c.w_yf, c.w_tmp, c.w_zp, zf);
+    }
     c.launches += 2;
     TSP_CUDA(cudaGetLastError());
 }

@@ -3,6 +3,9 @@
 // every numerical step is a kernel in apply.cu / amg.cu / ilu.cu / krylov.cu.
 #include <cstdio>
 #include <cstring>
+#include <list>
+#include <map>
+#include <mutex>
 
 #include "tsp_internal.cuh"
 
@@ -11,6 +14,83 @@ namespace tsp {
 static thread_local std::string g_err;
 thread_local cudaStream_t g_alloc_stream = 0;
 void set_error(const std::string &m) { g_err = m; }
+static bool dbg_on() { static const bool on = getenv("TSP_DEBUG") != nullptr; return on; }
+double dbg_now()
+{
+    if (!dbg_on()) return 0.0;
+    timespec t; clock_gettime(CLOCK_MONOTONIC, &t);
+    return t.tv_sec + 1e-9 * t.tv_nsec;
+}
+// per-stream cache of released device blocks, exact size (see tsp_internal.cuh); bounded, LRU-evicted
+namespace {
+struct Cache {
+    std::multimap<size_t, void *> free;
+    std::list<std::pair<size_t, void *>> lru;   // insertion order, for eviction
+    size_t bytes = 0;
+};
+std::mutex g_cache_mu;
+std::map<cudaStream_t, Cache> g_cache;
+constexpr size_t kCacheMax = size_t(48) << 30;
+}  // namespace
+void *dev_alloc(size_t bytes, cudaStream_t s)
+{
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        auto &C = g_cache[s];
+        auto it = C.free.find(bytes);
+        if (it != C.free.end()) {
+            void *p = it->second;
+            C.free.erase(it);
+            for (auto l = C.lru.begin(); l != C.lru.end(); ++l)
+                if (l->second == p) { C.lru.erase(l); break; }
+            C.bytes -= bytes;
+            return p;
+        }
+    }
+    void *p = nullptr;
+    const double t0 = dbg_now();
+    cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    if (e == cudaErrorMemoryAllocation) {          // give the cached blocks back and retry once
+        (void)cudaGetLastError();
+        dev_cache_flush(s);
+        e = cudaMallocAsync(&p, bytes, s);
+    }
+    TSP_CUDA(e);
+    dbg_alloc(t0, bytes);
+    return p;
+}
+void dev_free(void *p, size_t bytes, cudaStream_t s)
+{
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto &C = g_cache[s];
+    C.free.emplace(bytes, p);
+    C.lru.emplace_back(bytes, p);
+    C.bytes += bytes;
+    while (C.bytes > kCacheMax && !C.lru.empty()) {
+        auto [b, q] = C.lru.front();
+        C.lru.pop_front();
+        auto range = C.free.equal_range(b);
+        for (auto it = range.first; it != range.second; ++it)
+            if (it->second == q) { C.free.erase(it); break; }
+        C.bytes -= b;
+        cudaFreeAsync(q, s);
+    }
+}
+void dev_cache_flush(cudaStream_t s)
+{
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cache.find(s);
+    if (it == g_cache.end()) return;
+    for (auto &kv : it->second.free) cudaFreeAsync(kv.second, s);
+    g_cache.erase(it);
+}
+
+void dbg_alloc(double t0, size_t bytes)
+{
+    if (!dbg_on()) return;
+    const double dt = dbg_now() - t0;
+    if (dt > 2e-3) fprintf(stderr, "[tsp alloc] %.1f MB took %.1f ms\n", bytes / 1e6, dt * 1e3);
+}
 
 // bind the allocation stream of this API call; keep the default pool resident
 struct StreamScope {
@@ -105,6 +185,7 @@ tsp_status tsp_default_options(tsp_options *o)
     o->amg_theta = 0.25; o->amg_coarse_max = 64; o->amg_max_levels = 12; o->zblock = 16;
     o->tile_x = o->tile_y = o->tile_z = 16;
     o->rsl_iters = 2; o->fs_modulus_scale = 1.0;
+    o->second_stage = 0; o->local_sweeps = 1;
     return TSP_OK;
 }
 
@@ -136,6 +217,8 @@ tsp_status tsp_create(tsp_handle *out, const tsp_desc *d)
     if (c->o.tile_x <= 0 || c->o.tile_y <= 0 || c->o.tile_z <= 0) c->o.tile_x = c->o.tile_y = c->o.tile_z = 16;
     if (c->o.replicate_rows <= 0) c->o.replicate_rows = 32768;
     if (c->o.rsl_iters <= 0) c->o.rsl_iters = 2;
+    if (c->o.local_sweeps <= 0) c->o.local_sweeps = 1;
+    TSP_REQUIRE(c->o.second_stage == 0 || c->o.second_stage == 1, TSP_ERR_INVALID_ARG, "second_stage must be 0 (ILU0) or 1 (BGS)");
     if (!(c->o.fs_modulus_scale > 0)) c->o.fs_modulus_scale = 1.0;
     TSP_REQUIRE(c->o.cpr_mode == 0 || c->o.cpr_mode == 1, TSP_ERR_INVALID_ARG, "cpr_mode must be 0 (quasi) or 1 (true IMPES)");
     TSP_REQUIRE(c->o.aps_mode == 0 || c->o.aps_mode == 1, TSP_ERR_INVALID_ARG, "aps_mode must be 0 (full) or 1 (diagonal)");
@@ -421,8 +504,11 @@ void tsp_destroy(tsp_handle h)
     cudaStreamSynchronize(h->s);
     for (auto &e : h->prof.pool) cudaEventDestroy(e);
     Comm *cm = h->comm;
+    cudaStream_t s = h->s;
     delete h;
     delete cm;
+    dev_cache_flush(s);
+    cudaStreamSynchronize(s);
 }
 
 }  // extern "C"

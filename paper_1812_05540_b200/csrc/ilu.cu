@@ -80,8 +80,10 @@ __device__ __forceinline__ void mm2(const double a[4], const double b[4], double
 }
 
 // a5: one thread per x-line, lines in (j+k) order, cells along x sequential
+// plain = 1 (second stage = hybrid block GS): D_K = A_KK^-1 without the ILU Schur updates
 __global__ void k_ilu_factor(TileGeo g, const int32_t *__restrict__ lines, const int32_t *__restrict__ lvlptr,
-                             const double *__restrict__ ival, double *__restrict__ dinv, unsigned long long *__restrict__ npert)
+                             const double *__restrict__ ival, double *__restrict__ dinv, unsigned long long *__restrict__ npert,
+                             int plain)
 {
     const int64_t t = blockIdx.x;
     const int TI = t % g.ntx, TJ = (t / g.ntx) % g.nty, TK = t / ((int64_t)g.ntx * g.nty);
@@ -93,7 +95,7 @@ __global__ void k_ilu_factor(TileGeo g, const int32_t *__restrict__ lines, const
             for (int li = 0; li < len; ++li) {
                 double U[4];
                 ld2x2(ival, g, t, lk, lj, 3, li, U);
-                for (int s = 0; s < 3; ++s) {
+                for (int s = 0; s < (plain ? 0 : 3); ++s) {
                     int nlk = lk, nlj = lj, nli = li;
                     if (s == 0) nlk--; else if (s == 1) nlj--; else nli--;
                     if (nlk < 0 || nlj < 0 || nli < 0) continue;   // outside the tile: dropped (block Jacobi)
@@ -162,6 +164,7 @@ __device__ __forceinline__ void pf_load(const double *__restrict__ ival, const d
     for (int e = 0; e < 4; ++e) P[12 + e] = dinv[didx(g, t, lk, lj, e, li)];
 }
 
+template <bool BGS>
 __global__ void __launch_bounds__(256) k_ilu_apply2(TileGeo g, const int32_t *__restrict__ lines, const int32_t *__restrict__ lvlptr,
                                                     const double *__restrict__ ival, const double *__restrict__ dinv,
                                                     const double *__restrict__ yf, const double *__restrict__ zs,
@@ -243,6 +246,11 @@ __global__ void __launch_bounds__(256) k_ilu_apply2(TileGeo g, const int32_t *__
         }
         affine_scan<true>(M, c, lseg, W);
         if (ok) { sm[sidx(g, lk, lj, li)] = c[0]; sm[sidx(g, lk, lj, li) + 1] = c[1]; }
+        if (BGS && ok) {                          // hybrid block GS: the forward sweep is the whole M_L (step 8)
+            const int64_t gc = gi + sy * (TJ * g.ty + lj) + sz * (TK * g.tz + lk);
+            zout[2 * gc] = zs[gc] + c[0];
+            zout[2 * gc + 1] = zp[gc] + c[1];
+        }
         // prefetch the next level's blocks (or the backward sweep's first level)
         {
             const int ln = l + 1 < g.nlev ? l + 1 : g.nlev - 1;
@@ -254,7 +262,8 @@ __global__ void __launch_bounds__(256) k_ilu_apply2(TileGeo g, const int32_t *__
         }
         __syncthreads();
     }
-    // ---------------- backward
+    // ---------------- backward (ILU only)
+    if constexpr (!BGS)
     for (int l = g.nlev - 1; l >= 0; --l) {
         const int idx = lvlptr[l] + slot0;
         const bool lv = idx < lvlptr[l + 1];
@@ -342,7 +351,7 @@ void ilu_setup(Ctx &c, const double *)
     if (c.Nc) k_ilu_fill<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(g, c.ny, c.ff.rp, c.ff.gci.p ? c.ff.gci.p : c.ff.ci.p, c.ff.v, c.fs_eff,
                                                              c.ilu_val);
     c.dcount.zero(c.s);
-    k_ilu_factor<<<c.ntiles, 32, 0, c.s>>>(g, c.ilu_cells, c.ilu_lvlptr, c.ilu_val, c.ilu_dinv, c.dcount);
+    k_ilu_factor<<<c.ntiles, 32, 0, c.s>>>(g, c.ilu_cells, c.ilu_lvlptr, c.ilu_val, c.ilu_dinv, c.dcount, c.o.second_stage == 1);
     TSP_CUDA(cudaGetLastError());
     unsigned long long np = 0;
     TSP_CUDA(cudaMemcpyAsync(&np, c.dcount, sizeof(np), cudaMemcpyDeviceToHost, c.s));
@@ -357,13 +366,14 @@ void ilu_apply_fused(Ctx &c, const double *yf, const double *zs, const double *z
     const size_t smem = sizeof(double) * 2 * (size_t)g.tx * g.ty * g.tz;
     static bool attr_set = false;
     if (!attr_set) {
-        TSP_CUDA(cudaFuncSetAttribute(k_ilu_apply2, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        TSP_CUDA(cudaFuncSetAttribute(k_ilu_apply2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        TSP_CUDA(cudaFuncSetAttribute(k_ilu_apply2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         attr_set = true;
     }
     TSP_REQUIRE(smem <= 227 * 1024, TSP_ERR_INVALID_ARG, "ILU tile too large for shared memory");
     const double *zs_gh = c.gh_f2.p, *zp_gh = c.gh_f2.p ? c.gh_f2.p + c.hf.nghost() : nullptr;
     prof_begin(c, PK_ILU);
-    if (c.ntiles) k_ilu_apply2<<<c.ntiles, 256, smem, c.s>>>(g, c.ilu_cells, c.ilu_lvlptr, c.ilu_val, c.ilu_dinv, yf, zs, zp, zs_gh,
+    if (c.ntiles) (c.o.second_stage == 1 ? k_ilu_apply2<true> : k_ilu_apply2<false>)<<<c.ntiles, 256, smem, c.s>>>(g, c.ilu_cells, c.ilu_lvlptr, c.ilu_val, c.ilu_dinv, yf, zs, zp, zs_gh,
                                                            zp_gh, zf_out);
     prof_end(c, PK_ILU, (28.0 * 8 + 32 + 16 + 16 + 16) * c.Nc);
     c.launches += 1;

@@ -32,26 +32,36 @@ struct Error {
     } while (0)
 
 // ------------------------------------------------------------------ device buffers
-// Stream-ordered allocation (cudaMallocAsync on the stream of the API call in
-// progress, pool kept resident): setup allocates per level without device syncs.
+// Stream-ordered allocation on the stream of the API call in progress, through a per-stream
+// cache of released blocks keyed by exact size (capi.cu): a repeated tsp_setup requests the same
+// sizes, so after the first one no allocation reaches the driver (the stream-ordered pool grew
+// by a few hundred MB now and then under the interleaved lifetimes of the two hierarchies, and a
+// growth step cost 0.1-0.6 s).  Reuse within one stream is safe in stream order.
 extern thread_local cudaStream_t g_alloc_stream;
+double dbg_now();                              // TSP_DEBUG: wall clock (0 when off)
+void dbg_alloc(double t0, size_t bytes);       // TSP_DEBUG: report slow allocations
+void *dev_alloc(size_t bytes, cudaStream_t s);
+void dev_free(void *p, size_t bytes, cudaStream_t s);
+void dev_cache_flush(cudaStream_t s);          // return the stream's cached blocks to the pool
 template <class T>
 struct DBuf {
     T *p = nullptr;
     size_t n = 0;
+    cudaStream_t st = 0;
     DBuf() = default;
     DBuf(const DBuf &) = delete;
     DBuf &operator=(const DBuf &) = delete;
-    DBuf(DBuf &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
-    DBuf &operator=(DBuf &&o) noexcept { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; return *this; }
+    DBuf(DBuf &&o) noexcept : p(o.p), n(o.n), st(o.st) { o.p = nullptr; o.n = 0; }
+    DBuf &operator=(DBuf &&o) noexcept { release(); p = o.p; n = o.n; st = o.st; o.p = nullptr; o.n = 0; return *this; }
     ~DBuf() { release(); }
     void alloc(size_t count) {
         release();
         n = count;
-        if (count) TSP_CUDA(cudaMallocAsync((void **)&p, sizeof(T) * count, g_alloc_stream));
+        st = g_alloc_stream;
+        if (count) p = (T *)dev_alloc(sizeof(T) * count, st);
     }
     void zero(cudaStream_t s) { if (n) TSP_CUDA(cudaMemsetAsync(p, 0, sizeof(T) * n, s)); }
-    void release() { if (p) cudaFreeAsync(p, g_alloc_stream); p = nullptr; n = 0; }
+    void release() { if (p) dev_free(p, sizeof(T) * n, st); p = nullptr; n = 0; }
     operator T *() const { return p; }
 };
 

@@ -29,7 +29,8 @@ class tsp_options(C.Structure):
     _fields_ = [("amg_theta", C.c_double), ("amg_coarse_max", C.c_int), ("amg_max_levels", C.c_int),
                 ("zblock", C.c_int), ("tile_x", C.c_int), ("tile_y", C.c_int), ("tile_z", C.c_int),
                 ("replicate_rows", C.c_int), ("cpr_mode", C.c_int), ("aps_mode", C.c_int), ("fs_mode", C.c_int),
-                ("rsl_iters", C.c_int), ("fs_modulus_scale", C.c_double), ("reserved", C.c_int * 4)]
+                ("rsl_iters", C.c_int), ("fs_modulus_scale", C.c_double), ("second_stage", C.c_int),
+                ("local_sweeps", C.c_int), ("reserved", C.c_int * 2)]
 
 
 class tsp_bsr(C.Structure):

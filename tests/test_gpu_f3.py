@@ -1,4 +1,5 @@
-"""GPU parity of the setup variants against the oracle: true-IMPES
+"""GPU parity of the setup variants and of the second-stage options
+(NEXT-f2: hybrid block Gauss-Seidel, repeated sweeps) against the oracle: true-IMPES
 (eq:CPR_CSL), diagonal A_ps in step 4, fixed-stress modulus scale (remark
 P:443) and RSL fixed stress (eq:FS_RSL).  Same bars as tests/test_gpu_parity.py:
 D^(CPR) and the pressure hierarchy bit-exact, apply <= 1e-10, FGMRES +-1.  RSL goes
@@ -20,6 +21,9 @@ VARIANTS = {
     "true_diag": dict(cpr_mode=1, aps_mode=1),
     "scale": dict(fs_modulus_scale=2.0),
     "rsl": dict(fs_mode=1, rsl_iters=2),
+    # NEXT-f2: the second stage
+    "bgs3": dict(second_stage=1, local_sweeps=3),
+    "ilu2": dict(local_sweeps=2),
 }
 PROBLEMS = {
     "C1": dict(config="C1"),
@@ -100,7 +104,7 @@ def test_rsl_needs_mechanics_first(dev):
         g.setup(TSP_SETUP_FLOW)
 
 
-@pytest.mark.parametrize("vname", ["true", "rsl"])
+@pytest.mark.parametrize("vname", ["true", "rsl", "bgs3"])
 def test_variant_sharded_bitwise(dev, vname):
     """z-slabs (P = 2, 4): D^(CPR), D_fs, one apply and the FGMRES solution bitwise equal to P = 1
     (true-IMPES needs the column entries of the neighbour ranks' boundary rows)."""
