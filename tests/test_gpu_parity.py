@@ -202,3 +202,17 @@ def test_c4_sampled_apply_and_operator(dev):
     xs = torch.zeros(pb.n, dtype=torch.float64, device=dev)
     info = g.solve(_cuda(pb.b), xs)
     assert info["status"] == "OK" and info["true_relres"] <= 1e-8
+
+
+@pytest.mark.parametrize("m", [5, 17])
+def test_solve_parity_short_restart(dev, m):
+    """FGMRES(m) with many restart cycles: every cycle ends with the DCGS2 completion of its last
+    Hessenberg column (krylov.cu); iteration counts and the true residual against the oracle's MGS."""
+    pb, o, g = _pair("C2")
+    xo, io = o.solve(pb.b, rtol=1e-8, m=m, maxit=3000)
+    x = torch.zeros(pb.n, dtype=torch.float64, device=dev)
+    ig = g.solve(_cuda(pb.b), x, rtol=1e-8, restart=m, max_iters=3000)
+    assert ig["status"] == "OK" and io["status"] == 0
+    assert ig["restarts"] >= 2
+    assert abs(ig["iterations"] - io["iterations"]) <= max(1, io["iterations"] // 100)
+    assert ig["true_relres"] <= 1e-8

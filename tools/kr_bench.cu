@@ -571,6 +571,12 @@ int main(int argc, char **argv)
         timeit(nm, vb * (nv + 1), [&] { mdot2<4, 4><<<nch, KB>>>(nv, V, n, V + (nv - 1) * n, w, CH, n, part, nch); });
         snprintf(nm, 64, "mdot2i G4 U2");
         timeit(nm, vb * (nv + 1), [&] { mdot2i<4, 2><<<nch, KB>>>(nv, V, n, V + (nv - 1) * n, w, CH, n, part, nch); });
+        snprintf(nm, 64, "mdot2i G4 U4");
+        timeit(nm, vb * (nv + 1), [&] { mdot2i<4, 4><<<nch, KB>>>(nv, V, n, V + (nv - 1) * n, w, CH, n, part, nch); });
+        snprintf(nm, 64, "mdot2i G2 U8");
+        timeit(nm, vb * (nv + 1), [&] { mdot2i<2, 8><<<nch, KB>>>(nv, V, n, V + (nv - 1) * n, w, CH, n, part, nch); });
+        snprintf(nm, 64, "mdot2i G2 U4");
+        timeit(nm, vb * (nv + 1), [&] { mdot2i<2, 4><<<nch, KB>>>(nv, V, n, V + (nv - 1) * n, w, CH, n, part, nch); });
         snprintf(nm, 64, "mdot2i G8 U2");
         timeit(nm, vb * (nv + 1), [&] { mdot2i<8, 2><<<nch, KB>>>(nv, V, n, V + (nv - 1) * n, w, CH, n, part, nch); });
         snprintf(nm, 64, "mdot2n G4 U2");
