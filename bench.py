@@ -351,10 +351,18 @@ def main():
         d2h = xh.numel() * 8
 
         def e2e_step():
+            t0 = time.perf_counter()
             h = Tsp(pp, **topo, **lib_opts)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
             h.setup()
+            t2 = time.perf_counter()
             inf = h.solve(bh.numpy(), xh.numpy())
+            t3 = time.perf_counter()
             h.close()
+            t4 = time.perf_counter()
+            print(f"[bench] e2e create {1e3 * (t1 - t0):.0f} ms setup {1e3 * (t2 - t1):.0f} ms solve {1e3 * (t3 - t2):.0f} ms "
+                  f"destroy {1e3 * (t4 - t3):.0f} ms", file=sys.stderr, flush=True)
             return inf
 
         e2e_step()

@@ -272,12 +272,7 @@ tsp_status tsp_create(tsp_handle *out, const tsp_desc *d)
     reduce_setup(*c);
     c->fs.alloc(2 * (size_t)std::max(c->Nc, 1));
     if (c->Nc) TSP_CUDA(cudaMemcpyAsync(c->fs, d->fs_diag, sizeof(double) * 2 * c->Nc, on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->s));
-    {
-        std::vector<double> fsh(2 * (size_t)c->Nc);
-        if (c->Nc) TSP_CUDA(cudaMemcpyAsync(fsh.data(), c->fs, sizeof(double) * fsh.size(), cudaMemcpyDeviceToHost, c->s));
-        TSP_CUDA(cudaStreamSynchronize(c->s));
-        for (double v : fsh) TSP_REQUIRE(v >= 0.0, TSP_ERR_INVALID_ARG, "negative fixed-stress diagonal (S:355)");
-    }
+    TSP_REQUIRE(all_nonneg(*c, c->fs, 2 * (int64_t)c->Nc), TSP_ERR_INVALID_ARG, "negative fixed-stress diagonal (S:355)");
     sell_from_csr(*c, c->uu, c->s_uu, 9);
     sell_from_csr(*c, c->uf, c->s_uf, 6);
     sell_from_csr(*c, c->fu, c->s_fu, 6);

@@ -28,22 +28,55 @@ void csr_upload(Ctx &c, Csr &A, int n, int m, int nc, const int32_t *rp, const i
     }
 }
 
-// host-side validation: monotone row pointers, sorted unique in-range columns
-void check_csr(Ctx &c, const Csr &A, const char *name)
+// validation on the device (one flag back to the host): rowptr[0] == 0, monotone row pointers,
+// in-range and strictly increasing (sorted, unique) columns in every row
+__global__ void k_check_csr(int n, int m, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, unsigned *flag)
 {
-    std::vector<int32_t> rp(A.n + 1), ci(A.nnz);
-    TSP_CUDA(cudaMemcpyAsync(rp.data(), A.rp, sizeof(int32_t) * (A.n + 1), cudaMemcpyDeviceToHost, c.s));
-    if (A.nnz) TSP_CUDA(cudaMemcpyAsync(ci.data(), A.ci, sizeof(int32_t) * A.nnz, cudaMemcpyDeviceToHost, c.s));
-    TSP_CUDA(cudaStreamSynchronize(c.s));
-    TSP_REQUIRE(rp[0] == 0, TSP_ERR_INVALID_ARG, std::string(name) + ": rowptr[0] != 0");
-    for (int i = 0; i < A.n; ++i) {
-        TSP_REQUIRE(rp[i + 1] >= rp[i], TSP_ERR_INVALID_ARG, std::string(name) + ": rowptr not monotone");
-        for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
-            TSP_REQUIRE(ci[q] >= 0 && ci[q] < A.m, TSP_ERR_INVALID_ARG, std::string(name) + ": column out of range");
-            TSP_REQUIRE(q == rp[i] || ci[q] > ci[q - 1], TSP_ERR_INVALID_ARG,
-                        std::string(name) + ": columns not sorted/unique in a row");
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    unsigned f = 0;
+    if (i == 0 && rp[0] != 0) f |= 1u;
+    if (i < n) {
+        const int64_t a = rp[i], b = rp[i + 1];
+        if (b < a) f |= 2u;
+        for (int64_t q = a; q < b; ++q) {
+            const int j = ci[q];
+            if (j < 0 || j >= m) f |= 4u;
+            if (q > a && j <= ci[q - 1]) f |= 8u;
         }
     }
+    if (f) atomicOr(flag, f);
+}
+
+void check_csr(Ctx &c, const Csr &A, const char *name)
+{
+    DBuf<unsigned> flag; flag.alloc(1); flag.zero(c.s);
+    k_check_csr<<<grid_for(A.n + 1, 256), 256, 0, c.s>>>(A.n, A.m, A.rp, A.ci, flag);
+    c.launches++;
+    unsigned f = 0;
+    TSP_CUDA(cudaMemcpyAsync(&f, flag.p, sizeof(f), cudaMemcpyDeviceToHost, c.s));
+    TSP_CUDA(cudaStreamSynchronize(c.s));
+    TSP_REQUIRE(!(f & 1u), TSP_ERR_INVALID_ARG, std::string(name) + ": rowptr[0] != 0");
+    TSP_REQUIRE(!(f & 2u), TSP_ERR_INVALID_ARG, std::string(name) + ": rowptr not monotone");
+    TSP_REQUIRE(!(f & 4u), TSP_ERR_INVALID_ARG, std::string(name) + ": column out of range");
+    TSP_REQUIRE(!(f & 8u), TSP_ERR_INVALID_ARG, std::string(name) + ": columns not sorted/unique in a row");
+}
+
+// every value >= 0 (the fixed-stress diagonal)
+__global__ void k_check_nonneg(int64_t n, const double *__restrict__ v, unsigned *flag)
+{
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < n && !(v[k] >= 0.0)) atomicOr(flag, 1u);
+}
+bool all_nonneg(Ctx &c, const double *v, int64_t n)
+{
+    DBuf<unsigned> flag; flag.alloc(1); flag.zero(c.s);
+    if (n) k_check_nonneg<<<grid_for(n, 256), 256, 0, c.s>>>(n, v, flag);
+    c.launches++;
+    unsigned f = 0;
+    TSP_CUDA(cudaMemcpyAsync(&f, flag.p, sizeof(f), cudaMemcpyDeviceToHost, c.s));
+    TSP_CUDA(cudaStreamSynchronize(c.s));
+    return f == 0;
 }
 
 __global__ void k_sell_width(int n, const int32_t *__restrict__ rp, int64_t *__restrict__ w)

@@ -258,6 +258,7 @@ void *scratch(Ctx &c, size_t bytes);
 void csr_upload(Ctx &c, Csr &A, int n, int m, int nc, const int32_t *rp, const int32_t *ci, const double *v, bool on_device);
 void sell_from_csr(Ctx &c, const Csr &A, Sell &S, int bs, const int *val_map = nullptr);
 void check_csr(Ctx &c, const Csr &A, const char *name);
+bool all_nonneg(Ctx &c, const double *v, int64_t n);
 
 // operator / Algorithm 1 pieces (apply.cu)
 void op_apply(Ctx &c, const double *x, double *y);
