@@ -513,25 +513,13 @@ static int64_t rowptr_from_counts(Ctx &c, DBuf<int32_t> &cnt, DBuf<int32_t> &rp,
     return d2h1(c, rp.p + n);
 }
 
-static void spgemm(Ctx &c, const Csr &X, const Csr &Y, Csr &C, int nc)
+// one k_spgemm launch with (value sets, lanes per row, hash slots) chosen at run time
+static void spgemm_launch(Ctx &c, int ncv, int G, int HS, int fill, const Csr &X, const Csr &Y, int32_t *cnt, Csr &C, int *ovf)
 {
-    C.n = X.n; C.m = Y.m; C.nc = nc;
-    DBuf<int32_t> cnt; cnt.alloc(X.n + 1);
-    DBuf<int> ovf; ovf.alloc(1);
-    // lanes per row from Y's mean row length; attempts grow the per-row hash table on overflow
-    const double ymean = Y.n ? (double)Y.nnz / Y.n : 0.0;
-    // (measured at C5: 4 lanes per row halve the scalar A P; with 3 value sets the per-row tables limit
-    //  occupancy and a full warp per row is faster)
-    const int G0 = nc == 3 ? 32 : ymean <= 4.0 ? 4 : ymean <= 8.0 ? 8 : 32;
-    for (int attempt = 0; attempt < 3; ++attempt) {
-        ovf.zero(c.s);
-        const int G = attempt == 0 ? G0 : 32;
-        const int HS = attempt == 0 ? (G0 < 32 ? 64 : 128) : attempt == 1 ? 512 : 4096;
-        const int threads = attempt == 2 ? 32 : attempt == 1 ? 128 : 256;
-        const int groups = threads / G;
-        size_t smem = (((size_t)groups * (HS + 1) * sizeof(int) + 15) & ~(size_t)15) + (size_t)groups * (HS * nc + 1) * sizeof(double);
-        int grid = std::max(1, std::min((int)((X.n + groups - 1) / groups), c.sm_count * 64));
-        auto launch = [&](int fill) {
+    const int threads = HS >= 4096 ? 32 : HS >= 512 ? 128 : 256;
+    const int groups = threads / G;
+    const size_t smem = (((size_t)groups * (HS + 1) * sizeof(int) + 15) & ~(size_t)15) + (size_t)groups * (HS * ncv + 1) * sizeof(double);
+    const int grid = std::max(1, std::min((int)((X.n + groups - 1) / groups), c.sm_count * 64));
 #define SPG(NCV, GV_, HSV)                                                                                                \
     do {                                                                                                                  \
         cudaFuncSetAttribute(k_spgemm<NCV, GV_, HSV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
@@ -540,24 +528,42 @@ static void spgemm(Ctx &c, const Csr &X, const Csr &Y, Csr &C, int nc)
     } while (0)
 #define SPG_NC(NCV)                                                                                                       \
     do {                                                                                                                  \
-        if (attempt == 0 && G == 4) SPG(NCV, 4, 64);                                                                      \
-        else if (attempt == 0 && G == 8) SPG(NCV, 8, 64);                                                                 \
-        else if (attempt == 0) SPG(NCV, 32, 128);                                                                         \
-        else if (attempt == 1) SPG(NCV, 32, 512);                                                                         \
+        if (G == 4 && HS == 64) SPG(NCV, 4, 64);                                                                          \
+        else if (G == 8 && HS == 64) SPG(NCV, 8, 64);                                                                     \
+        else if (HS == 128) SPG(NCV, 32, 128);                                                                            \
+        else if (HS == 512) SPG(NCV, 32, 512);                                                                            \
         else SPG(NCV, 32, 4096);                                                                                          \
     } while (0)
-            if (nc == 1) SPG_NC(1);
-            else SPG_NC(3);
+    if (ncv == 1) SPG_NC(1);
+    else SPG_NC(3);
 #undef SPG_NC
 #undef SPG
-            TSP_CUDA(cudaGetLastError());
-            c.launches++;
-        };
-        launch(0);
+    TSP_CUDA(cudaGetLastError());
+    c.launches++;
+}
+
+static void spgemm(Ctx &c, const Csr &X, const Csr &Y, Csr &C, int nc)
+{
+    C.n = X.n; C.m = Y.m; C.nc = nc;
+    DBuf<int32_t> cnt; cnt.alloc(X.n + 1);
+    DBuf<int> ovf; ovf.alloc(1);
+    // Lanes per row from Y's mean row length; attempts grow the per-row hash table on overflow.  The
+    // symbolic pass (counts) does not touch values, so it always runs the scalar kernel, whose small
+    // tables keep occupancy high; the numeric pass with 3 value sets uses a full warp per row (measured
+    // at C5: with G = 4 its per-row tables limit occupancy).
+    const double ymean = Y.n ? (double)Y.nnz / Y.n : 0.0;
+    const int G0 = ymean <= 4.0 ? 4 : ymean <= 8.0 ? 8 : 32;
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        const int Gs = attempt == 0 ? G0 : 32;
+        const int HSs = attempt == 0 ? (G0 < 32 ? 64 : 128) : attempt == 1 ? 512 : 4096;
+        const int Gf = nc == 3 ? 32 : Gs;
+        const int HSf = (attempt == 0 && Gf == 32) ? 128 : HSs;   // >= HSs: the counts fit
+        ovf.zero(c.s);
+        spgemm_launch(c, 1, Gs, HSs, 0, X, Y, cnt, C, ovf);
         if (d2h1(c, ovf.p)) continue;
         C.nnz = rowptr_from_counts(c, cnt, C.rp, X.n);
         C.ci.alloc(C.nnz); C.v.alloc(C.nnz * nc);
-        launch(1);
+        spgemm_launch(c, nc, Gf, HSf, 1, X, Y, cnt, C, ovf);
         TSP_REQUIRE(!d2h1(c, ovf.p), TSP_ERR_INVALID_ARG, "spgemm: row too dense");
         return;
     }
