@@ -948,7 +948,7 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
     // apply-side layouts and work vectors
     for (size_t l = 0; l < H.L.size(); ++l) {
         Level &L = H.L[l];
-        sell_from_csr(c, L.A, L.sA, nc);
+        if (!(l == 0 && nc == 3 && c.sym_sdc.ok && !L.coarsest)) sell_from_csr(c, L.A, L.sA, nc);   // sym.cu covers it
         if (!L.coarsest) {
             sell_from_csr(c, L.P, L.sP, nc);
             sell_from_csr(c, L.R, L.sR, nc);
@@ -1166,11 +1166,14 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     // pre-smooth + residual (needs b and D^-1 of the ghost rows)
     if (L.dist) halo_exchange(c, *L.hp, NC, b, L.gh_b);
     const GV gb = gv(b, n, L.dist ? L.gh_b.p : nullptr), gd = gv(L.dinv, n, ghd);
+    const bool sym0 = mech && l == 0 && c.sym_sdc.ok;     // structured symmetric level 0 (sym.cu)
+    const double bA0 = sym0 ? sym_bytes(c, 3) : bA;
     prof_begin(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P);
-    if (wA) (L.dist ? csr_vec<NC, 1, true> : csr_vec<NC, 1, false>)(wA, c.s, n, L.A, gd, gb, gv(nullptr, 0), L.x2, L.r);
+    if (sym0) sym_vcycle_pre(c, n, gd, gb, L.x2, L.r);
+    else if (wA) (L.dist ? csr_vec<NC, 1, true> : csr_vec<NC, 1, false>)(wA, c.s, n, L.A, gd, gb, gv(nullptr, 0), L.x2, L.r);
     else if (n) (L.dist ? k_vc_pre<NC, true> : k_vc_pre<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
         n, L.sA.off, L.sA.col, L.sA.val, gd, gb, L.x2, L.r);
-    prof_end(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P, bA + 4 * vec);
+    prof_end(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P, bA0 + 4 * vec);
     // restriction (local rows of R); a replicated next level is gathered on every rank
     Level &Lc = H.L[l + 1];
     const bool gather = L.dist && !L.next_dist;
@@ -1198,10 +1201,11 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     if (L.dist) halo_exchange(c, *L.hp, NC, L.x2, L.gh_x);
     const GV gx = gv(L.x2, n, L.dist ? L.gh_x.p : nullptr);
     prof_begin(c, mech ? PK_VC_POST_U : PK_VC_POST_P);
-    if (wA) (L.dist ? csr_vec<NC, 2, true> : csr_vec<NC, 2, false>)(wA, c.s, n, L.A, gv(L.dinv, n), gv(b, n), gx, xout, nullptr);
+    if (sym0) sym_vcycle_post(c, n, L.dinv, b, gx, xout);
+    else if (wA) (L.dist ? csr_vec<NC, 2, true> : csr_vec<NC, 2, false>)(wA, c.s, n, L.A, gv(L.dinv, n), gv(b, n), gx, xout, nullptr);
     else if (n) (L.dist ? k_vc_post<NC, true> : k_vc_post<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
         n, L.sA.off, L.sA.col, L.sA.val, L.dinv, b, gx, xout);
-    prof_end(c, mech ? PK_VC_POST_U : PK_VC_POST_P, bA + 4 * vec);
+    prof_end(c, mech ? PK_VC_POST_U : PK_VC_POST_P, bA0 + 4 * vec);
     c.launches += 4;
 }
 

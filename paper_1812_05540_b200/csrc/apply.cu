@@ -125,9 +125,10 @@ void op_apply(Ctx &c, const double *x, double *y)
     halo_exchange(c, c.hf, 2, xf, c.gh_f);
     const GV gu = gv(xu, c.Nn, c.gh_u.p), gf = gv(xf, c.Nc, c.gh_f.p);
     prof_begin(c, PK_OP_NODE);
-    if (c.Nn) (c.comm ? k_op_node<true> : k_op_node<false>)<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(
-        c.Nn, c.s_uu.off, c.s_uu.col, c.s_uu.val, c.s_uf.off, c.s_uf.col, c.s_uf.val, gu, gf, yu);
-    prof_end(c, PK_OP_NODE, sell_bytes(c.s_uu) + sell_bytes(c.s_uf) + 48.0 * c.Nn + 16.0 * c.Nc);
+    if (!sym_op_node(c, gu, gf, yu) && c.Nn)
+        (c.comm ? k_op_node<true> : k_op_node<false>)<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(
+            c.Nn, c.s_uu.off, c.s_uu.col, c.s_uu.val, c.s_uf.off, c.s_uf.col, c.s_uf.val, gu, gf, yu);
+    prof_end(c, PK_OP_NODE, (c.sym_uu.ok ? sym_bytes(c, 9) : sell_bytes(c.s_uu)) + sell_bytes(c.s_uf) + 48.0 * c.Nn + 16.0 * c.Nc);
     prof_begin(c, PK_OP_CELL);
     if (c.Nc) (c.comm ? k_op_cell<0, true> : k_op_cell<0, false>)<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(
         c.Nc, c.s_fu.off, c.s_fu.col, c.s_fu.val, c.s_ff.off, c.s_ff.col, c.s_ff.val, gu, gf, nullptr, yf);

@@ -273,7 +273,9 @@ tsp_status tsp_create(tsp_handle *out, const tsp_desc *d)
     c->fs.alloc(2 * (size_t)std::max(c->Nc, 1));
     if (c->Nc) TSP_CUDA(cudaMemcpyAsync(c->fs, d->fs_diag, sizeof(double) * 2 * c->Nc, on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->s));
     TSP_REQUIRE(all_nonneg(*c, c->fs, 2 * (int64_t)c->Nc), TSP_ERR_INVALID_ARG, "negative fixed-stress diagonal (S:355)");
-    sell_from_csr(*c, c->uu, c->s_uu, 9);
+    // structured symmetric A_uu (sym.cu) when it applies, else the SELL copy of A_uu
+    sym_build(*c);
+    if (!c->sym_uu.ok) sell_from_csr(*c, c->uu, c->s_uu, 9);
     sell_from_csr(*c, c->uf, c->s_uf, 6);
     sell_from_csr(*c, c->fu, c->s_fu, 6);
     sell_from_csr(*c, c->ff, c->s_ff, 4);
@@ -372,7 +374,8 @@ tsp_status tsp_get_stats(tsp_handle h, tsp_stats *s)
             const double nc = L.nc, vec = 8.0 * nc * L.n;
             if (L.coarsest) { apply_bytes += 8.0 * L.n * L.n * nc + 2 * vec; continue; }
             auto sb = [](const Sell &S) { return (double)S.slots * 32 * (4.0 + 8.0 * S.bs); };
-            apply_bytes += 2 * sb(L.sA) + sb(L.sR) + sb(L.sP) + 11 * vec;
+            const double bA = (w == 0 && l == 0 && h->sym_sdc.ok) ? sym_bytes(*h, 3) : sb(L.sA);
+            apply_bytes += 2 * bA + sb(L.sR) + sb(L.sP) + 11 * vec;
         }
         s->skipped_dss = h->skipped_dss;
         s->perturbed_pivots = h->perturbed + h->mech.perturbed + h->pres.perturbed;
@@ -384,7 +387,7 @@ tsp_status tsp_get_stats(tsp_handle h, tsp_stats *s)
     apply_bytes += sb(h->s_aps) + 40 * Nc;                     // steps 3-4
     apply_bytes += (28.0 * 8 + 32 + 48) * Nc;                  // steps 6-8
     s->bytes_apply = apply_bytes;
-    s->bytes_operator = sb(h->s_uu) + sb(h->s_uf) + sb(h->s_fu) + sb(h->s_ff) + 16 * n;
+    s->bytes_operator = (h->sym_uu.ok ? sym_bytes(*h, 9) : sb(h->s_uu)) + sb(h->s_uf) + sb(h->s_fu) + sb(h->s_ff) + 16 * n;
     // Gram-Schmidt depends on the Krylov index: counted exactly per solve (tsp_solve_info.bytes_krylov)
     s->bytes_iter_base = s->bytes_apply + s->bytes_operator;
     s->bytes_per_krylov_vec = 8 * n;

@@ -88,6 +88,26 @@ struct Sell {
     DBuf<double> val;             // slots * 32 * bs
 };
 
+// Structured storage of a 27-point node operator (sym.cu): no column indices (the neighbour follows
+// from the grid); the block entries that are exactly symmetric over the whole matrix (B(i,j)[r][c] ==
+// B(j,i)[c][r] for every pair, detected at create) are kept only for the diagonal block and the 13 "upper"
+// neighbours -- a lower neighbour reads them, transposed, from that neighbour's upper slot -- and the
+// other entries are kept for all 27 neighbours.  Rows whose lower z-plane belongs to rank-1 keep those
+// 9 blocks' symmetric entries explicitly (gl).  Used when the pattern is the full clipped 27-point
+// stencil (checked at create); the generic SELL path otherwise.
+struct SymMap {
+    int bs, ks, kf;               // values per block (9: A_uu, 3: SDC), symmetric / full entries
+    int full[9], idx[9];          // per block entry: 1 = kept for all 27 neighbours; index in its array
+    int tr[9];                    // transposed entry (bs = 9), identity for bs = 3
+};
+struct Sym27 {
+    bool ok = false;
+    SymMap m{};
+    DBuf<double> val_s;           // [slice][14][ks][32]: diagonal + 13 upper blocks, symmetric entries
+    DBuf<double> val_f;           // [slice][27][kf][32]: all neighbours, the other entries
+    DBuf<double> gl;              // [slice of local node plane 0][9][ks][32]
+};
+
 // ------------------------------------------------------------------ multi-GPU (row e)
 struct Ctx;
 // Communicator of the z-slab decomposition: halos with rank-1 / rank+1, allgather.
@@ -221,6 +241,8 @@ struct Ctx {
                                   // uu and the full ff stay (A_uf, A_fu and A_uu's values live in the SELL copies)
     DBuf<double> uu_sdc;          // a2: SDC values of A_uu (3 per block), extracted at create
     Sell s_uu, s_uf, s_fu, s_ff;  // SELL copies (operator rows)
+    Sym27 sym_uu, sym_sdc;        // structured symmetric A_uu (operator) and A_uu^SDC (level-0 smoother)
+    unsigned sym_asym = 0;        // their mask of non-symmetric block entries
     DBuf<double> fs;              // 2 per cell, as given (tsp_desc.fs_diag)
     DBuf<double> fs_eff;          // 2 per cell: the D_fs a1 uses (given / fs_modulus_scale, or RSL)
     DBuf<double> cpr_dss, cpr_dps; // D_ss^(CPR), D_ps^(CPR) (a3)
@@ -262,6 +284,11 @@ bool all_nonneg(Ctx &c, const double *v, int64_t n);
 
 // operator / Algorithm 1 pieces (apply.cu)
 void op_apply(Ctx &c, const double *x, double *y);
+void sym_build(Ctx &c);           // sym_uu / sym_sdc from the uploaded A_uu (tsp_create)
+bool sym_op_node(Ctx &c, const GV &gu, const GV &gf, double *yu);                      // A_uu x_u + A_uf x_f, if sym_uu.ok
+bool sym_vcycle_pre(Ctx &c, int n, const GV &dinv, const GV &b, double *x, double *r);   // level-0 SDC, if sym_sdc.ok
+bool sym_vcycle_post(Ctx &c, int n, const double *dinv, const double *b, const GV &x, double *xo);
+double sym_bytes(const Ctx &c, int bs);   // bytes of one stream over a Sym27 with bs values per block
 void prec_apply(Ctx &c, const double *v, double *z);
 
 // setup (setup_flow.cu, amg_setup.cu, ilu.cu)

@@ -216,3 +216,33 @@ def test_solve_parity_short_restart(dev, m):
     assert ig["restarts"] >= 2
     assert abs(ig["iterations"] - io["iterations"]) <= max(1, io["iterations"] // 100)
     assert ig["true_relres"] <= 1e-8
+
+
+@pytest.mark.parametrize("name", ["C2", "R1"])
+def test_structured_symmetric_path_is_bitwise_the_generic_one(dev, name):
+    """sym.cu (structured symmetric A_uu for the operator and the level-0 mechanics smoother) sums the same
+    27 blocks in the same order as the generic SELL kernels: operator, one Algorithm 1 application and the
+    FGMRES solution are bitwise equal with and without it (TSP_NO_SYM forces the generic path)."""
+    import os
+    from paper_1812_05540_b200 import Tsp
+    pb = _problem(name)
+    v = _cuda(np.random.default_rng(31).uniform(-1, 1, pb.n))
+    out = []
+    for nosym in (False, True):
+        if nosym:
+            os.environ["TSP_NO_SYM"] = "1"
+        try:
+            g = Tsp(pb).setup()
+        finally:
+            os.environ.pop("TSP_NO_SYM", None)
+        y, z, x = (torch.empty(pb.n, dtype=torch.float64, device=dev) for _ in range(3))
+        g.apply_operator(v, y)
+        g.apply_preconditioner(v, z)
+        x.zero_()
+        info = g.solve(_cuda(pb.b), x)
+        torch.cuda.synchronize()
+        out.append((y.cpu().numpy(), z.cpu().numpy(), x.cpu().numpy(), info["iterations"], g.stats()["bytes_operator"]))
+        g.close()
+    (y1, z1, x1, i1, b1), (y2, z2, x2, i2, b2) = out
+    assert np.array_equal(y1, y2) and np.array_equal(z1, z2) and np.array_equal(x1, x2) and i1 == i2
+    assert b1 < 0.9 * b2          # the structured path streams fewer operator bytes (no indices, mirrored entries)
