@@ -60,6 +60,7 @@ def lib():
         L.orc_apply.argtypes = [C.c_void_p, _F64, _F64]
         L.orc_apply_operator.argtypes = [C.c_void_p, _F64, _F64]
         L.orc_solve.argtypes = [C.c_void_p, _F64, _F64, C.c_double, C.c_int, C.c_int, _P(Info)]
+        L.orc_richardson.argtypes = [C.c_void_p, _F64, _F64, C.c_double, C.c_int, _P(Info)]
         L.orc_num_levels.argtypes = [C.c_void_p, C.c_int]
         L.orc_level_sizes.argtypes = [C.c_void_p, C.c_int, C.c_int, _P(C.c_int64)]
         L.orc_level_export.argtypes = [C.c_void_p, C.c_int, C.c_int, _I32, _I32, _F64, _I32, _I32, _I32, _F64, _F64]
@@ -170,6 +171,13 @@ class Oracle:
         lib().orc_solve(self.h, _p(b), _p(x), rtol, m, maxit, C.byref(info))
         return x, dict(iterations=info.iterations, restarts=info.restarts, status=info.status,
                        est_relres=info.est_relres, true_relres=info.true_relres, t_solve=info.t_solve)
+
+    def richardson(self, b, rtol=1e-8, maxit=1000):
+        b = np.ascontiguousarray(b, np.float64)
+        x = np.zeros(self.n)
+        info = Info()
+        lib().orc_richardson(self.h, _p(b), _p(x), rtol, maxit, C.byref(info))
+        return x, dict(iterations=info.iterations, status=info.status, true_relres=info.true_relres)
 
     def num_levels(self, which):
         return lib().orc_num_levels(self.h, which)

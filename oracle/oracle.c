@@ -1089,6 +1089,37 @@ void orc_apply_operator(orc *h, const double *x, double *y)
  * right-preconditioned, flexible form: Z keeps M^-1 v_j. */
 static double dot(const double *a, const double *b, int n) { double s = 0.0; for (int i = 0; i < n; ++i) s += a[i] * b[i]; return s; }
 
+/* the "sequential" embedding of the remark at P:640-642: Richardson iteration x <- x + M^-1 (b - A x),
+ * x0 = 0, stopped when ||b - A x|| <= rtol ||b||; iterations = preconditioner applications */
+int orc_richardson(orc *h, const double *b, double *x, double rtol, int maxit, orc_info *info)
+{
+    double t0 = now_s();
+    int n = h->n;
+    memset(info, 0, sizeof(*info));
+    double *r = (double *)xmalloc(sizeof(double) * n), *z = (double *)xmalloc(sizeof(double) * n);
+    double bn = sqrt(dot(b, b, n));
+    int it = 0, status = 1;
+    memset(x, 0, sizeof(double) * n);
+    for (;;) {
+        orc_apply_operator(h, x, r);
+        for (int i = 0; i < n; ++i) r[i] = b[i] - r[i];
+        double rn = sqrt(dot(r, r, n));
+        info->true_relres = bn > 0.0 ? rn / bn : 0.0;
+        info->est_relres = info->true_relres;
+        if (rn <= rtol * bn) { status = 0; break; }
+        if (!isfinite(rn)) { status = 2; break; }
+        if (it >= maxit) { status = 1; break; }
+        orc_apply(h, r, z);
+        for (int i = 0; i < n; ++i) x[i] = x[i] + z[i];
+        ++it;
+    }
+    free(r); free(z);
+    info->iterations = it;
+    info->status = status;
+    info->t_solve = now_s() - t0;
+    return status;
+}
+
 int orc_solve(orc *h, const double *b, double *x, double rtol, int m, int maxit, orc_info *info)
 {
     double t0 = now_s();

@@ -58,6 +58,7 @@ int orc_setup(orc *h);                                    /* rows a1-a5 */
 int orc_apply(orc *h, const double *v, double *z);        /* Algorithm 1 */
 void orc_apply_operator(orc *h, const double *x, double *y);   /* eq:jac_system */
 int orc_solve(orc *h, const double *b, double *x, double rtol, int m, int maxit, orc_info *info);
+int orc_richardson(orc *h, const double *b, double *x, double rtol, int maxit, orc_info *info);   /* remark P:640-642 */
 /* diagnostics / parity hooks */
 int orc_num_levels(orc *h, int which);                    /* which: 0 mechanics SDC, 1 pressure */
 void orc_level_sizes(orc *h, int which, int lvl, int64_t out[6]); /* n, nnz(A), nagg, nnz(P), nc, coarsest */

@@ -212,3 +212,23 @@ def test_second_stage_variants_converge(opts):
     pb = synth.generate("C1")
     x, info = oracle.Oracle(pb, **opts).setup().solve(pb.b, rtol=1e-8, m=64)
     assert info["status"] == 0 and info["true_relres"] <= 1e-8
+
+
+# ---------------------------------------------------------------- NEXT-f4 (iii): sequential (Richardson) embedding
+def test_richardson_embedding_exact_and_decoupled():
+    """Remark P:640-642: x <- x + M^-1 (b - A x).  With A_uf = A_fu = 0 and exact sub-solves M^-1 = A^-1, so one
+    step solves the system; with the coupling and an exact mechanics solve it is the fixed-stress sequential
+    scheme, a contraction: it converges to the dense solution."""
+    import scipy.sparse as sp
+    pb = synth.generate("C1")
+    o = oracle.Oracle(pb, mech_mode=1).setup()
+    x, info = o.richardson(pb.b, rtol=1e-8, maxit=1000)
+    A, _ = synth.to_scipy(pb)
+    assert info["status"] == 0 and info["true_relres"] <= 1e-8
+    assert np.linalg.norm(x - pb.x_rand) <= 1e-4 * np.linalg.norm(pb.x_rand)   # cond(A) ~ 1e4 at rtol 1e-8
+    pb.uf_val[:] = 0.0; pb.fu_val[:] = 0.0
+    A, _ = synth.to_scipy(pb)
+    b = A @ pb.x_rand
+    o2 = oracle.Oracle(pb, mech_mode=1, ff_mode=1).setup()
+    x2, info2 = o2.richardson(b, rtol=1e-8, maxit=10)
+    assert info2["iterations"] == 1 and info2["true_relres"] <= 1e-10
