@@ -128,7 +128,7 @@ def oracle_sample(config, gpu_iters, sample_iters=3, reps=1, opts=None):
     same generator recipe on a 1/8 sub-grid, scaled linearly in DoF (the
     oracle's setup and iteration are O(n)).  Step = setup + gpu_iters * t_iter."""
     import oracle
-    full = synth.sizes(*(synth.CONFIGS[config][k] for k in ("nx", "ny", "nz")))["n"]
+    full = synth.sizes(*(ALL_CONFIGS[config][k] for k in ("nx", "ny", "nz")))["n"]
     kw = {}
     if config in SAMPLE_GRID:
         kw = dict(zip(("nx", "ny", "nz"), SAMPLE_GRID[config]))
@@ -154,17 +154,18 @@ def oracle_sample(config, gpu_iters, sample_iters=3, reps=1, opts=None):
 
 # FGMRES(64) iterations to 1e-8 measured on the CUDA path (tests/test_gpu_parity.py keeps
 # the oracle within +-1 of them); used to scale the reference arm's bounded sample.
-GPU_ITERS = {"C1": 41, "C2": 61, "C3": 120, "C4": 110, "C5": 347}
+GPU_ITERS = {"C1": 41, "C2": 61, "C3": 120, "C4": 109, "C5": 256}   # measured FGMRES counts (parity: the oracle's +-1)
+ALL_CONFIGS = {**synth.CONFIGS, **synth.WORKLOADS}
 
 
 def run_reference(args, ws, rank):
     """--impl reference: the CPU oracle timed on the host cores (rank 0 only)."""
     if rank != 0:
         return 0
-    iters = args.ref_iters or GPU_ITERS[args.config]
+    iters = args.ref_iters or GPU_ITERS.get(args.config, 100)
     cpu = oracle_sample(args.config, iters, sample_iters=args.ref_sample_iters, reps=max(args.steps, 1), opts=args.lib_opts)
     value = cpu["value"]
-    g = synth.CONFIGS[args.config]
+    g = ALL_CONFIGS[args.config]
     line = {"impl": "reference", "metric": "preconditioned FGMRES iters/s", "value": value, "unit": "iter/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": cpu["step_s"] * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -181,7 +182,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=list(synth.CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=list(ALL_CONFIGS))
     ap.add_argument("--impl", default="tsp", choices=["tsp", "reference"])
     ap.add_argument("--opts", default="", help="library options key=value[,key=value] (tsp_options), e.g. "
                     "cpr_mode=1,aps_mode=1 -- the setup variants of SURVEY NEXT-f3; default: the paper's choices")

@@ -32,7 +32,9 @@ class Params(C.Structure):
         ("mu_w", C.c_double), ("mu_nw", C.c_double), ("rho_s", C.c_double), ("p0", C.c_double),
         ("swr", C.c_double), ("snwr", C.c_double),
         ("well_dbhp", C.c_double), ("rw_over_h", C.c_double), ("state_dp", C.c_double), ("p_unit", C.c_double), ("length", C.c_double),
-        ("wells", C.c_int), ("dirichlet_bottom", C.c_int), ("row_scale", C.c_int), ("pad_", C.c_int),
+        ("wells", C.c_int), ("dirichlet_bottom", C.c_int), ("row_scale", C.c_int),
+        ("burden", C.c_int), ("well_pattern", C.c_int), ("pad2_", C.c_int),
+        ("burden_perm", C.c_double), ("burden_phi", C.c_double),
     ]
 
 
@@ -74,7 +76,7 @@ DEFAULTS = dict(
     rho_w0=1035.0, rho_nw0=863.0, c_w=4.34e-10, c_nw=1.98e-10,
     mu_w=1e-3, mu_nw=5e-3, rho_s=2650.0, p0=1e7, swr=0.2, snwr=0.2,
     well_dbhp=5e6, rw_over_h=0.1, state_dp=0.0, p_unit=1e6, length=10000.0, wells=1, dirichlet_bottom=1, row_scale=1,
-    seed=0, recipe=1,
+    seed=0, recipe=1, burden=0, well_pattern=0, burden_perm=1e-17, burden_phi=0.01,
 )
 
 # BASELINE.json configs[0..4] (C1..C5); recipes per SURVEY D17.
@@ -84,6 +86,13 @@ CONFIGS = {
     "C3": dict(nx=64, ny=64, nz=64, recipe=3, perm_sigma=3.0),
     "C4": dict(nx=128, ny=128, nz=64, recipe=4, perm_sigma=2.0),
     "C5": dict(nx=256, ny=256, nz=128, recipe=5, perm_sigma=2.0),
+}
+# Second workload (SURVEY NEXT-f4 ii, DESIGN.md R-s10): the SPE10-based example's shape -- 60 x 220 x 252 cells,
+# 0.01 mD / 1 % over- and underburden, homogeneous E = 5000 MPa, nu = 0.25, five wells -- with the
+# correlated generator (D17) in the 84 reservoir layers, since the SPE10 data are not available.
+WORKLOADS = {
+    "S10": dict(nx=60, ny=220, nz=252, recipe=4, perm_median=1e-14, perm_sigma=3.0, E_median=5e9, E_sigma=0.0,
+                burden=84, well_pattern=1),   # cells 167 m: the R-geom convention (normalised 10 km domain side)
 }
 
 
@@ -136,7 +145,7 @@ def generate(config: str | None = None, **overrides) -> Problem:
     configs[0..4]); keyword overrides change any Params field (e.g. nx=3, biot=0)."""
     kw = dict(DEFAULTS)
     if config is not None:
-        kw.update(CONFIGS[config])
+        kw.update(CONFIGS[config] if config in CONFIGS else WORKLOADS[config])
     kw.update(overrides)
     p = Params(**{k: v for k, v in kw.items() if k in dict(Params._fields_)})
     s = sizes(p.nx, p.ny, p.nz)

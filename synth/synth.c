@@ -47,7 +47,11 @@ typedef struct {
     int wells;             /* 1: vertical injector in column (0,0), producer in (nx-1,ny-1) */
     int dirichlet_bottom;  /* 1: all 3 displacement components fixed at z = 0 */
     int row_scale;         /* 1: block-row scaling (D12) */
-    int pad_;
+    int burden;            /* SPE10-shaped workload (R-s10): this many seal layers at the top and at the bottom */
+    int well_pattern;      /* 0: the corner pair above; 1: injector in the centre column, producers in the 4
+                              corner columns, perforated through the reservoir layers only */
+    int pad2_;
+    double burden_perm, burden_phi;   /* seal units: 0.01 mD, 1 % */
 } synth_params;
 
 typedef struct {
@@ -180,6 +184,11 @@ static void make_fields(const synth_params *P, double *E, double *perm, double *
     }
     st = stream_seed(P->seed, 3);
     for (int64_t c = 0; c < nc; ++c) phi[c] = 0.15 + 0.10 * unif(&st);
+    if (P->burden > 0)                                   /* over- and underburden seal layers */
+        for (int64_t c = 0; c < nc; ++c) {
+            int64_t k = c / (nx * ny);
+            if (k < P->burden || k >= nz - P->burden) { perm[c] = P->burden_perm; phi[c] = P->burden_phi; }
+        }
     st = stream_seed(P->seed, 4);
     for (int64_t c = 0; c < nc; ++c) sat[c] = 0.2 + 0.6 * unif(&st);
 }
@@ -373,7 +382,8 @@ int synth_generate(const synth_params *P, synth_out *O)
     /* well geometry (D15): WI of eq:well_index with r_w = rw_over_h * h, s_k = 0 */
     const double rpe = 0.28 * sqrt(h * h + h * h) / 2.0;
     const double lnr = log(rpe / (P->rw_over_h * h));
-    const double zbh = (nz - 0.5) * h;
+    const int kw0 = P->burden > 0 ? P->burden : 0, kw1 = P->burden > 0 ? nz - P->burden : nz;   /* perforated layers */
+    const double zbh = (kw1 - 0.5) * h;
     const double pbh_ref = P->p0 + P->rho_w0 * g * (ztop - zbh);
 #pragma omp parallel for schedule(static)
     for (int64_t c = 0; c < Nc; ++c) {
@@ -446,6 +456,11 @@ int synth_generate(const synth_params *P, synth_out *O)
         /* wells (eq:peaceman, eq:peaceman2; derivatives P:1042-1095; residual sign P:941) */
         if (P->wells) {
             int inj = (i == 0 && j == 0), prod = (i == nx - 1 && j == ny - 1);
+            if (P->well_pattern == 1) {
+                inj = (i == nx / 2 && j == ny / 2);
+                prod = (i == 0 || i == nx - 1) && (j == 0 || j == ny - 1);
+            }
+            if (k < kw0 || k >= kw1) inj = prod = 0;
             if (inj || prod) {
                 double WI = 2 * M_PI * h * perm[c] / lnr;
                 double pbh = pbh_ref + (inj ? P->well_dbhp : -P->well_dbhp);
