@@ -90,7 +90,14 @@ CONFIGS = {
 # Second workload (SURVEY NEXT-f4 ii, DESIGN.md R-s10): the SPE10-based example's shape -- 60 x 220 x 252 cells,
 # 0.01 mD / 1 % over- and underburden, homogeneous E = 5000 MPa, nu = 0.25, five wells -- with the
 # correlated generator (D17) in the 84 reservoir layers, since the SPE10 data are not available.
+_STAIR = dict(recipe=6, E_median=5e9, E_sigma=0.0, mu_w=3e-4, mu_nw=3e-3, well_pattern=2)
 WORKLOADS = {
+    # Staircase benchmark (SURVEY NEXT-f4 i, DESIGN.md R-stair): Table 1's staircase column on the four grids of
+    # Table 2 (levels 2 and 3 are the C4 and C5 grids), channel geometry by the documented convention
+    "ST0": dict(nx=32, ny=32, nz=16, **_STAIR),
+    "ST1": dict(nx=64, ny=64, nz=32, **_STAIR),
+    "ST2": dict(nx=128, ny=128, nz=64, **_STAIR),
+    "ST3": dict(nx=256, ny=256, nz=128, **_STAIR),
     "S10": dict(nx=60, ny=220, nz=252, recipe=4, perm_median=1e-14, perm_sigma=3.0, E_median=5e9, E_sigma=0.0,
                 burden=84, well_pattern=1),   # cells 167 m: the R-geom convention (normalised 10 km domain side)
 }

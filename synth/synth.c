@@ -152,6 +152,25 @@ static void correlated_field(const synth_params *P, double *g)
     for (int64_t c = 0; c < nc; ++c) g[c] = (g[c] - m) * isd;
 }
 
+/* Staircase benchmark geometry (R-stair; the paper gives it only as a figure): a channel of
+ * width 1/8 of the side winds once around the domain at an inset of 1/8 in four straight legs, each leg one
+ * quarter of the height lower than the previous one -- a descending square spiral "staircase".  Leg 0 runs
+ * along +x near y = 1/8 in the top quarter, leg 1 along +y near x = 7/8, leg 2 along -x near y = 7/8, leg 3
+ * along -y near x = 1/8 in the bottom quarter; at each corner the channel spans both legs' z-bands.
+ * Normalised cell-centre coordinates u, v, w in [0, 1). */
+static int stair_channel(double u, double v, double w)
+{
+    const double a = 0.125, b = 0.25, c = 0.75, d = 0.875;
+    int q = (int)(4.0 * (1.0 - w)); if (q > 3) q = 3;          /* z band: 0 = top quarter ... 3 = bottom */
+    const int in_s = (v >= a && v < b), in_e = (u >= c && u < d), in_n = (v >= c && v < d), in_w = (u >= a && u < b);
+    const int ux = (u >= a && u < d), vy = (v >= a && v < d);
+    if ((q == 0 || q == 1) && in_s && ux && (q == 0 || in_e)) return 1;   /* leg 0 (+ its corner step into leg 1) */
+    if ((q == 1 || q == 2) && in_e && vy && (q == 1 || in_n)) return 1;   /* leg 1 */
+    if ((q == 2 || q == 3) && in_n && ux && (q == 2 || in_w)) return 1;   /* leg 2 */
+    if (q == 3 && in_w && vy) return 1;                                    /* leg 3 */
+    return 0;
+}
+
 static void make_fields(const synth_params *P, double *E, double *perm, double *phi, double *sat)
 {
     int64_t nx = P->nx, ny = P->ny, nz = P->nz, nc = nx * ny * nz;
@@ -184,6 +203,13 @@ static void make_fields(const synth_params *P, double *E, double *perm, double *
     }
     st = stream_seed(P->seed, 3);
     for (int64_t c = 0; c < nc; ++c) phi[c] = 0.15 + 0.10 * unif(&st);
+    if (P->recipe == 6)                                  /* staircase: 1000 mD / 0.20 channel in 1 mD / 0.05 seal (Table 1) */
+        for (int64_t c = 0; c < nc; ++c) {
+            const int64_t i = c % nx, j = (c / nx) % ny, k = c / (nx * ny);
+            const int ch = stair_channel((i + 0.5) / nx, (j + 0.5) / ny, (k + 0.5) / nz);
+            perm[c] = ch ? 1000 * 9.869233e-16 : 9.869233e-16;
+            phi[c] = ch ? 0.20 : 0.05;
+        }
     if (P->burden > 0)                                   /* over- and underburden seal layers */
         for (int64_t c = 0; c < nc; ++c) {
             int64_t k = c / (nx * ny);
@@ -459,6 +485,12 @@ int synth_generate(const synth_params *P, synth_out *O)
             if (P->well_pattern == 1) {
                 inj = (i == nx / 2 && j == ny / 2);
                 prod = (i == 0 || i == nx - 1) && (j == 0 || j == ny - 1);
+            }
+            if (P->well_pattern == 2) {                  /* staircase: channel ends, channel cells only */
+                const int ci0 = (int)(0.1875 * nx), cj0 = (int)(0.1875 * ny);
+                inj = (i == (int)(0.5 * nx) && j == cj0);
+                prod = (i == ci0 && j == (int)(0.5 * ny));
+                if (!stair_channel((i + 0.5) / nx, (j + 0.5) / ny, (k + 0.5) / nz)) inj = prod = 0;
             }
             if (k < kw0 || k >= kw1) inj = prod = 0;
             if (inj || prod) {
