@@ -210,19 +210,33 @@ def main():
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    pb = synth.generate(args.config)
-    n_glob = pb.n
     topo = {}
     if ws > 1:
-        # z-slab decomposition (row e): this rank's owned block rows, NCCL over NVLink for halos/reductions
+        # z-slab decomposition (row e): this rank's owned block rows, NCCL over NVLink for halos/reductions.
+        # The generator builds the global Jacobian (~26 GB of host memory at C5); ranks take turns so that only
+        # one global copy exists at a time, and each keeps its slab only.
+        import gc
         from paper_1812_05540_b200 import TSP_COMM_NCCL, nccl_unique_id
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        lp = synth.local_problem(pb, rank, ws)
-        b_host = lp.local(pb.b, pb.Nn)
+        for turn in range(ws):
+            if turn == rank:
+                pb = synth.generate(args.config)
+                lp = synth.local_problem(pb, rank, ws)
+                b_host = np.ascontiguousarray(lp.local(pb.b, pb.Nn))
+                shape = synth.Problem(nx=pb.nx, ny=pb.ny, nz=pb.nz, params={}, **{k: None for k in (
+                    "uu_rowptr", "uu_col", "uu_val", "uf_rowptr", "uf_col", "uf_val", "fu_rowptr", "fu_col", "fu_val",
+                    "ff_rowptr", "ff_col", "ff_val", "fs", "x_rand", "b")})
+                n_glob = pb.n
+                del pb
+                gc.collect()
+                pb = shape
+            dist.barrier()
         src = lp
         topo = dict(rank=rank, nranks=ws, comm_kind=TSP_COMM_NCCL, comm_arg=obj[0])
     else:
+        pb = synth.generate(args.config)
+        n_glob = pb.n
         src, b_host = pb, pb.b
     n = src.n
     g = Tsp(src, **topo, **lib_opts)

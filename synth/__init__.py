@@ -239,7 +239,8 @@ class LocalProblem:
 
 def _rows(rp, ci, v, r0, nr):
     a, b = rp[r0], rp[r0 + nr]
-    return (rp[r0:r0 + nr + 1] - a).astype(np.int32), np.ascontiguousarray(ci[a:b]), np.ascontiguousarray(v[a:b])
+    # copies: a rank's slab must not keep the global arrays alive (bench.py frees them)
+    return (rp[r0:r0 + nr + 1] - a).astype(np.int32), ci[a:b].copy(), v[a:b].copy()
 
 
 def local_problem(pb: Problem, rank: int, nranks: int, zblock: int = 16) -> LocalProblem:
@@ -249,4 +250,4 @@ def local_problem(pb: Problem, rank: int, nranks: int, zblock: int = 16) -> Loca
         rp, ci, v = _rows(getattr(pb, name + "_rowptr"), getattr(pb, name + "_col"), getattr(pb, name + "_val"), r0, nr)
         d[name + "_rowptr"], d[name + "_col"], d[name + "_val"] = rp, ci, v
     return LocalProblem(nx=pb.nx, ny=pb.ny, nz=pb.nz, rank=rank, nranks=nranks, node0=n0, cell0=c0,
-                        fs=np.ascontiguousarray(pb.fs[c0:c0 + ncl]), Nn=nn, Nc=ncl, **d)
+                        fs=pb.fs[c0:c0 + ncl].copy(), Nn=nn, Nc=ncl, **d)
