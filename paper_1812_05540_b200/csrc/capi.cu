@@ -302,6 +302,7 @@ tsp_status tsp_setup(tsp_handle h, unsigned what)
 {
     if (!h) { set_error("null handle"); return TSP_ERR_INVALID_ARG; }
     API_BEGIN
+    krylov_graphs_drop(*h);             // the graphs bake in the hierarchy's buffer addresses
     if (what & TSP_SETUP_MECH) setup_mech(*h);
     if (what & TSP_SETUP_FLOW) setup_flow(*h);
     TSP_CUDA(cudaStreamSynchronize(h->s));
@@ -501,6 +502,9 @@ void tsp_destroy(tsp_handle h)
     StreamScope ss_(h->s);
     cudaStreamSynchronize(h->s);
     for (auto &e : h->prof.pool) cudaEventDestroy(e);
+    krylov_graphs_drop(*h);
+    if (h->kcol_host) cudaFreeHost(h->kcol_host);
+    if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
     Comm *cm = h->comm;
     cudaStream_t s = h->s;
     delete h;

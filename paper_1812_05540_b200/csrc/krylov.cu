@@ -263,9 +263,10 @@ __global__ void __launch_bounds__(KB) k_update(int64_t n, int k, const double *_
         x[r] = acc;
     }
 }
-// y = x / *s
+// y = x / *s (nothing when *s == 0: a lucky breakdown leaves w as it is)
 __global__ void k_scale_inv(int64_t n, const double *__restrict__ s, const double *__restrict__ x, double *__restrict__ y)
 {
+    if (*s == 0.0) return;
     const double a = 1.0 / *s;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) y[r] = a * x[r];
 }
@@ -389,11 +390,65 @@ struct Hess {
     }
 };
 
+void krylov_graphs_drop(Ctx &c)
+{
+    for (auto &g : c.kgraph)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+    c.kgraph.assign(c.kgraph.size(), Ctx::KGraph{});
+}
+
+// Iteration j's body: eager the first time (one-time attribute settings happen there), then captured into a
+// graph and replayed -- ~70 dependent launches per iteration become one, which is what bounds small problems.
+template <class F>
+static void run_body(Ctx &c, Kr &K, int j, bool use_graph, F &body)
+{
+    if (!use_graph || j >= (int)c.kgraph.size()) { body(); return; }
+    auto &G = c.kgraph[j];
+    if (!G.exec && !G.seen) { body(); G.seen = true; return; }
+    if (G.failed) { body(); return; }
+    if (!G.exec) {
+        const int64_t l0 = c.launches;
+        const double b0 = K.bytes;
+        cudaGraph_t graph = nullptr;
+        // capture on a private stream (the API stream may be the legacy default stream, which cannot capture);
+        // the body launches on c.s, so c.s points at it meanwhile
+        if (!c.cap_stream) TSP_CUDA(cudaStreamCreateWithFlags(&c.cap_stream, cudaStreamNonBlocking));
+        const cudaStream_t api = c.s;
+        c.s = c.cap_stream;
+        TSP_CUDA(cudaStreamBeginCapture(c.s, cudaStreamCaptureModeThreadLocal));
+        try {
+            body();
+        } catch (const Error &e) {                  // not capturable here: end the capture, run eagerly from now on
+            cudaStreamEndCapture(c.s, &graph);
+            c.s = api;
+            if (graph) cudaGraphDestroy(graph);
+            (void)cudaGetLastError();
+            if (getenv("TSP_DEBUG")) fprintf(stderr, "[tsp graph] capture of iteration %d failed: %s\n", j, e.msg.c_str());
+            G.failed = true;
+            c.launches = l0; K.bytes = b0;
+            body();
+            return;
+        }
+        const cudaError_t ec = cudaStreamEndCapture(c.s, &graph);
+        c.s = api;
+        TSP_CUDA(ec);
+        TSP_CUDA(cudaGraphInstantiate(&G.exec, graph, 0));
+        cudaGraphDestroy(graph);
+        G.launches = c.launches - l0;
+        G.bytes = K.bytes - b0;
+        c.launches = l0; K.bytes = b0;
+    }
+    TSP_CUDA(cudaGraphLaunch(G.exec, c.s));
+    c.launches += G.launches;
+    K.bytes += G.bytes;
+}
+
 void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, tsp_solve_info &info)
 {
     const int m = std::max(1, std::min(o.restart, 120));
     const int64_t n = c.n, ld = (n + 31) & ~(int64_t)31;
     if (c.kcap != m || c.V.n != (size_t)(m + 1) * ld) {
+        krylov_graphs_drop(c);
         c.V.alloc((size_t)(m + 1) * ld);
         c.Z.alloc((size_t)m * ld);
         c.kr.alloc(std::max<int64_t>(n, 1));
@@ -412,6 +467,11 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
 
     Hess H(m);
     std::vector<double> yv(m), col(2 * (m + 2) + 8);
+    if (!c.kcol_host) TSP_CUDA(cudaMallocHost((void **)&c.kcol_host, sizeof(double) * (2 * (120 + 2) + 8)));
+    if ((int)c.kgraph.size() != m) { krylov_graphs_drop(c); c.kgraph.resize(m); }
+    // CUDA graphs for the iteration body: one rank, no profiling (its events are per launch)
+    const bool no_graph = getenv("TSP_NO_GRAPH") != nullptr;
+    const bool use_graph = !c.comm && !c.prof.on && !no_graph;
     double bn;
     K.norm(b, dh);
     TSP_CUDA(cudaMemcpyAsync(&bn, dh, sizeof(double), cudaMemcpyDeviceToHost, c.s));
@@ -445,13 +505,18 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
             for (int j = 0; j < m; ++j) {
                 double *uj = V + (size_t)j * ld, *zj = Z + (size_t)j * ld, *w = V + (size_t)(j + 1) * ld;
                 double *d = dh, *sc = dh + 2 * (j + 1), *rho = sc + 2;
-                prec_apply(c, uj, zj);                 // z_j = M^-1 u_j (Algorithm 1)
-                op_apply(c, zj, w);                    // w = A z_j
-                K.mdot2(V, j, w, d, sc);               // [V_{j-1} u_j]^T [u_j w], alpha_j, h_j
-                K.dcgs_update(V, j, d, sc, w, rho);    // v_j, w -> w - V_j h, rho = ||w||
-                TSP_CUDA(cudaMemcpyAsync(col.data(), dh, sizeof(double) * (2 * (j + 1) + 3), cudaMemcpyDeviceToHost, c.s));
+                // the iteration body: device work only, ending with the scalars copied to pinned host memory
+                auto body = [&]() {
+                    prec_apply(c, uj, zj);                 // z_j = M^-1 u_j (Algorithm 1)
+                    op_apply(c, zj, w);                    // w = A z_j
+                    K.mdot2(V, j, w, d, sc);               // [V_{j-1} u_j]^T [u_j w], alpha_j, h_j
+                    K.dcgs_update(V, j, d, sc, w, rho);    // v_j, w -> w - V_j h, rho = ||w||
+                    K.scale_inv(rho, w, w);                // u_{j+1} = w / rho (skipped when rho == 0)
+                    TSP_CUDA(cudaMemcpyAsync(c.kcol_host, dh, sizeof(double) * (2 * (j + 1) + 3), cudaMemcpyDeviceToHost, c.s));
+                };
+                run_body(c, K, j, use_graph, body);
                 TSP_CUDA(cudaStreamSynchronize(c.s));
-                const double *dd = col.data(), alpha = dd[2 * (j + 1)], hj = dd[2 * (j + 1) + 1], rj = dd[2 * (j + 1) + 2];
+                const double *dd = c.kcol_host, alpha = dd[2 * (j + 1)], hj = dd[2 * (j + 1) + 1], rj = dd[2 * (j + 1) + 2];
                 TSP_REQUIRE(std::isfinite(alpha) && std::isfinite(hj) && std::isfinite(rj), TSP_ERR_NUMERIC,
                             "non-finite Arnoldi coefficients (loss of orthogonality)");
                 info.reorth++;
@@ -465,7 +530,6 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
                 H.raw[j][j + 1] = rj;                  // provisional: u_{j+1} taken as v_{j+1}
                 H.rotate(j);
                 rho_prev = rj;
-                if (rj != 0.0) K.scale_inv(rho, w, w); // u_{j+1} = w / rho
                 ++it; k = j + 1;
                 info.est_relres = std::fabs(H.g[j + 1]) / bn;
                 if (rj == 0.0) { lucky = true; break; }

@@ -262,6 +262,12 @@ struct Ctx {
     // Krylov storage
     DBuf<double> V, Z, kw, kr, kx, kb, kh, kpart;
     int kcap = 0;
+    // CUDA graphs of the FGMRES iteration body, one per Krylov index j (krylov.cu); dropped by every
+    // tsp_setup and basis reallocation (they bake in buffer addresses)
+    struct KGraph { cudaGraphExec_t exec = nullptr; bool seen = false, failed = false; int64_t launches = 0; double bytes = 0; };
+    std::vector<KGraph> kgraph;
+    double *kcol_host = nullptr;       // pinned: the iteration's dots / scalars, read by the host
+    cudaStream_t cap_stream = nullptr; // private stream the graphs are captured on
     // counters
     int64_t launches = 0, skipped_dss = 0, perturbed = 0;
     DBuf<unsigned long long> dcount;  // device counters scratch
@@ -305,6 +311,7 @@ void partition(int nx, int ny, int nz, int zblock, int rank, int nranks, int64_t
 void reduce_setup(Ctx &c);
 
 // Krylov (krylov.cu)
+void krylov_graphs_drop(Ctx &c);
 void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, tsp_solve_info &info);
 
 }  // namespace tsp

@@ -246,3 +246,24 @@ def test_structured_symmetric_path_is_bitwise_the_generic_one(dev, name):
     (y1, z1, x1, i1, b1), (y2, z2, x2, i2, b2) = out
     assert np.array_equal(y1, y2) and np.array_equal(z1, z2) and np.array_equal(x1, x2) and i1 == i2
     assert b1 < 0.9 * b2          # the structured path streams fewer operator bytes (no indices, mirrored entries)
+
+
+def test_cuda_graph_iterations_are_bitwise_the_eager_ones(dev):
+    """krylov.cu replays the FGMRES iteration body from per-index CUDA graphs (captured on a second use); two
+    solves with graphs and one without (TSP_NO_GRAPH) give the same solution bit for bit."""
+    import os
+    pb, o, g = _pair("C2")
+    b = _cuda(pb.b)
+    xs = []
+    for nograph in (True, False, False):        # eager; first use (eager + marks); captured + replayed
+        if nograph:
+            os.environ["TSP_NO_GRAPH"] = "1"
+        try:
+            x = torch.zeros(pb.n, dtype=torch.float64, device=dev)
+            info = g.solve(b, x, rtol=1e-8, restart=20)
+        finally:
+            os.environ.pop("TSP_NO_GRAPH", None)
+        torch.cuda.synchronize()
+        xs.append((x.cpu().numpy(), info["iterations"]))
+    assert xs[0][1] == xs[1][1] == xs[2][1]
+    assert np.array_equal(xs[0][0], xs[1][0]) and np.array_equal(xs[0][0], xs[2][0])
