@@ -154,7 +154,7 @@ def oracle_sample(config, gpu_iters, sample_iters=3, reps=1, opts=None):
 
 # FGMRES(64) iterations to 1e-8 measured on the CUDA path (tests/test_gpu_parity.py keeps
 # the oracle within +-1 of them); used to scale the reference arm's bounded sample.
-GPU_ITERS = {"C1": 41, "C2": 61, "C3": 120, "C4": 109, "C5": 256}   # measured FGMRES counts (parity: the oracle's +-1)
+GPU_ITERS = {"C1": 41, "C2": 61, "C3": 217, "C4": 109, "C5": 256, "S10": 190, "ST3": 315}   # measured FGMRES counts (parity: the oracle's +-1)
 ALL_CONFIGS = {**synth.CONFIGS, **synth.WORKLOADS}
 
 
