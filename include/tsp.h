@@ -120,8 +120,8 @@ enum { TSP_SETUP_MECH = 1, TSP_SETUP_FLOW = 2 };
 
 typedef struct {
     double rtol;                 /* ||b - A x|| <= rtol ||b||, default 1e-8 */
-    int restart;                 /* FGMRES(m), default 64 */
-    int max_iters;               /* default 1000 */
+    int restart;                 /* FGMRES(m), default 64; clamped to [1, 120] */
+    int max_iters;               /* preconditioner applications, default 1000; 0 = only the true residual of x0 */
     int x0_zero;                 /* 1: ignore x on input, start from 0 */
     int host_ptrs;               /* 1: b and x are host pointers (copies are on the stream) */
 } tsp_solve_opts;
@@ -191,8 +191,12 @@ tsp_status tsp_apply_preconditioner(tsp_handle h, const double *v, double *z);
 /* y = A x with the original Jacobian (row a12).  Device pointers, asynchronous. */
 tsp_status tsp_apply_operator(tsp_handle h, const double *x, double *y);
 
-/* Right-preconditioned FGMRES(m) with CGS2 Arnoldi.  Returns TSP_OK,
- * TSP_NOT_CONVERGED (x = last iterate) or an error.  Synchronises. */
+/* Right-preconditioned FGMRES(m) with classical Gram-Schmidt applied twice, the second pass
+ * delayed one iteration (DCGS2, DESIGN.md R-krylov).  b, x: device pointers of length n (host pointers if
+ * o->host_ptrs; copies on the stream); x is x0 on input (zero if o->x0_zero) and the solution on output.
+ * Converged when the TRUE residual ||b - A x|| <= rtol ||b|| (recomputed at the end of every cycle; b = 0
+ * gives x = 0).  Returns TSP_OK, TSP_NOT_CONVERGED (x = last iterate, info->true_relres its residual) or an
+ * error (TSP_ERR_NUMERIC on a non-finite Arnoldi coefficient).  Collective over the ranks; synchronises. */
 tsp_status tsp_solve(tsp_handle h, const double *b, double *x, const tsp_solve_opts *o, tsp_solve_info *info);
 void tsp_default_solve_opts(tsp_solve_opts *o);
 

@@ -267,3 +267,26 @@ def test_cuda_graph_iterations_are_bitwise_the_eager_ones(dev):
         xs.append((x.cpu().numpy(), info["iterations"]))
     assert xs[0][1] == xs[1][1] == xs[2][1]
     assert np.array_equal(xs[0][0], xs[1][0]) and np.array_equal(xs[0][0], xs[2][0])
+
+
+def test_solve_edge_cases(dev):
+    """tsp_solve semantics (include/tsp.h): max_iters = 0 reports x0's true residual; b = 0 gives x = 0 at once;
+    a non-zero x0 (x0_zero = False) converges to the same solution; restart > 120 is clamped."""
+    pb, o, g = _pair("C1")
+    b = _cuda(pb.b)
+    x = torch.zeros(pb.n, dtype=torch.float64, device=dev)
+    info = g.solve(b, x, max_iters=0)
+    assert info["status"] == "NOT_CONVERGED" and info["iterations"] == 0 and abs(info["true_relres"] - 1.0) < 1e-14
+    z = torch.zeros_like(b)
+    x.fill_(3.0)
+    info = g.solve(z, x)
+    assert info["status"] == "OK" and info["iterations"] == 0 and float(x.abs().max()) == 0.0
+    x_ref = torch.zeros_like(b)
+    g.solve(b, x_ref)
+    x0 = x_ref + 1e-3 * _cuda(np.random.default_rng(3).uniform(-1, 1, pb.n))
+    info = g.solve(b, x0, x0_zero=False)
+    assert info["status"] == "OK" and info["true_relres"] <= 1e-8
+    assert torch.linalg.norm(x0 - x_ref) <= 1e-3 * torch.linalg.norm(x_ref)   # both at rtol 1e-8, cond(A) ~ 1e4
+    x1 = torch.zeros_like(b)
+    info = g.solve(b, x1, restart=500)
+    assert info["status"] == "OK" and info["restarts"] == 0

@@ -488,6 +488,15 @@ int main(int argc, char **argv)
     long n = argc > 1 ? atol(argv[1]) : 42000000;
     int nv = argc > 2 ? atoi(argv[2]) : 30;
     double *V, *w, *part, *h;
+    // optional extra device footprint (GB) to mimic the solver's ~110 GB working set (TLB reach)
+    const double extra_gb = argc > 3 ? atof(argv[3]) : 0.0;
+    std::vector<void *> extra;
+    for (double gb = 0; gb < extra_gb; gb += 4.0) {
+        void *p = nullptr;
+        if (cudaMalloc(&p, (size_t)4 << 30) != cudaSuccess) break;
+        cudaMemset(p, 0, (size_t)4 << 30);
+        extra.push_back(p);
+    }
     cudaMalloc(&V, sizeof(double) * n * (nv + 1));
     cudaMalloc(&w, sizeof(double) * n);
     cudaMalloc(&part, sizeof(double) * 200000 * 70);
@@ -571,6 +580,8 @@ int main(int argc, char **argv)
         timeit(nm, vb * (nv + 1), [&] { mdot2<4, 4><<<nch, KB>>>(nv, V, n, V + (nv - 1) * n, w, CH, n, part, nch); });
         snprintf(nm, 64, "mdot2i G4 U2");
         timeit(nm, vb * (nv + 1), [&] { mdot2i<4, 2><<<nch, KB>>>(nv, V, n, V + (nv - 1) * n, w, CH, n, part, nch); });
+        snprintf(nm, 64, "mdot2i G4 U2 misaligned+5");
+        timeit(nm, vb * (nv + 1), [&] { mdot2i<4, 2><<<nch, KB>>>(nv, V + 5, n, V + (nv - 1) * n + 5, w + 5, CH, n - 8, part, nch); });
         snprintf(nm, 64, "mdot2i G4 U4");
         timeit(nm, vb * (nv + 1), [&] { mdot2i<4, 4><<<nch, KB>>>(nv, V, n, V + (nv - 1) * n, w, CH, n, part, nch); });
         snprintf(nm, 64, "mdot2i G2 U8");
