@@ -290,3 +290,28 @@ def test_solve_edge_cases(dev):
     x1 = torch.zeros_like(b)
     info = g.solve(b, x1, restart=500)
     assert info["status"] == "OK" and info["restarts"] == 0
+
+
+@pytest.mark.parametrize("grid", [(1, 1, 1), (2, 1, 1), (1, 1, 20), (1, 17, 3), (33, 2, 1), (5, 4, 17)])
+def test_degenerate_grids(dev, grid):
+    """Edge cases of the structured path: single cells, columns, slabs one cell thick, a clipped 33-wide tile,
+    a z-extent crossing one z-block boundary.  Operator, one application and FGMRES against the oracle."""
+    from paper_1812_05540_b200 import Tsp
+    nx, ny, nz = grid
+    pb = synth.generate(nx=nx, ny=ny, nz=nz, recipe=2, perm_sigma=1.0)
+    o = oracle.Oracle(pb).setup()
+    g = Tsp(pb).setup()
+    v = np.random.default_rng(17).uniform(-1, 1, pb.n)
+    y = torch.empty(pb.n, dtype=torch.float64, device=dev)
+    z = torch.empty(pb.n, dtype=torch.float64, device=dev)
+    g.apply_operator(_cuda(v), y)
+    g.apply_preconditioner(_cuda(v), z)
+    torch.cuda.synchronize()
+    yo, zo = o.operator(v), o.apply(v)
+    assert np.linalg.norm(y.cpu().numpy() - yo) <= 1e-13 * np.linalg.norm(yo)
+    assert np.linalg.norm(z.cpu().numpy() - zo) <= 1e-10 * np.linalg.norm(zo)
+    xo, io = o.solve(pb.b, rtol=1e-8, m=64)
+    x = torch.zeros(pb.n, dtype=torch.float64, device=dev)
+    ig = g.solve(_cuda(pb.b), x, rtol=1e-8)
+    assert ig["status"] == "OK" and io["status"] == 0 and abs(ig["iterations"] - io["iterations"]) <= 1
+    g.close()
