@@ -117,3 +117,14 @@ def test_sharded_bitwise_equals_single(problem, P, rep):
                 for L in Ls:
                     for k in ("A_rp", "A_ci", "A_v", "dl1"):
                         assert np.array_equal(L[k], L1[k]), (w, l, k)
+
+
+def test_more_ranks_than_z_blocks_is_rejected():
+    """nz = 20 has two z-blocks of 16 planes: a rank must own at least one (include/tsp.h, tsp_create), so P = 4
+    is refused with TSP_ERR_INVALID_ARG and a message, on every rank, instead of hanging in a collective."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1812_05540_b200.tsp import TspError
+    pb = synth.generate(nx=9, ny=7, nz=20, recipe=2, perm_sigma=1.5)
+    with pytest.raises(TspError, match="more ranks than z-blocks"):
+        _run_ranks(pb, 4, _work(pb))
