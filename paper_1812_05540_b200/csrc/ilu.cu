@@ -39,6 +39,15 @@ __device__ __forceinline__ int64_t didx(const TileGeo &g, int64_t t, int lk, int
 }
 __device__ __forceinline__ int sidx(const TileGeo &g, int lk, int lj, int li) { return ((lk * g.ty + lj) * g.tx + li) * 2; }
 
+// line `slot` of wavefront level l (lj + lk = l, lk ascending; same order as the host's line table)
+__device__ __forceinline__ bool line_at(const TileGeo &g, int l, int slot, int &lj, int &lk)
+{
+    const int lo = max(0, l - g.ty + 1), hi = min(l, g.tz - 1);
+    lk = lo + slot; lj = l - lk;
+    if (lk > hi) { lj = lk = 0; return false; }
+    return true;
+}
+
 // fill the tile-ordered S_ff^FS = A_ff + diag(D_sp, D_pp) blocks (a1 folded in)
 // (column ids are GLOBAL cell ids: neighbours in the ranks below/above keep their stencil slot)
 __global__ void k_ilu_fill(TileGeo g, int nyg, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
@@ -147,15 +156,12 @@ __device__ __forceinline__ void affine_scan(double M[4], double c[2], int lseg, 
     }
 }
 
-// steps 6-8 fused (P:629-634), pipelined form:
-//  phase 0 (fully parallel, coalesced): w = y - S^FS z for every cell of the tile -> shared memory
-//  forward / backward line wavefronts: per level only 4 blocks per cell are read from global
-//  memory, and they are prefetched into registers one level ahead (before the barrier).
-// One line per W-lane segment; requires (lines per level) <= segments per CTA.
-__device__ __forceinline__ void pf_load(const double *__restrict__ ival, const double *__restrict__ dinv, const TileGeo &g,
-                                        int64_t t, int lk, int lj, int li, bool ok, const int s3[3], double P[16])
+// register prefetch of a line's 3 off-diagonal blocks (forward: -y,-z,-x; backward: +y,+z,+x) and D_K
+__device__ __forceinline__ void pf_load_dir(const double *__restrict__ ival, const double *__restrict__ dinv, const TileGeo &g,
+                                            int64_t t, int lk, int lj, int li, bool ok, bool fwd, double P[16])
 {
     if (!ok) return;
+    const int s3[3] = {fwd ? 1 : 5, fwd ? 0 : 6, fwd ? 2 : 4};
 #pragma unroll
     for (int q = 0; q < 3; ++q)
 #pragma unroll
@@ -164,8 +170,44 @@ __device__ __forceinline__ void pf_load(const double *__restrict__ ival, const d
     for (int e = 0; e < 4; ++e) P[12 + e] = dinv[didx(g, t, lk, lj, e, li)];
 }
 
+// phase-0 slot batch [S0, S1): loads first, then the accumulation in slot order (same rounding as slot by slot)
+#define P0_BATCH(S0, S1)                                                                                         \
+    {                                                                                                            \
+        constexpr int dxs[7] = {0, 0, -1, 0, 1, 0, 0}, dys[7] = {0, -1, 0, 0, 0, 1, 0}, dzs[7] = {-1, 0, 0, 0, 0, 0, 1}; \
+        double Z0[7], Z1[7], AA[7][4];                                                                           \
+        bool use[7];                                                                                             \
+        _Pragma("unroll") for (int s = S0; s < S1; ++s) {                                                        \
+            const int ni = gi + dxs[s], nj = gj + dys[s], nk = gk + dzs[s];                                      \
+            use[s] = ni >= 0 && nj >= 0 && ni < g.nx && nj < g.ny;                                               \
+            const double *p0 = zs, *p1 = zp;                                                                     \
+            int64_t q = gc + dxs[s] + dys[s] * sy + dzs[s] * sz;                                                 \
+            if (dzs[s] < 0 && nk < 0) {                                                                          \
+                use[s] = use[s] && g.nlo; p0 = zs_gh; p1 = zp_gh; q = (int64_t)nj * g.nx + ni;                   \
+            } else if (dzs[s] > 0 && nk >= g.nz) {                                                               \
+                use[s] = use[s] && g.nhi; p0 = zs_gh + g.nlo; p1 = zp_gh + g.nlo; q = (int64_t)nj * g.nx + ni;   \
+            }                                                                                                    \
+            if (!use[s]) { p0 = zs; p1 = zp; q = gc; }                                                           \
+            Z0[s] = __ldg(p0 + q); Z1[s] = __ldg(p1 + q);                                                        \
+            _Pragma("unroll") for (int e = 0; e < 4; ++e) AA[s][e] = __ldg(ival + vidx(g, t, lk, lj, s, e, li)); \
+        }                                                                                                        \
+        _Pragma("unroll") for (int s = S0; s < S1; ++s)                                                          \
+            if (use[s]) {                                                                                        \
+                r0 -= AA[s][0] * Z0[s] + AA[s][1] * Z1[s];                                                       \
+                r1 -= AA[s][2] * Z0[s] + AA[s][3] * Z1[s];                                                       \
+            }                                                                                                    \
+    }
+#define P0B 4   // slots per load batch (all 7 at once costs occupancy; measured on C5)
+
+// steps 6-8 fused (P:629-634), pipelined form:
+//  phase 0 (fully parallel, coalesced): w = y - S^FS z for every cell of the tile -> shared memory,
+//  each cell's loads issued in two batches (phase 0 was latency bound with one round trip per slot)
+//  forward / backward line wavefronts: per level only 4 blocks per cell (and z for step 8) are read
+//  from global memory, prefetched into registers one level ahead and issued before the scan, so the
+//  load overlaps the scan and the barrier.  3 CTAs per SM (the shared-memory limit) matter more than
+//  a deeper prefetch: at 2 CTAs per SM the kernel is 1.5x slower (measured on C5).
+// One line per W-lane segment; requires (lines per level) <= segments per CTA.
 template <bool BGS>
-__global__ void __launch_bounds__(256) k_ilu_apply2(TileGeo g, const int32_t *__restrict__ lines, const int32_t *__restrict__ lvlptr,
+__global__ void __launch_bounds__(256, 3) k_ilu_apply2(TileGeo g, const int32_t *__restrict__ lines, const int32_t *__restrict__ lvlptr,
                                                     const double *__restrict__ ival, const double *__restrict__ dinv,
                                                     const double *__restrict__ yf, const double *__restrict__ zs,
                                                     const double *__restrict__ zp, const double *__restrict__ zs_gh,
@@ -186,44 +228,24 @@ __global__ void __launch_bounds__(256) k_ilu_apply2(TileGeo g, const int32_t *__
         if (!(xin && gj < g.ny && gk < g.nz)) continue;
         const int64_t gc = gi + sy * gj + sz * gk;
         double r0 = yf[2 * gc], r1 = yf[2 * gc + 1];
-        const int dxs[7] = {0, 0, -1, 0, 1, 0, 0}, dys[7] = {0, -1, 0, 0, 0, 1, 0}, dzs[7] = {-1, 0, 0, 0, 0, 0, 1};
-#pragma unroll
-        for (int s = 0; s < 7; ++s) {
-            const int ni = gi + dxs[s], nj = gj + dys[s], nk = gk + dzs[s];
-            if (ni < 0 || nj < 0 || ni >= g.nx || nj >= g.ny) continue;
-            double z0, z1;
-            if (nk < 0) {                       // plane below the slab: halo from rank-1
-                if (!g.nlo) continue;
-                z0 = zs_gh[nj * g.nx + ni]; z1 = zp_gh[nj * g.nx + ni];
-            } else if (nk >= g.nz) {            // plane above the slab: halo from rank+1
-                if (!g.nhi) continue;
-                z0 = zs_gh[g.nlo + nj * g.nx + ni]; z1 = zp_gh[g.nlo + nj * g.nx + ni];
-            } else {
-                const int64_t gn = gc + dxs[s] + dys[s] * sy + dzs[s] * sz;
-                z0 = zs[gn]; z1 = zp[gn];
-            }
-            double A[4];
-            ld2x2(ival, g, t, lk, lj, s, li, A);
-            r0 -= A[0] * z0 + A[1] * z1;
-            r1 -= A[2] * z0 + A[3] * z1;
-        }
+        // all loads of a batch of slots are issued before the first use (branch-free addressing: absent
+        // neighbours read a dummy and are masked), so a cell costs P0B round trips instead of 7
+        P0_BATCH(0, P0B)
+        P0_BATCH(P0B, 7)
         sm[sidx(g, lk, lj, li)] = r0;
         sm[sidx(g, lk, lj, li) + 1] = r1;
     }
     // ---------------- forward
-    const int fw[3] = {1, 0, 2}, bw[3] = {5, 6, 4};   // (-y, -z, -x) and (+y, +z, +x)
-    double P[16];
+    double P[16], zn0 = 0, zn1 = 0;   // zn: z at the backward sweep's next cell (step 8)
     {
-        const int idx = lvlptr[0] + slot0;
-        const bool lv = idx < lvlptr[1];
-        const int lj = lv ? (lines[idx] & 0xffff) : 0, lk = lv ? (lines[idx] >> 16) : 0;
-        pf_load(ival, dinv, g, t, lk, lj, li, lv && xin && TJ * g.ty + lj < g.ny && TK * g.tz + lk < g.nz, fw, P);
+        int lj, lk;
+        const bool lv = line_at(g, 0, slot0, lj, lk);
+        pf_load_dir(ival, dinv, g, t, lk, lj, li, lv && xin && TJ * g.ty + lj < g.ny && TK * g.tz + lk < g.nz, true, P);
     }
     __syncthreads();
     for (int l = 0; l < g.nlev; ++l) {
-        const int idx = lvlptr[l] + slot0;
-        const bool lv = idx < lvlptr[l + 1];
-        const int lj = lv ? (lines[idx] & 0xffff) : 0, lk = lv ? (lines[idx] >> 16) : 0;
+        int lj, lk;
+        const bool lv = line_at(g, l, slot0, lj, lk);
         const bool ok = lv && xin && TJ * g.ty + lj < g.ny && TK * g.tz + lk < g.nz;
         double M[4] = {0, 0, 0, 0}, c[2] = {0, 0};
         if (ok) {
@@ -244,6 +266,18 @@ __global__ void __launch_bounds__(256) k_ilu_apply2(TileGeo g, const int32_t *__
                 M[0] = -T[0]; M[1] = -T[1]; M[2] = -T[2]; M[3] = -T[3];
             }
         }
+        // prefetch the next level's blocks (or the backward sweep's first level) while the scan runs
+        {
+            const int ln = l + 1 < g.nlev ? l + 1 : g.nlev - 1;
+            int ljn, lkn;
+            const bool lvn = line_at(g, ln, slot0, ljn, lkn);
+            const bool okn = lvn && xin && TJ * g.ty + ljn < g.ny && TK * g.tz + lkn < g.nz && (!BGS || l + 1 < g.nlev);
+            pf_load_dir(ival, dinv, g, t, lkn, ljn, li, okn, l + 1 < g.nlev, P);
+            if (!BGS && l + 1 == g.nlev && okn) {
+                const int64_t gcn = gi + sy * (TJ * g.ty + ljn) + sz * (TK * g.tz + lkn);
+                zn0 = zs[gcn]; zn1 = zp[gcn];
+            }
+        }
         affine_scan<true>(M, c, lseg, W);
         if (ok) { sm[sidx(g, lk, lj, li)] = c[0]; sm[sidx(g, lk, lj, li) + 1] = c[1]; }
         if (BGS && ok) {                          // hybrid block GS: the forward sweep is the whole M_L (step 8)
@@ -251,23 +285,13 @@ __global__ void __launch_bounds__(256) k_ilu_apply2(TileGeo g, const int32_t *__
             zout[2 * gc] = zs[gc] + c[0];
             zout[2 * gc + 1] = zp[gc] + c[1];
         }
-        // prefetch the next level's blocks (or the backward sweep's first level)
-        {
-            const int ln = l + 1 < g.nlev ? l + 1 : g.nlev - 1;
-            const int idn = lvlptr[ln] + slot0;
-            const bool lvn = idn < lvlptr[ln + 1];
-            const int ljn = lvn ? (lines[idn] & 0xffff) : 0, lkn = lvn ? (lines[idn] >> 16) : 0;
-            pf_load(ival, dinv, g, t, lkn, ljn, li, lvn && xin && TJ * g.ty + ljn < g.ny && TK * g.tz + lkn < g.nz,
-                    l + 1 < g.nlev ? fw : bw, P);
-        }
         __syncthreads();
     }
     // ---------------- backward (ILU only)
     if constexpr (!BGS)
     for (int l = g.nlev - 1; l >= 0; --l) {
-        const int idx = lvlptr[l] + slot0;
-        const bool lv = idx < lvlptr[l + 1];
-        const int lj = lv ? (lines[idx] & 0xffff) : 0, lk = lv ? (lines[idx] >> 16) : 0;
+        int lj, lk;
+        const bool lv = line_at(g, l, slot0, lj, lk);
         const int gj = TJ * g.ty + lj, gk = TK * g.tz + lk;
         const bool ok = lv && xin && gj < g.ny && gk < g.nz;
         double M[4] = {0, 0, 0, 0}, c[2] = {0, 0};
@@ -289,18 +313,23 @@ __global__ void __launch_bounds__(256) k_ilu_apply2(TileGeo g, const int32_t *__
                 M[0] = -T[0]; M[1] = -T[1]; M[2] = -T[2]; M[3] = -T[3];
             }
         }
+        const double zc0 = zn0, zc1 = zn1;
+        if (l > 0) {
+            int ljn, lkn;
+            const bool lvn = line_at(g, l - 1, slot0, ljn, lkn);
+            const bool okn = lvn && xin && TJ * g.ty + ljn < g.ny && TK * g.tz + lkn < g.nz;
+            pf_load_dir(ival, dinv, g, t, lkn, ljn, li, okn, false, P);
+            if (okn) {
+                const int64_t gcn = gi + sy * (TJ * g.ty + ljn) + sz * (TK * g.tz + lkn);
+                zn0 = zs[gcn]; zn1 = zp[gcn];
+            }
+        }
         affine_scan<false>(M, c, lseg, W);
         if (ok) {
             sm[sidx(g, lk, lj, li)] = c[0]; sm[sidx(g, lk, lj, li) + 1] = c[1];
             const int64_t gc = gi + sy * gj + sz * gk;
-            zout[2 * gc] = zs[gc] + c[0];        // step 8
-            zout[2 * gc + 1] = zp[gc] + c[1];
-        }
-        if (l > 0) {
-            const int idn = lvlptr[l - 1] + slot0;
-            const bool lvn = idn < lvlptr[l];
-            const int ljn = lvn ? (lines[idn] & 0xffff) : 0, lkn = lvn ? (lines[idn] >> 16) : 0;
-            pf_load(ival, dinv, g, t, lkn, ljn, li, lvn && xin && TJ * g.ty + ljn < g.ny && TK * g.tz + lkn < g.nz, bw, P);
+            zout[2 * gc] = zc0 + c[0];           // step 8
+            zout[2 * gc + 1] = zc1 + c[1];
         }
         __syncthreads();
     }
@@ -373,8 +402,9 @@ void ilu_apply_fused(Ctx &c, const double *yf, const double *zs, const double *z
     TSP_REQUIRE(smem <= 227 * 1024, TSP_ERR_INVALID_ARG, "ILU tile too large for shared memory");
     const double *zs_gh = c.gh_f2.p, *zp_gh = c.gh_f2.p ? c.gh_f2.p + c.hf.nghost() : nullptr;
     prof_begin(c, PK_ILU);
-    if (c.ntiles) (c.o.second_stage == 1 ? k_ilu_apply2<true> : k_ilu_apply2<false>)<<<c.ntiles, 256, smem, c.s>>>(g, c.ilu_cells, c.ilu_lvlptr, c.ilu_val, c.ilu_dinv, yf, zs, zp, zs_gh,
-                                                           zp_gh, zf_out);
+    if (c.ntiles)
+        (c.o.second_stage == 1 ? k_ilu_apply2<true> : k_ilu_apply2<false>)<<<c.ntiles, 256, smem, c.s>>>(
+            g, c.ilu_cells, c.ilu_lvlptr, c.ilu_val, c.ilu_dinv, yf, zs, zp, zs_gh, zp_gh, zf_out);
     prof_end(c, PK_ILU, (28.0 * 8 + 32 + 16 + 16 + 16) * c.Nc);
     c.launches += 1;
     TSP_CUDA(cudaGetLastError());
