@@ -179,12 +179,14 @@ def test_device_inputs(dev):
 
 
 @pytest.mark.slow
-def test_c4_sampled_apply_and_operator(dev):
-    """BASELINE.json's C4 size in the bench's launch configuration: operator
-    rows sampled against a direct row evaluation from the input blocks, and a
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_full_size_sampled_apply_and_operator(dev, name):
+    """BASELINE.json's full sizes (C5 is the configuration bench.py times), in the bench's launch
+    configuration: operator rows sampled against a direct row evaluation from the input blocks,
+    linearity of the whole two-stage preconditioner (a property that holds at any size), and a
     solve that converges with a verified true residual."""
     from paper_1812_05540_b200 import Tsp
-    pb = synth.generate("C4")
+    pb = synth.generate(name)
     g = Tsp(pb).setup()
     x = np.random.default_rng(13).uniform(-1, 1, pb.n)
     y = torch.empty(pb.n, dtype=torch.float64, device=dev)
@@ -199,9 +201,19 @@ def test_c4_sampled_apply_and_operator(dev):
         for q in range(pb.uf_rowptr[node], pb.uf_rowptr[node + 1]):
             ref += pb.uf_val[q] @ xf[2 * pb.uf_col[q]:2 * pb.uf_col[q] + 2]
         np.testing.assert_allclose(got[3 * node:3 * node + 3], ref, rtol=1e-12, atol=1e-14 * np.abs(ref).max())
+    # M^-1 is linear: M(a x + v) = a M(x) + M(v) up to rounding
+    v = np.random.default_rng(15).uniform(-1, 1, pb.n)
+    zx, zv, zs = (torch.empty(pb.n, dtype=torch.float64, device=dev) for _ in range(3))
+    g.apply_preconditioner(_cuda(x), zx)
+    g.apply_preconditioner(_cuda(v), zv)
+    g.apply_preconditioner(_cuda(0.75 * x + v), zs)
+    lin = (0.75 * zx + zv - zs).norm().item() / zs.norm().item()
+    assert lin <= 1e-11, lin
+    del zx, zv, zs, y
     xs = torch.zeros(pb.n, dtype=torch.float64, device=dev)
     info = g.solve(_cuda(pb.b), xs)
     assert info["status"] == "OK" and info["true_relres"] <= 1e-8
+    g.close()
 
 
 @pytest.mark.parametrize("m", [5, 17])
