@@ -96,15 +96,12 @@ void dbg_alloc(double t0, size_t bytes)
 struct StreamScope {
     explicit StreamScope(cudaStream_t s) {
         g_alloc_stream = s;
-        static bool pool_set = false;
-        if (!pool_set) {
-            int dev = 0;
-            cudaMemPool_t pool;
-            if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-                uint64_t thr = UINT64_MAX;
-                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-            }
-            pool_set = true;
+        // per call (idempotent, thread-safe, ~1 us): the pool belongs to the current device
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
     }
 };

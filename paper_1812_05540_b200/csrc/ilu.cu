@@ -370,6 +370,9 @@ void ilu_setup(Ctx &c, const double *)
         TSP_CUDA(cudaMemcpyAsync(c.ilu_lvlptr, lvlptr.data(), sizeof(int32_t) * lvlptr.size(), cudaMemcpyHostToDevice, c.s));
         TSP_CUDA(cudaStreamSynchronize(c.s));
     }
+    // per handle (the attribute is per device; tsp_setup runs on the handle's device)
+    TSP_CUDA(cudaFuncSetAttribute(k_ilu_apply2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    TSP_CUDA(cudaFuncSetAttribute(k_ilu_apply2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     c.ntx = g.ntx; c.nty = g.nty; c.ntz = g.ntz;
     c.ntiles = g.ntx * g.nty * g.ntz;
     const size_t per_tile = (size_t)g.tz * g.ty * g.W;
@@ -393,12 +396,6 @@ void ilu_apply_fused(Ctx &c, const double *yf, const double *zs, const double *z
 {
     TileGeo g = geo(c);
     const size_t smem = sizeof(double) * 2 * (size_t)g.tx * g.ty * g.tz;
-    static bool attr_set = false;
-    if (!attr_set) {
-        TSP_CUDA(cudaFuncSetAttribute(k_ilu_apply2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        TSP_CUDA(cudaFuncSetAttribute(k_ilu_apply2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr_set = true;
-    }
     TSP_REQUIRE(smem <= 227 * 1024, TSP_ERR_INVALID_ARG, "ILU tile too large for shared memory");
     const double *zs_gh = c.gh_f2.p, *zp_gh = c.gh_f2.p ? c.gh_f2.p + c.hf.nghost() : nullptr;
     prof_begin(c, PK_ILU);
