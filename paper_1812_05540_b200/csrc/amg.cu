@@ -295,23 +295,32 @@ __device__ void pfill_row(int i, int nc, const int32_t *__restrict__ rp, const i
                           const int32_t *__restrict__ prp, int32_t *pci, double *pv, int *overflow)
 {
     int32_t tmp[PMAX];
-    int cnt = collect_aggs(i, rp, ci, E, agg, tmp, overflow);
-    int64_t o = prp[i];
-    for (int t = 0; t < cnt; ++t) {
-        int J = tmp[t];
-        pci[o + t] = J;
-        for (int c = 0; c < nc; ++c) {
-            double di = d[(int64_t)i * nc + c];
-            double w = (di != 0.0) ? __ddiv_rn(om.w[c], di) : 0.0;
-            double s = 0.0;
-            for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
-                int j = ci[q];
-                if (!((j == i) || E[q]) || agg[j] != J) continue;
-                double a = (j == i) ? di : v[q * nc + c];
-                s = __dadd_rn(s, a);
-            }
-            double delta = (J == agg[i]) ? 1.0 : 0.0;
-            pv[(o + t) * nc + c] = __dsub_rn(delta, __dmul_rn(w, s));
+    double s[PMAX];
+    const int cnt = collect_aggs(i, rp, ci, E, agg, tmp, overflow);
+    const int64_t o = prp[i];
+    for (int t = 0; t < cnt; ++t) pci[o + t] = tmp[t];
+    if (!cnt) return;
+    const int ai = agg[i];
+    for (int c = 0; c < nc; ++c) {
+        const double di = d[(int64_t)i * nc + c];
+        const double w = (di != 0.0) ? __ddiv_rn(om.w[c], di) : 0.0;
+        for (int t = 0; t < cnt; ++t) s[t] = 0.0;
+        // one pass over the row: entry q adds to the sum of its aggregate; each sum is still the fold over
+        // the row in q order restricted to that aggregate (R-prolong), as in the per-aggregate loop
+        for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+            const int j = ci[q];
+            if (!((j == i) || E[q])) continue;
+            const int J = agg[j];
+            if (J < 0) continue;
+            int t = 0;
+            while (t < cnt && tmp[t] != J) ++t;
+            if (t == cnt) continue;   // only after an overflow (the row is then rejected)
+            const double a = (j == i) ? di : v[q * nc + c];
+            s[t] = __dadd_rn(s[t], a);
+        }
+        for (int t = 0; t < cnt; ++t) {
+            const double delta = (tmp[t] == ai) ? 1.0 : 0.0;
+            pv[(o + t) * nc + c] = __dsub_rn(delta, __dmul_rn(w, s[t]));
         }
     }
 }
