@@ -196,77 +196,37 @@ __global__ void k_phase2(int n, int nc, const int32_t *__restrict__ rp, const in
 
 // ------------------------------------------------------------------ smoothed prolongator (R-prolong)
 // d_i = a_ii + fold_{weak j} a_ij ; ratio_i = fold_j |a^F_ij| / |d_i|
-__device__ void pdiag_row(int i, int nc, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
-                          const double *__restrict__ v, const uint8_t *__restrict__ E, double *d, unsigned long long *rho_bits)
+// thread per (row, component), each fold serial in q order; rho reduced per block first (measured at C5: 2-4x
+// faster than a warp per row with the entries broadcast by shuffles)
+__global__ void __launch_bounds__(256) k_pdiag(int n, int nc, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                                                 const double *__restrict__ v, const uint8_t *__restrict__ E, double *d,
+                                                 unsigned long long *rho_bits)
 {
-    int64_t qd = -1;
-    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) if (ci[q] == i) { qd = q; break; }
-    for (int c = 0; c < nc; ++c) {
+    __shared__ unsigned long long bm[3];
+    if (threadIdx.x < 3) bm[threadIdx.x] = 0ULL;
+    __syncthreads();
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < (int64_t)n * nc) {
+        const int i = (int)(t / nc), c = (int)(t % nc);
+        const int64_t q0 = rp[i], q1 = rp[i + 1];
+        int64_t qd = -1;
+        for (int64_t q = q0; q < q1; ++q) if (ci[q] == i) { qd = q; break; }
         double di = qd >= 0 ? v[qd * nc + c] : 0.0;
-        for (int64_t q = rp[i]; q < rp[i + 1]; ++q)
+        for (int64_t q = q0; q < q1; ++q)
             if (ci[q] != i && !E[q]) di = __dadd_rn(di, v[q * nc + c]);
         d[(int64_t)i * nc + c] = di;
-        if (di == 0.0) continue;
-        double s = 0.0;
-        for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
-            double a = (ci[q] == i) ? di : (E[q] ? v[q * nc + c] : 0.0);
-            s = __dadd_rn(s, fabs(a));
-        }
-        double r = __ddiv_rn(s, fabs(di));
-        atomicMax(rho_bits + c, (unsigned long long)__double_as_longlong(r));   // r >= 0: bit order = value order
-    }
-}
-// the three values of a lane's entry, the one of component `lane` (lanes 0..2) picked without local memory
-__device__ __forceinline__ double pick3(const double (&x)[3], int k) { return k == 0 ? x[0] : k == 1 ? x[1] : x[2]; }
-
-// one warp per row: entries loaded coalesced (lane = entry), the folds stay sequential in q order (shuffles to
-// lanes 0..nc-1, one component each), so d and rho are bitwise the serial definition; rows > 32 entries: lane 0
-// runs the serial code
-__global__ void __launch_bounds__(256) k_pdiag(int n, int nc, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
-                                               const double *__restrict__ v, const uint8_t *__restrict__ E, double *d,
-                                               unsigned long long *rho_bits)
-{
-    const int lane = threadIdx.x & 31;
-    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += (gridDim.x * blockDim.x) >> 5) {
-        const int64_t q0 = rp[i];
-        const int len = (int)(rp[i + 1] - q0);
-        if (len > 32) {
-            if (lane == 0) pdiag_row(i, nc, rp, ci, v, E, d, rho_bits);
-            continue;
-        }
-        const bool has = lane < len;
-        const int cq = has ? ci[q0 + lane] : -1;
-        const int eq = has ? E[q0 + lane] : 0;
-        double vq[3] = {0.0, 0.0, 0.0};
-        for (int c = 0; c < nc; ++c) vq[c] = has ? v[(q0 + lane) * nc + c] : 0.0;
-        const unsigned dm = __ballot_sync(0xffffffffu, has && cq == i);
-        const int qd = dm ? __ffs(dm) - 1 : 0;
-        double dv[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) dv[c] = __shfl_sync(0xffffffffu, vq[c], qd);
-        double di = (dm && lane < nc) ? pick3(dv, lane) : 0.0;
-        for (int t = 0; t < len; ++t) {
-            const int ct = __shfl_sync(0xffffffffu, cq, t), et = __shfl_sync(0xffffffffu, eq, t);
-            double vt[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) vt[c] = __shfl_sync(0xffffffffu, vq[c], t);
-            if (lane < nc && ct != i && !et) di = __dadd_rn(di, pick3(vt, lane));
-        }
-        if (lane < nc) d[(int64_t)i * nc + lane] = di;
-        double s = 0.0;
-        for (int t = 0; t < len; ++t) {
-            const int ct = __shfl_sync(0xffffffffu, cq, t), et = __shfl_sync(0xffffffffu, eq, t);
-            double vt[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) vt[c] = __shfl_sync(0xffffffffu, vq[c], t);
-            const double a = (ct == i) ? di : (et ? pick3(vt, lane < 3 ? lane : 0) : 0.0);
-            s = __dadd_rn(s, fabs(a));
-        }
-        if (lane < nc && di != 0.0) {
+        if (di != 0.0) {
+            double s = 0.0;
+            for (int64_t q = q0; q < q1; ++q) {
+                const double a = (ci[q] == i) ? di : (E[q] ? v[q * nc + c] : 0.0);
+                s = __dadd_rn(s, fabs(a));
+            }
             const double r = __ddiv_rn(s, fabs(di));
-            atomicMax(rho_bits + lane, (unsigned long long)__double_as_longlong(r));
+            atomicMax(&bm[c], (unsigned long long)__double_as_longlong(r));   // r >= 0: bit order = value order
         }
     }
+    __syncthreads();
+    if (threadIdx.x < nc && bm[threadIdx.x]) atomicMax(rho_bits + threadIdx.x, bm[threadIdx.x]);
 }
 struct Omega { double w[3]; };
 #define PMAX 512
@@ -930,7 +890,7 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
         // prolongator
         DBuf<double> d; d.alloc((size_t)std::max(n, 1) * nc);
         DBuf<unsigned long long> rho; rho.alloc(3); rho.zero(c.s);
-        if (n) k_pdiag<<<std::min(grid_for((int64_t)n * 32, 256), c.sm_count * 32), 256, 0, c.s>>>(n, nc, Lf.A.rp, Lf.A.ci, Lf.A.v, E, d, rho);
+        if (n) k_pdiag<<<grid_for((int64_t)n * nc, 256), 256, 0, c.s>>>(n, nc, Lf.A.rp, Lf.A.ci, Lf.A.v, E, d, rho);
         unsigned long long rb[3] = {0, 0, 0};
         TSP_CUDA(cudaMemcpyAsync(rb, rho.p, sizeof(rb), cudaMemcpyDeviceToHost, c.s));
         TSP_CUDA(cudaStreamSynchronize(c.s));
