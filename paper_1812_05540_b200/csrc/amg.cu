@@ -38,22 +38,21 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t x)
 __device__ __forceinline__ uint64_t prio(int i) { return ((uint64_t)fmix32((uint32_t)i) << 32) | (uint64_t)(uint32_t)i; }
 
 // ------------------------------------------------------------------ l1 norms: d_i = fold_j |a_ij|
+// thread per (row, component): the fold of each component stays serial in q order
 __global__ void k_l1(int n, int nc, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const double *__restrict__ v,
                      double *dl1, double *dinv)
 {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    for (int c = 0; c < nc; ++c) {
-        double s = 0.0, aii = 0.0;
-        for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
-            s = __dadd_rn(s, fabs(v[q * nc + c]));
-            if (ci[q] == i) aii = v[q * nc + c];
-        }
-        if (aii < 0.0) s = -s;                             // R-l1: the sign of the diagonal
-
-        dl1[(int64_t)i * nc + c] = s;
-        dinv[(int64_t)i * nc + c] = s != 0.0 ? 1.0 / s : 0.0;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)n * nc) return;
+    const int i = (int)(t / nc), c = (int)(t % nc);
+    double s = 0.0, aii = 0.0;
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+        s = __dadd_rn(s, fabs(v[q * nc + c]));
+        if (ci[q] == i) aii = v[q * nc + c];
     }
+    if (aii < 0.0) s = -s;                                 // R-l1: the sign of the diagonal
+    dl1[t] = s;
+    dinv[t] = s != 0.0 ? 1.0 / s : 0.0;
 }
 
 __device__ __forceinline__ double meas(const double *__restrict__ v, int64_t q, int nc)
@@ -64,19 +63,27 @@ __device__ __forceinline__ double meas(const double *__restrict__ v, int64_t q, 
 }
 
 // ------------------------------------------------------------------ strength (R-strength)
+// 8 lanes per row: the row max is order independent (exact), each entry's flag is its own
+constexpr int kStrG = 8;
 __global__ void k_strength(int n, int nc, int nown, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
                            const double *__restrict__ v, const int32_t *__restrict__ zb, double theta, uint8_t *S)
 {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int i = (int)(t / kStrG), sub = (int)(t % kStrG);
+    const bool ok = i < n;
+    const int64_t q0 = ok ? rp[i] : 0, q1 = ok ? rp[i + 1] : 0;
     double m = 0.0;
-    for (int64_t q = rp[i]; q < rp[i + 1]; ++q)
-        if (ci[q] != i) { double t = meas(v, q, nc); if (t > m) m = t; }
-    double thr = __dmul_rn(theta, m);
-    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
-        int j = ci[q];
+    for (int64_t q = q0 + sub; q < q1; q += kStrG)
+        if (ci[q] != i) { double u = meas(v, q, nc); if (u > m) m = u; }
+#pragma unroll
+    for (int o = kStrG / 2; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o, kStrG));
+    if (!ok) return;
+    const double thr = __dmul_rn(theta, m);
+    const int zi = zb[i];
+    for (int64_t q = q0 + sub; q < q1; q += kStrG) {
+        const int j = ci[q];
         // columns of other ranks (j >= nown) lie in other z-blocks by construction
-        S[q] = (j != i && m > 0.0 && j < nown && zb[i] == zb[j] && meas(v, q, nc) >= thr) ? 1 : 0;
+        S[q] = (j != i && m > 0.0 && j < nown && zi == zb[j] && meas(v, q, nc) >= thr) ? 1 : 0;
     }
 }
 
@@ -818,7 +825,7 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
         const int n = L.n;
         const int nown = n;   // rows of this rank; columns >= nown are ghosts
         L.dl1.alloc((size_t)std::max(n, 1) * nc); L.dinv.alloc((size_t)std::max(n, 1) * nc);
-        if (n) k_l1<<<grid_for(n, 256), 256, 0, c.s>>>(n, nc, L.A.rp, L.A.ci, L.A.v, L.dl1, L.dinv);
+        if (n) k_l1<<<grid_for((int64_t)n * nc, 256), 256, 0, c.s>>>(n, nc, L.A.rp, L.A.ci, L.A.v, L.dl1, L.dinv);
         c.launches++;
         if (L.dist && L.hp->any()) {
             L.dinv_gh.alloc((size_t)std::max(L.hp->nghost(), 1) * nc);
@@ -833,7 +840,7 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
         DBuf<uint8_t> S, E; S.alloc(L.A.nnz + 1); E.alloc(L.A.nnz + 1);
         err.zero(c.s);
         if (n) {
-            k_strength<<<grid_for(n, 256), 256, 0, c.s>>>(n, nc, nown, L.A.rp, L.A.ci, L.A.v, L.zb, c.o.amg_theta, S);
+            k_strength<<<grid_for((int64_t)n * kStrG, 256), 256, 0, c.s>>>(n, nc, nown, L.A.rp, L.A.ci, L.A.v, L.zb, c.o.amg_theta, S);
             k_symm<<<grid_for(n, 256), 256, 0, c.s>>>(n, nown, L.dist ? 1 : 0, L.A.rp, L.A.ci, S, E, err);
         }
         c.launches += 2;
