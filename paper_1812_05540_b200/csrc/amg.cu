@@ -87,12 +87,14 @@ __global__ void k_strength(int n, int nc, int nown, const int32_t *__restrict__ 
     }
 }
 
+// kStrG lanes per row, one entry (and its transpose search) per lane at a time
 __global__ void k_symm(int n, int nown, int linear, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
                        const uint8_t *__restrict__ S, uint8_t *E, int *err)
 {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int i = (int)(t / kStrG), sub = (int)(t % kStrG);
     if (i >= n) return;
-    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+    for (int64_t q = rp[i] + sub; q < rp[i + 1]; q += kStrG) {
         int j = ci[q];
         if (j == i || j >= nown) { E[q] = 0; continue; }
         int64_t lo = rp[j], hi = rp[j + 1] - 1, qt = -1;
@@ -841,7 +843,7 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
         err.zero(c.s);
         if (n) {
             k_strength<<<grid_for((int64_t)n * kStrG, 256), 256, 0, c.s>>>(n, nc, nown, L.A.rp, L.A.ci, L.A.v, L.zb, c.o.amg_theta, S);
-            k_symm<<<grid_for(n, 256), 256, 0, c.s>>>(n, nown, L.dist ? 1 : 0, L.A.rp, L.A.ci, S, E, err);
+            k_symm<<<grid_for((int64_t)n * kStrG, 256), 256, 0, c.s>>>(n, nown, L.dist ? 1 : 0, L.A.rp, L.A.ci, S, E, err);
         }
         c.launches += 2;
         TSP_REQUIRE(!d2h1(c, err.p), TSP_ERR_INVALID_ARG, "AMG input pattern is not structurally symmetric");
