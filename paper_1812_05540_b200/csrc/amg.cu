@@ -259,38 +259,38 @@ __device__ int collect_aggs(int i, const int32_t *__restrict__ rp, const int32_t
     }
     return cnt;
 }
-__device__ void pfill_row(int i, int nc, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, const double *__restrict__ v,
-                          const uint8_t *__restrict__ E, const int32_t *__restrict__ agg, const double *__restrict__ d, const Omega &om,
-                          const int32_t *__restrict__ prp, int32_t *pci, double *pv, int *overflow)
+// one (row, component): the aggregates of the row (every component's thread collects them; component 0
+// writes the column ids), then one pass over the row -- each sum is still the fold over the row in q order
+// restricted to its aggregate (R-prolong)
+__device__ void pfill_row(int i, int c, int nc, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                          const double *__restrict__ v, const uint8_t *__restrict__ E, const int32_t *__restrict__ agg,
+                          const double *__restrict__ d, const Omega &om, const int32_t *__restrict__ prp, int32_t *pci,
+                          double *pv, int *overflow)
 {
     int32_t tmp[PMAX];
     double s[PMAX];
     const int cnt = collect_aggs(i, rp, ci, E, agg, tmp, overflow);
     const int64_t o = prp[i];
-    for (int t = 0; t < cnt; ++t) pci[o + t] = tmp[t];
+    if (c == 0) for (int t = 0; t < cnt; ++t) pci[o + t] = tmp[t];
     if (!cnt) return;
     const int ai = agg[i];
-    for (int c = 0; c < nc; ++c) {
-        const double di = d[(int64_t)i * nc + c];
-        const double w = (di != 0.0) ? __ddiv_rn(om.w[c], di) : 0.0;
-        for (int t = 0; t < cnt; ++t) s[t] = 0.0;
-        // one pass over the row: entry q adds to the sum of its aggregate; each sum is still the fold over
-        // the row in q order restricted to that aggregate (R-prolong), as in the per-aggregate loop
-        for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
-            const int j = ci[q];
-            if (!((j == i) || E[q])) continue;
-            const int J = agg[j];
-            if (J < 0) continue;
-            int t = 0;
-            while (t < cnt && tmp[t] != J) ++t;
-            if (t == cnt) continue;   // only after an overflow (the row is then rejected)
-            const double a = (j == i) ? di : v[q * nc + c];
-            s[t] = __dadd_rn(s[t], a);
-        }
-        for (int t = 0; t < cnt; ++t) {
-            const double delta = (tmp[t] == ai) ? 1.0 : 0.0;
-            pv[(o + t) * nc + c] = __dsub_rn(delta, __dmul_rn(w, s[t]));
-        }
+    const double di = d[(int64_t)i * nc + c];
+    const double w = (di != 0.0) ? __ddiv_rn(om.w[c], di) : 0.0;
+    for (int t = 0; t < cnt; ++t) s[t] = 0.0;
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+        const int j = ci[q];
+        if (!((j == i) || E[q])) continue;
+        const int J = agg[j];
+        if (J < 0) continue;
+        int t = 0;
+        while (t < cnt && tmp[t] != J) ++t;
+        if (t == cnt) continue;   // only after an overflow (the row is then rejected)
+        const double a = (j == i) ? di : v[q * nc + c];
+        s[t] = __dadd_rn(s[t], a);
+    }
+    for (int t = 0; t < cnt; ++t) {
+        const double delta = (tmp[t] == ai) ? 1.0 : 0.0;
+        pv[(o + t) * nc + c] = __dsub_rn(delta, __dmul_rn(w, s[t]));
     }
 }
 
@@ -307,8 +307,8 @@ __global__ void k_pfill(int n, int nc, const int32_t *__restrict__ rp, const int
                         const uint8_t *__restrict__ E, const int32_t *__restrict__ agg, const double *__restrict__ d, Omega om,
                         const int32_t *__restrict__ prp, int32_t *pci, double *pv, int *overflow)
 {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) pfill_row(i, nc, rp, ci, v, E, agg, d, om, prp, pci, pv, overflow);
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < (int64_t)n * nc) pfill_row((int)(t / nc), (int)(t % nc), nc, rp, ci, v, E, agg, d, om, prp, pci, pv, overflow);
 }
 
 // ------------------------------------------------------------------ transpose helpers
@@ -922,7 +922,7 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
         Lf.P.n = n; Lf.P.m = nagg; Lf.P.nc = nc;
         Lf.P.nnz = rowptr_from_counts(c, cnt, Lf.P.rp, n);
         Lf.P.ci.alloc(std::max<int64_t>(Lf.P.nnz, 1)); Lf.P.v.alloc(std::max<int64_t>(Lf.P.nnz, 1) * nc);
-        if (n) k_pfill<<<grid_for(n, 128), 128, 0, c.s>>>(n, nc, Lf.A.rp, Lf.A.ci, Lf.A.v, E, Lf.agg, d, om, Lf.P.rp, Lf.P.ci, Lf.P.v, err);
+        if (n) k_pfill<<<grid_for((int64_t)n * nc, 128), 128, 0, c.s>>>(n, nc, Lf.A.rp, Lf.A.ci, Lf.A.v, E, Lf.agg, d, om, Lf.P.rp, Lf.P.ci, Lf.P.v, err);
         c.launches += 3;
         TSP_REQUIRE(!d2h1(c, err.p), TSP_ERR_INVALID_ARG, "prolongator row exceeds 512 aggregates");
         dbg_mark(c, "agg+P", lvl);
