@@ -210,15 +210,12 @@ def main():
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    topo = {}
     if ws > 1:
         # z-slab decomposition (row e): this rank's owned block rows, NCCL over NVLink for halos/reductions.
         # The generator builds the global Jacobian (~26 GB of host memory at C5); ranks take turns so that only
         # one global copy exists at a time, and each keeps its slab only.
         import gc
         from paper_1812_05540_b200 import TSP_COMM_NCCL, nccl_unique_id
-        obj = [nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
         for turn in range(ws):
             if turn == rank:
                 pb = synth.generate(args.config)
@@ -233,13 +230,22 @@ def main():
                 pb = shape
             dist.barrier()
         src = lp
-        topo = dict(rank=rank, nranks=ws, comm_kind=TSP_COMM_NCCL, comm_arg=obj[0])
+
+        def new_topo():
+            # collective: a fresh NCCL unique id per communicator (an id's bootstrap root serves one
+            # ncclCommInitRank), broadcast from rank 0
+            obj = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            return dict(rank=rank, nranks=ws, comm_kind=TSP_COMM_NCCL, comm_arg=obj[0])
     else:
         pb = synth.generate(args.config)
         n_glob = pb.n
         src, b_host = pb, pb.b
+
+        def new_topo():
+            return {}
     n = src.n
-    g = Tsp(src, **topo, **lib_opts)
+    g = Tsp(src, **new_topo(), **lib_opts)
     b = torch.from_numpy(np.ascontiguousarray(b_host)).to(dev)
     x = torch.zeros(n, dtype=torch.float64, device=dev)
 
@@ -367,7 +373,7 @@ def main():
 
         def e2e_step():
             t0 = time.perf_counter()
-            h = Tsp(pp, **topo, **lib_opts)
+            h = Tsp(pp, **new_topo(), **lib_opts)
             torch.cuda.synchronize()
             t1 = time.perf_counter()
             h.setup()
