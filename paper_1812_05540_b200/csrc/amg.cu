@@ -564,7 +564,8 @@ static void spgemm_launch(Ctx &c, int ncv, int G, int HS, int fill, const Csr &X
     } while (0)
 #define SPG_NC(NCV)                                                                                                       \
     do {                                                                                                                  \
-        if (G == 8 && HS == 64) SPG(NCV, 8, 64);                                                                          \
+        if (G == 4 && HS == 64) SPG(NCV, 4, 64);                                                                          \
+        else if (G == 8 && HS == 64) SPG(NCV, 8, 64);                                                                     \
         else if (HS == 128) SPG(NCV, 32, 128);                                                                            \
         else if (HS == 512) SPG(NCV, 32, 512);                                                                            \
         else SPG(NCV, 32, 4096);                                                                                          \
@@ -582,12 +583,13 @@ static void spgemm(Ctx &c, const Csr &X, const Csr &Y, Csr &C, int nc)
     C.n = X.n; C.m = Y.m; C.nc = nc;
     DBuf<int32_t> cnt; cnt.alloc(X.n + 1);
     DBuf<int> ovf; ovf.alloc(1);
-    // Lanes per row from Y's mean row length (8 for the prolongators, whose rows are ~4 long; 32 otherwise);
+    // Lanes per row from Y's mean row length (8 for the prolongators, whose rows are ~4 long -- 4 for the
+    // scalar 7-point A P; 32 otherwise);
     // attempts grow the per-row hash table on overflow.  The symbolic pass (counts) touches no values and
     // runs the scalar kernel.  Measured at C5: 8 lanes beat 4 (4: the numeric pass's per-group tables
     // limit occupancy) and 32 (mechanics level-0 A P: 73.6 -> 36.2 ms for both passes).
-    const double ymean = Y.n ? (double)Y.nnz / Y.n : 0.0;
-    const int G0 = ymean <= 8.0 ? 8 : 32;
+    const double ymean = Y.n ? (double)Y.nnz / Y.n : 0.0, xmean = X.n ? (double)X.nnz / X.n : 0.0;
+    const int G0 = ymean > 8.0 ? 32 : (nc == 1 && xmean <= 8.0 && ymean <= 4.0) ? 4 : 8;   // 4: 7-point A P
     for (int attempt = 0; attempt < 3; ++attempt) {
         const int Gs = attempt == 0 ? G0 : 32;
         const int HSs = attempt == 0 ? (G0 < 32 ? 64 : 128) : attempt == 1 ? 512 : 4096;
