@@ -75,6 +75,8 @@ def lib():
         L.orc_amg_level_sizes.argtypes = [C.c_void_p, C.c_int, _P(C.c_int64)]
         L.orc_amg_level_export.argtypes = [C.c_void_p, C.c_int, _I32, _I32, _F64, _I32, _I32, _I32, _F64, _F64]
         L.orc_amg_free.argtypes = [C.c_void_p]
+        L.orc_amg_level_detail.argtypes = [C.c_void_p, C.c_int, _I32, _I32, _F64]
+        L.orc_strength.argtypes = [C.c_int, C.c_int, _I32, _I32, _F64, _I32, C.c_double, _P(C.c_uint8)]
         L.orc_ilu_build.argtypes = [C.c_int] * 6 + [_I32, _I32, _F64]
         L.orc_ilu_build.restype = C.c_void_p
         L.orc_ilu_apply.argtypes = [C.c_void_p, _F64, _F64]
@@ -222,6 +224,19 @@ def mis2(rp, ci, hashes, rounds=False):
     return st, nr.value
 
 
+def strength(rp, ci, v, zb, theta=0.25):
+    """Symmetrised strength flags (one per stored entry) of R-strength."""
+    n = len(rp) - 1
+    v = np.ascontiguousarray(v, np.float64)
+    nc = 1 if v.ndim == 1 else v.shape[1]
+    E = np.zeros(int(rp[-1]), np.uint8)
+    rc = lib().orc_strength(n, nc, _p(np.ascontiguousarray(rp, np.int32)), _p(np.ascontiguousarray(ci, np.int32)), _p(v),
+                            _p(np.ascontiguousarray(zb, np.int32)), theta, E.ctypes.data_as(_P(C.c_uint8)))
+    if rc != 0:
+        raise ValueError("pattern not structurally symmetric")
+    return E.astype(bool)
+
+
 def fmix32(x):
     x = np.asarray(x, np.uint64) & 0xFFFFFFFF
     x ^= x >> 16
@@ -256,6 +271,14 @@ class Amg:
         x = np.zeros_like(b)
         lib().orc_amg_vcycle(self.h, _p(b), _p(x))
         return x
+
+    def detail(self, lvl):
+        """(MIS(2) state, phase-1 aggregate ids, omega per component) of a non-coarsest level."""
+        n = self.levels()[lvl]["n"]
+        st, ph1, om = np.empty(n, np.int32), np.empty(n, np.int32), np.empty(self.nc)
+        if lib().orc_amg_level_detail(self.h, lvl, _p(st), _p(ph1), _p(om)) != 0:
+            raise ValueError(f"level {lvl} is the coarsest")
+        return st, ph1, om
 
     def levels(self):
         L = lib()

@@ -119,6 +119,7 @@ typedef struct {
     mcsr A; int32_t *zb; double *dl1[3];
     int coarsest;
     int nagg; int32_t *agg;       /* aggregate id per row, -1 = not aggregated */
+    int32_t *st, *ph1;            /* MIS(2) state and phase-1 aggregate per row (kept for the pins) */
     mcsr P, R;
     double *lu[3]; int *piv[3];
     double omega[3];
@@ -277,7 +278,7 @@ int orc_mis2(int n, const int32_t *rp, const int32_t *ci, const uint32_t *hash, 
  * its strong neighbours; phase 2 = each remaining non-isolated node joins the
  * phase-1 aggregate of its strong neighbour of maximal measure, ties to the
  * smallest aggregate id. */
-static int aggregate(const mcsr *A, const uint8_t *E, const int32_t *st, int32_t *agg)
+static int aggregate(const mcsr *A, const uint8_t *E, const int32_t *st, int32_t *agg, int32_t *ph1_out)
 {
     int n = A->n, nagg = 0;
     int32_t *rid = (int32_t *)xmalloc(sizeof(int32_t) * (n + 1));
@@ -301,6 +302,7 @@ static int aggregate(const mcsr *A, const uint8_t *E, const int32_t *st, int32_t
         }
         agg[v] = best;
     }
+    if (ph1_out) memcpy(ph1_out, ph1, sizeof(int32_t) * n);
     free(rid); free(ph1);
     return nagg;
 }
@@ -505,12 +507,14 @@ static ohier *amg_build(const mcsr *A0, const int32_t *zb0, const orc_opts *o)
         int32_t *st = (int32_t *)xmalloc(sizeof(int32_t) * (n + 1));
         mis2_greedy(n, grp, gci, hs, st);
         L->agg = (int32_t *)xmalloc(sizeof(int32_t) * (n + 1));
-        L->nagg = aggregate(&L->A, E, st, L->agg);
+        L->ph1 = (int32_t *)xmalloc(sizeof(int32_t) * (n + 1));
+        L->nagg = aggregate(&L->A, E, st, L->agg, L->ph1);
         if (L->nagg == 0 || (double)L->nagg > 0.8 * (double)n) {
             /* coarsening stagnation: direct solve at this level */
             H->fallbacks++;
             free(E); free(grp); free(gci); free(hs); free(st);
             free(L->agg); L->agg = NULL; L->nagg = 0;
+            free(L->ph1); L->ph1 = NULL;
             if (make_coarsest(H, L)) goto fail;
             break;
         }
@@ -522,7 +526,8 @@ static ohier *amg_build(const mcsr *A0, const int32_t *zb0, const orc_opts *o)
         mcsr_free(&AP);
         Lc->zb = (int32_t *)xmalloc(sizeof(int32_t) * (L->nagg + 1));
         for (int i = 0; i < n; ++i) if (st[i] == ST_ROOT) Lc->zb[L->agg[i]] = L->zb[i];
-        free(E); free(grp); free(gci); free(hs); free(st);
+        L->st = st;
+        free(E); free(grp); free(gci); free(hs);
         ++lvl;
     }
     H->nl = lvl + 1;
@@ -538,7 +543,7 @@ static void amg_free(ohier *H)
     for (int l = 0; l < 16; ++l) {
         olevel *L = &H->L[l];
         mcsr_free(&L->A); mcsr_free(&L->P); mcsr_free(&L->R);
-        free(L->zb); free(L->agg);
+        free(L->zb); free(L->agg); free(L->st); free(L->ph1);
         for (int c = 0; c < 3; ++c) { free(L->dl1[c]); free(L->lu[c]); free(L->piv[c]); }
     }
     free(H);
@@ -1285,3 +1290,25 @@ void orc_amg_level_export(void *hier, int lvl, int32_t *A_rp, int32_t *A_ci, dou
                           int32_t *agg, int32_t *P_rp, int32_t *P_ci, double *P_v, double *dl1)
 { level_export((ohier *)hier, lvl, A_rp, A_ci, A_v, agg, P_rp, P_ci, P_v, dl1); }
 void orc_amg_free(void *hier) { amg_free((ohier *)hier); }
+/* pins: the MIS(2) state, the phase-1 aggregates and omega_c of a non-coarsest level (returns -1 otherwise) */
+int orc_amg_level_detail(void *hier, int lvl, int32_t *st, int32_t *ph1, double *omega)
+{
+    ohier *H = (ohier *)hier;
+    olevel *L = &H->L[lvl];
+    if (lvl >= H->nl || L->coarsest || !L->st) return -1;
+    if (st) memcpy(st, L->st, sizeof(int32_t) * L->A.n);
+    if (ph1) memcpy(ph1, L->ph1, sizeof(int32_t) * L->A.n);
+    if (omega) for (int c = 0; c < H->nc; ++c) omega[c] = L->omega[c];
+    return 0;
+}
+/* pins: the symmetrised strength graph E (one byte per stored entry) of R-strength */
+int orc_strength(int n, int nc, const int32_t *rp, const int32_t *ci, const double *v, const int32_t *zb,
+                 double theta, uint8_t *E)
+{
+    mcsr A; mcsr_alloc(&A, n, n, nc, rp[n]);
+    memcpy(A.rp, rp, sizeof(int32_t) * (n + 1)); memcpy(A.ci, ci, sizeof(int32_t) * rp[n]);
+    for (int64_t q = 0; q < rp[n]; ++q) for (int c = 0; c < nc; ++c) A.v[c][q] = v[q * nc + c];
+    int rc = strength(&A, zb, theta, E);
+    mcsr_free(&A);
+    return rc;
+}

@@ -79,6 +79,9 @@ void orc_amg_level_sizes(void *hier, int lvl, int64_t out[6]);
 void orc_amg_level_export(void *hier, int lvl, int32_t *A_rp, int32_t *A_ci, double *A_v,
                           int32_t *agg, int32_t *P_rp, int32_t *P_ci, double *P_v, double *dl1);
 void orc_amg_free(void *hier);
+int orc_amg_level_detail(void *hier, int lvl, int32_t *st, int32_t *ph1, double *omega);
+int orc_strength(int n, int nc, const int32_t *rp, const int32_t *ci, const double *v, const int32_t *zb,
+                 double theta, uint8_t *E);
 void *orc_ilu_build(int nx, int ny, int nz, int tx, int ty, int tz, const int32_t *rp, const int32_t *ci,
                     const double *v);
 void orc_ilu_apply(void *ilu, const double *w, double *dz);
