@@ -111,6 +111,23 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(use), "window": "timed region" if inside else "whole run"}
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def domain_m(nx, ny, nz):
+    """Physical extent of the generated domain (DESIGN.md R-geom: BASELINE.json's unit cube is the normalised
+    domain of side synth.DEFAULTS['length'] = 10 km; cubic cells, h = length / nx)."""
+    L = synth.DEFAULTS["length"]
+    return [L, L * ny / nx, L * nz / nx]
+
+
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -149,11 +166,16 @@ def oracle_sample(config, gpu_iters, sample_iters=3, reps=1, opts=None):
             + (f", 1/{scale:.0f} of the DoF, times scaled x{scale:.2f}" if scale > 1.001 else "") + f"): full setup "
             f"{t_setup:.2f}s + {its} FGMRES iterations at {t_iter:.3f}s; step = setup + {gpu_iters} iterations")
     return dict(value=gpu_iters / step, unit="iter/s", cores=1, kind="oracle", t_setup_s=t_setup * scale,
-                t_iter_s=t_iter * scale, step_s=step, sample=what)
+                t_iter_s=t_iter * scale, step_s=step, sample=what, cpu_model=cpu_model(), host_nproc=os.cpu_count(),
+                measured={"grid": [pb.nx, pb.ny, pb.nz], "dof": pb.n, "setup_s": t_setup, "iterations": its,
+                          "s_per_iteration": t_iter, "dof_scale_to_workload": scale},
+                scaled="linear in DoF to the workload (the oracle's setup and iteration are O(n))" if scale > 1.001
+                else "none: the sample is the workload")
 
 
-# FGMRES(64) iterations to 1e-8 measured on the CUDA path (tests/test_gpu_parity.py keeps
-# the oracle within +-1 of them); used to scale the reference arm's bounded sample.
+# FGMRES(64) iterations to 1e-8 measured on the CUDA path; used to scale the reference arm's bounded sample.
+# tests/test_gpu_parity.py::test_full_parity_large holds the oracle within +-1 of the GPU on C3, C4 and ST1
+# (C1, C2 in test_solve_parity); C5, S10 and ST3 are not solved by the oracle in the tests.
 GPU_ITERS = {"C1": 41, "C2": 61, "C3": 217, "C4": 109, "C5": 256, "S10": 190, "ST3": 315}   # measured FGMRES counts (parity: the oracle's +-1)
 ALL_CONFIGS = {**synth.CONFIGS, **synth.WORKLOADS}
 
@@ -170,8 +192,10 @@ def run_reference(args, ws, rank):
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": cpu["step_s"] * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "grid": [g["nx"], g["ny"], g["nz"]],
-                       "dof": synth.sizes(g["nx"], g["ny"], g["nz"])["n"]},
-            "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": "oracle", "sample": cpu["sample"]},
+                       "dof": synth.sizes(g["nx"], g["ny"], g["nz"])["n"], "domain_m": domain_m(g["nx"], g["ny"], g["nz"])},
+            "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": "oracle", "sample": cpu["sample"],
+                             "cpu_model": cpu["cpu_model"], "host_nproc": cpu["host_nproc"], "measured": cpu["measured"],
+                             "scaled": cpu["scaled"]},
             "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -259,8 +283,10 @@ def main():
         return g.solve(b, x, rtol=1e-8, restart=64, max_iters=1000)
 
     # warm-up; the last warm-up step records every kernel class (the per-class table and the choice of
-    # the dominant class); the timed steps then record only the dominant class, whose live CUDA-event
-    # times give the roofline (two events per recorded launch; recording all classes costs ~2 %)
+    # the dominant class).  The timed steps run with profiling OFF, i.e. exactly the user's path (the FGMRES
+    # iteration body replayed from CUDA graphs; per-launch timing events would force it eager).  The
+    # dominant class's per-launch time is then measured live, with CUDA events on the launching stream, in
+    # one extra profiled step right after the timed region (same kernels, same inputs).
     clocks = Clocks(local)
     for w in range(max(args.warmup, 0)):
         if w == args.warmup - 1:
@@ -274,14 +300,12 @@ def main():
 
     if clocks.p is None:
         clocks.start()
-    g.prof_enable(True)
-    if dom_name:
-        g.prof_classes([dom_name])
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stream = torch.cuda.current_stream()
+    launches0 = g.stats()["launches"]
     clocks.begin()
     e0.record(stream)
     iters, infos = 0, []
@@ -297,8 +321,15 @@ def main():
     ms = e0.elapsed_time(e1)
     clocks.end()
     clk = clocks.stop()
-    prof = g.prof_read()
     st = g.stats()
+    launches_timed = st["launches"] - launches0
+    # roofline step: the dominant class only, events around each of its launches
+    g.prof_enable(True)
+    if dom_name:
+        g.prof_classes([dom_name])
+    step()
+    torch.cuda.synchronize()
+    prof = g.prof_read()
     g.prof_enable(False)
     g.prof_classes(None)
 
@@ -417,6 +448,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "grid": [pb.nx, pb.ny, pb.nz], "dof": n_glob,
+                       "domain_m": domain_m(pb.nx, pb.ny, pb.nz),
                        **({"options": lib_opts} if lib_opts else {}),
                        "step": "tsp_setup(MECH|FLOW) + FGMRES(64) to rtol 1e-8",
                        "parallelism": "single GPU" if ws == 1 else f"z-slab decomposition over {ws} GPUs (NCCL)",
@@ -433,9 +465,12 @@ def main():
             "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": ncu_traffic(dname)[0], "ncu_dram_pct": ncu_traffic(dname)[1],
                          "peak_source": peak_src,
+                         "measured": "CUDA events around every launch of this class on the launching stream, in one "
+                                     "profiled step right after the timed region (the timed steps run unprofiled)",
+                         "share_of_step": prof_all.get(dname, {}).get("ms", 0.0) / max(sum(p["ms"] for p in prof_all.values()), 1e-12),
                          "bytes_per_launch": d["bytes"] / d["launches"], "ms_per_launch": d["ms"] / d["launches"]},
             "kernels": kernel_table,
-            "gpu_launches": int(st["launches"]),
+            "gpu_launches": int(launches_timed),
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,

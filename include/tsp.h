@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define TSP_ABI_VERSION 2
+#define TSP_ABI_VERSION 3
 
 typedef int tsp_status;
 enum {
@@ -99,6 +99,20 @@ typedef struct {
  * per fixed chunk in global order).  Requires 1 <= P <= nzb. */
 enum { TSP_COMM_NONE = 0, TSP_COMM_NCCL = 1, TSP_COMM_LOCAL = 2 };
 
+/* Device-memory callbacks (BASELINE.json north_star: "PyTorch only for device memory").
+ * When `alloc` is non-NULL EVERY device buffer of the handle (matrices, hierarchies, Krylov basis, work
+ * vectors, CUB scratch) is obtained from alloc(bytes, stream, ctx) and returned through
+ * free(ptr, bytes, stream, ctx), both on the handle's stream (stream-ordered: a block freed on the stream
+ * may be reused by later work on the same stream).  alloc returns a device pointer on the handle's device,
+ * aligned to 256 bytes, or NULL when out of memory (the call then fails with TSP_ERR_OOM).  The callbacks
+ * are called only from inside this library's API calls on the calling host thread (tsp_destroy included),
+ * and must stay valid until tsp_destroy returns.  alloc = NULL: the library's own stream-ordered pool. */
+typedef struct {
+    void *(*alloc)(size_t bytes, void *stream, void *ctx);
+    void (*free)(void *ptr, size_t bytes, void *stream, void *ctx);
+    void *ctx;
+} tsp_allocator;
+
 typedef struct {
     int nx, ny, nz;              /* GLOBAL grid in cells: N_n = (nx+1)(ny+1)(nz+1), N_c = nx ny nz */
     int rank, nranks;            /* this rank and the number of ranks (one per GPU) */
@@ -114,6 +128,7 @@ typedef struct {
     tsp_bsr A_ff;                /* 2x2 [[A_ss, A_sp],[A_ps, A_pp]], N_c x N_c */
     const double *fs_diag;       /* 2*N_c: (D_sp, D_pp) per cell, eq:FS_Dps_Dpp P:435-436, row-scaled */
     tsp_options opts;
+    tsp_allocator allocator;     /* device memory callbacks; zero-initialised = the library's pool */
 } tsp_desc;
 
 enum { TSP_SETUP_MECH = 1, TSP_SETUP_FLOW = 2 };
@@ -135,6 +150,8 @@ typedef struct {
     double t_solve_s;
     int reorth;                  /* basis vectors re-orthogonalised (DCGS2: every one, one step late) */
     double bytes_krylov;         /* algorithmic bytes of the Gram-Schmidt / normalisation / x-update kernels */
+    int dcgs_fallbacks;          /* iterations whose Pythagorean DCGS2 norm lost > 6 digits to cancellation and took
+                                    the explicit two-pass Gram-Schmidt instead (env TSP_DCGS2_FALLBACK: all of them) */
 } tsp_solve_info;
 
 typedef struct {
@@ -146,6 +163,9 @@ typedef struct {
     double bytes_operator;       /* algorithmic bytes of one tsp_apply_operator */
     double bytes_iter_base;      /* per FGMRES iteration excluding Gram-Schmidt: apply + operator */
     double bytes_per_krylov_vec; /* bytes of one basis-vector pass (8 n); exact Krylov bytes: tsp_solve_info */
+    int64_t allocs_callback;     /* device allocations made through tsp_desc.allocator since tsp_create */
+    int64_t allocs_pool;         /* device allocations made from the library's own pool since tsp_create */
+    int64_t bytes_live;          /* device bytes the handle holds right now */
 } tsp_stats;
 
 /* per-kernel-class timing (CUDA events on the handle's stream), for roofline */
@@ -222,6 +242,22 @@ tsp_status tsp_prof_classes(tsp_handle h, unsigned mask);
 /* Test hook (after TSP_SETUP_FLOW): this rank's D_ss^(CPR), D_ps^(CPR) (N_c,local each) and the fixed-stress
  * diagonal actually used by a1, (D_sp, D_pp) per cell (2 N_c,local); host buffers, any may be NULL. */
 tsp_status tsp_export_cpr(tsp_handle h, double *dss, double *dps, double *fs_eff);
+
+/* Test hook (parity coverage): how often each kernel variant was chosen by the setups of this handle.
+ * out[TSP_NVARIANTS], indexed by TSP_VAR_*: the Galerkin product's per-row hash table (64 / 128 / 512 / 4096
+ * slots; 512 and 4096 are the overflow retries) and lanes per row (4 / 8 / 32), both counted per launch; the
+ * vector-CSR lanes per row of each coarse level's smoother A (0 = sliced-ELL / 8 / 16 / 32) and of each
+ * level's restriction R, counted per level.  Test knobs (environment, read by every setup):
+ * TSP_SPGEMM_MIN_SLOTS=512|4096 starts the products at the overflow tables (bitwise the same hierarchy);
+ * TSP_FORCE_LANES=0|8|16|32 forces one vector-CSR variant on every level. */
+enum {
+    TSP_VAR_SPGEMM_HS64 = 0, TSP_VAR_SPGEMM_HS128, TSP_VAR_SPGEMM_HS512, TSP_VAR_SPGEMM_HS4096,
+    TSP_VAR_SPGEMM_G4, TSP_VAR_SPGEMM_G8, TSP_VAR_SPGEMM_G32,
+    TSP_VAR_LANES_A0, TSP_VAR_LANES_A8, TSP_VAR_LANES_A16, TSP_VAR_LANES_A32,
+    TSP_VAR_LANES_R0, TSP_VAR_LANES_R8, TSP_VAR_LANES_R16, TSP_VAR_LANES_R32,
+    TSP_NVARIANTS
+};
+tsp_status tsp_variant_counts(tsp_handle h, int64_t out[TSP_NVARIANTS]);
 
 void tsp_destroy(tsp_handle h);
 

@@ -28,6 +28,14 @@ static int lanes_for(int64_t nnz, int64_t rows)
     if (rows <= 0 || nnz < 12 * rows) return 0;
     return nnz < 40 * rows ? 8 : nnz < 96 * rows ? 16 : 32;
 }
+// test knob TSP_FORCE_LANES=0|8|16|32: every level uses that vector-CSR variant (parity coverage of each
+// lanes_for choice on small grids; the setup products are unaffected, apply sums change order only)
+static int lanes_forced(int lanes)
+{
+    const char *e = getenv("TSP_FORCE_LANES");
+    return e ? atoi(e) : lanes;
+}
+static int lanes_idx(int lanes) { return lanes == 0 ? 0 : lanes == 8 ? 1 : lanes == 16 ? 2 : 3; }
 
 
 __device__ __forceinline__ uint32_t fmix32(uint32_t x)
@@ -576,6 +584,8 @@ static void spgemm_launch(Ctx &c, int ncv, int G, int HS, int fill, const Csr &X
 #undef SPG
     TSP_CUDA(cudaGetLastError());
     c.launches++;
+    c.variants[TSP_VAR_SPGEMM_HS64 + (HS == 64 ? 0 : HS == 128 ? 1 : HS == 512 ? 2 : 3)]++;
+    c.variants[TSP_VAR_SPGEMM_G4 + (G == 4 ? 0 : G == 8 ? 1 : 2)]++;
 }
 
 static void spgemm(Ctx &c, const Csr &X, const Csr &Y, Csr &C, int nc)
@@ -586,11 +596,16 @@ static void spgemm(Ctx &c, const Csr &X, const Csr &Y, Csr &C, int nc)
     // Lanes per row from Y's mean row length (8 for the prolongators, whose rows are ~4 long -- 4 for the
     // scalar 7-point A P; 32 otherwise);
     // attempts grow the per-row hash table on overflow.  The symbolic pass (counts) touches no values and
-    // runs the scalar kernel.  Measured at C5: 8 lanes beat 4 (4: the numeric pass's per-group tables
-    // limit occupancy) and 32 (mechanics level-0 A P: 73.6 -> 36.2 ms for both passes).
+    // runs the scalar kernel.  Measured at C5: 8 lanes beat 32 for the prolongator products (mechanics level-0
+    // A P: 73.6 -> 36.2 ms for both passes); for the scalar 7-point A P 4 lanes beat 8 (pressure level 0:
+    // 10.8 -> 9.7 ms).
     const double ymean = Y.n ? (double)Y.nnz / Y.n : 0.0, xmean = X.n ? (double)X.nnz / X.n : 0.0;
     const int G0 = ymean > 8.0 ? 32 : (nc == 1 && xmean <= 8.0 && ymean <= 4.0) ? 4 : 8;   // 4: 7-point A P
-    for (int attempt = 0; attempt < 3; ++attempt) {
+    // test knob TSP_SPGEMM_MIN_SLOTS=512|4096: start at the overflow tables (bitwise the same products; lets
+    // the parity tests cover the paths the full-size configs take)
+    const char *ms = getenv("TSP_SPGEMM_MIN_SLOTS");
+    const int first = !ms ? 0 : atoi(ms) >= 4096 ? 2 : atoi(ms) >= 512 ? 1 : 0;
+    for (int attempt = first; attempt < 3; ++attempt) {
         const int Gs = attempt == 0 ? G0 : 32;
         const int HSs = attempt == 0 ? (G0 < 32 ? 64 : 128) : attempt == 1 ? 512 : 4096;
         const int Gf = Gs, HSf = HSs;
@@ -975,6 +990,10 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
             int64_t mx = 1;
             for (auto v : Lf.rep_counts) mx = std::max(mx, v);
             Lf.rep_buf.alloc((size_t)mx * nc * (c.nranks + 1));
+            Lf.rep_offs_d.alloc(c.nranks + 1);           // uploaded once, read by every V-cycle's gather
+            TSP_CUDA(cudaMemcpyAsync(Lf.rep_offs_d, Lf.rep_offs.data(), sizeof(int64_t) * (c.nranks + 1),
+                                     cudaMemcpyHostToDevice, c.s));
+            TSP_CUDA(cudaStreamSynchronize(c.s));
             Lf.P.m = (int)nagg_glob;
             if (Lf.P.nnz) TSP_CUDA(cudaMemcpyAsync(Lf.P.ci, Pg.ci, 4 * Lf.P.nnz, cudaMemcpyDeviceToDevice, c.s));
         } else {
@@ -998,8 +1017,10 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
                 st.assign(4, 0);
                 for (int r = 0; r < c.nranks; ++r) for (int k = 0; k < 4; ++k) st[k] += all[4 * r + k];
             }
-            L.warpA = l > 0 ? lanes_for(st[0], st[1]) : 0;
-            L.warpR = lanes_for(st[2], st[3]);
+            L.warpA = l > 0 ? lanes_forced(lanes_for(st[0], st[1])) : 0;
+            L.warpR = lanes_forced(lanes_for(st[2], st[3]));
+            if (l > 0 && !L.coarsest) c.variants[TSP_VAR_LANES_A0 + lanes_idx(L.warpA)]++;
+            if (!L.coarsest) c.variants[TSP_VAR_LANES_R0 + lanes_idx(L.warpR)]++;
         }
         if (L.dist) {
             const size_t g = (size_t)std::max(L.hp->nghost(), 1) * nc;
@@ -1224,9 +1245,7 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
         for (auto v : L.rep_counts) mx = std::max(mx, v);
         double *recv = L.rep_buf.p + (size_t)mx * NC;
         c.comm->allgather(L.rep_buf.p, recv, sizeof(double) * mx * NC, c.s);
-        DBuf<int64_t> offs; offs.alloc(c.nranks + 1);
-        TSP_CUDA(cudaMemcpyAsync(offs, L.rep_offs.data(), sizeof(int64_t) * (c.nranks + 1), cudaMemcpyHostToDevice, c.s));
-        k_rep_compact<<<dim3(grid_for(mx * NC, 256), c.nranks), 256, 0, c.s>>>(c.nranks, NC, mx, offs, recv, Lc.b);
+        k_rep_compact<<<dim3(grid_for(mx * NC, 256), c.nranks), 256, 0, c.s>>>(c.nranks, NC, mx, L.rep_offs_d, recv, Lc.b);
         c.launches++;
     }
     vcycle_rec<NC>(c, H, l + 1, Lc.b, Lc.x);

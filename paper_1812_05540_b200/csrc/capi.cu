@@ -13,6 +13,7 @@ namespace tsp {
 
 static thread_local std::string g_err;
 thread_local cudaStream_t g_alloc_stream = 0;
+thread_local AllocState *g_alloc_state = nullptr;
 void set_error(const std::string &m) { g_err = m; }
 static bool dbg_on() { static const bool on = getenv("TSP_DEBUG") != nullptr; return on; }
 double dbg_now()
@@ -32,8 +33,16 @@ std::mutex g_cache_mu;
 std::map<cudaStream_t, Cache> g_cache;
 constexpr size_t kCacheMax = size_t(48) << 30;
 }  // namespace
-void *dev_alloc(size_t bytes, cudaStream_t s)
+void *dev_alloc(size_t bytes, cudaStream_t s, AllocState *as)
 {
+    if (as && as->al.alloc) {                      // the caller's allocator (tsp_desc.allocator)
+        void *p = as->al.alloc(bytes, (void *)s, as->al.ctx);
+        TSP_REQUIRE(p != nullptr, TSP_ERR_OOM, "tsp_desc.allocator returned NULL");
+        as->n_cb++;
+        as->bytes_live += (int64_t)bytes;
+        return p;
+    }
+    if (as) { as->n_pool++; as->bytes_live += (int64_t)bytes; }
     {
         std::lock_guard<std::mutex> lk(g_cache_mu);
         auto &C = g_cache[s];
@@ -59,8 +68,10 @@ void *dev_alloc(size_t bytes, cudaStream_t s)
     dbg_alloc(t0, bytes);
     return p;
 }
-void dev_free(void *p, size_t bytes, cudaStream_t s)
+void dev_free(void *p, size_t bytes, cudaStream_t s, AllocState *as)
 {
+    if (as) as->bytes_live -= (int64_t)bytes;
+    if (as && as->al.alloc) { as->al.free(p, bytes, (void *)s, as->al.ctx); return; }
     std::lock_guard<std::mutex> lk(g_cache_mu);
     auto &C = g_cache[s];
     C.free.emplace(bytes, p);
@@ -94,8 +105,10 @@ void dbg_alloc(double t0, size_t bytes)
 
 // bind the allocation stream of this API call; keep the default pool resident
 struct StreamScope {
-    explicit StreamScope(cudaStream_t s) {
+    ~StreamScope() { g_alloc_state = nullptr; }
+    explicit StreamScope(cudaStream_t s, AllocState *as = nullptr) {
         g_alloc_stream = s;
+        g_alloc_state = as;
         // per call (idempotent, thread-safe, ~1 us): the pool belongs to the current device
         int dev = 0;
         cudaMemPool_t pool;
@@ -157,18 +170,36 @@ using namespace tsp;
 
 struct tsp_ctx : Ctx {};
 
-#define API_BEGIN try { StreamScope ss_(h ? h->s : (cudaStream_t)0);
+#define API_BEGIN try { StreamScope ss_(h ? h->s : (cudaStream_t)0, h ? &h->alloc : nullptr);
 #define API_END                                                                                     \
     }                                                                                               \
     catch (const tsp::Error &e) {                                                                   \
         set_error(e.msg);                                                                           \
         return e.st;                                                                                \
     }                                                                                               \
+    catch (const std::bad_alloc &) {                                                                \
+        set_error("host allocation failed");                                                        \
+        return TSP_ERR_OOM;                                                                         \
+    }                                                                                               \
     catch (const std::exception &e) {                                                               \
         set_error(e.what());                                                                        \
         return TSP_ERR_CUDA;                                                                        \
     }                                                                                               \
+    catch (...) {                                                                                   \
+        set_error("unknown exception");                                                             \
+        return TSP_ERR_CUDA;                                                                        \
+    }                                                                                               \
     return TSP_OK;
+
+// status of the exception in flight (inside a catch block): every exception is mapped, none escapes extern "C"
+static tsp_status status_of_current_exception()
+{
+    try { throw; }
+    catch (const tsp::Error &e) { set_error(e.msg); return e.st; }
+    catch (const std::bad_alloc &) { set_error("host allocation failed"); return TSP_ERR_OOM; }
+    catch (const std::exception &e) { set_error(e.what()); return TSP_ERR_CUDA; }
+    catch (...) { set_error("unknown exception"); return TSP_ERR_CUDA; }
+}
 
 extern "C" {
 
@@ -207,7 +238,9 @@ tsp_status tsp_create(tsp_handle *out, const tsp_desc *d)
     TSP_REQUIRE(d->fs_diag, TSP_ERR_INVALID_ARG, "null fs_diag");
     c = new tsp_ctx();
     c->s = (cudaStream_t)d->stream;
-    StreamScope ss2_(c->s);
+    TSP_REQUIRE(!d->allocator.alloc == !d->allocator.free, TSP_ERR_INVALID_ARG, "allocator: alloc and free go together");
+    c->alloc.al = d->allocator;
+    StreamScope ss2_(c->s, &c->alloc);
     c->o = d->opts;
     if (c->o.amg_theta <= 0 || c->o.amg_coarse_max <= 0) { int rr = c->o.replicate_rows; tsp_default_options(&c->o); c->o.replicate_rows = rr; }
     if (c->o.zblock <= 0) c->o.zblock = 16;
@@ -287,11 +320,11 @@ tsp_status tsp_create(tsp_handle *out, const tsp_desc *d)
     *out = c;
     return TSP_OK;
     }
-    catch (const tsp::Error &e) {
-        set_error(e.msg);
+    catch (...) {
+        const tsp_status st = status_of_current_exception();
         (void)h;
         if (c) { Comm *cm = c->comm; delete c; delete cm; }
-        return e.st;
+        return st;
     }
 }
 
@@ -350,12 +383,18 @@ tsp_status tsp_solve(tsp_handle h, const double *b, double *x, const tsp_solve_o
     if (info) *info = inf;
     return inf.status;
     }
-    catch (const tsp::Error &e) {
-        set_error(e.msg);
-        inf.status = e.st;
+    catch (...) {
+        inf.status = status_of_current_exception();
         if (info) *info = inf;
-        return e.st;
+        return inf.status;
     }
+}
+
+tsp_status tsp_variant_counts(tsp_handle h, int64_t out[TSP_NVARIANTS])
+{
+    if (!h || !out) { set_error("null argument"); return TSP_ERR_INVALID_ARG; }
+    for (int k = 0; k < TSP_NVARIANTS; ++k) out[k] = h->variants[k];
+    return TSP_OK;
 }
 
 tsp_status tsp_get_stats(tsp_handle h, tsp_stats *s)
@@ -379,6 +418,9 @@ tsp_status tsp_get_stats(tsp_handle h, tsp_stats *s)
         s->perturbed_pivots = h->perturbed + h->mech.perturbed + h->pres.perturbed;
         s->coarsening_fallbacks = h->mech.fallbacks + h->pres.fallbacks;
     }
+    s->allocs_callback = h->alloc.n_cb;
+    s->allocs_pool = h->alloc.n_pool;
+    s->bytes_live = h->alloc.bytes_live;
     auto sb = [](const Sell &S) { return (double)S.slots * 32 * (4.0 + 8.0 * S.bs); };
     const double Nn = h->Nn, Nc = h->Nc, n = (double)h->n;
     apply_bytes += sb(h->s_fu) + 24 * Nn + 32 * Nc;            // step 2
@@ -496,7 +538,7 @@ tsp_status tsp_prof_read(tsp_handle h, tsp_prof *out)
 void tsp_destroy(tsp_handle h)
 {
     if (!h) return;
-    StreamScope ss_(h->s);
+    StreamScope ss_(h->s, &h->alloc);
     cudaStreamSynchronize(h->s);
     for (auto &e : h->prof.pool) cudaEventDestroy(e);
     krylov_graphs_drop(*h);

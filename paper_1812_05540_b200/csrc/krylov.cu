@@ -161,16 +161,34 @@ __global__ void __launch_bounds__(KB) k_mdot2(int nv, const double *__restrict__
 // DCGS2 scalars from the pass-1 dots d = [V_{j-1} u ; u.u | V_{j-1} w ; u.w] (2(j+1) values):
 // s = d[0..j), gamma = d[j], a = d[j+1..2j+1), b = d[2j+1];
 // alpha = sqrt(gamma - s.s) (norm of the re-orthogonalised u), h_j = (b - s.a) / alpha (= v_j . w).
-// sc[0] = alpha, sc[1] = h_j; alpha <= 0 (u numerically inside span V) is reported as NaN.
-__global__ void k_dcgs_coef(int j, const double *__restrict__ d, double *__restrict__ sc)
+// sc[0] = alpha, sc[1] = h_j.  When the Pythagorean difference loses more than 6 digits to cancellation
+// (gamma - s.s <= 1e-6 gamma: u nearly inside span V) or is not finite, sc[0] = 0 flags the iteration for
+// the explicit two-pass fallback on the host (k_dcgs_update then leaves u and w untouched).
+constexpr double kPythagorasMin = 1e-6;
+__global__ void k_dcgs_coef(int j, const double *__restrict__ d, double *__restrict__ sc, int force_fallback)
 {
     if (threadIdx.x) return;
     double ss = 0.0, sa = 0.0;
     for (int t = 0; t < j; ++t) { ss = fma(d[t], d[t], ss); sa = fma(d[t], d[j + 1 + t], sa); }
     const double a2 = d[j] - ss;
-    const double alpha = a2 > 0.0 ? sqrt(a2) : nan("");
+    if (force_fallback || !(a2 > kPythagorasMin * d[j]) || !isfinite(a2)) { sc[0] = 0.0; sc[1] = 0.0; return; }
+    const double alpha = sqrt(a2);
     sc[0] = alpha;
     sc[1] = (d[2 * j + 1] - sa) / alpha;
+}
+
+// w -= sum_t h[t] V_t (t < nv): the explicit Gram-Schmidt subtraction of the fallback
+__global__ void __launch_bounds__(KB) k_gs_sub(int nv, const double *__restrict__ V, int64_t ldv, const double *__restrict__ h,
+                                               double *__restrict__ w, int64_t n)
+{
+    __shared__ double hs[128];
+    for (int t = threadIdx.x; t < nv; t += KB) hs[t] = h[t];
+    __syncthreads();
+    for (int64_t r = blockIdx.x * (int64_t)KB + threadIdx.x; r < n; r += (int64_t)gridDim.x * KB) {
+        double acc = 0.0;
+        for (int t = 0; t < nv; ++t) acc = fma(hs[t], __ldcs(V + t * ldv + r), acc);
+        w[r] -= acc;
+    }
 }
 
 // DCGS2 pass 2 (fused): v_j = (u - V_{j-1} s) / alpha (in place of u); w <- w - V_{j-1} a - h_j v_j;
@@ -185,8 +203,12 @@ __global__ void __launch_bounds__(KB) k_dcgs_update(int j, const double *__restr
     __shared__ double red[KB / 32];
     const int k = blockIdx.x;
     const int64_t beg = be[2 * k], end = be[2 * k + 1];
-    for (int t = threadIdx.x; t < j; t += KB) { ss[t] = d[t]; as[t] = d[j + 1 + t]; }
     const double alpha = sc[0], hj = sc[1];
+    if (alpha == 0.0) {                                    // fallback flagged by k_dcgs_coef: touch nothing
+        if (threadIdx.x == 0) part[k] = 0.0;
+        return;
+    }
+    for (int t = threadIdx.x; t < j; t += KB) { ss[t] = d[t]; as[t] = d[j + 1 + t]; }
     __syncthreads();
     double nrm = 0.0;
     for (int64_t r = beg + threadIdx.x; r < end; r += KB) {
@@ -281,6 +303,7 @@ struct Kr {
     int64_t n, ld;                    // basis vectors are ld = n rounded up to 32 apart (256-B aligned)
     int nblk;
     double bytes = 0;                 // algorithmic bytes of the Krylov kernels (tsp_solve_info.bytes_krylov)
+    int force_fallback = 0;           // test knob TSP_DCGS2_FALLBACK: every iteration takes the explicit path
     DBuf<double> pall;
     Kr(Ctx &c_, int maxv) : c(c_), n(c_.n), ld((c_.n + 31) & ~(int64_t)31)
     {
@@ -317,7 +340,7 @@ struct Kr {
         prof_begin(c, PK_DOT);
         k_mdot2<<<c.nchunk_loc, KB, 0, c.s>>>(j + 1, V, ld, V + (size_t)j * ld, w, c.chunk_beg, c.kpart, c.nchunk_loc);
         finish(2 * (j + 1), d, 0);
-        k_dcgs_coef<<<1, 32, 0, c.s>>>(j, d, sc);
+        k_dcgs_coef<<<1, 32, 0, c.s>>>(j, d, sc, force_fallback);
         prof_end(c, PK_DOT, 8.0 * n * (j + 2));
         bytes += 8.0 * n * (j + 2);
         c.launches += 2;
@@ -330,6 +353,15 @@ struct Kr {
         finish(1, rho, 2);
         prof_end(c, PK_AXPY, 8.0 * n * (j + 4));
         bytes += 8.0 * n * (j + 4);
+        c.launches++;
+    }
+    // w -= V_{0..nv-1} h (h on the device)
+    void gs_sub(const double *V, int nv, const double *h, double *w)
+    {
+        prof_begin(c, PK_AXPY);
+        k_gs_sub<<<nblk, KB, 0, c.s>>>(nv, V, ld, h, w, n);
+        prof_end(c, PK_AXPY, 8.0 * n * (nv + 2));
+        bytes += 8.0 * n * (nv + 2);
         c.launches++;
     }
     void norm(const double *w, double *nrm)
@@ -413,14 +445,24 @@ static void run_body(Ctx &c, Kr &K, int j, bool use_graph, F &body)
         // capture on a private stream (the API stream may be the legacy default stream, which cannot capture);
         // the body launches on c.s, so c.s points at it meanwhile
         if (!c.cap_stream) TSP_CUDA(cudaStreamCreateWithFlags(&c.cap_stream, cudaStreamNonBlocking));
-        const cudaStream_t api = c.s;
+        // the capture is ended and c.s restored on every exit path, exceptions included
+        struct CaptureScope {
+            Ctx &c; cudaStream_t api; bool open = false;
+            ~CaptureScope()
+            {
+                if (open) { cudaGraph_t g = nullptr; cudaStreamEndCapture(c.s, &g); if (g) cudaGraphDestroy(g); (void)cudaGetLastError(); }
+                c.s = api;
+            }
+        } scope{c, c.s};
         c.s = c.cap_stream;
         TSP_CUDA(cudaStreamBeginCapture(c.s, cudaStreamCaptureModeThreadLocal));
+        scope.open = true;
         try {
             body();
         } catch (const Error &e) {                  // not capturable here: end the capture, run eagerly from now on
             cudaStreamEndCapture(c.s, &graph);
-            c.s = api;
+            scope.open = false;
+            c.s = scope.api;
             if (graph) cudaGraphDestroy(graph);
             (void)cudaGetLastError();
             if (getenv("TSP_DEBUG")) fprintf(stderr, "[tsp graph] capture of iteration %d failed: %s\n", j, e.msg.c_str());
@@ -430,7 +472,8 @@ static void run_body(Ctx &c, Kr &K, int j, bool use_graph, F &body)
             return;
         }
         const cudaError_t ec = cudaStreamEndCapture(c.s, &graph);
-        c.s = api;
+        scope.open = false;
+        c.s = scope.api;
         TSP_CUDA(ec);
         TSP_CUDA(cudaGraphInstantiate(&G.exec, graph, 0));
         cudaGraphDestroy(graph);
@@ -452,7 +495,7 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
         c.V.alloc((size_t)(m + 1) * ld);
         c.Z.alloc((size_t)m * ld);
         c.kr.alloc(std::max<int64_t>(n, 1));
-        c.kh.alloc(4 * (m + 2) + 8);
+        c.kh.alloc(5 * (m + 2) + 16);
         c.kpart.alloc((size_t)2 * (m + 2) * std::max(c.nchunk_loc, 1) + 64);
         c.seg_part.alloc((size_t)2 * (m + 2) * std::max(c.nseg_max, 1) + 64);
         c.kcap = m;
@@ -461,8 +504,12 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
     double *V = c.V, *Z = c.Z, *r = c.kr;
     // device scalars: d = pass-1 dots [0, 2(j+1)), then alpha, h_j, rho right behind them
     double *dh = c.kh;
-    cudaEvent_t e0, e1;
-    TSP_CUDA(cudaEventCreate(&e0)); TSP_CUDA(cudaEventCreate(&e1));
+    struct Events {                                  // destroyed on every exit path
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        ~Events() { if (e0) cudaEventDestroy(e0); if (e1) cudaEventDestroy(e1); }
+    } ev;
+    TSP_CUDA(cudaEventCreate(&ev.e0)); TSP_CUDA(cudaEventCreate(&ev.e1));
+    cudaEvent_t e0 = ev.e0, e1 = ev.e1;
     TSP_CUDA(cudaEventRecord(e0, c.s));
 
     Hess H(m);
@@ -479,7 +526,8 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
     TSP_REQUIRE(std::isfinite(bn), TSP_ERR_NUMERIC, "non-finite ||b||");
     if (o.x0_zero && n) TSP_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, c.s));
     int it = 0, status = TSP_NOT_CONVERGED;
-    info.restarts = 0; info.est_relres = 0; info.true_relres = 0; info.reorth = 0;
+    info.restarts = 0; info.est_relres = 0; info.true_relres = 0; info.reorth = 0; info.dcgs_fallbacks = 0;
+    K.force_fallback = getenv("TSP_DCGS2_FALLBACK") != nullptr;
     if (bn == 0.0) {
         if (n) TSP_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, c.s));
         status = TSP_OK;
@@ -516,16 +564,49 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
                 };
                 run_body(c, K, j, use_graph, body);
                 TSP_CUDA(cudaStreamSynchronize(c.s));
-                const double *dd = c.kcol_host, alpha = dd[2 * (j + 1)], hj = dd[2 * (j + 1) + 1], rj = dd[2 * (j + 1) + 2];
+                const double *dd = c.kcol_host;
+                double alpha = dd[2 * (j + 1)], hj = dd[2 * (j + 1) + 1], rj = dd[2 * (j + 1) + 2];
                 TSP_REQUIRE(std::isfinite(alpha) && std::isfinite(hj) && std::isfinite(rj), TSP_ERR_NUMERIC,
-                            "non-finite Arnoldi coefficients (loss of orthogonality)");
+                            "non-finite Arnoldi coefficients");
+                std::vector<double> s_j(dd, dd + j), a_j(dd + j + 1, dd + 2 * j + 1);
+                if (alpha == 0.0) {
+                    // k_dcgs_coef flagged the Pythagorean norm (u_j nearly inside span V, or the test knob): u_j
+                    // and w are untouched.  Explicit two-pass path: v_j = (u_j - V s)/||u_j - V s||, then
+                    // classical Gram-Schmidt of w against V_0..V_j applied twice, rho = ||w||.
+                    info.dcgs_fallbacks++;
+                    double *fb = dh + 4 * (m + 2) + 8;       // device scratch of m + 2 values
+                    double host[2 * (120 + 2)];
+                    K.gs_sub(V, j, dh, uj);                   // dh[0..j) = s
+                    K.norm(uj, fb);
+                    TSP_CUDA(cudaMemcpyAsync(host, fb, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+                    TSP_CUDA(cudaStreamSynchronize(c.s));
+                    alpha = host[0];
+                    TSP_REQUIRE(alpha > 0.0 && std::isfinite(alpha), TSP_ERR_NUMERIC, "Arnoldi vector inside the Krylov basis");
+                    K.scale_inv(fb, uj, uj);
+                    std::vector<double> h(j + 1, 0.0);
+                    for (int pass = 0; pass < 2; ++pass) {
+                        K.mdot(V, j + 1, w, fb);
+                        K.gs_sub(V, j + 1, fb, w);
+                        TSP_CUDA(cudaMemcpyAsync(host, fb, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, c.s));
+                        TSP_CUDA(cudaStreamSynchronize(c.s));
+                        for (int t = 0; t <= j; ++t) h[t] += host[t];
+                    }
+                    K.norm(w, fb);
+                    K.scale_inv(fb, w, w);
+                    TSP_CUDA(cudaMemcpyAsync(host, fb, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+                    TSP_CUDA(cudaStreamSynchronize(c.s));
+                    rj = host[0];
+                    TSP_REQUIRE(std::isfinite(rj), TSP_ERR_NUMERIC, "non-finite Arnoldi norm");
+                    for (int t = 0; t < j; ++t) a_j[t] = h[t];
+                    hj = h[j];
+                }
                 info.reorth++;
-                if (j > 0) H.complete(j - 1, rho_prev, dd, alpha);   // column j-1 now exact
+                if (j > 0) H.complete(j - 1, rho_prev, s_j.data(), alpha);   // column j-1 now exact
                 else {                                                  // u_0 = r/beta: v_0 = u_0/alpha
                     H.g[0] = H.gin[0] = beta * alpha;
                 }
                 H.raw[j].assign(j + 2, 0.0);
-                for (int t = 0; t < j; ++t) H.raw[j][t] = dd[j + 1 + t];
+                for (int t = 0; t < j; ++t) H.raw[j][t] = a_j[t];
                 H.raw[j][j] = hj;
                 H.raw[j][j + 1] = rj;                  // provisional: u_{j+1} taken as v_{j+1}
                 H.rotate(j);
@@ -542,7 +623,18 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
                 TSP_CUDA(cudaStreamSynchronize(c.s));
                 double ss = 0.0;
                 for (int t = 0; t < k; ++t) ss = std::fma(col[t], col[t], ss);
-                const double a2 = col[k] - ss;
+                double a2 = col[k] - ss;
+                if (!(a2 > 1e-6 * col[k]) || K.force_fallback) {      // explicit norm of u_k - V s (see above)
+                    info.dcgs_fallbacks++;
+                    double *fb = dh + 4 * (m + 2) + 8;
+                    double *uk = V + (size_t)k * ld;
+                    K.gs_sub(V, k, dh, uk);
+                    K.norm(uk, fb);
+                    double an;
+                    TSP_CUDA(cudaMemcpyAsync(&an, fb, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+                    TSP_CUDA(cudaStreamSynchronize(c.s));
+                    a2 = an * an;
+                }
                 TSP_REQUIRE(a2 > 0.0 && std::isfinite(a2), TSP_ERR_NUMERIC, "loss of orthogonality in the last Arnoldi vector");
                 H.complete(k - 1, rho_prev, col.data(), std::sqrt(a2));
                 info.est_relres = std::fabs(H.g[k]) / bn;
@@ -565,7 +657,6 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
     TSP_CUDA(cudaEventSynchronize(e1));
     float ms = 0;
     TSP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-    cudaEventDestroy(e0); cudaEventDestroy(e1);
     info.iterations = it;
     info.status = status;
     info.t_solve_s = ms * 1e-3;

@@ -18,6 +18,7 @@ void csr_upload(Ctx &c, Csr &A, int n, int m, int nc, const int32_t *rp, const i
     } else {
         nnz = rp[n];
     }
+    TSP_REQUIRE(nnz >= 0, TSP_ERR_INVALID_ARG, "rowptr[n] < 0");
     A.nnz = nnz;
     A.rp.alloc(n + 1); A.ci.alloc(nnz); A.v.alloc(nnz * nc);
     cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
@@ -28,9 +29,11 @@ void csr_upload(Ctx &c, Csr &A, int n, int m, int nc, const int32_t *rp, const i
     }
 }
 
-// validation on the device (one flag back to the host): rowptr[0] == 0, monotone row pointers,
-// in-range and strictly increasing (sorted, unique) columns in every row
-__global__ void k_check_csr(int n, int m, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci, unsigned *flag)
+// validation on the device (one flag back to the host): rowptr[0] == 0, monotone row pointers inside
+// [0, nnz] (a row outside is flagged and not read), in-range and strictly increasing (sorted, unique)
+// columns in every row
+__global__ void k_check_csr(int n, int m, int64_t nnz, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                            unsigned *flag)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i > n) return;
@@ -38,7 +41,7 @@ __global__ void k_check_csr(int n, int m, const int32_t *__restrict__ rp, const 
     if (i == 0 && rp[0] != 0) f |= 1u;
     if (i < n) {
         const int64_t a = rp[i], b = rp[i + 1];
-        if (b < a) f |= 2u;
+        if (b < a || a < 0 || b > nnz) { atomicOr(flag, f | 2u); return; }
         for (int64_t q = a; q < b; ++q) {
             const int j = ci[q];
             if (j < 0 || j >= m) f |= 4u;
@@ -51,13 +54,13 @@ __global__ void k_check_csr(int n, int m, const int32_t *__restrict__ rp, const 
 void check_csr(Ctx &c, const Csr &A, const char *name)
 {
     DBuf<unsigned> flag; flag.alloc(1); flag.zero(c.s);
-    k_check_csr<<<grid_for(A.n + 1, 256), 256, 0, c.s>>>(A.n, A.m, A.rp, A.ci, flag);
+    k_check_csr<<<grid_for(A.n + 1, 256), 256, 0, c.s>>>(A.n, A.m, A.nnz, A.rp, A.ci, flag);
     c.launches++;
     unsigned f = 0;
     TSP_CUDA(cudaMemcpyAsync(&f, flag.p, sizeof(f), cudaMemcpyDeviceToHost, c.s));
     TSP_CUDA(cudaStreamSynchronize(c.s));
     TSP_REQUIRE(!(f & 1u), TSP_ERR_INVALID_ARG, std::string(name) + ": rowptr[0] != 0");
-    TSP_REQUIRE(!(f & 2u), TSP_ERR_INVALID_ARG, std::string(name) + ": rowptr not monotone");
+    TSP_REQUIRE(!(f & 2u), TSP_ERR_INVALID_ARG, std::string(name) + ": rowptr not monotone or outside [0, nnz]");
     TSP_REQUIRE(!(f & 4u), TSP_ERR_INVALID_ARG, std::string(name) + ": column out of range");
     TSP_REQUIRE(!(f & 8u), TSP_ERR_INVALID_ARG, std::string(name) + ": columns not sorted/unique in a row");
 }

@@ -37,31 +37,39 @@ struct Error {
 // sizes, so after the first one no allocation reaches the driver (the stream-ordered pool grew
 // by a few hundred MB now and then under the interleaved lifetimes of the two hierarchies, and a
 // growth step cost 0.1-0.6 s).  Reuse within one stream is safe in stream order.
+// With a caller allocator (tsp_desc.allocator) every buffer goes through its callbacks instead.
+struct AllocState {
+    tsp_allocator al{};
+    int64_t n_cb = 0, n_pool = 0, bytes_live = 0;
+};
 extern thread_local cudaStream_t g_alloc_stream;
+extern thread_local AllocState *g_alloc_state;  // the handle whose API call is in progress on this thread
 double dbg_now();                              // TSP_DEBUG: wall clock (0 when off)
 void dbg_alloc(double t0, size_t bytes);       // TSP_DEBUG: report slow allocations
-void *dev_alloc(size_t bytes, cudaStream_t s);
-void dev_free(void *p, size_t bytes, cudaStream_t s);
+void *dev_alloc(size_t bytes, cudaStream_t s, AllocState *as);
+void dev_free(void *p, size_t bytes, cudaStream_t s, AllocState *as);
 void dev_cache_flush(cudaStream_t s);          // return the stream's cached blocks to the pool
 template <class T>
 struct DBuf {
     T *p = nullptr;
     size_t n = 0;
     cudaStream_t st = 0;
+    AllocState *as = nullptr;
     DBuf() = default;
     DBuf(const DBuf &) = delete;
     DBuf &operator=(const DBuf &) = delete;
-    DBuf(DBuf &&o) noexcept : p(o.p), n(o.n), st(o.st) { o.p = nullptr; o.n = 0; }
-    DBuf &operator=(DBuf &&o) noexcept { release(); p = o.p; n = o.n; st = o.st; o.p = nullptr; o.n = 0; return *this; }
+    DBuf(DBuf &&o) noexcept : p(o.p), n(o.n), st(o.st), as(o.as) { o.p = nullptr; o.n = 0; }
+    DBuf &operator=(DBuf &&o) noexcept { release(); p = o.p; n = o.n; st = o.st; as = o.as; o.p = nullptr; o.n = 0; return *this; }
     ~DBuf() { release(); }
     void alloc(size_t count) {
         release();
         n = count;
         st = g_alloc_stream;
-        if (count) p = (T *)dev_alloc(sizeof(T) * count, st);
+        as = g_alloc_state;
+        if (count) p = (T *)dev_alloc(sizeof(T) * count, st, as);
     }
     void zero(cudaStream_t s) { if (n) TSP_CUDA(cudaMemsetAsync(p, 0, sizeof(T) * n, s)); }
-    void release() { if (p) dev_free(p, sizeof(T) * n, st); p = nullptr; n = 0; }
+    void release() { if (p) dev_free(p, sizeof(T) * n, st, as); p = nullptr; n = 0; }
     operator T *() const { return p; }
 };
 
@@ -174,6 +182,7 @@ struct Level {
     DBuf<double> dinv_gh;              // ghost copy of dinv (dist)
     DBuf<double> gh_b, gh_x;           // ghost buffers for b and x (dist)
     std::vector<int64_t> rep_counts, rep_offs;  // next level replicated: rows per rank (allgather)
+    DBuf<int64_t> rep_offs_d;          // rep_offs on the device (uploaded once at setup)
     DBuf<double> rep_buf;              // padded allgather buffer
     Csr A;                        // level operator (local column ids if dist)
     DBuf<int32_t> zb;             // z-block per row
@@ -212,6 +221,7 @@ struct Prof {
 
 // ------------------------------------------------------------------ the handle
 struct Ctx {
+    AllocState alloc;                  // FIRST member: outlives every buffer of the handle
     // Nn, Nc, n and nz are this rank's LOCAL (owned) sizes; *_glob the global ones
     int nx, ny, nz, Nn, Nc;
     int64_t n;
@@ -270,6 +280,7 @@ struct Ctx {
     cudaStream_t cap_stream = nullptr; // private stream the graphs are captured on
     // counters
     int64_t launches = 0, skipped_dss = 0, perturbed = 0;
+    int64_t variants[TSP_NVARIANTS] = {};   // kernel-variant choices of the setup (tsp_variant_counts)
     DBuf<unsigned long long> dcount;  // device counters scratch
     DBuf<uint8_t> scratch; size_t scratch_bytes = 0;
     Prof prof;

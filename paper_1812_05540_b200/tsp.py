@@ -37,12 +37,51 @@ class tsp_bsr(C.Structure):
     _fields_ = [("rowptr", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p)]
 
 
+_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+
+
+class tsp_allocator(C.Structure):
+    _fields_ = [("alloc", _ALLOC_FN), ("free", _FREE_FN), ("ctx", C.c_void_p)]
+
+
 class tsp_desc(C.Structure):
     _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("rank", C.c_int), ("nranks", C.c_int),
                 ("comm_kind", C.c_int), ("comm_arg", C.c_void_p),
                 ("stream", C.c_void_p), ("inputs_on_device", C.c_int),
                 ("A_uu", tsp_bsr), ("A_uf", tsp_bsr), ("A_fu", tsp_bsr), ("A_ff", tsp_bsr),
-                ("fs_diag", C.c_void_p), ("opts", tsp_options)]
+                ("fs_diag", C.c_void_p), ("opts", tsp_options), ("allocator", tsp_allocator)]
+
+
+class TorchAllocator:
+    """include/tsp.h tsp_allocator routed to torch's CUDA caching allocator
+    (torch.cuda.caching_allocator_alloc / caching_allocator_delete): the library's device memory then lives in
+    the same pool as the caller's tensors.  Marshalling only; counts the calls for the tests."""
+
+    def __init__(self, torch, device):
+        self.torch, self.device = torch, device
+        self.allocs = self.frees = 0
+        self.live_bytes = self.peak_bytes = 0
+
+        def _alloc(nbytes, stream, ctx):
+            try:
+                p = torch.cuda.caching_allocator_alloc(int(nbytes), self.device, int(stream or 0))
+            except Exception:                                   # out of memory: the library reports TSP_ERR_OOM
+                return None
+            self.allocs += 1
+            self.live_bytes += int(nbytes)
+            self.peak_bytes = max(self.peak_bytes, self.live_bytes)
+            return p
+
+        def _free(ptr, nbytes, stream, ctx):
+            torch.cuda.caching_allocator_delete(ptr)
+            self.frees += 1
+            self.live_bytes -= int(nbytes)
+
+        self._cbs = (_ALLOC_FN(_alloc), _FREE_FN(_free))     # kept alive as long as the handle
+
+    def struct(self):
+        return tsp_allocator(self._cbs[0], self._cbs[1], None)
 
 
 class tsp_solve_opts(C.Structure):
@@ -53,14 +92,15 @@ class tsp_solve_opts(C.Structure):
 class tsp_solve_info(C.Structure):
     _fields_ = [("iterations", C.c_int), ("restarts", C.c_int), ("status", C.c_int),
                 ("est_relres", C.c_double), ("true_relres", C.c_double), ("t_solve_s", C.c_double),
-                ("reorth", C.c_int), ("bytes_krylov", C.c_double)]
+                ("reorth", C.c_int), ("bytes_krylov", C.c_double), ("dcgs_fallbacks", C.c_int)]
 
 
 class tsp_stats(C.Structure):
     _fields_ = [("levels", C.c_int * 2), ("rows", (C.c_int64 * 16) * 2), ("nnz", (C.c_int64 * 16) * 2),
                 ("launches", C.c_int64), ("skipped_dss", C.c_int64), ("perturbed_pivots", C.c_int64),
                 ("coarsening_fallbacks", C.c_int64), ("bytes_apply", C.c_double), ("bytes_operator", C.c_double),
-                ("bytes_iter_base", C.c_double), ("bytes_per_krylov_vec", C.c_double)]
+                ("bytes_iter_base", C.c_double), ("bytes_per_krylov_vec", C.c_double),
+                ("allocs_callback", C.c_int64), ("allocs_pool", C.c_int64), ("bytes_live", C.c_int64)]
 
 
 TSP_PROF_MAX = 32
@@ -105,7 +145,8 @@ def lib():
         L.tsp_local_world_destroy.restype = None
         L.tsp_partition.argtypes = [C.c_int] * 6 + [_P(C.c_int64)]
         L.tsp_level_dist.argtypes = [C.c_void_p, C.c_int, C.c_int, _P(C.c_int64)]
-        if L.tsp_abi_version() != 2:
+        L.tsp_variant_counts.argtypes = [C.c_void_p, _P(C.c_int64)]
+        if L.tsp_abi_version() != 3:
             raise RuntimeError("libtsp ABI version mismatch")
         _LIB = L
     return _LIB
@@ -115,7 +156,11 @@ EXPORTED = ["tsp_abi_version", "tsp_last_error", "tsp_default_options", "tsp_cre
             "tsp_apply_preconditioner", "tsp_apply_operator", "tsp_solve", "tsp_default_solve_opts",
             "tsp_get_stats", "tsp_level_sizes", "tsp_export_level", "tsp_prof_enable", "tsp_prof_read",
             "tsp_prof_classes", "tsp_export_cpr", "tsp_destroy", "tsp_nccl_unique_id", "tsp_local_world_create", "tsp_local_world_destroy",
-            "tsp_partition", "tsp_level_dist"]
+            "tsp_partition", "tsp_level_dist", "tsp_variant_counts"]
+
+# include/tsp.h TSP_VAR_* order
+VARIANTS = ["spgemm_hs64", "spgemm_hs128", "spgemm_hs512", "spgemm_hs4096", "spgemm_g4", "spgemm_g8", "spgemm_g32",
+            "lanes_A0", "lanes_A8", "lanes_A16", "lanes_A32", "lanes_R0", "lanes_R8", "lanes_R16", "lanes_R32"]
 
 TSP_COMM_NONE, TSP_COMM_NCCL, TSP_COMM_LOCAL = 0, 1, 2
 
@@ -184,7 +229,10 @@ class Tsp:
     """One handle.  `arrays` is a synth.Problem (numpy, host) -- or any object
     with the same attribute names holding CUDA torch tensors (device=True)."""
 
-    def __init__(self, pb, stream=None, device_inputs=False, rank=0, nranks=1, comm_kind=0, comm_arg=None, **opts):
+    def __init__(self, pb, stream=None, device_inputs=False, rank=0, nranks=1, comm_kind=0, comm_arg=None,
+                 allocator="torch", **opts):
+        """allocator: "torch" (default) routes every device buffer of the handle through torch's caching
+        allocator (tsp_desc.allocator); None keeps the library's own stream-ordered pool."""
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("libtsp needs a CUDA device (no CPU fallback)")
@@ -218,6 +266,12 @@ class Tsp:
             setattr(d, "A_" + name, b)
         d.fs_diag = arr(pb.fs)
         d.opts = default_options(**opts)
+        self.allocator = None
+        if allocator == "torch":
+            self.allocator = TorchAllocator(torch, torch.cuda.current_device())
+            d.allocator = self.allocator.struct()
+        elif allocator is not None:
+            raise ValueError("allocator must be 'torch' or None")
         h = C.c_void_p()
         _check(L.tsp_create(C.byref(h), C.byref(d)), "tsp_create")
         self.h = h
@@ -250,7 +304,7 @@ class Tsp:
         _check(rc, "tsp_solve", ok=(0, 1))
         return dict(iterations=info.iterations, restarts=info.restarts, status=STATUS.get(info.status, info.status),
                     est_relres=info.est_relres, true_relres=info.true_relres, t_solve_s=info.t_solve_s,
-                    reorth=info.reorth, bytes_krylov=info.bytes_krylov)
+                    reorth=info.reorth, bytes_krylov=info.bytes_krylov, dcgs_fallbacks=info.dcgs_fallbacks)
 
     def stats(self):
         s = tsp_stats()
@@ -260,6 +314,12 @@ class Tsp:
         out["rows"] = [list(s.rows[w])[: s.levels[w]] for w in range(2)]
         out["nnz"] = [list(s.nnz[w])[: s.levels[w]] for w in range(2)]
         return out
+
+    def variants(self):
+        """Test hook: kernel-variant choices of this handle's setups (include/tsp.h tsp_variant_counts)."""
+        o = (C.c_int64 * len(VARIANTS))()
+        _check(lib().tsp_variant_counts(self.h, o), "tsp_variant_counts")
+        return dict(zip(VARIANTS, list(o)))
 
     def num_levels(self, which):
         return self.stats()["levels"][which]

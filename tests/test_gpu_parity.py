@@ -327,3 +327,181 @@ def test_degenerate_grids(dev, grid):
     ig = g.solve(_cuda(pb.b), x, rtol=1e-8)
     assert ig["status"] == "OK" and io["status"] == 0 and abs(ig["iterations"] - io["iterations"]) <= 1
     g.close()
+
+
+# ---------------------------------------------------------------- BASELINE.json's larger configs (SURVEY c.5)
+_VARIANTS = {}
+
+
+def _note_variants(g):
+    for k, v in g.variants().items():
+        _VARIANTS[k] = _VARIANTS.get(k, 0) + v
+
+
+def _hier_equal(o, g):
+    for which in (0, 1):
+        H_o, H_g = o.hierarchy(which), g.hierarchy(which)
+        assert len(H_o) == len(H_g), which
+        for lo, lg in zip(H_o, H_g):
+            assert lo["n"] == lg["n"] and lo["nnz"] == lg["nnz"] and lo["coarsest"] == lg["coarsest"]
+            for k in ("A_rp", "A_ci", "A_v", "dl1") + (() if lo["coarsest"] else ("agg", "P_rp", "P_ci", "P_v")):
+                assert np.array_equal(lo[k], lg[k]), (which, k)
+        del H_o, H_g
+
+
+def _apply_ok(pb, o, g, dev, vs):
+    z = torch.empty(pb.n, dtype=torch.float64, device=dev)
+    nu = 3 * pb.Nn
+    for v in vs:
+        g.apply_preconditioner(_cuda(v), z)
+        torch.cuda.synchronize()
+        ref = o.apply(v)
+        got = z.cpu().numpy()
+        assert np.linalg.norm(got - ref) <= 1e-10 * np.linalg.norm(ref)
+        for sl in (slice(0, nu), slice(nu, None, 2), slice(nu + 1, None, 2)):
+            assert np.linalg.norm(got[sl] - ref[sl]) <= 1e-10 * np.linalg.norm(ref[sl])
+
+
+LARGE = {
+    "C3": dict(config="C3"),                     # BASELINE.json configs[2]
+    "C4": dict(config="C4"),                     # configs[3] = the staircase L2 grid
+    "ST1": dict(config="ST1"),                   # staircase level 1, Table 1 contrast 1000:1
+    # SPE10-shaped sub-grid (R-s10): seal layers of 0.01 mD / 1 % above and below a correlated reservoir
+    "S10s": dict(config="S10", nx=30, ny=44, nz=84, burden=28),
+}
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", list(LARGE))
+def test_full_parity_large(dev, name):
+    """The full parity bar on C3, C4 and the f4 workloads: operator <= 1e-13, both hierarchies bit-exact,
+    three applications <= 1e-10 (also per field), FGMRES +-1 with both true residuals <= 1e-8."""
+    from paper_1812_05540_b200 import Tsp
+    _cache.clear()
+    kw = dict(LARGE[name])
+    pb = synth.generate(kw.pop("config"), **kw)
+    o = oracle.Oracle(pb).setup()
+    g = Tsp(pb).setup()
+    _note_variants(g)
+    x = np.random.default_rng(11).uniform(-1, 1, pb.n)
+    y = torch.empty(pb.n, dtype=torch.float64, device=dev)
+    g.apply_operator(_cuda(x), y)
+    torch.cuda.synchronize()
+    ref = o.operator(x)
+    assert np.linalg.norm(y.cpu().numpy() - ref) <= 1e-13 * np.linalg.norm(ref)
+    del y
+    _hier_equal(o, g)
+    rng = np.random.default_rng(12)
+    _apply_ok(pb, o, g, dev, (pb.b, rng.uniform(-1, 1, pb.n), rng.standard_normal(pb.n)))
+    xo, io = o.solve(pb.b, rtol=1e-8, m=64)
+    xg = torch.zeros(pb.n, dtype=torch.float64, device=dev)
+    ig = g.solve(_cuda(pb.b), xg, rtol=1e-8, restart=64)
+    assert ig["status"] == "OK" and io["status"] == 0
+    assert abs(ig["iterations"] - io["iterations"]) <= 1, (ig["iterations"], io["iterations"])
+    assert ig["true_relres"] <= 1e-8 and io["true_relres"] <= 1e-8
+    r = pb.b - o.operator(xg.cpu().numpy())
+    assert np.linalg.norm(r) <= 1e-8 * np.linalg.norm(pb.b)
+    print(f"[parity {name}] n={pb.n} iterations gpu {ig['iterations']} oracle {io['iterations']}")
+    g.close()
+
+
+@pytest.mark.slow
+def test_c5_hierarchy_and_apply(dev):
+    """The benchmarked configuration (C5, 42.3M DoF, what bench.py times): both hierarchies bit-exact against
+    the oracle's setup and two applications of Algorithm 1 <= 1e-10 (also per field)."""
+    from paper_1812_05540_b200 import Tsp
+    _cache.clear()
+    pb = synth.generate("C5")
+    g = Tsp(pb).setup()
+    _note_variants(g)
+    o = oracle.Oracle(pb).setup()
+    _hier_equal(o, g)
+    _apply_ok(pb, o, g, dev, (pb.b, np.random.default_rng(12).uniform(-1, 1, pb.n)))
+    g.close()
+
+
+@pytest.mark.parametrize("slots", [512, 4096])
+def test_spgemm_overflow_tables_bit_exact(dev, slots, monkeypatch):
+    """TSP_SPGEMM_MIN_SLOTS starts the Galerkin products at the overflow tables the large configs reach
+    (C5: 512 slots): the hierarchies stay bit-exact with the oracle."""
+    from paper_1812_05540_b200 import Tsp
+    pb, o, _ = _pair("R1")
+    monkeypatch.setenv("TSP_SPGEMM_MIN_SLOTS", str(slots))
+    g = Tsp(pb).setup()
+    v = g.variants()
+    _note_variants(g)
+    assert v[f"spgemm_hs{slots}"] > 0 and v["spgemm_hs64"] == v["spgemm_hs128"] == 0
+    _hier_equal(o, g)
+    g.close()
+
+
+@pytest.mark.parametrize("lanes", [0, 8, 16, 32])
+def test_every_lane_variant_under_parity(dev, lanes, monkeypatch):
+    """TSP_FORCE_LANES puts every coarse level and restriction on one vector-CSR variant: each variant the
+    lanes_for choice can take gives the oracle's application <= 1e-10."""
+    from paper_1812_05540_b200 import Tsp
+    pb, o, _ = _pair("C2")
+    monkeypatch.setenv("TSP_FORCE_LANES", str(lanes))
+    g = Tsp(pb).setup()
+    v = g.variants()
+    _note_variants(g)
+    assert v[f"lanes_A{lanes}"] > 0 and v[f"lanes_R{lanes}"] > 0
+    _apply_ok(pb, o, g, dev, (pb.b, np.random.default_rng(3).uniform(-1, 1, pb.n)))
+    g.close()
+
+
+def test_variant_coverage_summary(dev):
+    """Every kernel variant the setup can choose ran in a test above that compared with the oracle."""
+    print("[variants under parity]", _VARIANTS)
+    for k in ("spgemm_hs64", "spgemm_hs128", "spgemm_hs512", "spgemm_hs4096", "spgemm_g4", "spgemm_g8", "spgemm_g32",
+              "lanes_A0", "lanes_A8", "lanes_A16", "lanes_A32", "lanes_R0", "lanes_R8", "lanes_R16", "lanes_R32"):
+        assert _VARIANTS.get(k, 0) > 0, k
+
+
+def test_torch_allocator_routes_every_buffer(dev):
+    """tsp_desc.allocator (include/tsp.h): with torch's caching allocator every device buffer of the handle
+    goes through the callbacks (none from the library's pool), all are returned at tsp_destroy, and the
+    results are bitwise those of the library's own pool."""
+    from paper_1812_05540_b200 import Tsp
+    pb = _problem("R1")
+    out = []
+    for alloc in ("torch", None):
+        g = Tsp(pb, allocator=alloc).setup()
+        x = torch.zeros(pb.n, dtype=torch.float64, device=dev)
+        info = g.solve(_cuda(pb.b), x)
+        torch.cuda.synchronize()
+        st = g.stats()
+        if alloc == "torch":
+            A = g.allocator
+            assert st["allocs_pool"] == 0 and st["allocs_callback"] == A.allocs > 100
+            assert st["bytes_live"] == A.live_bytes > 0
+            assert torch.cuda.memory_allocated() >= A.live_bytes
+        else:
+            assert st["allocs_callback"] == 0 and st["allocs_pool"] > 100
+        g.close()
+        if alloc == "torch":
+            assert A.frees == A.allocs and A.live_bytes == 0
+        out.append((x.cpu().numpy(), info["iterations"]))
+    assert out[0][1] == out[1][1] and np.array_equal(out[0][0], out[1][0])
+
+
+def test_dcgs2_explicit_fallback_path(dev, monkeypatch):
+    """krylov.cu: when the Pythagorean norm of DCGS2 loses more than 6 digits (u_j nearly inside the basis) the
+    iteration takes an explicit two-pass classical Gram-Schmidt instead of failing.  TSP_DCGS2_FALLBACK forces it
+    on every iteration: FGMRES still matches the oracle's MGS within +-1 and reaches the tolerance."""
+    from paper_1812_05540_b200 import Tsp
+    pb, o, _ = _pair("C2")
+    monkeypatch.setenv("TSP_DCGS2_FALLBACK", "1")
+    g = Tsp(pb).setup()
+    for m in (64, 17):
+        x = torch.zeros(pb.n, dtype=torch.float64, device=dev)
+        ig = g.solve(_cuda(pb.b), x, rtol=1e-8, restart=m)
+        xo, io = o.solve(pb.b, rtol=1e-8, m=m)
+        assert ig["status"] == "OK" and ig["dcgs_fallbacks"] >= ig["iterations"]
+        assert abs(ig["iterations"] - io["iterations"]) <= 1 and ig["true_relres"] <= 1e-8
+    g.close()
+    monkeypatch.delenv("TSP_DCGS2_FALLBACK")
+    g = Tsp(pb).setup()
+    x = torch.zeros(pb.n, dtype=torch.float64, device=dev)
+    assert g.solve(_cuda(pb.b), x)["dcgs_fallbacks"] == 0
+    g.close()
