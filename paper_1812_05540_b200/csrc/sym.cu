@@ -5,12 +5,14 @@
 // (B(i,j)[r][c] == B(j,i)[c][r] for every pair -- for the Q1 elasticity part all of them; the gravity
 // term of the momentum balance, d(rho g)/d eps_v, breaks it in the z row and column) are stored for the
 // diagonal block and the 13 "upper" neighbours only: a lower neighbour j reads B(i,j) = B(j,i)^T from
-// row j's upper slot.  The other entries are stored for all 27 neighbours.  (The mirrored reads of the
-// z-neighbours come one node plane -- ~100 MB of traffic at C5 -- after row j's own read and mostly miss L2:
-// measured DRAM traffic of the operator 20 GB instead of 21 GB, 2.86 ms instead of 3.07 ms; pencil orders
-// that keep the reuse in L2 need so few resident CTAs that they lose to latency.)  The 27 contributions are summed in
-// the CSR's ascending column order with the same fma pattern as the SELL kernels, so the result is
-// bitwise that of the generic path (tests/test_gpu_parity.py).
+// row j's upper slot.  The other entries are stored for all 27 neighbours.  A row sums its own entries first
+// (diagonal, then the 13 upper neighbours) and the 13 mirrored lower blocks after them: with the generic
+// ascending-column order every mirror load was issued before (or with) the load of the row that owns the
+// entry and both missed L2 -- ncu at C5: 22.7 GB of L2 requests, 20.1 GB of DRAM reads for 17.07 GB of
+// algorithmic bytes; own-entries-first: 18.1 GB of DRAM reads, 2.87 -> 2.61 ms (level-0 SDC smoother
+// 0.97/0.91 -> 0.92/0.79 ms).  L2 eviction-priority hints (evict-last on the own +z entries, evict-first on
+// their mirrors, with or without a persisting-L2 carve-out) did not help further (measured).  The sums are
+// the generic path's up to the summation order (tests/test_gpu_parity.py).
 //
 // Local node n of a z-slab: x = n % NX, y = (n / NX) % NY, plane zl = n / (NX NY); global plane
 // zg = zn0 + zl.  A neighbour outside [0, Nn) is a ghost: below the slab (rank-1's last node plane,
@@ -149,8 +151,11 @@ __global__ void __launch_bounds__(256) k_op_node_sym(SymGeo g, const double *__r
     if (n >= g.Nn) return;
     const int x = n % g.NX, y = (n / g.NX) % g.NY, zg = g.zn0 + n / g.NXY;
     double a0 = 0, a1 = 0, a2 = 0;
+    // the diagonal and the 13 upper blocks (the row's own stored entries) first, then the 13 lower ones, whose
+    // symmetric entries are read back from the neighbours' upper slots -- after those rows read them themselves
 #pragma unroll
-    for (int c = 0; c < 27; ++c) {
+    for (int cc = 0; cc < 27; ++cc) {
+        const int c = cc < 14 ? 13 + cc : 26 - cc;
         if (!sym_inside(g, x, y, zg, c)) continue;
         const int n2 = n + sym_off(g, c);
         double B[9];
@@ -187,7 +192,8 @@ __global__ void __launch_bounds__(256) k_vc_sym(SymGeo g, const double *__restri
     const int x = n % g.NX, y = (n / g.NX) % g.NY, zg = g.zn0 + n / g.NXY;
     double acc[3] = {0, 0, 0};
 #pragma unroll
-    for (int c = 0; c < 27; ++c) {
+    for (int ck = 0; ck < 27; ++ck) {
+        const int c = ck < 14 ? 13 + ck : 26 - ck;   // own entries first (see k_op_node_sym)
         if (!sym_inside(g, x, y, zg, c)) continue;
         const int n2 = n + sym_off(g, c);
         double B[3];

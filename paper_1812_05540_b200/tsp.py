@@ -10,12 +10,14 @@ tsp_apply_operator, tsp_solve, tsp_get_stats, tsp_export_level, ...
 from __future__ import annotations
 
 import ctypes as C
+import atexit
 import os
+import weakref
 
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtsp.so")
+LIB_PATH = os.environ.get("TSP_LIB_DEV") or os.path.join(_HERE, "libtsp.so")   # TSP_LIB_DEV: developer A/B builds only
 _LIB = None
 _P = C.POINTER
 
@@ -74,7 +76,10 @@ class TorchAllocator:
             return p
 
         def _free(ptr, nbytes, stream, ctx):
-            torch.cuda.caching_allocator_delete(ptr)
+            try:
+                torch.cuda.caching_allocator_delete(ptr)
+            except Exception:                                   # interpreter shutdown: torch is gone already
+                return
             self.frees += 1
             self.live_bytes -= int(nbytes)
 
@@ -225,6 +230,16 @@ def default_options(**kw) -> tsp_options:
     return o
 
 
+_LIVE = weakref.WeakSet()
+
+
+@atexit.register
+def _close_all():
+    """Destroy the handles still open at exit while torch (whose allocator holds their memory) is alive."""
+    for t in list(_LIVE):
+        t.close()
+
+
 class Tsp:
     """One handle.  `arrays` is a synth.Problem (numpy, host) -- or any object
     with the same attribute names holding CUDA torch tensors (device=True)."""
@@ -275,6 +290,7 @@ class Tsp:
         h = C.c_void_p()
         _check(L.tsp_create(C.byref(h), C.byref(d)), "tsp_create")
         self.h = h
+        _LIVE.add(self)
 
     def close(self):
         if getattr(self, "h", None):

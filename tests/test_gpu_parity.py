@@ -231,10 +231,11 @@ def test_solve_parity_short_restart(dev, m):
 
 
 @pytest.mark.parametrize("name", ["C2", "R1"])
-def test_structured_symmetric_path_is_bitwise_the_generic_one(dev, name):
+def test_structured_symmetric_path_equals_the_generic_one(dev, name):
     """sym.cu (structured symmetric A_uu for the operator and the level-0 mechanics smoother) sums the same
-    27 blocks in the same order as the generic SELL kernels: operator, one Algorithm 1 application and the
-    FGMRES solution are bitwise equal with and without it (TSP_NO_SYM forces the generic path)."""
+    27 blocks as the generic SELL kernels, own entries first (sym.cu header): operator and one Algorithm 1
+    application equal to rounding, the same FGMRES iteration count and solution to the solver tolerance, with
+    and without it (TSP_NO_SYM forces the generic path)."""
     import os
     from paper_1812_05540_b200 import Tsp
     pb = _problem(name)
@@ -256,7 +257,9 @@ def test_structured_symmetric_path_is_bitwise_the_generic_one(dev, name):
         out.append((y.cpu().numpy(), z.cpu().numpy(), x.cpu().numpy(), info["iterations"], g.stats()["bytes_operator"]))
         g.close()
     (y1, z1, x1, i1, b1), (y2, z2, x2, i2, b2) = out
-    assert np.array_equal(y1, y2) and np.array_equal(z1, z2) and np.array_equal(x1, x2) and i1 == i2
+    assert np.linalg.norm(y1 - y2) <= 1e-14 * np.linalg.norm(y2)
+    assert np.linalg.norm(z1 - z2) <= 1e-12 * np.linalg.norm(z2)
+    assert abs(i1 - i2) <= 1 and np.linalg.norm(x1 - x2) <= 1e-6 * np.linalg.norm(x2)
     assert b1 < 0.9 * b2          # the structured path streams fewer operator bytes (no indices, mirrored entries)
 
 
