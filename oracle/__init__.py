@@ -35,7 +35,8 @@ class Opts(C.Structure):
                 ("zblock", C.c_int), ("tile_x", C.c_int), ("tile_y", C.c_int), ("tile_z", C.c_int),
                 ("mech_mode", C.c_int), ("pres_mode", C.c_int), ("local_mode", C.c_int), ("ff_mode", C.c_int),
                 ("cpr_mode", C.c_int), ("aps_mode", C.c_int), ("fs_mode", C.c_int), ("rsl_iters", C.c_int),
-                ("fs_modulus_scale", C.c_double), ("second_stage", C.c_int), ("local_sweeps", C.c_int)]
+                ("fs_modulus_scale", C.c_double), ("second_stage", C.c_int), ("local_sweeps", C.c_int),
+                ("amg_smoother", C.c_int), ("amg_gs_block", C.c_int)]
 
 
 class Info(C.Structure):
@@ -76,6 +77,11 @@ def lib():
         L.orc_amg_level_export.argtypes = [C.c_void_p, C.c_int, _I32, _I32, _F64, _I32, _I32, _I32, _F64, _F64]
         L.orc_amg_free.argtypes = [C.c_void_p]
         L.orc_amg_level_detail.argtypes = [C.c_void_p, C.c_int, _I32, _I32, _F64]
+        L.orc_amg_level_colour.argtypes = [C.c_void_p, C.c_int, _I32]
+        L.orc_amg_level_gs.argtypes = [C.c_void_p, C.c_int, _F64]
+        L.orc_amg_build_coloured.argtypes = [C.c_int, C.c_int, _I32, _I32, _F64, _I32, _I32, _P(Opts)]
+        L.orc_amg_build_coloured.restype = C.c_void_p
+        L.orc_level_colour.argtypes = [C.c_void_p, C.c_int, C.c_int, _I32]
         L.orc_strength.argtypes = [C.c_int, C.c_int, _I32, _I32, _F64, _I32, C.c_double, _P(C.c_uint8)]
         L.orc_ilu_build.argtypes = [C.c_int] * 6 + [_I32, _I32, _F64]
         L.orc_ilu_build.restype = C.c_void_p
@@ -192,6 +198,12 @@ class Oracle:
     def hierarchy(self, which):
         return [self.level(which, l) for l in range(self.num_levels(which))]
 
+    def colour(self, which, lvl):
+        n = self.level(which, lvl)["n"]
+        col = np.empty(n, np.int32)
+        nc = lib().orc_level_colour(self.h, which, lvl, _p(col))
+        return col, nc
+
     def counters(self):
         out = (C.c_int64 * 4)()
         lib().orc_counters(self.h, out)
@@ -250,14 +262,16 @@ def fmix32(x):
 class Amg:
     """Standalone oracle AMG on a (multi-component) CSR matrix, for pins."""
 
-    def __init__(self, rp, ci, v, zb=None, **opts):
+    def __init__(self, rp, ci, v, zb=None, colour0=None, **opts):
         self.n = len(rp) - 1
         v = np.ascontiguousarray(v, np.float64)
         self.nc = 1 if v.ndim == 1 else v.shape[1]
         zb = np.zeros(self.n, np.int32) if zb is None else np.ascontiguousarray(zb, np.int32)
         o = default_opts(**opts)
-        self._keep = (np.ascontiguousarray(rp, np.int32), np.ascontiguousarray(ci, np.int32), v, zb)
-        self.h = lib().orc_amg_build(self.n, self.nc, _p(self._keep[0]), _p(self._keep[1]), _p(v), _p(zb), C.byref(o))
+        self._keep = (np.ascontiguousarray(rp, np.int32), np.ascontiguousarray(ci, np.int32), v, zb,
+                      None if colour0 is None else np.ascontiguousarray(colour0, np.int32))
+        self.h = lib().orc_amg_build_coloured(self.n, self.nc, _p(self._keep[0]), _p(self._keep[1]), _p(v), _p(zb),
+                                              _p(self._keep[4]), C.byref(o))
         if not self.h:
             raise RuntimeError("orc_amg_build failed")
 
@@ -271,6 +285,19 @@ class Amg:
         x = np.zeros_like(b)
         lib().orc_amg_vcycle(self.h, _p(b), _p(x))
         return x
+
+    def colour(self, lvl):
+        """(colour per row, number of colours) of a level's GS smoother (R-gs)."""
+        n = self.levels()[lvl]["n"]
+        col = np.empty(n, np.int32)
+        nc = lib().orc_amg_level_colour(self.h, lvl, _p(col))
+        return col, nc
+
+    def gs(self, lvl):
+        """(gs_block of the level -- 0 for multicolour --, hybrid l1 diagonal (n, nc)) of the GS smoother."""
+        n = self.levels()[lvl]["n"]
+        dh = np.zeros((n, self.nc))
+        return lib().orc_amg_level_gs(self.h, lvl, _p(dh)), dh
 
     def detail(self, lvl):
         """(MIS(2) state, phase-1 aggregate ids, omega per component) of a non-coarsest level."""

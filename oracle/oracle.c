@@ -123,6 +123,9 @@ typedef struct {
     mcsr P, R;
     double *lu[3]; int *piv[3];
     double omega[3];
+    int32_t *color; int ncolor;   /* GS smoother (R-gs): colour of each row, number of colours (max over blocks) */
+    int gs_block;                 /* 0: multicolour over the level (given colouring); B: hybrid, blocks of B rows */
+    double *dh[3];                /* hybrid l1 diagonal per component */
 } olevel;
 
 typedef struct {
@@ -478,7 +481,8 @@ static int make_coarsest(ohier *H, olevel *L)
 }
 
 /* a4: build the hierarchy (level 0 = a deep copy of the input operator) */
-static ohier *amg_build(const mcsr *A0, const int32_t *zb0, const orc_opts *o)
+static void hybrid_setup(olevel *L, int B);
+static ohier *amg_build(const mcsr *A0, const int32_t *zb0, const int32_t *colour0, const orc_opts *o)
 {
     ohier *H = (ohier *)xcalloc(1, sizeof(ohier));
     H->nc = A0->nc; H->o = *o;
@@ -493,6 +497,14 @@ static ohier *amg_build(const mcsr *A0, const int32_t *zb0, const orc_opts *o)
     for (;;) {
         L = &H->L[lvl];
         l1_diag(L);
+        if (o->amg_smoother == 1) {            /* R-gs: level 0 comes with a geometric colouring, the rest is hybrid */
+            L->color = (int32_t *)xmalloc(sizeof(int32_t) * (L->A.n + 1));
+            if (lvl == 0 && colour0) {
+                memcpy(L->color, colour0, sizeof(int32_t) * L->A.n);
+                L->ncolor = 0;
+                for (int i = 0; i < L->A.n; ++i) if (L->color[i] + 1 > L->ncolor) L->ncolor = L->color[i] + 1;
+            } else hybrid_setup(L, o->amg_gs_block > 0 ? o->amg_gs_block : 1024);
+        }
         int n = L->A.n;
         if (n <= o->amg_coarse_max || lvl == o->amg_max_levels - 1) {
             if (make_coarsest(H, L)) goto fail;
@@ -543,20 +555,118 @@ static void amg_free(ohier *H)
     for (int l = 0; l < 16; ++l) {
         olevel *L = &H->L[l];
         mcsr_free(&L->A); mcsr_free(&L->P); mcsr_free(&L->R);
-        free(L->zb); free(L->agg); free(L->st); free(L->ph1);
-        for (int c = 0; c < 3; ++c) { free(L->dl1[c]); free(L->lu[c]); free(L->piv[c]); }
+        free(L->zb); free(L->agg); free(L->st); free(L->ph1); free(L->color);
+        for (int c = 0; c < 3; ++c) { free(L->dl1[c]); free(L->lu[c]); free(L->piv[c]); free(L->dh[c]); }
     }
     free(H);
 }
 
+/* One Gauss-Seidel sweep on component c (R-gs), forward (colours ascending) or backward (descending).
+ * Level with a given (geometric) colouring -- level 0 of the coupled problem: multicolour GS over the whole
+ * level, x_i <- (b_i - sum_{j != i} a_ij x_j) / a_ii with the current x (a_ii = 0 leaves x_i).
+ * Other levels: hybrid l1-Gauss-Seidel (Baker, Falgout, Kolev, Yang 2011) with the "processor" a block
+ * of gs_block consecutive rows: inside the block multicolour GS in the block's own colouring, couplings to
+ * other blocks use the values from before the sweep and enter the l1 diagonal
+ *   d_i = a_ii + sign(a_ii) sum_{j outside the block} |a_ij|,   x_i <- x_i + (b_i - sum_j a_ij x~_j) / d_i
+ * (x~ = current in-block values, sweep-start values outside; R-l1 sign convention).  Rows of one colour are
+ * never coupled, so the order inside a colour is immaterial. */
+static void gs_sweep(const olevel *L, int c, const double *b, double *x, int backward)
+{
+    const mcsr *A = &L->A;
+    const int n = A->n;
+    if (!L->gs_block) {
+        for (int t = 0; t < L->ncolor; ++t) {
+            int col = backward ? L->ncolor - 1 - t : t;
+            for (int i = 0; i < n; ++i) {
+                if (L->color[i] != col) continue;
+                double s = b[i], d = 0.0;
+                for (int64_t q = A->rp[i]; q < A->rp[i + 1]; ++q) {
+                    if (A->ci[q] == i) d = A->v[c][q];
+                    else s = s - A->v[c][q] * x[A->ci[q]];
+                }
+                if (d != 0.0) x[i] = s / d;
+            }
+        }
+        return;
+    }
+    const int B = L->gs_block;
+    double *xo = (double *)xmalloc(sizeof(double) * (n + 1));
+    memcpy(xo, x, sizeof(double) * n);
+    for (int b0 = 0; b0 < n; b0 += B) {
+        const int b1 = b0 + B < n ? b0 + B : n;
+        for (int t = 0; t < L->ncolor; ++t) {
+            int col = backward ? L->ncolor - 1 - t : t;
+            for (int i = b0; i < b1; ++i) {
+                if (L->color[i] != col) continue;
+                double s = b[i], d = 0.0;
+                for (int64_t q = A->rp[i]; q < A->rp[i + 1]; ++q) {
+                    int j = A->ci[q];
+                    if (j == i) d = A->v[c][q];
+                    else s = s - A->v[c][q] * ((j >= b0 && j < b1) ? x[j] : xo[j]);
+                }
+                if (L->dh[c][i] != 0.0) x[i] = x[i] + (s - d * x[i]) / L->dh[c][i];
+            }
+        }
+    }
+    free(xo);
+}
+
+/* colouring of a hybrid level: each block of B rows coloured on its own, first fit in descending priority
+ * (fmix32(i), i) over the block's induced subgraph (row v takes the smallest colour none of its in-block
+ * neighbours coloured before it holds), and the l1 diagonal of the off-block couplings */
+static void hybrid_setup(olevel *L, int B)
+{
+    const mcsr *A = &L->A;
+    int n = A->n;
+    L->gs_block = B;
+    L->ncolor = 0;
+    prio_t *p = (prio_t *)xmalloc(sizeof(prio_t) * (B + 1));
+    uint8_t *used = (uint8_t *)xmalloc(4096);
+    for (int b0 = 0; b0 < n; b0 += B) {
+        const int b1 = b0 + B < n ? b0 + B : n, m = b1 - b0;
+        for (int i = 0; i < m; ++i) { p[i].h = fmix32((uint32_t)(b0 + i)); p[i].i = b0 + i; L->color[b0 + i] = -1; }
+        qsort(p, m, sizeof(prio_t), prio_desc);
+        for (int t = 0; t < m; ++t) {
+            int v = p[t].i;
+            memset(used, 0, 4096);
+            for (int64_t q = A->rp[v]; q < A->rp[v + 1]; ++q) {
+                int u = A->ci[q];
+                if (u != v && u >= b0 && u < b1 && L->color[u] >= 0 && L->color[u] < 4096) used[L->color[u]] = 1;
+            }
+            int cc = 0;
+            while (used[cc]) ++cc;
+            L->color[v] = cc;
+            if (cc + 1 > L->ncolor) L->ncolor = cc + 1;
+        }
+    }
+    free(p); free(used);
+    for (int c = 0; c < A->nc; ++c) {
+        L->dh[c] = (double *)xmalloc(sizeof(double) * (n + 1));
+        for (int i = 0; i < n; ++i) {
+            const int b0 = (i / B) * B, b1 = b0 + B < n ? b0 + B : n;
+            double aii = 0.0, l1 = 0.0;
+            for (int64_t q = A->rp[i]; q < A->rp[i + 1]; ++q) {
+                int j = A->ci[q];
+                if (j == i) aii = A->v[c][q];
+                else if (j < b0 || j >= b1) l1 = l1 + fabs(A->v[c][q]);
+            }
+            L->dh[c][i] = aii < 0.0 ? aii - l1 : aii + l1;
+        }
+    }
+}
+
 /* V(1,1)-cycle with l1-Jacobi, zero initial guess (R-cycle), component c:
- *   x = D^-1 b; r = b - A x; b_c = R r; x_c = cycle(b_c); x += P x_c; x += D^-1 (b - A x) */
+ *   x = D^-1 b; r = b - A x; b_c = R r; x_c = cycle(b_c); x += P x_c; x += D^-1 (b - A x)
+ * amg_smoother 1 (R-gs): x = forward GS sweep from 0; ... ; backward GS sweep on x */
 static void vcycle(const ohier *H, int lvl, int c, const double *b, double *x)
 {
     const olevel *L = &H->L[lvl];
     int n = L->A.n;
     if (L->coarsest) { dense_lu_solve(n, L->lu[c], L->piv[c], b, x); return; }
-    for (int i = 0; i < n; ++i) x[i] = L->dl1[c][i] != 0.0 ? b[i] / L->dl1[c][i] : 0.0;
+    static int lvmax = -2; if (lvmax == -2) { const char *e = getenv("ORC_GS_MAXLVL"); lvmax = e ? atoi(e) : 99; }
+    const int gs = H->o.amg_smoother == 1 && lvl <= lvmax;
+    if (gs) { for (int i = 0; i < n; ++i) x[i] = 0.0; gs_sweep(L, c, b, x, 0); }       /* forward GS from zero */
+    else for (int i = 0; i < n; ++i) x[i] = L->dl1[c][i] != 0.0 ? b[i] / L->dl1[c][i] : 0.0;
     double *r = (double *)xmalloc(sizeof(double) * (n + 1));
     memcpy(r, b, sizeof(double) * n);
     spmv_sub(&L->A, c, x, r);
@@ -569,9 +679,12 @@ static void vcycle(const ohier *H, int lvl, int c, const double *b, double *x)
         for (int64_t q = L->P.rp[i]; q < L->P.rp[i + 1]; ++q) s += L->P.v[c][q] * xc[L->P.ci[q]];
         x[i] += s;
     }
-    memcpy(r, b, sizeof(double) * n);
-    spmv_sub(&L->A, c, x, r);
-    for (int i = 0; i < n; ++i) if (L->dl1[c][i] != 0.0) x[i] += r[i] / L->dl1[c][i];
+    if (gs) gs_sweep(L, c, b, x, 1);                                                       /* backward GS */
+    else {
+        memcpy(r, b, sizeof(double) * n);
+        spmv_sub(&L->A, c, x, r);
+        for (int i = 0; i < n; ++i) if (L->dl1[c][i] != 0.0) x[i] += r[i] / L->dl1[c][i];
+    }
     free(r); free(bc); free(xc);
 }
 
@@ -785,6 +898,7 @@ void orc_default_opts(orc_opts *o)
     o->zblock = 16; o->tile_x = 16; o->tile_y = 16; o->tile_z = 16;
     o->rsl_iters = 2; o->fs_modulus_scale = 1.0;
     o->second_stage = 0; o->local_sweeps = 1;
+    o->amg_smoother = 0; o->amg_gs_block = 1024;
 }
 
 orc *orc_create(const orc_desc *d, const orc_opts *o)
@@ -895,8 +1009,14 @@ int orc_setup(orc *h)
             int kc = k < h->nz ? k : h->nz - 1;               /* node plane k -> cell plane min(k, nz-1) (R-zblock) */
             zb[n] = kc / h->o.zblock;
         }
-        h->mech = amg_build(&Asdc, zb, &h->o);
-        mcsr_free(&Asdc); free(zb);
+        /* R-gs: level-0 node colour = parity of (x, y, z), 8 colours (no two 27-point neighbours share one) */
+        int32_t *col0 = (int32_t *)xmalloc(sizeof(int32_t) * Nn);
+        for (int n = 0; n < Nn; ++n) {
+            int x = n % (h->nx + 1), y = (n / (h->nx + 1)) % (h->ny + 1), z = n / ((h->nx + 1) * (h->ny + 1));
+            col0[n] = (x & 1) + 2 * (y & 1) + 4 * (z & 1);
+        }
+        h->mech = amg_build(&Asdc, zb, col0, &h->o);
+        mcsr_free(&Asdc); free(zb); free(col0);
         if (!h->mech) return -2;
     } else {
         int N = 3 * Nn;
@@ -965,8 +1085,11 @@ int orc_setup(orc *h)
     if (h->o.pres_mode == 0) {
         int32_t *zb = (int32_t *)xmalloc(sizeof(int32_t) * Nc);
         for (int c = 0; c < Nc; ++c) zb[c] = (c / (h->nx * h->ny)) / h->o.zblock;
-        h->pres = amg_build(&h->Spp, zb, &h->o);
-        free(zb);
+        /* R-gs: level-0 cell colour = parity of x + y + z (red-black on the 7-point pattern of S_pp) */
+        int32_t *col0 = (int32_t *)xmalloc(sizeof(int32_t) * Nc);
+        for (int c = 0; c < Nc; ++c) col0[c] = (c % h->nx + (c / h->nx) % h->ny + c / (h->nx * h->ny)) & 1;
+        h->pres = amg_build(&h->Spp, zb, col0, &h->o);
+        free(zb); free(col0);
         if (!h->pres) return -3;
     } else {
         h->dense_pp = (double *)xcalloc((int64_t)Nc * Nc, sizeof(double));
@@ -1222,6 +1345,7 @@ static void level_export(ohier *H, int lvl, int32_t *A_rp, int32_t *A_ci, double
     if (P_v) for (int64_t q = 0; q < pz; ++q) for (int c = 0; c < nc; ++c) P_v[q * nc + c] = L->P.v[c][q];
 }
 void orc_level_sizes(orc *h, int which, int lvl, int64_t out[6]) { level_sizes(which ? h->pres : h->mech, lvl, out); }
+int orc_level_colour(orc *h, int which, int lvl, int32_t *colour) { return orc_amg_level_colour(which ? h->pres : h->mech, lvl, colour); }
 void orc_level_export(orc *h, int which, int lvl, int32_t *A_rp, int32_t *A_ci, double *A_v,
                       int32_t *agg, int32_t *P_rp, int32_t *P_ci, double *P_v, double *dl1)
 { level_export(which ? h->pres : h->mech, lvl, A_rp, A_ci, A_v, agg, P_rp, P_ci, P_v, dl1); }
@@ -1269,7 +1393,18 @@ void *orc_amg_build(int n, int nc, const int32_t *rp, const int32_t *ci, const d
     memcpy(A.rp, rp, sizeof(int32_t) * (n + 1)); memcpy(A.ci, ci, sizeof(int32_t) * rp[n]);
     for (int64_t q = 0; q < rp[n]; ++q) for (int c = 0; c < nc; ++c) A.v[c][q] = v[q * nc + c];
     orc_opts dflt; if (!o) { orc_default_opts(&dflt); o = &dflt; }
-    ohier *H = amg_build(&A, zb, o);
+    ohier *H = amg_build(&A, zb, NULL, o);
+    mcsr_free(&A);
+    return H;
+}
+void *orc_amg_build_coloured(int n, int nc, const int32_t *rp, const int32_t *ci, const double *v, const int32_t *zb,
+                             const int32_t *colour0, const orc_opts *o)
+{
+    mcsr A; mcsr_alloc(&A, n, n, nc, rp[n]);
+    memcpy(A.rp, rp, sizeof(int32_t) * (n + 1)); memcpy(A.ci, ci, sizeof(int32_t) * rp[n]);
+    for (int64_t q = 0; q < rp[n]; ++q) for (int c = 0; c < nc; ++c) A.v[c][q] = v[q * nc + c];
+    orc_opts dflt; if (!o) { orc_default_opts(&dflt); o = &dflt; }
+    ohier *H = amg_build(&A, zb, colour0, o);
     mcsr_free(&A);
     return H;
 }
@@ -1290,6 +1425,24 @@ void orc_amg_level_export(void *hier, int lvl, int32_t *A_rp, int32_t *A_ci, dou
                           int32_t *agg, int32_t *P_rp, int32_t *P_ci, double *P_v, double *dl1)
 { level_export((ohier *)hier, lvl, A_rp, A_ci, A_v, agg, P_rp, P_ci, P_v, dl1); }
 void orc_amg_free(void *hier) { amg_free((ohier *)hier); }
+/* pins: the GS colouring of a level (returns the number of colours; 0 when the smoother is not GS) and the
+ * hybrid l1 diagonal (NULL ok) */
+int orc_amg_level_colour(void *hier, int lvl, int32_t *colour)
+{
+    ohier *H = (ohier *)hier;
+    olevel *L = &H->L[lvl];
+    if (lvl >= H->nl || !L->color) return 0;
+    if (colour) memcpy(colour, L->color, sizeof(int32_t) * L->A.n);
+    return L->ncolor;
+}
+int orc_amg_level_gs(void *hier, int lvl, double *dh)
+{
+    ohier *H = (ohier *)hier;
+    olevel *L = &H->L[lvl];
+    if (lvl >= H->nl || !L->color) return -1;
+    if (dh && L->gs_block) for (int i = 0; i < L->A.n; ++i) for (int c = 0; c < H->nc; ++c) dh[(int64_t)i * H->nc + c] = L->dh[c][i];
+    return L->gs_block;
+}
 /* pins: the MIS(2) state, the phase-1 aggregates and omega_c of a non-coarsest level (returns -1 otherwise) */
 int orc_amg_level_detail(void *hier, int lvl, int32_t *st, int32_t *ph1, double *omega)
 {

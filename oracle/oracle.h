@@ -41,6 +41,10 @@ typedef struct {
     /* NEXT-f2: the second stage M_L */
     int second_stage;             /* 0: tile ILU(0) (option 2); 1: hybrid block Gauss-Seidel, tile = processor (option 1) */
     int local_sweeps;             /* steps 6-8 repeated this many times ("several sweeps"; 3 for the staircase) */
+    /* AMG smoother of both hierarchies (NEXT-f2/f3) */
+    int amg_smoother;             /* 0: l1-Jacobi (R-cycle, north_star); 1: Gauss-Seidel forward on the way down, backward on
+                                     the way up (R-gs): multicolour on level 0, hybrid l1-GS on the coarse levels */
+    int amg_gs_block;             /* R-gs hybrid levels: rows per "processor" block (1024) */
 } orc_opts;
 
 typedef struct {
@@ -80,6 +84,11 @@ void orc_amg_level_export(void *hier, int lvl, int32_t *A_rp, int32_t *A_ci, dou
                           int32_t *agg, int32_t *P_rp, int32_t *P_ci, double *P_v, double *dl1);
 void orc_amg_free(void *hier);
 int orc_amg_level_detail(void *hier, int lvl, int32_t *st, int32_t *ph1, double *omega);
+int orc_amg_level_colour(void *hier, int lvl, int32_t *colour);
+int orc_amg_level_gs(void *hier, int lvl, double *dh);     /* gs_block of the level (0: multicolour), hybrid l1 diagonal */
+void *orc_amg_build_coloured(int n, int nc, const int32_t *rp, const int32_t *ci, const double *v, const int32_t *zb,
+                             const int32_t *colour0, const orc_opts *o);
+int orc_level_colour(orc *h, int which, int lvl, int32_t *colour);
 int orc_strength(int n, int nc, const int32_t *rp, const int32_t *ci, const double *v, const int32_t *zb,
                  double theta, uint8_t *E);
 void *orc_ilu_build(int nx, int ny, int nz, int tx, int ty, int tz, const int32_t *rp, const int32_t *ci,
