@@ -79,7 +79,12 @@ typedef struct {
     int second_stage;            /* 0 tile ILU(0) (the paper's option 2, SPE10); 1 hybrid block Gauss-Seidel with the
                                     16^3 tile as the "processor" (option 1, the staircase) */
     int local_sweeps;            /* Algorithm 1 steps 6-8 repeated this many times (default 1; the staircase used 3) */
-    int reserved[2];
+    /* AMG smoother of both hierarchies */
+    int amg_smoother;            /* 0 l1-Jacobi (north_star; R-cycle); 1 Gauss-Seidel, forward on the way down and backward
+                                    on the way up (reading R-gs): multicolour GS on level 0 (parity colourings), hybrid
+                                    l1-GS on the coarse levels with blocks of amg_gs_block rows as the "processors";
+                                    single GPU only */
+    int amg_gs_block;            /* rows per hybrid block (default 1024, range [32, 1024]) */
 } tsp_options;
 
 /* BSR block matrix given to tsp_create (nrows block rows). */
@@ -228,6 +233,11 @@ tsp_status tsp_get_stats(tsp_handle h, tsp_stats *s);
 tsp_status tsp_level_sizes(tsp_handle h, int which, int lvl, int64_t out6[6]);
 tsp_status tsp_export_level(tsp_handle h, int which, int lvl, int32_t *A_rp, int32_t *A_ci, double *A_v,
                             int32_t *agg, int32_t *P_rp, int32_t *P_ci, double *P_v, double *dl1);
+
+/* Test hook (amg_smoother = 1): the Gauss-Seidel colouring of level `lvl` -- colour per row (int32, n) --
+ * and the level's gs_block (0: multicolour over the level; B: hybrid blocks of B rows) in *block.  Returns
+ * TSP_ERR_STATE when the smoother is not GS or the level is the coarsest. */
+tsp_status tsp_export_colour(tsp_handle h, int which, int lvl, int32_t *colour, int *block, int *ncolour);
 
 /* multi-GPU layout of a level: out3 = {distributed (rows split over ranks), global rows,
  * first global row of this rank}.  Replicated levels are complete on every rank. */

@@ -1027,6 +1027,7 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
             L.gh_b.alloc(g); L.gh_x.alloc(g);
         }
     }
+    gs_setup(c, H, nc);                    // Gauss-Seidel smoother layouts (amg_smoother = 1)
     dbg_mark(c, "sell+vectors", 99);
     TSP_CUDA(cudaStreamSynchronize(c.s));
 }
@@ -1125,6 +1126,28 @@ __global__ void __launch_bounds__(256) k_vc_post(int n, const int64_t *__restric
         xo[t] = x.own[t] + dinv[t] * (b[t] - acc[c]);
     }
 }
+// residual r = b - A x (Gauss-Seidel smoother: after the forward sweep)
+template <int NC>
+__global__ void __launch_bounds__(256) k_sell_resid(int n, const int64_t *__restrict__ off, const int32_t *__restrict__ col,
+                                                    const double *__restrict__ val, const double *__restrict__ b,
+                                                    const double *__restrict__ x, double *__restrict__ r)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int s = i >> 5, lane = i & 31;
+    double acc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+    const int64_t b0 = off[s], b1 = off[s + 1];
+#pragma unroll 2
+    for (int64_t slot = b0; slot < b1; ++slot) {
+        const int j = __ldcs(col + slot * 32 + lane);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c] = fma(__ldcs(val + (slot * NC + c) * 32 + lane), __ldg(x + (int64_t)j * NC + c), acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) r[(int64_t)i * NC + c] = b[(int64_t)i * NC + c] - acc[c];
+}
 // coarsest: x = A_c^-1 b per component
 template <int NC>
 __global__ void k_coarse(int n, const double *__restrict__ inv, const double *__restrict__ b, double *__restrict__ x)
@@ -1142,7 +1165,8 @@ __global__ void k_coarse(int n, const double *__restrict__ inv, const double *__
 // group of G lanes (G | 32) per row strides the row's entries (coalesced [q][c] values),
 // then a fixed shuffle tree inside the group.  32/G rows per warp keep several dependent
 // load chains in flight.
-// MODE 0: y = A x ; MODE 1: pre (x = D^-1 b, r = b - A D^-1 b) ; MODE 2: post (xo = x + D^-1 (b - A x))
+// MODE 0: y = A x ; MODE 1: pre (x = D^-1 b, r = b - A D^-1 b) ; MODE 2: post (xo = x + D^-1 (b - A x));
+// MODE 3: residual r = b - A x
 template <int NC, int MODE, bool D, int G>
 __global__ void __launch_bounds__(256) k_csr_vec(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
                                                  const double *__restrict__ v, GV dinv, GV b, GV x,
@@ -1177,6 +1201,7 @@ __global__ void __launch_bounds__(256) k_csr_vec(int n, const int32_t *__restric
         const int64_t t = (int64_t)i * NC + sub;
         if (MODE == 0) out1[t] = a;
         else if (MODE == 1) { out1[t] = b.own[t] * dinv.own[t]; out2[t] = b.own[t] - a; }
+        else if (MODE == 3) out1[t] = b.own[t] - a;
         else out1[t] = x.own[t] + dinv.own[t] * (b.own[t] - a);
     }
 }
@@ -1225,12 +1250,19 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     const GV gb = gv(b, n, L.dist ? L.gh_b.p : nullptr), gd = gv(L.dinv, n, ghd);
     const bool sym0 = mech && l == 0 && c.sym_sdc.ok;     // structured symmetric level 0 (sym.cu)
     const double bA0 = sym0 ? sym_bytes(c, 3) : bA;
+    const bool gs = c.o.amg_smoother == 1;   // Gauss-Seidel (gs.cu, R-gs): single GPU, never distributed
     prof_begin(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P);
-    if (sym0) sym_vcycle_pre(c, n, gd, gb, L.x2, L.r);
+    if (gs) {
+        gs_sweep<NC>(c, L, false, b, nullptr, L.x2);                      // forward sweep from zero
+        if (sym0) sym_vcycle_resid(c, n, b, gv(L.x2, n), L.r);
+        else if (wA) csr_vec<NC, 3, false>(wA, c.s, n, L.A, gv(nullptr, 0), gv(b, n), gv(L.x2, n), L.r, nullptr);
+        else if (n) k_sell_resid<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sA.off, L.sA.col, L.sA.val, b, L.x2, L.r);
+    }
+    else if (sym0) sym_vcycle_pre(c, n, gd, gb, L.x2, L.r);
     else if (wA) (L.dist ? csr_vec<NC, 1, true> : csr_vec<NC, 1, false>)(wA, c.s, n, L.A, gd, gb, gv(nullptr, 0), L.x2, L.r);
     else if (n) (L.dist ? k_vc_pre<NC, true> : k_vc_pre<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
         n, L.sA.off, L.sA.col, L.sA.val, gd, gb, L.x2, L.r);
-    prof_end(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P, bA0 + 4 * vec);
+    prof_end(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P, gs ? gs_sweep_bytes(L, NC) + bA0 + 3 * vec : bA0 + 4 * vec);
     // restriction (local rows of R); a replicated next level is gathered on every rank
     Level &Lc = H.L[l + 1];
     const bool gather = L.dist && !L.next_dist;
@@ -1256,11 +1288,12 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     if (L.dist) halo_exchange(c, *L.hp, NC, L.x2, L.gh_x);
     const GV gx = gv(L.x2, n, L.dist ? L.gh_x.p : nullptr);
     prof_begin(c, mech ? PK_VC_POST_U : PK_VC_POST_P);
-    if (sym0) sym_vcycle_post(c, n, L.dinv, b, gx, xout);
+    if (gs) gs_sweep<NC>(c, L, true, b, L.x2, xout);                      // backward sweep
+    else if (sym0) sym_vcycle_post(c, n, L.dinv, b, gx, xout);
     else if (wA) (L.dist ? csr_vec<NC, 2, true> : csr_vec<NC, 2, false>)(wA, c.s, n, L.A, gv(L.dinv, n), gv(b, n), gx, xout, nullptr);
     else if (n) (L.dist ? k_vc_post<NC, true> : k_vc_post<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
         n, L.sA.off, L.sA.col, L.sA.val, L.dinv, b, gx, xout);
-    prof_end(c, mech ? PK_VC_POST_U : PK_VC_POST_P, bA0 + 4 * vec);
+    prof_end(c, mech ? PK_VC_POST_U : PK_VC_POST_P, gs ? gs_sweep_bytes(L, NC) : bA0 + 4 * vec);
     c.launches += 4;
 }
 

@@ -214,6 +214,7 @@ tsp_status tsp_default_options(tsp_options *o)
     o->tile_x = o->tile_y = o->tile_z = 16;
     o->rsl_iters = 2; o->fs_modulus_scale = 1.0;
     o->second_stage = 0; o->local_sweeps = 1;
+    o->amg_smoother = 0; o->amg_gs_block = 1024;
     return TSP_OK;
 }
 
@@ -249,6 +250,8 @@ tsp_status tsp_create(tsp_handle *out, const tsp_desc *d)
     if (c->o.rsl_iters <= 0) c->o.rsl_iters = 2;
     if (c->o.local_sweeps <= 0) c->o.local_sweeps = 1;
     TSP_REQUIRE(c->o.second_stage == 0 || c->o.second_stage == 1, TSP_ERR_INVALID_ARG, "second_stage must be 0 (ILU0) or 1 (BGS)");
+    if (c->o.amg_gs_block <= 0) c->o.amg_gs_block = 1024;
+    TSP_REQUIRE(c->o.amg_smoother == 0 || c->o.amg_smoother == 1, TSP_ERR_INVALID_ARG, "amg_smoother must be 0 (l1-Jacobi) or 1 (GS)");
     if (!(c->o.fs_modulus_scale > 0)) c->o.fs_modulus_scale = 1.0;
     TSP_REQUIRE(c->o.cpr_mode == 0 || c->o.cpr_mode == 1, TSP_ERR_INVALID_ARG, "cpr_mode must be 0 (quasi) or 1 (true IMPES)");
     TSP_REQUIRE(c->o.aps_mode == 0 || c->o.aps_mode == 1, TSP_ERR_INVALID_ARG, "aps_mode must be 0 (full) or 1 (diagonal)");
@@ -388,6 +391,20 @@ tsp_status tsp_solve(tsp_handle h, const double *b, double *x, const tsp_solve_o
         if (info) *info = inf;
         return inf.status;
     }
+}
+
+tsp_status tsp_export_colour(tsp_handle h, int which, int lvl, int32_t *colour, int *block, int *ncolour)
+{
+    if (!h) { set_error("null handle"); return TSP_ERR_INVALID_ARG; }
+    API_BEGIN
+    Hier &H = which ? h->pres : h->mech;
+    TSP_REQUIRE(lvl >= 0 && lvl < (int)H.L.size(), TSP_ERR_INVALID_ARG, "no such level");
+    const Level &L = H.L[lvl];
+    TSP_REQUIRE(h->o.amg_smoother == 1 && !L.coarsest, TSP_ERR_STATE, "no Gauss-Seidel colouring on this level");
+    if (block) *block = L.gs_block;
+    if (ncolour) *ncolour = L.ncolor;
+    if (colour) gs_export_colour(*h, L, colour);
+    API_END
 }
 
 tsp_status tsp_variant_counts(tsp_handle h, int64_t out[TSP_NVARIANTS])

@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(256) k_op_node_sym(SymGeo g, const double *__r
 }
 
 // level-0 SDC smoother (3 scalar components on one node graph), MODE 1 pre: x = D^-1 b, r = b - A D^-1 b;
-// MODE 2 post: xo = x + D^-1 (b - A x)
+// MODE 2 post: xo = x + D^-1 (b - A x); MODE 3 residual (Gauss-Seidel smoother): out1 = b - A x
 template <int ASYM, int MODE, bool D>
 __global__ void __launch_bounds__(256) k_vc_sym(SymGeo g, const double *__restrict__ vs, const double *__restrict__ vf,
                                                 const double *__restrict__ gl, GV dinv, GV b, GV xin, double *__restrict__ out1,
@@ -212,6 +212,8 @@ __global__ void __launch_bounds__(256) k_vc_sym(SymGeo g, const double *__restri
             const double bi = b.own[t];
             out1[t] = bi * dinv.own[t];
             out2[t] = bi - acc[cc];
+        } else if (MODE == 3) {
+            out1[t] = b.own[t] - acc[cc];
         } else {
             out1[t] = xin.own[t] + dinv.own[t] * (b.own[t] - acc[cc]);
         }
@@ -330,6 +332,21 @@ bool sym_vcycle_post(Ctx &c, int n, const double *dinv, const double *b, const G
 #define VCS(A)                                                                                                    \
     (c.comm ? k_vc_sym<A, 2, true> : k_vc_sym<A, 2, false>)<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(                        \
         g, S.val_s, S.val_f, S.gl, gv(dinv, n), gv(b, n), x, xo, nullptr)
+    if (n) {
+        if (c.sym_asym == 0) VCS(0u);
+        else VCS(kAsymZ);
+    }
+#undef VCS
+    return true;
+}
+bool sym_vcycle_resid(Ctx &c, int n, const double *b, const GV &x, double *r)
+{
+    if (!c.sym_sdc.ok || n != c.Nn) return false;
+    const SymGeo g = sym_geo(c);
+    const Sym27 &S = c.sym_sdc;
+#define VCS(A)                                                                                                    \
+    (c.comm ? k_vc_sym<A, 3, true> : k_vc_sym<A, 3, false>)<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(                        \
+        g, S.val_s, S.val_f, S.gl, gv(nullptr, 0), gv(b, n), x, r, nullptr)
     if (n) {
         if (c.sym_asym == 0) VCS(0u);
         else VCS(kAsymZ);

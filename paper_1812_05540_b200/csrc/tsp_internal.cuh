@@ -183,6 +183,15 @@ struct Level {
     DBuf<double> gh_b, gh_x;           // ghost buffers for b and x (dist)
     std::vector<int64_t> rep_counts, rep_offs;  // next level replicated: rows per rank (allgather)
     DBuf<int64_t> rep_offs_d;          // rep_offs on the device (uploaded once at setup)
+    // Gauss-Seidel smoother (tsp_options.amg_smoother = 1, gs.cu): level 0 multicolour (gs_block = 0), coarse
+    // levels hybrid l1-GS over blocks of gs_block rows
+    int gs_block = 0, ncolor = 0;
+    DBuf<int16_t> gsc;                 // hybrid: colour of each row inside its block
+    DBuf<double> dh;                   // hybrid: l1 diagonal per (row, component)
+    Sell sAc;                          // multicolour: colour-ordered SELL copy of A (a slice holds one colour)
+    DBuf<int32_t> gperm;               // multicolour: SELL row -> level row (-1 = padding)
+    std::vector<int64_t> cslice;       // multicolour: first SELL row of each colour (+ end)
+    DBuf<double> diag;                 // multicolour: a_ii per (row, component)
     DBuf<double> rep_buf;              // padded allgather buffer
     Csr A;                        // level operator (local column ids if dist)
     DBuf<int32_t> zb;             // z-block per row
@@ -314,6 +323,12 @@ void setup_mech(Ctx &c);
 void setup_flow(Ctx &c);
 void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_halo, int64_t row_off0, int64_t nglob0);
 void amg_vcycle(Ctx &c, Hier &H, const double *b, double *x, bool mech);
+// gs.cu: Gauss-Seidel smoother (R-gs)
+void gs_setup(Ctx &c, Hier &H, int nc);
+template <int NC> void gs_sweep(Ctx &c, Level &L, bool backward, const double *b, const double *xin, double *xout);
+double gs_sweep_bytes(const Level &L, int nc);
+void gs_export_colour(Ctx &c, const Level &L, int32_t *host_out);
+bool sym_vcycle_resid(Ctx &c, int n, const double *b, const GV &x, double *r);   // level-0 SDC r = b - A x, if sym_sdc.ok
 void ilu_setup(Ctx &c, const double *sff_vals);
 void ilu_apply_fused(Ctx &c, const double *yf, const double *zs, const double *zp, double *zf_out);
 

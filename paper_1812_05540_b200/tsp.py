@@ -32,7 +32,7 @@ class tsp_options(C.Structure):
                 ("zblock", C.c_int), ("tile_x", C.c_int), ("tile_y", C.c_int), ("tile_z", C.c_int),
                 ("replicate_rows", C.c_int), ("cpr_mode", C.c_int), ("aps_mode", C.c_int), ("fs_mode", C.c_int),
                 ("rsl_iters", C.c_int), ("fs_modulus_scale", C.c_double), ("second_stage", C.c_int),
-                ("local_sweeps", C.c_int), ("reserved", C.c_int * 2)]
+                ("local_sweeps", C.c_int), ("amg_smoother", C.c_int), ("amg_gs_block", C.c_int)]
 
 
 class tsp_bsr(C.Structure):
@@ -151,6 +151,7 @@ def lib():
         L.tsp_partition.argtypes = [C.c_int] * 6 + [_P(C.c_int64)]
         L.tsp_level_dist.argtypes = [C.c_void_p, C.c_int, C.c_int, _P(C.c_int64)]
         L.tsp_variant_counts.argtypes = [C.c_void_p, _P(C.c_int64)]
+        L.tsp_export_colour.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, _P(C.c_int), _P(C.c_int)]
         if L.tsp_abi_version() != 3:
             raise RuntimeError("libtsp ABI version mismatch")
         _LIB = L
@@ -161,7 +162,7 @@ EXPORTED = ["tsp_abi_version", "tsp_last_error", "tsp_default_options", "tsp_cre
             "tsp_apply_preconditioner", "tsp_apply_operator", "tsp_solve", "tsp_default_solve_opts",
             "tsp_get_stats", "tsp_level_sizes", "tsp_export_level", "tsp_prof_enable", "tsp_prof_read",
             "tsp_prof_classes", "tsp_export_cpr", "tsp_destroy", "tsp_nccl_unique_id", "tsp_local_world_create", "tsp_local_world_destroy",
-            "tsp_partition", "tsp_level_dist", "tsp_variant_counts"]
+            "tsp_partition", "tsp_level_dist", "tsp_variant_counts", "tsp_export_colour"]
 
 # include/tsp.h TSP_VAR_* order
 VARIANTS = ["spgemm_hs64", "spgemm_hs128", "spgemm_hs512", "spgemm_hs4096", "spgemm_g4", "spgemm_g8", "spgemm_g32",
@@ -330,6 +331,14 @@ class Tsp:
         out["rows"] = [list(s.rows[w])[: s.levels[w]] for w in range(2)]
         out["nnz"] = [list(s.nnz[w])[: s.levels[w]] for w in range(2)]
         return out
+
+    def colour(self, which, lvl):
+        """Test hook: (colour per row, gs_block, number of colours) of a level's Gauss-Seidel smoother."""
+        n = self.level(which, lvl)["n"]
+        col = np.empty(n, np.int32)
+        blk, nc = C.c_int(0), C.c_int(0)
+        _check(lib().tsp_export_colour(self.h, which, lvl, col.ctypes.data, C.byref(blk), C.byref(nc)), "tsp_export_colour")
+        return col, blk.value, nc.value
 
     def variants(self):
         """Test hook: kernel-variant choices of this handle's setups (include/tsp.h tsp_variant_counts)."""
