@@ -181,7 +181,8 @@ constexpr int kGsMaxColours = 256;
 // is coloured once all its higher-priority in-block neighbours are, with the smallest colour none of them holds
 // (= the sequential first fit in descending priority)
 __global__ void __launch_bounds__(kGsThreads) k_gs_colour(int n, int B, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
-                                                          int16_t *__restrict__ col, int *__restrict__ maxcol)
+                                                          int16_t *__restrict__ col, int *__restrict__ maxcol,
+                                                          int32_t *__restrict__ coff, int32_t *__restrict__ order)
 {
     __shared__ int16_t cs[kGsMaxBlock];
     const int b0 = blockIdx.x * B, b1 = min(n, b0 + B);
@@ -221,6 +222,25 @@ __global__ void __launch_bounds__(kGsThreads) k_gs_colour(int n, int B, const in
         if (!__syncthreads_or(left)) break;
     }
     for (int r = b0 + threadIdx.x; r < b1; r += blockDim.x) col[r] = cs[r - b0];
+    // rows of the block grouped by colour (the sweep's warps take a colour's rows from this list; the order
+    // inside a colour is immaterial -- no two rows of a colour are coupled)
+    __shared__ int cnt[kGsMaxColours + 1];
+    for (int k = threadIdx.x; k <= kGsMaxColours; k += blockDim.x) cnt[k] = 0;
+    __syncthreads();
+    for (int r = b0 + threadIdx.x; r < b1; r += blockDim.x) {
+        const int k = cs[r - b0];
+        if (k < kGsMaxColours) atomicAdd(&cnt[k + 1], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int k = 0; k < kGsMaxColours; ++k) cnt[k + 1] += cnt[k];
+    __syncthreads();
+    for (int k = threadIdx.x; k <= kGsMaxColours; k += blockDim.x) coff[(int64_t)blockIdx.x * (kGsMaxColours + 1) + k] = b0 + cnt[k];
+    __syncthreads();
+    for (int r = b0 + threadIdx.x; r < b1; r += blockDim.x) {
+        const int k = cs[r - b0];
+        if (k < kGsMaxColours) order[b0 + atomicAdd(&cnt[k], 1)] = r;
+    }
 }
 // hybrid l1 diagonal d_i = a_ii + sign(a_ii) sum_{j outside i's block} |a_ij| per component
 __global__ void k_gs_dh(int n, int nc, int B, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
@@ -238,42 +258,57 @@ __global__ void k_gs_dh(int n, int nc, int B, const int32_t *__restrict__ rp, co
     }
     dh[t] = aii < 0.0 ? aii - l1 : aii + l1;
 }
-// one hybrid sweep: block of B rows per CTA, xs = the block's x in shared memory; ZERO: from x = 0 (no xin)
+// one hybrid sweep: block of B rows per CTA, xs = the block's x in shared memory; ZERO: from x = 0 (no xin).
+// Per colour, a warp per row: the lanes stride the row's entries, a shuffle tree sums them, lane 0 updates.
+constexpr int kGsSweepThreads = 1024;   // a warp per row of the current colour: 32 rows of a colour in flight
 template <int NC, bool ZERO>
-__global__ void __launch_bounds__(kGsThreads) k_gs_hyb(int n, int B, int ncol, int backward, const int32_t *__restrict__ rp,
+__global__ void __launch_bounds__(kGsSweepThreads) k_gs_hyb(int n, int B, int ncol, int backward, const int32_t *__restrict__ rp,
                                                        const int32_t *__restrict__ ci, const double *__restrict__ v,
-                                                       const double *__restrict__ dh, const int16_t *__restrict__ col,
-                                                       const double *__restrict__ b, const double *__restrict__ xin,
-                                                       double *__restrict__ xout)
+                                                       const double *__restrict__ dh, const int32_t *__restrict__ coff,
+                                                       const int32_t *__restrict__ order, const double *__restrict__ b,
+                                                       const double *__restrict__ xin, double *__restrict__ xout)
 {
     __shared__ double xs[kGsMaxBlock * NC];
     const int b0 = blockIdx.x * B, b1 = min(n, b0 + B);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
     for (int t = threadIdx.x; t < (b1 - b0) * NC; t += blockDim.x) xs[t] = ZERO ? 0.0 : xin[(int64_t)b0 * NC + t];
     __syncthreads();
+    const int32_t *co = coff + (int64_t)blockIdx.x * (kGsMaxColours + 1);
     for (int k = 0; k < ncol; ++k) {
         const int cl = backward ? ncol - 1 - k : k;
-        for (int r = b0 + threadIdx.x; r < b1; r += blockDim.x) {
-            if (col[r] != cl) continue;
+        const int o0 = co[cl], o1 = co[cl + 1];
+        for (int o = o0 + warp; o < o1; o += nwarp) {
+            const int r = order[o];
             double s[NC], d[NC];
 #pragma unroll
-            for (int c = 0; c < NC; ++c) { s[c] = b[(int64_t)r * NC + c]; d[c] = 0.0; }
-            for (int64_t q = rp[r]; q < rp[r + 1]; ++q) {
-                const int j = ci[q];
+            for (int c = 0; c < NC; ++c) { s[c] = 0.0; d[c] = 0.0; }
+            const int64_t q1 = rp[r + 1];
+#pragma unroll 2
+            for (int64_t q = rp[r] + lane; q < q1; q += 32) {
+                const int j = __ldg(ci + q);
                 const bool inb = j >= b0 && j < b1;
 #pragma unroll
                 for (int c = 0; c < NC; ++c) {
-                    const double a = v[q * NC + c];
+                    const double a = __ldg(v + q * NC + c);
                     if (j == r) d[c] = a;
-                    else if (inb) s[c] -= a * xs[(j - b0) * NC + c];
-                    else if (!ZERO) s[c] -= a * xin[(int64_t)j * NC + c];
+                    else if (inb) s[c] = fma(a, xs[(j - b0) * NC + c], s[c]);
+                    else if (!ZERO) s[c] = fma(a, __ldg(xin + (int64_t)j * NC + c), s[c]);
                 }
             }
 #pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                const double dd = dh[(int64_t)r * NC + c];
-                double &xr = xs[(r - b0) * NC + c];
-                if (dd != 0.0) xr = xr + (s[c] - d[c] * xr) / dd;
-            }
+            for (int c = 0; c < NC; ++c)
+#pragma unroll
+                for (int off = 16; off; off >>= 1) {
+                    s[c] += __shfl_xor_sync(0xffffffffu, s[c], off);
+                    d[c] += __shfl_xor_sync(0xffffffffu, d[c], off);
+                }
+            if (lane == 0)
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const double dd = dh[(int64_t)r * NC + c];
+                    double &xr = xs[(r - b0) * NC + c];
+                    if (dd != 0.0) xr = xr + ((b[(int64_t)r * NC + c] - s[c]) - d[c] * xr) / dd;
+                }
         }
         __syncthreads();
     }
@@ -289,7 +324,9 @@ static void gs_setup_hybrid(Ctx &c, Level &L, int nc)
     L.dh.alloc((size_t)std::max(n, 1) * nc);
     DBuf<int> mx; mx.alloc(1); mx.zero(c.s);
     const int nb = (n + B - 1) / B;
-    if (nb) k_gs_colour<<<nb, kGsThreads, 0, c.s>>>(n, B, L.A.rp, L.A.ci, L.gsc, mx);
+    L.gcoff.alloc((size_t)std::max(nb, 1) * (kGsMaxColours + 1));
+    L.gorder.alloc(std::max(n, 1));
+    if (nb) k_gs_colour<<<nb, kGsThreads, 0, c.s>>>(n, B, L.A.rp, L.A.ci, L.gsc, mx, L.gcoff, L.gorder);
     if (n) k_gs_dh<<<grid_for((int64_t)n * nc, 256), 256, 0, c.s>>>(n, nc, B, L.A.rp, L.A.ci, L.A.v, L.dh);
     int m = -1;
     TSP_CUDA(cudaMemcpyAsync(&m, mx.p, sizeof(int), cudaMemcpyDeviceToHost, c.s));
@@ -332,8 +369,10 @@ void gs_sweep(Ctx &c, Level &L, bool backward, const double *b, const double *xi
         }
     } else {
         const int nb = (n + L.gs_block - 1) / L.gs_block;
-        if (!xin) k_gs_hyb<NC, true><<<nb, kGsThreads, 0, c.s>>>(n, L.gs_block, L.ncolor, backward, L.A.rp, L.A.ci, L.A.v, L.dh, L.gsc, b, nullptr, xout);
-        else k_gs_hyb<NC, false><<<nb, kGsThreads, 0, c.s>>>(n, L.gs_block, L.ncolor, backward, L.A.rp, L.A.ci, L.A.v, L.dh, L.gsc, b, xin, xout);
+        if (!xin) k_gs_hyb<NC, true><<<nb, kGsSweepThreads, 0, c.s>>>(n, L.gs_block, L.ncolor, backward, L.A.rp, L.A.ci, L.A.v, L.dh,
+                                                                 L.gcoff, L.gorder, b, nullptr, xout);
+        else k_gs_hyb<NC, false><<<nb, kGsSweepThreads, 0, c.s>>>(n, L.gs_block, L.ncolor, backward, L.A.rp, L.A.ci, L.A.v, L.dh,
+                                                             L.gcoff, L.gorder, b, xin, xout);
         c.launches++;
     }
     TSP_CUDA(cudaGetLastError());

@@ -188,6 +188,7 @@ struct Level {
     int gs_block = 0, ncolor = 0;
     DBuf<int16_t> gsc;                 // hybrid: colour of each row inside its block
     DBuf<double> dh;                   // hybrid: l1 diagonal per (row, component)
+    DBuf<int32_t> gcoff, gorder;       // hybrid: per block, first position of each colour in gorder (rows by colour)
     Sell sAc;                          // multicolour: colour-ordered SELL copy of A (a slice holds one colour)
     DBuf<int32_t> gperm;               // multicolour: SELL row -> level row (-1 = padding)
     std::vector<int64_t> cslice;       // multicolour: first SELL row of each colour (+ end)

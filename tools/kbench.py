@@ -13,7 +13,8 @@ from paper_1812_05540_b200 import Tsp  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C5"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 pb = synth.generate(cfg)
-g = Tsp(pb).setup()
+opts = {k: int(v) for k, v in (kv.split("=") for kv in filter(None, os.environ.get("KB_OPTS", "").split(",")))}
+g = Tsp(pb, **opts).setup()
 v = torch.from_numpy(np.random.default_rng(1).uniform(-1, 1, pb.n)).cuda()
 y = torch.empty_like(v)
 for _ in range(3):
