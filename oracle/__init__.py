@@ -58,6 +58,8 @@ def lib():
         L.orc_create.restype = C.c_void_p
         L.orc_destroy.argtypes = [C.c_void_p]
         L.orc_setup.argtypes = [C.c_void_p]
+        L.orc_setup_flow.argtypes = [C.c_void_p, C.c_int]
+        L.orc_update_values.argtypes = [C.c_void_p, _P(Desc)]
         L.orc_apply.argtypes = [C.c_void_p, _F64, _F64]
         L.orc_apply_operator.argtypes = [C.c_void_p, _F64, _F64]
         L.orc_solve.argtypes = [C.c_void_p, _F64, _F64, C.c_double, C.c_int, C.c_int, _P(Info)]
@@ -156,6 +158,22 @@ class Oracle:
         rc = lib().orc_setup(self.h)
         if rc != 0:
             raise RuntimeError(f"orc_setup failed ({rc})")
+        return self
+
+    def update_values(self, pb):
+        """A Newton step's new values on the same patterns (orc_update_values)."""
+        keep = [np.ascontiguousarray(x) for x in (
+            pb.uu_rowptr, pb.uu_col, pb.uu_val, pb.uf_rowptr, pb.uf_col, pb.uf_val,
+            pb.fu_rowptr, pb.fu_col, pb.fu_val, pb.ff_rowptr, pb.ff_col, pb.ff_val, pb.fs)]
+        d = Desc(pb.nx, pb.ny, pb.nz, *[_p(x) for x in keep])
+        if lib().orc_update_values(self.h, C.byref(d)) != 0:
+            raise ValueError("orc_update_values: the patterns changed")
+        return self
+
+    def setup_flow(self, refresh=False):
+        rc = lib().orc_setup_flow(self.h, int(refresh))
+        if rc != 0:
+            raise RuntimeError(f"orc_setup_flow failed ({rc})")
         return self
 
     def apply(self, v):

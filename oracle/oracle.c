@@ -125,6 +125,7 @@ typedef struct {
     double omega[3];
     int32_t *color; int ncolor;   /* GS smoother (R-gs): colour of each row, number of colours (max over blocks) */
     int gs_block;                 /* 0: multicolour over the level (given colouring); B: hybrid, blocks of B rows */
+    uint8_t *E;                   /* symmetrised strength flags per stored entry (kept for the frozen refresh) */
     double *dh[3];                /* hybrid l1 diagonal per component */
 } olevel;
 
@@ -482,6 +483,7 @@ static int make_coarsest(ohier *H, olevel *L)
 
 /* a4: build the hierarchy (level 0 = a deep copy of the input operator) */
 static void hybrid_setup(olevel *L, int B);
+static int make_coarsest(ohier *H, olevel *L);
 static ohier *amg_build(const mcsr *A0, const int32_t *zb0, const int32_t *colour0, const orc_opts *o)
 {
     ohier *H = (ohier *)xcalloc(1, sizeof(ohier));
@@ -539,7 +541,8 @@ static ohier *amg_build(const mcsr *A0, const int32_t *zb0, const int32_t *colou
         Lc->zb = (int32_t *)xmalloc(sizeof(int32_t) * (L->nagg + 1));
         for (int i = 0; i < n; ++i) if (st[i] == ST_ROOT) Lc->zb[L->agg[i]] = L->zb[i];
         L->st = st;
-        free(E); free(grp); free(gci); free(hs);
+        L->E = E;
+        free(grp); free(gci); free(hs);
         ++lvl;
     }
     H->nl = lvl + 1;
@@ -555,7 +558,7 @@ static void amg_free(ohier *H)
     for (int l = 0; l < 16; ++l) {
         olevel *L = &H->L[l];
         mcsr_free(&L->A); mcsr_free(&L->P); mcsr_free(&L->R);
-        free(L->zb); free(L->agg); free(L->st); free(L->ph1); free(L->color);
+        free(L->zb); free(L->agg); free(L->st); free(L->ph1); free(L->color); free(L->E);
         for (int c = 0; c < 3; ++c) { free(L->dl1[c]); free(L->lu[c]); free(L->piv[c]); free(L->dh[c]); }
     }
     free(H);
@@ -653,6 +656,41 @@ static void hybrid_setup(olevel *L, int B)
             L->dh[c][i] = aii < 0.0 ? aii - l1 : aii + l1;
         }
     }
+}
+
+/* Frozen-aggregation refresh (NEXT-f1, reading R-refresh): the values of A_0 changed, its pattern did not.
+ * Strength graphs, MIS(2), aggregates, the P / R / A_c patterns and the GS colourings of the previous build are
+ * kept; recomputed in the build's own order and arithmetic: l1 norms, the filtered diagonal with the KEPT strength
+ * flags, rho and omega, P's values, R = P^T, A_c = R (A P), the hybrid l1 diagonals and the coarsest LU. */
+static int amg_refresh(ohier *H, const mcsr *A0)
+{
+    olevel *L0 = &H->L[0];
+    if (A0->n != L0->A.n || mnnz(A0) != mnnz(&L0->A)) return -1;
+    for (int64_t q = 0; q < mnnz(A0); ++q) if (A0->ci[q] != L0->A.ci[q]) return -1;
+    for (int c = 0; c < A0->nc; ++c) memcpy(L0->A.v[c], A0->v[c], sizeof(double) * mnnz(A0));
+    H->perturbed = 0;
+    for (int lvl = 0; lvl < H->nl; ++lvl) {
+        olevel *L = &H->L[lvl];
+        for (int c = 0; c < 3; ++c) { free(L->dl1[c]); L->dl1[c] = NULL; free(L->dh[c]); L->dh[c] = NULL; }
+        l1_diag(L);
+        if (L->gs_block) hybrid_setup(L, L->gs_block);
+        if (L->coarsest) {
+            for (int c = 0; c < 3; ++c) { free(L->lu[c]); L->lu[c] = NULL; free(L->piv[c]); L->piv[c] = NULL; }
+            if (make_coarsest(H, L)) return -2;
+            break;
+        }
+        mcsr_free(&L->P); mcsr_free(&L->R);
+        build_P(L, L->E);
+        transpose(&L->P, &L->R);
+        mcsr AP; spgemm(&L->A, &L->P, &AP);
+        mcsr Ac; spgemm(&L->R, &AP, &Ac);
+        mcsr_free(&AP);
+        olevel *Lc = &H->L[lvl + 1];
+        if (Ac.n != Lc->A.n || mnnz(&Ac) != mnnz(&Lc->A)) { mcsr_free(&Ac); return -3; }
+        mcsr_free(&Lc->A);
+        Lc->A = Ac;
+    }
+    return 0;
 }
 
 /* V(1,1)-cycle with l1-Jacobi, zero initial guess (R-cycle), component c:
@@ -992,7 +1030,7 @@ static void rsl_diag(orc *h, double *out)
 int orc_setup(orc *h)
 {
     double t0 = now_s();
-    int Nc = h->Nc, Nn = h->Nn;
+    int Nn = h->Nn;
     /* ---- a2 + a4 (mechanics): M_uu^-1 = amg(A_uu^SDC), three components on one
      *      node graph */
     if (h->o.mech_mode == 0) {
@@ -1025,6 +1063,27 @@ int orc_setup(orc *h)
         dense_from_bsr(&h->uu, h->dense_uu, N);
         dense_lu(N, h->dense_uu, h->piv_uu, &h->perturbed);
     }
+    (void)t0;
+    return orc_setup_flow(h, 0);
+}
+
+/* the flow phase (rows a1, a3, a4 pressure, a5; redone per Newton step).  refresh = 1: the values
+ * changed since the last flow setup, the patterns did not; the pressure hierarchy keeps its structure (frozen
+ * aggregation, amg_refresh) and only its values are recomputed (NEXT-f1, reading R-refresh). */
+int orc_setup_flow(orc *h, int refresh)
+{
+    int Nc = h->Nc, Nn = h->Nn;
+    if (refresh && (!h->pres || h->o.pres_mode != 0)) return -4;
+    /* products of a previous flow phase */
+    mcsr *m[] = {&h->Ass, &h->Asp, &h->Aps, &h->App, &h->Asp_fs, &h->App_fs, &h->Asu, &h->Apu, &h->Spp};
+    for (size_t k = 0; k < sizeof(m) / sizeof(m[0]); ++k) mcsr_free(m[k]);
+    bsr_free(&h->Sff);
+    free(h->Dss); free(h->Dps); free(h->fs_eff); h->Dss = h->Dps = h->fs_eff = NULL;
+    orc_ilu_free(h->ilu); h->ilu = NULL;
+    free(h->dense_pp); free(h->piv_pp); free(h->dense_ff); free(h->piv_ff); free(h->dense_schur); free(h->piv_schur);
+    h->dense_pp = h->dense_ff = h->dense_schur = NULL; h->piv_pp = h->piv_ff = h->piv_schur = NULL;
+    if (!refresh) { amg_free(h->pres); h->pres = NULL; }
+    h->skipped_dss = 0;
     /* ---- a1 input: the fixed-stress diagonal D_fs -- given (eq:FS_Dps_Dpp), divided by
      *      fs_modulus_scale (remark P:443), or by row-sum lumping (eq:FS_RSL) */
     bsr_rowslice(&h->fu, 0, &h->Asu); bsr_rowslice(&h->fu, 1, &h->Apu);
@@ -1082,7 +1141,9 @@ int orc_setup(orc *h)
     }
 
     /* ---- a4 (pressure): M_pp^-1 = amg(S_pp^(CPR-FS)) */
-    if (h->o.pres_mode == 0) {
+    if (refresh) {
+        if (amg_refresh(h->pres, &h->Spp)) return -5;
+    } else if (h->o.pres_mode == 0) {
         int32_t *zb = (int32_t *)xmalloc(sizeof(int32_t) * Nc);
         for (int c = 0; c < Nc; ++c) zb[c] = (c / (h->nx * h->ny)) / h->o.zblock;
         /* R-gs: level-0 cell colour = parity of x + y + z (red-black on the 7-point pattern of S_pp) */
@@ -1129,7 +1190,6 @@ int orc_setup(orc *h)
         free(Auu); free(pv); free(Auf); free(Afu); free(col); free(sol);
     }
     h->setup_done = 1;
-    (void)t0;
     return 0;
 }
 
@@ -1370,6 +1430,26 @@ void orc_get_cpr(orc *h, double *Dss, double *Dps, double *fs_eff)
     if (Dss) memcpy(Dss, h->Dss, sizeof(double) * h->Nc);
     if (Dps) memcpy(Dps, h->Dps, sizeof(double) * h->Nc);
     if (fs_eff) memcpy(fs_eff, h->fs_eff, sizeof(double) * 2 * h->Nc);
+}
+
+static int bsr_same_pattern(const obsr *B, const int32_t *rp, const int32_t *ci)
+{
+    for (int i = 0; i <= B->nr; ++i) if (B->rp[i] != rp[i]) return 0;
+    for (int64_t q = 0; q < B->rp[B->nr]; ++q) if (B->ci[q] != ci[q]) return 0;
+    return 1;
+}
+/* a Newton step's new Jacobian values on the same patterns (NEXT-f1): the operator uses them at once; the flow
+ * setup products follow with orc_setup_flow, the mechanics hierarchy stays as built */
+int orc_update_values(orc *h, const orc_desc *d)
+{
+    obsr *B[4] = {&h->uu, &h->uf, &h->fu, &h->ff};
+    const int32_t *rp[4] = {d->uu_rowptr, d->uf_rowptr, d->fu_rowptr, d->ff_rowptr};
+    const int32_t *ci[4] = {d->uu_col, d->uf_col, d->fu_col, d->ff_col};
+    const double *v[4] = {d->uu_val, d->uf_val, d->fu_val, d->ff_val};
+    for (int k = 0; k < 4; ++k) if (!bsr_same_pattern(B[k], rp[k], ci[k])) return -1;
+    for (int k = 0; k < 4; ++k) memcpy(B[k]->v, v[k], sizeof(double) * B[k]->bm * B[k]->bn * B[k]->rp[B[k]->nr]);
+    memcpy(h->fs, d->fs, sizeof(double) * 2 * h->Nc);
+    return 0;
 }
 
 void orc_destroy(orc *h)

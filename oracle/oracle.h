@@ -59,6 +59,8 @@ void orc_default_opts(orc_opts *o);
 orc *orc_create(const orc_desc *d, const orc_opts *o);
 void orc_destroy(orc *h);
 int orc_setup(orc *h);                                    /* rows a1-a5 */
+int orc_setup_flow(orc *h, int refresh);                  /* rows a1, a3, a4 (pressure), a5; refresh: frozen aggregation */
+int orc_update_values(orc *h, const orc_desc *d);          /* new values, same patterns (Newton step); -1 on a pattern change */
 int orc_apply(orc *h, const double *v, double *z);        /* Algorithm 1 */
 void orc_apply_operator(orc *h, const double *x, double *y);   /* eq:jac_system */
 int orc_solve(orc *h, const double *b, double *x, double rtol, int m, int maxit, orc_info *info);
