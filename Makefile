@@ -23,10 +23,17 @@ synth/libsynth.so: synth/synth.c
 oracle/liboracle.so: $(wildcard oracle/*.c) $(wildcard oracle/*.h)
 	$(HOSTCC) $(ORCFLAGS) -shared -o $@ $(wildcard oracle/*.c) -lm
 
-paper_1812_05540_b200/libtsp.so: $(TSP_SRC) $(TSP_HDR)
-	$(NVCC) $(NVFLAGS) -Iinclude -shared -o $@ $(TSP_SRC) -lcudart
+TSP_OBJ  = $(patsubst paper_1812_05540_b200/csrc/%.cu,build/tsp/%.o,$(TSP_SRC))
+
+# one object per translation unit (make -j compiles them in parallel), then one shared library
+build/tsp/%.o: paper_1812_05540_b200/csrc/%.cu $(TSP_HDR)
+	@mkdir -p build/tsp
+	$(NVCC) $(NVFLAGS) -Iinclude -c -o $@ $<
+
+paper_1812_05540_b200/libtsp.so: $(TSP_OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(TSP_OBJ) -lcudart
 
 clean:
-	rm -f synth/libsynth.so oracle/liboracle.so paper_1812_05540_b200/libtsp.so
+	rm -rf synth/libsynth.so oracle/liboracle.so paper_1812_05540_b200/libtsp.so build/tsp
 
 .PHONY: all synth oracle tsp clean

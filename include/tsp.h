@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define TSP_ABI_VERSION 3
+#define TSP_ABI_VERSION 4
 
 typedef int tsp_status;
 enum {
@@ -136,7 +136,12 @@ typedef struct {
     tsp_allocator allocator;     /* device memory callbacks; zero-initialised = the library's pool */
 } tsp_desc;
 
-enum { TSP_SETUP_MECH = 1, TSP_SETUP_FLOW = 2 };
+/* TSP_SETUP_REFRESH (with TSP_SETUP_FLOW, DESIGN.md R-refresh): the flow phase after
+ * tsp_update_values -- every a1/a3/a5 product is recomputed from the new values, and the pressure AMG keeps the
+ * strength flags, MIS(2) aggregates and every pattern of its last full build (frozen aggregation) while all of
+ * its values are recomputed in the build's own order and arithmetic (bit-identical to a full build whenever
+ * that build would choose the same aggregates).  TSP_ERR_STATE without a previous completed TSP_SETUP_FLOW. */
+enum { TSP_SETUP_MECH = 1, TSP_SETUP_FLOW = 2, TSP_SETUP_REFRESH = 4 };
 
 typedef struct {
     double rtol;                 /* ||b - A x|| <= rtol ||b||, default 1e-8 */
@@ -208,6 +213,17 @@ tsp_status tsp_create(tsp_handle *out, const tsp_desc *d);
  * (fixed stress, quasi-IMPES, pressure AMG, tile ILU(0)), per Newton step
  * (P:519).  Synchronises the stream. */
 tsp_status tsp_setup(tsp_handle h, unsigned what);
+
+/* A Newton step's new Jacobian values on the SAME patterns (the flow setup is
+ * redone every Newton step, the mechanics setup once per simulation).  Reads from `d` only nx, ny, nz, rank,
+ * nranks (must equal the handle's), inputs_on_device, the four blocks and fs_diag; everything else is ignored.
+ * Every rowptr / col array must equal the one given to tsp_create (else TSP_ERR_INVALID_ARG and the handle is
+ * unchanged); a negative fs_diag entry is TSP_ERR_INVALID_ARG.  Afterwards tsp_apply_operator uses the
+ * new values at once, and tsp_apply_preconditioner / tsp_solve return TSP_ERR_STATE until the flow phase has been
+ * redone on them (tsp_setup(TSP_SETUP_FLOW | TSP_SETUP_REFRESH) for a Newton step).  The mechanics AMG stays as
+ * built (once per simulation); TSP_SETUP_MECH rebuilds it from the new A_uu^SDC.  Collective over the
+ * ranks; synchronises the stream. */
+tsp_status tsp_update_values(tsp_handle h, const tsp_desc *d);
 
 /* z = M^-1 v (Algorithm 1).  Device pointers, length n = 3 N_n + 2 N_c, must
  * not alias.  Asynchronous on the handle's stream. */

@@ -761,7 +761,7 @@ static void ghost_rows(Ctx &c, Halo &H, const Csr &Pg, Csr &Pext, int nc)
 }
 
 // allgather the rows of a distributed matrix (global columns) into one full copy per rank
-static void gather_rows(Ctx &c, const Csr &A, const DBuf<int32_t> &zb, Csr &F, DBuf<int32_t> &zbF, int nc,
+static void gather_rows(Ctx &c, const Csr &A, const int32_t *zb, Csr &F, DBuf<int32_t> &zbF, int nc,
                         std::vector<int64_t> &counts)
 {
     std::vector<int64_t> me = {(int64_t)A.n, A.nnz};
@@ -817,15 +817,26 @@ static void gather_rows(Ctx &c, const Csr &A, const DBuf<int32_t> &zb, Csr &F, D
 // `row_off0`).  A coarse level stays distributed while its global size exceeds
 // opts.replicate_rows; below that it is gathered onto every rank and the rest of the
 // hierarchy is built redundantly (identical data => identical results on all ranks).
-void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_halo, int64_t row_off0, int64_t nglob0)
+//
+// refresh = true (frozen aggregation, NEXT-f1, DESIGN.md R-refresh): A0 holds new values on the pattern the
+// hierarchy H was built from; the strength flags, MIS(2) roots, aggregates and every pattern of H are kept and
+// every value is recomputed in the build's own order and arithmetic (l1 norms, filtered diagonal with the KEPT
+// strength flags, rho and omega, P, R = P^T, A_c = R (A P), the coarsest inverse) -- the oracle's amg_refresh.
+void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_halo, int64_t row_off0, int64_t nglob0,
+               bool refresh)
 {
     dbg_mark(c, "start", -1);
-    H.L.clear();
-    dbg_mark(c, "free old", -2);
-    H.L.reserve(16);
-    H.nc = nc;
-    H.L.emplace_back();
-    {
+    if (refresh) {
+        TSP_REQUIRE(!H.L.empty() && H.nc == nc && H.L[0].A.n == A0.n && H.L[0].A.nnz == A0.nnz, TSP_ERR_STATE,
+                    "refresh: no hierarchy of this pattern to refresh");
+        H.perturbed = 0;
+        H.L[0].A = std::move(A0);          // same pattern (checked by the caller), new values
+    } else {
+        H.L.clear();
+        dbg_mark(c, "free old", -2);
+        H.L.reserve(16);
+        H.nc = nc;
+        H.L.emplace_back();
         Level &L0 = H.L[0];
         L0.A = std::move(A0);
         L0.zb = std::move(zb0);
@@ -850,69 +861,78 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
             L.dinv_gh.alloc((size_t)std::max(L.hp->nghost(), 1) * nc);
             halo_exchange(c, *L.hp, nc, L.dinv, L.dinv_gh);
         }
-        if (L.nglob <= c.o.amg_coarse_max || lvl == maxl - 1) {
+        if (refresh ? L.coarsest != 0 : (L.nglob <= c.o.amg_coarse_max || lvl == maxl - 1)) {
             TSP_REQUIRE(!L.dist, TSP_ERR_INVALID_ARG, "the distributed fine level is too small for this many ranks");
             make_coarsest(c, H, L);
             break;
         }
-        // strength + symmetrisation
-        DBuf<uint8_t> S, E; S.alloc(L.A.nnz + 1); E.alloc(L.A.nnz + 1);
-        err.zero(c.s);
-        if (n) {
-            k_strength<<<grid_for((int64_t)n * kStrG, 256), 256, 0, c.s>>>(n, nc, nown, L.A.rp, L.A.ci, L.A.v, L.zb, c.o.amg_theta, S);
-            k_symm<<<grid_for((int64_t)n * kStrG, 256), 256, 0, c.s>>>(n, nown, L.dist ? 1 : 0, L.A.rp, L.A.ci, S, E, err);
+        int nagg = L.nagg;
+        int64_t nagg_glob = L.nagg_glob, coarse_off = L.coarse_off;
+        if (!refresh) {
+            // strength + symmetrisation (the flags E are kept for a later refresh)
+            DBuf<uint8_t> S; S.alloc(L.A.nnz + 1);
+            DBuf<uint8_t> &E = L.E; E.alloc(L.A.nnz + 1);
+            err.zero(c.s);
+            if (n) {
+                k_strength<<<grid_for((int64_t)n * kStrG, 256), 256, 0, c.s>>>(n, nc, nown, L.A.rp, L.A.ci, L.A.v, L.zb, c.o.amg_theta, S);
+                k_symm<<<grid_for((int64_t)n * kStrG, 256), 256, 0, c.s>>>(n, nown, L.dist ? 1 : 0, L.A.rp, L.A.ci, S, E, err);
+            }
+            c.launches += 2;
+            TSP_REQUIRE(!d2h1(c, err.p), TSP_ERR_INVALID_ARG, "AMG input pattern is not structurally symmetric");
+            // MIS(2) rounds: the strength graph never leaves a z-block, so each rank runs its own rounds
+            DBuf<int8_t> st; st.alloc(std::max(n, 1));
+            DBuf<uint64_t> t1; t1.alloc(std::max(n, 1));
+            DBuf<uint8_t> newr, near1; newr.alloc(std::max(n, 1)); near1.alloc(std::max(n, 1));
+            if (n) k_mis_init<<<grid_for(n, 256), 256, 0, c.s>>>(n, L.A.rp, E, st);
+            c.launches++;
+            const int off = (int)L.row_off;
+            for (int round = 0; round < 1000 && n; ++round) {
+                k_mis_t1<<<grid_for(n, 256), 256, 0, c.s>>>(n, off, L.A.rp, L.A.ci, E, st, t1);
+                k_mis_root<<<grid_for(n, 256), 256, 0, c.s>>>(n, off, L.A.rp, L.A.ci, E, st, t1, newr);
+                k_mis_near<<<grid_for(n, 256), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, E, newr, st, near1);
+                c.dcount.zero(c.s);
+                k_mis_out<<<grid_for(n, 256), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, E, near1, st, c.dcount);
+                c.launches += 4;
+                if (d2h1(c, c.dcount.p) == 0) break;
+            }
+            dbg_mark(c, "strength+mis", lvl);
+            // aggregates: local numbering by ascending root, global = coarse_off + local
+            DBuf<int32_t> flag, rid, ph1;
+            flag.alloc(n + 1); rid.alloc(n + 1); ph1.alloc(std::max(n, 1));
+            if (n) k_rootflag<<<grid_for(n, 256), 256, 0, c.s>>>(n, st, flag);
+            TSP_CUDA(cudaMemsetAsync(flag.p + n, 0, sizeof(int32_t), c.s));
+            exclusive_scan<int32_t>(c, flag, rid, n + 1);
+            nagg = d2h1(c, rid.p + n);
+            nagg_glob = nagg; coarse_off = 0;
+            if (L.dist) {
+                std::vector<int64_t> all = host_allgather<int64_t>(c, std::vector<int64_t>{(int64_t)nagg});
+                nagg_glob = 0;
+                for (int r = 0; r < c.nranks; ++r) { if (r < c.rank) coarse_off += all[r]; nagg_glob += all[r]; }
+            }
+            if (nagg_glob == 0 || (double)nagg_glob > 0.8 * (double)L.nglob) {   // stagnation: direct solve here
+                TSP_REQUIRE(!L.dist, TSP_ERR_SINGULAR, "coarsening stagnated on a distributed level");
+                H.fallbacks++;
+                make_coarsest(c, H, L);
+                break;
+            }
+            L.nagg = nagg;
+            L.nagg_glob = nagg_glob;
+            L.coarse_off = coarse_off;
+            L.agg.alloc(std::max(n, 1));
+            H.L.emplace_back();
+            Level &Lc = H.L[lvl + 1];
+            Level &Lf = H.L[lvl];   // re-fetch after emplace_back
+            Lc.zb.alloc(std::max(nagg, 1));
+            TSP_CUDA(cudaMemsetAsync(ph1, 0xff, sizeof(int32_t) * std::max(n, 1), c.s));
+            if (n) {
+                k_phase1<<<grid_for(n, 256), 256, 0, c.s>>>(n, Lf.A.rp, Lf.A.ci, Lf.E, st, rid, Lf.zb, ph1, Lc.zb);
+                k_phase2<<<grid_for(n, 256), 256, 0, c.s>>>(n, nc, Lf.A.rp, Lf.A.ci, Lf.A.v, Lf.E, st, ph1, Lf.agg);
+            }
+            c.launches += 3;
         }
-        c.launches += 2;
-        TSP_REQUIRE(!d2h1(c, err.p), TSP_ERR_INVALID_ARG, "AMG input pattern is not structurally symmetric");
-        // MIS(2) rounds: the strength graph never leaves a z-block, so each rank runs its own rounds
-        DBuf<int8_t> st; st.alloc(std::max(n, 1));
-        DBuf<uint64_t> t1; t1.alloc(std::max(n, 1));
-        DBuf<uint8_t> newr, near1; newr.alloc(std::max(n, 1)); near1.alloc(std::max(n, 1));
-        if (n) k_mis_init<<<grid_for(n, 256), 256, 0, c.s>>>(n, L.A.rp, E, st);
-        c.launches++;
-        const int off = (int)L.row_off;
-        for (int round = 0; round < 1000 && n; ++round) {
-            k_mis_t1<<<grid_for(n, 256), 256, 0, c.s>>>(n, off, L.A.rp, L.A.ci, E, st, t1);
-            k_mis_root<<<grid_for(n, 256), 256, 0, c.s>>>(n, off, L.A.rp, L.A.ci, E, st, t1, newr);
-            k_mis_near<<<grid_for(n, 256), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, E, newr, st, near1);
-            c.dcount.zero(c.s);
-            k_mis_out<<<grid_for(n, 256), 256, 0, c.s>>>(n, L.A.rp, L.A.ci, E, near1, st, c.dcount);
-            c.launches += 4;
-            if (d2h1(c, c.dcount.p) == 0) break;
-        }
-        dbg_mark(c, "strength+mis", lvl);
-        // aggregates: local numbering by ascending root, global = coarse_off + local
-        DBuf<int32_t> flag, rid, ph1;
-        flag.alloc(n + 1); rid.alloc(n + 1); ph1.alloc(std::max(n, 1));
-        if (n) k_rootflag<<<grid_for(n, 256), 256, 0, c.s>>>(n, st, flag);
-        TSP_CUDA(cudaMemsetAsync(flag.p + n, 0, sizeof(int32_t), c.s));
-        exclusive_scan<int32_t>(c, flag, rid, n + 1);
-        const int nagg = d2h1(c, rid.p + n);
-        int64_t nagg_glob = nagg, coarse_off = 0;
-        if (L.dist) {
-            std::vector<int64_t> all = host_allgather<int64_t>(c, std::vector<int64_t>{(int64_t)nagg});
-            nagg_glob = 0;
-            for (int r = 0; r < c.nranks; ++r) { if (r < c.rank) coarse_off += all[r]; nagg_glob += all[r]; }
-        }
-        if (nagg_glob == 0 || (double)nagg_glob > 0.8 * (double)L.nglob) {   // stagnation: direct solve here
-            TSP_REQUIRE(!L.dist, TSP_ERR_SINGULAR, "coarsening stagnated on a distributed level");
-            H.fallbacks++;
-            make_coarsest(c, H, L);
-            break;
-        }
-        L.nagg = nagg;
-        L.coarse_off = coarse_off;
-        L.agg.alloc(std::max(n, 1));
-        H.L.emplace_back();
         Level &Lc = H.L[lvl + 1];
-        Level &Lf = H.L[lvl];   // re-fetch after emplace_back
-        Lc.zb.alloc(std::max(nagg, 1));
-        TSP_CUDA(cudaMemsetAsync(ph1, 0xff, sizeof(int32_t) * std::max(n, 1), c.s));
-        if (n) {
-            k_phase1<<<grid_for(n, 256), 256, 0, c.s>>>(n, Lf.A.rp, Lf.A.ci, E, st, rid, Lf.zb, ph1, Lc.zb);
-            k_phase2<<<grid_for(n, 256), 256, 0, c.s>>>(n, nc, Lf.A.rp, Lf.A.ci, Lf.A.v, E, st, ph1, Lf.agg);
-        }
-        c.launches += 3;
+        Level &Lf = H.L[lvl];
+        const uint8_t *E = Lf.E.p;
         // prolongator
         DBuf<double> d; d.alloc((size_t)std::max(n, 1) * nc);
         DBuf<unsigned long long> rho; rho.alloc(3); rho.zero(c.s);
@@ -982,7 +1002,8 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
         } else if (Lf.dist) {
             // gather the coarse level onto every rank; the prolongator then addresses the full vector
             DBuf<int32_t> zbF;
-            gather_rows(c, Ac, Lc.zb, Lc.A, zbF, nc, Lf.rep_counts);
+            // (refresh: Lc.zb is already the gathered copy; this rank's rows start at coarse_off)
+            gather_rows(c, Ac, refresh ? Lc.zb.p + coarse_off : Lc.zb.p, Lc.A, zbF, nc, Lf.rep_counts);
             Lc.zb = std::move(zbF);
             Lc.dist = false;
             Lf.rep_offs.assign(c.nranks + 1, 0);

@@ -315,7 +315,7 @@ tsp_status tsp_create(tsp_handle *out, const tsp_desc *d)
     // keep only what the setup phases read: A_uu's pattern + SDC values (a2), A_ff in full (a1, a3, a5)
     extract_sdc(*c);
     c->uu.v.release();
-    for (Csr *A : {&c->uf, &c->fu}) { A->v.release(); A->ci.release(); A->gci.release(); A->rp.release(); }
+    for (Csr *A : {&c->uf, &c->fu}) A->v.release();   // patterns stay (tsp_update_values checks them)
     c->w_yf.alloc(2 * (size_t)c->Nc); c->w_wp.alloc(c->Nc); c->w_zp.alloc(c->Nc); c->w_tmp.alloc(c->Nc);
     c->kx.alloc(c->n); c->kb.alloc(c->n);
     c->dcount.alloc(4);
@@ -336,9 +336,68 @@ tsp_status tsp_setup(tsp_handle h, unsigned what)
     if (!h) { set_error("null handle"); return TSP_ERR_INVALID_ARG; }
     API_BEGIN
     krylov_graphs_drop(*h);             // the graphs bake in the hierarchy's buffer addresses
+    TSP_REQUIRE(!(what & TSP_SETUP_REFRESH) || (what & TSP_SETUP_FLOW), TSP_ERR_INVALID_ARG,
+                "TSP_SETUP_REFRESH goes with TSP_SETUP_FLOW");
     if (what & TSP_SETUP_MECH) setup_mech(*h);
-    if (what & TSP_SETUP_FLOW) setup_flow(*h);
+    if (what & TSP_SETUP_FLOW) setup_flow(*h, (what & TSP_SETUP_REFRESH) != 0);
     TSP_CUDA(cudaStreamSynchronize(h->s));
+    API_END
+}
+
+// 1 if (rp, ci) of `a` and `b` differ anywhere (rows n, entries nnz)
+__global__ void k_pattern_diff(int n, int64_t nnz, const int32_t *__restrict__ rpa, const int32_t *__restrict__ cia,
+                               const int32_t *__restrict__ rpb, const int32_t *__restrict__ cib, unsigned *flag)
+{
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if ((t <= n && rpa[t] != rpb[t]) || (t < nnz && cia[t] != cib[t])) atomicOr(flag, 1u);
+}
+
+tsp_status tsp_update_values(tsp_handle h, const tsp_desc *d)
+{
+    if (!h || !d) { set_error("null argument"); return TSP_ERR_INVALID_ARG; }
+    API_BEGIN
+    Ctx &c = *h;
+    TSP_REQUIRE(d->nx == c.nx && d->ny == c.ny && d->nz == c.nz_glob && d->rank == c.rank && d->nranks == c.nranks,
+                TSP_ERR_INVALID_ARG, "update_values: grid or rank differs from tsp_create");
+    const tsp_bsr *bs[4] = {&d->A_uu, &d->A_uf, &d->A_fu, &d->A_ff};
+    for (int k = 0; k < 4; ++k)
+        TSP_REQUIRE(bs[k]->rowptr && bs[k]->col && bs[k]->val, TSP_ERR_INVALID_ARG, "null matrix pointer");
+    TSP_REQUIRE(d->fs_diag, TSP_ERR_INVALID_ARG, "null fs_diag");
+    const bool on_dev = d->inputs_on_device != 0;
+    Csr *cur[4] = {&c.uu, &c.uf, &c.fu, &c.ff};
+    const int ncv[4] = {9, 6, 6, 4};
+    const char *names[4] = {"A_uu", "A_uf", "A_fu", "A_ff"};
+    Csr nw[4];
+    DBuf<unsigned> flag; flag.alloc(1);
+    for (int k = 0; k < 4; ++k) {             // upload + compare with the stored pattern (global column ids)
+        const Csr &A = *cur[k];
+        csr_upload(c, nw[k], A.n, A.m, ncv[k], bs[k]->rowptr, bs[k]->col, bs[k]->val, on_dev);
+        TSP_REQUIRE(nw[k].nnz == A.nnz, TSP_ERR_INVALID_ARG, std::string("update_values: ") + names[k] + " pattern changed");
+        flag.zero(c.s);
+        k_pattern_diff<<<grid_for(std::max<int64_t>(A.nnz, A.n + 1), 256), 256, 0, c.s>>>(
+            A.n, A.nnz, nw[k].rp, nw[k].ci, A.rp, A.gci.p ? A.gci.p : A.ci.p, flag);
+        c.launches++;
+        unsigned f = 0;
+        TSP_CUDA(cudaMemcpyAsync(&f, flag.p, sizeof(f), cudaMemcpyDeviceToHost, c.s));
+        TSP_CUDA(cudaStreamSynchronize(c.s));
+        TSP_REQUIRE(!f, TSP_ERR_INVALID_ARG, std::string("update_values: ") + names[k] + " pattern changed");
+    }
+    DBuf<double> fs; fs.alloc(2 * (size_t)std::max(c.Nc, 1));
+    if (c.Nc) TSP_CUDA(cudaMemcpyAsync(fs, d->fs_diag, sizeof(double) * 2 * c.Nc, on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.s));
+    TSP_REQUIRE(all_nonneg(c, fs, 2 * (int64_t)c.Nc), TSP_ERR_INVALID_ARG, "negative fixed-stress diagonal (S:355)");
+    // commit: new values into the stored patterns (local column ids) and the apply layouts
+    krylov_graphs_drop(c);                    // the graphs bake in the SELL buffers' addresses
+    c.fs = std::move(fs);
+    for (int k = 0; k < 4; ++k) cur[k]->v = std::move(nw[k].v);
+    if (!sym_refill_uu(c)) sell_from_csr(c, c.uu, c.s_uu, 9);
+    extract_sdc(c);                           // input of the next TSP_SETUP_MECH (a2)
+    c.sdc_stale = true;
+    sell_from_csr(c, c.uf, c.s_uf, 6);
+    sell_from_csr(c, c.fu, c.s_fu, 6);
+    sell_from_csr(c, c.ff, c.s_ff, 4);
+    c.uu.v.release(); c.uf.v.release(); c.fu.v.release();
+    c.flow_ready = false;                     // apply / solve wait for the flow phase on the new values
+    TSP_CUDA(cudaStreamSynchronize(c.s));
     API_END
 }
 

@@ -163,6 +163,7 @@ void setup_mech(Ctx &c)
     c.mech_ready = false;
     dbg_mark(c, "mech begin", -1);
     c.mech.L.clear();                     // free the previous hierarchy first: its memory is reused below
+    if (c.sdc_stale) { sym_refill_sdc(c); c.sdc_stale = false; }   // A_uu changed since create (tsp_update_values)
     Csr A;
     copy_pattern(c, c.uu, A, 3);
     prof_begin(c, PK_SETUP);
@@ -207,11 +208,15 @@ static void rsl_diag(Ctx &c)
     c.launches += 3;
 }
 
-void setup_flow(Ctx &c)
+// refresh (NEXT-f1, R-refresh): the values of A_ff / A_fu / D_fs changed since the last flow setup
+// (tsp_update_values), the patterns did not: every a1/a3/a5 product is recomputed and the pressure hierarchy
+// keeps its strength flags, aggregates and patterns (amg_build refresh, the oracle's amg_refresh)
+void setup_flow(Ctx &c, bool refresh)
 {
-    c.flow_ready = false;
+    TSP_REQUIRE(!refresh || c.flow_built, TSP_ERR_STATE, "TSP_SETUP_REFRESH needs a completed TSP_SETUP_FLOW on this handle");
+    c.flow_ready = c.flow_built = false;
     dbg_mark(c, "flow begin", -1);
-    c.pres.L.clear();
+    if (!refresh) c.pres.L.clear();
     // a1 input: the fixed-stress diagonal (given / scale, or RSL)
     c.fs_eff.alloc(2 * (size_t)std::max(c.Nc, 1));
     if (c.o.fs_mode == 1) rsl_diag(c);
@@ -260,10 +265,10 @@ void setup_flow(Ctx &c)
     if (c.Nc) k_zb_cells<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(c.Nc, c.nx, c.ny, c.k0, c.o.zblock, zb);
     c.launches += 3;
     dbg_mark(c, "flow qimpes", -2);
-    amg_build(c, c.pres, S, zb, 1, &c.hf, c.cell_off, c.Nc_glob);   // a4 (pressure): M_pp^-1 = amg(S_pp)
+    amg_build(c, c.pres, S, zb, 1, &c.hf, c.cell_off, c.Nc_glob, refresh);   // a4 (pressure): M_pp^-1 = amg(S_pp)
     ilu_setup(c, nullptr);                // a5: tile ILU(0) of P S_ff^FS P^T
     dbg_mark(c, "ilu", -2);
-    c.flow_ready = true;
+    c.flow_ready = c.flow_built = true;
 }
 
 }  // namespace tsp

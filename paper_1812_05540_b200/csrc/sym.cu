@@ -39,8 +39,9 @@ __device__ __forceinline__ int sym_off(const SymGeo &g, int c) { return (c % 3 -
 
 // pattern check (bit 31: not the clipped 27-point stencil in ascending order) and the 9-bit mask of block
 // entries (r,c) with B(i,j)[r][c] != B(j,i)[c][r] for some owned pair
+// bs = 9: the 3x3 blocks of A_uu; bs = 3: SDC values (x,x), (y,y), (z,z) of each block (bit 4e for value e)
 __global__ void k_sym_check(SymGeo g, int64_t node_off, const int32_t *__restrict__ rp, const int32_t *__restrict__ gci,
-                            const double *__restrict__ v, unsigned *flag)
+                            const double *__restrict__ v, int bs, unsigned *flag)
 {
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= g.Nn) return;
@@ -60,9 +61,14 @@ __global__ void k_sym_check(SymGeo g, int64_t node_off, const int32_t *__restric
                 for (int64_t p = rp[n2]; p < rp[n2 + 1]; ++p)
                     if (gci[p] == gid) {
                         found = true;
-                        for (int r = 0; r < 3; ++r)
-                            for (int cc = 0; cc < 3; ++cc)
-                                if (v[q * 9 + r * 3 + cc] != v[p * 9 + cc * 3 + r]) f |= 1u << (r * 3 + cc);
+                        if (bs == 9) {
+                            for (int r = 0; r < 3; ++r)
+                                for (int cc = 0; cc < 3; ++cc)
+                                    if (v[q * 9 + r * 3 + cc] != v[p * 9 + cc * 3 + r]) f |= 1u << (r * 3 + cc);
+                        } else {
+                            for (int e = 0; e < 3; ++e)
+                                if (v[q * 3 + e] != v[p * 3 + e]) f |= 1u << (4 * e);
+                        }
                         break;
                     }
                 if (!found) f |= 1u << 31;
@@ -74,8 +80,8 @@ __global__ void k_sym_check(SymGeo g, int64_t node_off, const int32_t *__restric
     if (f) atomicOr(flag, f);
 }
 
-// fill from the 3x3 blocks of A_uu (`src[e]`: block entry of stored value e)
-__global__ void k_sym_fill(SymGeo g, SymMap m, const int32_t *__restrict__ rp, const double *__restrict__ v, int s0, int s1, int s2,
+// fill from `v` (`stride` values per block entry; `src[e]`: the offset of stored value e in an entry)
+__global__ void k_sym_fill(SymGeo g, SymMap m, const int32_t *__restrict__ rp, const double *__restrict__ v, int stride, int s0, int s1, int s2,
                            int s3, int s4, int s5, int s6, int s7, int s8, double *__restrict__ vs, double *__restrict__ vf,
                            double *__restrict__ gl)
 {
@@ -88,7 +94,7 @@ __global__ void k_sym_fill(SymGeo g, SymMap m, const int32_t *__restrict__ rp, c
         if (!sym_inside(g, x, y, zg, c)) continue;
         const bool ghost_lower = c < 9 && n + sym_off(g, c) < 0;
         for (int e = 0; e < m.bs; ++e) {
-            const double val = v[q * 9 + src[e]];
+            const double val = v[q * stride + src[e]];
             if (m.full[e]) vf[sidx_f(n, c, m.idx[e], m.kf)] = val;
             else if (c >= 13) vs[sidx_s(n, c - 13, m.idx[e], m.ks)] = val;
             else if (ghost_lower) gl[sidx_g(n, c, m.idx[e], m.ks)] = val;
@@ -234,8 +240,10 @@ static SymGeo sym_geo(const Ctx &c)
     return g;
 }
 
-// `src[e]`: the 3x3-block entry behind stored value e; `asym`: 9-bit mask of the non-symmetric block entries
-static void sym_fill_one(Ctx &c, const SymGeo &g, int bs, const int *src, unsigned asym, Sym27 &S)
+// `src[e]`: the 3x3-block entry behind stored value e; `asym`: 9-bit mask of the non-symmetric block entries;
+// values read from `v` (`stride` per block entry, stored value e at offset rd[e]; default: A_uu's blocks)
+static void sym_fill_one(Ctx &c, const SymGeo &g, int bs, const int *src, unsigned asym, Sym27 &S,
+                         const double *v = nullptr, int stride = 9, const int *rd = nullptr)
 {
     SymMap &m = S.m;
     m.bs = bs; m.ks = m.kf = 0;
@@ -251,8 +259,9 @@ static void sym_fill_one(Ctx &c, const SymGeo &g, int bs, const int *src, unsign
     S.val_f.alloc((size_t)std::max(nsl, 1) * 27 * std::max(m.kf, 1) * 32); S.val_f.zero(c.s);
     S.gl.alloc((size_t)std::max(nsl0, 1) * 9 * std::max(m.ks, 1) * 32); S.gl.zero(c.s);
     int s9[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (int e = 0; e < bs; ++e) s9[e] = src[e];
-    if (c.Nn) k_sym_fill<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(g, m, c.uu.rp, c.uu.v, s9[0], s9[1], s9[2], s9[3], s9[4], s9[5], s9[6],
+    for (int e = 0; e < bs; ++e) s9[e] = rd ? rd[e] : src[e];
+    if (!v) v = c.uu.v;
+    if (c.Nn) k_sym_fill<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(g, m, c.uu.rp, v, stride, s9[0], s9[1], s9[2], s9[3], s9[4], s9[5], s9[6],
                                                               s9[7], s9[8], S.val_s, S.val_f, S.gl);
     c.launches++;
     S.ok = true;
@@ -268,7 +277,7 @@ void sym_build(Ctx &c)
     if (c.comm && !((g.nlo == 0 || g.nlo == g.NXY) && (c.hu.nrecv[1] == 0 || c.hu.nrecv[1] == g.NXY))) f = 1u << 31;
     const int32_t *gci = c.uu.gci.p ? c.uu.gci.p : c.uu.ci.p;
     DBuf<unsigned> flag; flag.alloc(1); flag.zero(c.s);
-    if (c.Nn) k_sym_check<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(g, c.node_off, c.uu.rp, gci, c.uu.v, flag);
+    if (c.Nn) k_sym_check<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(g, c.node_off, c.uu.rp, gci, c.uu.v, 9, flag);
     c.launches++;
     unsigned fd = 0;
     TSP_CUDA(cudaMemcpyAsync(&fd, flag.p, sizeof(fd), cudaMemcpyDeviceToHost, c.s));
@@ -289,6 +298,57 @@ void sym_build(Ctx &c)
     c.sym_asym = asym;
     sym_fill_one(c, g, 9, id9, asym, c.sym_uu);
     sym_fill_one(c, g, 3, sdc, asym, c.sym_sdc);
+}
+
+// mask of non-symmetric entries of `v` (bs 9: A_uu blocks, bs 3: SDC values), bit 31 = not the 27-point
+// stencil; the same on every rank
+static unsigned sym_mask(Ctx &c, const SymGeo &g, const double *v, int bs)
+{
+    const int32_t *gci = c.uu.gci.p ? c.uu.gci.p : c.uu.ci.p;
+    DBuf<unsigned> flag; flag.alloc(1); flag.zero(c.s);
+    if (c.Nn) k_sym_check<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(g, c.node_off, c.uu.rp, gci, v, bs, flag);
+    c.launches++;
+    unsigned f = 0;
+    TSP_CUDA(cudaMemcpyAsync(&f, flag.p, sizeof(f), cudaMemcpyDeviceToHost, c.s));
+    TSP_CUDA(cudaStreamSynchronize(c.s));
+    if (c.comm) {
+        std::vector<int64_t> all = host_allgather<int64_t>(c, std::vector<int64_t>{(int64_t)f});
+        for (auto a : all) f |= (unsigned)a;
+    }
+    return f;
+}
+
+// tsp_update_values: new A_uu values (c.uu.v) on the same pattern.  The structured operator keeps its layout
+// when the new values are symmetric wherever the layout assumes it (their mask is inside sym_asym); otherwise
+// the operator falls back to the generic SELL copy.  Returns whether the structured copy is in use.
+bool sym_refill_uu(Ctx &c)
+{
+    if (!c.sym_uu.ok) return false;
+    const SymGeo g = sym_geo(c);
+    const unsigned f = sym_mask(c, g, c.uu.v, 9);
+    if ((f >> 31) || (f & 0x1ffu & ~c.sym_asym)) {
+        c.sym_uu.ok = false;
+        c.sym_uu.val_s.release(); c.sym_uu.val_f.release(); c.sym_uu.gl.release();
+        return false;
+    }
+    const int id9[9] = {0, 1, 2, 3, 4, 5, 6, 7, 8};
+    sym_fill_one(c, g, 9, id9, c.sym_asym, c.sym_uu);
+    return true;
+}
+
+// TSP_SETUP_MECH after tsp_update_values: the level-0 SDC smoother copy from the new SDC values (c.uu_sdc)
+void sym_refill_sdc(Ctx &c)
+{
+    if (!c.sym_sdc.ok) return;
+    const SymGeo g = sym_geo(c);
+    const unsigned f = sym_mask(c, g, c.uu_sdc, 3);
+    if ((f >> 31) || (f & 0x1ffu & ~c.sym_asym)) {
+        c.sym_sdc.ok = false;
+        c.sym_sdc.val_s.release(); c.sym_sdc.val_f.release(); c.sym_sdc.gl.release();
+        return;
+    }
+    const int sdc[3] = {0, 4, 8}, rd[3] = {0, 1, 2};
+    sym_fill_one(c, g, 3, sdc, c.sym_asym, c.sym_sdc, c.uu_sdc, 3, rd);
 }
 
 // ---- launchers used by apply.cu (operator) and amg.cu (level-0 mechanics smoother); the layouts are

@@ -199,6 +199,8 @@ struct Level {
     DBuf<double> dl1;             // l1 row norms [n][nc]
     DBuf<double> dinv;            // 1 / dl1
     DBuf<int32_t> agg;            // aggregate per row (-1 = none)
+    DBuf<uint8_t> E;              // symmetrised strength flag per entry of A (kept for the frozen refresh)
+    int64_t nagg_glob = 0;        // aggregates over all ranks
     Csr P, R;
     Sell sA, sP, sR;
     DBuf<double> cinv;            // coarsest: dense inverse [nc][n][n]
@@ -277,6 +279,9 @@ struct Ctx {
     int ilu_nlev = 0, ilu_tsize = 0, ntiles = 0, ntx = 0, nty = 0, ntz = 0;
     Hier mech, pres;
     bool mech_ready = false, flow_ready = false;
+    bool flow_built = false;      // the last TSP_SETUP_FLOW completed (its hierarchy can be refreshed); flow_ready is
+                                  // also cleared by tsp_update_values (apply / solve need the flow phase first)
+    bool sdc_stale = false;       // tsp_update_values changed A_uu: sym_sdc is refilled by the next TSP_SETUP_MECH
     // work vectors
     DBuf<double> w_yf, w_wp, w_zp, w_zf2, w_tmp;
     // Krylov storage
@@ -312,6 +317,8 @@ bool all_nonneg(Ctx &c, const double *v, int64_t n);
 // operator / Algorithm 1 pieces (apply.cu)
 void op_apply(Ctx &c, const double *x, double *y);
 void sym_build(Ctx &c);           // sym_uu / sym_sdc from the uploaded A_uu (tsp_create)
+bool sym_refill_uu(Ctx &c);       // tsp_update_values: sym_uu from the new c.uu.v (false: generic SELL needed)
+void sym_refill_sdc(Ctx &c);      // TSP_SETUP_MECH after an update: sym_sdc from c.uu_sdc
 bool sym_op_node(Ctx &c, const GV &gu, const GV &gf, double *yu);                      // A_uu x_u + A_uf x_f, if sym_uu.ok
 bool sym_vcycle_pre(Ctx &c, int n, const GV &dinv, const GV &b, double *x, double *r);   // level-0 SDC, if sym_sdc.ok
 bool sym_vcycle_post(Ctx &c, int n, const double *dinv, const double *b, const GV &x, double *xo);
@@ -321,8 +328,9 @@ void prec_apply(Ctx &c, const double *v, double *z);
 // setup (setup_flow.cu, amg_setup.cu, ilu.cu)
 void extract_sdc(Ctx &c);
 void setup_mech(Ctx &c);
-void setup_flow(Ctx &c);
-void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_halo, int64_t row_off0, int64_t nglob0);
+void setup_flow(Ctx &c, bool refresh = false);
+void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_halo, int64_t row_off0, int64_t nglob0,
+               bool refresh = false);   // refresh: frozen aggregation, values only (R-refresh)
 void amg_vcycle(Ctx &c, Hier &H, const double *b, double *x, bool mech);
 // gs.cu: Gauss-Seidel smoother (R-gs)
 void gs_setup(Ctx &c, Hier &H, int nc);

@@ -23,6 +23,7 @@ _P = C.POINTER
 
 TSP_SETUP_MECH = 1
 TSP_SETUP_FLOW = 2
+TSP_SETUP_REFRESH = 4     # with TSP_SETUP_FLOW: frozen-aggregation value refresh after update_values (NEXT-f1)
 STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "INVALID_ARG", -2: "DIM_MISMATCH", -3: "STATE", -4: "CUDA",
           -5: "NCCL", -6: "OOM", -7: "SINGULAR", -8: "NUMERIC"}
 
@@ -129,6 +130,7 @@ def lib():
         L.tsp_default_options.argtypes = [_P(tsp_options)]
         L.tsp_create.argtypes = [_P(C.c_void_p), _P(tsp_desc)]
         L.tsp_setup.argtypes = [C.c_void_p, C.c_uint]
+        L.tsp_update_values.argtypes = [C.c_void_p, _P(tsp_desc)]
         L.tsp_apply_preconditioner.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.tsp_apply_operator.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.tsp_solve.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, _P(tsp_solve_opts), _P(tsp_solve_info)]
@@ -152,13 +154,13 @@ def lib():
         L.tsp_level_dist.argtypes = [C.c_void_p, C.c_int, C.c_int, _P(C.c_int64)]
         L.tsp_variant_counts.argtypes = [C.c_void_p, _P(C.c_int64)]
         L.tsp_export_colour.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, _P(C.c_int), _P(C.c_int)]
-        if L.tsp_abi_version() != 3:
+        if L.tsp_abi_version() != 4:
             raise RuntimeError("libtsp ABI version mismatch")
         _LIB = L
     return _LIB
 
 
-EXPORTED = ["tsp_abi_version", "tsp_last_error", "tsp_default_options", "tsp_create", "tsp_setup",
+EXPORTED = ["tsp_abi_version", "tsp_last_error", "tsp_default_options", "tsp_create", "tsp_setup", "tsp_update_values",
             "tsp_apply_preconditioner", "tsp_apply_operator", "tsp_solve", "tsp_default_solve_opts",
             "tsp_get_stats", "tsp_level_sizes", "tsp_export_level", "tsp_prof_enable", "tsp_prof_read",
             "tsp_prof_classes", "tsp_export_cpr", "tsp_destroy", "tsp_nccl_unique_id", "tsp_local_world_create", "tsp_local_world_destroy",
@@ -257,18 +259,9 @@ class Tsp:
         self.n = pb.n
         self.torch = torch
         self.stream = stream if stream is not None else torch.cuda.current_stream()
+        self._grid = (rank, nranks)
         keep = []
-
-        def arr(x):
-            if device_inputs or hasattr(x, "data_ptr"):   # CUDA tensors, or pinned host tensors
-                keep.append(x)
-                return _ptr(x)
-            y = np.ascontiguousarray(x)
-            keep.append(y)
-            return _ptr(y)
-
-        d = tsp_desc()
-        d.nx, d.ny, d.nz, d.rank, d.nranks = pb.nx, pb.ny, pb.nz, rank, nranks
+        d = self._desc(pb, device_inputs, keep)
         d.comm_kind = comm_kind
         if isinstance(comm_arg, (bytes, bytearray)):
             self._uid = C.create_string_buffer(bytes(comm_arg), 128)
@@ -276,11 +269,6 @@ class Tsp:
         else:
             d.comm_arg = comm_arg
         d.stream = C.c_void_p(self.stream.cuda_stream)
-        d.inputs_on_device = int(device_inputs)
-        for name in ("uu", "uf", "fu", "ff"):
-            b = tsp_bsr(arr(getattr(pb, name + "_rowptr")), arr(getattr(pb, name + "_col")), arr(getattr(pb, name + "_val")))
-            setattr(d, "A_" + name, b)
-        d.fs_diag = arr(pb.fs)
         d.opts = default_options(**opts)
         self.allocator = None
         if allocator == "torch":
@@ -293,6 +281,26 @@ class Tsp:
         self.h = h
         _LIVE.add(self)
 
+    def _desc(self, pb, device_inputs, keep):
+        """tsp_desc with the grid, this rank and the four blocks + fs_diag of `pb` (arrays kept alive in `keep`)."""
+        def arr(x):
+            if device_inputs or hasattr(x, "data_ptr"):   # CUDA tensors, or pinned host tensors
+                keep.append(x)
+                return _ptr(x)
+            y = np.ascontiguousarray(x)
+            keep.append(y)
+            return _ptr(y)
+
+        d = tsp_desc()
+        d.nx, d.ny, d.nz = pb.nx, pb.ny, pb.nz
+        d.rank, d.nranks = self._grid
+        d.inputs_on_device = int(device_inputs)
+        for name in ("uu", "uf", "fu", "ff"):
+            b = tsp_bsr(arr(getattr(pb, name + "_rowptr")), arr(getattr(pb, name + "_col")), arr(getattr(pb, name + "_val")))
+            setattr(d, "A_" + name, b)
+        d.fs_diag = arr(pb.fs)
+        return d
+
     def close(self):
         if getattr(self, "h", None):
             lib().tsp_destroy(self.h)
@@ -303,6 +311,18 @@ class Tsp:
     def setup(self, what=TSP_SETUP_MECH | TSP_SETUP_FLOW):
         _check(lib().tsp_setup(self.h, what), "tsp_setup")
         return self
+
+    def update_values(self, pb, device_inputs=False):
+        """tsp_update_values: a Newton step's new values on the same patterns (NEXT-f1)."""
+        keep = []
+        d = self._desc(pb, device_inputs, keep)
+        _check(lib().tsp_update_values(self.h, C.byref(d)), "tsp_update_values")
+        self.pb = pb
+        return self
+
+    def setup_flow(self, refresh=False):
+        """tsp_setup(FLOW [| REFRESH]): the per-Newton flow phase; refresh keeps the pressure aggregation."""
+        return self.setup(TSP_SETUP_FLOW | (TSP_SETUP_REFRESH if refresh else 0))
 
     def apply_preconditioner(self, v, z):
         _check(lib().tsp_apply_preconditioner(self.h, _ptr(v), _ptr(z)), "tsp_apply_preconditioner")
