@@ -80,11 +80,16 @@ typedef struct {
                                     16^3 tile as the "processor" (option 1, the staircase) */
     int local_sweeps;            /* Algorithm 1 steps 6-8 repeated this many times (default 1; the staircase used 3) */
     /* AMG smoother of both hierarchies */
-    int amg_smoother;            /* 0 l1-Jacobi (north_star; R-cycle); 1 Gauss-Seidel, forward on the way down and backward
+    int amg_smoother;            /* 0 l1-Jacobi (north_star; R-cycle); 2 Chebyshev (below); 1 Gauss-Seidel, forward on the way down and backward
                                     on the way up (reading R-gs): multicolour GS on level 0 (parity colourings), hybrid
                                     l1-GS on the coarse levels with blocks of amg_gs_block rows as the "processors";
                                     single GPU only */
     int amg_gs_block;            /* rows per hybrid block (default 1024, range [32, 1024]) */
+    /* amg_smoother = 2: Chebyshev polynomial smoother on D_l1^-1 A (north_star "Jacobi/Chebyshev"; SURVEY NEXT-f3;
+       DESIGN.md R-cheb): amg_cheb_degree steps of the Chebyshev iteration per pre-/post-smoothing on the interval
+       [amg_cheb_lower, 1] (1 = the l1 bound of the spectrum); multi-GPU capable */
+    int amg_cheb_degree;         /* default 2, range [1, 8] */
+    double amg_cheb_lower;       /* default 0.3, range (0, 1) */
 } tsp_options;
 
 /* BSR block matrix given to tsp_create (nrows block rows). */

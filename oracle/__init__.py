@@ -36,7 +36,8 @@ class Opts(C.Structure):
                 ("mech_mode", C.c_int), ("pres_mode", C.c_int), ("local_mode", C.c_int), ("ff_mode", C.c_int),
                 ("cpr_mode", C.c_int), ("aps_mode", C.c_int), ("fs_mode", C.c_int), ("rsl_iters", C.c_int),
                 ("fs_modulus_scale", C.c_double), ("second_stage", C.c_int), ("local_sweeps", C.c_int),
-                ("amg_smoother", C.c_int), ("amg_gs_block", C.c_int)]
+                ("amg_smoother", C.c_int), ("amg_gs_block", C.c_int), ("amg_cheb_degree", C.c_int),
+                ("amg_cheb_lower", C.c_double)]
 
 
 class Info(C.Structure):
@@ -68,6 +69,7 @@ def lib():
         L.orc_level_sizes.argtypes = [C.c_void_p, C.c_int, C.c_int, _P(C.c_int64)]
         L.orc_level_export.argtypes = [C.c_void_p, C.c_int, C.c_int, _I32, _I32, _F64, _I32, _I32, _I32, _F64, _F64]
         L.orc_counters.argtypes = [C.c_void_p, _P(C.c_int64)]
+        L.orc_cheb_smooth.argtypes = [C.c_int, _I32, _I32, _F64, C.c_int, C.c_double, _F64, _F64, _F64]
         L.orc_get_spp.argtypes = [C.c_void_p, _F64, _I32, _I32, _F64]
         L.orc_get_cpr.argtypes = [C.c_void_p, _F64, _F64, _F64]
         L.orc_mis2.argtypes = [C.c_int, _I32, _I32, _U32, C.c_int, _I32, _P(C.c_int)]
@@ -275,6 +277,17 @@ def fmix32(x):
     x = (x * 0xC2B2AE35) & 0xFFFFFFFF
     x ^= x >> 16
     return x.astype(np.uint32)
+
+
+def cheb_smooth(rp, ci, v, b, x0=None, degree=2, lower=0.3):
+    """R-cheb: `degree` Chebyshev steps on D_l1^-1 A (scalar CSR) from x0 (None = 0)."""
+    n = len(rp) - 1
+    keep = [np.ascontiguousarray(rp, np.int32), np.ascontiguousarray(ci, np.int32), np.ascontiguousarray(v, np.float64),
+            np.ascontiguousarray(b, np.float64), None if x0 is None else np.ascontiguousarray(x0, np.float64)]
+    x = np.empty(n)
+    if lib().orc_cheb_smooth(n, _p(keep[0]), _p(keep[1]), _p(keep[2]), degree, lower, _p(keep[3]), _p(keep[4]), _p(x)):
+        raise ValueError("orc_cheb_smooth: bad degree / interval")
+    return x
 
 
 class Amg:

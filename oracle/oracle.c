@@ -693,6 +693,57 @@ static int amg_refresh(ohier *H, const mcsr *A0)
     return 0;
 }
 
+/* Chebyshev smoother (reading R-cheb; north_star "fused Jacobi/Chebyshev ... AMG smoothers"): `degree` steps of
+ * the Chebyshev iteration (Saad, Iterative Methods for Sparse Linear Systems, Alg. 12.1) for D^-1 A x = D^-1 b with
+ * D the signed l1 diagonal (R-l1), on the interval [a, b] = [lower, 1] -- b = 1 because D_l1 >= A (Gershgorin on the
+ * rows of D_l1^-1 A), a = lower * b (hypre's default fraction 0.3):
+ *   theta = (b + a)/2, delta = (b - a)/2, sigma = theta/delta, rho_0 = 1/sigma
+ *   r_0 = D^-1 (b - A x_0), d_0 = r_0 / theta, x_1 = x_0 + d_0
+ *   for k = 1 .. degree-1:  rho_k = 1/(2 sigma - rho_{k-1}),  r_k = D^-1 (b - A x_k),
+ *                           d_k = rho_k rho_{k-1} d_{k-1} + (2 rho_k / delta) r_k,  x_{k+1} = x_k + d_k
+ * dl1 == 0 rows take r = 0 (as l1-Jacobi). from_zero: x_0 = 0 (then r_0 = D^-1 b without a product). */
+static void cheb_smooth(const mcsr *A, int c, const double *dl1, int degree, double lower, const double *b, double *x,
+                        int from_zero)
+{
+    const int n = A->n;
+    const double bb = 1.0, aa = lower * bb;
+    const double theta = 0.5 * (bb + aa), delta = 0.5 * (bb - aa), sigma = theta / delta;
+    double *r = (double *)xmalloc(sizeof(double) * (n + 1)), *d = (double *)xmalloc(sizeof(double) * (n + 1));
+    double rho = 1.0 / sigma;
+    for (int k = 0; k < degree; ++k) {
+        /* r_k = D^-1 (b - A x_k) */
+        for (int i = 0; i < n; ++i) {
+            double s = b[i];
+            if (!(k == 0 && from_zero))
+                for (int64_t q = A->rp[i]; q < A->rp[i + 1]; ++q) s -= A->v[c][q] * x[A->ci[q]];
+            r[i] = dl1[i] != 0.0 ? s / dl1[i] : 0.0;
+        }
+        if (k == 0) {
+            for (int i = 0; i < n; ++i) { d[i] = r[i] / theta; x[i] = (from_zero ? 0.0 : x[i]) + d[i]; }
+        } else {
+            const double rho_new = 1.0 / (2.0 * sigma - rho);
+            for (int i = 0; i < n; ++i) { d[i] = rho_new * rho * d[i] + (2.0 * rho_new / delta) * r[i]; x[i] = x[i] + d[i]; }
+            rho = rho_new;
+        }
+    }
+    free(r); free(d);
+}
+
+int orc_cheb_smooth(int n, const int32_t *rp, const int32_t *ci, const double *v, int degree, double lower,
+                    const double *b, const double *x0, double *x)
+{
+    if (degree < 1 || !(lower > 0.0 && lower < 1.0)) return -1;
+    olevel L; memset(&L, 0, sizeof(L));
+    mcsr_alloc(&L.A, n, n, 1, rp[n]);
+    memcpy(L.A.rp, rp, sizeof(int32_t) * (n + 1)); memcpy(L.A.ci, ci, sizeof(int32_t) * rp[n]);
+    memcpy(L.A.v[0], v, sizeof(double) * rp[n]);
+    l1_diag(&L);
+    for (int i = 0; i < n; ++i) x[i] = x0 ? x0[i] : 0.0;
+    cheb_smooth(&L.A, 0, L.dl1[0], degree, lower, b, x, x0 == NULL);
+    free(L.dl1[0]); mcsr_free(&L.A);
+    return 0;
+}
+
 /* V(1,1)-cycle with l1-Jacobi, zero initial guess (R-cycle), component c:
  *   x = D^-1 b; r = b - A x; b_c = R r; x_c = cycle(b_c); x += P x_c; x += D^-1 (b - A x)
  * amg_smoother 1 (R-gs): x = forward GS sweep from 0; ... ; backward GS sweep on x */
@@ -703,7 +754,9 @@ static void vcycle(const ohier *H, int lvl, int c, const double *b, double *x)
     if (L->coarsest) { dense_lu_solve(n, L->lu[c], L->piv[c], b, x); return; }
     static int lvmax = -2; if (lvmax == -2) { const char *e = getenv("ORC_GS_MAXLVL"); lvmax = e ? atoi(e) : 99; }
     const int gs = H->o.amg_smoother == 1 && lvl <= lvmax;
+    const int cheb = H->o.amg_smoother == 2;
     if (gs) { for (int i = 0; i < n; ++i) x[i] = 0.0; gs_sweep(L, c, b, x, 0); }       /* forward GS from zero */
+    else if (cheb) cheb_smooth(&L->A, c, L->dl1[c], H->o.amg_cheb_degree, H->o.amg_cheb_lower, b, x, 1);
     else for (int i = 0; i < n; ++i) x[i] = L->dl1[c][i] != 0.0 ? b[i] / L->dl1[c][i] : 0.0;
     double *r = (double *)xmalloc(sizeof(double) * (n + 1));
     memcpy(r, b, sizeof(double) * n);
@@ -718,6 +771,7 @@ static void vcycle(const ohier *H, int lvl, int c, const double *b, double *x)
         x[i] += s;
     }
     if (gs) gs_sweep(L, c, b, x, 1);                                                       /* backward GS */
+    else if (cheb) cheb_smooth(&L->A, c, L->dl1[c], H->o.amg_cheb_degree, H->o.amg_cheb_lower, b, x, 0);
     else {
         memcpy(r, b, sizeof(double) * n);
         spmv_sub(&L->A, c, x, r);
@@ -937,6 +991,7 @@ void orc_default_opts(orc_opts *o)
     o->rsl_iters = 2; o->fs_modulus_scale = 1.0;
     o->second_stage = 0; o->local_sweeps = 1;
     o->amg_smoother = 0; o->amg_gs_block = 1024;
+    o->amg_cheb_degree = 2; o->amg_cheb_lower = 0.3;
 }
 
 orc *orc_create(const orc_desc *d, const orc_opts *o)

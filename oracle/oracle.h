@@ -45,6 +45,9 @@ typedef struct {
     int amg_smoother;             /* 0: l1-Jacobi (R-cycle, north_star); 1: Gauss-Seidel forward on the way down, backward on
                                      the way up (R-gs): multicolour on level 0, hybrid l1-GS on the coarse levels */
     int amg_gs_block;             /* R-gs hybrid levels: rows per "processor" block (1024) */
+    /* amg_smoother 2: Chebyshev polynomial smoother (north_star "Jacobi/Chebyshev"; reading R-cheb) */
+    int amg_cheb_degree;          /* polynomial degree per smoothing step (2) */
+    double amg_cheb_lower;        /* interval [lower, 1] of D_l1^-1 A (the l1 bound makes 1 the upper end), 0.3 */
 } orc_opts;
 
 typedef struct {
@@ -99,4 +102,7 @@ void orc_ilu_apply(void *ilu, const double *w, double *dz);
 void orc_ilu_free(void *ilu);
 void *orc_bgs_build(int nx, int ny, int nz, int tx, int ty, int tz, const int32_t *rp, const int32_t *ci, const double *v);
 void orc_bgs_apply(void *bgs, const double *w, double *dz);     /* one hbgs sweep from zero: tile (L+D)^-1 w */
+/* R-cheb: `degree` Chebyshev steps on D_l1^-1 A (scalar CSR, the oracle's l1 rule) from x0 (NULL = 0) */
+int orc_cheb_smooth(int n, const int32_t *rp, const int32_t *ci, const double *v, int degree, double lower,
+                    const double *b, const double *x0, double *x);
 #endif

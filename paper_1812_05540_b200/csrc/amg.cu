@@ -1031,6 +1031,7 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
         }
         size_t m = (size_t)std::max(L.n, 1) * nc;
         L.b.alloc(m); L.x.alloc(m); L.x2.alloc(m); L.r.alloc(m);
+        if (c.o.amg_smoother == 2) L.dcheb.alloc(m); else L.dcheb.release();
         {   // kernel choice from global mean row lengths, so every rank computes a row exactly like P = 1
             std::vector<int64_t> st = {L.A.nnz, (int64_t)L.n, L.coarsest ? 0 : L.R.nnz, L.coarsest ? 0 : (int64_t)L.R.n};
             if (L.dist) {
@@ -1147,11 +1148,11 @@ __global__ void __launch_bounds__(256) k_vc_post(int n, const int64_t *__restric
         xo[t] = x.own[t] + dinv[t] * (b[t] - acc[c]);
     }
 }
-// residual r = b - A x (Gauss-Seidel smoother: after the forward sweep)
-template <int NC>
+// residual r = b - A x (Gauss-Seidel smoother after the forward sweep; Chebyshev steps; x ghost-aware)
+template <int NC, bool D>
 __global__ void __launch_bounds__(256) k_sell_resid(int n, const int64_t *__restrict__ off, const int32_t *__restrict__ col,
                                                     const double *__restrict__ val, const double *__restrict__ b,
-                                                    const double *__restrict__ x, double *__restrict__ r)
+                                                    GV x, double *__restrict__ r)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -1164,10 +1165,21 @@ __global__ void __launch_bounds__(256) k_sell_resid(int n, const int64_t *__rest
     for (int64_t slot = b0; slot < b1; ++slot) {
         const int j = __ldcs(col + slot * 32 + lane);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) acc[c] = fma(__ldcs(val + (slot * NC + c) * 32 + lane), __ldg(x + (int64_t)j * NC + c), acc[c]);
+        for (int c = 0; c < NC; ++c) acc[c] = fma(__ldcs(val + (slot * NC + c) * 32 + lane), gvld<D>(x, j, c, NC), acc[c]);
     }
 #pragma unroll
     for (int c = 0; c < NC; ++c) r[(int64_t)i * NC + c] = b[(int64_t)i * NC + c] - acc[c];
+}
+// one Chebyshev step after its residual (R-cheb): d = alpha d + beta D^-1 r (alpha ignored when first);
+// xo = x + d (x == nullptr: from zero).  In place (xo == x) is fine: every entry is its own.
+__global__ void k_cheb_upd(int64_t m, const double *__restrict__ r, const double *__restrict__ dinv, double *__restrict__ d,
+                           const double *x, double *xo, double alpha, double beta, int first)
+{
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= m) return;
+    const double dn = (first ? 0.0 : alpha * d[t]) + beta * (dinv[t] * r[t]);
+    d[t] = dn;
+    xo[t] = (x ? x[t] : 0.0) + dn;
 }
 // coarsest: x = A_c^-1 b per component
 template <int NC>
@@ -1249,6 +1261,45 @@ __global__ void k_rep_compact(int nranks, int nc, int64_t mx, const int64_t *__r
 static double sbytes(const Sell &S) { return (double)S.slots * 32 * (4.0 + 8.0 * S.bs); }
 static double cbytes(const Csr &A) { return (double)A.nnz * (4.0 + 8.0 * A.nc); }
 
+// r = b - A x on level l (x's ghosts exchanged first on a distributed level)
+template <int NC>
+static void level_resid(Ctx &c, Level &L, bool sym0, const double *b, const double *x, double *r)
+{
+    const int n = L.n;
+    if (L.dist) halo_exchange(c, *L.hp, NC, x, L.gh_x);
+    const GV gx = gv(x, n, L.dist ? L.gh_x.p : nullptr);
+    if (sym0) sym_vcycle_resid(c, n, b, gx, r);
+    else if (L.warpA) (L.dist ? csr_vec<NC, 3, true> : csr_vec<NC, 3, false>)(L.warpA, c.s, n, L.A, gv(nullptr, 0), gv(b, n), gx, r, nullptr);
+    else if (n) (L.dist ? k_sell_resid<NC, true> : k_sell_resid<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
+        n, L.sA.off, L.sA.col, L.sA.val, b, gx, r);
+    c.launches++;
+}
+
+// Chebyshev smoother (R-cheb; the oracle's cheb_smooth): `amg_cheb_degree` steps of the Chebyshev iteration on
+// D_l1^-1 A over [lower, 1]; from_zero: x_0 = 0 (the first step needs no product), else x_0 = xin.  Result in x
+// (x != xin).  Steps: residual kernel + one elementwise update.
+template <int NC>
+static void cheb_run(Ctx &c, Level &L, bool sym0, const double *b, const double *xin, double *x, bool from_zero)
+{
+    const int64_t m = (int64_t)L.n * NC;
+    const double bb = 1.0, aa = c.o.amg_cheb_lower * bb;
+    const double theta = 0.5 * (bb + aa), delta = 0.5 * (bb - aa), sigma = theta / delta;
+    double rho = 1.0 / sigma;
+    for (int k = 0; k < c.o.amg_cheb_degree; ++k) {
+        const double *xk = k == 0 ? (from_zero ? nullptr : xin) : x;
+        const double *r = b;
+        if (xk) { level_resid<NC>(c, L, sym0, b, xk, L.r); r = L.r; }
+        double alpha = 0.0, beta = 1.0 / theta;
+        if (k > 0) {
+            const double rho_new = 1.0 / (2.0 * sigma - rho);
+            alpha = rho_new * rho; beta = 2.0 * rho_new / delta;
+            rho = rho_new;
+        }
+        if (m) k_cheb_upd<<<grid_for(m, 256), 256, 0, c.s>>>(m, r, L.dinv, L.dcheb, xk, x, alpha, beta, k == 0);
+        c.launches++;
+    }
+}
+
 template <int NC>
 static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
 {
@@ -1272,18 +1323,22 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     const bool sym0 = mech && l == 0 && c.sym_sdc.ok;     // structured symmetric level 0 (sym.cu)
     const double bA0 = sym0 ? sym_bytes(c, 3) : bA;
     const bool gs = c.o.amg_smoother == 1;   // Gauss-Seidel (gs.cu, R-gs): single GPU, never distributed
+    const bool cheb = c.o.amg_smoother == 2; // Chebyshev (R-cheb)
+    const int deg = c.o.amg_cheb_degree;
     prof_begin(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P);
     if (gs) {
         gs_sweep<NC>(c, L, false, b, nullptr, L.x2);                      // forward sweep from zero
-        if (sym0) sym_vcycle_resid(c, n, b, gv(L.x2, n), L.r);
-        else if (wA) csr_vec<NC, 3, false>(wA, c.s, n, L.A, gv(nullptr, 0), gv(b, n), gv(L.x2, n), L.r, nullptr);
-        else if (n) k_sell_resid<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sA.off, L.sA.col, L.sA.val, b, L.x2, L.r);
+        level_resid<NC>(c, L, sym0, b, L.x2, L.r);
+    } else if (cheb) {
+        cheb_run<NC>(c, L, sym0, b, nullptr, L.x2, true);
+        level_resid<NC>(c, L, sym0, b, L.x2, L.r);
     }
     else if (sym0) sym_vcycle_pre(c, n, gd, gb, L.x2, L.r);
     else if (wA) (L.dist ? csr_vec<NC, 1, true> : csr_vec<NC, 1, false>)(wA, c.s, n, L.A, gd, gb, gv(nullptr, 0), L.x2, L.r);
     else if (n) (L.dist ? k_vc_pre<NC, true> : k_vc_pre<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
         n, L.sA.off, L.sA.col, L.sA.val, gd, gb, L.x2, L.r);
-    prof_end(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P, gs ? gs_sweep_bytes(L, NC) + bA0 + 3 * vec : bA0 + 4 * vec);
+    prof_end(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P, gs ? gs_sweep_bytes(L, NC) + bA0 + 3 * vec
+                                                  : cheb ? deg * (bA0 + 3 * vec) + (deg - 1) * 7 * vec + 4 * vec : bA0 + 4 * vec);
     // restriction (local rows of R); a replicated next level is gathered on every rank
     Level &Lc = H.L[l + 1];
     const bool gather = L.dist && !L.next_dist;
@@ -1306,15 +1361,16 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     if (n) k_prolong<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sP.off, L.sP.col, L.sP.val, Lc.x, L.x2);
     prof_end(c, mech ? PK_VC_PROL_U : PK_VC_PROL_P, sbytes(L.sP) + 2 * vec + 8.0 * NC * Lc.n);
     // post-smooth (needs x of the ghost rows)
-    if (L.dist) halo_exchange(c, *L.hp, NC, L.x2, L.gh_x);
+    if (L.dist && !cheb) halo_exchange(c, *L.hp, NC, L.x2, L.gh_x);
     const GV gx = gv(L.x2, n, L.dist ? L.gh_x.p : nullptr);
     prof_begin(c, mech ? PK_VC_POST_U : PK_VC_POST_P);
     if (gs) gs_sweep<NC>(c, L, true, b, L.x2, xout);                      // backward sweep
+    else if (cheb) cheb_run<NC>(c, L, sym0, b, L.x2, xout, false);
     else if (sym0) sym_vcycle_post(c, n, L.dinv, b, gx, xout);
     else if (wA) (L.dist ? csr_vec<NC, 2, true> : csr_vec<NC, 2, false>)(wA, c.s, n, L.A, gv(L.dinv, n), gv(b, n), gx, xout, nullptr);
     else if (n) (L.dist ? k_vc_post<NC, true> : k_vc_post<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
         n, L.sA.off, L.sA.col, L.sA.val, L.dinv, b, gx, xout);
-    prof_end(c, mech ? PK_VC_POST_U : PK_VC_POST_P, gs ? gs_sweep_bytes(L, NC) : bA0 + 4 * vec);
+    prof_end(c, mech ? PK_VC_POST_U : PK_VC_POST_P, gs ? gs_sweep_bytes(L, NC) : cheb ? deg * (bA0 + 3 * vec + 7 * vec) : bA0 + 4 * vec);
     c.launches += 4;
 }
 

@@ -215,6 +215,7 @@ tsp_status tsp_default_options(tsp_options *o)
     o->rsl_iters = 2; o->fs_modulus_scale = 1.0;
     o->second_stage = 0; o->local_sweeps = 1;
     o->amg_smoother = 0; o->amg_gs_block = 1024;
+    o->amg_cheb_degree = 2; o->amg_cheb_lower = 0.3;
     return TSP_OK;
 }
 
@@ -251,7 +252,12 @@ tsp_status tsp_create(tsp_handle *out, const tsp_desc *d)
     if (c->o.local_sweeps <= 0) c->o.local_sweeps = 1;
     TSP_REQUIRE(c->o.second_stage == 0 || c->o.second_stage == 1, TSP_ERR_INVALID_ARG, "second_stage must be 0 (ILU0) or 1 (BGS)");
     if (c->o.amg_gs_block <= 0) c->o.amg_gs_block = 1024;
-    TSP_REQUIRE(c->o.amg_smoother == 0 || c->o.amg_smoother == 1, TSP_ERR_INVALID_ARG, "amg_smoother must be 0 (l1-Jacobi) or 1 (GS)");
+    TSP_REQUIRE(c->o.amg_smoother >= 0 && c->o.amg_smoother <= 2, TSP_ERR_INVALID_ARG,
+                "amg_smoother must be 0 (l1-Jacobi), 1 (GS) or 2 (Chebyshev)");
+    if (c->o.amg_cheb_degree == 0) c->o.amg_cheb_degree = 2;
+    if (c->o.amg_cheb_lower == 0.0) c->o.amg_cheb_lower = 0.3;
+    TSP_REQUIRE(c->o.amg_cheb_degree >= 1 && c->o.amg_cheb_degree <= 8, TSP_ERR_INVALID_ARG, "amg_cheb_degree must be in [1, 8]");
+    TSP_REQUIRE(c->o.amg_cheb_lower > 0.0 && c->o.amg_cheb_lower < 1.0, TSP_ERR_INVALID_ARG, "amg_cheb_lower must be in (0, 1)");
     if (!(c->o.fs_modulus_scale > 0)) c->o.fs_modulus_scale = 1.0;
     TSP_REQUIRE(c->o.cpr_mode == 0 || c->o.cpr_mode == 1, TSP_ERR_INVALID_ARG, "cpr_mode must be 0 (quasi) or 1 (true IMPES)");
     TSP_REQUIRE(c->o.aps_mode == 0 || c->o.aps_mode == 1, TSP_ERR_INVALID_ARG, "aps_mode must be 0 (full) or 1 (diagonal)");

@@ -206,6 +206,7 @@ struct Level {
     DBuf<double> cinv;            // coarsest: dense inverse [nc][n][n]
     // apply work vectors [n][nc]
     DBuf<double> b, x, x2, r;
+    DBuf<double> dcheb;           // Chebyshev smoother direction (amg_smoother = 2)
 };
 
 struct Hier {

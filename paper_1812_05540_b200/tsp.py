@@ -33,7 +33,8 @@ class tsp_options(C.Structure):
                 ("zblock", C.c_int), ("tile_x", C.c_int), ("tile_y", C.c_int), ("tile_z", C.c_int),
                 ("replicate_rows", C.c_int), ("cpr_mode", C.c_int), ("aps_mode", C.c_int), ("fs_mode", C.c_int),
                 ("rsl_iters", C.c_int), ("fs_modulus_scale", C.c_double), ("second_stage", C.c_int),
-                ("local_sweeps", C.c_int), ("amg_smoother", C.c_int), ("amg_gs_block", C.c_int)]
+                ("local_sweeps", C.c_int), ("amg_smoother", C.c_int), ("amg_gs_block", C.c_int),
+                ("amg_cheb_degree", C.c_int), ("amg_cheb_lower", C.c_double)]
 
 
 class tsp_bsr(C.Structure):

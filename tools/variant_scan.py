@@ -14,7 +14,16 @@ VARIANTS = [
     ("hbgs x3 (staircase M_L)", dict(second_stage=1, local_sweeps=3)),
     ("ILU x2", dict(local_sweeps=2)),
     ("ILU x2 + modulus 1.8 + diagonal A_ps", dict(local_sweeps=2, fs_modulus_scale=1.8, aps_mode=1)),
+    ("GS AMG smoothers (P:711)", dict(amg_smoother=1)),
+    ("GS AMG smoothers + hbgs x3 (the paper's staircase settings)", dict(amg_smoother=1, second_stage=1, local_sweeps=3)),
+    ("GS AMG smoothers + ILU x2", dict(amg_smoother=1, local_sweeps=2)),
+    ("Chebyshev(2) AMG smoothers", dict(amg_smoother=2)),
+    ("Chebyshev(3) AMG smoothers", dict(amg_smoother=2, amg_cheb_degree=3)),
+    ("Chebyshev(2) on [0.1, 1]", dict(amg_smoother=2, amg_cheb_lower=0.1)),
+    ("Chebyshev(2) AMG smoothers + ILU x2", dict(amg_smoother=2, local_sweeps=2)),
 ]
+if len(sys.argv) > 2:   # only the variants whose name contains this word
+    VARIANTS = [v for v in VARIANTS if sys.argv[2] in v[0]]
 pb = synth.generate(cfg)
 b = torch.from_numpy(pb.b).cuda()
 for name, opts in VARIANTS:
