@@ -1031,7 +1031,7 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
         }
         size_t m = (size_t)std::max(L.n, 1) * nc;
         L.b.alloc(m); L.x.alloc(m); L.x2.alloc(m); L.r.alloc(m);
-        if (c.o.amg_smoother == 2) L.dcheb.alloc(m); else L.dcheb.release();
+        if (c.o.amg_smoother == 2) { L.dcheb.alloc(m); L.xc.alloc(m); } else { L.dcheb.release(); L.xc.release(); }
         {   // kernel choice from global mean row lengths, so every rank computes a row exactly like P = 1
             std::vector<int64_t> st = {L.A.nnz, (int64_t)L.n, L.coarsest ? 0 : L.R.nnz, L.coarsest ? 0 : (int64_t)L.R.n};
             if (L.dist) {
@@ -1170,6 +1170,34 @@ __global__ void __launch_bounds__(256) k_sell_resid(int n, const int64_t *__rest
 #pragma unroll
     for (int c = 0; c < NC; ++c) r[(int64_t)i * NC + c] = b[(int64_t)i * NC + c] - acc[c];
 }
+// fused Chebyshev step on a SELL operator (R-cheb, cheb_epi): PRE gathers sc dinv_j b_j, STEP gathers x_j
+template <int NC, bool D, bool PRE>
+__global__ void __launch_bounds__(256) k_cheb_sell(int n, const int64_t *__restrict__ off, const int32_t *__restrict__ col,
+                                                   const double *__restrict__ val, GV dinv, GV b, GV x, ChebArgs ca,
+                                                   double *__restrict__ xo)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int s = i >> 5, lane = i & 31;
+    double acc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+    const int64_t b0 = off[s], b1 = off[s + 1];
+#pragma unroll 2
+    for (int64_t slot = b0; slot < b1; ++slot) {
+        const int j = __ldcs(col + slot * 32 + lane);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            const double xv = PRE ? ca.sc * (gvld<D>(dinv, j, c, NC) * gvld<D>(b, j, c, NC)) : gvld<D>(x, j, c, NC);
+            acc[c] = fma(__ldcs(val + (slot * NC + c) * 32 + lane), xv, acc[c]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const int64_t t = (int64_t)i * NC + c;
+        cheb_epi<PRE>(t, acc[c], b.own[t], dinv.own[t], PRE ? 0.0 : x.own[t], ca, xo);
+    }
+}
 // one Chebyshev step after its residual (R-cheb): d = alpha d + beta D^-1 r (alpha ignored when first);
 // xo = x + d (x == nullptr: from zero).  In place (xo == x) is fine: every entry is its own.
 __global__ void k_cheb_upd(int64_t m, const double *__restrict__ r, const double *__restrict__ dinv, double *__restrict__ d,
@@ -1199,11 +1227,11 @@ __global__ void k_coarse(int n, const double *__restrict__ inv, const double *__
 // then a fixed shuffle tree inside the group.  32/G rows per warp keep several dependent
 // load chains in flight.
 // MODE 0: y = A x ; MODE 1: pre (x = D^-1 b, r = b - A D^-1 b) ; MODE 2: post (xo = x + D^-1 (b - A x));
-// MODE 3: residual r = b - A x
+// MODE 3: residual r = b - A x ; MODE 4 / 5: fused Chebyshev PRE / STEP (cheb_epi, R-cheb)
 template <int NC, int MODE, bool D, int G>
 __global__ void __launch_bounds__(256) k_csr_vec(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
                                                  const double *__restrict__ v, GV dinv, GV b, GV x,
-                                                 double *__restrict__ out1, double *__restrict__ out2)
+                                                 double *__restrict__ out1, double *__restrict__ out2, ChebArgs ca)
 {
     const int sub = threadIdx.x & (G - 1);
     const int i = blockIdx.x * (blockDim.x / G) + (threadIdx.x / G);
@@ -1218,7 +1246,8 @@ __global__ void __launch_bounds__(256) k_csr_vec(int n, const int32_t *__restric
             const int j = ci[q];
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
-                const double xv = MODE == 1 ? gvld<D>(b, j, c, NC) * gvld<D>(dinv, j, c, NC) : gvld<D>(x, j, c, NC);
+                const double xv = MODE == 1 ? gvld<D>(b, j, c, NC) * gvld<D>(dinv, j, c, NC)
+                                : MODE == 4 ? ca.sc * (gvld<D>(dinv, j, c, NC) * gvld<D>(b, j, c, NC)) : gvld<D>(x, j, c, NC);
                 acc[c] = fma(__ldcs(v + q * NC + c), xv, acc[c]);
             }
         }
@@ -1235,18 +1264,20 @@ __global__ void __launch_bounds__(256) k_csr_vec(int n, const int32_t *__restric
         if (MODE == 0) out1[t] = a;
         else if (MODE == 1) { out1[t] = b.own[t] * dinv.own[t]; out2[t] = b.own[t] - a; }
         else if (MODE == 3) out1[t] = b.own[t] - a;
+        else if (MODE == 4 || MODE == 5) cheb_epi<MODE == 4>(t, a, b.own[t], dinv.own[t], MODE == 5 ? x.own[t] : 0.0, ca, out1);
         else out1[t] = x.own[t] + dinv.own[t] * (b.own[t] - a);
     }
 }
 template <int NC, int MODE, bool D>
-static void csr_vec(int G, cudaStream_t s, int n, const Csr &A, GV dinv, GV b, GV x, double *o1, double *o2)
+static void csr_vec(int G, cudaStream_t s, int n, const Csr &A, GV dinv, GV b, GV x, double *o1, double *o2,
+                    const ChebArgs &ca)
 {
     if (!n) return;
     const int rows = 256 / G;
     const dim3 grid((unsigned)((n + rows - 1) / rows));
-    if (G == 8) k_csr_vec<NC, MODE, D, 8><<<grid, 256, 0, s>>>(n, A.rp, A.ci, A.v, dinv, b, x, o1, o2);
-    else if (G == 16) k_csr_vec<NC, MODE, D, 16><<<grid, 256, 0, s>>>(n, A.rp, A.ci, A.v, dinv, b, x, o1, o2);
-    else k_csr_vec<NC, MODE, D, 32><<<grid, 256, 0, s>>>(n, A.rp, A.ci, A.v, dinv, b, x, o1, o2);
+    if (G == 8) k_csr_vec<NC, MODE, D, 8><<<grid, 256, 0, s>>>(n, A.rp, A.ci, A.v, dinv, b, x, o1, o2, ca);
+    else if (G == 16) k_csr_vec<NC, MODE, D, 16><<<grid, 256, 0, s>>>(n, A.rp, A.ci, A.v, dinv, b, x, o1, o2, ca);
+    else k_csr_vec<NC, MODE, D, 32><<<grid, 256, 0, s>>>(n, A.rp, A.ci, A.v, dinv, b, x, o1, o2, ca);
 }
 // compact the padded allgather [rank][mx*nc] into the full replicated vector
 __global__ void k_rep_compact(int nranks, int nc, int64_t mx, const int64_t *__restrict__ offs, const double *__restrict__ buf,
@@ -1269,34 +1300,76 @@ static void level_resid(Ctx &c, Level &L, bool sym0, const double *b, const doub
     if (L.dist) halo_exchange(c, *L.hp, NC, x, L.gh_x);
     const GV gx = gv(x, n, L.dist ? L.gh_x.p : nullptr);
     if (sym0) sym_vcycle_resid(c, n, b, gx, r);
-    else if (L.warpA) (L.dist ? csr_vec<NC, 3, true> : csr_vec<NC, 3, false>)(L.warpA, c.s, n, L.A, gv(nullptr, 0), gv(b, n), gx, r, nullptr);
+    else if (L.warpA) (L.dist ? csr_vec<NC, 3, true> : csr_vec<NC, 3, false>)(L.warpA, c.s, n, L.A, gv(nullptr, 0), gv(b, n), gx, r, nullptr, ChebArgs{});
     else if (n) (L.dist ? k_sell_resid<NC, true> : k_sell_resid<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
         n, L.sA.off, L.sA.col, L.sA.val, b, gx, r);
     c.launches++;
 }
 
 // Chebyshev smoother (R-cheb; the oracle's cheb_smooth): `amg_cheb_degree` steps of the Chebyshev iteration on
-// D_l1^-1 A over [lower, 1]; from_zero: x_0 = 0 (the first step needs no product), else x_0 = xin.  Result in x
-// (x != xin).  Steps: residual kernel + one elementwise update.
+// D_l1^-1 A over [lower, 1].  Fused kernels (cheb_epi): pre-smoothing from zero does steps 0 and 1 in ONE product
+// (PRE), every further step and each post-smoothing step is one product + epilogue (STEP); degree 1 pre-smoothing
+// is the elementwise x = D^-1 b / theta.  x_0 = xin (post) or 0 (pre); the result lands in `x` (!= xin); `tmp` is
+// the ping-pong buffer.
 template <int NC>
-static void cheb_run(Ctx &c, Level &L, bool sym0, const double *b, const double *xin, double *x, bool from_zero)
+static void cheb_step(Ctx &c, Level &L, bool sym0, bool pre, const double *b, const double *xk, const ChebArgs &a, double *xo)
+{
+    const int n = L.n;
+    const GV gd = gv(L.dinv, n, L.dist ? L.dinv_gh.p : nullptr);
+    GV gb = gv(b, n), gx = gv(nullptr, 0);
+    if (pre) {
+        if (L.dist) { halo_exchange(c, *L.hp, NC, b, L.gh_b); gb = gv(b, n, L.gh_b.p); }
+    } else {
+        if (L.dist) halo_exchange(c, *L.hp, NC, xk, L.gh_x);
+        gx = gv(xk, n, L.dist ? L.gh_x.p : nullptr);
+    }
+    if (sym0) sym_vcycle_cheb(c, n, pre, gd, gb, gx, a, xo);
+    else if (L.warpA) {
+        if (pre) (L.dist ? csr_vec<NC, 4, true> : csr_vec<NC, 4, false>)(L.warpA, c.s, n, L.A, gd, gb, gx, xo, nullptr, a);
+        else (L.dist ? csr_vec<NC, 5, true> : csr_vec<NC, 5, false>)(L.warpA, c.s, n, L.A, gd, gb, gx, xo, nullptr, a);
+    } else if (n) {
+#define CHS(DD, PP) k_cheb_sell<NC, DD, PP><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sA.off, L.sA.col, L.sA.val, gd, gb, gx, a, xo)
+        if (L.dist) { if (pre) CHS(true, true); else CHS(true, false); }
+        else { if (pre) CHS(false, true); else CHS(false, false); }
+#undef CHS
+    }
+    c.launches++;
+}
+
+template <int NC>
+static void cheb_run(Ctx &c, Level &L, bool sym0, const double *b, const double *xin, double *x, double *tmp, bool from_zero)
 {
     const int64_t m = (int64_t)L.n * NC;
+    const int deg = c.o.amg_cheb_degree;
     const double bb = 1.0, aa = c.o.amg_cheb_lower * bb;
     const double theta = 0.5 * (bb + aa), delta = 0.5 * (bb - aa), sigma = theta / delta;
+    std::vector<double> al(deg, 0.0), be(deg, 1.0 / theta);   // step k: d_k = al[k] d_{k-1} + be[k] D^-1 r_k
     double rho = 1.0 / sigma;
-    for (int k = 0; k < c.o.amg_cheb_degree; ++k) {
-        const double *xk = k == 0 ? (from_zero ? nullptr : xin) : x;
-        const double *r = b;
-        if (xk) { level_resid<NC>(c, L, sym0, b, xk, L.r); r = L.r; }
-        double alpha = 0.0, beta = 1.0 / theta;
-        if (k > 0) {
-            const double rho_new = 1.0 / (2.0 * sigma - rho);
-            alpha = rho_new * rho; beta = 2.0 * rho_new / delta;
-            rho = rho_new;
+    for (int k = 1; k < deg; ++k) {
+        const double rn = 1.0 / (2.0 * sigma - rho);
+        al[k] = rn * rho; be[k] = 2.0 * rn / delta;
+        rho = rn;
+    }
+    // buffers: the steps alternate between x and tmp so that the last one writes x
+    int k = 0;
+    const double *cur = xin;
+    const int launches = from_zero ? deg - 1 : deg;   // PRE covers steps 0 and 1
+    double *dst = (launches % 2 == 1) ? x : tmp;      // alternate so that the last launch writes x
+    if (from_zero) {
+        if (deg == 1) {
+            if (m) k_cheb_upd<<<grid_for(m, 256), 256, 0, c.s>>>(m, b, L.dinv, L.dcheb, nullptr, x, 0.0, 1.0 / theta, 1);
+            c.launches++;
+            return;
         }
-        if (m) k_cheb_upd<<<grid_for(m, 256), 256, 0, c.s>>>(m, r, L.dinv, L.dcheb, xk, x, alpha, beta, k == 0);
-        c.launches++;
+        ChebArgs a{nullptr, deg > 2 ? L.dcheb.p : nullptr, al[1], be[1], 1.0 / theta};
+        cheb_step<NC>(c, L, sym0, true, b, nullptr, a, dst);
+        cur = dst; dst = (dst == x) ? tmp : x;
+        k = 2;
+    }
+    for (; k < deg; ++k) {
+        ChebArgs a{k == 0 ? nullptr : L.dcheb.p, k + 1 < deg ? L.dcheb.p : nullptr, al[k], be[k], 0.0};
+        cheb_step<NC>(c, L, sym0, false, b, cur, a, dst);
+        cur = dst; dst = (dst == x) ? tmp : x;
     }
 }
 
@@ -1330,22 +1403,22 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
         gs_sweep<NC>(c, L, false, b, nullptr, L.x2);                      // forward sweep from zero
         level_resid<NC>(c, L, sym0, b, L.x2, L.r);
     } else if (cheb) {
-        cheb_run<NC>(c, L, sym0, b, nullptr, L.x2, true);
+        cheb_run<NC>(c, L, sym0, b, nullptr, L.x2, L.xc, true);
         level_resid<NC>(c, L, sym0, b, L.x2, L.r);
     }
     else if (sym0) sym_vcycle_pre(c, n, gd, gb, L.x2, L.r);
-    else if (wA) (L.dist ? csr_vec<NC, 1, true> : csr_vec<NC, 1, false>)(wA, c.s, n, L.A, gd, gb, gv(nullptr, 0), L.x2, L.r);
+    else if (wA) (L.dist ? csr_vec<NC, 1, true> : csr_vec<NC, 1, false>)(wA, c.s, n, L.A, gd, gb, gv(nullptr, 0), L.x2, L.r, ChebArgs{});
     else if (n) (L.dist ? k_vc_pre<NC, true> : k_vc_pre<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
         n, L.sA.off, L.sA.col, L.sA.val, gd, gb, L.x2, L.r);
     prof_end(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P, gs ? gs_sweep_bytes(L, NC) + bA0 + 3 * vec
-                                                  : cheb ? deg * (bA0 + 3 * vec) + (deg - 1) * 7 * vec + 4 * vec : bA0 + 4 * vec);
+                                                  : cheb ? (deg - 1) * (bA0 + 5 * vec) + bA0 + 3 * vec : bA0 + 4 * vec);
     // restriction (local rows of R); a replicated next level is gathered on every rank
     Level &Lc = H.L[l + 1];
     const bool gather = L.dist && !L.next_dist;
     const int nr = L.sR.nrows;
     double *rdst = gather ? L.rep_buf.p + (size_t)c.nranks * 0 : Lc.b.p;
     prof_begin(c, mech ? PK_VC_RESTR_U : PK_VC_RESTR_P);
-    if (wR) csr_vec<NC, 0, false>(wR, c.s, nr, L.R, gv(nullptr, 0), gv(nullptr, 0), gv(L.r, n), rdst, nullptr);
+    if (wR) csr_vec<NC, 0, false>(wR, c.s, nr, L.R, gv(nullptr, 0), gv(nullptr, 0), gv(L.r, n), rdst, nullptr, ChebArgs{});
     else if (nr) k_sell_mv<NC><<<grid_for(nr, 256), 256, 0, c.s>>>(nr, L.sR.off, L.sR.col, L.sR.val, L.r, rdst);
     prof_end(c, mech ? PK_VC_RESTR_U : PK_VC_RESTR_P, bR + vec + 8.0 * NC * nr);
     if (gather) {
@@ -1365,12 +1438,12 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     const GV gx = gv(L.x2, n, L.dist ? L.gh_x.p : nullptr);
     prof_begin(c, mech ? PK_VC_POST_U : PK_VC_POST_P);
     if (gs) gs_sweep<NC>(c, L, true, b, L.x2, xout);                      // backward sweep
-    else if (cheb) cheb_run<NC>(c, L, sym0, b, L.x2, xout, false);
+    else if (cheb) cheb_run<NC>(c, L, sym0, b, L.x2, xout, L.xc, false);
     else if (sym0) sym_vcycle_post(c, n, L.dinv, b, gx, xout);
-    else if (wA) (L.dist ? csr_vec<NC, 2, true> : csr_vec<NC, 2, false>)(wA, c.s, n, L.A, gv(L.dinv, n), gv(b, n), gx, xout, nullptr);
+    else if (wA) (L.dist ? csr_vec<NC, 2, true> : csr_vec<NC, 2, false>)(wA, c.s, n, L.A, gv(L.dinv, n), gv(b, n), gx, xout, nullptr, ChebArgs{});
     else if (n) (L.dist ? k_vc_post<NC, true> : k_vc_post<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
         n, L.sA.off, L.sA.col, L.sA.val, L.dinv, b, gx, xout);
-    prof_end(c, mech ? PK_VC_POST_U : PK_VC_POST_P, gs ? gs_sweep_bytes(L, NC) : cheb ? deg * (bA0 + 3 * vec + 7 * vec) : bA0 + 4 * vec);
+    prof_end(c, mech ? PK_VC_POST_U : PK_VC_POST_P, gs ? gs_sweep_bytes(L, NC) : cheb ? deg * (bA0 + 5 * vec) : bA0 + 4 * vec);
     c.launches += 4;
 }
 

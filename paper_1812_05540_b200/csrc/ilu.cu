@@ -206,6 +206,13 @@ __device__ __forceinline__ void pf_load_dir(const double *__restrict__ ival, con
 //  load overlaps the scan and the barrier.  3 CTAs per SM (the shared-memory limit) matter more than
 //  a deeper prefetch: at 2 CTAs per SM the kernel is 1.5x slower (measured on C5).
 // One line per W-lane segment; requires (lines per level) <= segments per CTA.
+#ifdef TSP_ILU_TIMING
+__device__ unsigned long long g_ilu_t[8192][4];
+__device__ __forceinline__ unsigned long long gtimer() { unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; }
+#define ILU_T(k) do { if (threadIdx.x == 0 && blockIdx.x < 8192) g_ilu_t[blockIdx.x][k] = gtimer(); } while (0)
+#else
+#define ILU_T(k) do { } while (0)
+#endif
 template <bool BGS>
 __global__ void __launch_bounds__(256, 3) k_ilu_apply2(TileGeo g, const int32_t *__restrict__ lines, const int32_t *__restrict__ lvlptr,
                                                     const double *__restrict__ ival, const double *__restrict__ dinv,
@@ -221,6 +228,7 @@ __global__ void __launch_bounds__(256, 3) k_ilu_apply2(TileGeo g, const int32_t 
     const int slot0 = (threadIdx.x >> 5) * (32 / W) + lane / W, nslots = (blockDim.x >> 5) * (32 / W);
     const int li = lseg, gi = TI * g.tx + li;
     const bool xin = li < g.tx && gi < g.nx;
+    ILU_T(0);
     // ---------------- phase 0: w = y - S^FS z (step 6)
     for (int line = slot0; line < g.ty * g.tz; line += nslots) {
         const int lj = line % g.ty, lk = line / g.ty;
@@ -243,6 +251,7 @@ __global__ void __launch_bounds__(256, 3) k_ilu_apply2(TileGeo g, const int32_t 
         pf_load_dir(ival, dinv, g, t, lk, lj, li, lv && xin && TJ * g.ty + lj < g.ny && TK * g.tz + lk < g.nz, true, P);
     }
     __syncthreads();
+    ILU_T(1);
     for (int l = 0; l < g.nlev; ++l) {
         int lj, lk;
         const bool lv = line_at(g, l, slot0, lj, lk);
@@ -287,6 +296,7 @@ __global__ void __launch_bounds__(256, 3) k_ilu_apply2(TileGeo g, const int32_t 
         }
         __syncthreads();
     }
+    ILU_T(2);
     // ---------------- backward (ILU only)
     if constexpr (!BGS)
     for (int l = g.nlev - 1; l >= 0; --l) {
@@ -333,7 +343,14 @@ __global__ void __launch_bounds__(256, 3) k_ilu_apply2(TileGeo g, const int32_t 
         }
         __syncthreads();
     }
+    ILU_T(3);
 }
+#ifdef TSP_ILU_TIMING
+extern "C" int tsp_dev_ilu_timers(unsigned long long *out, int n)
+{
+    return (int)cudaMemcpyFromSymbol(out, g_ilu_t, sizeof(unsigned long long) * 4 * (size_t)n);
+}
+#endif
 
 static TileGeo geo(const Ctx &c)
 {

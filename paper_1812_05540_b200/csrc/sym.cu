@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(256) k_op_node_sym(SymGeo g, const double *__r
 template <int ASYM, int MODE, bool D>
 __global__ void __launch_bounds__(256) k_vc_sym(SymGeo g, const double *__restrict__ vs, const double *__restrict__ vf,
                                                 const double *__restrict__ gl, GV dinv, GV b, GV xin, double *__restrict__ out1,
-                                                double *__restrict__ out2)
+                                                double *__restrict__ out2, ChebArgs ca)
 {
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= g.Nn) return;
@@ -207,7 +207,8 @@ __global__ void __launch_bounds__(256) k_vc_sym(SymGeo g, const double *__restri
         const int j = sym_xidx(g, n2);
 #pragma unroll
         for (int cc = 0; cc < 3; ++cc) {
-            const double xv = MODE == 1 ? gvld<D>(b, j, cc, 3) * gvld<D>(dinv, j, cc, 3) : gvld<D>(xin, j, cc, 3);
+            const double xv = MODE == 1 ? gvld<D>(b, j, cc, 3) * gvld<D>(dinv, j, cc, 3)
+                            : MODE == 4 ? ca.sc * (gvld<D>(dinv, j, cc, 3) * gvld<D>(b, j, cc, 3)) : gvld<D>(xin, j, cc, 3);
             acc[cc] = fma(B[cc], xv, acc[cc]);
         }
     }
@@ -220,6 +221,8 @@ __global__ void __launch_bounds__(256) k_vc_sym(SymGeo g, const double *__restri
             out2[t] = bi - acc[cc];
         } else if (MODE == 3) {
             out1[t] = b.own[t] - acc[cc];
+        } else if (MODE == 4 || MODE == 5) {
+            cheb_epi<MODE == 4>(t, acc[cc], b.own[t], dinv.own[t], MODE == 5 ? xin.own[t] : 0.0, ca, out1);
         } else {
             out1[t] = xin.own[t] + dinv.own[t] * (b.own[t] - acc[cc]);
         }
@@ -376,7 +379,7 @@ bool sym_vcycle_pre(Ctx &c, int n, const GV &dinv, const GV &b, double *x, doubl
     const Sym27 &S = c.sym_sdc;
 #define VCS(A)                                                                                                    \
     (c.comm ? k_vc_sym<A, 1, true> : k_vc_sym<A, 1, false>)<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(                        \
-        g, S.val_s, S.val_f, S.gl, dinv, b, gv(nullptr, 0), x, r)
+        g, S.val_s, S.val_f, S.gl, dinv, b, gv(nullptr, 0), x, r, ChebArgs{})
     if (n) {
         if (c.sym_asym == 0) VCS(0u);
         else VCS(kAsymZ);
@@ -391,10 +394,25 @@ bool sym_vcycle_post(Ctx &c, int n, const double *dinv, const double *b, const G
     const Sym27 &S = c.sym_sdc;
 #define VCS(A)                                                                                                    \
     (c.comm ? k_vc_sym<A, 2, true> : k_vc_sym<A, 2, false>)<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(                        \
-        g, S.val_s, S.val_f, S.gl, gv(dinv, n), gv(b, n), x, xo, nullptr)
+        g, S.val_s, S.val_f, S.gl, gv(dinv, n), gv(b, n), x, xo, nullptr, ChebArgs{})
     if (n) {
         if (c.sym_asym == 0) VCS(0u);
         else VCS(kAsymZ);
+    }
+#undef VCS
+    return true;
+}
+bool sym_vcycle_cheb(Ctx &c, int n, bool pre, const GV &dinv, const GV &b, const GV &x, const ChebArgs &a, double *xo)
+{
+    if (!c.sym_sdc.ok || n != c.Nn) return false;
+    const SymGeo g = sym_geo(c);
+    const Sym27 &S = c.sym_sdc;
+#define VCS(A, M)                                                                                                 \
+    (c.comm ? k_vc_sym<A, M, true> : k_vc_sym<A, M, false>)<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(                        \
+        g, S.val_s, S.val_f, S.gl, dinv, b, x, xo, nullptr, a)
+    if (n) {
+        if (c.sym_asym == 0) { if (pre) VCS(0u, 4); else VCS(0u, 5); }
+        else { if (pre) VCS(kAsymZ, 4); else VCS(kAsymZ, 5); }
     }
 #undef VCS
     return true;
@@ -406,7 +424,7 @@ bool sym_vcycle_resid(Ctx &c, int n, const double *b, const GV &x, double *r)
     const Sym27 &S = c.sym_sdc;
 #define VCS(A)                                                                                                    \
     (c.comm ? k_vc_sym<A, 3, true> : k_vc_sym<A, 3, false>)<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(                        \
-        g, S.val_s, S.val_f, S.gl, gv(nullptr, 0), gv(b, n), x, r, nullptr)
+        g, S.val_s, S.val_f, S.gl, gv(nullptr, 0), gv(b, n), x, r, nullptr, ChebArgs{})
     if (n) {
         if (c.sym_asym == 0) VCS(0u);
         else VCS(kAsymZ);

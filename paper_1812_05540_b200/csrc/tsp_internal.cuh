@@ -158,6 +158,31 @@ __device__ __forceinline__ double gvld(const GV &g, int64_t j, int c, int nc)
     return __ldg(g.own + j * nc + c);
 }
 
+// Fused Chebyshev smoothing step (R-cheb; amg.cu cheb_run): the row epilogue shared by the SELL, vector-CSR and
+// structured kernels.  PRE = the first two steps from zero in one product (the kernel gathers sc dinv_j b_j,
+// i.e. A x_1 with x_1 = D^-1 b / theta):  x_1 = sc dinv_i b_i, d_1 = alpha x_1 + beta dinv_i (b_i - acc),
+// xo = x_1 + d_1.  STEP = one step from x (the kernel gathers x_j): d = alpha dprev_i + beta dinv_i (b_i - acc)
+// (dprev == nullptr: first step, d = beta dinv_i (b_i - acc)), xo = x_i + d.  dout (may be nullptr) keeps d.
+struct ChebArgs {
+    const double *dprev;
+    double *dout;
+    double alpha, beta, sc;
+};
+template <bool PRE>
+__device__ __forceinline__ void cheb_epi(int64_t t, double acc, double bi, double di, double xi, const ChebArgs &a, double *xo)
+{
+    if (PRE) {
+        const double x1 = a.sc * (di * bi);
+        const double d = a.alpha * x1 + a.beta * (di * (bi - acc));
+        if (a.dout) a.dout[t] = d;
+        xo[t] = x1 + d;
+    } else {
+        const double d = (a.dprev ? a.alpha * a.dprev[t] : 0.0) + a.beta * (di * (bi - acc));
+        if (a.dout) a.dout[t] = d;
+        xo[t] = xi + d;
+    }
+}
+
 // builds the plan from the GLOBAL column ids of a row-distributed CSR (own rows =
 // global [own_off, own_off + nown)) and rewrites `lcols` with local ids
 void halo_build(Ctx &c, Halo &H, int nown, int64_t own_off, const int32_t *gcols, int64_t nnz, int32_t *lcols);
@@ -206,7 +231,7 @@ struct Level {
     DBuf<double> cinv;            // coarsest: dense inverse [nc][n][n]
     // apply work vectors [n][nc]
     DBuf<double> b, x, x2, r;
-    DBuf<double> dcheb;           // Chebyshev smoother direction (amg_smoother = 2)
+    DBuf<double> dcheb, xc;       // Chebyshev smoother (amg_smoother = 2): direction, ping-pong iterate
 };
 
 struct Hier {
@@ -339,6 +364,8 @@ template <int NC> void gs_sweep(Ctx &c, Level &L, bool backward, const double *b
 double gs_sweep_bytes(const Level &L, int nc);
 void gs_export_colour(Ctx &c, const Level &L, int32_t *host_out);
 bool sym_vcycle_resid(Ctx &c, int n, const double *b, const GV &x, double *r);   // level-0 SDC r = b - A x, if sym_sdc.ok
+// level-0 SDC fused Chebyshev step (cheb_epi), if sym_sdc.ok
+bool sym_vcycle_cheb(Ctx &c, int n, bool pre, const GV &dinv, const GV &b, const GV &x, const ChebArgs &a, double *xo);
 void ilu_setup(Ctx &c, const double *sff_vals);
 void ilu_apply_fused(Ctx &c, const double *yf, const double *zs, const double *zp, double *zf_out);
 
