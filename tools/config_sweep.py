@@ -1,0 +1,67 @@
+"""Per-config records: for each BASELINE.json config that the oracle can run in full on the host
+(C1-C4), one JSON line with the GPU path (setup + FGMRES(64) to 1e-8, device-timed, the bench's step) next to the
+oracle's FULL run of the same step on the same input (its own setup and its own FGMRES to 1e-8 on one host core;
+no extrapolation).  Also the preconditioner apply alone, GDoF/s, and the iteration counts of both sides.
+  python tools/config_sweep.py [C1 C2 C3 C4]   > profiles/r02_configs.jsonl"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+from paper_1812_05540_b200 import Tsp  # noqa: E402
+
+cfgs = sys.argv[1:] or ["C1", "C2", "C3", "C4"]
+dev = torch.device("cuda", 0)
+for cfg in cfgs:
+    pb = synth.generate(cfg)
+    g = Tsp(pb)
+    b = torch.from_numpy(pb.b).to(dev)
+    x = torch.zeros(pb.n, dtype=torch.float64, device=dev)
+    steps = []
+    for rep in range(4):                      # 2 warm-up steps, 2 timed
+        x.zero_()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        g.setup()
+        e1.record()
+        info = g.solve(b, x, rtol=1e-8, restart=64, max_iters=1000)
+        e2.record()
+        torch.cuda.synchronize()
+        steps.append((e0.elapsed_time(e1), e1.elapsed_time(e2), info))
+    su = float(np.mean([s[0] for s in steps[2:]]))
+    so = float(np.mean([s[1] for s in steps[2:]]))
+    it = steps[-1][2]["iterations"]
+    z = torch.empty_like(b)
+    for _ in range(3):
+        g.apply_preconditioner(b, z)
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for _ in range(20):
+        g.apply_preconditioner(b, z)
+    a1.record()
+    torch.cuda.synchronize()
+    apply_ms = a0.elapsed_time(a1) / 20
+    g.close()
+    # the oracle, full step on the same input
+    t0 = time.perf_counter()
+    o = oracle.Oracle(pb).setup()
+    t1 = time.perf_counter()
+    _, io = o.solve(pb.b, rtol=1e-8, m=64)
+    t2 = time.perf_counter()
+    rec = {"config": cfg, "grid": [pb.nx, pb.ny, pb.nz], "dof": pb.n,
+           "gpu": {"iterations": it, "setup_ms": su, "solve_ms": so, "step_ms": su + so,
+                   "iters_per_s": it / ((su + so) * 1e-3), "ms_per_iter": so / max(it, 1),
+                   "apply_ms": apply_ms, "apply_gdof_per_s": pb.n / (apply_ms * 1e-3) / 1e9,
+                   "true_relres": steps[-1][2]["true_relres"]},
+           "oracle": {"iterations": io["iterations"], "status": io["status"], "setup_s": t1 - t0, "solve_s": t2 - t1,
+                      "step_s": t2 - t0, "iters_per_s": io["iterations"] / (t2 - t0), "cores": 1,
+                      "kind": "oracle (plain C, full run, no extrapolation)"},
+           "iterations_match_pm1": abs(io["iterations"] - it) <= 1,
+           "speedup_step": (t2 - t0) / ((su + so) * 1e-3)}
+    print(json.dumps(rec), flush=True)
