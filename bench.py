@@ -43,7 +43,7 @@ def ncu_traffic(kernel_class):
     """(DRAM bytes per launch, ncu DRAM % of peak) of a kernel class from the committed ncu --set full
     capture, or (None, None)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
             k = json.load(f)["kernels"][kernel_class]
         return float(k["dram_bytes_per_launch"]), k.get("ncu_dram_pct_of_peak")
     except Exception:
@@ -236,25 +236,28 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     if ws > 1:
-        # z-slab decomposition (row e): this rank's owned block rows, NCCL over NVLink for halos/reductions.
-        # The generator builds the global Jacobian (~26 GB of host memory at C5); ranks take turns so that only
-        # one global copy exists at a time, and each keeps its slab only.
-        import gc
-        from paper_1812_05540_b200 import TSP_COMM_NCCL, nccl_unique_id
-        for turn in range(ws):
-            if turn == rank:
-                pb = synth.generate(args.config)
-                lp = synth.local_problem(pb, rank, ws)
-                b_host = np.ascontiguousarray(lp.local(pb.b, pb.Nn))
-                shape = synth.Problem(nx=pb.nx, ny=pb.ny, nz=pb.nz, params={}, **{k: None for k in (
-                    "uu_rowptr", "uu_col", "uu_val", "uf_rowptr", "uf_col", "uf_val", "fu_rowptr", "fu_col", "fu_val",
-                    "ff_rowptr", "ff_col", "ff_val", "fs", "x_rand", "b")})
-                n_glob = pb.n
-                del pb
-                gc.collect()
-                pb = shape
-            dist.barrier()
-        src = lp
+        # z-slab decomposition (row e): every rank draws the per-cell fields of the global grid (0.4 GB at C5; no
+        # Jacobian on the host) and assembles ITS slab's rows on its own GPU (tsp_assemble, NEXT-f1); the row
+        # scaling takes the maxima over the ranks.  NCCL over NVLink for halos and reductions.
+        from paper_1812_05540_b200 import TSP_COMM_NCCL, assemble, nccl_unique_id
+        fl = synth.fields(args.config)
+
+        def gmax(m):
+            t = torch.tensor(m, dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return t.tolist()
+
+        src = assemble(fl["params"], fl, rank=rank, nranks=ws, global_max=gmax)
+        prm = fl["params"]
+        _, _, n0, nn, c0, ncl = synth.slab_partition(prm["nx"], prm["ny"], prm["nz"], 16, rank, ws)
+        sz_g = synth.sizes(prm["nx"], prm["ny"], prm["nz"])
+        xr = fl["x_rand"]
+        x_loc = np.concatenate([xr[3 * n0:3 * (n0 + nn)], xr[3 * sz_g["Nn"] + 2 * c0:3 * sz_g["Nn"] + 2 * (c0 + ncl)]])
+        n_glob = sz_g["n"]
+        pb = synth.Problem(nx=prm["nx"], ny=prm["ny"], nz=prm["nz"], params=prm, **{k: None for k in (
+            "uu_rowptr", "uu_col", "uu_val", "uf_rowptr", "uf_col", "uf_val", "fu_rowptr", "fu_col", "fu_val",
+            "ff_rowptr", "ff_col", "ff_val", "fs", "x_rand", "b")})
+        del fl
 
         def new_topo():
             # collective: a fresh NCCL unique id per communicator (an id's bootstrap root serves one
@@ -271,7 +274,13 @@ def main():
             return {}
     n = src.n
     g = Tsp(src, **new_topo(), **lib_opts)
-    b = torch.from_numpy(np.ascontiguousarray(b_host)).to(dev)
+    if ws > 1:                                     # b = A x_rand on the device (the generator's right-hand side)
+        b = torch.empty(n, dtype=torch.float64, device=dev)
+        g.apply_operator(torch.from_numpy(x_loc).to(dev), b)
+        torch.cuda.synchronize()
+        b_host = b.cpu().numpy()
+    else:
+        b = torch.from_numpy(np.ascontiguousarray(b_host)).to(dev)
     x = torch.zeros(n, dtype=torch.float64, device=dev)
 
     setup_s = []
@@ -441,11 +450,15 @@ def main():
         torch.cuda.empty_cache()
     del b, x
     if not args.no_e2e:
+        def host_pinned(v):
+            t = v.cpu() if torch.is_tensor(v) else torch.from_numpy(np.ascontiguousarray(v))
+            return t.contiguous().pin_memory()
+
         pin = {}
         for k in ("uu", "uf", "fu", "ff"):
-            for s in ("_rowptr", "_col", "_val"):
-                pin[k + s] = torch.from_numpy(np.ascontiguousarray(getattr(src, k + s))).pin_memory()
-        pin["fs"] = torch.from_numpy(np.ascontiguousarray(src.fs)).pin_memory()
+            for s_ in ("_rowptr", "_col", "_val"):
+                pin[k + s_] = host_pinned(getattr(src, k + s_))
+        pin["fs"] = host_pinned(src.fs)
 
         class Pinned:
             pass
@@ -491,6 +504,51 @@ def main():
         e2e = {"value": float(eit.item()) / (float(ems.item()) * 1e-3), "unit": "iter/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "what": "tsp_create from pinned host blocks + tsp_setup(MECH|FLOW) + tsp_solve(host b -> host x) + tsp_destroy"}
+        del pin, pp
+
+    # ---- end to end from the per-cell FIELDS (the GPU-resident pipeline, NEXT-f1): pinned host fields and x_rand
+    # -> device, tsp_assemble on the GPU, tsp_create from device blocks, b = A x_rand, setup, solve, x -> host
+    e2e_asm = None
+    if not args.no_e2e and ws == 1 and not lib_opts:
+        try:
+            from paper_1812_05540_b200 import assemble
+            fl = synth.fields(args.config)
+            hf = {k: torch.from_numpy(np.ascontiguousarray(fl[k])).pin_memory() for k in ("E", "perm", "phi", "sat", "pres", "well", "x_rand")}
+            xh2 = torch.zeros(n, dtype=torch.float64).pin_memory()
+            h2d_a = sum(v.numel() * v.element_size() for v in hf.values())
+
+            def asm_step():
+                d = {k: v.to(dev, non_blocking=True) for k, v in hf.items()}
+                ap = assemble(fl["params"], d)
+                h = Tsp(ap)
+                del ap
+                bb = torch.empty(n, dtype=torch.float64, device=dev)
+                h.apply_operator(d["x_rand"], bb)
+                h.setup()
+                xx = torch.zeros(n, dtype=torch.float64, device=dev)
+                inf = h.solve(bb, xx)
+                xh2.copy_(xx, non_blocking=True)
+                torch.cuda.synchronize()
+                h.close()
+                return inf
+
+            asm_step()
+            torch.cuda.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            a_iters = 0
+            for _ in range(args.steps):
+                a_iters += asm_step()["iterations"]
+            g1.record(stream)
+            torch.cuda.synchronize()
+            e2e_asm = {"value": a_iters / (g0.elapsed_time(g1) * 1e-3), "unit": "iter/s", "h2d_bytes_per_step": int(h2d_a),
+                       "d2h_bytes_per_step": int(xh2.numel() * 8),
+                       "what": "pinned host fields + x_rand -> device, tsp_assemble + tsp_assemble_scale, tsp_create from "
+                               "device blocks, b = A x_rand, tsp_setup(MECH|FLOW), tsp_solve, x -> host, tsp_destroy"}
+            del hf
+        except Exception as e:   # reported, never fatal for the headline
+            e2e_asm = {"error": str(e)}
+        torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -531,6 +589,7 @@ def main():
             "gpu_launches": int(launches_timed),
             "clocks": clk,
             "e2e": e2e,
+            "e2e_gpu_assembly": e2e_asm,
             "cpu_baseline": cpu,
             "true_relres": infos[-1]["true_relres"],
             "hierarchy_rows": st["rows"],

@@ -1024,7 +1024,10 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
     // apply-side layouts and work vectors
     for (size_t l = 0; l < H.L.size(); ++l) {
         Level &L = H.L[l];
-        if (!(l == 0 && nc == 3 && c.sym_sdc.ok && !L.coarsest)) sell_from_csr(c, L.A, L.sA, nc);   // sym.cu covers it
+        if (l == 0 && nc == 1 && !L.coarsest) p7_build(c, L.A);            // pressure level 0: p7.cu when 7-point
+        const bool structured = l == 0 && !L.coarsest && ((nc == 3 && c.sym_sdc.ok) || (nc == 1 && c.p7_ok));
+        if (!structured) sell_from_csr(c, L.A, L.sA, nc);                  // sym.cu / p7.cu cover level 0
+        else L.sA = Sell{};
         if (!L.coarsest) {
             sell_from_csr(c, L.P, L.sP, nc);
             sell_from_csr(c, L.R, L.sR, nc);
@@ -1299,7 +1302,8 @@ static void level_resid(Ctx &c, Level &L, bool sym0, const double *b, const doub
     const int n = L.n;
     if (L.dist) halo_exchange(c, *L.hp, NC, x, L.gh_x);
     const GV gx = gv(x, n, L.dist ? L.gh_x.p : nullptr);
-    if (sym0) sym_vcycle_resid(c, n, b, gx, r);
+    if (NC == 1 && &L == &c.pres.L[0] && c.p7_ok) p7_launch(c, 3, gv(nullptr, 0), gv(b, n), gx, r, nullptr, ChebArgs{});
+    else if (sym0) sym_vcycle_resid(c, n, b, gx, r);
     else if (L.warpA) (L.dist ? csr_vec<NC, 3, true> : csr_vec<NC, 3, false>)(L.warpA, c.s, n, L.A, gv(nullptr, 0), gv(b, n), gx, r, nullptr, ChebArgs{});
     else if (n) (L.dist ? k_sell_resid<NC, true> : k_sell_resid<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
         n, L.sA.off, L.sA.col, L.sA.val, b, gx, r);
@@ -1323,7 +1327,8 @@ static void cheb_step(Ctx &c, Level &L, bool sym0, bool pre, const double *b, co
         if (L.dist) halo_exchange(c, *L.hp, NC, xk, L.gh_x);
         gx = gv(xk, n, L.dist ? L.gh_x.p : nullptr);
     }
-    if (sym0) sym_vcycle_cheb(c, n, pre, gd, gb, gx, a, xo);
+    if (NC == 1 && &L == &c.pres.L[0] && c.p7_ok) p7_launch(c, pre ? 4 : 5, gd, gb, gx, xo, nullptr, a);
+    else if (sym0) sym_vcycle_cheb(c, n, pre, gd, gb, gx, a, xo);
     else if (L.warpA) {
         if (pre) (L.dist ? csr_vec<NC, 4, true> : csr_vec<NC, 4, false>)(L.warpA, c.s, n, L.A, gd, gb, gx, xo, nullptr, a);
         else (L.dist ? csr_vec<NC, 5, true> : csr_vec<NC, 5, false>)(L.warpA, c.s, n, L.A, gd, gb, gx, xo, nullptr, a);
@@ -1394,7 +1399,8 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     if (L.dist) halo_exchange(c, *L.hp, NC, b, L.gh_b);
     const GV gb = gv(b, n, L.dist ? L.gh_b.p : nullptr), gd = gv(L.dinv, n, ghd);
     const bool sym0 = mech && l == 0 && c.sym_sdc.ok;     // structured symmetric level 0 (sym.cu)
-    const double bA0 = sym0 ? sym_bytes(c, 3) : bA;
+    const bool p70 = !mech && l == 0 && c.p7_ok;          // structured 7-point pressure level 0 (p7.cu)
+    const double bA0 = sym0 ? sym_bytes(c, 3) : p70 ? p7_bytes(c) : bA;
     const bool gs = c.o.amg_smoother == 1;   // Gauss-Seidel (gs.cu, R-gs): single GPU, never distributed
     const bool cheb = c.o.amg_smoother == 2; // Chebyshev (R-cheb)
     const int deg = c.o.amg_cheb_degree;
@@ -1406,6 +1412,7 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
         cheb_run<NC>(c, L, sym0, b, nullptr, L.x2, L.xc, true);
         level_resid<NC>(c, L, sym0, b, L.x2, L.r);
     }
+    else if (p70) p7_launch(c, 1, gd, gb, gv(nullptr, 0), L.x2, L.r, ChebArgs{});
     else if (sym0) sym_vcycle_pre(c, n, gd, gb, L.x2, L.r);
     else if (wA) (L.dist ? csr_vec<NC, 1, true> : csr_vec<NC, 1, false>)(wA, c.s, n, L.A, gd, gb, gv(nullptr, 0), L.x2, L.r, ChebArgs{});
     else if (n) (L.dist ? k_vc_pre<NC, true> : k_vc_pre<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
@@ -1439,6 +1446,7 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     prof_begin(c, mech ? PK_VC_POST_U : PK_VC_POST_P);
     if (gs) gs_sweep<NC>(c, L, true, b, L.x2, xout);                      // backward sweep
     else if (cheb) cheb_run<NC>(c, L, sym0, b, L.x2, xout, L.xc, false);
+    else if (p70) p7_launch(c, 2, gv(L.dinv, n), gv(b, n), gx, xout, nullptr, ChebArgs{});
     else if (sym0) sym_vcycle_post(c, n, L.dinv, b, gx, xout);
     else if (wA) (L.dist ? csr_vec<NC, 2, true> : csr_vec<NC, 2, false>)(wA, c.s, n, L.A, gv(L.dinv, n), gv(b, n), gx, xout, nullptr, ChebArgs{});
     else if (n) (L.dist ? k_vc_post<NC, true> : k_vc_post<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(

@@ -458,6 +458,58 @@ tsp_status tsp_solve(tsp_handle h, const double *b, double *x, const tsp_solve_o
     }
 }
 
+static tsp_status check_asm(const tsp_asm_params *p, int rank, int nranks, int zblock)
+{
+    if (!p) { set_error("null params"); return TSP_ERR_INVALID_ARG; }
+    if (p->nx <= 0 || p->ny <= 0 || p->nz <= 0 || nranks < 1 || rank < 0 || rank >= nranks) {
+        set_error("assembly: bad grid or rank");
+        return TSP_ERR_INVALID_ARG;
+    }
+    const int zb = zblock > 0 ? zblock : 16;
+    if (nranks > (p->nz + zb - 1) / zb) { set_error("more ranks than z-blocks"); return TSP_ERR_INVALID_ARG; }
+    return TSP_OK;
+}
+
+tsp_status tsp_assembly_sizes(const tsp_asm_params *p, int rank, int nranks, int zblock, int64_t out6[6])
+{
+    if (tsp_status st = check_asm(p, rank, nranks, zblock)) return st;
+    if (!out6) { set_error("null argument"); return TSP_ERR_INVALID_ARG; }
+    try {
+        assembly_sizes(*p, rank, nranks, zblock, out6);
+        return TSP_OK;
+    } catch (...) {
+        return status_of_current_exception();
+    }
+}
+
+tsp_status tsp_assemble(const tsp_asm_params *p, int rank, int nranks, int zblock, const tsp_cell_fields *f,
+                        tsp_bsr_out blocks[4], double *fs, double row_max[3], void *stream)
+{
+    if (tsp_status st = check_asm(p, rank, nranks, zblock)) return st;
+    if (!f || !blocks || !row_max) { set_error("null argument"); return TSP_ERR_INVALID_ARG; }
+    try {
+        StreamScope ss_((cudaStream_t)stream, nullptr);
+        assemble((cudaStream_t)stream, *p, rank, nranks, zblock, *f, blocks, fs, row_max);
+        return TSP_OK;
+    } catch (...) {
+        return status_of_current_exception();
+    }
+}
+
+tsp_status tsp_assemble_scale(const tsp_asm_params *p, int rank, int nranks, int zblock, const double row_max[3],
+                              tsp_bsr_out blocks[4], double *fs, double scales[3], void *stream)
+{
+    if (tsp_status st = check_asm(p, rank, nranks, zblock)) return st;
+    if (!blocks || !row_max || !fs) { set_error("null argument"); return TSP_ERR_INVALID_ARG; }
+    try {
+        StreamScope ss_((cudaStream_t)stream, nullptr);
+        assemble_scale((cudaStream_t)stream, *p, rank, nranks, zblock, row_max, blocks, fs, scales);
+        return TSP_OK;
+    } catch (...) {
+        return status_of_current_exception();
+    }
+}
+
 tsp_status tsp_export_colour(tsp_handle h, int which, int lvl, int32_t *colour, int *block, int *ncolour)
 {
     if (!h) { set_error("null handle"); return TSP_ERR_INVALID_ARG; }
@@ -493,7 +545,8 @@ tsp_status tsp_get_stats(tsp_handle h, tsp_stats *s)
             const double nc = L.nc, vec = 8.0 * nc * L.n;
             if (L.coarsest) { apply_bytes += 8.0 * L.n * L.n * nc + 2 * vec; continue; }
             auto sb = [](const Sell &S) { return (double)S.slots * 32 * (4.0 + 8.0 * S.bs); };
-            const double bA = (w == 0 && l == 0 && h->sym_sdc.ok) ? sym_bytes(*h, 3) : sb(L.sA);
+            const double bA = (w == 0 && l == 0 && h->sym_sdc.ok) ? sym_bytes(*h, 3)
+                            : (w == 1 && l == 0 && h->p7_ok) ? p7_bytes(*h) : sb(L.sA);
             apply_bytes += 2 * bA + sb(L.sR) + sb(L.sP) + 11 * vec;
         }
         s->skipped_dss = h->skipped_dss;

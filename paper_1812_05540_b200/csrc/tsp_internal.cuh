@@ -290,6 +290,8 @@ struct Ctx {
     DBuf<double> uu_sdc;          // a2: SDC values of A_uu (3 per block), extracted at create
     Sell s_uu, s_uf, s_fu, s_ff;  // SELL copies (operator rows)
     Sym27 sym_uu, sym_sdc;        // structured symmetric A_uu (operator) and A_uu^SDC (level-0 smoother)
+    bool p7_ok = false;           // structured 7-point pressure level 0 (p7.cu) in use
+    DBuf<double> p7_val;          // its values [slice][7][32]
     unsigned sym_asym = 0;        // their mask of non-symmetric block entries
     DBuf<double> fs;              // 2 per cell, as given (tsp_desc.fs_diag)
     DBuf<double> fs_eff;          // 2 per cell: the D_fs a1 uses (given / fs_modulus_scale, or RSL)
@@ -351,6 +353,11 @@ bool sym_vcycle_post(Ctx &c, int n, const double *dinv, const double *b, const G
 double sym_bytes(const Ctx &c, int bs);   // bytes of one stream over a Sym27 with bs values per block
 void prec_apply(Ctx &c, const double *v, double *z);
 
+// p7.cu: structured 7-point pressure level 0 (mode 1 pre, 2 post, 3 residual, 4 / 5 Chebyshev PRE / STEP)
+void p7_build(Ctx &c, const Csr &A);
+double p7_bytes(const Ctx &c);
+void p7_launch(Ctx &c, int mode, const GV &dinv, const GV &b, const GV &x, double *o1, double *o2, const ChebArgs &ca);
+
 // setup (setup_flow.cu, amg_setup.cu, ilu.cu)
 void extract_sdc(Ctx &c);
 void setup_mech(Ctx &c);
@@ -368,6 +375,13 @@ bool sym_vcycle_resid(Ctx &c, int n, const double *b, const GV &x, double *r);  
 bool sym_vcycle_cheb(Ctx &c, int n, bool pre, const GV &dinv, const GV &b, const GV &x, const ChebArgs &a, double *xo);
 void ilu_setup(Ctx &c, const double *sff_vals);
 void ilu_apply_fused(Ctx &c, const double *yf, const double *zs, const double *zp, double *zf_out);
+
+// assemble.cu: GPU assembly of the linearised Jacobian (NEXT-f1)
+void assembly_sizes(const tsp_asm_params &P, int rank, int nranks, int zblock, int64_t out[6]);
+void assemble(cudaStream_t s, const tsp_asm_params &P, int rank, int nranks, int zblock, const tsp_cell_fields &f,
+              tsp_bsr_out blk[4], double *fs, double row_max[3]);
+void assemble_scale(cudaStream_t s, const tsp_asm_params &P, int rank, int nranks, int zblock, const double row_max[3],
+                    tsp_bsr_out blk[4], double *fs, double scales[3]);
 
 // partition of the z-slab decomposition (include/tsp.h)
 void partition(int nx, int ny, int nz, int zblock, int rank, int nranks, int64_t out6[6]);

@@ -263,6 +263,35 @@ def test_structured_symmetric_path_equals_the_generic_one(dev, name):
     assert b1 < 0.9 * b2          # the structured path streams fewer operator bytes (no indices, mirrored entries)
 
 
+@pytest.mark.parametrize("name", ["C2", "R1", "DEG"])
+@pytest.mark.parametrize("smoother", [0, 1, 2])
+def test_structured_7point_pressure_level_equals_the_generic_one(dev, name, smoother):
+    """p7.cu (index-free 7-point pressure level 0) sums the same entries in the same (ascending-column) order as
+    the sliced-ELL kernels: one Algorithm 1 application BITWISE equal with and without it (TSP_NO_P7 forces the
+    generic path), for the l1-Jacobi, Gauss-Seidel (its residual) and Chebyshev smoothers; degenerate grids
+    (a single x-column, DEG) resolve the coinciding stencil offsets geometrically."""
+    import os
+    from paper_1812_05540_b200 import Tsp
+    pb = synth.generate(nx=1, ny=3, nz=48, recipe=2) if name == "DEG" else _problem(name)
+    v = _cuda(np.random.default_rng(32).uniform(-1, 1, pb.n))
+    out = []
+    for nop7 in (False, True):
+        if nop7:
+            os.environ["TSP_NO_P7"] = "1"
+        try:
+            g = Tsp(pb, amg_smoother=smoother).setup()
+        finally:
+            os.environ.pop("TSP_NO_P7", None)
+        z = torch.empty(pb.n, dtype=torch.float64, device=dev)
+        g.apply_preconditioner(v, z)
+        torch.cuda.synchronize()
+        out.append((z.cpu().numpy(), g.stats()["bytes_apply"]))
+        g.close()
+    (z1, b1), (z2, b2) = out
+    assert np.array_equal(z1, z2)
+    assert b1 < b2                # fewer algorithmic bytes without the column indices
+
+
 def test_cuda_graph_iterations_are_bitwise_the_eager_ones(dev):
     """krylov.cu replays the FGMRES iteration body from per-index CUDA graphs (captured on a second use); two
     solves with graphs and one without (TSP_NO_GRAPH) give the same solution bit for bit."""
