@@ -248,6 +248,53 @@ void tsp_default_solve_opts(tsp_solve_opts *o);
 
 tsp_status tsp_get_stats(tsp_handle h, tsp_stats *s);
 
+/* ---- GPU assembly of the linearised Jacobian (Appendix B) --------------------------
+ * The four blocks of eq:jac_system and the fixed-stress diagonals (eq:FS_Dps_Dpp) of the
+ * synthetic poromechanics problem, assembled on the device from per-cell fields at a linearisation state, in the
+ * layout and units tsp_create consumes (pressure unit p_unit on the p columns, R-punit; block rows scaled by
+ * 1 / max row l1 norm, R-scale; bottom nodes Dirichlet identity rows / zero columns, R-dirichlet).
+ * Physics: Q1 elasticity with 2x2x2 Gauss and the gravity term, Biot coupling, two-phase TPFA with single-point
+ * upwinding and phase-averaged densities, Peaceman wells, Corey n = 2. */
+typedef struct {
+    int nx, ny, nz;              /* GLOBAL grid (cells); cubic cells of side h = length / nx (R-geom) */
+    double length;
+    double nu, biot, gravity, dt;
+    double rho_w0, rho_nw0, c_w, c_nw, mu_w, mu_nw, rho_s, p0;   /* fluids, solid density, reference pressure (Pa) */
+    double swr, snwr;            /* residual saturations of the Corey curves */
+    double well_dbhp, rw_over_h; /* BHP offset of injectors (+) and producers (-) from hydrostatic; r_w / h (R-wells) */
+    double p_unit;               /* Pa per unit of the pressure unknown (R-punit) */
+    int burden;                  /* seal layers at top and bottom: perforations stop above them (R-s10) */
+    int dirichlet_bottom, row_scale;
+} tsp_asm_params;
+
+/* per-cell fields of the GLOBAL grid (device pointers, N_c entries each, cell (i,j,k) = i + nx (j + ny k)):
+ * Young's modulus (Pa), permeability (m^2), porosity, water saturation, pressure (Pa) at the linearisation state,
+ * and the well perforation of the cell (0 none, 1 water injector, 2 producer; NULL = no wells) */
+typedef struct {
+    const double *E, *perm, *phi, *sat, *pres;
+    const int8_t *well;
+} tsp_cell_fields;
+
+/* a device BSR block the assembly writes (rowptr: rows + 1, col / val: sizes from tsp_assembly_sizes) */
+typedef struct {
+    int32_t *rowptr, *col;
+    double *val;
+} tsp_bsr_out;
+
+/* this rank's rows (the z-slab of include/tsp.h with opts.zblock = `zblock`) and block counts:
+ * out6 = {N_n local, N_c local, blocks of A_uu, A_uf, A_fu, A_ff}.  Host only. */
+tsp_status tsp_assembly_sizes(const tsp_asm_params *p, int rank, int nranks, int zblock, int64_t out6[6]);
+/* blocks = {A_uu, A_uf, A_fu, A_ff}: this rank's rows with GLOBAL column ids, fs: 2 per local cell.  Writes the
+ * unscaled values (p_unit applied) and returns in row_max (host) this rank's maxima of the row l1 norms of
+ * (A_uu rows, A_ss entries, A_pp entries); the caller takes the maximum over the ranks and passes it to
+ * tsp_assemble_scale, which applies the block-row scaling and the Dirichlet rows (scales out: 1/max, host).
+ * Ordered on `stream` (cudaStream_t; 0 = legacy default); both calls synchronise it.  Errors: TSP_ERR_INVALID_ARG
+ * on null pointers or a bad grid, TSP_ERR_CUDA. */
+tsp_status tsp_assemble(const tsp_asm_params *p, int rank, int nranks, int zblock, const tsp_cell_fields *f,
+                        tsp_bsr_out blocks[4], double *fs, double row_max[3], void *stream);
+tsp_status tsp_assemble_scale(const tsp_asm_params *p, int rank, int nranks, int zblock, const double row_max[3],
+                              tsp_bsr_out blocks[4], double *fs, double scales[3], void *stream);
+
 /* Test hook (row c.5 parity): copy level `lvl` of hierarchy `which` (0 mech, 1
  * pressure) to host buffers.  Sizes: out6 = {n, nnz(A), nagg, nnz(P), nc,
  * coarsest}.  Any buffer may be NULL; A_v/P_v/dl1 are [entry][nc]. */

@@ -1,0 +1,452 @@
+// assemble.cu -- GPU assembly of the linearised coupled Jacobian ("GPU assembly of the Appendix B
+// Jacobian"): the four blocks of eq:jac_system and the fixed-stress diagonals (eq:FS_Dps_Dpp)
+// from per-cell fields, in exactly the layout tsp_create consumes, directly in device memory -- the host never holds
+// the 27 GB of a C5 Jacobian.  The synthetic generator (synth/synth.c) assembles the same matrices on the CPU and is
+// the oracle of this step (tests/test_gpu_assemble.py); the two share no code.
+//
+// Physics (P:n = PAPER.md lines):
+//   Q1 elasticity, 2x2x2 Gauss: A_uu = int grad(N_a)^T C grad(N_b) + the gravity term g d(rho)/d(eps_v)
+//   Biot coupling:  A_us = g drho/ds int N_a e_z;  A_up = -b int dN_a/dx_d + g drho/dp int N_a e_z
+//   A_su, A_pu:     s rho_w b int dN_a/dx_d, (1-s) rho_nw b int dN_a/dx_d
+//   A_ff:           accumulation + TPFA two-phase fluxes with single-point upwinding and
+//                   phase-averaged densities (eq:num_flux_approx P:207-216, eq:avg_density P:218-227,
+//                   eq:jac_f_int P:1104-1137; sign convention SURVEY D24) + Peaceman wells (eq:peaceman P:240-257)
+//   fluids / rel-perm: P:714-721; porosity: eq:linearized_porosity P:141
+//   units of p (R-punit), block-row scaling 1/max row l1 (R-scale), bottom Dirichlet rows (R-dirichlet)
+// One thread per row gathers every contribution of the row in a fixed order (no atomics on values).  A z-slab rank
+// assembles its owned rows with global column ids; the row scaling needs the global row maxima, so the assembly is
+// split: tsp_assemble (values + this rank's maxima) and tsp_assemble_scale (global scales + Dirichlet rows).
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "tsp_internal.cuh"
+
+namespace tsp {
+
+// Gauss integrals of the Q1 shape functions on a cube of side h (local node a = ax + 2 ay + 4 az):
+//   KK[a][b][d][e] = int dN_a/dx_d dN_b/dx_e,  NB[a][b][e] = int N_a dN_b/dx_e,  NI[a] = int N_a,  DN[a][d] = int dN_a/dx_d
+struct Q1 {
+    double KK[8][8][3][3], NB[8][8][3], NI[8], DN[8][3];
+};
+
+static void q1_tables(double h, Q1 &q)
+{
+    memset(&q, 0, sizeof(q));
+    const double xg[2] = {-1.0 / std::sqrt(3.0), 1.0 / std::sqrt(3.0)};
+    const double jac = 0.5 * h, wdet = jac * jac * jac;   // unit Gauss weights, |J| = (h/2)^3
+    for (int p = 0; p < 8; ++p) {
+        const double xi[3] = {xg[p & 1], xg[(p >> 1) & 1], xg[(p >> 2) & 1]};
+        double N[8], G[8][3];
+        for (int a = 0; a < 8; ++a) {
+            double f[3], df[3];
+            for (int d = 0; d < 3; ++d) {
+                const double sgn = ((a >> d) & 1) ? 1.0 : -1.0;
+                f[d] = 0.5 * (1.0 + sgn * xi[d]);
+                df[d] = 0.5 * sgn / jac;
+            }
+            N[a] = f[0] * f[1] * f[2];
+            G[a][0] = df[0] * f[1] * f[2];
+            G[a][1] = f[0] * df[1] * f[2];
+            G[a][2] = f[0] * f[1] * df[2];
+        }
+        for (int a = 0; a < 8; ++a) {
+            q.NI[a] += N[a] * wdet;
+            for (int d = 0; d < 3; ++d) q.DN[a][d] += G[a][d] * wdet;
+            for (int b = 0; b < 8; ++b)
+                for (int d = 0; d < 3; ++d) {
+                    q.NB[a][b][d] += N[a] * G[b][d] * wdet;
+                    for (int e = 0; e < 3; ++e) q.KK[a][b][d][e] += G[a][d] * G[b][e] * wdet;
+                }
+        }
+    }
+}
+
+struct AsmGeo {
+    int nx, ny, nz;
+    int64_t node0, cell0;   // first owned node / cell (global)
+    int nn, ncl;            // owned nodes / cells
+    double h;
+};
+
+// state of one cell at the linearisation point (Lame constants, densities, relative permeabilities and the
+// derivatives the blocks need)
+struct CellSt {
+    double lam, mu, Kdr, phi, s, p, z;
+    double rw, rn, drw, drn, krw, krn, dkrw, dkrn;
+    double drho_de, drho_ds, drho_dp, dphi_dp;
+};
+
+__device__ __forceinline__ CellSt cell_st(const tsp_asm_params &P, const AsmGeo &g, int64_t c, const double *__restrict__ E,
+                                          const double *__restrict__ phi, const double *__restrict__ sat,
+                                          const double *__restrict__ pres)
+{
+    CellSt C;
+    const double nu = P.nu, b = P.biot, e = E[c];
+    C.lam = e * nu / ((1 + nu) * (1 - 2 * nu));
+    C.mu = e / (2 * (1 + nu));
+    C.Kdr = e / (3 * (1 - 2 * nu));
+    C.phi = phi[c]; C.s = sat[c]; C.p = pres[c];
+    C.z = (c / ((int64_t)g.nx * g.ny) + 0.5) * g.h;
+    C.rw = P.rho_w0 * (1 + P.c_w * (C.p - P.p0));
+    C.rn = P.rho_nw0 * (1 + P.c_nw * (C.p - P.p0));
+    C.drw = P.rho_w0 * P.c_w;
+    C.drn = P.rho_nw0 * P.c_nw;
+    const double span = 1.0 - P.swr - P.snwr;
+    double se = (C.s - P.swr) / span, dse = 1.0 / span;
+    if (se <= 0) { se = 0; dse = 0; }
+    if (se >= 1) { se = 1; dse = 0; }
+    C.krw = se * se; C.dkrw = 2 * se * dse;                  // Corey n = 2
+    C.krn = (1 - se) * (1 - se); C.dkrn = -2 * (1 - se) * dse;
+    C.dphi_dp = (b - C.phi) * (1 - b) / C.Kdr;               // eq:linearized_porosity; d phi / d eps_v = b
+    const double bracket = -P.rho_s + C.s * C.rw + (1 - C.s) * C.rn;
+    C.drho_de = bracket * b;
+    C.drho_ds = C.phi * (C.rw - C.rn);
+    C.drho_dp = bracket * C.dphi_dp + C.s * C.phi * C.drw + (1 - C.s) * C.phi * C.drn;
+    return C;
+}
+
+// ---------------------------------------------------------------- row lengths
+__global__ void k_asm_counts(AsmGeo g, int32_t *cuu, int32_t *cuf, int32_t *cff)
+{
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int NX = g.nx + 1, NY = g.ny + 1;
+    if (t < g.nn) {
+        const int64_t n = g.node0 + t;
+        const int i = n % NX, j = (n / NX) % NY, k = n / ((int64_t)NX * NY);
+        const int ex = (i > 0) + (i < g.nx), ey = (j > 0) + (j < g.ny), ez = (k > 0) + (k < g.nz);
+        cuu[t] = (1 + ex) * (1 + ey) * (1 + ez);
+        cuf[t] = ex * ey * ez;
+    }
+    if (t < g.ncl) {
+        const int64_t c = g.cell0 + t;
+        const int i = c % g.nx, j = (c / g.nx) % g.ny, k = c / ((int64_t)g.nx * g.ny);
+        cff[t] = 1 + (i > 0) + (i < g.nx - 1) + (j > 0) + (j < g.ny - 1) + (k > 0) + (k < g.nz - 1);
+    }
+}
+
+// ---------------------------------------------------------------- node rows: A_uu, A_uf
+__global__ void __launch_bounds__(128) k_asm_node(tsp_asm_params P, AsmGeo g, const Q1 *__restrict__ q,
+                                                  const double *__restrict__ E, const double *__restrict__ phi,
+                                                  const double *__restrict__ sat, const double *__restrict__ pres,
+                                                  const int32_t *__restrict__ rpu, int32_t *__restrict__ cu, double *__restrict__ vu,
+                                                  const int32_t *__restrict__ rpf, int32_t *__restrict__ cf, double *__restrict__ vf)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= g.nn) return;
+    const int NX = g.nx + 1, NY = g.ny + 1;
+    const int64_t n = g.node0 + t;
+    const int i = n % NX, j = (n / NX) % NY, k = n / ((int64_t)NX * NY);
+    const double gr = P.gravity, b = P.biot;
+    // columns: the clipped 27 neighbours in ascending id (z, then y, then x offsets), the <= 8 adjacent cells likewise
+    int slot27[27];
+    int64_t qu = rpu[t];
+    for (int o = 0; o < 27; ++o) {
+        const int ii = i + o % 3 - 1, jj = j + (o / 3) % 3 - 1, kk = k + o / 9 - 1;
+        if (ii < 0 || ii > g.nx || jj < 0 || jj > g.ny || kk < 0 || kk > g.nz) { slot27[o] = -1; continue; }
+        slot27[o] = (int)(qu - rpu[t]);
+        cu[qu] = (int32_t)(ii + (int64_t)NX * (jj + (int64_t)NY * kk));
+        for (int e = 0; e < 9; ++e) vu[9 * qu + e] = 0.0;
+        ++qu;
+    }
+    int64_t qf = rpf[t];
+    for (int o = 0; o < 8; ++o) {          // adjacent element (i-1+ox, j-1+oy, k-1+oz)
+        const int ci = i - 1 + (o & 1), cj = j - 1 + ((o >> 1) & 1), ck = k - 1 + ((o >> 2) & 1);
+        if (ci < 0 || ci >= g.nx || cj < 0 || cj >= g.ny || ck < 0 || ck >= g.nz) continue;
+        const int64_t c = ci + (int64_t)g.nx * (cj + (int64_t)g.ny * ck);
+        cf[qf] = (int32_t)c;
+        const CellSt C = cell_st(P, g, c, E, phi, sat, pres);
+        const int a = (1 - (o & 1)) + 2 * (1 - ((o >> 1) & 1)) + 4 * (1 - ((o >> 2) & 1));   // node n inside element c
+        for (int bl = 0; bl < 8; ++bl) {
+            // node m = corner bl of element c; its offset from n picks the block
+            const int dx = (bl & 1) - (a & 1), dy = ((bl >> 1) & 1) - ((a >> 1) & 1), dz = ((bl >> 2) & 1) - ((a >> 2) & 1);
+            double *B = vu + 9 * (rpu[t] + slot27[(dz + 1) * 9 + (dy + 1) * 3 + (dx + 1)]);
+            const double tr = q->KK[a][bl][0][0] + q->KK[a][bl][1][1] + q->KK[a][bl][2][2];
+            for (int d = 0; d < 3; ++d)
+                for (int e = 0; e < 3; ++e) {
+                    double v = C.lam * q->KK[a][bl][d][e] + C.mu * q->KK[a][bl][e][d];
+                    if (d == e) v += C.mu * tr;
+                    if (d == 2) v += gr * C.drho_de * q->NB[a][bl][e];
+                    B[3 * d + e] += v;
+                }
+        }
+        double *F = vf + 6 * qf;
+        for (int d = 0; d < 3; ++d) {
+            F[2 * d] = d == 2 ? gr * C.drho_ds * q->NI[a] : 0.0;
+            F[2 * d + 1] = (-b * q->DN[a][d] + (d == 2 ? gr * C.drho_dp * q->NI[a] : 0.0)) * P.p_unit;
+        }
+        ++qf;
+    }
+}
+
+// ---------------------------------------------------------------- cell rows: A_fu, A_ff, wells, D_fs
+__global__ void __launch_bounds__(128) k_asm_cell(tsp_asm_params P, AsmGeo g, const Q1 *__restrict__ q,
+                                                  const double *__restrict__ E, const double *__restrict__ perm,
+                                                  const double *__restrict__ phi, const double *__restrict__ sat,
+                                                  const double *__restrict__ pres, const int8_t *__restrict__ well,
+                                                  int32_t *__restrict__ cfu, double *__restrict__ vfu,
+                                                  const int32_t *__restrict__ rpf, int32_t *__restrict__ cff, double *__restrict__ vff,
+                                                  double *__restrict__ fs)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= g.ncl) return;
+    const int NX = g.nx + 1, NY = g.ny + 1;
+    const int64_t c = g.cell0 + t, P2 = (int64_t)g.nx * g.ny;
+    const int i = c % g.nx, j = (c / g.nx) % g.ny, k = c / P2;
+    const double h = g.h, V = h * h * h, gr = P.gravity, b = P.biot, dt = P.dt, pu = P.p_unit;
+    const CellSt K = cell_st(P, g, c, E, phi, sat, pres);
+    // A_fu: the 8 corner nodes of the cell
+    for (int a = 0; a < 8; ++a) {
+        const int64_t qq = 8 * (int64_t)t + a;
+        cfu[qq] = (int32_t)((i + (a & 1)) + (int64_t)NX * ((j + ((a >> 1) & 1)) + (int64_t)NY * (k + ((a >> 2) & 1))));
+        for (int d = 0; d < 3; ++d) {
+            vfu[6 * qq + d] = K.s * K.rw * b * q->DN[a][d];
+            vfu[6 * qq + 3 + d] = (1 - K.s) * K.rn * b * q->DN[a][d];
+        }
+    }
+    // A_ff: 7-point pattern in ascending column order
+    int64_t nb[7];
+    int np = 0;
+    if (k > 0) nb[np++] = c - P2;
+    if (j > 0) nb[np++] = c - g.nx;
+    if (i > 0) nb[np++] = c - 1;
+    nb[np++] = c;
+    if (i < g.nx - 1) nb[np++] = c + 1;
+    if (j < g.ny - 1) nb[np++] = c + g.nx;
+    if (k < g.nz - 1) nb[np++] = c + P2;
+    const int64_t r0 = rpf[t];
+    int dpos = 0;
+    for (int u = 0; u < np; ++u) {
+        cff[r0 + u] = (int32_t)nb[u];
+        for (int e = 0; e < 4; ++e) vff[4 * (r0 + u) + e] = 0.0;
+        if (nb[u] == c) dpos = u;
+    }
+    double *D = vff + 4 * (r0 + dpos);
+    // accumulation: d(phi rho_alpha s_alpha V)/d(s, p)
+    D[0] += V * K.phi * K.rw;
+    D[1] += V * (K.s * K.rw * K.dphi_dp + K.phi * K.s * K.drw);
+    D[2] += V * (-K.phi * K.rn);
+    D[3] += V * ((1 - K.s) * K.rn * K.dphi_dp + K.phi * (1 - K.s) * K.drn);
+    // faces
+    for (int u = 0; u < np; ++u) {
+        const int64_t o = nb[u];
+        if (o == c) continue;
+        const int64_t cK = c < o ? c : o, cL = c < o ? o : c;
+        const CellSt A = (cK == c) ? K : cell_st(P, g, cK, E, phi, sat, pres);
+        const CellSt B = (cL == c) ? K : cell_st(P, g, cL, E, phi, sat, pres);
+        const double tK = h * h * perm[cK] * (h / 2) / ((h / 2) * (h / 2));     // eq:half_trans
+        const double tL = h * h * perm[cL] * (h / 2) / ((h / 2) * (h / 2));
+        const double T = (tK + tL) > 0 ? tK * tL / (tK + tL) : 0.0;           // eq:trans
+        const double dz = B.z - A.z, sgn = (c == cK) ? -1.0 : 1.0;
+        const int posK = (cK == c) ? dpos : u, posL = (cL == c) ? dpos : u;
+        for (int ph = 0; ph < 2; ++ph) {
+            const double rK = ph ? A.rn : A.rw, rL = ph ? B.rn : B.rw, dK = ph ? A.drn : A.drw, dL = ph ? B.drn : B.drw;
+            const double krK = ph ? A.krn : A.krw, krL = ph ? B.krn : B.krw, dkK = ph ? A.dkrn : A.dkrw, dkL = ph ? B.dkrn : B.dkrw;
+            const double mu = ph ? P.mu_nw : P.mu_w;
+            const bool inK = krK > 0, inL = krL > 0;
+            double vr = 0, dvK = 0, dvL = 0;                          // eq:avg_density over the phases present
+            if (inK && inL) { vr = 0.5 * (rK + rL); dvK = 0.5 * dK; dvL = 0.5 * dL; }
+            else if (inK) { vr = rK; dvK = dK; }
+            else if (inL) { vr = rL; dvL = dL; }
+            const double Phi = T * ((B.p - A.p) + vr * gr * dz);
+            const bool upL = Phi > 0;                                  // ties upstream = K
+            const double rup = upL ? rL : rK, drup = upL ? dL : dK, lup = (upL ? krL : krK) / mu, dkup = upL ? dkL : dkK;
+            const double dFds = rup / mu * Phi * dkup;
+            const double dFdpK = (upL ? 0.0 : drup * lup) * Phi + rup * lup * T * (-1.0 + dvK * gr * dz);
+            const double dFdpL = (upL ? drup * lup : 0.0) * Phi + rup * lup * T * (1.0 + dvL * gr * dz);
+            const double cf = sgn * dt;
+            vff[4 * (r0 + (upL ? posL : posK)) + 2 * ph] += cf * dFds;
+            vff[4 * (r0 + posK) + 2 * ph + 1] += cf * dFdpK;
+            vff[4 * (r0 + posL) + 2 * ph + 1] += cf * dFdpL;
+        }
+    }
+    // Peaceman wells: water injector at BHP + dbhp, producers at BHP - dbhp (per-cell perforation flags)
+    const int wt = well ? well[c] : 0;
+    if (wt) {
+        const int kw1 = P.burden > 0 ? g.nz - P.burden : g.nz;
+        const double zbh = (kw1 - 0.5) * h, ztop = g.nz * h;
+        const double pbh = P.p0 + P.rho_w0 * gr * (ztop - zbh) + (wt == 1 ? P.well_dbhp : -P.well_dbhp);
+        const double re = 0.28 * sqrt(h * h + h * h) / 2.0;
+        const double WI = 2 * M_PI * h * perm[c] / log(re / (P.rw_over_h * h));
+        const double lw = K.krw / P.mu_w, ln = K.krn / P.mu_nw;
+        for (int ph = 0; ph < 2; ++ph) {
+            const double r = ph ? K.rn : K.rw, dr = ph ? K.drn : K.drw;
+            const double Phi = WI * ((pbh + r * gr * zbh) - (K.p + r * gr * K.z));
+            const double dPhi = WI * (-1.0 + dr * gr * (zbh - K.z));
+            double dqs = 0, dqp = 0;
+            if (wt == 1) {
+                if (ph == 0 && Phi > 0) {                              // water-only injection with the total mobility
+                    dqs = r * (K.dkrw / P.mu_w + K.dkrn / P.mu_nw) * Phi;
+                    dqp = dr * (lw + ln) * Phi + r * (lw + ln) * dPhi;
+                }
+            } else if (Phi < 0) {                                      // production of each phase
+                const double l = ph ? ln : lw, dk = ph ? K.dkrn : K.dkrw, mu = ph ? P.mu_nw : P.mu_w;
+                dqs = r * dk / mu * Phi;
+                dqp = dr * l * Phi + r * l * dPhi;
+            }
+            D[2 * ph] += -dt * dqs;
+            D[2 * ph + 1] += -dt * dqp;
+        }
+    }
+    // pressure unit on the p columns (R-punit)
+    for (int u = 0; u < np; ++u) { vff[4 * (r0 + u) + 1] *= pu; vff[4 * (r0 + u) + 3] *= pu; }
+    // fixed-stress diagonals (eq:FS_Dps_Dpp), in p-column units
+    fs[2 * t] = V * b * b / K.Kdr * K.s * K.rw * pu;
+    fs[2 * t + 1] = V * b * b / K.Kdr * (1 - K.s) * K.rn * pu;
+}
+
+// ---------------------------------------------------------------- row maxima of the l1 norms (R-scale)
+// u: sum_{q, e} |A_uu[q][d][e]| per node row d; s: sum_q |A_ss|; p: sum_q |A_pp| (the reference's measure)
+__global__ void k_asm_rowmax(AsmGeo g, const int32_t *__restrict__ rpu, const double *__restrict__ vu,
+                             const int32_t *__restrict__ rpf, const double *__restrict__ vff, unsigned long long *mx)
+{
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double mu_ = 0, ms = 0, mp = 0;
+    if (t < g.nn)
+        for (int d = 0; d < 3; ++d) {
+            double s = 0;
+            for (int64_t q = rpu[t]; q < rpu[t + 1]; ++q)
+                for (int e = 0; e < 3; ++e) s += fabs(vu[9 * q + 3 * d + e]);
+            mu_ = fmax(mu_, s);
+        }
+    if (t < g.ncl) {
+        for (int64_t q = rpf[t]; q < rpf[t + 1]; ++q) { ms += fabs(vff[4 * q]); mp += fabs(vff[4 * q + 3]); }
+    }
+    // values >= 0: their bit patterns order like the values
+    if (mu_ > 0) atomicMax(mx + 0, (unsigned long long)__double_as_longlong(mu_));
+    if (ms > 0) atomicMax(mx + 1, (unsigned long long)__double_as_longlong(ms));
+    if (mp > 0) atomicMax(mx + 2, (unsigned long long)__double_as_longlong(mp));
+}
+
+// ---------------------------------------------------------------- scaling + Dirichlet rows (R-scale, R-dirichlet)
+__global__ void k_asm_scale_nodes(AsmGeo g, double su, int dirichlet, const int32_t *__restrict__ rpu, const int32_t *__restrict__ cu,
+                                  double *__restrict__ vu, const int32_t *__restrict__ rpf, double *__restrict__ vf)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= g.nn) return;
+    const int64_t nbot = (int64_t)(g.nx + 1) * (g.ny + 1), n = g.node0 + t;
+    const bool fixed_row = dirichlet && n < nbot;
+    for (int64_t q = rpu[t]; q < rpu[t + 1]; ++q) {
+        const bool fixed_col = dirichlet && cu[q] < nbot;
+        for (int e = 0; e < 9; ++e) vu[9 * q + e] = (fixed_row || fixed_col) ? 0.0 : vu[9 * q + e] * su;
+        if (fixed_row && cu[q] == n) { vu[9 * q] = 1.0; vu[9 * q + 4] = 1.0; vu[9 * q + 8] = 1.0; }
+    }
+    for (int64_t q = rpf[t]; q < rpf[t + 1]; ++q)
+        for (int e = 0; e < 6; ++e) vf[6 * q + e] = fixed_row ? 0.0 : vf[6 * q + e] * su;
+}
+__global__ void k_asm_scale_cells(AsmGeo g, double ss, double sp, int dirichlet, const int32_t *__restrict__ cfu,
+                                  double *__restrict__ vfu, const int32_t *__restrict__ rpf, double *__restrict__ vff,
+                                  double *__restrict__ fs)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= g.ncl) return;
+    const int64_t nbot = (int64_t)(g.nx + 1) * (g.ny + 1);
+    for (int a = 0; a < 8; ++a) {
+        const int64_t q = 8 * (int64_t)t + a;
+        const bool fixed_col = dirichlet && cfu[q] < nbot;
+        for (int d = 0; d < 3; ++d) {
+            vfu[6 * q + d] = fixed_col ? 0.0 : vfu[6 * q + d] * ss;
+            vfu[6 * q + 3 + d] = fixed_col ? 0.0 : vfu[6 * q + 3 + d] * sp;
+        }
+    }
+    for (int64_t q = rpf[t]; q < rpf[t + 1]; ++q) {
+        vff[4 * q] *= ss; vff[4 * q + 1] *= ss; vff[4 * q + 2] *= sp; vff[4 * q + 3] *= sp;
+    }
+    fs[2 * t] *= ss; fs[2 * t + 1] *= sp;
+}
+
+static AsmGeo asm_geo(const tsp_asm_params &P, int rank, int nranks, int zblock)
+{
+    int64_t part[6];
+    partition(P.nx, P.ny, P.nz, zblock > 0 ? zblock : 16, rank, nranks, part);
+    AsmGeo g;
+    g.nx = P.nx; g.ny = P.ny; g.nz = P.nz;
+    g.node0 = part[2]; g.nn = (int)part[3]; g.cell0 = part[4]; g.ncl = (int)part[5];
+    g.h = (P.length > 0 ? P.length : 1.0) / P.nx;
+    return g;
+}
+
+void assembly_sizes(const tsp_asm_params &P, int rank, int nranks, int zblock, int64_t out[6])
+{
+    const AsmGeo g = asm_geo(P, rank, nranks, zblock);
+    const int NX = P.nx + 1, NY = P.ny + 1;
+    int64_t buu = 0, buf = 0, bff = 0;
+    std::vector<int> cx(NX), cy(NY);   // per-coordinate factors, summed plane by plane
+    for (int64_t n = g.node0; n < g.node0 + g.nn; ++n) {
+        const int i = n % NX, j = (n / NX) % NY, k = n / ((int64_t)NX * NY);
+        const int ex = (i > 0) + (i < P.nx), ey = (j > 0) + (j < P.ny), ez = (k > 0) + (k < P.nz);
+        buu += (1 + ex) * (1 + ey) * (1 + ez);
+        buf += ex * ey * ez;
+    }
+    for (int64_t c = g.cell0; c < g.cell0 + g.ncl; ++c) {
+        const int i = c % P.nx, j = (c / P.nx) % P.ny, k = c / ((int64_t)P.nx * P.ny);
+        bff += 1 + (i > 0) + (i < P.nx - 1) + (j > 0) + (j < P.ny - 1) + (k > 0) + (k < P.nz - 1);
+    }
+    out[0] = g.nn; out[1] = g.ncl; out[2] = buu; out[3] = buf; out[4] = 8 * (int64_t)g.ncl; out[5] = bff;
+}
+
+void assemble(cudaStream_t s, const tsp_asm_params &P, int rank, int nranks, int zblock, const tsp_cell_fields &f,
+              tsp_bsr_out blk[4], double *fs, double row_max[3])
+{
+    TSP_REQUIRE(P.nx > 0 && P.ny > 0 && P.nz > 0, TSP_ERR_INVALID_ARG, "assemble: grid dimensions must be positive");
+    TSP_REQUIRE(f.E && f.perm && f.phi && f.sat && f.pres, TSP_ERR_INVALID_ARG, "assemble: null field");
+    for (int k = 0; k < 4; ++k)
+        TSP_REQUIRE(blk[k].rowptr && blk[k].col && blk[k].val, TSP_ERR_INVALID_ARG, "assemble: null output block");
+    TSP_REQUIRE(fs, TSP_ERR_INVALID_ARG, "assemble: null fs");
+    const AsmGeo g = asm_geo(P, rank, nranks, zblock);
+    Q1 q;
+    q1_tables(g.h, q);
+    DBuf<Q1> dq; dq.alloc(1);
+    DBuf<int32_t> cnt; cnt.alloc((size_t)3 * (std::max(g.nn, g.ncl) + 1));
+    int32_t *cuu = cnt.p, *cuf = cnt.p + std::max(g.nn, g.ncl) + 1, *cff = cuf + std::max(g.nn, g.ncl) + 1;
+    TSP_CUDA(cudaMemcpyAsync(dq.p, &q, sizeof(Q1), cudaMemcpyHostToDevice, s));
+    const int m = std::max(g.nn, g.ncl);
+    if (m) k_asm_counts<<<grid_for(m, 256), 256, 0, s>>>(g, cuu, cuf, cff);
+    auto scan = [&](int32_t *c, int len, int32_t *rp) {
+        TSP_CUDA(cudaMemsetAsync(c + len, 0, sizeof(int32_t), s));
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, c, rp, len + 1, s);
+        DBuf<uint8_t> tmp; tmp.alloc(std::max<size_t>(tb, 1));
+        cub::DeviceScan::ExclusiveSum(tmp.p, tb, c, rp, len + 1, s);
+    };
+    scan(cuu, g.nn, blk[0].rowptr);
+    scan(cuf, g.nn, blk[1].rowptr);
+    scan(cff, g.ncl, blk[3].rowptr);
+    {   // A_fu: 8 nodes per cell
+        std::vector<int32_t> rp(g.ncl + 1);
+        for (int c = 0; c <= g.ncl; ++c) rp[c] = 8 * c;
+        TSP_CUDA(cudaMemcpyAsync(blk[2].rowptr, rp.data(), sizeof(int32_t) * (g.ncl + 1), cudaMemcpyHostToDevice, s));
+        TSP_CUDA(cudaStreamSynchronize(s));   // rp is a host temporary
+    }
+    if (g.nn) k_asm_node<<<grid_for(g.nn, 128), 128, 0, s>>>(P, g, dq.p, f.E, f.phi, f.sat, f.pres, blk[0].rowptr, blk[0].col,
+                                                            blk[0].val, blk[1].rowptr, blk[1].col, blk[1].val);
+    if (g.ncl) k_asm_cell<<<grid_for(g.ncl, 128), 128, 0, s>>>(P, g, dq.p, f.E, f.perm, f.phi, f.sat, f.pres, f.well, blk[2].col,
+                                                              blk[2].val, blk[3].rowptr, blk[3].col, blk[3].val, fs);
+    DBuf<unsigned long long> mx; mx.alloc(3); mx.zero(s);
+    if (m) k_asm_rowmax<<<grid_for(m, 256), 256, 0, s>>>(g, blk[0].rowptr, blk[0].val, blk[3].rowptr, blk[3].val, mx);
+    TSP_CUDA(cudaGetLastError());
+    unsigned long long hb[3];
+    TSP_CUDA(cudaMemcpyAsync(hb, mx.p, sizeof(hb), cudaMemcpyDeviceToHost, s));
+    TSP_CUDA(cudaStreamSynchronize(s));
+    for (int k = 0; k < 3; ++k) memcpy(&row_max[k], &hb[k], sizeof(double));
+}
+
+void assemble_scale(cudaStream_t s, const tsp_asm_params &P, int rank, int nranks, int zblock, const double row_max[3],
+                    tsp_bsr_out blk[4], double *fs, double scales[3])
+{
+    const AsmGeo g = asm_geo(P, rank, nranks, zblock);
+    double sc[3] = {1.0, 1.0, 1.0};
+    if (P.row_scale)
+        for (int k = 0; k < 3; ++k) sc[k] = row_max[k] > 0 ? 1.0 / row_max[k] : 1.0;
+    if (g.nn) k_asm_scale_nodes<<<grid_for(g.nn, 128), 128, 0, s>>>(g, sc[0], P.dirichlet_bottom, blk[0].rowptr, blk[0].col,
+                                                                   blk[0].val, blk[1].rowptr, blk[1].val);
+    if (g.ncl) k_asm_scale_cells<<<grid_for(g.ncl, 128), 128, 0, s>>>(g, sc[1], sc[2], P.dirichlet_bottom, blk[2].col, blk[2].val,
+                                                                     blk[3].rowptr, blk[3].val, fs);
+    TSP_CUDA(cudaGetLastError());
+    TSP_CUDA(cudaStreamSynchronize(s));
+    if (scales) for (int k = 0; k < 3; ++k) scales[k] = sc[k];
+}
+
+}  // namespace tsp

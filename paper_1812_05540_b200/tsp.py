@@ -41,6 +41,24 @@ class tsp_bsr(C.Structure):
     _fields_ = [("rowptr", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p)]
 
 
+class tsp_asm_params(C.Structure):
+    _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("length", C.c_double),
+                ("nu", C.c_double), ("biot", C.c_double), ("gravity", C.c_double), ("dt", C.c_double),
+                ("rho_w0", C.c_double), ("rho_nw0", C.c_double), ("c_w", C.c_double), ("c_nw", C.c_double),
+                ("mu_w", C.c_double), ("mu_nw", C.c_double), ("rho_s", C.c_double), ("p0", C.c_double),
+                ("swr", C.c_double), ("snwr", C.c_double), ("well_dbhp", C.c_double), ("rw_over_h", C.c_double),
+                ("p_unit", C.c_double), ("burden", C.c_int), ("dirichlet_bottom", C.c_int), ("row_scale", C.c_int)]
+
+
+class tsp_cell_fields(C.Structure):
+    _fields_ = [("E", C.c_void_p), ("perm", C.c_void_p), ("phi", C.c_void_p), ("sat", C.c_void_p),
+                ("pres", C.c_void_p), ("well", C.c_void_p)]
+
+
+class tsp_bsr_out(C.Structure):
+    _fields_ = [("rowptr", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p)]
+
+
 _ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 _FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 
@@ -155,6 +173,11 @@ def lib():
         L.tsp_level_dist.argtypes = [C.c_void_p, C.c_int, C.c_int, _P(C.c_int64)]
         L.tsp_variant_counts.argtypes = [C.c_void_p, _P(C.c_int64)]
         L.tsp_export_colour.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, _P(C.c_int), _P(C.c_int)]
+        L.tsp_assembly_sizes.argtypes = [_P(tsp_asm_params), C.c_int, C.c_int, C.c_int, _P(C.c_int64)]
+        L.tsp_assemble.argtypes = [_P(tsp_asm_params), C.c_int, C.c_int, C.c_int, _P(tsp_cell_fields), _P(tsp_bsr_out),
+                                   C.c_void_p, _P(C.c_double), C.c_void_p]
+        L.tsp_assemble_scale.argtypes = [_P(tsp_asm_params), C.c_int, C.c_int, C.c_int, _P(C.c_double), _P(tsp_bsr_out),
+                                         C.c_void_p, _P(C.c_double), C.c_void_p]
         if L.tsp_abi_version() != 4:
             raise RuntimeError("libtsp ABI version mismatch")
         _LIB = L
@@ -165,7 +188,8 @@ EXPORTED = ["tsp_abi_version", "tsp_last_error", "tsp_default_options", "tsp_cre
             "tsp_apply_preconditioner", "tsp_apply_operator", "tsp_solve", "tsp_default_solve_opts",
             "tsp_get_stats", "tsp_level_sizes", "tsp_export_level", "tsp_prof_enable", "tsp_prof_read",
             "tsp_prof_classes", "tsp_export_cpr", "tsp_destroy", "tsp_nccl_unique_id", "tsp_local_world_create", "tsp_local_world_destroy",
-            "tsp_partition", "tsp_level_dist", "tsp_variant_counts", "tsp_export_colour"]
+            "tsp_partition", "tsp_level_dist", "tsp_variant_counts", "tsp_export_colour",
+            "tsp_assembly_sizes", "tsp_assemble", "tsp_assemble_scale"]
 
 # include/tsp.h TSP_VAR_* order
 VARIANTS = ["spgemm_hs64", "spgemm_hs128", "spgemm_hs512", "spgemm_hs4096", "spgemm_g4", "spgemm_g8", "spgemm_g32",
@@ -179,6 +203,67 @@ def partition(nx, ny, nz, zblock, rank, nranks):
     out = (C.c_int64 * 6)()
     _check(lib().tsp_partition(nx, ny, nz, zblock, rank, nranks, out), "tsp_partition")
     return tuple(out)
+
+
+class AssembledProblem:
+    """The blocks of tsp_assemble in device memory (torch CUDA tensors) with the attributes Tsp(...,
+    device_inputs=True) reads; for a z-slab rank they are its owned rows with global column ids."""
+
+    def __init__(self, nx, ny, nz, Nn, Nc, arrays, scales, row_max):
+        self.nx, self.ny, self.nz, self.Nn, self.Nc = nx, ny, nz, Nn, Nc
+        self.n = 3 * Nn + 2 * Nc
+        self.scales, self.row_max = scales, row_max
+        for k, v in arrays.items():
+            setattr(self, k, v)
+
+
+ASM_KEYS = ("nu", "biot", "gravity", "dt", "rho_w0", "rho_nw0", "c_w", "c_nw", "mu_w", "mu_nw", "rho_s", "p0",
+            "swr", "snwr", "well_dbhp", "rw_over_h", "p_unit", "length", "burden", "dirichlet_bottom", "row_scale")
+
+
+def assemble(params: dict, fields: dict, rank=0, nranks=1, zblock=16, stream=None, global_max=None):
+    """GPU assembly of the Jacobian (tsp_assemble + tsp_assemble_scale).  `params`: the physical
+    parameters (keys of include/tsp.h tsp_asm_params, e.g. synth.params_of(config)); `fields`: per-cell arrays of
+    the GLOBAL grid (E, perm, phi, sat, pres as float64, well as int8; numpy or CUDA tensors).  `global_max`:
+    callable turning this rank's 3 row maxima into the maxima over all ranks (needed when nranks > 1)."""
+    import torch
+    L = lib()
+    P = tsp_asm_params(nx=params["nx"], ny=params["ny"], nz=params["nz"],
+                       **{k: (int(params[k]) if k in ("burden", "dirichlet_bottom", "row_scale") else float(params[k]))
+                          for k in ASM_KEYS})
+    sz = (C.c_int64 * 6)()
+    _check(L.tsp_assembly_sizes(C.byref(P), rank, nranks, zblock, sz), "tsp_assembly_sizes")
+    Nn, Nc, Buu, Buf, Bfu, Bff = (int(v) for v in sz)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    keep = {}
+    for k in ("E", "perm", "phi", "sat", "pres"):
+        keep[k] = torch.as_tensor(fields[k], dtype=torch.float64).to(dev).contiguous()
+    if fields.get("well") is not None:
+        keep["well"] = torch.as_tensor(fields["well"], dtype=torch.int8).to(dev).contiguous()
+    f = tsp_cell_fields(*(keep[k].data_ptr() for k in ("E", "perm", "phi", "sat", "pres")),
+                        keep["well"].data_ptr() if "well" in keep else None)
+    a = {}
+    for name, rows, nb, bs in (("uu", Nn, Buu, 9), ("uf", Nn, Buf, 6), ("fu", Nc, Bfu, 6), ("ff", Nc, Bff, 4)):
+        a[name + "_rowptr"] = torch.empty(rows + 1, dtype=torch.int32, device=dev)
+        a[name + "_col"] = torch.empty(max(nb, 1), dtype=torch.int32, device=dev)
+        a[name + "_val"] = torch.empty(max(nb, 1) * bs, dtype=torch.float64, device=dev)
+    a["fs"] = torch.empty(max(2 * Nc, 1), dtype=torch.float64, device=dev)
+    blocks = (tsp_bsr_out * 4)(*(tsp_bsr_out(a[n + "_rowptr"].data_ptr(), a[n + "_col"].data_ptr(), a[n + "_val"].data_ptr())
+                                 for n in ("uu", "uf", "fu", "ff")))
+    st = stream if stream is not None else torch.cuda.current_stream()
+    rmax = (C.c_double * 3)()
+    _check(L.tsp_assemble(C.byref(P), rank, nranks, zblock, C.byref(f), blocks, C.c_void_p(a["fs"].data_ptr()), rmax,
+                          C.c_void_p(st.cuda_stream)), "tsp_assemble")
+    mx = list(rmax)
+    if nranks > 1:
+        if global_max is None:
+            raise ValueError("assemble: nranks > 1 needs global_max (the row maxima over all ranks)")
+        mx = list(global_max(mx))
+    gmx = (C.c_double * 3)(*mx)
+    sc = (C.c_double * 3)()
+    _check(L.tsp_assemble_scale(C.byref(P), rank, nranks, zblock, gmx, blocks, C.c_void_p(a["fs"].data_ptr()), sc,
+                                C.c_void_p(st.cuda_stream)), "tsp_assemble_scale")
+    return AssembledProblem(params["nx"], params["ny"], params["nz"], Nn, Nc, a, list(sc), mx)
 
 
 def nccl_unique_id() -> bytes:
@@ -284,6 +369,8 @@ class Tsp:
 
     def _desc(self, pb, device_inputs, keep):
         """tsp_desc with the grid, this rank and the four blocks + fs_diag of `pb` (arrays kept alive in `keep`)."""
+        device_inputs = device_inputs or bool(getattr(pb.uu_val, "is_cuda", False))
+
         def arr(x):
             if device_inputs or hasattr(x, "data_ptr"):   # CUDA tensors, or pinned host tensors
                 keep.append(x)
@@ -295,7 +382,7 @@ class Tsp:
         d = tsp_desc()
         d.nx, d.ny, d.nz = pb.nx, pb.ny, pb.nz
         d.rank, d.nranks = self._grid
-        d.inputs_on_device = int(device_inputs)
+        d.inputs_on_device = int(device_inputs or bool(getattr(pb.uu_val, "is_cuda", False)))
         for name in ("uu", "uf", "fu", "ff"):
             b = tsp_bsr(arr(getattr(pb, name + "_rowptr")), arr(getattr(pb, name + "_col")), arr(getattr(pb, name + "_val")))
             setattr(d, "A_" + name, b)

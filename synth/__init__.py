@@ -66,6 +66,8 @@ def _lib():
         _LIB.synth_sizes.argtypes = [_P(Params), _P(C.c_int64)]
         _LIB.synth_generate.argtypes = [_P(Params), _P(Out)]
         _LIB.synth_generate.restype = C.c_int
+        _LIB.synth_fields.argtypes = [_P(Params)] + [_F64] * 6 + [_P(C.c_int8)]
+        _LIB.synth_fields.restype = C.c_int
     return _LIB
 
 
@@ -175,6 +177,34 @@ def generate(config: str | None = None, **overrides) -> Problem:
     if rc != 0:
         raise ValueError(f"synth_generate failed ({rc})")
     return Problem(nx=p.nx, ny=p.ny, nz=p.nz, params=kw, fields=f, scales=scales, **a)
+
+
+def params_of(config: str | None = None, **overrides) -> dict:
+    """The full parameter set of a config (DEFAULTS < config < overrides)."""
+    kw = dict(DEFAULTS)
+    if config is not None:
+        kw.update(CONFIGS[config] if config in CONFIGS else WORKLOADS[config])
+    kw.update(overrides)
+    return kw
+
+
+def fields(config: str | None = None, x_rand: bool = True, **overrides) -> dict:
+    """The per-cell state of `generate` (E, perm, phi, sat, pres; same seeded streams, same values), the well
+    perforation of each cell (0 none, 1 injector, 2 producer) and x_rand,
+    WITHOUT assembling the Jacobian: the input of the GPU assembly (tsp_assemble)."""
+    kw = params_of(config, **overrides)
+    p = Params(**{k: v for k, v in kw.items() if k in dict(Params._fields_)})
+    s = sizes(p.nx, p.ny, p.nz)
+    f = {k: np.empty(s["Nc"]) for k in ("E", "perm", "phi", "sat", "pres")}
+    xr = np.empty(s["n"]) if x_rand else None
+    f["well"] = np.empty(s["Nc"], np.int8)
+    rc = _lib().synth_fields(C.byref(p), *(f[k].ctypes.data_as(_F64) for k in ("E", "perm", "phi", "sat", "pres")),
+                             xr.ctypes.data_as(_F64) if xr is not None else None, f["well"].ctypes.data_as(_P(C.c_int8)))
+    if rc != 0:
+        raise ValueError(f"synth_fields failed ({rc})")
+    f["x_rand"] = xr
+    f["params"] = kw
+    return f
 
 
 def to_scipy(pb: Problem):

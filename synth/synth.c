@@ -285,6 +285,62 @@ static void cell_state(const synth_params *P, double E, double phi, double s, do
     C->drho_dp = bracket * C->dphi_dp + s * phi * C->drw + (1 - s) * phi * C->drnw; /* P:1030, drho_s/dp = 0 */
 }
 
+/* well placement (R-wells, R-s10, R-stair): 0 none, 1 injector, 2 producer perforation in cell (i, j, k) */
+static int well_type(const synth_params *P, int i, int j, int k)
+{
+    const int nx = P->nx, ny = P->ny, nz = P->nz;
+    const int kw0 = P->burden > 0 ? P->burden : 0, kw1 = P->burden > 0 ? nz - P->burden : nz;   /* perforated layers */
+    int inj = (i == 0 && j == 0), prod = (i == nx - 1 && j == ny - 1);
+    if (P->well_pattern == 1) {
+        inj = (i == nx / 2 && j == ny / 2);
+        prod = (i == 0 || i == nx - 1) && (j == 0 || j == ny - 1);
+    }
+    if (P->well_pattern == 2) {                  /* staircase: channel ends, channel cells only */
+        const int ci0 = (int)(0.1875 * nx), cj0 = (int)(0.1875 * ny);
+        inj = (i == (int)(0.5 * nx) && j == cj0);
+        prod = (i == ci0 && j == (int)(0.5 * ny));
+        if (!stair_channel((i + 0.5) / nx, (j + 0.5) / ny, (k + 0.5) / nz)) inj = prod = 0;
+    }
+    if (k < kw0 || k >= kw1) inj = prod = 0;
+    return inj ? 1 : prod ? 2 : 0;
+}
+
+/* ------------------------------------------------------------------ state only */
+/* The per-cell fields (E, perm, phi, sat) and linearisation pressure of synth_generate, and x_rand, without
+ * assembling the Jacobian: the input of a GPU assembly.  Same streams, same values. */
+static void state_pressure(const synth_params *P, double *pres)
+{
+    const int nx = P->nx, ny = P->ny, nz = P->nz;
+    const int64_t Nc = (int64_t)nx * ny * nz;
+    const double h = (P->length > 0 ? P->length : 1.0) / nx, g = P->gravity, ztop = nz * h;
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < Nc; ++c) {
+        int64_t k = c / ((int64_t)nx * ny);
+        double zc = (k + 0.5) * h;
+        int64_t ci = c % nx, cj = (c / nx) % ny;
+        double xy = ((ci + 0.5) + (cj + 0.5)) / (double)(nx + ny);
+        pres[c] = P->p0 + P->rho_w0 * g * (ztop - zc) + P->state_dp * (1.0 - 2.0 * xy);
+    }
+}
+static void draw_x_rand(const synth_params *P, double *x, int64_t n)
+{
+    uint64_t st = stream_seed(P->seed, 0);
+    for (int64_t q = 0; q < n; ++q) x[q] = -1.0 + 2.0 * unif(&st);
+}
+int synth_fields(const synth_params *P, double *E, double *perm, double *phi, double *sat, double *pres, double *x_rand,
+                 int8_t *well)
+{
+    if (P->nx < 1 || P->ny < 1 || P->nz < 1) return -1;
+    int64_t sz[8]; synth_sizes(P, sz);
+    make_fields(P, E, perm, phi, sat);
+    state_pressure(P, pres);
+    if (well)
+        for (int64_t c = 0; c < sz[1]; ++c)
+            well[c] = (int8_t)(P->wells ? well_type(P, (int)(c % P->nx), (int)((c / P->nx) % P->ny), (int)(c / ((int64_t)P->nx * P->ny))) : 0);
+    if (x_rand) draw_x_rand(P, x_rand, sz[6]);
+    return 0;
+}
+
 /* ------------------------------------------------------------------ generator */
 int synth_generate(const synth_params *P, synth_out *O)
 {
@@ -299,17 +355,14 @@ int synth_generate(const synth_params *P, synth_out *O)
     double *E = O->E, *perm = O->perm, *phi = O->phi, *sat = O->sat, *pres = O->pres;
     make_fields(P, E, perm, phi, sat);
 
+    /* linearisation state (DESIGN.md R-state): hydrostatic + a linear injector->producer drawdown of
+       +-state_dp along the (x+y) diagonal, so every face carries flow and SPU upwinding is exercised */
+    state_pressure(P, pres);
     cell_t *C = (cell_t *)malloc(sizeof(cell_t) * Nc);
 #pragma omp parallel for schedule(static)
     for (int64_t c = 0; c < Nc; ++c) {
         int64_t k = c / ((int64_t)nx * ny);
         double zc = (k + 0.5) * h;
-        /* linearisation state (DESIGN.md R-state): hydrostatic + a linear injector->producer
-           drawdown of +-state_dp along the (x+y) diagonal, so every face carries flow and
-           SPU upwinding is exercised */
-        int64_t ci = c % nx, cj = (c / nx) % ny;
-        double xy = ((ci + 0.5) + (cj + 0.5)) / (double)(nx + ny);
-        pres[c] = P->p0 + P->rho_w0 * g * (ztop - zc) + P->state_dp * (1.0 - 2.0 * xy);
         cell_state(P, E[c], phi[c], sat[c], pres[c], zc, &C[c]);
     }
     q1_t Q; q1_integrals(h, &Q);
@@ -408,7 +461,7 @@ int synth_generate(const synth_params *P, synth_out *O)
     /* well geometry (D15): WI of eq:well_index with r_w = rw_over_h * h, s_k = 0 */
     const double rpe = 0.28 * sqrt(h * h + h * h) / 2.0;
     const double lnr = log(rpe / (P->rw_over_h * h));
-    const int kw0 = P->burden > 0 ? P->burden : 0, kw1 = P->burden > 0 ? nz - P->burden : nz;   /* perforated layers */
+    const int kw1 = P->burden > 0 ? nz - P->burden : nz;   /* bottom of the perforated layers */
     const double zbh = (kw1 - 0.5) * h;
     const double pbh_ref = P->p0 + P->rho_w0 * g * (ztop - zbh);
 #pragma omp parallel for schedule(static)
@@ -481,18 +534,8 @@ int synth_generate(const synth_params *P, synth_out *O)
         }
         /* wells (eq:peaceman, eq:peaceman2; derivatives P:1042-1095; residual sign P:941) */
         if (P->wells) {
-            int inj = (i == 0 && j == 0), prod = (i == nx - 1 && j == ny - 1);
-            if (P->well_pattern == 1) {
-                inj = (i == nx / 2 && j == ny / 2);
-                prod = (i == 0 || i == nx - 1) && (j == 0 || j == ny - 1);
-            }
-            if (P->well_pattern == 2) {                  /* staircase: channel ends, channel cells only */
-                const int ci0 = (int)(0.1875 * nx), cj0 = (int)(0.1875 * ny);
-                inj = (i == (int)(0.5 * nx) && j == cj0);
-                prod = (i == ci0 && j == (int)(0.5 * ny));
-                if (!stair_channel((i + 0.5) / nx, (j + 0.5) / ny, (k + 0.5) / nz)) inj = prod = 0;
-            }
-            if (k < kw0 || k >= kw1) inj = prod = 0;
+            const int wt = well_type(P, i, j, k);
+            const int inj = wt == 1, prod = wt == 2;
             if (inj || prod) {
                 double WI = 2 * M_PI * h * perm[c] / lnr;
                 double pbh = pbh_ref + (inj ? P->well_dbhp : -P->well_dbhp);
@@ -601,9 +644,7 @@ int synth_generate(const synth_params *P, synth_out *O)
     }
 
     /* ---------------- x_rand (seed stream 0) and b = A x_rand */
-    const int64_t n = sz[6];
-    uint64_t st = stream_seed(P->seed, 0);
-    for (int64_t q = 0; q < n; ++q) O->x_rand[q] = -1.0 + 2.0 * unif(&st);
+    draw_x_rand(P, O->x_rand, sz[6]);
     const double *xu = O->x_rand, *xf = O->x_rand + 3 * Nn;
 #pragma omp parallel for schedule(static)
     for (int64_t r = 0; r < Nn; ++r) {
