@@ -153,7 +153,10 @@ class Oracle:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().orc_destroy(self.h)
+            try:
+                lib().orc_destroy(self.h)
+            except TypeError:       # interpreter shutdown: the module globals are already gone
+                pass
             self.h = None
 
     def setup(self):
