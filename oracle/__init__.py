@@ -40,6 +40,14 @@ class Opts(C.Structure):
                 ("amg_cheb_lower", C.c_double)]
 
 
+class Phys(C.Structure):
+    _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("length", C.c_double), ("nu", C.c_double),
+                ("biot", C.c_double), ("gravity", C.c_double), ("rho_w0", C.c_double), ("rho_nw0", C.c_double),
+                ("c_w", C.c_double), ("c_nw", C.c_double), ("mu_w", C.c_double), ("mu_nw", C.c_double),
+                ("rho_s", C.c_double), ("p0", C.c_double), ("swr", C.c_double), ("snwr", C.c_double),
+                ("well_dbhp", C.c_double), ("rw_over_h", C.c_double), ("burden", C.c_int), ("dirichlet_bottom", C.c_int)]
+
+
 class Info(C.Structure):
     _fields_ = [("iterations", C.c_int), ("restarts", C.c_int), ("status", C.c_int),
                 ("est_relres", C.c_double), ("true_relres", C.c_double),
@@ -70,6 +78,9 @@ def lib():
         L.orc_level_export.argtypes = [C.c_void_p, C.c_int, C.c_int, _I32, _I32, _F64, _I32, _I32, _I32, _F64, _F64]
         L.orc_counters.argtypes = [C.c_void_p, _P(C.c_int64)]
         L.orc_cheb_smooth.argtypes = [C.c_int, _I32, _I32, _F64, C.c_int, C.c_double, _F64, _F64, _F64]
+        L.orc_residual.argtypes = [_P(Phys), C.c_double, _F64, _F64, _F64, _F64, _P(C.c_int8), _F64, _F64, _F64]
+        L.orc_masses.argtypes = [_P(Phys), _F64, _F64, _F64, _F64, _F64]
+        L.orc_porosity.argtypes = [_P(Phys), _F64, _F64, _F64, _F64, _F64]
         L.orc_get_spp.argtypes = [C.c_void_p, _F64, _I32, _I32, _F64]
         L.orc_get_cpr.argtypes = [C.c_void_p, _F64, _F64, _F64]
         L.orc_mis2.argtypes = [C.c_int, _I32, _I32, _U32, C.c_int, _I32, _P(C.c_int)]
@@ -280,6 +291,44 @@ def fmix32(x):
     x = (x * 0xC2B2AE35) & 0xFFFFFFFF
     x ^= x >> 16
     return x.astype(np.uint32)
+
+
+def phys(params):
+    """orc_phys from a synth parameter dict (synth.params_of)."""
+    return Phys(**{k: params[k] for k, _ in Phys._fields_})
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, np.float64)
+
+
+def residual(params, fields, x, mprev, dt):
+    """r(x) of Appendix B.1 (raw units; x = [u | (s, p [Pa])]); fields: E, perm, phi0, pref, well."""
+    P = phys(params)
+    keep = [_f64(fields[k]) for k in ("E", "perm", "phi0", "pref")] + [_f64(x), _f64(mprev)]
+    w = np.ascontiguousarray(fields["well"], np.int8) if fields.get("well") is not None else None
+    R = np.empty(len(x))
+    rc = lib().orc_residual(C.byref(P), float(dt), *(_p(a) for a in keep[:4]),
+                            w.ctypes.data_as(_P(C.c_int8)) if w is not None else None, _p(keep[4]), _p(keep[5]), _p(R))
+    if rc:
+        raise ValueError("orc_residual failed")
+    return R
+
+
+def masses(params, fields, x):
+    P = phys(params)
+    keep = [_f64(fields[k]) for k in ("E", "phi0", "pref")] + [_f64(x)]
+    m = np.empty(2 * params["nx"] * params["ny"] * params["nz"])
+    lib().orc_masses(C.byref(P), *(_p(a) for a in keep), _p(m))
+    return m
+
+
+def porosity(params, fields, x):
+    P = phys(params)
+    keep = [_f64(fields[k]) for k in ("E", "phi0", "pref")] + [_f64(x)]
+    phi = np.empty(params["nx"] * params["ny"] * params["nz"])
+    lib().orc_porosity(C.byref(P), *(_p(a) for a in keep), _p(phi))
+    return phi
 
 
 def cheb_smooth(rp, ci, v, b, x0=None, degree=2, lower=0.3):

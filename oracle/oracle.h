@@ -105,4 +105,17 @@ void orc_bgs_apply(void *bgs, const double *w, double *dz);     /* one hbgs swee
 /* R-cheb: `degree` Chebyshev steps on D_l1^-1 A (scalar CSR, the oracle's l1 rule) from x0 (NULL = 0) */
 int orc_cheb_smooth(int n, const int32_t *rp, const int32_t *ci, const double *v, int degree, double lower,
                     const double *b, const double *x0, double *x);
+/* ---- residual.c: the nonlinear residual of Appendix B.1 (raw units, p in Pa) ---- */
+typedef struct {
+    int nx, ny, nz;
+    double length, nu, biot, gravity;
+    double rho_w0, rho_nw0, c_w, c_nw, mu_w, mu_nw, rho_s, p0, swr, snwr;
+    double well_dbhp, rw_over_h;
+    int burden, dirichlet_bottom;
+} orc_phys;
+/* R = r(x) with x = [u node-major | (s, p [Pa]) per cell]; mprev = (V m_w, V m_nw) per cell of the previous step */
+int orc_residual(const orc_phys *P, double dt, const double *E, const double *perm, const double *phi0, const double *pref,
+                 const int8_t *well, const double *x, const double *mprev, double *R);
+void orc_masses(const orc_phys *P, const double *E, const double *phi0, const double *pref, const double *x, double *m);
+void orc_porosity(const orc_phys *P, const double *E, const double *phi0, const double *pref, const double *x, double *phi);
 #endif

@@ -68,6 +68,8 @@ def _lib():
         _LIB.synth_generate.restype = C.c_int
         _LIB.synth_fields.argtypes = [_P(Params)] + [_F64] * 6 + [_P(C.c_int8)]
         _LIB.synth_fields.restype = C.c_int
+        _LIB.synth_assemble_state.argtypes = [_P(Params)] + [_F64] * 6 + [_P(Out)]
+        _LIB.synth_assemble_state.restype = C.c_int
     return _LIB
 
 
@@ -205,6 +207,36 @@ def fields(config: str | None = None, x_rand: bool = True, **overrides) -> dict:
     f["x_rand"] = xr
     f["params"] = kw
     return f
+
+
+def assemble_state(params: dict, E, perm, phi, sat, pres, phi0=None) -> Problem:
+    """The Jacobian blocks at a given state (synth_assemble_state: the CPU assembler at arbitrary fields; phi the
+    porosity at the state, phi0 the reference porosity of eq:linearized_porosity, pres in Pa).  x_rand and b are
+    not produced (zeros)."""
+    p = Params(**{k: v for k, v in params.items() if k in dict(Params._fields_)})
+    s = sizes(p.nx, p.ny, p.nz)
+    Nn, Nc = s["Nn"], s["Nc"]
+    a = dict(
+        uu_rowptr=np.empty(Nn + 1, np.int32), uu_col=np.empty(s["Buu"], np.int32), uu_val=np.empty((s["Buu"], 3, 3)),
+        uf_rowptr=np.empty(Nn + 1, np.int32), uf_col=np.empty(s["Buf"], np.int32), uf_val=np.empty((s["Buf"], 3, 2)),
+        fu_rowptr=np.empty(Nc + 1, np.int32), fu_col=np.empty(s["Bfu"], np.int32), fu_val=np.empty((s["Bfu"], 2, 3)),
+        ff_rowptr=np.empty(Nc + 1, np.int32), ff_col=np.empty(s["Bff"], np.int32), ff_val=np.empty((s["Bff"], 2, 2)),
+        fs=np.empty((Nc, 2)), x_rand=np.zeros(s["n"]), b=np.zeros(s["n"]),
+    )
+    f = {k: np.ascontiguousarray(v, np.float64) for k, v in dict(E=E, perm=perm, phi=phi, sat=sat, pres=pres).items()}
+    f0 = np.ascontiguousarray(phi0, np.float64) if phi0 is not None else None
+    scales = np.empty(3)
+
+    def ptr(x):
+        return x.ctypes.data_as(_I32 if x.dtype == np.int32 else _F64)
+
+    o = Out(**{k: ptr(v) for k, v in a.items()}, **{k: ptr(np.empty(Nc)) for k in ("E", "perm", "phi", "sat", "pres")},
+            scales=ptr(scales))
+    rc = _lib().synth_assemble_state(C.byref(p), *(ptr(f[k]) for k in ("E", "perm", "phi")),
+                                     ptr(f0) if f0 is not None else None, ptr(f["sat"]), ptr(f["pres"]), C.byref(o))
+    if rc != 0:
+        raise ValueError(f"synth_assemble_state failed ({rc})")
+    return Problem(nx=p.nx, ny=p.ny, nz=p.nz, params=dict(params), fields=f, scales=scales, **a)
 
 
 def to_scipy(pb: Problem):

@@ -260,7 +260,8 @@ typedef struct {
     double drho_deps, drho_ds, drho_dp, dphi_dp, dphi_deps;
 } cell_t;
 
-static void cell_state(const synth_params *P, double E, double phi, double s, double p, double z, cell_t *C)
+/* phi: porosity at the state; phi0: the reference porosity of eq:linearized_porosity (its compressibility term) */
+static void cell_state(const synth_params *P, double E, double phi, double phi0, double s, double p, double z, cell_t *C)
 {
     double nu = P->nu, b = P->biot;
     C->lam = E * nu / ((1 + nu) * (1 - 2 * nu));
@@ -278,7 +279,7 @@ static void cell_state(const synth_params *P, double E, double phi, double s, do
     C->krw = sh * sh; C->dkrw = 2 * sh * dsh;
     C->krnw = (1 - sh) * (1 - sh); C->dkrnw = -2 * (1 - sh) * dsh;
     C->dphi_deps = b;                                   /* eq:linearized_porosity */
-    C->dphi_dp = (b - phi) * (1 - b) / C->Kdr;
+    C->dphi_dp = (b - phi0) * (1 - b) / C->Kdr;
     double bracket = -P->rho_s + s * C->rw + (1 - s) * C->rnw;
     C->drho_deps = bracket * C->dphi_deps;
     C->drho_ds = phi * (C->rw - C->rnw);
@@ -342,28 +343,22 @@ int synth_fields(const synth_params *P, double *E, double *perm, double *phi, do
 }
 
 /* ------------------------------------------------------------------ generator */
-int synth_generate(const synth_params *P, synth_out *O)
+/* the Jacobian blocks at the state given by the cell fields (phi0 = NULL: phi is also the reference porosity) */
+static void assemble_at(const synth_params *P, const double *E, const double *perm, const double *phi, const double *phi0,
+                        const double *sat, const double *pres, synth_out *O)
 {
     const int nx = P->nx, ny = P->ny, nz = P->nz;
-    if (nx < 1 || ny < 1 || nz < 1) return -1;
     int64_t sz[8]; synth_sizes(P, sz);
     const int64_t Nn = sz[0], Nc = sz[1];
     const int NX = nx + 1, NY = ny + 1;
     const double h = (P->length > 0 ? P->length : 1.0) / nx, V = h * h * h, g = P->gravity, b = P->biot, dt = P->dt;
     const double ztop = nz * h;
-
-    double *E = O->E, *perm = O->perm, *phi = O->phi, *sat = O->sat, *pres = O->pres;
-    make_fields(P, E, perm, phi, sat);
-
-    /* linearisation state (DESIGN.md R-state): hydrostatic + a linear injector->producer drawdown of
-       +-state_dp along the (x+y) diagonal, so every face carries flow and SPU upwinding is exercised */
-    state_pressure(P, pres);
     cell_t *C = (cell_t *)malloc(sizeof(cell_t) * Nc);
 #pragma omp parallel for schedule(static)
     for (int64_t c = 0; c < Nc; ++c) {
         int64_t k = c / ((int64_t)nx * ny);
         double zc = (k + 0.5) * h;
-        cell_state(P, E[c], phi[c], sat[c], pres[c], zc, &C[c]);
+        cell_state(P, E[c], phi[c], phi0 ? phi0[c] : phi[c], sat[c], pres[c], zc, &C[c]);
     }
     q1_t Q; q1_integrals(h, &Q);
 
@@ -643,6 +638,20 @@ int synth_generate(const synth_params *P, synth_out *O)
             if (O->fu_col[q] < nbot) memset(&O->fu_val[6 * q], 0, 6 * sizeof(double));
     }
 
+    free(C);
+}
+
+int synth_generate(const synth_params *P, synth_out *O)
+{
+    if (P->nx < 1 || P->ny < 1 || P->nz < 1) return -1;
+    int64_t sz[8]; synth_sizes(P, sz);
+    const int64_t Nn = sz[0], Nc = sz[1];
+    make_fields(P, O->E, O->perm, O->phi, O->sat);
+    /* linearisation state (DESIGN.md R-state): hydrostatic + a linear injector->producer drawdown of
+       +-state_dp along the (x+y) diagonal, so every face carries flow and SPU upwinding is exercised */
+    state_pressure(P, O->pres);
+    assemble_at(P, O->E, O->perm, O->phi, NULL, O->sat, O->pres, O);
+
     /* ---------------- x_rand (seed stream 0) and b = A x_rand */
     draw_x_rand(P, O->x_rand, sz[6]);
     const double *xu = O->x_rand, *xf = O->x_rand + 3 * Nn;
@@ -664,6 +673,17 @@ int synth_generate(const synth_params *P, synth_out *O)
             for (int d = 0; d < 2; ++d) for (int e = 0; e < 2; ++e) y[d] += O->ff_val[4 * q + 2 * d + e] * xf[2 * (int64_t)O->ff_col[q] + e];
         O->b[3 * Nn + 2 * r] = y[0]; O->b[3 * Nn + 2 * r + 1] = y[1];
     }
-    free(C);
+    (void)Nc;
+    return 0;
+}
+
+/* the Jacobian at a given state (the CPU reference of the GPU assembly inside a Newton loop):
+ * fields E, perm, phi (porosity at the state), phi0 (reference porosity, NULL = phi), sat, pres (Pa); the
+ * generator's fields, x_rand and b of `O` are not touched */
+int synth_assemble_state(const synth_params *P, const double *E, const double *perm, const double *phi, const double *phi0,
+                         const double *sat, const double *pres, synth_out *O)
+{
+    if (P->nx < 1 || P->ny < 1 || P->nz < 1) return -1;
+    assemble_at(P, E, perm, phi, phi0, sat, pres, O);
     return 0;
 }
