@@ -269,10 +269,13 @@ typedef struct {
 
 /* per-cell fields of the GLOBAL grid (device pointers, N_c entries each, cell (i,j,k) = i + nx (j + ny k)):
  * Young's modulus (Pa), permeability (m^2), porosity, water saturation, pressure (Pa) at the linearisation state,
- * and the well perforation of the cell (0 none, 1 water injector, 2 producer; NULL = no wells) */
+ * the well perforation of the cell (0 none, 1 water injector, 2 producer; NULL = no wells), and the reference
+ * porosity phi_0 of eq:linearized_porosity whose compressibility term (b - phi_0)(1 - b)/K_dr enters the
+ * p-derivatives (NULL = phi: the state is the reference state) */
 typedef struct {
     const double *E, *perm, *phi, *sat, *pres;
     const int8_t *well;
+    const double *phi0;
 } tsp_cell_fields;
 
 /* a device BSR block the assembly writes (rowptr: rows + 1, col / val: sizes from tsp_assembly_sizes) */
@@ -294,6 +297,43 @@ tsp_status tsp_assemble(const tsp_asm_params *p, int rank, int nranks, int zbloc
                         tsp_bsr_out blocks[4], double *fs, double row_max[3], void *stream);
 tsp_status tsp_assemble_scale(const tsp_asm_params *p, int rank, int nranks, int zblock, const double row_max[3],
                               tsp_bsr_out blocks[4], double *fs, double scales[3], void *stream);
+
+/* ---- the nonlinear step: residual of Appendix B.1 and Newton ----------------------
+ * State x (device, n = 3 N_n + 2 N_c): [u node-major (m) | (s, p [Pa]) per cell] -- raw pressure, unlike the
+ * linear system's unknown p / p_unit.  `ref` fields: E, perm, well as for tsp_assemble, phi = the REFERENCE
+ * porosity phi_0 and pres = the reference pressure p_ref of eq:linearized_porosity (phi = phi_0 + b eps_v +
+ * (b - phi_0)(1 - b)/K_dr (p - p_ref), eps_v averaged over the cell); sat is not read.  Single GPU. */
+/* r = r(x) in raw units (N for momentum rows, kg for mass rows); mprev: (V m_w, V m_nw) per cell of the previous
+ * step (tsp_masses); Dirichlet rows 0.  Synchronises `stream`. */
+tsp_status tsp_residual(const tsp_asm_params *p, const tsp_cell_fields *ref, double dt, const double *x, const double *mprev,
+                        double *r, void *stream);
+tsp_status tsp_masses(const tsp_asm_params *p, const tsp_cell_fields *ref, const double *x, double *m, void *stream);
+
+typedef struct {
+    double rtol;                 /* converged when ||S0 r|| <= rtol ||S0 r_0|| (S0: the step's first row scales), 1e-6 */
+    double atol;                 /* or ||S0 r|| <= atol, default 0 */
+    int max_newton;              /* 12 */
+    double lin_rtol;             /* FGMRES tolerance of every Newton system, 1e-8 */
+    int max_lin_iters;           /* 1000 */
+    int refresh;                 /* 1: per-Newton flow setup with frozen pressure aggregation (TSP_SETUP_REFRESH) */
+    int max_halvings;            /* backtracking line search: alpha halved at most this often, 5 */
+} tsp_newton_opts;
+typedef struct {
+    int newton_iters, lin_iters, halvings, status;   /* status 0 converged, 1 not */
+    double res0, res;            /* ||S0 r|| at the start and at exit */
+    double res_hist[16];         /* per Newton iteration */
+    int lin_hist[16];            /* FGMRES iterations per Newton iteration */
+} tsp_newton_info;
+void tsp_default_newton_opts(tsp_newton_opts *o);
+/* One implicit time step (dt) by Newton's method with backtracking line search on the handle `h` (created from a
+ * Jacobian of the same grid, tsp_setup(MECH) done): per iteration the Jacobian is re-assembled at x on the device
+ * (tsp_assemble), pushed into h (tsp_update_values), the flow phase redone (TSP_SETUP_FLOW[|REFRESH]; the mechanics
+ * AMG stays) and J dx = -S r solved by the two-stage preconditioned FGMRES; x += alpha dx with alpha halved
+ * until ||S0 r|| decreases (saturation kept in [0, 1]).  r_off (device, 3 N_n, may be NULL): a momentum residual
+ * subtracted from every evaluation (the initial-state equilibrium, so that u measures the displacement since t0).
+ * x is updated in place.  Returns TSP_OK, TSP_NOT_CONVERGED (info filled) or an error. */
+tsp_status tsp_newton_step(tsp_handle h, const tsp_asm_params *p, const tsp_cell_fields *ref, double dt, double *x,
+                           const double *mprev, const double *r_off, const tsp_newton_opts *o, tsp_newton_info *info);
 
 /* Test hook (row c.5 parity): copy level `lvl` of hierarchy `which` (0 mech, 1
  * pressure) to host buffers.  Sizes: out6 = {n, nnz(A), nagg, nnz(P), nc,

@@ -81,7 +81,7 @@ struct CellSt {
 
 __device__ __forceinline__ CellSt cell_st(const tsp_asm_params &P, const AsmGeo &g, int64_t c, const double *__restrict__ E,
                                           const double *__restrict__ phi, const double *__restrict__ sat,
-                                          const double *__restrict__ pres)
+                                          const double *__restrict__ pres, const double *__restrict__ phi0 = nullptr)
 {
     CellSt C;
     const double nu = P.nu, b = P.biot, e = E[c];
@@ -100,7 +100,7 @@ __device__ __forceinline__ CellSt cell_st(const tsp_asm_params &P, const AsmGeo 
     if (se >= 1) { se = 1; dse = 0; }
     C.krw = se * se; C.dkrw = 2 * se * dse;                  // Corey n = 2
     C.krn = (1 - se) * (1 - se); C.dkrn = -2 * (1 - se) * dse;
-    C.dphi_dp = (b - C.phi) * (1 - b) / C.Kdr;               // eq:linearized_porosity; d phi / d eps_v = b
+    C.dphi_dp = (b - (phi0 ? phi0[c] : C.phi)) * (1 - b) / C.Kdr;   // eq:linearized_porosity; d phi / d eps_v = b
     const double bracket = -P.rho_s + C.s * C.rw + (1 - C.s) * C.rn;
     C.drho_de = bracket * b;
     C.drho_ds = C.phi * (C.rw - C.rn);
@@ -131,6 +131,7 @@ __global__ void k_asm_counts(AsmGeo g, int32_t *cuu, int32_t *cuf, int32_t *cff)
 __global__ void __launch_bounds__(128) k_asm_node(tsp_asm_params P, AsmGeo g, const Q1 *__restrict__ q,
                                                   const double *__restrict__ E, const double *__restrict__ phi,
                                                   const double *__restrict__ sat, const double *__restrict__ pres,
+                                                  const double *__restrict__ phi0,
                                                   const int32_t *__restrict__ rpu, int32_t *__restrict__ cu, double *__restrict__ vu,
                                                   const int32_t *__restrict__ rpf, int32_t *__restrict__ cf, double *__restrict__ vf)
 {
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(128) k_asm_node(tsp_asm_params P, AsmGeo g, co
         if (ci < 0 || ci >= g.nx || cj < 0 || cj >= g.ny || ck < 0 || ck >= g.nz) continue;
         const int64_t c = ci + (int64_t)g.nx * (cj + (int64_t)g.ny * ck);
         cf[qf] = (int32_t)c;
-        const CellSt C = cell_st(P, g, c, E, phi, sat, pres);
+        const CellSt C = cell_st(P, g, c, E, phi, sat, pres, phi0);
         const int a = (1 - (o & 1)) + 2 * (1 - ((o >> 1) & 1)) + 4 * (1 - ((o >> 2) & 1));   // node n inside element c
         for (int bl = 0; bl < 8; ++bl) {
             // node m = corner bl of element c; its offset from n picks the block
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(128) k_asm_cell(tsp_asm_params P, AsmGeo g, co
                                                   const double *__restrict__ E, const double *__restrict__ perm,
                                                   const double *__restrict__ phi, const double *__restrict__ sat,
                                                   const double *__restrict__ pres, const int8_t *__restrict__ well,
-                                                  int32_t *__restrict__ cfu, double *__restrict__ vfu,
+                                                  const double *__restrict__ phi0, int32_t *__restrict__ cfu, double *__restrict__ vfu,
                                                   const int32_t *__restrict__ rpf, int32_t *__restrict__ cff, double *__restrict__ vff,
                                                   double *__restrict__ fs)
 {
@@ -196,7 +197,7 @@ __global__ void __launch_bounds__(128) k_asm_cell(tsp_asm_params P, AsmGeo g, co
     const int64_t c = g.cell0 + t, P2 = (int64_t)g.nx * g.ny;
     const int i = c % g.nx, j = (c / g.nx) % g.ny, k = c / P2;
     const double h = g.h, V = h * h * h, gr = P.gravity, b = P.biot, dt = P.dt, pu = P.p_unit;
-    const CellSt K = cell_st(P, g, c, E, phi, sat, pres);
+    const CellSt K = cell_st(P, g, c, E, phi, sat, pres, phi0);
     // A_fu: the 8 corner nodes of the cell
     for (int a = 0; a < 8; ++a) {
         const int64_t qq = 8 * (int64_t)t + a;
@@ -234,8 +235,8 @@ __global__ void __launch_bounds__(128) k_asm_cell(tsp_asm_params P, AsmGeo g, co
         const int64_t o = nb[u];
         if (o == c) continue;
         const int64_t cK = c < o ? c : o, cL = c < o ? o : c;
-        const CellSt A = (cK == c) ? K : cell_st(P, g, cK, E, phi, sat, pres);
-        const CellSt B = (cL == c) ? K : cell_st(P, g, cL, E, phi, sat, pres);
+        const CellSt A = (cK == c) ? K : cell_st(P, g, cK, E, phi, sat, pres, phi0);
+        const CellSt B = (cL == c) ? K : cell_st(P, g, cL, E, phi, sat, pres, phi0);
         const double tK = h * h * perm[cK] * (h / 2) / ((h / 2) * (h / 2));     // eq:half_trans
         const double tL = h * h * perm[cL] * (h / 2) / ((h / 2) * (h / 2));
         const double T = (tK + tL) > 0 ? tK * tL / (tK + tL) : 0.0;           // eq:trans
@@ -357,6 +358,217 @@ __global__ void k_asm_scale_cells(AsmGeo g, double ss, double sp, int dirichlet,
     fs[2 * t] *= ss; fs[2 * t + 1] *= sp;
 }
 
+// ---------------------------------------------------------------- residual of Appendix B.1, raw units
+// x = [u node-major | (s, p [Pa]) per cell]; porosity phi = phi_0 + b eps_v + (b - phi_0)(1 - b)/K_dr (p - p_ref)
+// with eps_v the cell average (eq:linearized_porosity); the gravity term integrates the mixture density pointwise
+// (its porosity carries the Gauss point's eps_v).  Its CPU reference is residual.c of the test oracle.
+struct ResSt {
+    double lam, mu, Kdr, s, p, z, phi, phi_e0, rw, rn, krw, krn;
+};
+__device__ __forceinline__ int64_t cell_node(const AsmGeo &g, int64_t c, int a)
+{
+    const int64_t NX = g.nx + 1, NY = g.ny + 1;
+    const int64_t i = c % g.nx, j = (c / g.nx) % g.ny, k = c / ((int64_t)g.nx * g.ny);
+    return (i + (a & 1)) + NX * ((j + ((a >> 1) & 1)) + NY * (k + ((a >> 2) & 1)));
+}
+__device__ ResSt res_st(const tsp_asm_params &P, const AsmGeo &g, const Q1 *__restrict__ q, int64_t c, const double *__restrict__ E,
+                        const double *__restrict__ phi0, const double *__restrict__ pref, const double *__restrict__ x,
+                        int64_t Nn, bool strain)
+{
+    ResSt C;
+    const double nu = P.nu, b = P.biot, V = g.h * g.h * g.h;
+    C.lam = E[c] * nu / ((1 + nu) * (1 - 2 * nu));
+    C.mu = E[c] / (2 * (1 + nu));
+    C.Kdr = E[c] / (3 * (1 - 2 * nu));
+    C.s = x[3 * Nn + 2 * c];
+    C.p = x[3 * Nn + 2 * c + 1];
+    C.z = (c / ((int64_t)g.nx * g.ny) + 0.5) * g.h;
+    double ev = 0.0;
+    if (strain)
+        for (int a = 0; a < 8; ++a) {
+            const int64_t n = cell_node(g, c, a);
+            for (int d = 0; d < 3; ++d) ev += q->DN[a][d] * x[3 * n + d];
+        }
+    C.phi_e0 = phi0[c] + (b - phi0[c]) * (1 - b) / C.Kdr * (C.p - pref[c]);
+    C.phi = C.phi_e0 + b * ev / V;
+    C.rw = P.rho_w0 * (1 + P.c_w * (C.p - P.p0));
+    C.rn = P.rho_nw0 * (1 + P.c_nw * (C.p - P.p0));
+    const double span = 1.0 - P.swr - P.snwr;
+    double se = (C.s - P.swr) / span;
+    se = se < 0 ? 0 : se > 1 ? 1 : se;
+    C.krw = se * se;
+    C.krn = (1 - se) * (1 - se);
+    return C;
+}
+
+__global__ void __launch_bounds__(128) k_res_node(tsp_asm_params P, AsmGeo g, const Q1 *__restrict__ q, const double *__restrict__ E,
+                                                  const double *__restrict__ phi0, const double *__restrict__ pref,
+                                                  const double *__restrict__ x, int64_t Nn, double *__restrict__ r)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= g.nn) return;
+    const int NX = g.nx + 1, NY = g.ny + 1;
+    const int64_t n = g.node0 + t;
+    const int i = n % NX, j = (n / NX) % NY, k = n / ((int64_t)NX * NY);
+    const double gr = P.gravity, b = P.biot;
+    double R[3] = {0.0, 0.0, 0.0};
+    if (!(P.dirichlet_bottom && n < (int64_t)NX * NY))
+        for (int o = 0; o < 8; ++o) {
+            const int ci = i - 1 + (o & 1), cj = j - 1 + ((o >> 1) & 1), ck = k - 1 + ((o >> 2) & 1);
+            if (ci < 0 || ci >= g.nx || cj < 0 || cj >= g.ny || ck < 0 || ck >= g.nz) continue;
+            const int64_t c = ci + (int64_t)g.nx * (cj + (int64_t)g.ny * ck);
+            const ResSt C = res_st(P, g, q, c, E, phi0, pref, x, Nn, false);
+            const double bracket = -P.rho_s + C.s * C.rw + (1 - C.s) * C.rn;
+            const double rho0 = P.rho_s + C.phi_e0 * bracket;
+            const int a = (1 - (o & 1)) + 2 * (1 - ((o >> 1) & 1)) + 4 * (1 - ((o >> 2) & 1));
+            double u[8][3];
+            for (int bb = 0; bb < 8; ++bb) {
+                const int64_t m = cell_node(g, c, bb);
+                for (int e = 0; e < 3; ++e) u[bb][e] = x[3 * m + e];
+            }
+            for (int d = 0; d < 3; ++d) {
+                double v = 0.0;
+                for (int bb = 0; bb < 8; ++bb) {
+                    const double tr = q->KK[a][bb][0][0] + q->KK[a][bb][1][1] + q->KK[a][bb][2][2];
+                    for (int e = 0; e < 3; ++e) {
+                        double kk = C.lam * q->KK[a][bb][d][e] + C.mu * q->KK[a][bb][e][d];
+                        if (d == e) kk += C.mu * tr;
+                        v += kk * u[bb][e];
+                        if (d == 2) v += gr * bracket * b * q->NB[a][bb][e] * u[bb][e];
+                    }
+                }
+                v -= b * C.p * q->DN[a][d];
+                if (d == 2) v += gr * rho0 * q->NI[a];
+                R[d] += v;
+            }
+        }
+    for (int d = 0; d < 3; ++d) r[3 * (int64_t)t + d] = R[d];
+}
+
+__global__ void __launch_bounds__(128) k_res_cell(tsp_asm_params P, AsmGeo g, const Q1 *__restrict__ q, const double *__restrict__ E,
+                                                  const double *__restrict__ perm, const double *__restrict__ phi0,
+                                                  const double *__restrict__ pref, const int8_t *__restrict__ well,
+                                                  const double *__restrict__ x, int64_t Nn, const double *__restrict__ mprev,
+                                                  double dt, double *__restrict__ r)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= g.ncl) return;
+    const int64_t c = g.cell0 + t, P2 = (int64_t)g.nx * g.ny;
+    const int i = c % g.nx, j = (c / g.nx) % g.ny, k = c / P2;
+    const double h = g.h, V = h * h * h, gr = P.gravity;
+    const ResSt K = res_st(P, g, q, c, E, phi0, pref, x, Nn, true);
+    double rw = V * K.phi * K.rw * K.s - mprev[2 * t];
+    double rn = V * K.phi * K.rn * (1 - K.s) - mprev[2 * t + 1];
+    int64_t nb[6];
+    int np = 0;
+    if (k > 0) nb[np++] = c - P2;
+    if (j > 0) nb[np++] = c - g.nx;
+    if (i > 0) nb[np++] = c - 1;
+    if (i < g.nx - 1) nb[np++] = c + 1;
+    if (j < g.ny - 1) nb[np++] = c + g.nx;
+    if (k < g.nz - 1) nb[np++] = c + P2;
+    for (int u = 0; u < np; ++u) {
+        const int64_t o = nb[u], cK = c < o ? c : o, cL = c < o ? o : c;
+        const ResSt O = res_st(P, g, q, o, E, phi0, pref, x, Nn, false);
+        const ResSt &A = (cK == c) ? K : O, &B = (cL == c) ? K : O;
+        const double tK = h * h * perm[cK] * (h / 2) / ((h / 2) * (h / 2)), tL = h * h * perm[cL] * (h / 2) / ((h / 2) * (h / 2));
+        const double T = (tK + tL) > 0 ? tK * tL / (tK + tL) : 0.0;
+        const double dz = B.z - A.z, sgn = (c == cK) ? -1.0 : 1.0;
+        for (int ph = 0; ph < 2; ++ph) {
+            const double rK = ph ? A.rn : A.rw, rL = ph ? B.rn : B.rw, kK = ph ? A.krn : A.krw, kL = ph ? B.krn : B.krw;
+            const double mu = ph ? P.mu_nw : P.mu_w;
+            const double ravg = (kK > 0 && kL > 0) ? 0.5 * (rK + rL) : kK > 0 ? rK : kL > 0 ? rL : 0.0;
+            const double Phi = T * ((B.p - A.p) + ravg * gr * dz);
+            const bool fromL = Phi > 0;
+            const double F = (fromL ? rL : rK) * (fromL ? kL : kK) / mu * Phi;
+            (ph ? rn : rw) += sgn * dt * F;
+        }
+    }
+    const int wt = well ? well[c] : 0;
+    if (wt) {
+        const int kw1 = P.burden > 0 ? g.nz - P.burden : g.nz;
+        const double zbh = (kw1 - 0.5) * h, ztop = g.nz * h;
+        const double pbh = P.p0 + P.rho_w0 * gr * (ztop - zbh) + (wt == 1 ? P.well_dbhp : -P.well_dbhp);
+        const double re = 0.28 * sqrt(h * h + h * h) / 2.0;
+        const double WI = 2 * M_PI * h * perm[c] / log(re / (P.rw_over_h * h));
+        const double lw = K.krw / P.mu_w, ln = K.krn / P.mu_nw;
+        for (int ph = 0; ph < 2; ++ph) {
+            const double rr = ph ? K.rn : K.rw;
+            const double Phi = WI * ((pbh + rr * gr * zbh) - (K.p + rr * gr * K.z));
+            double src = 0.0;
+            if (wt == 1) { if (ph == 0 && Phi > 0) src = rr * (lw + ln) * Phi; }
+            else if (Phi < 0) src = rr * (ph ? ln : lw) * Phi;
+            (ph ? rn : rw) -= dt * src;
+        }
+    }
+    r[3 * Nn + 2 * (int64_t)t] = rw;
+    r[3 * Nn + 2 * (int64_t)t + 1] = rn;
+}
+
+// current porosity, saturation and pressure of every cell at x (the fields of the Jacobian at the state)
+__global__ void k_state_fields(tsp_asm_params P, AsmGeo g, const Q1 *__restrict__ q, const double *__restrict__ E,
+                               const double *__restrict__ phi0, const double *__restrict__ pref, const double *__restrict__ x,
+                               int64_t Nn, double *__restrict__ phi, double *__restrict__ sat, double *__restrict__ pres)
+{
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= (int64_t)g.nx * g.ny * g.nz) return;
+    const ResSt C = res_st(P, g, q, c, E, phi0, pref, x, Nn, true);
+    phi[c] = C.phi; sat[c] = C.s; pres[c] = C.p;
+}
+__global__ void k_masses(tsp_asm_params P, AsmGeo g, const Q1 *__restrict__ q, const double *__restrict__ E,
+                         const double *__restrict__ phi0, const double *__restrict__ pref, const double *__restrict__ x,
+                         int64_t Nn, double *__restrict__ m)
+{
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= (int64_t)g.nx * g.ny * g.nz) return;
+    const ResSt C = res_st(P, g, q, c, E, phi0, pref, x, Nn, true);
+    const double V = g.h * g.h * g.h;
+    m[2 * c] = V * C.phi * C.rw * C.s;
+    m[2 * c + 1] = V * C.phi * C.rn * (1 - C.s);
+}
+
+static AsmGeo asm_geo(const tsp_asm_params &P, int rank, int nranks, int zblock);
+
+struct Q1Dev {
+    DBuf<Q1> q;
+    explicit Q1Dev(cudaStream_t s, double h)
+    {
+        Q1 t;
+        q1_tables(h, t);
+        q.alloc(1);
+        TSP_CUDA(cudaMemcpyAsync(q.p, &t, sizeof(Q1), cudaMemcpyHostToDevice, s));
+        TSP_CUDA(cudaStreamSynchronize(s));
+    }
+};
+
+void residual(cudaStream_t s, const tsp_asm_params &P, const tsp_cell_fields &ref, double dt, const double *x, const double *mprev,
+              double *r)
+{
+    TSP_REQUIRE(ref.E && ref.perm && ref.phi && ref.pres && x && mprev && r, TSP_ERR_INVALID_ARG, "residual: null pointer");
+    const AsmGeo g = asm_geo(P, 0, 1, 16);
+    Q1Dev q(s, g.h);
+    const int64_t Nn = g.nn;
+    if (g.nn) k_res_node<<<grid_for(g.nn, 128), 128, 0, s>>>(P, g, q.q.p, ref.E, ref.phi, ref.pres, x, Nn, r);
+    if (g.ncl) k_res_cell<<<grid_for(g.ncl, 128), 128, 0, s>>>(P, g, q.q.p, ref.E, ref.perm, ref.phi, ref.pres, ref.well, x, Nn,
+                                                              mprev, dt, r);
+    TSP_CUDA(cudaGetLastError());
+}
+void state_fields(cudaStream_t s, const tsp_asm_params &P, const tsp_cell_fields &ref, const double *x, double *phi, double *sat,
+                  double *pres)
+{
+    const AsmGeo g = asm_geo(P, 0, 1, 16);
+    Q1Dev q(s, g.h);
+    if (g.ncl) k_state_fields<<<grid_for(g.ncl, 128), 128, 0, s>>>(P, g, q.q.p, ref.E, ref.phi, ref.pres, x, g.nn, phi, sat, pres);
+    TSP_CUDA(cudaGetLastError());
+}
+void masses(cudaStream_t s, const tsp_asm_params &P, const tsp_cell_fields &ref, const double *x, double *m)
+{
+    const AsmGeo g = asm_geo(P, 0, 1, 16);
+    Q1Dev q(s, g.h);
+    if (g.ncl) k_masses<<<grid_for(g.ncl, 128), 128, 0, s>>>(P, g, q.q.p, ref.E, ref.phi, ref.pres, x, g.nn, m);
+    TSP_CUDA(cudaGetLastError());
+}
+
 static AsmGeo asm_geo(const tsp_asm_params &P, int rank, int nranks, int zblock)
 {
     int64_t part[6];
@@ -420,9 +632,9 @@ void assemble(cudaStream_t s, const tsp_asm_params &P, int rank, int nranks, int
         TSP_CUDA(cudaMemcpyAsync(blk[2].rowptr, rp.data(), sizeof(int32_t) * (g.ncl + 1), cudaMemcpyHostToDevice, s));
         TSP_CUDA(cudaStreamSynchronize(s));   // rp is a host temporary
     }
-    if (g.nn) k_asm_node<<<grid_for(g.nn, 128), 128, 0, s>>>(P, g, dq.p, f.E, f.phi, f.sat, f.pres, blk[0].rowptr, blk[0].col,
+    if (g.nn) k_asm_node<<<grid_for(g.nn, 128), 128, 0, s>>>(P, g, dq.p, f.E, f.phi, f.sat, f.pres, f.phi0, blk[0].rowptr, blk[0].col,
                                                             blk[0].val, blk[1].rowptr, blk[1].col, blk[1].val);
-    if (g.ncl) k_asm_cell<<<grid_for(g.ncl, 128), 128, 0, s>>>(P, g, dq.p, f.E, f.perm, f.phi, f.sat, f.pres, f.well, blk[2].col,
+    if (g.ncl) k_asm_cell<<<grid_for(g.ncl, 128), 128, 0, s>>>(P, g, dq.p, f.E, f.perm, f.phi, f.sat, f.pres, f.well, f.phi0, blk[2].col,
                                                               blk[2].val, blk[3].rowptr, blk[3].col, blk[3].val, fs);
     DBuf<unsigned long long> mx; mx.alloc(3); mx.zero(s);
     if (m) k_asm_rowmax<<<grid_for(m, 256), 256, 0, s>>>(g, blk[0].rowptr, blk[0].val, blk[3].rowptr, blk[3].val, mx);

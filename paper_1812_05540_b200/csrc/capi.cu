@@ -103,21 +103,19 @@ void dbg_alloc(double t0, size_t bytes)
     if (dt > 2e-3) fprintf(stderr, "[tsp alloc] %.1f MB took %.1f ms\n", bytes / 1e6, dt * 1e3);
 }
 
-// bind the allocation stream of this API call; keep the default pool resident
-struct StreamScope {
-    ~StreamScope() { g_alloc_state = nullptr; }
-    explicit StreamScope(cudaStream_t s, AllocState *as = nullptr) {
-        g_alloc_stream = s;
-        g_alloc_state = as;
-        // per call (idempotent, thread-safe, ~1 us): the pool belongs to the current device
-        int dev = 0;
-        cudaMemPool_t pool;
-        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
+StreamScope::StreamScope(cudaStream_t s, AllocState *as) : prev_stream(g_alloc_stream), prev_state(g_alloc_state)
+{
+    g_alloc_stream = s;
+    g_alloc_state = as;
+    // per call (idempotent, thread-safe, ~1 us): the pool belongs to the current device
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-};
+}
+StreamScope::~StreamScope() { g_alloc_stream = prev_stream; g_alloc_state = prev_state; }
 
 void *scratch(Ctx &c, size_t bytes)
 {
@@ -168,7 +166,6 @@ void prof_end(Ctx &c, int cls, double bytes)
 
 using namespace tsp;
 
-struct tsp_ctx : Ctx {};
 
 #define API_BEGIN try { StreamScope ss_(h ? h->s : (cudaStream_t)0, h ? &h->alloc : nullptr);
 #define API_END                                                                                     \
@@ -192,7 +189,7 @@ struct tsp_ctx : Ctx {};
     return TSP_OK;
 
 // status of the exception in flight (inside a catch block): every exception is mapped, none escapes extern "C"
-static tsp_status status_of_current_exception()
+tsp_status tsp::status_of_current_exception()
 {
     try { throw; }
     catch (const tsp::Error &e) { set_error(e.msg); return e.st; }

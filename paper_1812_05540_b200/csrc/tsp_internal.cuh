@@ -44,6 +44,14 @@ struct AllocState {
 };
 extern thread_local cudaStream_t g_alloc_stream;
 extern thread_local AllocState *g_alloc_state;  // the handle whose API call is in progress on this thread
+// binds the allocation stream / allocator of an API call (restores the enclosing call's on exit: API calls nest)
+struct StreamScope {
+    cudaStream_t prev_stream;
+    AllocState *prev_state;
+    explicit StreamScope(cudaStream_t s, AllocState *as = nullptr);
+    ~StreamScope();
+};
+tsp_status status_of_current_exception();        // inside a catch block: the tsp_status of the exception
 double dbg_now();                              // TSP_DEBUG: wall clock (0 when off)
 void dbg_alloc(double t0, size_t bytes);       // TSP_DEBUG: report slow allocations
 void *dev_alloc(size_t bytes, cudaStream_t s, AllocState *as);
@@ -383,6 +391,13 @@ void assemble(cudaStream_t s, const tsp_asm_params &P, int rank, int nranks, int
 void assemble_scale(cudaStream_t s, const tsp_asm_params &P, int rank, int nranks, int zblock, const double row_max[3],
                     tsp_bsr_out blk[4], double *fs, double scales[3]);
 
+// Appendix B.1 residual, state fields and masses at x (single rank; ref: E, perm, phi = phi_0, pres = p_ref, well)
+void residual(cudaStream_t s, const tsp_asm_params &P, const tsp_cell_fields &ref, double dt, const double *x, const double *mprev,
+              double *r);
+void state_fields(cudaStream_t s, const tsp_asm_params &P, const tsp_cell_fields &ref, const double *x, double *phi, double *sat,
+                  double *pres);
+void masses(cudaStream_t s, const tsp_asm_params &P, const tsp_cell_fields &ref, const double *x, double *m);
+
 // partition of the z-slab decomposition (include/tsp.h)
 void partition(int nx, int ny, int nz, int zblock, int rank, int nranks, int64_t out6[6]);
 void reduce_setup(Ctx &c);
@@ -392,3 +407,6 @@ void krylov_graphs_drop(Ctx &c);
 void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, tsp_solve_info &info);
 
 }  // namespace tsp
+
+// the opaque handle of include/tsp.h
+struct tsp_ctx : tsp::Ctx {};

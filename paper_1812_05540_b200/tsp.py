@@ -52,11 +52,21 @@ class tsp_asm_params(C.Structure):
 
 class tsp_cell_fields(C.Structure):
     _fields_ = [("E", C.c_void_p), ("perm", C.c_void_p), ("phi", C.c_void_p), ("sat", C.c_void_p),
-                ("pres", C.c_void_p), ("well", C.c_void_p)]
+                ("pres", C.c_void_p), ("well", C.c_void_p), ("phi0", C.c_void_p)]
 
 
 class tsp_bsr_out(C.Structure):
     _fields_ = [("rowptr", C.c_void_p), ("col", C.c_void_p), ("val", C.c_void_p)]
+
+
+class tsp_newton_opts(C.Structure):
+    _fields_ = [("rtol", C.c_double), ("atol", C.c_double), ("max_newton", C.c_int), ("lin_rtol", C.c_double),
+                ("max_lin_iters", C.c_int), ("refresh", C.c_int), ("max_halvings", C.c_int)]
+
+
+class tsp_newton_info(C.Structure):
+    _fields_ = [("newton_iters", C.c_int), ("lin_iters", C.c_int), ("halvings", C.c_int), ("status", C.c_int),
+                ("res0", C.c_double), ("res", C.c_double), ("res_hist", C.c_double * 16), ("lin_hist", C.c_int * 16)]
 
 
 _ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -178,6 +188,13 @@ def lib():
                                    C.c_void_p, _P(C.c_double), C.c_void_p]
         L.tsp_assemble_scale.argtypes = [_P(tsp_asm_params), C.c_int, C.c_int, C.c_int, _P(C.c_double), _P(tsp_bsr_out),
                                          C.c_void_p, _P(C.c_double), C.c_void_p]
+        L.tsp_residual.argtypes = [_P(tsp_asm_params), _P(tsp_cell_fields), C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_void_p]
+        L.tsp_masses.argtypes = [_P(tsp_asm_params), _P(tsp_cell_fields), C.c_void_p, C.c_void_p, C.c_void_p]
+        L.tsp_default_newton_opts.argtypes = [_P(tsp_newton_opts)]
+        L.tsp_default_newton_opts.restype = None
+        L.tsp_newton_step.argtypes = [C.c_void_p, _P(tsp_asm_params), _P(tsp_cell_fields), C.c_double, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, _P(tsp_newton_opts), _P(tsp_newton_info)]
         if L.tsp_abi_version() != 4:
             raise RuntimeError("libtsp ABI version mismatch")
         _LIB = L
@@ -189,7 +206,8 @@ EXPORTED = ["tsp_abi_version", "tsp_last_error", "tsp_default_options", "tsp_cre
             "tsp_get_stats", "tsp_level_sizes", "tsp_export_level", "tsp_prof_enable", "tsp_prof_read",
             "tsp_prof_classes", "tsp_export_cpr", "tsp_destroy", "tsp_nccl_unique_id", "tsp_local_world_create", "tsp_local_world_destroy",
             "tsp_partition", "tsp_level_dist", "tsp_variant_counts", "tsp_export_colour",
-            "tsp_assembly_sizes", "tsp_assemble", "tsp_assemble_scale"]
+            "tsp_assembly_sizes", "tsp_assemble", "tsp_assemble_scale", "tsp_residual", "tsp_masses",
+            "tsp_default_newton_opts", "tsp_newton_step"]
 
 # include/tsp.h TSP_VAR_* order
 VARIANTS = ["spgemm_hs64", "spgemm_hs128", "spgemm_hs512", "spgemm_hs4096", "spgemm_g4", "spgemm_g8", "spgemm_g32",
@@ -240,8 +258,11 @@ def assemble(params: dict, fields: dict, rank=0, nranks=1, zblock=16, stream=Non
         keep[k] = torch.as_tensor(fields[k], dtype=torch.float64).to(dev).contiguous()
     if fields.get("well") is not None:
         keep["well"] = torch.as_tensor(fields["well"], dtype=torch.int8).to(dev).contiguous()
+    if fields.get("phi0") is not None:
+        keep["phi0"] = torch.as_tensor(fields["phi0"], dtype=torch.float64).to(dev).contiguous()
     f = tsp_cell_fields(*(keep[k].data_ptr() for k in ("E", "perm", "phi", "sat", "pres")),
-                        keep["well"].data_ptr() if "well" in keep else None)
+                        keep["well"].data_ptr() if "well" in keep else None,
+                        keep["phi0"].data_ptr() if "phi0" in keep else None)
     a = {}
     for name, rows, nb, bs in (("uu", Nn, Buu, 9), ("uf", Nn, Buf, 6), ("fu", Nc, Bfu, 6), ("ff", Nc, Bff, 4)):
         a[name + "_rowptr"] = torch.empty(rows + 1, dtype=torch.int32, device=dev)
@@ -264,6 +285,41 @@ def assemble(params: dict, fields: dict, rank=0, nranks=1, zblock=16, stream=Non
     _check(L.tsp_assemble_scale(C.byref(P), rank, nranks, zblock, gmx, blocks, C.c_void_p(a["fs"].data_ptr()), sc,
                                 C.c_void_p(st.cuda_stream)), "tsp_assemble_scale")
     return AssembledProblem(params["nx"], params["ny"], params["nz"], Nn, Nc, a, list(sc), mx)
+
+
+def _asm_params(params):
+    return tsp_asm_params(nx=params["nx"], ny=params["ny"], nz=params["nz"],
+                          **{k: (int(params[k]) if k in ("burden", "dirichlet_bottom", "row_scale") else float(params[k]))
+                             for k in ASM_KEYS})
+
+
+def _ref_fields(ref):
+    """tsp_cell_fields of the reference state: E, perm, phi (= phi_0), pres (= p_ref), well (CUDA tensors)."""
+    return tsp_cell_fields(ref["E"].data_ptr(), ref["perm"].data_ptr(), ref["phi"].data_ptr(), None, ref["pres"].data_ptr(),
+                           ref["well"].data_ptr() if ref.get("well") is not None else None, None)
+
+
+def residual(params, ref, x, mprev, dt, out=None, stream=None):
+    """tsp_residual: r(x) of Appendix B.1 in raw units (x = [u | (s, p [Pa])], CUDA tensors)."""
+    import torch
+    out = torch.empty_like(x) if out is None else out
+    st = stream if stream is not None else torch.cuda.current_stream()
+    P, f = _asm_params(params), _ref_fields(ref)
+    _check(lib().tsp_residual(C.byref(P), C.byref(f), float(dt), C.c_void_p(x.data_ptr()), C.c_void_p(mprev.data_ptr()),
+                              C.c_void_p(out.data_ptr()), C.c_void_p(st.cuda_stream)), "tsp_residual")
+    return out
+
+
+def masses(params, ref, x, stream=None):
+    """tsp_masses: (V m_w, V m_nw) per cell at x."""
+    import torch
+    nc = params["nx"] * params["ny"] * params["nz"]
+    m = torch.empty(2 * nc, dtype=torch.float64, device=x.device)
+    st = stream if stream is not None else torch.cuda.current_stream()
+    P, f = _asm_params(params), _ref_fields(ref)
+    _check(lib().tsp_masses(C.byref(P), C.byref(f), C.c_void_p(x.data_ptr()), C.c_void_p(m.data_ptr()),
+                            C.c_void_p(st.cuda_stream)), "tsp_masses")
+    return m
 
 
 def nccl_unique_id() -> bytes:
@@ -411,6 +467,23 @@ class Tsp:
     def setup_flow(self, refresh=False):
         """tsp_setup(FLOW [| REFRESH]): the per-Newton flow phase; refresh keeps the pressure aggregation."""
         return self.setup(TSP_SETUP_FLOW | (TSP_SETUP_REFRESH if refresh else 0))
+
+    def newton_step(self, params, ref, x, mprev, dt, r_off=None, **opts):
+        """tsp_newton_step: one implicit time step by Newton with line search (x updated in place)."""
+        o = tsp_newton_opts()
+        lib().tsp_default_newton_opts(C.byref(o))
+        for k, v in opts.items():
+            setattr(o, k, v)
+        info = tsp_newton_info()
+        P, f = _asm_params(params), _ref_fields(ref)
+        rc = lib().tsp_newton_step(self.h, C.byref(P), C.byref(f), float(dt), C.c_void_p(x.data_ptr()),
+                                   C.c_void_p(mprev.data_ptr()), C.c_void_p(r_off.data_ptr()) if r_off is not None else None,
+                                   C.byref(o), C.byref(info))
+        _check(rc, "tsp_newton_step", ok=(0, 1))
+        k = info.newton_iters
+        return dict(newton_iters=k, lin_iters=info.lin_iters, halvings=info.halvings,
+                    status="OK" if info.status == 0 else "NOT_CONVERGED", res0=info.res0, res=info.res,
+                    res_hist=list(info.res_hist)[:min(k + 1, 16)], lin_hist=list(info.lin_hist)[:min(k, 16)])
 
     def apply_preconditioner(self, v, z):
         _check(lib().tsp_apply_preconditioner(self.h, _ptr(v), _ptr(z)), "tsp_apply_preconditioner")
