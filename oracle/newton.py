@@ -24,6 +24,7 @@ def newton_step(params, ref, x, mprev, dt, r_off=None, rtol=1e-6, atol=0.0, max_
                 max_halvings=5, **oracle_opts):
     """One implicit time step; x (numpy, [u | (s, p [Pa])]) is updated in place.  ref: E, perm, phi0, pref, well."""
     import synth
+    params = dict(params, dt=dt)                      # the Jacobian of this step's time step
     nx, ny, nz = params["nx"], params["ny"], params["nz"]
     nu = 3 * (nx + 1) * (ny + 1) * (nz + 1)
     info = dict(newton_iters=0, lin_iters=0, halvings=0, res_hist=[], lin_hist=[], status="NOT_CONVERGED")

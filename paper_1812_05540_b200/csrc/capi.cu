@@ -387,11 +387,36 @@ tsp_status tsp_update_values(tsp_handle h, const tsp_desc *d)
     }
     DBuf<double> fs; fs.alloc(2 * (size_t)std::max(c.Nc, 1));
     if (c.Nc) TSP_CUDA(cudaMemcpyAsync(fs, d->fs_diag, sizeof(double) * 2 * c.Nc, on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.s));
+    DBuf<double> vals[4];
+    for (int k = 0; k < 4; ++k) vals[k] = std::move(nw[k].v);
+    commit_values(c, vals, fs);
+    API_END
+}
+
+}  // extern "C"
+
+namespace tsp {
+// 1 if (rp, ci) of a device block differ from the stored pattern of A (global column ids when distributed)
+bool pattern_differs(Ctx &c, const Csr &A, const int32_t *rp, const int32_t *ci)
+{
+    DBuf<unsigned> flag; flag.alloc(1); flag.zero(c.s);
+    k_pattern_diff<<<grid_for(std::max<int64_t>(A.nnz, A.n + 1), 256), 256, 0, c.s>>>(A.n, A.nnz, rp, ci, A.rp,
+                                                                                  A.gci.p ? A.gci.p : A.ci.p, flag);
+    c.launches++;
+    unsigned f = 0;
+    TSP_CUDA(cudaMemcpyAsync(&f, flag.p, sizeof(f), cudaMemcpyDeviceToHost, c.s));
+    TSP_CUDA(cudaStreamSynchronize(c.s));
+    return f != 0;
+}
+// new values (moved in: A_uu 9, A_uf 6, A_fu 6, A_ff 4 per block entry, on the stored patterns) and D_fs; the apply
+// layouts are refilled, the flow phase must be redone (tsp_update_values)
+void commit_values(Ctx &c, DBuf<double> vals[4], DBuf<double> &fs)
+{
     TSP_REQUIRE(all_nonneg(c, fs, 2 * (int64_t)c.Nc), TSP_ERR_INVALID_ARG, "negative fixed-stress diagonal (S:355)");
-    // commit: new values into the stored patterns (local column ids) and the apply layouts
+    Csr *cur[4] = {&c.uu, &c.uf, &c.fu, &c.ff};
     krylov_graphs_drop(c);                    // the graphs bake in the SELL buffers' addresses
     c.fs = std::move(fs);
-    for (int k = 0; k < 4; ++k) cur[k]->v = std::move(nw[k].v);
+    for (int k = 0; k < 4; ++k) cur[k]->v = std::move(vals[k]);
     if (!sym_refill_uu(c)) sell_from_csr(c, c.uu, c.s_uu, 9);
     extract_sdc(c);                           // input of the next TSP_SETUP_MECH (a2)
     c.sdc_stale = true;
@@ -401,8 +426,10 @@ tsp_status tsp_update_values(tsp_handle h, const tsp_desc *d)
     c.uu.v.release(); c.uf.v.release(); c.fu.v.release();
     c.flow_ready = false;                     // apply / solve wait for the flow phase on the new values
     TSP_CUDA(cudaStreamSynchronize(c.s));
-    API_END
 }
+}  // namespace tsp
+
+extern "C" {
 
 tsp_status tsp_apply_preconditioner(tsp_handle h, const double *v, double *z)
 {

@@ -84,6 +84,12 @@ struct NewtonWork {
         r.alloc(n); rc.alloc(n); rhs.alloc(n); y.alloc(n); xt.alloc(n);
         part.alloc(1024); nrm.alloc(1);
     }
+    void realloc_values()   // after commit_values took the assembled values
+    {
+        const int64_t bs[4] = {9, 6, 6, 4};
+        for (int k = 0; k < 4; ++k) val[k].alloc(std::max<int64_t>(b[k], 1) * bs[k]);
+        fs.alloc(std::max<int64_t>(2 * nc, 1));
+    }
 };
 
 static double wnorm(cudaStream_t s, NewtonWork &W, const double *r, const double sc[3])
@@ -152,6 +158,9 @@ tsp_status tsp_newton_step(tsp_handle h, const tsp_asm_params *p, const tsp_cell
         TSP_REQUIRE(c.mech_ready, TSP_ERR_STATE, "tsp_newton_step: run tsp_setup(TSP_SETUP_MECH) first");
         TSP_REQUIRE(p->nx == c.nx && p->ny == c.ny && p->nz == c.nz_glob, TSP_ERR_INVALID_ARG, "tsp_newton_step: grid differs");
         const cudaStream_t s = c.s;
+        tsp_asm_params Pd = *p;
+        Pd.dt = dt;                                           // the Jacobian of this step's time step
+        p = &Pd;
         NewtonWork W;
         W.alloc(*p);
         const int64_t nu = 3 * W.nn, n = W.n;
@@ -162,6 +171,7 @@ tsp_status tsp_newton_step(tsp_handle h, const tsp_asm_params *p, const tsp_cell
         info->status = 1;
         for (int it = 0;; ++it) {
             // the Jacobian at x and its row scales
+            for (int k = 0; k < 4; ++k) blk[k] = tsp_bsr_out{W.rp[k].p, W.ci[k].p, W.val[k].p};
             state_fields(s, *p, *ref, x, W.phi, W.sat, W.pres);
             const tsp_cell_fields at{ref->E, ref->perm, W.phi.p, W.sat.p, W.pres.p, ref->well, ref->phi};
             double rmax[3], sc[3];
@@ -177,16 +187,17 @@ tsp_status tsp_newton_step(tsp_handle h, const tsp_asm_params *p, const tsp_cell
             if (it < 16) info->res_hist[it] = nrm;
             if (nrm <= o.atol || nrm <= o.rtol * norm0 || norm0 == 0.0) { info->status = 0; break; }
             if (it >= o.max_newton) break;
-            // the linear system of this iteration: update the handle's values, per-Newton flow setup, FGMRES
-            tsp_desc d;
-            memset(&d, 0, sizeof(d));
-            d.nx = c.nx; d.ny = c.ny; d.nz = c.nz_glob; d.rank = 0; d.nranks = 1; d.inputs_on_device = 1;
-            tsp_bsr *bs[4] = {&d.A_uu, &d.A_uf, &d.A_fu, &d.A_ff};
-            for (int k = 0; k < 4; ++k) *bs[k] = tsp_bsr{W.rp[k].p, W.ci[k].p, W.val[k].p};
-            d.fs_diag = W.fs.p;
-            tsp_status st = tsp_update_values(h, &d);
-            if (st != TSP_OK) return st;
-            st = tsp_setup(h, TSP_SETUP_FLOW | (o.refresh && c.flow_built ? TSP_SETUP_REFRESH : 0));
+            // the linear system of this iteration: the assembled values move into the handle (same patterns, checked
+            // once), per-Newton flow setup, FGMRES
+            if (it == 0) {
+                const Csr *cur[4] = {&c.uu, &c.uf, &c.fu, &c.ff};
+                for (int k = 0; k < 4; ++k)
+                    TSP_REQUIRE(cur[k]->nnz == W.b[k] && !pattern_differs(c, *cur[k], W.rp[k], W.ci[k]), TSP_ERR_INVALID_ARG,
+                                "tsp_newton_step: the handle's patterns are not this grid's");
+            }
+            commit_values(c, W.val, W.fs);
+            W.realloc_values();
+            tsp_status st = tsp_setup(h, TSP_SETUP_FLOW | (o.refresh && c.flow_built ? TSP_SETUP_REFRESH : 0));
             if (st != TSP_OK) return st;
             tsp_solve_opts so;
             tsp_default_solve_opts(&so);

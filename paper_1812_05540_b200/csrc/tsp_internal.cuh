@@ -391,6 +391,10 @@ void assemble(cudaStream_t s, const tsp_asm_params &P, int rank, int nranks, int
 void assemble_scale(cudaStream_t s, const tsp_asm_params &P, int rank, int nranks, int zblock, const double row_max[3],
                     tsp_bsr_out blk[4], double *fs, double scales[3]);
 
+// capi.cu: value update on the stored patterns (tsp_update_values; the Newton step moves its assembled values in)
+bool pattern_differs(Ctx &c, const Csr &A, const int32_t *rp, const int32_t *ci);
+void commit_values(Ctx &c, DBuf<double> vals[4], DBuf<double> &fs);
+
 // Appendix B.1 residual, state fields and masses at x (single rank; ref: E, perm, phi = phi_0, pres = p_ref, well)
 void residual(cudaStream_t s, const tsp_asm_params &P, const tsp_cell_fields &ref, double dt, const double *x, const double *mprev,
               double *r);
