@@ -103,3 +103,71 @@ def test_solve_on_the_device_assembled_jacobian(dev):
     assert info["status"] == "OK" and abs(info["iterations"] - ih["iterations"]) <= 1
     assert torch.linalg.norm(x - xh) <= 1e-6 * torch.linalg.norm(xh)
     g.close(); h.close()
+
+
+def test_slab_pipeline_from_fields_is_rank_invariant(dev):
+    """The multi-GPU bench pipeline on the in-process communicator: every rank assembles its slab from the global
+    fields (row maxima combined over the ranks), creates its handle from device blocks, forms b = A x_rand on the
+    device (a collective operator) and solves -- the glued solution and the iteration count equal the single-rank
+    run of the same pipeline BITWISE."""
+    import threading
+    from paper_1812_05540_b200 import LocalWorld, Tsp, TSP_COMM_LOCAL, assemble
+    kw = dict(nx=12, ny=10, nz=64, recipe=2, perm_sigma=2.0)
+    f = synth.fields(**kw)
+    prm = f["params"]
+    s = synth.sizes(prm["nx"], prm["ny"], prm["nz"])
+
+    def run(P):
+        world = LocalWorld(P) if P > 1 else None
+        maxima, lock, barrier = [None] * P, threading.Lock(), threading.Barrier(P)
+        out, errs = [None] * P, []
+
+        def gmax(r):
+            def fn(m):
+                with lock:
+                    maxima[r] = m
+                barrier.wait()
+                return list(np.max(np.array(maxima), axis=0))
+            return fn
+
+        def body(r):
+            try:
+                st = torch.cuda.Stream()
+                with torch.cuda.stream(st):
+                    ap = assemble(prm, f, rank=r, nranks=P, stream=st, global_max=gmax(r))
+                    _, _, n0, nn, c0, ncl = synth.slab_partition(prm["nx"], prm["ny"], prm["nz"], 16, r, P)
+                    xr = f["x_rand"]
+                    xl = np.concatenate([xr[3 * n0:3 * (n0 + nn)], xr[3 * s["Nn"] + 2 * c0:3 * s["Nn"] + 2 * (c0 + ncl)]])
+                    kwc = dict(rank=r, nranks=P, comm_kind=TSP_COMM_LOCAL, comm_arg=world.h) if P > 1 else {}
+                    g = Tsp(ap, stream=st, **kwc).setup()
+                    b = torch.empty(ap.n, dtype=torch.float64, device=dev)
+                    g.apply_operator(_cuda_t(xl), b)
+                    x = torch.zeros_like(b)
+                    info = g.solve(b, x, rtol=1e-8)
+                    torch.cuda.synchronize()
+                    out[r] = (x.cpu().numpy(), info["iterations"], nn)
+                    g.close()
+            except Exception as e:   # pragma: no cover - surfaced below
+                errs.append(e)
+
+        ts = [threading.Thread(target=body, args=(r,)) for r in range(P)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        if world:
+            world.close()
+        if errs:
+            raise errs[0]
+        return out
+
+    (x1, it1, _), = run(1)
+    parts = run(2)
+    u = np.concatenate([p[0][:3 * p[2]] for p in parts])
+    fl = np.concatenate([p[0][3 * p[2]:] for p in parts])
+    assert np.array_equal(np.concatenate([u, fl]), x1)
+    assert parts[0][1] == parts[1][1] == it1
+
+
+def _cuda_t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
