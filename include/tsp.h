@@ -302,7 +302,8 @@ tsp_status tsp_assemble_scale(const tsp_asm_params *p, int rank, int nranks, int
  * State x (device, n = 3 N_n + 2 N_c): [u node-major (m) | (s, p [Pa]) per cell] -- raw pressure, unlike the
  * linear system's unknown p / p_unit.  `ref` fields: E, perm, well as for tsp_assemble, phi = the REFERENCE
  * porosity phi_0 and pres = the reference pressure p_ref of eq:linearized_porosity (phi = phi_0 + b eps_v +
- * (b - phi_0)(1 - b)/K_dr (p - p_ref), eps_v averaged over the cell); sat is not read.  Single GPU. */
+ * (b - phi_0)(1 - b)/K_dr (p - p_ref), eps_v averaged over the cell); sat is not read.  tsp_residual and
+ * tsp_masses take GLOBAL vectors (one GPU); tsp_newton_residual / tsp_newton_step work on z-slab ranks. */
 /* r = r(x) in raw units (N for momentum rows, kg for mass rows); mprev: (V m_w, V m_nw) per cell of the previous
  * step (tsp_masses); Dirichlet rows 0.  Synchronises `stream`. */
 tsp_status tsp_residual(const tsp_asm_params *p, const tsp_cell_fields *ref, double dt, const double *x, const double *mprev,
@@ -325,13 +326,21 @@ typedef struct {
     int lin_hist[16];            /* FGMRES iterations per Newton iteration */
 } tsp_newton_info;
 void tsp_default_newton_opts(tsp_newton_opts *o);
+/* this rank's residual rows r (its [u_own | f_own], raw units) at the rank-local state x (gathered over the ranks
+ * of h); mprev (this rank's cells, or NULL: the masses at x).  Collective; synchronises. */
+tsp_status tsp_newton_residual(tsp_handle h, const tsp_asm_params *p, const tsp_cell_fields *ref, double dt, const double *x,
+                               const double *mprev, double *r);
 /* One implicit time step (dt) by Newton's method with backtracking line search on the handle `h` (created from a
  * Jacobian of the same grid, tsp_setup(MECH) done): per iteration the Jacobian is re-assembled at x on the device
- * (tsp_assemble), pushed into h (tsp_update_values), the flow phase redone (TSP_SETUP_FLOW[|REFRESH]; the mechanics
- * AMG stays) and J dx = -S r solved by the two-stage preconditioned FGMRES; x += alpha dx with alpha halved
- * until ||S0 r|| decreases (saturation kept in [0, 1]).  r_off (device, 3 N_n, may be NULL): a momentum residual
+ * (tsp_assemble), moved into h, the flow phase redone (TSP_SETUP_FLOW[|REFRESH]; the mechanics AMG stays)
+ * and J dx = -S r solved by the two-stage preconditioned FGMRES; x += alpha dx with alpha halved until ||S0 r||
+ * decreases (saturation kept in [0, 1]).  r_off (device, 3 N_n, may be NULL): a momentum residual
  * subtracted from every evaluation (the initial-state equilibrium, so that u measures the displacement since t0).
- * x is updated in place.  Returns TSP_OK, TSP_NOT_CONVERGED (info filled) or an error. */
+ * On z-slab ranks (handle with a communicator) x, mprev, r_off are the rank's parts ([u_own | f_own], its cells, its
+ * 3 N_n momentum rows); the state is gathered over the ranks for the residual and the state fields, the norms are
+ * taken over the gathered residual, so every rank takes the same decisions and the step is bitwise the one-rank
+ * step.  mprev NULL: the masses at x (the start of the step).  x is updated in place.  Returns TSP_OK,
+ * TSP_NOT_CONVERGED (info filled) or an error. */
 tsp_status tsp_newton_step(tsp_handle h, const tsp_asm_params *p, const tsp_cell_fields *ref, double dt, double *x,
                            const double *mprev, const double *r_off, const tsp_newton_opts *o, tsp_newton_info *info);
 

@@ -401,6 +401,7 @@ __device__ ResSt res_st(const tsp_asm_params &P, const AsmGeo &g, const Q1 *__re
     return C;
 }
 
+// x: the GLOBAL state (NnG nodes); r: this rank's rows [u_own | f_own] (g.nn, g.ncl)
 __global__ void __launch_bounds__(128) k_res_node(tsp_asm_params P, AsmGeo g, const Q1 *__restrict__ q, const double *__restrict__ E,
                                                   const double *__restrict__ phi0, const double *__restrict__ pref,
                                                   const double *__restrict__ x, int64_t Nn, double *__restrict__ r)
@@ -451,6 +452,7 @@ __global__ void __launch_bounds__(128) k_res_cell(tsp_asm_params P, AsmGeo g, co
                                                   const double *__restrict__ x, int64_t Nn, const double *__restrict__ mprev,
                                                   double dt, double *__restrict__ r)
 {
+    // mprev: this rank's cells; r: this rank's rows (the cell part starts after its 3 g.nn node rows)
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= g.ncl) return;
     const int64_t c = g.cell0 + t, P2 = (int64_t)g.nx * g.ny;
@@ -501,8 +503,8 @@ __global__ void __launch_bounds__(128) k_res_cell(tsp_asm_params P, AsmGeo g, co
             (ph ? rn : rw) -= dt * src;
         }
     }
-    r[3 * Nn + 2 * (int64_t)t] = rw;
-    r[3 * Nn + 2 * (int64_t)t + 1] = rn;
+    r[3 * (int64_t)g.nn + 2 * (int64_t)t] = rw;
+    r[3 * (int64_t)g.nn + 2 * (int64_t)t + 1] = rn;
 }
 
 // current porosity, saturation and pressure of every cell at x (the fields of the Jacobian at the state)
@@ -542,12 +544,12 @@ struct Q1Dev {
 };
 
 void residual(cudaStream_t s, const tsp_asm_params &P, const tsp_cell_fields &ref, double dt, const double *x, const double *mprev,
-              double *r)
+              double *r, int rank, int nranks, int zblock)
 {
     TSP_REQUIRE(ref.E && ref.perm && ref.phi && ref.pres && x && mprev && r, TSP_ERR_INVALID_ARG, "residual: null pointer");
-    const AsmGeo g = asm_geo(P, 0, 1, 16);
+    const AsmGeo g = asm_geo(P, rank, nranks, zblock);
     Q1Dev q(s, g.h);
-    const int64_t Nn = g.nn;
+    const int64_t Nn = (int64_t)(P.nx + 1) * (P.ny + 1) * (P.nz + 1);   // x is the global state
     if (g.nn) k_res_node<<<grid_for(g.nn, 128), 128, 0, s>>>(P, g, q.q.p, ref.E, ref.phi, ref.pres, x, Nn, r);
     if (g.ncl) k_res_cell<<<grid_for(g.ncl, 128), 128, 0, s>>>(P, g, q.q.p, ref.E, ref.perm, ref.phi, ref.pres, ref.well, x, Nn,
                                                               mprev, dt, r);
@@ -567,6 +569,15 @@ void masses(cudaStream_t s, const tsp_asm_params &P, const tsp_cell_fields &ref,
     Q1Dev q(s, g.h);
     if (g.ncl) k_masses<<<grid_for(g.ncl, 128), 128, 0, s>>>(P, g, q.q.p, ref.E, ref.phi, ref.pres, x, g.nn, m);
     TSP_CUDA(cudaGetLastError());
+}
+// this rank's cells of a global per-cell array pair (V m_w, V m_nw)
+void masses_local(cudaStream_t s, const tsp_asm_params &P, const tsp_cell_fields &ref, const double *xg, double *m_local, int rank,
+                  int nranks, int zblock)
+{
+    const AsmGeo gl = asm_geo(P, rank, nranks, zblock);
+    DBuf<double> mg; mg.alloc((size_t)std::max<int64_t>(2 * (int64_t)P.nx * P.ny * P.nz, 1));
+    masses(s, P, ref, xg, mg);
+    if (gl.ncl) TSP_CUDA(cudaMemcpyAsync(m_local, mg.p + 2 * gl.cell0, sizeof(double) * 2 * gl.ncl, cudaMemcpyDeviceToDevice, s));
 }
 
 static AsmGeo asm_geo(const tsp_asm_params &P, int rank, int nranks, int zblock)

@@ -66,25 +66,27 @@ __global__ void k_newton_update(int64_t nu, int64_t n, const double *__restrict_
 }
 
 struct NewtonWork {
-    int64_t nn, nc, n, b[4];
+    int64_t nn, nc, n, b[4];            // this rank's rows
+    int64_t NnG, NcG, NG;               // global sizes
     DBuf<int32_t> rp[4], ci[4];
-    DBuf<double> val[4], fs, phi, sat, pres, r, rc, rhs, y, xt, part, nrm;
-    void alloc(const tsp_asm_params &P)
+    DBuf<double> val[4], fs, phi, sat, pres, r, rc, rhs, y, xt, xg, rg, part, nrm, mp, sbuf, rbuf;
+    void alloc(const tsp_asm_params &P, int rank, int nranks, int zblock)
     {
         int64_t sz[6];
-        assembly_sizes(P, 0, 1, 16, sz);
+        assembly_sizes(P, rank, nranks, zblock, sz);
         nn = sz[0]; nc = sz[1]; n = 3 * nn + 2 * nc;
-        const int64_t rows[4] = {nn, nn, nc, nc}, bs[4] = {9, 6, 6, 4};
+        NnG = (int64_t)(P.nx + 1) * (P.ny + 1) * (P.nz + 1); NcG = (int64_t)P.nx * P.ny * P.nz; NG = 3 * NnG + 2 * NcG;
+        const int64_t rows[4] = {nn, nn, nc, nc};
         for (int k = 0; k < 4; ++k) {
             b[k] = sz[2 + k];
-            rp[k].alloc(rows[k] + 1); ci[k].alloc(std::max<int64_t>(b[k], 1)); val[k].alloc(std::max<int64_t>(b[k], 1) * bs[k]);
+            rp[k].alloc(rows[k] + 1); ci[k].alloc(std::max<int64_t>(b[k], 1));
         }
-        fs.alloc(std::max<int64_t>(2 * nc, 1));
-        phi.alloc(std::max<int64_t>(nc, 1)); sat.alloc(std::max<int64_t>(nc, 1)); pres.alloc(std::max<int64_t>(nc, 1));
-        r.alloc(n); rc.alloc(n); rhs.alloc(n); y.alloc(n); xt.alloc(n);
-        part.alloc(1024); nrm.alloc(1);
+        realloc_values();
+        phi.alloc(std::max<int64_t>(NcG, 1)); sat.alloc(std::max<int64_t>(NcG, 1)); pres.alloc(std::max<int64_t>(NcG, 1));
+        r.alloc(n); rc.alloc(n); rhs.alloc(n); y.alloc(n); xt.alloc(n); xg.alloc(NG); rg.alloc(NG);
+        part.alloc(1024); nrm.alloc(1); mp.alloc(std::max<int64_t>(2 * nc, 1));
     }
-    void realloc_values()   // after commit_values took the assembled values
+    void realloc_values()   // (again) after commit_values took the assembled values
     {
         const int64_t bs[4] = {9, 6, 6, 4};
         for (int k = 0; k < 4; ++k) val[k].alloc(std::max<int64_t>(b[k], 1) * bs[k]);
@@ -92,10 +94,39 @@ struct NewtonWork {
     }
 };
 
-static double wnorm(cudaStream_t s, NewtonWork &W, const double *r, const double sc[3])
+// the ranks' [u_own | f_own] gathered into the global [u | f] (identical on every rank; a copy on one rank)
+static void gather_state(Ctx &c, NewtonWork &W, const double *xl, double *xg)
 {
-    const int nb = (int)std::min<int64_t>(1024, (W.n + kNT - 1) / kNT);
-    if (W.n) k_wnorm_part<<<nb, kNT, 0, s>>>(3 * W.nn, W.n, r, sc[0], sc[1], sc[2], W.part);
+    const cudaStream_t s = c.s;
+    if (!c.comm) { TSP_CUDA(cudaMemcpyAsync(xg, xl, sizeof(double) * W.n, cudaMemcpyDeviceToDevice, s)); return; }
+    const int P = c.nranks;
+    std::vector<int64_t> parts(6 * (size_t)P);
+    int64_t mu = 1, mf = 1;
+    for (int r = 0; r < P; ++r) {
+        partition(c.nx, c.ny, c.nz_glob, c.o.zblock, r, P, &parts[6 * r]);
+        mu = std::max(mu, 3 * parts[6 * r + 3]); mf = std::max(mf, 2 * parts[6 * r + 5]);
+    }
+    const int64_t blk = mu + mf;
+    if (W.sbuf.n < (size_t)blk) W.sbuf.alloc(blk);
+    if (W.rbuf.n < (size_t)blk * P) W.rbuf.alloc(blk * P);
+    TSP_CUDA(cudaMemcpyAsync(W.sbuf.p, xl, sizeof(double) * 3 * W.nn, cudaMemcpyDeviceToDevice, s));
+    TSP_CUDA(cudaMemcpyAsync(W.sbuf.p + mu, xl + 3 * W.nn, sizeof(double) * 2 * W.nc, cudaMemcpyDeviceToDevice, s));
+    c.comm->allgather(W.sbuf.p, W.rbuf.p, sizeof(double) * blk, s);
+    for (int r = 0; r < P; ++r) {
+        const int64_t *q = &parts[6 * r];
+        if (q[3]) TSP_CUDA(cudaMemcpyAsync(xg + 3 * q[2], W.rbuf.p + r * blk, sizeof(double) * 3 * q[3], cudaMemcpyDeviceToDevice, s));
+        if (q[5]) TSP_CUDA(cudaMemcpyAsync(xg + 3 * W.NnG + 2 * q[4], W.rbuf.p + r * blk + mu, sizeof(double) * 2 * q[5],
+                                           cudaMemcpyDeviceToDevice, s));
+    }
+}
+
+// ||S0 r|| over the GLOBAL residual (gathered): every rank computes the same number, equal to the one-rank value
+static double wnorm(Ctx &c, NewtonWork &W, const double *rl, const double sc[3])
+{
+    const cudaStream_t s = c.s;
+    gather_state(c, W, rl, W.rg);
+    const int nb = (int)std::min<int64_t>(1024, (W.NG + kNT - 1) / kNT);
+    if (W.NG) k_wnorm_part<<<nb, kNT, 0, s>>>(3 * W.NnG, W.NG, W.rg, sc[0], sc[1], sc[2], W.part);
     k_sum_parts<<<1, 1, 0, s>>>(nb, W.part, W.nrm);
     double v = 0.0;
     TSP_CUDA(cudaMemcpyAsync(&v, W.nrm.p, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -146,7 +177,7 @@ void tsp_default_newton_opts(tsp_newton_opts *o)
 tsp_status tsp_newton_step(tsp_handle h, const tsp_asm_params *p, const tsp_cell_fields *ref, double dt, double *x,
                            const double *mprev, const double *r_off, const tsp_newton_opts *opts, tsp_newton_info *info)
 {
-    if (!h || !p || !ref || !x || !mprev || !info) { set_error("null argument"); return TSP_ERR_INVALID_ARG; }
+    if (!h || !p || !ref || !x || !info) { set_error("null argument"); return TSP_ERR_INVALID_ARG; }
     tsp_newton_opts o;
     tsp_default_newton_opts(&o);
     if (opts) o = *opts;
@@ -154,34 +185,50 @@ tsp_status tsp_newton_step(tsp_handle h, const tsp_asm_params *p, const tsp_cell
     try {
         Ctx &c = *h;
         StreamScope ss_(c.s, &c.alloc);
-        TSP_REQUIRE(c.nranks == 1, TSP_ERR_INVALID_ARG, "tsp_newton_step is single-GPU");
         TSP_REQUIRE(c.mech_ready, TSP_ERR_STATE, "tsp_newton_step: run tsp_setup(TSP_SETUP_MECH) first");
         TSP_REQUIRE(p->nx == c.nx && p->ny == c.ny && p->nz == c.nz_glob, TSP_ERR_INVALID_ARG, "tsp_newton_step: grid differs");
         const cudaStream_t s = c.s;
+        const int rank = c.rank, P = c.nranks, zb = c.o.zblock;
         tsp_asm_params Pd = *p;
         Pd.dt = dt;                                           // the Jacobian of this step's time step
         p = &Pd;
         NewtonWork W;
-        W.alloc(*p);
+        W.alloc(*p, rank, P, zb);
+        TSP_REQUIRE(W.n == c.n, TSP_ERR_INVALID_ARG, "tsp_newton_step: the handle's rows are not this rank's slab");
         const int64_t nu = 3 * W.nn, n = W.n;
-        tsp_bsr_out blk[4];
-        for (int k = 0; k < 4; ++k) blk[k] = tsp_bsr_out{W.rp[k].p, W.ci[k].p, W.val[k].p};
+        // masses of the state at the start of the step (unless given)
+        const double *mp = mprev;
+        if (!mp) {
+            gather_state(c, W, x, W.xg);
+            masses_local(s, *p, *ref, W.xg, W.mp, rank, P, zb);
+            mp = W.mp;
+        }
+        auto eval = [&](const double *xl, double *rl) {       // this rank's residual rows at the local state xl
+            gather_state(c, W, xl, W.xg);
+            residual(s, *p, *ref, dt, W.xg, mp, rl, rank, P, zb);
+        };
         double S0[3] = {1, 1, 1};
         double norm0 = 0.0;
         info->status = 1;
         for (int it = 0;; ++it) {
-            // the Jacobian at x and its row scales
+            // the Jacobian at x (this rank's slab, the state fields of the whole grid) and its row scales
+            tsp_bsr_out blk[4];
             for (int k = 0; k < 4; ++k) blk[k] = tsp_bsr_out{W.rp[k].p, W.ci[k].p, W.val[k].p};
-            state_fields(s, *p, *ref, x, W.phi, W.sat, W.pres);
+            gather_state(c, W, x, W.xg);
+            state_fields(s, *p, *ref, W.xg, W.phi, W.sat, W.pres);
             const tsp_cell_fields at{ref->E, ref->perm, W.phi.p, W.sat.p, W.pres.p, ref->well, ref->phi};
             double rmax[3], sc[3];
-            assemble(s, *p, 0, 1, 16, at, blk, W.fs, rmax);
-            assemble_scale(s, *p, 0, 1, 16, rmax, blk, W.fs, sc);
+            assemble(s, *p, rank, P, zb, at, blk, W.fs, rmax);
+            if (c.comm) {                                     // the row maxima over the ranks (exact)
+                std::vector<double> all = host_allgather<double>(c, std::vector<double>(rmax, rmax + 3));
+                for (int r = 0; r < P; ++r) for (int k = 0; k < 3; ++k) rmax[k] = std::max(rmax[k], all[3 * r + k]);
+            }
+            assemble_scale(s, *p, rank, P, zb, rmax, blk, W.fs, sc);
             if (it == 0) memcpy(S0, sc, sizeof(S0));
             // residual (minus the initial-state momentum offset)
-            residual(s, *p, *ref, dt, x, mprev, W.r);
+            eval(x, W.r);
             if (n) k_newton_rhs<<<grid_for(n, 256), 256, 0, s>>>(nu, n, W.r, r_off, sc[0], sc[1], sc[2], W.rhs, W.rc);
-            const double nrm = wnorm(s, W, W.rc, S0);
+            const double nrm = wnorm(c, W, W.rc, S0);
             if (it == 0) { norm0 = nrm; info->res0 = nrm; }
             info->res = nrm;
             if (it < 16) info->res_hist[it] = nrm;
@@ -207,13 +254,13 @@ tsp_status tsp_newton_step(tsp_handle h, const tsp_asm_params *p, const tsp_cell
             if (st != TSP_OK && st != TSP_NOT_CONVERGED) return st;
             info->lin_iters += si.iterations;
             if (it < 16) info->lin_hist[it] = si.iterations;
-            // backtracking line search on the S0-scaled residual norm
+            // backtracking line search on the S0-scaled residual norm (the same decisions on every rank)
             double alpha = 1.0, nt = 0.0;
             for (int hv = 0;; ++hv) {
                 if (n) k_newton_update<<<grid_for(n, 256), 256, 0, s>>>(nu, n, x, W.y, alpha, p->p_unit, W.xt);
-                residual(s, *p, *ref, dt, W.xt, mprev, W.r);
+                eval(W.xt, W.r);
                 if (n) k_newton_rhs<<<grid_for(n, 256), 256, 0, s>>>(nu, n, W.r, r_off, 1.0, 1.0, 1.0, W.rhs, W.rc);
-                nt = wnorm(s, W, W.rc, S0);
+                nt = wnorm(c, W, W.rc, S0);
                 if (nt <= (1.0 - 1e-4 * alpha) * nrm || hv >= o.max_halvings) break;
                 alpha *= 0.5;
                 info->halvings++;
@@ -224,6 +271,27 @@ tsp_status tsp_newton_step(tsp_handle h, const tsp_asm_params *p, const tsp_cell
         }
         TSP_CUDA(cudaStreamSynchronize(s));
         return info->status == 0 ? TSP_OK : TSP_NOT_CONVERGED;
+    } catch (...) {
+        return status_of_current_exception();
+    }
+}
+
+tsp_status tsp_newton_residual(tsp_handle h, const tsp_asm_params *p, const tsp_cell_fields *ref, double dt, const double *x,
+                               const double *mprev, double *r)
+{
+    if (!h || !p || !ref || !x || !r) { set_error("null argument"); return TSP_ERR_INVALID_ARG; }
+    try {
+        Ctx &c = *h;
+        StreamScope ss_(c.s, &c.alloc);
+        NewtonWork W;
+        W.alloc(*p, c.rank, c.nranks, c.o.zblock);
+        TSP_REQUIRE(W.n == c.n, TSP_ERR_INVALID_ARG, "tsp_newton_residual: the handle's rows are not this rank's slab");
+        gather_state(c, W, x, W.xg);
+        const double *mp = mprev;
+        if (!mp) { masses_local(c.s, *p, *ref, W.xg, W.mp, c.rank, c.nranks, c.o.zblock); mp = W.mp; }
+        residual(c.s, *p, *ref, dt, W.xg, mp, r, c.rank, c.nranks, c.o.zblock);
+        TSP_CUDA(cudaStreamSynchronize(c.s));
+        return TSP_OK;
     } catch (...) {
         return status_of_current_exception();
     }

@@ -396,8 +396,11 @@ bool pattern_differs(Ctx &c, const Csr &A, const int32_t *rp, const int32_t *ci)
 void commit_values(Ctx &c, DBuf<double> vals[4], DBuf<double> &fs);
 
 // Appendix B.1 residual, state fields and masses at x (single rank; ref: E, perm, phi = phi_0, pres = p_ref, well)
+// residual rows of `rank` (its [u_own | f_own]) from the GLOBAL state x; mprev: this rank's cells
 void residual(cudaStream_t s, const tsp_asm_params &P, const tsp_cell_fields &ref, double dt, const double *x, const double *mprev,
-              double *r);
+              double *r, int rank = 0, int nranks = 1, int zblock = 16);
+void masses_local(cudaStream_t s, const tsp_asm_params &P, const tsp_cell_fields &ref, const double *xg, double *m_local, int rank,
+                  int nranks, int zblock);
 void state_fields(cudaStream_t s, const tsp_asm_params &P, const tsp_cell_fields &ref, const double *x, double *phi, double *sat,
                   double *pres);
 void masses(cudaStream_t s, const tsp_asm_params &P, const tsp_cell_fields &ref, const double *x, double *m);

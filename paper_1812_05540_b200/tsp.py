@@ -191,6 +191,8 @@ def lib():
         L.tsp_residual.argtypes = [_P(tsp_asm_params), _P(tsp_cell_fields), C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_void_p]
         L.tsp_masses.argtypes = [_P(tsp_asm_params), _P(tsp_cell_fields), C.c_void_p, C.c_void_p, C.c_void_p]
+        L.tsp_newton_residual.argtypes = [C.c_void_p, _P(tsp_asm_params), _P(tsp_cell_fields), C.c_double, C.c_void_p,
+                                          C.c_void_p, C.c_void_p]
         L.tsp_default_newton_opts.argtypes = [_P(tsp_newton_opts)]
         L.tsp_default_newton_opts.restype = None
         L.tsp_newton_step.argtypes = [C.c_void_p, _P(tsp_asm_params), _P(tsp_cell_fields), C.c_double, C.c_void_p, C.c_void_p,
@@ -207,7 +209,7 @@ EXPORTED = ["tsp_abi_version", "tsp_last_error", "tsp_default_options", "tsp_cre
             "tsp_prof_classes", "tsp_export_cpr", "tsp_destroy", "tsp_nccl_unique_id", "tsp_local_world_create", "tsp_local_world_destroy",
             "tsp_partition", "tsp_level_dist", "tsp_variant_counts", "tsp_export_colour",
             "tsp_assembly_sizes", "tsp_assemble", "tsp_assemble_scale", "tsp_residual", "tsp_masses",
-            "tsp_default_newton_opts", "tsp_newton_step"]
+            "tsp_default_newton_opts", "tsp_newton_step", "tsp_newton_residual"]
 
 # include/tsp.h TSP_VAR_* order
 VARIANTS = ["spgemm_hs64", "spgemm_hs128", "spgemm_hs512", "spgemm_hs4096", "spgemm_g4", "spgemm_g8", "spgemm_g32",
@@ -468,8 +470,18 @@ class Tsp:
         """tsp_setup(FLOW [| REFRESH]): the per-Newton flow phase; refresh keeps the pressure aggregation."""
         return self.setup(TSP_SETUP_FLOW | (TSP_SETUP_REFRESH if refresh else 0))
 
+    def newton_residual(self, params, ref, x, dt, mprev=None, out=None):
+        """tsp_newton_residual: this rank's residual rows at the rank-local state x (collective)."""
+        out = self.torch.empty_like(x) if out is None else out
+        P, f = _asm_params(params), _ref_fields(ref)
+        _check(lib().tsp_newton_residual(self.h, C.byref(P), C.byref(f), float(dt), C.c_void_p(x.data_ptr()),
+                                         C.c_void_p(mprev.data_ptr()) if mprev is not None else None,
+                                         C.c_void_p(out.data_ptr())), "tsp_newton_residual")
+        return out
+
     def newton_step(self, params, ref, x, mprev, dt, r_off=None, **opts):
-        """tsp_newton_step: one implicit time step by Newton with line search (x updated in place)."""
+        """tsp_newton_step: one implicit time step by Newton with line search (x updated in place; mprev None: the
+        masses at x)."""
         o = tsp_newton_opts()
         lib().tsp_default_newton_opts(C.byref(o))
         for k, v in opts.items():
@@ -477,7 +489,8 @@ class Tsp:
         info = tsp_newton_info()
         P, f = _asm_params(params), _ref_fields(ref)
         rc = lib().tsp_newton_step(self.h, C.byref(P), C.byref(f), float(dt), C.c_void_p(x.data_ptr()),
-                                   C.c_void_p(mprev.data_ptr()), C.c_void_p(r_off.data_ptr()) if r_off is not None else None,
+                                   C.c_void_p(mprev.data_ptr()) if mprev is not None else None,
+                                   C.c_void_p(r_off.data_ptr()) if r_off is not None else None,
                                    C.byref(o), C.byref(info))
         _check(rc, "tsp_newton_step", ok=(0, 1))
         k = info.newton_iters

@@ -101,3 +101,67 @@ def test_newton_steps_match_the_oracle(dev, cfg, kw, nsteps):
             assert abs(a - b) <= 1e-5 * io["res_hist"][0], (step, io["res_hist"], ig["res_hist"])
         for sl in (slice(0, 3 * Nn), slice(3 * Nn, None, 2), slice(3 * Nn + 1, None, 2)):
             assert np.linalg.norm(xg[sl] - xo[sl]) <= 1e-6 * max(np.linalg.norm(xo[sl]), 1e-30), (step, sl)
+
+
+def test_newton_step_is_rank_invariant(dev):
+    """Two z-slab ranks on the in-process communicator, each with its slab's handle (device assembly from the global
+    fields): one Newton time step gives BITWISE the one-rank state, residual history and iteration counts (the state
+    and the residual are gathered, the norms taken over the gathered residual, the linear solves are P-invariant)."""
+    import threading
+    from paper_1812_05540_b200 import LocalWorld, Tsp, TSP_COMM_LOCAL, assemble
+    kw = dict(nx=12, ny=10, nz=64, recipe=2, perm_sigma=2.0)
+    prm, f, s, x0, ref_o, ref_g = _setup(None, **kw)
+    Nn = s["Nn"]
+    m0 = oracle.masses(prm, ref_o, x0)
+    roff = oracle.residual(prm, ref_o, x0, m0, prm["dt"])[:3 * Nn]
+
+    def run(P):
+        world = LocalWorld(P) if P > 1 else None
+        maxima, lock, barrier = [None] * P, threading.Lock(), threading.Barrier(P)
+        out, errs = [None] * P, []
+
+        def gmax(r):
+            def fn(m):
+                with lock:
+                    maxima[r] = m
+                barrier.wait()
+                return list(np.max(np.array(maxima), axis=0))
+            return fn
+
+        def body(r):
+            try:
+                st = torch.cuda.Stream()
+                with torch.cuda.stream(st):
+                    _, _, n0, nn, c0, ncl = synth.slab_partition(prm["nx"], prm["ny"], prm["nz"], 16, r, P)
+                    ap = assemble(prm, dict(f, phi0=f["phi"]), rank=r, nranks=P, stream=st, global_max=gmax(r))
+                    kwc = dict(rank=r, nranks=P, comm_kind=TSP_COMM_LOCAL, comm_arg=world.h) if P > 1 else {}
+                    g = Tsp(ap, stream=st, **kwc)
+                    g.setup(1)
+                    xl = np.concatenate([x0[3 * n0:3 * (n0 + nn)], x0[3 * Nn + 2 * c0:3 * Nn + 2 * (c0 + ncl)]])
+                    x = _cuda(xl)
+                    info = g.newton_step(prm, ref_g, x, None, prm["dt"], r_off=_cuda(roff[3 * n0:3 * (n0 + nn)]))
+                    torch.cuda.synchronize()
+                    out[r] = (x.cpu().numpy(), info, nn)
+                    g.close()
+            except Exception as e:   # pragma: no cover - surfaced below
+                errs.append(e)
+
+        ts = [threading.Thread(target=body, args=(r,)) for r in range(P)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        if world:
+            world.close()
+        if errs:
+            raise errs[0]
+        return out
+
+    (x1, i1, _), = run(1)
+    parts = run(2)
+    u = np.concatenate([p[0][:3 * p[2]] for p in parts])
+    fl = np.concatenate([p[0][3 * p[2]:] for p in parts])
+    assert i1["status"] == "OK"
+    assert np.array_equal(np.concatenate([u, fl]), x1)
+    for p in parts:
+        assert p[1]["res_hist"] == i1["res_hist"] and p[1]["lin_hist"] == i1["lin_hist"]
