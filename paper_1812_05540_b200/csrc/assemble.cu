@@ -128,51 +128,43 @@ __global__ void k_asm_counts(AsmGeo g, int32_t *cuu, int32_t *cuf, int32_t *cff)
 }
 
 // ---------------------------------------------------------------- node rows: A_uu, A_uf
-__global__ void __launch_bounds__(128) k_asm_node(tsp_asm_params P, AsmGeo g, const Q1 *__restrict__ q,
+// One thread per node row.  The row's <= 8 elements are summarised first (Lame constants, g d(rho)/d(eps_v), the
+// node's local index a); then each of the <= 27 blocks is summed in registers over the elements shared with that
+// neighbour, in ascending element order, and written once (no read-modify-write of global memory).
+__global__ void __launch_bounds__(128) k_asm_node(tsp_asm_params P, AsmGeo g, const Q1 *q,
                                                   const double *__restrict__ E, const double *__restrict__ phi,
                                                   const double *__restrict__ sat, const double *__restrict__ pres,
                                                   const double *__restrict__ phi0,
                                                   const int32_t *__restrict__ rpu, int32_t *__restrict__ cu, double *__restrict__ vu,
-                                                  const int32_t *__restrict__ rpf, int32_t *__restrict__ cf, double *__restrict__ vf)
+                                                  const int32_t *__restrict__ rpf, int32_t *__restrict__ cf, double *__restrict__ vf,
+                                                  unsigned long long *mx)
 {
+    __shared__ Q1 qs;                                   // the Gauss tables, read ~4500 times per row
+    for (int e = threadIdx.x; e < (int)(sizeof(Q1) / sizeof(double)); e += blockDim.x)
+        ((double *)&qs)[e] = ((const double *)q)[e];
+    __syncthreads();
+    q = &qs;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= g.nn) return;
+    double rowmax = 0.0;                                // max over d of the row's l1 norm (R-scale), fused
+    if (t < g.nn) {
     const int NX = g.nx + 1, NY = g.ny + 1;
     const int64_t n = g.node0 + t;
     const int i = n % NX, j = (n / NX) % NY, k = n / ((int64_t)NX * NY);
     const double gr = P.gravity, b = P.biot;
-    // columns: the clipped 27 neighbours in ascending id (z, then y, then x offsets), the <= 8 adjacent cells likewise
-    int slot27[27];
-    int64_t qu = rpu[t];
-    for (int o = 0; o < 27; ++o) {
-        const int ii = i + o % 3 - 1, jj = j + (o / 3) % 3 - 1, kk = k + o / 9 - 1;
-        if (ii < 0 || ii > g.nx || jj < 0 || jj > g.ny || kk < 0 || kk > g.nz) { slot27[o] = -1; continue; }
-        slot27[o] = (int)(qu - rpu[t]);
-        cu[qu] = (int32_t)(ii + (int64_t)NX * (jj + (int64_t)NY * kk));
-        for (int e = 0; e < 9; ++e) vu[9 * qu + e] = 0.0;
-        ++qu;
-    }
+    // the adjacent elements o = (i-1+ox, j-1+oy, k-1+oz): presence, Lame constants, g d(rho)/d(eps_v); A_uf entries
+    double lam[8], mu[8], gde[8];
+    unsigned present = 0;
     int64_t qf = rpf[t];
-    for (int o = 0; o < 8; ++o) {          // adjacent element (i-1+ox, j-1+oy, k-1+oz)
+    for (int o = 0; o < 8; ++o) {
         const int ci = i - 1 + (o & 1), cj = j - 1 + ((o >> 1) & 1), ck = k - 1 + ((o >> 2) & 1);
+        lam[o] = mu[o] = gde[o] = 0.0;
         if (ci < 0 || ci >= g.nx || cj < 0 || cj >= g.ny || ck < 0 || ck >= g.nz) continue;
+        present |= 1u << o;
         const int64_t c = ci + (int64_t)g.nx * (cj + (int64_t)g.ny * ck);
-        cf[qf] = (int32_t)c;
         const CellSt C = cell_st(P, g, c, E, phi, sat, pres, phi0);
-        const int a = (1 - (o & 1)) + 2 * (1 - ((o >> 1) & 1)) + 4 * (1 - ((o >> 2) & 1));   // node n inside element c
-        for (int bl = 0; bl < 8; ++bl) {
-            // node m = corner bl of element c; its offset from n picks the block
-            const int dx = (bl & 1) - (a & 1), dy = ((bl >> 1) & 1) - ((a >> 1) & 1), dz = ((bl >> 2) & 1) - ((a >> 2) & 1);
-            double *B = vu + 9 * (rpu[t] + slot27[(dz + 1) * 9 + (dy + 1) * 3 + (dx + 1)]);
-            const double tr = q->KK[a][bl][0][0] + q->KK[a][bl][1][1] + q->KK[a][bl][2][2];
-            for (int d = 0; d < 3; ++d)
-                for (int e = 0; e < 3; ++e) {
-                    double v = C.lam * q->KK[a][bl][d][e] + C.mu * q->KK[a][bl][e][d];
-                    if (d == e) v += C.mu * tr;
-                    if (d == 2) v += gr * C.drho_de * q->NB[a][bl][e];
-                    B[3 * d + e] += v;
-                }
-        }
+        lam[o] = C.lam; mu[o] = C.mu; gde[o] = gr * C.drho_de;
+        const int a = (1 - (o & 1)) + 2 * (1 - ((o >> 1) & 1)) + 4 * (1 - ((o >> 2) & 1));   // node n inside element o
+        cf[qf] = (int32_t)c;
         double *F = vf + 6 * qf;
         for (int d = 0; d < 3; ++d) {
             F[2 * d] = d == 2 ? gr * C.drho_ds * q->NI[a] : 0.0;
@@ -180,6 +172,48 @@ __global__ void __launch_bounds__(128) k_asm_node(tsp_asm_params P, AsmGeo g, co
         }
         ++qf;
     }
+    // the clipped 27 neighbours m = n + (dx, dy, dz), ascending id; block (n, m) sums the elements holding both
+    int64_t qu = rpu[t];
+    double rs[3] = {0.0, 0.0, 0.0};
+    for (int dz = -1; dz <= 1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int ii = i + dx, jj = j + dy, kk = k + dz;
+                if (ii < 0 || ii > g.nx || jj < 0 || jj > g.ny || kk < 0 || kk > g.nz) continue;
+                double B[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+                for (int o = 0; o < 8; ++o) {
+                    if (!((present >> o) & 1u)) continue;
+                    // element o spans nodes i-1+ox .. i+ox (per axis): it holds m iff each offset lies in its span
+                    const int ox = o & 1, oy = (o >> 1) & 1, oz = (o >> 2) & 1;
+                    const int bx = dx + 1 - ox, by = dy + 1 - oy, bz = dz + 1 - oz;   // m's local coordinates
+                    if (bx < 0 || bx > 1 || by < 0 || by > 1 || bz < 0 || bz > 1) continue;
+                    const int a = (1 - ox) + 2 * (1 - oy) + 4 * (1 - oz), bl = bx + 2 * by + 4 * bz;
+                    const double tr = q->KK[a][bl][0][0] + q->KK[a][bl][1][1] + q->KK[a][bl][2][2];
+                    for (int d = 0; d < 3; ++d)
+                        for (int e = 0; e < 3; ++e) {
+                            double v = lam[o] * q->KK[a][bl][d][e] + mu[o] * q->KK[a][bl][e][d];
+                            if (d == e) v += mu[o] * tr;
+                            if (d == 2) v += gde[o] * q->NB[a][bl][e];
+                            B[3 * d + e] += v;
+                        }
+                }
+                cu[qu] = (int32_t)(ii + (int64_t)NX * (jj + (int64_t)NY * kk));
+                for (int e = 0; e < 9; ++e) vu[9 * qu + e] = B[e];
+                for (int d = 0; d < 3; ++d)
+                    for (int e = 0; e < 3; ++e) rs[d] += fabs(B[3 * d + e]);
+                ++qu;
+            }
+    rowmax = fmax(rs[0], fmax(rs[1], rs[2]));
+    }
+    // values >= 0: their bit patterns order like the values; one atomic per warp
+    for (int o = 16; o; o >>= 1) rowmax = fmax(rowmax, __shfl_xor_sync(0xffffffffu, rowmax, o));
+    if ((threadIdx.x & 31) == 0 && rowmax > 0) atomicMax(mx, (unsigned long long)__double_as_longlong(rowmax));
+}
+
+__global__ void k_asm_fu_rowptr(int ncl, int32_t *rp)
+{
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c <= ncl) rp[c] = 8 * c;
 }
 
 // ---------------------------------------------------------------- cell rows: A_fu, A_ff, wells, D_fs
@@ -189,10 +223,11 @@ __global__ void __launch_bounds__(128) k_asm_cell(tsp_asm_params P, AsmGeo g, co
                                                   const double *__restrict__ pres, const int8_t *__restrict__ well,
                                                   const double *__restrict__ phi0, int32_t *__restrict__ cfu, double *__restrict__ vfu,
                                                   const int32_t *__restrict__ rpf, int32_t *__restrict__ cff, double *__restrict__ vff,
-                                                  double *__restrict__ fs)
+                                                  double *__restrict__ fs, unsigned long long *mx)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= g.ncl) return;
+    double ms = 0.0, mp = 0.0;                          // the row's l1 norms of A_ss and A_pp entries (R-scale), fused
+    if (t < g.ncl) {
     const int NX = g.nx + 1, NY = g.ny + 1;
     const int64_t c = g.cell0 + t, P2 = (int64_t)g.nx * g.ny;
     const int i = c % g.nx, j = (c / g.nx) % g.ny, k = c / P2;
@@ -296,66 +331,55 @@ __global__ void __launch_bounds__(128) k_asm_cell(tsp_asm_params P, AsmGeo g, co
     // fixed-stress diagonals (eq:FS_Dps_Dpp), in p-column units
     fs[2 * t] = V * b * b / K.Kdr * K.s * K.rw * pu;
     fs[2 * t + 1] = V * b * b / K.Kdr * (1 - K.s) * K.rn * pu;
-}
-
-// ---------------------------------------------------------------- row maxima of the l1 norms (R-scale)
-// u: sum_{q, e} |A_uu[q][d][e]| per node row d; s: sum_q |A_ss|; p: sum_q |A_pp| (the reference's measure)
-__global__ void k_asm_rowmax(AsmGeo g, const int32_t *__restrict__ rpu, const double *__restrict__ vu,
-                             const int32_t *__restrict__ rpf, const double *__restrict__ vff, unsigned long long *mx)
-{
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    double mu_ = 0, ms = 0, mp = 0;
-    if (t < g.nn)
-        for (int d = 0; d < 3; ++d) {
-            double s = 0;
-            for (int64_t q = rpu[t]; q < rpu[t + 1]; ++q)
-                for (int e = 0; e < 3; ++e) s += fabs(vu[9 * q + 3 * d + e]);
-            mu_ = fmax(mu_, s);
-        }
-    if (t < g.ncl) {
-        for (int64_t q = rpf[t]; q < rpf[t + 1]; ++q) { ms += fabs(vff[4 * q]); mp += fabs(vff[4 * q + 3]); }
+    for (int u = 0; u < np; ++u) { ms += fabs(vff[4 * (r0 + u)]); mp += fabs(vff[4 * (r0 + u) + 3]); }
     }
-    // values >= 0: their bit patterns order like the values
-    if (mu_ > 0) atomicMax(mx + 0, (unsigned long long)__double_as_longlong(mu_));
-    if (ms > 0) atomicMax(mx + 1, (unsigned long long)__double_as_longlong(ms));
-    if (mp > 0) atomicMax(mx + 2, (unsigned long long)__double_as_longlong(mp));
+    for (int o = 16; o; o >>= 1) {
+        ms = fmax(ms, __shfl_xor_sync(0xffffffffu, ms, o));
+        mp = fmax(mp, __shfl_xor_sync(0xffffffffu, mp, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (ms > 0) atomicMax(mx + 1, (unsigned long long)__double_as_longlong(ms));
+        if (mp > 0) atomicMax(mx + 2, (unsigned long long)__double_as_longlong(mp));
+    }
 }
 
 // ---------------------------------------------------------------- scaling + Dirichlet rows (R-scale, R-dirichlet)
-__global__ void k_asm_scale_nodes(AsmGeo g, double su, int dirichlet, const int32_t *__restrict__ rpu, const int32_t *__restrict__ cu,
-                                  double *__restrict__ vu, const int32_t *__restrict__ rpf, double *__restrict__ vf)
+// elementwise over the value arrays (coalesced); `qfix`: the entries of the rank's fixed (bottom) rows, [0, rp[nfix])
+__global__ void k_scale_uu(int64_t nv, double su, int dirichlet, int64_t nbot, const int32_t *__restrict__ rpu, int nfix,
+                           const int32_t *__restrict__ cu, double *__restrict__ vu)
 {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= g.nn) return;
-    const int64_t nbot = (int64_t)(g.nx + 1) * (g.ny + 1), n = g.node0 + t;
-    const bool fixed_row = dirichlet && n < nbot;
-    for (int64_t q = rpu[t]; q < rpu[t + 1]; ++q) {
-        const bool fixed_col = dirichlet && cu[q] < nbot;
-        for (int e = 0; e < 9; ++e) vu[9 * q + e] = (fixed_row || fixed_col) ? 0.0 : vu[9 * q + e] * su;
-        if (fixed_row && cu[q] == n) { vu[9 * q] = 1.0; vu[9 * q + 4] = 1.0; vu[9 * q + 8] = 1.0; }
-    }
-    for (int64_t q = rpf[t]; q < rpf[t + 1]; ++q)
-        for (int e = 0; e < 6; ++e) vf[6 * q + e] = fixed_row ? 0.0 : vf[6 * q + e] * su;
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= nv) return;
+    const int64_t q = idx / 9;
+    const bool fixed = dirichlet && (q < rpu[nfix] || cu[q] < nbot);
+    vu[idx] = fixed ? 0.0 : vu[idx] * su;
 }
-__global__ void k_asm_scale_cells(AsmGeo g, double ss, double sp, int dirichlet, const int32_t *__restrict__ cfu,
-                                  double *__restrict__ vfu, const int32_t *__restrict__ rpf, double *__restrict__ vff,
-                                  double *__restrict__ fs)
+__global__ void k_fix_diag(int nfix, int64_t node0, const int32_t *__restrict__ rpu, const int32_t *__restrict__ cu, double *__restrict__ vu)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= g.ncl) return;
-    const int64_t nbot = (int64_t)(g.nx + 1) * (g.ny + 1);
-    for (int a = 0; a < 8; ++a) {
-        const int64_t q = 8 * (int64_t)t + a;
-        const bool fixed_col = dirichlet && cfu[q] < nbot;
-        for (int d = 0; d < 3; ++d) {
-            vfu[6 * q + d] = fixed_col ? 0.0 : vfu[6 * q + d] * ss;
-            vfu[6 * q + 3 + d] = fixed_col ? 0.0 : vfu[6 * q + 3 + d] * sp;
-        }
-    }
-    for (int64_t q = rpf[t]; q < rpf[t + 1]; ++q) {
-        vff[4 * q] *= ss; vff[4 * q + 1] *= ss; vff[4 * q + 2] *= sp; vff[4 * q + 3] *= sp;
-    }
-    fs[2 * t] *= ss; fs[2 * t + 1] *= sp;
+    if (t >= nfix) return;
+    for (int64_t q = rpu[t]; q < rpu[t + 1]; ++q)
+        if (cu[q] == node0 + t) { vu[9 * q] = 1.0; vu[9 * q + 4] = 1.0; vu[9 * q + 8] = 1.0; }
+}
+__global__ void k_scale_uf(int64_t nv, double su, const int32_t *__restrict__ rpf, int nfix, double *__restrict__ vf)
+{
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= nv) return;
+    vf[idx] = idx / 6 < rpf[nfix] ? 0.0 : vf[idx] * su;
+}
+__global__ void k_scale_fu(int64_t nv, double ss, double sp, int dirichlet, int64_t nbot, const int32_t *__restrict__ cfu,
+                           double *__restrict__ v)
+{
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= nv) return;
+    const int64_t q = idx / 6;
+    v[idx] = (dirichlet && cfu[q] < nbot) ? 0.0 : v[idx] * ((idx % 6) < 3 ? ss : sp);
+}
+__global__ void k_scale_ff(int64_t nv, double ss, double sp, double *__restrict__ v, int64_t nfs, double *__restrict__ fs)
+{
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx < nv) v[idx] *= (idx & 3) < 2 ? ss : sp;
+    if (idx < nfs) fs[idx] *= (idx & 1) ? sp : ss;
 }
 
 // ---------------------------------------------------------------- residual of Appendix B.1, raw units
@@ -591,22 +615,26 @@ static AsmGeo asm_geo(const tsp_asm_params &P, int rank, int nranks, int zblock)
     return g;
 }
 
+// block counts of this rank's rows: the per-node and per-cell counts factor over the axes, so the sums do too
 void assembly_sizes(const tsp_asm_params &P, int rank, int nranks, int zblock, int64_t out[6])
 {
     const AsmGeo g = asm_geo(P, rank, nranks, zblock);
     const int NX = P.nx + 1, NY = P.ny + 1;
-    int64_t buu = 0, buf = 0, bff = 0;
-    std::vector<int> cx(NX), cy(NY);   // per-coordinate factors, summed plane by plane
-    for (int64_t n = g.node0; n < g.node0 + g.nn; ++n) {
-        const int i = n % NX, j = (n / NX) % NY, k = n / ((int64_t)NX * NY);
-        const int ex = (i > 0) + (i < P.nx), ey = (j > 0) + (j < P.ny), ez = (k > 0) + (k < P.nz);
-        buu += (1 + ex) * (1 + ey) * (1 + ez);
-        buf += ex * ey * ez;
-    }
-    for (int64_t c = g.cell0; c < g.cell0 + g.ncl; ++c) {
-        const int i = c % P.nx, j = (c / P.nx) % P.ny, k = c / ((int64_t)P.nx * P.ny);
-        bff += 1 + (i > 0) + (i < P.nx - 1) + (j > 0) + (j < P.ny - 1) + (k > 0) + (k < P.nz - 1);
-    }
+    auto e1 = [](int i, int n) { return (int64_t)((i > 0) + (i < n)); };          // adjacent cells along an axis
+    int64_t sx1 = 0, sx0 = 0, sy1 = 0, sy0 = 0, sz1 = 0, sz0 = 0;
+    for (int i = 0; i < NX; ++i) { sx1 += 1 + e1(i, P.nx); sx0 += e1(i, P.nx); }
+    for (int j = 0; j < NY; ++j) { sy1 += 1 + e1(j, P.ny); sy0 += e1(j, P.ny); }
+    const int64_t kn0 = g.node0 / ((int64_t)NX * NY), kn1 = kn0 + g.nn / ((int64_t)NX * NY);
+    for (int64_t k = kn0; k < kn1; ++k) { sz1 += 1 + e1((int)k, P.nz); sz0 += e1((int)k, P.nz); }
+    const int64_t buu = sx1 * sy1 * sz1, buf = sx0 * sy0 * sz0;
+    // cells: 1 + neighbours along x, y, z
+    const int64_t P2 = (int64_t)P.nx * P.ny, kc0 = g.cell0 / P2, nzl = g.ncl / P2;
+    auto nb = [](int64_t i, int64_t n) { return (int64_t)((i > 0) + (i < n - 1)); };
+    int64_t fx = 0, fy = 0, fz = 0;
+    for (int i = 0; i < P.nx; ++i) fx += nb(i, P.nx);
+    for (int j = 0; j < P.ny; ++j) fy += nb(j, P.ny);
+    for (int64_t k = kc0; k < kc0 + nzl; ++k) fz += nb(k, P.nz);
+    const int64_t bff = g.ncl + fx * P.ny * nzl + fy * P.nx * nzl + fz * P2;
     out[0] = g.nn; out[1] = g.ncl; out[2] = buu; out[3] = buf; out[4] = 8 * (int64_t)g.ncl; out[5] = bff;
 }
 
@@ -637,18 +665,12 @@ void assemble(cudaStream_t s, const tsp_asm_params &P, int rank, int nranks, int
     scan(cuu, g.nn, blk[0].rowptr);
     scan(cuf, g.nn, blk[1].rowptr);
     scan(cff, g.ncl, blk[3].rowptr);
-    {   // A_fu: 8 nodes per cell
-        std::vector<int32_t> rp(g.ncl + 1);
-        for (int c = 0; c <= g.ncl; ++c) rp[c] = 8 * c;
-        TSP_CUDA(cudaMemcpyAsync(blk[2].rowptr, rp.data(), sizeof(int32_t) * (g.ncl + 1), cudaMemcpyHostToDevice, s));
-        TSP_CUDA(cudaStreamSynchronize(s));   // rp is a host temporary
-    }
-    if (g.nn) k_asm_node<<<grid_for(g.nn, 128), 128, 0, s>>>(P, g, dq.p, f.E, f.phi, f.sat, f.pres, f.phi0, blk[0].rowptr, blk[0].col,
-                                                            blk[0].val, blk[1].rowptr, blk[1].col, blk[1].val);
-    if (g.ncl) k_asm_cell<<<grid_for(g.ncl, 128), 128, 0, s>>>(P, g, dq.p, f.E, f.perm, f.phi, f.sat, f.pres, f.well, f.phi0, blk[2].col,
-                                                              blk[2].val, blk[3].rowptr, blk[3].col, blk[3].val, fs);
+    k_asm_fu_rowptr<<<grid_for(g.ncl + 1, 256), 256, 0, s>>>(g.ncl, blk[2].rowptr);   // A_fu: 8 nodes per cell
     DBuf<unsigned long long> mx; mx.alloc(3); mx.zero(s);
-    if (m) k_asm_rowmax<<<grid_for(m, 256), 256, 0, s>>>(g, blk[0].rowptr, blk[0].val, blk[3].rowptr, blk[3].val, mx);
+    if (g.nn) k_asm_node<<<grid_for(g.nn, 128), 128, 0, s>>>(P, g, dq.p, f.E, f.phi, f.sat, f.pres, f.phi0, blk[0].rowptr, blk[0].col,
+                                                            blk[0].val, blk[1].rowptr, blk[1].col, blk[1].val, mx.p);
+    if (g.ncl) k_asm_cell<<<grid_for(g.ncl, 128), 128, 0, s>>>(P, g, dq.p, f.E, f.perm, f.phi, f.sat, f.pres, f.well, f.phi0, blk[2].col,
+                                                              blk[2].val, blk[3].rowptr, blk[3].col, blk[3].val, fs, mx.p);
     TSP_CUDA(cudaGetLastError());
     unsigned long long hb[3];
     TSP_CUDA(cudaMemcpyAsync(hb, mx.p, sizeof(hb), cudaMemcpyDeviceToHost, s));
@@ -663,10 +685,16 @@ void assemble_scale(cudaStream_t s, const tsp_asm_params &P, int rank, int nrank
     double sc[3] = {1.0, 1.0, 1.0};
     if (P.row_scale)
         for (int k = 0; k < 3; ++k) sc[k] = row_max[k] > 0 ? 1.0 / row_max[k] : 1.0;
-    if (g.nn) k_asm_scale_nodes<<<grid_for(g.nn, 128), 128, 0, s>>>(g, sc[0], P.dirichlet_bottom, blk[0].rowptr, blk[0].col,
-                                                                   blk[0].val, blk[1].rowptr, blk[1].val);
-    if (g.ncl) k_asm_scale_cells<<<grid_for(g.ncl, 128), 128, 0, s>>>(g, sc[1], sc[2], P.dirichlet_bottom, blk[2].col, blk[2].val,
-                                                                     blk[3].rowptr, blk[3].val, fs);
+    int64_t sz[6];
+    assembly_sizes(P, rank, nranks, zblock, sz);
+    const int64_t nbot = (int64_t)(P.nx + 1) * (P.ny + 1);
+    const int nfix = P.dirichlet_bottom ? (int)std::max<int64_t>(0, std::min<int64_t>(nbot - g.node0, g.nn)) : 0;
+    const int64_t vuu = 9 * sz[2], vuf = 6 * sz[3], vfu = 6 * sz[4], vff = 4 * sz[5], nfs = 2 * (int64_t)g.ncl;
+    if (vuu) k_scale_uu<<<grid_for(vuu, 256), 256, 0, s>>>(vuu, sc[0], P.dirichlet_bottom, nbot, blk[0].rowptr, nfix, blk[0].col, blk[0].val);
+    if (nfix) k_fix_diag<<<grid_for(nfix, 128), 128, 0, s>>>(nfix, g.node0, blk[0].rowptr, blk[0].col, blk[0].val);
+    if (vuf) k_scale_uf<<<grid_for(vuf, 256), 256, 0, s>>>(vuf, sc[0], blk[1].rowptr, nfix, blk[1].val);
+    if (vfu) k_scale_fu<<<grid_for(vfu, 256), 256, 0, s>>>(vfu, sc[1], sc[2], P.dirichlet_bottom, nbot, blk[2].col, blk[2].val);
+    if (std::max(vff, nfs)) k_scale_ff<<<grid_for(std::max(vff, nfs), 256), 256, 0, s>>>(vff, sc[1], sc[2], blk[3].val, nfs, fs);
     TSP_CUDA(cudaGetLastError());
     TSP_CUDA(cudaStreamSynchronize(s));
     if (scales) for (int k = 0; k < 3; ++k) scales[k] = sc[k];

@@ -113,8 +113,14 @@ __global__ void __launch_bounds__(KB) k_mdot(int nv, const double *__restrict__ 
 // DCGS2 pass 1: part[t] = V_t . u, part[nv + t] = V_t . w for t < nv (V_{nv-1} is u itself), per chunk.
 // u and w chunks staged interleaved in shared memory (one 16-B load per row); KG2 vectors per group,
 // rows unrolled by 2, both products share each V load.
-constexpr int KG2 = 4;
-__global__ void __launch_bounds__(KB) k_mdot2(int nv, const double *__restrict__ V, int64_t ldv, const double *__restrict__ u,
+#ifndef TSP_KG2
+#define TSP_KG2 4
+#endif
+#ifndef TSP_MDOT2_MINB
+#define TSP_MDOT2_MINB 1
+#endif
+constexpr int KG2 = TSP_KG2;
+__global__ void __launch_bounds__(KB, TSP_MDOT2_MINB) k_mdot2(int nv, const double *__restrict__ V, int64_t ldv, const double *__restrict__ u,
                                               const double *__restrict__ w, const int64_t *__restrict__ be,
                                               double *__restrict__ part, int cmax)
 {
