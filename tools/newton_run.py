@@ -34,14 +34,16 @@ x = torch.from_numpy(x0).to(dev)
 torch.cuda.synchronize()
 t0 = time.perf_counter()
 ap = assemble(prm, dict(f, phi0=f["phi"]))
-g = Tsp(ap)
+# NEWTON_OPTS=amg_smoother=2,local_sweeps=2 : library options of the handle (e.g. the fastest linear variant)
+hopts = {k: int(v) for k, v in (kv.split("=") for kv in filter(None, os.environ.get("NEWTON_OPTS", "").split(",")))}
+g = Tsp(ap, **hopts)
 del ap
 g.setup(1)                                   # mechanics AMG once per simulation
 m0 = masses(prm, ref, x)
 r_off = residual(prm, ref, x, m0, prm["dt"])[:3 * Nn].contiguous()
 torch.cuda.synchronize()
 t_init = time.perf_counter() - t0
-print(json.dumps({"config": cfg, "dof": s["n"], "init_s": t_init}), flush=True)
+print(json.dumps({"config": cfg, "dof": s["n"], "init_s": t_init, "options": hopts}), flush=True)
 dbhp, t_sim, dt, tot_newton, tot_lin, t_all = prm["well_dbhp"], 0.0, dt0, 0, 0, 0.0
 for step in range(nsteps):
     p_step = dict(prm, well_dbhp=dbhp * min(1.0, (step + 1) / ramp))
