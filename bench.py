@@ -418,11 +418,12 @@ def main():
     g.close()
     torch.cuda.empty_cache()
 
-    # ---- time to solution of the fastest measured variant (Chebyshev(2) AMG smoothers, R-cheb, and two
-    # sweeps of the second stage); the headline above stays the default configuration.  Device-timed: setup + solve.
+    # ---- time to solution of the fastest measured variant (Chebyshev(2) smoother on [0.1, 1] in the
+    # mechanics AMG only, R-cheb, and two sweeps of the second stage); the headline above stays the default
+    # configuration.  Device-timed: setup + solve.
     variants = {}
     if not args.no_variants and not lib_opts:
-        vopts = dict(amg_smoother=2, local_sweeps=2)
+        vopts = dict(amg_smoother=2, amg_smoother_p=0, amg_cheb_lower=0.1, local_sweeps=2)
         try:
             gv_ = Tsp(src, **new_topo(), **vopts)
             xv = torch.zeros(n, dtype=torch.float64, device=dev)
@@ -441,7 +442,7 @@ def main():
                 res.append((v0.elapsed_time(v1), v1.elapsed_time(v2), inf))
             gv_.close()
             su, so, inf = res[-1]
-            variants["cheb2_ilu2"] = {"options": vopts, "iterations": inf["iterations"], "status": inf["status"],
+            variants["mech_cheb2_ilu2"] = {"options": vopts, "iterations": inf["iterations"], "status": inf["status"],
                                       "true_relres": inf["true_relres"], "setup_ms": su, "solve_ms": so,
                                       "step_ms": su + so, "iters_per_s": inf["iterations"] / ((su + so) * 1e-3),
                                       "default_step_ms": ms_max / args.steps}

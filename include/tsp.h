@@ -90,6 +90,7 @@ typedef struct {
        [amg_cheb_lower, 1] (1 = the l1 bound of the spectrum); multi-GPU capable */
     int amg_cheb_degree;         /* default 2, range [1, 8] */
     double amg_cheb_lower;       /* default 0.3, range (0, 1) */
+    int amg_smoother_p;          /* smoother of the pressure hierarchy only: -1 (default) = amg_smoother, else 0/1/2 */
 } tsp_options;
 
 /* BSR block matrix given to tsp_create (nrows block rows). */

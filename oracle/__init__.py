@@ -37,7 +37,7 @@ class Opts(C.Structure):
                 ("cpr_mode", C.c_int), ("aps_mode", C.c_int), ("fs_mode", C.c_int), ("rsl_iters", C.c_int),
                 ("fs_modulus_scale", C.c_double), ("second_stage", C.c_int), ("local_sweeps", C.c_int),
                 ("amg_smoother", C.c_int), ("amg_gs_block", C.c_int), ("amg_cheb_degree", C.c_int),
-                ("amg_cheb_lower", C.c_double)]
+                ("amg_cheb_lower", C.c_double), ("amg_smoother_p", C.c_int)]
 
 
 class Phys(C.Structure):

@@ -992,6 +992,7 @@ void orc_default_opts(orc_opts *o)
     o->second_stage = 0; o->local_sweeps = 1;
     o->amg_smoother = 0; o->amg_gs_block = 1024;
     o->amg_cheb_degree = 2; o->amg_cheb_lower = 0.3;
+    o->amg_smoother_p = -1;
 }
 
 orc *orc_create(const orc_desc *d, const orc_opts *o)
@@ -1204,7 +1205,9 @@ int orc_setup_flow(orc *h, int refresh)
         /* R-gs: level-0 cell colour = parity of x + y + z (red-black on the 7-point pattern of S_pp) */
         int32_t *col0 = (int32_t *)xmalloc(sizeof(int32_t) * Nc);
         for (int c = 0; c < Nc; ++c) col0[c] = (c % h->nx + (c / h->nx) % h->ny + c / (h->nx * h->ny)) & 1;
-        h->pres = amg_build(&h->Spp, zb, col0, &h->o);
+        orc_opts po = h->o;                   /* the pressure hierarchy's own smoother (amg_smoother_p) */
+        if (po.amg_smoother_p >= 0) po.amg_smoother = po.amg_smoother_p;
+        h->pres = amg_build(&h->Spp, zb, col0, &po);
         free(zb); free(col0);
         if (!h->pres) return -3;
     } else {

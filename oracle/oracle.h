@@ -48,6 +48,7 @@ typedef struct {
     /* amg_smoother 2: Chebyshev polynomial smoother (north_star "Jacobi/Chebyshev"; reading R-cheb) */
     int amg_cheb_degree;          /* polynomial degree per smoothing step (2) */
     double amg_cheb_lower;        /* interval [lower, 1] of D_l1^-1 A (the l1 bound makes 1 the upper end), 0.3 */
+    int amg_smoother_p;           /* smoother of the pressure hierarchy only (-1: amg_smoother) */
 } orc_opts;
 
 typedef struct {

@@ -826,6 +826,7 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
                bool refresh)
 {
     dbg_mark(c, "start", -1);
+    H.smoother = (nc == 1 && c.o.amg_smoother_p >= 0) ? c.o.amg_smoother_p : c.o.amg_smoother;
     if (refresh) {
         TSP_REQUIRE(!H.L.empty() && H.nc == nc && H.L[0].A.n == A0.n && H.L[0].A.nnz == A0.nnz, TSP_ERR_STATE,
                     "refresh: no hierarchy of this pattern to refresh");
@@ -1034,7 +1035,7 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
         }
         size_t m = (size_t)std::max(L.n, 1) * nc;
         L.b.alloc(m); L.x.alloc(m); L.x2.alloc(m); L.r.alloc(m);
-        if (c.o.amg_smoother == 2) { L.dcheb.alloc(m); L.xc.alloc(m); } else { L.dcheb.release(); L.xc.release(); }
+        if (H.smoother == 2) { L.dcheb.alloc(m); L.xc.alloc(m); } else { L.dcheb.release(); L.xc.release(); }
         {   // kernel choice from global mean row lengths, so every rank computes a row exactly like P = 1
             std::vector<int64_t> st = {L.A.nnz, (int64_t)L.n, L.coarsest ? 0 : L.R.nnz, L.coarsest ? 0 : (int64_t)L.R.n};
             if (L.dist) {
@@ -1401,8 +1402,8 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     const bool sym0 = mech && l == 0 && c.sym_sdc.ok;     // structured symmetric level 0 (sym.cu)
     const bool p70 = !mech && l == 0 && c.p7_ok;          // structured 7-point pressure level 0 (p7.cu)
     const double bA0 = sym0 ? sym_bytes(c, 3) : p70 ? p7_bytes(c) : bA;
-    const bool gs = c.o.amg_smoother == 1;   // Gauss-Seidel (gs.cu, R-gs): single GPU, never distributed
-    const bool cheb = c.o.amg_smoother == 2; // Chebyshev (R-cheb)
+    const bool gs = H.smoother == 1;         // Gauss-Seidel (gs.cu, R-gs): single GPU, never distributed
+    const bool cheb = H.smoother == 2;       // Chebyshev (R-cheb)
     const int deg = c.o.amg_cheb_degree;
     prof_begin(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P);
     if (gs) {

@@ -213,6 +213,7 @@ tsp_status tsp_default_options(tsp_options *o)
     o->second_stage = 0; o->local_sweeps = 1;
     o->amg_smoother = 0; o->amg_gs_block = 1024;
     o->amg_cheb_degree = 2; o->amg_cheb_lower = 0.3;
+    o->amg_smoother_p = -1;
     return TSP_OK;
 }
 
@@ -251,6 +252,8 @@ tsp_status tsp_create(tsp_handle *out, const tsp_desc *d)
     if (c->o.amg_gs_block <= 0) c->o.amg_gs_block = 1024;
     TSP_REQUIRE(c->o.amg_smoother >= 0 && c->o.amg_smoother <= 2, TSP_ERR_INVALID_ARG,
                 "amg_smoother must be 0 (l1-Jacobi), 1 (GS) or 2 (Chebyshev)");
+    TSP_REQUIRE(c->o.amg_smoother_p >= -1 && c->o.amg_smoother_p <= 2, TSP_ERR_INVALID_ARG,
+                "amg_smoother_p must be -1 (as amg_smoother), 0, 1 or 2");
     if (c->o.amg_cheb_degree == 0) c->o.amg_cheb_degree = 2;
     if (c->o.amg_cheb_lower == 0.0) c->o.amg_cheb_lower = 0.3;
     TSP_REQUIRE(c->o.amg_cheb_degree >= 1 && c->o.amg_cheb_degree <= 8, TSP_ERR_INVALID_ARG, "amg_cheb_degree must be in [1, 8]");
@@ -541,7 +544,7 @@ tsp_status tsp_export_colour(tsp_handle h, int which, int lvl, int32_t *colour, 
     Hier &H = which ? h->pres : h->mech;
     TSP_REQUIRE(lvl >= 0 && lvl < (int)H.L.size(), TSP_ERR_INVALID_ARG, "no such level");
     const Level &L = H.L[lvl];
-    TSP_REQUIRE(h->o.amg_smoother == 1 && !L.coarsest, TSP_ERR_STATE, "no Gauss-Seidel colouring on this level");
+    TSP_REQUIRE(H.smoother == 1 && !L.coarsest, TSP_ERR_STATE, "no Gauss-Seidel colouring on this level");
     if (block) *block = L.gs_block;
     if (ncolour) *ncolour = L.ncolor;
     if (colour) gs_export_colour(*h, L, colour);

@@ -338,7 +338,7 @@ static void gs_setup_hybrid(Ctx &c, Level &L, int nc)
 
 void gs_setup(Ctx &c, Hier &H, int nc)
 {
-    if (c.o.amg_smoother != 1) return;
+    if (H.smoother != 1) return;
     TSP_REQUIRE(c.nranks == 1, TSP_ERR_INVALID_ARG, "amg_smoother = 1 (Gauss-Seidel) is single-GPU only");
     TSP_REQUIRE(c.o.amg_gs_block >= 32 && c.o.amg_gs_block <= kGsMaxBlock, TSP_ERR_INVALID_ARG, "amg_gs_block must be in [32, 1024]");
     for (size_t l = 0; l < H.L.size(); ++l) {

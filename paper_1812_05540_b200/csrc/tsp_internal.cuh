@@ -244,6 +244,7 @@ struct Level {
 
 struct Hier {
     int nc = 1;
+    int smoother = 0;                  // 0 l1-Jacobi, 1 Gauss-Seidel, 2 Chebyshev (options, per hierarchy)
     std::vector<Level> L;
     int64_t fallbacks = 0, perturbed = 0;
 };

@@ -19,6 +19,8 @@ PROBLEMS = {
     "C2": (dict(config="C2"), {}),
     "R1": (dict(nx=19, ny=7, nz=21, recipe=2, perm_sigma=2.0), {}),
     "ST1": (dict(config="ST1"), {}),
+    "C2-pressure-only": (dict(config="C2"), dict(amg_smoother=0, amg_smoother_p=2)),
+    "R1-mech-only": (dict(nx=19, ny=7, nz=21, recipe=2, perm_sigma=2.0), dict(amg_smoother_p=0)),
 }
 
 
@@ -39,7 +41,7 @@ def test_cheb_parity(dev, name):
     kw, extra = PROBLEMS[name]
     kw = dict(kw)
     pb = synth.generate(kw.pop("config", None), **kw)
-    opts = dict(amg_smoother=2, **extra)
+    opts = {"amg_smoother": 2, **extra}
     o = oracle.Oracle(pb, **opts).setup()
     g = Tsp(pb, **opts).setup()
     rng = np.random.default_rng(5)

@@ -21,6 +21,14 @@ VARIANTS = [
     ("Chebyshev(3) AMG smoothers", dict(amg_smoother=2, amg_cheb_degree=3)),
     ("Chebyshev(2) on [0.1, 1]", dict(amg_smoother=2, amg_cheb_lower=0.1)),
     ("Chebyshev(2) AMG smoothers + ILU x2", dict(amg_smoother=2, local_sweeps=2)),
+    ("Chebyshev(2) pressure AMG only", dict(amg_smoother=0, amg_smoother_p=2)),
+    ("Chebyshev(2) pressure AMG only + ILU x2", dict(amg_smoother=0, amg_smoother_p=2, local_sweeps=2)),
+    ("Chebyshev(3) pressure AMG only", dict(amg_smoother=0, amg_smoother_p=2, amg_cheb_degree=3)),
+    ("Chebyshev(2) mechanics AMG only", dict(amg_smoother=2, amg_smoother_p=0)),
+    ("Chebyshev(2) mechanics AMG only + ILU x2", dict(amg_smoother=2, amg_smoother_p=0, local_sweeps=2)),
+    ("Chebyshev(3) mechanics AMG only", dict(amg_smoother=2, amg_smoother_p=0, amg_cheb_degree=3)),
+    ("Chebyshev(2) [0.1,1] mechanics AMG only", dict(amg_smoother=2, amg_smoother_p=0, amg_cheb_lower=0.1)),
+    ("Chebyshev(2) mechanics AMG only + modulus 1.8", dict(amg_smoother=2, amg_smoother_p=0, fs_modulus_scale=1.8)),
 ]
 if len(sys.argv) > 2:   # only the variants whose name contains this word
     VARIANTS = [v for v in VARIANTS if sys.argv[2] in v[0]]
