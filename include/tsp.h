@@ -177,7 +177,8 @@ typedef struct {
     int64_t skipped_dss, perturbed_pivots, coarsening_fallbacks;
     double bytes_apply;          /* algorithmic bytes of one tsp_apply_preconditioner */
     double bytes_operator;       /* algorithmic bytes of one tsp_apply_operator */
-    double bytes_iter_base;      /* per FGMRES iteration excluding Gram-Schmidt: apply + operator */
+    double bytes_iter_base;      /* per FGMRES iteration excluding Gram-Schmidt: apply + the operator as FGMRES applies it
+                                    (its cell rows reuse Algorithm 1's A_fu z_u, so A_fu is not streamed twice) */
     double bytes_per_krylov_vec; /* bytes of one basis-vector pass (8 n); exact Krylov bytes: tsp_solve_info */
     int64_t allocs_callback;     /* device allocations made through tsp_desc.allocator since tsp_create */
     int64_t allocs_pool;         /* device allocations made from the library's own pool since tsp_create */

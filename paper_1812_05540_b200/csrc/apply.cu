@@ -48,18 +48,24 @@ __global__ void __launch_bounds__(256) k_op_node(int Nn, const int64_t *__restri
     yu[3 * (int64_t)i] = a0; yu[3 * (int64_t)i + 1] = a1; yu[3 * (int64_t)i + 2] = a2;
 }
 
-// cell rows: y_f = [vf -] (A_fu x_u [+ A_ff x_f]);  mode 0: operator; mode 1: step 2, y_f = v_f - A_fu z_u
+// cell rows: y_f = [vf -] (A_fu x_u [+ A_ff x_f]);  mode 0: operator; mode 1: step 2, y_f = v_f - A_fu z_u;
+// mode 2: the operator right after Algorithm 1 on the same vector -- its step 2 left y2 = v_f - A_fu z_u, so
+// A_fu z_u = v_f - y2 and only A_ff is streamed: y_f = (v_f - y2) + A_ff x_f (y2 passed in `y2`)
 template <int MODE, bool D>
 __global__ void __launch_bounds__(256) k_op_cell(int Nc, const int64_t *__restrict__ off_fu, const int32_t *__restrict__ col_fu,
                                                  const double *__restrict__ val_fu, const int64_t *__restrict__ off_ff,
                                                  const int32_t *__restrict__ col_ff, const double *__restrict__ val_ff,
-                                                 GV xu, GV xf, const double *__restrict__ vf, double *__restrict__ yf)
+                                                 GV xu, GV xf, const double *__restrict__ vf, double *__restrict__ yf,
+                                                 const double *__restrict__ y2)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= Nc) return;
     const int s = i >> 5, lane = i & 31;
     double a0 = 0, a1 = 0;
-    {
+    if (MODE == 2) {
+        a0 = vf[2 * (int64_t)i] - y2[2 * (int64_t)i];
+        a1 = vf[2 * (int64_t)i + 1] - y2[2 * (int64_t)i + 1];
+    } else {
         const int64_t b0 = off_fu[s], b1 = off_fu[s + 1];
 #pragma unroll 2
         for (int64_t slot = b0; slot < b1; ++slot) {
@@ -70,7 +76,7 @@ __global__ void __launch_bounds__(256) k_op_cell(int Nc, const int64_t *__restri
             a1 = fma(__ldcs(v + 3 * 32), x0, a1); a1 = fma(__ldcs(v + 4 * 32), x1, a1); a1 = fma(__ldcs(v + 5 * 32), x2, a1);
         }
     }
-    if (MODE == 0) {
+    if (MODE == 0 || MODE == 2) {
         const int64_t b0 = off_ff[s], b1 = off_ff[s + 1];
 #pragma unroll 2
         for (int64_t slot = b0; slot < b1; ++slot) {
@@ -131,8 +137,30 @@ void op_apply(Ctx &c, const double *x, double *y)
     prof_end(c, PK_OP_NODE, (c.sym_uu.ok ? sym_bytes(c, 9) : sell_bytes(c.s_uu)) + sell_bytes(c.s_uf) + 48.0 * c.Nn + 16.0 * c.Nc);
     prof_begin(c, PK_OP_CELL);
     if (c.Nc) (c.comm ? k_op_cell<0, true> : k_op_cell<0, false>)<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(
-        c.Nc, c.s_fu.off, c.s_fu.col, c.s_fu.val, c.s_ff.off, c.s_ff.col, c.s_ff.val, gu, gf, nullptr, yf);
+        c.Nc, c.s_fu.off, c.s_fu.col, c.s_fu.val, c.s_ff.off, c.s_ff.col, c.s_ff.val, gu, gf, nullptr, yf, nullptr);
     prof_end(c, PK_OP_CELL, sell_bytes(c.s_fu) + sell_bytes(c.s_ff) + 24.0 * c.Nn + 32.0 * c.Nc);
+    c.launches += 2;
+    TSP_CUDA(cudaGetLastError());
+}
+
+// y = A z right after z = M^-1 v (the FGMRES body): the cell rows reuse step 2's A_fu z_u (k_op_cell<2>), so A_fu
+// is streamed once per iteration instead of twice (SELL(A_fu) x 52 B = 3.5 GB at C5)
+void op_apply_after_prec(Ctx &c, const double *v, const double *z, double *y)
+{
+    const double *xu = z, *xf = z + 3 * (int64_t)c.Nn;
+    double *yu = y, *yf = y + 3 * (int64_t)c.Nn;
+    halo_exchange(c, c.hu, 3, xu, c.gh_u);
+    halo_exchange(c, c.hf, 2, xf, c.gh_f);
+    const GV gu = gv(xu, c.Nn, c.gh_u.p), gf = gv(xf, c.Nc, c.gh_f.p);
+    prof_begin(c, PK_OP_NODE);
+    if (!sym_op_node(c, gu, gf, yu) && c.Nn)
+        (c.comm ? k_op_node<true> : k_op_node<false>)<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(
+            c.Nn, c.s_uu.off, c.s_uu.col, c.s_uu.val, c.s_uf.off, c.s_uf.col, c.s_uf.val, gu, gf, yu);
+    prof_end(c, PK_OP_NODE, (c.sym_uu.ok ? sym_bytes(c, 9) : sell_bytes(c.s_uu)) + sell_bytes(c.s_uf) + 48.0 * c.Nn + 16.0 * c.Nc);
+    prof_begin(c, PK_OP_CELL);
+    if (c.Nc) (c.comm ? k_op_cell<2, true> : k_op_cell<2, false>)<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(
+        c.Nc, nullptr, nullptr, nullptr, c.s_ff.off, c.s_ff.col, c.s_ff.val, gu, gf, v + 3 * (int64_t)c.Nn, yf, c.w_yf);
+    prof_end(c, PK_OP_CELL, sell_bytes(c.s_ff) + 64.0 * c.Nc);   // + v_f, y2, x_f read, y_f written
     c.launches += 2;
     TSP_CUDA(cudaGetLastError());
 }
@@ -149,7 +177,7 @@ void prec_apply(Ctx &c, const double *v, double *z)
     halo_exchange(c, c.hu, 3, zu, c.gh_u);
     prof_begin(c, PK_STEP2);
     if (c.Nc) (c.comm ? k_op_cell<1, true> : k_op_cell<1, false>)<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(
-        c.Nc, c.s_fu.off, c.s_fu.col, c.s_fu.val, nullptr, nullptr, nullptr, gv(zu, c.Nn, c.gh_u.p), gv(nullptr, 0), vf, c.w_yf);
+        c.Nc, c.s_fu.off, c.s_fu.col, c.s_fu.val, nullptr, nullptr, nullptr, gv(zu, c.Nn, c.gh_u.p), gv(nullptr, 0), vf, c.w_yf, nullptr);
     prof_end(c, PK_STEP2, sell_bytes(c.s_fu) + 24.0 * c.Nn + 32.0 * c.Nc);
     // steps 3-4
     halo_exchange(c, c.hf, 2, c.w_yf, c.gh_f);

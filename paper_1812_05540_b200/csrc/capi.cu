@@ -590,8 +590,11 @@ tsp_status tsp_get_stats(tsp_handle h, tsp_stats *s)
     apply_bytes += (28.0 * 8 + 32 + 48) * Nc;                  // steps 6-8
     s->bytes_apply = apply_bytes;
     s->bytes_operator = (h->sym_uu.ok ? sym_bytes(*h, 9) : sb(h->s_uu)) + sb(h->s_uf) + sb(h->s_fu) + sb(h->s_ff) + 16 * n;
-    // Gram-Schmidt depends on the Krylov index: counted exactly per solve (tsp_solve_info.bytes_krylov)
-    s->bytes_iter_base = s->bytes_apply + s->bytes_operator;
+    // Gram-Schmidt depends on the Krylov index: counted exactly per solve (tsp_solve_info.bytes_krylov).  The
+    // FGMRES operator reuses Algorithm 1's A_fu z_u (op_apply_after_prec): its cell rows stream A_ff only
+    static const bool no_fuse = getenv("TSP_NO_OP_FUSE") != nullptr;
+    const double op_iter = no_fuse ? s->bytes_operator : s->bytes_operator - sb(h->s_fu) - 24 * Nn + 32 * Nc;
+    s->bytes_iter_base = s->bytes_apply + op_iter;
     s->bytes_per_krylov_vec = 8 * n;
     s->launches = h->launches;
     return TSP_OK;

@@ -525,6 +525,7 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
     // CUDA graphs for the iteration body: one rank, no profiling (its events are per launch)
     const bool no_graph = getenv("TSP_NO_GRAPH") != nullptr;
     const bool use_graph = !c.comm && !c.prof.on && !no_graph;
+    static const bool no_fuse = getenv("TSP_NO_OP_FUSE") != nullptr;   // test knob: the full operator every iteration
     double bn;
     K.norm(b, dh);
     TSP_CUDA(cudaMemcpyAsync(&bn, dh, sizeof(double), cudaMemcpyDeviceToHost, c.s));
@@ -562,7 +563,8 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
                 // the iteration body: device work only, ending with the scalars copied to pinned host memory
                 auto body = [&]() {
                     prec_apply(c, uj, zj);                 // z_j = M^-1 u_j (Algorithm 1)
-                    op_apply(c, zj, w);                    // w = A z_j
+                    if (no_fuse) op_apply(c, zj, w);       // w = A z_j
+                    else op_apply_after_prec(c, uj, zj, w);   // (A_fu z_u reused from Algorithm 1's step 2)
                     K.mdot2(V, j, w, d, sc);               // [V_{j-1} u_j]^T [u_j w], alpha_j, h_j
                     K.dcgs_update(V, j, d, sc, w, rho);    // v_j, w -> w - V_j h, rho = ||w||
                     K.scale_inv(rho, w, w);                // u_{j+1} = w / rho (skipped when rho == 0)

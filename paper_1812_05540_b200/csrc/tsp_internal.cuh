@@ -361,6 +361,7 @@ bool sym_vcycle_pre(Ctx &c, int n, const GV &dinv, const GV &b, double *x, doubl
 bool sym_vcycle_post(Ctx &c, int n, const double *dinv, const double *b, const GV &x, double *xo);
 double sym_bytes(const Ctx &c, int bs);   // bytes of one stream over a Sym27 with bs values per block
 void prec_apply(Ctx &c, const double *v, double *z);
+void op_apply_after_prec(Ctx &c, const double *v, const double *z, double *y);   // A z right after z = M^-1 v
 
 // p7.cu: structured 7-point pressure level 0 (mode 1 pre, 2 post, 3 residual, 4 / 5 Chebyshev PRE / STEP)
 void p7_build(Ctx &c, const Csr &A);

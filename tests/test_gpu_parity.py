@@ -292,6 +292,33 @@ def test_structured_7point_pressure_level_equals_the_generic_one(dev, name, smoo
     assert b1 < b2                # fewer algorithmic bytes without the column indices
 
 
+@pytest.mark.parametrize("name", ["C2", "R1"])
+def test_fused_operator_after_the_preconditioner(dev, name):
+    """The FGMRES body computes A z_j right after z_j = M^-1 u_j and takes A_fu z_u from Algorithm 1's step 2
+    (y_f = v_f - A_fu z_u, so A_fu z_u = v_f - y_f): the same iteration count (+-1) and solution (to the solver
+    tolerance) as with the full operator (TSP_NO_OP_FUSE), and the true residual still meets rtol."""
+    import os
+    from paper_1812_05540_b200 import Tsp
+    pb = _problem(name)
+    out = []
+    for nofuse in (False, True):
+        if nofuse:
+            os.environ["TSP_NO_OP_FUSE"] = "1"
+        try:
+            g = Tsp(pb).setup()
+            x = torch.zeros(pb.n, dtype=torch.float64, device=dev)
+            info = g.solve(_cuda(pb.b), x, rtol=1e-8)
+            torch.cuda.synchronize()
+            out.append((x.cpu().numpy(), info, g.stats()["bytes_iter_base"]))
+            g.close()
+        finally:
+            os.environ.pop("TSP_NO_OP_FUSE", None)
+    (x1, i1, b1), (x2, i2, b2) = out
+    assert i1["status"] == "OK" and i1["true_relres"] <= 1e-8
+    assert abs(i1["iterations"] - i2["iterations"]) <= 1
+    assert np.linalg.norm(x1 - x2) <= 1e-6 * np.linalg.norm(x2)
+
+
 def test_cuda_graph_iterations_are_bitwise_the_eager_ones(dev):
     """krylov.cu replays the FGMRES iteration body from per-index CUDA graphs (captured on a second use); two
     solves with graphs and one without (TSP_NO_GRAPH) give the same solution bit for bit."""
