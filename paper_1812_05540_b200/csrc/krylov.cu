@@ -164,6 +164,123 @@ __global__ void __launch_bounds__(KB, TSP_MDOT2_MINB) k_mdot2(int nv, const doub
     }
 }
 
+// ---- the same pass with its operands moved by the TMA bulk-copy engine (cp.async.bulk + mbarrier) ----
+// One CTA per chunk as k_mdot2; one thread issues 1-D bulk copies of u and w (one each) and of the basis
+// vectors in ITEMS of (group of KG2 vectors) x (half chunk of 1024 rows) into a two-slot shared-memory ring
+// (slot = half), each slot completing an mbarrier by byte count; every thread waits on the slot's barrier
+// (phase = group parity).  The copy engine keeps the next item in flight while the CTA multiplies and
+// reduces the current one (k_mdot2 stalls on its own loads at every group's block reduction), and no
+// thread spends issue slots on address arithmetic for the stream.  Each thread still accumulates its rows
+// in the same order (tid, tid + 256, ...) and the same block_sum_multi<2 KG2> tree finishes every group:
+// the result is BITWISE k_mdot2's.  Requirements (checked by the caller): V, u, w 16-byte aligned, ldv
+// even; bulk copies start at the even row at or below the chunk start (off = 0 or 1 leading row) and end
+// at the even row at or above its end, which stays inside the ld-padded basis columns.
+constexpr int HR = kRedChunk / 2;         // rows per half chunk
+constexpr int HS = HR + 2;                // half-chunk slot length in doubles (+ the odd-offset row, 16-B multiple)
+constexpr int CS = kRedChunk + 2;         // u / w staging length
+constexpr size_t kMdotTmaSmem = sizeof(double) * (2 * CS + 2 * KG2 * HS);
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t *b, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *b)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t phase)
+{
+    uint32_t done;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(done) : "r"(smem_addr(b)), "r"(phase) : "memory");
+    } while (!done);
+}
+
+__global__ void __launch_bounds__(KB, 2) k_mdot2_tma(int nv, const double *__restrict__ V, int64_t ldv, const double *__restrict__ u,
+                                                     const double *__restrict__ w, const int64_t *__restrict__ be,
+                                                     double *__restrict__ part, int cmax)
+{
+    extern __shared__ __align__(128) double dsm[];
+    double *uS = dsm, *wS = dsm + CS, *ring = dsm + 2 * CS;          // ring[h][t][HS]
+    __shared__ __align__(8) uint64_t bar[3];                        // bar[h]: half h of the current group; bar[2]: u, w
+    __shared__ double red[KB / 32][2 * KG2];
+    const int k = blockIdx.x;
+    const int64_t beg = be[2 * k];
+    const int len = (int)(be[2 * k + 1] - beg);
+    const int64_t a0 = beg & ~(int64_t)1;
+    const int off = (int)(beg - a0);
+    const int ngroups = (nv + KG2 - 1) / KG2;
+    const int nh = len > HR ? 2 : 1;
+    auto half_bytes = [&](int h) {                                   // bytes of one vector's copy of half h
+        const int64_t r1 = beg + min(len, (h + 1) * HR);
+        return (uint32_t)(8 * (((r1 + 1) & ~(int64_t)1) - (a0 + h * HR)));
+    };
+    auto issue = [&](int g, int h) {                                 // thread 0: item (group g, half h) -> slot h
+        const int cnt = min(KG2, nv - g * KG2);
+        const uint32_t nb = half_bytes(h);
+        mbar_expect(&bar[h], nb * cnt);
+        for (int t = 0; t < cnt; ++t)
+            bulk_g2s(ring + (h * KG2 + t) * HS, V + (int64_t)(g * KG2 + t) * ldv + a0 + h * HR, nb, &bar[h]);
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); mbar_init(&bar[2], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t nb = (uint32_t)(8 * (((beg + len + 1) & ~(int64_t)1) - a0));
+        mbar_expect(&bar[2], 2 * nb);
+        bulk_g2s(uS, u + a0, nb, &bar[2]);
+        bulk_g2s(wS, w + a0, nb, &bar[2]);
+        for (int h = 0; h < nh; ++h) issue(0, h);
+    }
+    mbar_wait(&bar[2], 0);
+    for (int g = 0; g < ngroups; ++g) {
+        const int v0 = g * KG2, cnt = min(KG2, nv - v0);
+        double acc[2 * KG2];
+#pragma unroll
+        for (int t = 0; t < 2 * KG2; ++t) acc[t] = 0.0;
+        for (int h = 0; h < nh; ++h) {
+            mbar_wait(&bar[h], g & 1);
+            const double *sl = ring + h * KG2 * HS + off - h * HR;
+            const int r1 = min(len, (h + 1) * HR);
+            for (int i = h * HR + threadIdx.x; i < r1; i += KB) {
+                const double x = uS[off + i], y = wS[off + i];
+#pragma unroll
+                for (int t = 0; t < KG2; ++t)
+                    if (t < cnt) {
+                        const double va = sl[t * HS + i];
+                        acc[t] = fma(va, x, acc[t]);
+                        acc[KG2 + t] = fma(va, y, acc[KG2 + t]);
+                    }
+            }
+            if (h == 0 && nh == 2) {                                 // slot 0 read by all: refill it
+                __syncthreads();
+                if (threadIdx.x == 0 && g + 1 < ngroups) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    issue(g + 1, 0);
+                }
+            }
+        }
+        const double s = block_sum_multi<2 * KG2>(acc, red);          // its barriers: the last slot read by all
+        if (threadIdx.x == 0 && g + 1 < ngroups) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (nh == 2) issue(g + 1, 1);
+            else issue(g + 1, 0);
+        }
+        const int q = threadIdx.x;
+        if (q < 2 * KG2 && (q % KG2) < cnt) part[(int64_t)((q < KG2 ? 0 : nv) + v0 + q % KG2) * cmax + k] = s;
+    }
+}
+
 // DCGS2 scalars from the pass-1 dots d = [V_{j-1} u ; u.u | V_{j-1} w ; u.w] (2(j+1) values):
 // s = d[0..j), gamma = d[j], a = d[j+1..2j+1), b = d[2j+1];
 // alpha = sqrt(gamma - s.s) (norm of the re-orthogonalised u), h_j = (b - s.a) / alpha (= v_j . w).
@@ -310,11 +427,15 @@ struct Kr {
     int nblk;
     double bytes = 0;                 // algorithmic bytes of the Krylov kernels (tsp_solve_info.bytes_krylov)
     int force_fallback = 0;           // test knob TSP_DCGS2_FALLBACK: every iteration takes the explicit path
+    bool tma = true;                  // pass 1 by k_mdot2_tma (test knob TSP_NO_TMA, read per solve: k_mdot2)
     DBuf<double> pall;
     Kr(Ctx &c_, int maxv) : c(c_), n(c_.n), ld((c_.n + 31) & ~(int64_t)31)
     {
         nblk = (int)std::max<int64_t>(1, std::min<int64_t>((n + KB - 1) / KB, (int64_t)c.sm_count * 4));
         pall.alloc((size_t)std::max(c.nranks, 1) * maxv * std::max(c.nseg_max, 1) + 16);
+        static const bool smem_ok =
+            cudaFuncSetAttribute(k_mdot2_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMdotTmaSmem) == cudaSuccess;
+        tma = smem_ok && getenv("TSP_NO_TMA") == nullptr;
     }
     // chunk partials `kpart` ([nv][nchunk_loc]) -> segment sums -> (allgather) -> out[nv]
     void finish(int nv, double *out, int mode)
@@ -344,7 +465,12 @@ struct Kr {
     void mdot2(const double *V, int j, const double *w, double *d, double *sc)
     {
         prof_begin(c, PK_DOT);
-        k_mdot2<<<c.nchunk_loc, KB, 0, c.s>>>(j + 1, V, ld, V + (size_t)j * ld, w, c.chunk_beg, c.kpart, c.nchunk_loc);
+        // bulk copies: basis columns 16-B aligned (cudaMalloc base, ld a multiple of 32)
+        if (tma && ((uintptr_t)V & 15) == 0 && (ld & 1) == 0 && ((uintptr_t)w & 15) == 0)
+            k_mdot2_tma<<<c.nchunk_loc, KB, kMdotTmaSmem, c.s>>>(j + 1, V, ld, V + (size_t)j * ld, w, c.chunk_beg, c.kpart,
+                                                                 c.nchunk_loc);
+        else
+            k_mdot2<<<c.nchunk_loc, KB, 0, c.s>>>(j + 1, V, ld, V + (size_t)j * ld, w, c.chunk_beg, c.kpart, c.nchunk_loc);
         finish(2 * (j + 1), d, 0);
         k_dcgs_coef<<<1, 32, 0, c.s>>>(j, d, sc, force_fallback);
         prof_end(c, PK_DOT, 8.0 * n * (j + 2));
@@ -525,7 +651,7 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
     // CUDA graphs for the iteration body: one rank, no profiling (its events are per launch)
     const bool no_graph = getenv("TSP_NO_GRAPH") != nullptr;
     const bool use_graph = !c.comm && !c.prof.on && !no_graph;
-    static const bool no_fuse = getenv("TSP_NO_OP_FUSE") != nullptr;   // test knob: the full operator every iteration
+    const bool no_fuse = getenv("TSP_NO_OP_FUSE") != nullptr;   // test knob (read per solve): the full operator every iteration
     double bn;
     K.norm(b, dh);
     TSP_CUDA(cudaMemcpyAsync(&bn, dh, sizeof(double), cudaMemcpyDeviceToHost, c.s));

@@ -319,6 +319,33 @@ def test_fused_operator_after_the_preconditioner(dev, name):
     assert np.linalg.norm(x1 - x2) <= 1e-6 * np.linalg.norm(x2)
 
 
+@pytest.mark.parametrize("kw", [dict(config="C2"), dict(nx=4, ny=6, nz=18, recipe=2), dict(nx=24, ny=20, nz=40, recipe=1)])
+def test_tma_pass1_is_bitwise_the_plain_kernel(dev, kw):
+    """DCGS2 pass 1 by the bulk-copy pipeline (k_mdot2_tma) against the plain kernel (TSP_NO_TMA): the same
+    per-thread row order and reduction tree, so whole solves agree bit for bit.  The two grids give odd chunk
+    starts (3 Nn odd: every f chunk starts on an odd row), chunks of <= 1024 rows (one half only) next to full
+    two-half chunks, and Krylov indices up to 63 (groups of 1..4 vectors)."""
+    import os
+    from paper_1812_05540_b200 import Tsp
+    kw = dict(kw)
+    pb = synth.generate(kw.pop("config", None), **kw)
+    out = []
+    for plain in (False, True):
+        if plain:
+            os.environ["TSP_NO_TMA"] = "1"
+        try:
+            g = Tsp(pb).setup()
+            x = torch.zeros(pb.n, dtype=torch.float64, device=dev)
+            info = g.solve(_cuda(pb.b), x, rtol=1e-10, restart=64)
+            torch.cuda.synchronize()
+            out.append((x.cpu().numpy(), info["iterations"]))
+            g.close()
+        finally:
+            os.environ.pop("TSP_NO_TMA", None)
+    assert out[0][1] == out[1][1]
+    assert np.array_equal(out[0][0], out[1][0])
+
+
 def test_cuda_graph_iterations_are_bitwise_the_eager_ones(dev):
     """krylov.cu replays the FGMRES iteration body from per-index CUDA graphs (captured on a second use); two
     solves with graphs and one without (TSP_NO_GRAPH) give the same solution bit for bit."""

@@ -1,5 +1,6 @@
 """Developer A/B: device time per FGMRES iteration of repeated solves at a config (CUDA events), one process.
-  python tools/ab_solve.py [C5] [reps]   (environment knobs select the variant, e.g. TSP_NO_OP_FUSE=1)"""
+  python tools/ab_solve.py [C5] [reps]   (environment knobs select the variant, e.g. TSP_NO_OP_FUSE=1; prints a digest of x for bitwise A/B)"""
+import hashlib
 import os
 import sys
 
@@ -25,5 +26,6 @@ for _ in range(reps):
     e1.record()
     torch.cuda.synchronize()
     ms.append(e0.elapsed_time(e1) / info["iterations"])
-print(f"{cfg} {os.environ.get('TSP_NO_OP_FUSE', 'fused')}: {info['iterations']} it, ms/iter " + " ".join(f"{m:.3f}" for m in ms),
-      flush=True)
+knobs = ",".join(f"{k}={v}" for k, v in sorted(os.environ.items()) if k.startswith("TSP_")) or "default"
+digest = hashlib.sha1(x.cpu().numpy().tobytes()).hexdigest()[:12]
+print(f"{cfg} {knobs}: {info['iterations']} it, x sha1 {digest}, ms/iter " + " ".join(f"{m:.3f}" for m in ms), flush=True)
