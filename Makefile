@@ -12,9 +12,10 @@ NVFLAGS  = $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --
 TSP_SRC  = $(wildcard paper_1812_05540_b200/csrc/*.cu)
 TSP_HDR  = $(wildcard paper_1812_05540_b200/csrc/*.cuh) include/tsp.h
 
-all: synth oracle tsp
+all: synth oracle oracle_omp tsp
 synth: synth/libsynth.so
 oracle: oracle/liboracle.so
+oracle_omp: oracle/liboracle_omp.so
 tsp: paper_1812_05540_b200/libtsp.so
 
 synth/libsynth.so: synth/synth.c
@@ -22,6 +23,10 @@ synth/libsynth.so: synth/synth.c
 
 oracle/liboracle.so: $(wildcard oracle/*.c) $(wildcard oracle/*.h)
 	$(HOSTCC) $(ORCFLAGS) -shared -o $@ $(wildcard oracle/*.c) -lm
+
+# the same source with its OMP_ROWS loops on all host cores (timing-only oracle row, identical results)
+oracle/liboracle_omp.so: $(wildcard oracle/*.c) $(wildcard oracle/*.h)
+	$(HOSTCC) $(ORCFLAGS) -fopenmp -shared -o $@ $(wildcard oracle/*.c) -lm
 
 TSP_OBJ  = $(patsubst paper_1812_05540_b200/csrc/%.cu,build/tsp/%.o,$(TSP_SRC))
 
@@ -34,6 +39,6 @@ paper_1812_05540_b200/libtsp.so: $(TSP_OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(TSP_OBJ) -lcudart
 
 clean:
-	rm -rf synth/libsynth.so oracle/liboracle.so paper_1812_05540_b200/libtsp.so build/tsp
+	rm -rf synth/libsynth.so oracle/liboracle.so oracle/liboracle_omp.so paper_1812_05540_b200/libtsp.so build/tsp
 
-.PHONY: all synth oracle tsp clean
+.PHONY: all synth oracle oracle_omp tsp clean

@@ -57,10 +57,12 @@ class Info(C.Structure):
 def lib():
     global _LIB
     if _LIB is None:
-        path = os.path.join(_HERE, "liboracle.so")
-        src = [os.path.join(_HERE, f) for f in ("oracle.c", "oracle.h")]
+        # ORACLE_OMP=1: the OpenMP build of the same source (timing-only row; bitwise the same results)
+        omp = os.environ.get("ORACLE_OMP", "") not in ("", "0")
+        path = os.path.join(_HERE, "liboracle_omp.so" if omp else "liboracle.so")
+        src = [os.path.join(_HERE, f) for f in os.listdir(_HERE) if f.endswith((".c", ".h"))]
         if not os.path.exists(path) or any(os.path.getmtime(s) > os.path.getmtime(path) for s in src):
-            subprocess.check_call(["make", "-s", "-C", os.path.dirname(_HERE), "oracle"])
+            subprocess.check_call(["make", "-s", "-C", os.path.dirname(_HERE), "oracle_omp" if omp else "oracle"])
         L = C.CDLL(path)
         L.orc_default_opts.argtypes = [_P(Opts)]
         L.orc_create.argtypes = [_P(Desc), _P(Opts)]

@@ -2,7 +2,8 @@
  * oracle.c -- TEST INFRASTRUCTURE ONLY (see oracle.h).  Parity pinned by
  * tests/test_oracle_*.py; functions without a pin say so in DESIGN.md.
  *
- * Plain sequential C, -ffp-contract=off, IEEE double.  Written in the paper's
+ * Plain sequential C, -ffp-contract=off, IEEE double (OMP_ROWS below: an optional
+ * timing-only build runs row-independent loops on all host cores).  Written in the paper's
  * order and notation:
  *   a1 fixed stress          eq:Schur_1_FS P:406-417, eq:FS_Dps_Dpp P:418-437
  *   a2 SDC
@@ -21,6 +22,16 @@
 #include <stdlib.h>
 #include <string.h>
 #include <time.h>
+
+/* OMP_ROWS marks loops whose iterations are independent rows (nothing is summed across them).  The plain
+ * liboracle.so ignores it; liboracle_omp.so (-fopenmp, Makefile; loaded when ORACLE_OMP=1, the timing-only
+ * "oracle-omp" row of tools/config_sweep.py) runs those loops on all host cores with bitwise the same
+ * results: every dot product, Gauss-Seidel / ILU sweep and setup step stays sequential. */
+#ifdef _OPENMP
+#define OMP_ROWS _Pragma("omp parallel for schedule(static)")
+#else
+#define OMP_ROWS
+#endif
 
 static void *xmalloc(size_t n) { void *p = malloc(n ? n : 1); if (!p) { fprintf(stderr, "oracle: OOM\n"); abort(); } return p; }
 static void *xcalloc(size_t n, size_t s) { void *p = calloc(n ? n : 1, s ? s : 1); if (!p) { fprintf(stderr, "oracle: OOM\n"); abort(); } return p; }
@@ -50,6 +61,7 @@ static int64_t mnnz(const mcsr *A) { return A->rp[A->n]; }
 /* y = A_c x (one component) */
 static void spmv(const mcsr *A, int c, const double *x, double *y)
 {
+    OMP_ROWS
     for (int i = 0; i < A->n; ++i) {
         double s = 0.0;
         for (int64_t q = A->rp[i]; q < A->rp[i + 1]; ++q) s += A->v[c][q] * x[A->ci[q]];
@@ -59,6 +71,7 @@ static void spmv(const mcsr *A, int c, const double *x, double *y)
 /* y = y - A_c x */
 static void spmv_sub(const mcsr *A, int c, const double *x, double *y)
 {
+    OMP_ROWS
     for (int i = 0; i < A->n; ++i) {
         double s = 0.0;
         for (int64_t q = A->rp[i]; q < A->rp[i + 1]; ++q) s += A->v[c][q] * x[A->ci[q]];
@@ -712,6 +725,7 @@ static void cheb_smooth(const mcsr *A, int c, const double *dl1, int degree, dou
     double rho = 1.0 / sigma;
     for (int k = 0; k < degree; ++k) {
         /* r_k = D^-1 (b - A x_k) */
+        OMP_ROWS
         for (int i = 0; i < n; ++i) {
             double s = b[i];
             if (!(k == 0 && from_zero))
@@ -719,9 +733,11 @@ static void cheb_smooth(const mcsr *A, int c, const double *dl1, int degree, dou
             r[i] = dl1[i] != 0.0 ? s / dl1[i] : 0.0;
         }
         if (k == 0) {
+            OMP_ROWS
             for (int i = 0; i < n; ++i) { d[i] = r[i] / theta; x[i] = (from_zero ? 0.0 : x[i]) + d[i]; }
         } else {
             const double rho_new = 1.0 / (2.0 * sigma - rho);
+            OMP_ROWS
             for (int i = 0; i < n; ++i) { d[i] = rho_new * rho * d[i] + (2.0 * rho_new / delta) * r[i]; x[i] = x[i] + d[i]; }
             rho = rho_new;
         }
@@ -757,7 +773,10 @@ static void vcycle(const ohier *H, int lvl, int c, const double *b, double *x)
     const int cheb = H->o.amg_smoother == 2;
     if (gs) { for (int i = 0; i < n; ++i) x[i] = 0.0; gs_sweep(L, c, b, x, 0); }       /* forward GS from zero */
     else if (cheb) cheb_smooth(&L->A, c, L->dl1[c], H->o.amg_cheb_degree, H->o.amg_cheb_lower, b, x, 1);
-    else for (int i = 0; i < n; ++i) x[i] = L->dl1[c][i] != 0.0 ? b[i] / L->dl1[c][i] : 0.0;
+    else {
+        OMP_ROWS
+        for (int i = 0; i < n; ++i) x[i] = L->dl1[c][i] != 0.0 ? b[i] / L->dl1[c][i] : 0.0;
+    }
     double *r = (double *)xmalloc(sizeof(double) * (n + 1));
     memcpy(r, b, sizeof(double) * n);
     spmv_sub(&L->A, c, x, r);
@@ -765,6 +784,7 @@ static void vcycle(const ohier *H, int lvl, int c, const double *b, double *x)
     double *bc = (double *)xmalloc(sizeof(double) * (m + 1)), *xc = (double *)xcalloc(m + 1, sizeof(double));
     spmv(&L->R, c, r, bc);
     vcycle(H, lvl + 1, c, bc, xc);
+    OMP_ROWS
     for (int i = 0; i < n; ++i) {
         double s = 0.0;
         for (int64_t q = L->P.rp[i]; q < L->P.rp[i + 1]; ++q) s += L->P.v[c][q] * xc[L->P.ci[q]];
@@ -775,6 +795,7 @@ static void vcycle(const ohier *H, int lvl, int c, const double *b, double *x)
     else {
         memcpy(r, b, sizeof(double) * n);
         spmv_sub(&L->A, c, x, r);
+        OMP_ROWS
         for (int i = 0; i < n; ++i) if (L->dl1[c][i] != 0.0) x[i] += r[i] / L->dl1[c][i];
     }
     free(r); free(bc); free(xc);
@@ -1042,6 +1063,7 @@ static void mech_apply(orc *h, const double *vu, double *zu)
 /* y = A_uu x, 3x3 blocks (eq:jac_system) */
 static void uu_matvec(const orc *h, const double *x, double *y)
 {
+    OMP_ROWS
     for (int i = 0; i < h->Nn; ++i)
         for (int r = 0; r < 3; ++r) {
             double s = 0.0;
@@ -1314,6 +1336,7 @@ int orc_apply(orc *h, const double *v, double *z)
 /* ---------------- operator y = A x, eq:jac_system ---------------- */
 static void bsr_mv_add(const obsr *B, const double *x, double *y)
 {
+    OMP_ROWS
     for (int i = 0; i < B->nr; ++i)
         for (int r = 0; r < B->bm; ++r) {
             double s = 0.0;
@@ -1399,11 +1422,15 @@ int orc_solve(orc *h, const double *b, double *x, double rtol, int m, int maxit,
             for (int i = 0; i <= j; ++i) {                 /* MGS */
                 double hij = dot(w, V[i], n);
                 H[(size_t)j * (m + 1) + i] = hij;
+                OMP_ROWS
                 for (int t = 0; t < n; ++t) w[t] -= hij * V[i][t];
             }
             double hn = sqrt(dot(w, w, n));
             H[(size_t)j * (m + 1) + j + 1] = hn;
-            if (hn != 0.0) for (int t = 0; t < n; ++t) V[j + 1][t] = w[t] / hn;
+            if (hn != 0.0) {
+                OMP_ROWS
+                for (int t = 0; t < n; ++t) V[j + 1][t] = w[t] / hn;
+            }
             else breakdown = 1;
             for (int i = 0; i < j; ++i) {                  /* apply previous Givens rotations */
                 double a = H[(size_t)j * (m + 1) + i], c = H[(size_t)j * (m + 1) + i + 1];
@@ -1425,7 +1452,10 @@ int orc_solve(orc *h, const double *b, double *x, double rtol, int m, int maxit,
             for (int t = i + 1; t < k; ++t) s -= H[(size_t)t * (m + 1) + i] * yv[t];
             yv[i] = s / H[(size_t)i * (m + 1) + i];
         }
-        for (int i = 0; i < k; ++i) for (int t = 0; t < n; ++t) x[t] += yv[i] * Z[i][t];
+        for (int i = 0; i < k; ++i) {
+            OMP_ROWS
+            for (int t = 0; t < n; ++t) x[t] += yv[i] * Z[i][t];
+        }
         if (status == 2) break;
         if (breakdown && k == 0) break;
     }

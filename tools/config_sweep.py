@@ -1,10 +1,14 @@
 """Per-config records: for each BASELINE.json config that the oracle can run in full on the host
 (C1-C4), one JSON line with the GPU path (setup + FGMRES(64) to 1e-8, device-timed, the bench's step) next to the
 oracle's FULL run of the same step on the same input (its own setup and its own FGMRES to 1e-8 on one host core;
-no extrapolation).  Also the preconditioner apply alone, GDoF/s, and the iteration counts of both sides.
+no extrapolation), and the timing-only "oracle-omp" row: the OpenMP build of the same oracle source on all host
+cores (tools/oracle_run.py with ORACLE_OMP=1; row loops parallel, dot products / sweeps / setup sequential), whose x
+must be bitwise the single-core run's.  Also the preconditioner apply alone, GDoF/s, and the iteration counts.
   python tools/config_sweep.py [C1 C2 C3 C4]   > profiles/r02_configs.jsonl"""
+import hashlib
 import json
 import os
+import subprocess
 import sys
 import time
 
@@ -61,6 +65,11 @@ for cfg in cfgs:
     xo, io = o.solve(pb.b, rtol=1e-8, m=64)
     t2 = time.perf_counter()
     fwd_orc = float(np.linalg.norm(xo - pb.x_rand) / np.linalg.norm(pb.x_rand))
+    nproc = os.cpu_count()
+    env = dict(os.environ, ORACLE_OMP="1", OMP_NUM_THREADS=str(nproc))
+    out = subprocess.run([sys.executable, os.path.join(os.path.dirname(os.path.abspath(__file__)), "oracle_run.py"), cfg],
+                         env=env, capture_output=True, text=True, check=True).stdout
+    omp = json.loads(out.strip().splitlines()[-1])
     rec = {"config": cfg, "grid": [pb.nx, pb.ny, pb.nz], "dof": pb.n,
            "gpu": {"iterations": it, "setup_mech_ms": sm, "setup_flow_ms": sf, "setup_ms": su, "solve_ms": so,
                    "step_ms": su + so, "forward_error": fwd_gpu,
@@ -72,6 +81,11 @@ for cfg in cfgs:
                       "host_nproc": os.cpu_count(),
                       "step_s": t2 - t0, "iters_per_s": io["iterations"] / (t2 - t0), "cores": 1,
                       "kind": "oracle (plain C, full run, no extrapolation)"},
+           "oracle_omp": {"iterations": omp["iterations"], "setup_s": omp["setup_s"], "solve_s": omp["solve_s"],
+                          "step_s": omp["step_s"], "cores": nproc, "cpu_model": cpu_model,
+                          "bitwise_same_x": omp["x_sha1"] == hashlib.sha1(np.ascontiguousarray(xo).tobytes()).hexdigest(),
+                          "kind": "oracle-omp (timing only: OpenMP build of oracle.c, row loops on all cores)"},
+           "speedup_step_vs_omp": omp["step_s"] / ((su + so) * 1e-3),
            "iterations_match_pm1": abs(io["iterations"] - it) <= 1,
            "speedup_step": (t2 - t0) / ((su + so) * 1e-3)}
     print(json.dumps(rec), flush=True)
