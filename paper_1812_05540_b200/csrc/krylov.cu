@@ -180,29 +180,6 @@ constexpr int HS = HR + 2;                // half-chunk slot length in doubles (
 constexpr int CS = kRedChunk + 2;         // u / w staging length
 constexpr size_t kMdotTmaSmem = sizeof(double) * (2 * CS + 2 * KG2 * HS);
 
-__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count)
-{
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect(uint64_t *b, uint32_t bytes)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *b)
-{
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t phase)
-{
-    uint32_t done;
-    do {
-        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-                     : "=r"(done) : "r"(smem_addr(b)), "r"(phase) : "memory");
-    } while (!done);
-}
-
 __global__ void __launch_bounds__(KB, 2) k_mdot2_tma(int nv, const double *__restrict__ V, int64_t ldv, const double *__restrict__ u,
                                                      const double *__restrict__ w, const int64_t *__restrict__ be,
                                                      double *__restrict__ part, int cmax)
