@@ -12,13 +12,14 @@ namespace tsp {
 // ------------------------------------------------------------------ operator, node rows:
 // y_u = A_uu x_u + A_uf x_f
 template <bool D>
-__global__ void __launch_bounds__(256) k_op_node(int Nn, const int64_t *__restrict__ off_uu, const int32_t *__restrict__ col_uu,
+__global__ void __launch_bounds__(256) k_op_node(int cnt, Rows R, const int64_t *__restrict__ off_uu, const int32_t *__restrict__ col_uu,
                                                  const double *__restrict__ val_uu, const int64_t *__restrict__ off_uf,
                                                  const int32_t *__restrict__ col_uf, const double *__restrict__ val_uf,
                                                  GV xu, GV xf, double *__restrict__ yu)
 {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= Nn) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= cnt) return;
+    const int i = row_of(R, t);
     const int s = i >> 5, lane = i & 31;
     double a0 = 0, a1 = 0, a2 = 0;
     {
@@ -52,14 +53,15 @@ __global__ void __launch_bounds__(256) k_op_node(int Nn, const int64_t *__restri
 // mode 2: the operator right after Algorithm 1 on the same vector -- its step 2 left y2 = v_f - A_fu z_u, so
 // A_fu z_u = v_f - y2 and only A_ff is streamed: y_f = (v_f - y2) + A_ff x_f (y2 passed in `y2`)
 template <int MODE, bool D>
-__global__ void __launch_bounds__(256) k_op_cell(int Nc, const int64_t *__restrict__ off_fu, const int32_t *__restrict__ col_fu,
+__global__ void __launch_bounds__(256) k_op_cell(int cnt, Rows R, const int64_t *__restrict__ off_fu, const int32_t *__restrict__ col_fu,
                                                  const double *__restrict__ val_fu, const int64_t *__restrict__ off_ff,
                                                  const int32_t *__restrict__ col_ff, const double *__restrict__ val_ff,
                                                  GV xu, GV xf, const double *__restrict__ vf, double *__restrict__ yf,
                                                  const double *__restrict__ y2)
 {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= Nc) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= cnt) return;
+    const int i = row_of(R, t);
     const int s = i >> 5, lane = i & 31;
     double a0 = 0, a1 = 0;
     if (MODE == 2) {
@@ -123,47 +125,102 @@ __global__ void k_split_f(int Nc, const double *__restrict__ zf, double *__restr
 
 static double sell_bytes(const Sell &S) { return (double)S.slots * 32 * (4.0 + 8.0 * S.bs); }
 
-void op_apply(Ctx &c, const double *x, double *y)
+// ---- halo overlap on a z-slab (multi-GPU): the rows whose stencils reach a neighbour's planes are the first
+// node / cell plane (rank > 0) and the last one (rank < P - 1); everything else is computed on the main stream
+// while the halo exchange runs on the comm stream, then the boundary rows.  Same kernels and per-row arithmetic
+// as one launch over all rows: bitwise the same result (TSP_NO_OVERLAP: exchange first, one launch per kernel).
+struct Split {
+    bool on = false;
+    Rows in_n, bd_n, in_c, bd_c;
+    int cin_n = 0, cbd_n = 0, cin_c = 0, cbd_c = 0;
+};
+static Split slab_split(const Ctx &c)
+{
+    Split sp;
+    if (!c.comm || !c.cs || getenv("TSP_NO_OVERLAP")) return sp;
+    const int NXY = (c.nx + 1) * (c.ny + 1), CP = c.nx * c.ny;
+    const int lo = c.rank > 0, hi = c.rank < c.nranks - 1;
+    const int nlo = lo * NXY, nhi = hi * NXY, clo = lo * CP, chi = hi * CP;
+    if (c.Nn < nlo + nhi + NXY || c.Nc < clo + chi + CP) return sp;     // slab too thin to have interior planes
+    sp.on = true;
+    sp.in_n = Rows{nlo, c.Nn - nlo - nhi, c.Nn}; sp.cin_n = c.Nn - nlo - nhi;
+    sp.bd_n = Rows{0, nlo, c.Nn - nhi}; sp.cbd_n = nlo + nhi;
+    sp.in_c = Rows{clo, c.Nc - clo - chi, c.Nc}; sp.cin_c = c.Nc - clo - chi;
+    sp.bd_c = Rows{0, clo, c.Nc - chi}; sp.cbd_c = clo + chi;
+    return sp;
+}
+// the exchanges of `xchg` on the comm stream after everything already on the main stream; `interior` launched
+// first (so a host-blocking backend does not delay it), the main stream then waits for the halos
+template <class FI, class FX>
+static void overlapped(Ctx &c, FI interior, FX xchg)
+{
+    TSP_CUDA(cudaEventRecord(c.ev_x, c.s));
+    interior();
+    TSP_CUDA(cudaStreamWaitEvent(c.cs, c.ev_x, 0));
+    xchg(c.cs);
+    TSP_CUDA(cudaEventRecord(c.ev_h, c.cs));
+    TSP_CUDA(cudaStreamWaitEvent(c.s, c.ev_h, 0));
+}
+
+static void op_node_rows(Ctx &c, const GV &gu, const GV &gf, double *yu, Rows R, int cnt, double frac)
+{
+    prof_begin(c, PK_OP_NODE);
+    if (!sym_op_node(c, gu, gf, yu, R, cnt) && cnt)
+        (c.comm ? k_op_node<true> : k_op_node<false>)<<<grid_for(cnt, 256), 256, 0, c.s>>>(
+            cnt, R, c.s_uu.off, c.s_uu.col, c.s_uu.val, c.s_uf.off, c.s_uf.col, c.s_uf.val, gu, gf, yu);
+    prof_end(c, PK_OP_NODE, frac * ((c.sym_uu.ok ? sym_bytes(c, 9) : sell_bytes(c.s_uu)) + sell_bytes(c.s_uf) + 48.0 * c.Nn + 16.0 * c.Nc));
+    c.launches++;
+}
+// MODE 0: y_f = A_fu x_u + A_ff x_f; MODE 2: y_f = (v_f - y2) + A_ff x_f (see k_op_cell)
+template <int MODE>
+static void op_cell_rows(Ctx &c, const GV &gu, const GV &gf, const double *vf, double *yf, Rows R, int cnt, double frac)
+{
+    prof_begin(c, PK_OP_CELL);
+    if (cnt) {
+        if (MODE == 0)
+            (c.comm ? k_op_cell<0, true> : k_op_cell<0, false>)<<<grid_for(cnt, 256), 256, 0, c.s>>>(
+                cnt, R, c.s_fu.off, c.s_fu.col, c.s_fu.val, c.s_ff.off, c.s_ff.col, c.s_ff.val, gu, gf, nullptr, yf, nullptr);
+        else
+            (c.comm ? k_op_cell<2, true> : k_op_cell<2, false>)<<<grid_for(cnt, 256), 256, 0, c.s>>>(
+                cnt, R, nullptr, nullptr, nullptr, c.s_ff.off, c.s_ff.col, c.s_ff.val, gu, gf, vf, yf, c.w_yf);
+    }
+    prof_end(c, PK_OP_CELL, frac * (MODE == 0 ? sell_bytes(c.s_fu) + sell_bytes(c.s_ff) + 24.0 * c.Nn + 32.0 * c.Nc
+                                              : sell_bytes(c.s_ff) + 64.0 * c.Nc));   // MODE 2: + v_f, y2, x_f read, y_f written
+    c.launches++;
+}
+
+template <int MODE>
+static void op_common(Ctx &c, const double *x, const double *vf, double *y)
 {
     const double *xu = x, *xf = x + 3 * (int64_t)c.Nn;
     double *yu = y, *yf = y + 3 * (int64_t)c.Nn;
-    halo_exchange(c, c.hu, 3, xu, c.gh_u);
-    halo_exchange(c, c.hf, 2, xf, c.gh_f);
     const GV gu = gv(xu, c.Nn, c.gh_u.p), gf = gv(xf, c.Nc, c.gh_f.p);
-    prof_begin(c, PK_OP_NODE);
-    if (!sym_op_node(c, gu, gf, yu) && c.Nn)
-        (c.comm ? k_op_node<true> : k_op_node<false>)<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(
-            c.Nn, c.s_uu.off, c.s_uu.col, c.s_uu.val, c.s_uf.off, c.s_uf.col, c.s_uf.val, gu, gf, yu);
-    prof_end(c, PK_OP_NODE, (c.sym_uu.ok ? sym_bytes(c, 9) : sell_bytes(c.s_uu)) + sell_bytes(c.s_uf) + 48.0 * c.Nn + 16.0 * c.Nc);
-    prof_begin(c, PK_OP_CELL);
-    if (c.Nc) (c.comm ? k_op_cell<0, true> : k_op_cell<0, false>)<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(
-        c.Nc, c.s_fu.off, c.s_fu.col, c.s_fu.val, c.s_ff.off, c.s_ff.col, c.s_ff.val, gu, gf, nullptr, yf, nullptr);
-    prof_end(c, PK_OP_CELL, sell_bytes(c.s_fu) + sell_bytes(c.s_ff) + 24.0 * c.Nn + 32.0 * c.Nc);
-    c.launches += 2;
+    const Split sp = slab_split(c);
+    if (!sp.on) {
+        halo_exchange(c, c.hu, 3, xu, c.gh_u);
+        halo_exchange(c, c.hf, 2, xf, c.gh_f);
+        op_node_rows(c, gu, gf, yu, rows_all(c.Nn), c.Nn, 1.0);
+        op_cell_rows<MODE>(c, gu, gf, vf, yf, rows_all(c.Nc), c.Nc, 1.0);
+    } else {
+        const double fn = c.Nn ? (double)sp.cin_n / c.Nn : 0.0, fc = c.Nc ? (double)sp.cin_c / c.Nc : 0.0;
+        overlapped(c, [&] {
+            op_node_rows(c, gu, gf, yu, sp.in_n, sp.cin_n, fn);
+            op_cell_rows<MODE>(c, gu, gf, vf, yf, sp.in_c, sp.cin_c, fc);
+        }, [&](cudaStream_t s) {
+            halo_exchange(c, c.hu, 3, xu, c.gh_u, s);
+            halo_exchange(c, c.hf, 2, xf, c.gh_f, s);
+        });
+        op_node_rows(c, gu, gf, yu, sp.bd_n, sp.cbd_n, 1.0 - fn);
+        op_cell_rows<MODE>(c, gu, gf, vf, yf, sp.bd_c, sp.cbd_c, 1.0 - fc);
+    }
     TSP_CUDA(cudaGetLastError());
 }
 
+void op_apply(Ctx &c, const double *x, double *y) { op_common<0>(c, x, nullptr, y); }
+
 // y = A z right after z = M^-1 v (the FGMRES body): the cell rows reuse step 2's A_fu z_u (k_op_cell<2>), so A_fu
 // is streamed once per iteration instead of twice (SELL(A_fu) x 52 B = 3.5 GB at C5)
-void op_apply_after_prec(Ctx &c, const double *v, const double *z, double *y)
-{
-    const double *xu = z, *xf = z + 3 * (int64_t)c.Nn;
-    double *yu = y, *yf = y + 3 * (int64_t)c.Nn;
-    halo_exchange(c, c.hu, 3, xu, c.gh_u);
-    halo_exchange(c, c.hf, 2, xf, c.gh_f);
-    const GV gu = gv(xu, c.Nn, c.gh_u.p), gf = gv(xf, c.Nc, c.gh_f.p);
-    prof_begin(c, PK_OP_NODE);
-    if (!sym_op_node(c, gu, gf, yu) && c.Nn)
-        (c.comm ? k_op_node<true> : k_op_node<false>)<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(
-            c.Nn, c.s_uu.off, c.s_uu.col, c.s_uu.val, c.s_uf.off, c.s_uf.col, c.s_uf.val, gu, gf, yu);
-    prof_end(c, PK_OP_NODE, (c.sym_uu.ok ? sym_bytes(c, 9) : sell_bytes(c.s_uu)) + sell_bytes(c.s_uf) + 48.0 * c.Nn + 16.0 * c.Nc);
-    prof_begin(c, PK_OP_CELL);
-    if (c.Nc) (c.comm ? k_op_cell<2, true> : k_op_cell<2, false>)<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(
-        c.Nc, nullptr, nullptr, nullptr, c.s_ff.off, c.s_ff.col, c.s_ff.val, gu, gf, v + 3 * (int64_t)c.Nn, yf, c.w_yf);
-    prof_end(c, PK_OP_CELL, sell_bytes(c.s_ff) + 64.0 * c.Nc);   // + v_f, y2, x_f read, y_f written
-    c.launches += 2;
-    TSP_CUDA(cudaGetLastError());
-}
+void op_apply_after_prec(Ctx &c, const double *v, const double *z, double *y) { op_common<2>(c, z, v + 3 * (int64_t)c.Nn, y); }
 
 void prec_apply(Ctx &c, const double *v, double *z)
 {
@@ -173,12 +230,27 @@ void prec_apply(Ctx &c, const double *v, double *z)
     double *zu = z, *zf = z + nu;
     // step 1: z_u = M_uu^-1 v_u
     amg_vcycle(c, c.mech, vu, zu, true);
-    // step 2: y_f = v_f - A_fu z_u
-    halo_exchange(c, c.hu, 3, zu, c.gh_u);
-    prof_begin(c, PK_STEP2);
-    if (c.Nc) (c.comm ? k_op_cell<1, true> : k_op_cell<1, false>)<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(
-        c.Nc, c.s_fu.off, c.s_fu.col, c.s_fu.val, nullptr, nullptr, nullptr, gv(zu, c.Nn, c.gh_u.p), gv(nullptr, 0), vf, c.w_yf, nullptr);
-    prof_end(c, PK_STEP2, sell_bytes(c.s_fu) + 24.0 * c.Nn + 32.0 * c.Nc);
+    // step 2: y_f = v_f - A_fu z_u; on a slab the last cell plane (rank < P - 1) needs the node
+    // plane above, so it waits for the halo while the other planes run
+    {
+        const GV gz = gv(zu, c.Nn, c.gh_u.p);
+        auto step2 = [&](Rows R, int cnt, double frac) {
+            prof_begin(c, PK_STEP2);
+            if (cnt) (c.comm ? k_op_cell<1, true> : k_op_cell<1, false>)<<<grid_for(cnt, 256), 256, 0, c.s>>>(
+                cnt, R, c.s_fu.off, c.s_fu.col, c.s_fu.val, nullptr, nullptr, nullptr, gz, gv(nullptr, 0), vf, c.w_yf, nullptr);
+            prof_end(c, PK_STEP2, frac * (sell_bytes(c.s_fu) + 24.0 * c.Nn + 32.0 * c.Nc));
+            c.launches++;
+        };
+        const Split sp = slab_split(c);
+        if (!sp.on) {
+            halo_exchange(c, c.hu, 3, zu, c.gh_u);
+            step2(rows_all(c.Nc), c.Nc, 1.0);
+        } else {
+            const double fc = c.Nc ? (double)sp.cin_c / c.Nc : 0.0;
+            overlapped(c, [&] { step2(sp.in_c, sp.cin_c, fc); }, [&](cudaStream_t s) { halo_exchange(c, c.hu, 3, zu, c.gh_u, s); });
+            step2(sp.bd_c, sp.cbd_c, 1.0 - fc);
+        }
+    }
     // steps 3-4
     halo_exchange(c, c.hf, 2, c.w_yf, c.gh_f);
     prof_begin(c, PK_STEP34);
@@ -199,7 +271,7 @@ void prec_apply(Ctx &c, const double *v, double *z)
         halo_exchange(c, c.hf, 1, c.w_zp, c.gh_f2.p + ng);
         ilu_apply_fused(c, c.w_yf, c.w_tmp, c.w_zp, zf);
     }
-    c.launches += 2;
+    c.launches += 1;                                 // steps 3-4
     TSP_CUDA(cudaGetLastError());
 }
 

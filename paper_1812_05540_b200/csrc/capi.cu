@@ -162,6 +162,16 @@ void prof_end(Ctx &c, int cls, double bytes)
     cudaEventRecord(p.pool[r.e1], c.s);
 }
 
+// the halo-overlap stream and events of a sharded handle (created with its communicator in tsp_create)
+static void comm_stream_free(Ctx &c)
+{
+    if (c.cs) cudaStreamSynchronize(c.cs);
+    if (c.ev_x) cudaEventDestroy(c.ev_x);
+    if (c.ev_h) cudaEventDestroy(c.ev_h);
+    if (c.cs) cudaStreamDestroy(c.cs);
+    c.cs = nullptr; c.ev_x = c.ev_h = nullptr;
+}
+
 }  // namespace tsp
 
 using namespace tsp;
@@ -280,6 +290,9 @@ tsp_status tsp_create(tsp_handle *out, const tsp_desc *d)
         TSP_REQUIRE(d->comm_kind == TSP_COMM_NCCL || d->comm_kind == TSP_COMM_LOCAL, TSP_ERR_INVALID_ARG,
                     "nranks > 1 needs a communicator (comm_kind)");
         c->comm = make_comm(d->comm_kind, (void *)d->comm_arg, d->rank, d->nranks);
+        TSP_CUDA(cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking));      // halo overlap (apply.cu)
+        TSP_CUDA(cudaEventCreateWithFlags(&c->ev_x, cudaEventDisableTiming));
+        TSP_CUDA(cudaEventCreateWithFlags(&c->ev_h, cudaEventDisableTiming));
     }
     int dev = 0;
     TSP_CUDA(cudaGetDevice(&dev));
@@ -332,7 +345,7 @@ tsp_status tsp_create(tsp_handle *out, const tsp_desc *d)
     catch (...) {
         const tsp_status st = status_of_current_exception();
         (void)h;
-        if (c) { Comm *cm = c->comm; delete c; delete cm; }
+        if (c) { Comm *cm = c->comm; comm_stream_free(*c); delete c; delete cm; }
         return st;
     }
 }
@@ -709,6 +722,7 @@ void tsp_destroy(tsp_handle h)
     krylov_graphs_drop(*h);
     if (h->kcol_host) cudaFreeHost(h->kcol_host);
     if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
+    comm_stream_free(*h);
     Comm *cm = h->comm;
     cudaStream_t s = h->s;
     delete h;

@@ -118,16 +118,17 @@ __global__ void k_pack(int n, int nc, const int32_t *__restrict__ idx, const dou
     out[k] = x[(int64_t)idx[r] * nc + e];
 }
 
-void halo_exchange(Ctx &c, Halo &H, int nc, const double *x_own, double *ghost)
+void halo_exchange(Ctx &c, Halo &H, int nc, const double *x_own, double *ghost, cudaStream_t s)
 {
     if (!c.comm || !H.any()) return;
     const int ns = H.nsend[0] + H.nsend[1];
-    if (ns) k_pack<<<grid_for((int64_t)ns * nc, 256), 256, 0, c.s>>>(ns, nc, H.sidx, x_own, H.sbuf);
+    if (ns) k_pack<<<grid_for((int64_t)ns * nc, 256), 256, 0, s>>>(ns, nc, H.sidx, x_own, H.sbuf);
     c.launches++;
     const size_t b = sizeof(double) * nc;
     c.comm->neighbor_exchange(H.sbuf.p, b * H.nsend[0], ghost, b * H.nrecv[0], H.sbuf.p + (size_t)H.nsend[0] * nc,
-                              b * H.nsend[1], ghost + (size_t)H.nrecv[0] * nc, b * H.nrecv[1], c.s);
+                              b * H.nsend[1], ghost + (size_t)H.nrecv[0] * nc, b * H.nrecv[1], s);
 }
+void halo_exchange(Ctx &c, Halo &H, int nc, const double *x_own, double *ghost) { halo_exchange(c, H, nc, x_own, ghost, c.s); }
 
 // ------------------------------------------------------------------ reduction layout (R-reduce)
 // The global vector [u | f] is cut into SEGMENTS: the u rows of each z-block's node

@@ -151,10 +151,11 @@ template <int ASYM, bool D>
 __global__ void __launch_bounds__(256) k_op_node_sym(SymGeo g, const double *__restrict__ vs, const double *__restrict__ vf,
                                                      const double *__restrict__ gl, const int64_t *__restrict__ off_uf,
                                                      const int32_t *__restrict__ col_uf, const double *__restrict__ val_uf, GV xu,
-                                                     GV xf, double *__restrict__ yu)
+                                                     GV xf, double *__restrict__ yu, Rows R, int cnt)
 {
-    const int n = blockIdx.x * blockDim.x + threadIdx.x;
-    if (n >= g.Nn) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= cnt) return;
+    const int n = row_of(R, t);
     const int x = n % g.NX, y = (n / g.NX) % g.NY, zg = g.zn0 + n / g.NXY;
     double a0 = 0, a1 = 0, a2 = 0;
     // the diagonal and the 13 upper blocks (the row's own stored entries) first, then the 13 lower ones, whose
@@ -357,15 +358,15 @@ void sym_refill_sdc(Ctx &c)
 // ---- launchers used by apply.cu (operator) and amg.cu (level-0 mechanics smoother); the layouts are
 // instantiated for a fully symmetric block and for the poromechanics one (z row and column not symmetric)
 
-bool sym_op_node(Ctx &c, const GV &gu, const GV &gf, double *yu)
+bool sym_op_node(Ctx &c, const GV &gu, const GV &gf, double *yu, Rows R, int cnt)
 {
     if (!c.sym_uu.ok) return false;
     const SymGeo g = sym_geo(c);
     const Sym27 &S = c.sym_uu;
 #define OPS(A)                                                                                                    \
-    (c.comm ? k_op_node_sym<A, true> : k_op_node_sym<A, false>)<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(                    \
-        g, S.val_s, S.val_f, S.gl, c.s_uf.off, c.s_uf.col, c.s_uf.val, gu, gf, yu)
-    if (c.Nn) {
+    (c.comm ? k_op_node_sym<A, true> : k_op_node_sym<A, false>)<<<grid_for(cnt, 256), 256, 0, c.s>>>(                      \
+        g, S.val_s, S.val_f, S.gl, c.s_uf.off, c.s_uf.col, c.s_uf.val, gu, gf, yu, R, cnt)
+    if (cnt) {
         if (c.sym_asym == 0) OPS(0u);
         else OPS(kAsymZ);
     }

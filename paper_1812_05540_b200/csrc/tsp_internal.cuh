@@ -150,6 +150,14 @@ struct Halo {
     int nghost() const { return nrecv[0] + nrecv[1]; }
     bool any() const { return nsend[0] + nsend[1] + nrecv[0] + nrecv[1] > 0; }
 };
+// thread -> row map of a launch over up to two row ranges (the halo overlap launches the interior rows, then
+// the slab's boundary rows): t < na -> r0 + t, else r1 + (t - na)
+struct Rows {
+    int r0, na, r1;
+};
+inline Rows rows_all(int n) { return Rows{0, n, n}; }
+__device__ __forceinline__ int row_of(const Rows &R, int t) { return t < R.na ? R.r0 + t : R.r1 + (t - R.na); }
+
 // ghost-aware vector for kernels: row j < nown is own[j*nc..], else gh[(j-nown)*nc..]
 struct GV {
     const double *own;
@@ -198,6 +206,7 @@ void halo_build(Ctx &c, Halo &H, int nown, int64_t own_off, const int32_t *gcols
 void halo_remap(Ctx &c, const Halo &H, int64_t own_off, const int32_t *gcols, int64_t nnz, int32_t *lcols);
 // exchange: ghost[(nrecv0+nrecv1)*nc] <- neighbours' rows of x_own (nc values per row)
 void halo_exchange(Ctx &c, Halo &H, int nc, const double *x_own, double *ghost);
+void halo_exchange(Ctx &c, Halo &H, int nc, const double *x_own, double *ghost, cudaStream_t s);
 
 // One AMG level (setup products in CSR, apply operators in SELL).
 struct Level {
@@ -276,6 +285,9 @@ struct Ctx {
     int64_t Nn_glob = 0, Nc_glob = 0, n_glob = 0;
     int rank = 0, nranks = 1;
     Comm *comm = nullptr;
+    // halo overlap (comm != nullptr): exchanges run on `cs` while the interior rows run on `s`
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev_x = nullptr, ev_h = nullptr;
     int k0 = 0, k1 = 0;                // owned cell planes [k0, k1)
     int64_t node_off = 0, cell_off = 0;
     Halo hu, hf;                       // fine node / cell halos
@@ -356,7 +368,7 @@ void op_apply(Ctx &c, const double *x, double *y);
 void sym_build(Ctx &c);           // sym_uu / sym_sdc from the uploaded A_uu (tsp_create)
 bool sym_refill_uu(Ctx &c);       // tsp_update_values: sym_uu from the new c.uu.v (false: generic SELL needed)
 void sym_refill_sdc(Ctx &c);      // TSP_SETUP_MECH after an update: sym_sdc from c.uu_sdc
-bool sym_op_node(Ctx &c, const GV &gu, const GV &gf, double *yu);                      // A_uu x_u + A_uf x_f, if sym_uu.ok
+bool sym_op_node(Ctx &c, const GV &gu, const GV &gf, double *yu, Rows R, int cnt);                      // A_uu x_u + A_uf x_f, if sym_uu.ok
 bool sym_vcycle_pre(Ctx &c, int n, const GV &dinv, const GV &b, double *x, double *r);   // level-0 SDC, if sym_sdc.ok
 bool sym_vcycle_post(Ctx &c, int n, const double *dinv, const double *b, const GV &x, double *xo);
 double sym_bytes(const Ctx &c, int bs);   // bytes of one stream over a Sym27 with bs values per block
