@@ -23,9 +23,15 @@ namespace tsp {
 
 // lanes per row from the GLOBAL mean row length (0: sliced-ELL thread per row); measured at C5:
 // 8/16 lanes beat a full warp by 20-35 % on the pressure levels 1-2 and the level-0 restriction
-static int lanes_for(int64_t nnz, int64_t rows)
+// A level too small to fill the GPU even at a full warp per row (rows x 32 <= the SMs' resident threads) is
+// latency-bound, not bandwidth-bound: there every row gets 32 lanes, which shortens each lane's chain of
+// dependent loads (row pointer -> column -> gathered x) to one or two steps.  Measured at C5: the restrictions
+// into mechanics levels 4-6 took 7-28 us with a thread per row (sliced ELL, 8-20 dependent steps).
+static int lanes_for(int64_t nnz, int64_t rows, int sms)
 {
-    if (rows <= 0 || nnz < 12 * rows) return 0;
+    if (rows <= 0) return 0;
+    if (rows * 32 <= (int64_t)sms * 2048) return 32;
+    if (nnz < 12 * rows) return 0;
     return nnz < 40 * rows ? 8 : nnz < 96 * rows ? 16 : 32;
 }
 // test knob TSP_FORCE_LANES=0|8|16|32: every level uses that vector-CSR variant (parity coverage of each
@@ -1043,8 +1049,8 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
                 st.assign(4, 0);
                 for (int r = 0; r < c.nranks; ++r) for (int k = 0; k < 4; ++k) st[k] += all[4 * r + k];
             }
-            L.warpA = l > 0 ? lanes_forced(lanes_for(st[0], st[1])) : 0;
-            L.warpR = lanes_forced(lanes_for(st[2], st[3]));
+            L.warpA = l > 0 ? lanes_forced(lanes_for(st[0], st[1], c.sm_count)) : 0;
+            L.warpR = lanes_forced(lanes_for(st[2], st[3], c.sm_count));
             if (l > 0 && !L.coarsest) c.variants[TSP_VAR_LANES_A0 + lanes_idx(L.warpA)]++;
             if (!L.coarsest) c.variants[TSP_VAR_LANES_R0 + lanes_idx(L.warpR)]++;
         }
@@ -1059,32 +1065,17 @@ void amg_build(Ctx &c, Hier &H, Csr &A0, DBuf<int32_t> &zb0, int nc, Halo *fine_
 }
 
 // ------------------------------------------------------------------ V-cycle kernels (apply; free arithmetic)
-// pre-smooth from zero + residual: x = D^-1 b ; r = b - A D^-1 b   (b, D^-1 ghost-aware)
-template <int NC, bool D>
-__global__ void __launch_bounds__(256) k_vc_pre(int n, const int64_t *__restrict__ off, const int32_t *__restrict__ col,
-                                                const double *__restrict__ val, GV dinv, GV b, double *__restrict__ x,
-                                                double *__restrict__ r)
+// x = D^-1 b over the own values and, on a distributed level, over the ghost values (xg = bg dg): the first
+// half of pre-smoothing from zero on the coarse levels, whose residual r = b - A x then gathers ONE vector
+// (a fused pre-smoothing kernel gathering b and D^-1 per entry was L1-bound: C5 mechanics level 1
+// 152 us against 98 us for the same product in post-smoothing).  The same products b_j D^-1_j as the fused
+// form: results are bitwise unchanged.
+__global__ void k_dscale(int64_t m, const double *__restrict__ b, const double *__restrict__ dinv, double *__restrict__ x,
+                         int64_t mg, const double *__restrict__ bg, const double *__restrict__ dg, double *__restrict__ xg)
 {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int s = i >> 5, lane = i & 31;
-    double acc[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) acc[c] = 0.0;
-    const int64_t b0 = off[s], b1 = off[s + 1];
-#pragma unroll 2
-    for (int64_t slot = b0; slot < b1; ++slot) {
-        const int j = __ldcs(col + slot * 32 + lane);
-#pragma unroll
-        for (int c = 0; c < NC; ++c)
-            acc[c] = fma(__ldcs(val + (slot * NC + c) * 32 + lane), gvld<D>(b, j, c, NC) * gvld<D>(dinv, j, c, NC), acc[c]);
-    }
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        const double bi = b.own[(int64_t)i * NC + c];
-        x[(int64_t)i * NC + c] = bi * dinv.own[(int64_t)i * NC + c];
-        r[(int64_t)i * NC + c] = bi - acc[c];
-    }
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < m) x[t] = b[t] * dinv[t];
+    else if (t - m < mg) xg[t - m] = bg[t - m] * dg[t - m];
 }
 // y = S x  (restriction R r; rows and columns local)
 template <int NC>
@@ -1230,7 +1221,7 @@ __global__ void k_coarse(int n, const double *__restrict__ inv, const double *__
 // group of G lanes (G | 32) per row strides the row's entries (coalesced [q][c] values),
 // then a fixed shuffle tree inside the group.  32/G rows per warp keep several dependent
 // load chains in flight.
-// MODE 0: y = A x ; MODE 1: pre (x = D^-1 b, r = b - A D^-1 b) ; MODE 2: post (xo = x + D^-1 (b - A x));
+// MODE 0: y = A x ; MODE 2: post (xo = x + D^-1 (b - A x));
 // MODE 3: residual r = b - A x ; MODE 4 / 5: fused Chebyshev PRE / STEP (cheb_epi, R-cheb)
 template <int NC, int MODE, bool D, int G>
 __global__ void __launch_bounds__(256) k_csr_vec(int n, const int32_t *__restrict__ rp, const int32_t *__restrict__ ci,
@@ -1250,8 +1241,7 @@ __global__ void __launch_bounds__(256) k_csr_vec(int n, const int32_t *__restric
             const int j = ci[q];
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
-                const double xv = MODE == 1 ? gvld<D>(b, j, c, NC) * gvld<D>(dinv, j, c, NC)
-                                : MODE == 4 ? ca.sc * (gvld<D>(dinv, j, c, NC) * gvld<D>(b, j, c, NC)) : gvld<D>(x, j, c, NC);
+                const double xv = MODE == 4 ? ca.sc * (gvld<D>(dinv, j, c, NC) * gvld<D>(b, j, c, NC)) : gvld<D>(x, j, c, NC);
                 acc[c] = fma(__ldcs(v + q * NC + c), xv, acc[c]);
             }
         }
@@ -1266,7 +1256,6 @@ __global__ void __launch_bounds__(256) k_csr_vec(int n, const int32_t *__restric
         for (int c = 1; c < NC; ++c) if (sub == c) a = acc[c];
         const int64_t t = (int64_t)i * NC + sub;
         if (MODE == 0) out1[t] = a;
-        else if (MODE == 1) { out1[t] = b.own[t] * dinv.own[t]; out2[t] = b.own[t] - a; }
         else if (MODE == 3) out1[t] = b.own[t] - a;
         else if (MODE == 4 || MODE == 5) cheb_epi<MODE == 4>(t, a, b.own[t], dinv.own[t], MODE == 5 ? x.own[t] : 0.0, ca, out1);
         else out1[t] = x.own[t] + dinv.own[t] * (b.own[t] - a);
@@ -1415,9 +1404,15 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     }
     else if (p70) p7_launch(c, 1, gd, gb, gv(nullptr, 0), L.x2, L.r, ChebArgs{});
     else if (sym0) sym_vcycle_pre(c, n, gd, gb, L.x2, L.r);
-    else if (wA) (L.dist ? csr_vec<NC, 1, true> : csr_vec<NC, 1, false>)(wA, c.s, n, L.A, gd, gb, gv(nullptr, 0), L.x2, L.r, ChebArgs{});
-    else if (n) (L.dist ? k_vc_pre<NC, true> : k_vc_pre<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
-        n, L.sA.off, L.sA.col, L.sA.val, gd, gb, L.x2, L.r);
+    else if (n) {                        // coarse level: x = D^-1 b (k_dscale), then r = b - A x
+        const int64_t m = (int64_t)n * NC, mg = L.dist ? (int64_t)L.hp->nghost() * NC : 0;
+        k_dscale<<<grid_for(m + mg, 256), 256, 0, c.s>>>(m, b, L.dinv, L.x2, mg, L.gh_b.p, ghd, L.gh_x.p);
+        c.launches++;
+        const GV gx = gv(L.x2, n, L.dist ? L.gh_x.p : nullptr);
+        if (wA) (L.dist ? csr_vec<NC, 3, true> : csr_vec<NC, 3, false>)(wA, c.s, n, L.A, gv(nullptr, 0), gb, gx, L.r, nullptr, ChebArgs{});
+        else (L.dist ? k_sell_resid<NC, true> : k_sell_resid<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
+            n, L.sA.off, L.sA.col, L.sA.val, b, gx, L.r);
+    }
     prof_end(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P, gs ? gs_sweep_bytes(L, NC) + bA0 + 3 * vec
                                                   : cheb ? (deg - 1) * (bA0 + 5 * vec) + bA0 + 3 * vec : bA0 + 4 * vec);
     // restriction (local rows of R); a replicated next level is gathered on every rank
