@@ -1403,13 +1403,13 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
         level_resid<NC>(c, L, sym0, b, L.x2, L.r);
     }
     else if (p70) p7_launch(c, 1, gd, gb, gv(nullptr, 0), L.x2, L.r, ChebArgs{});
-    else if (sym0) sym_vcycle_pre(c, n, gd, gb, L.x2, L.r);
-    else if (n) {                        // coarse level: x = D^-1 b (k_dscale), then r = b - A x
+    else if (n) {                        // x = D^-1 b (k_dscale), then r = b - A x (one gathered vector)
         const int64_t m = (int64_t)n * NC, mg = L.dist ? (int64_t)L.hp->nghost() * NC : 0;
         k_dscale<<<grid_for(m + mg, 256), 256, 0, c.s>>>(m, b, L.dinv, L.x2, mg, L.gh_b.p, ghd, L.gh_x.p);
         c.launches++;
         const GV gx = gv(L.x2, n, L.dist ? L.gh_x.p : nullptr);
-        if (wA) (L.dist ? csr_vec<NC, 3, true> : csr_vec<NC, 3, false>)(wA, c.s, n, L.A, gv(nullptr, 0), gb, gx, L.r, nullptr, ChebArgs{});
+        if (sym0) sym_vcycle_resid(c, n, b, gx, L.r);
+        else if (wA) (L.dist ? csr_vec<NC, 3, true> : csr_vec<NC, 3, false>)(wA, c.s, n, L.A, gv(nullptr, 0), gb, gx, L.r, nullptr, ChebArgs{});
         else (L.dist ? k_sell_resid<NC, true> : k_sell_resid<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
             n, L.sA.off, L.sA.col, L.sA.val, b, gx, L.r);
     }

@@ -187,8 +187,8 @@ __global__ void __launch_bounds__(256) k_op_node_sym(SymGeo g, const double *__r
     yu[3 * (int64_t)n] = a0; yu[3 * (int64_t)n + 1] = a1; yu[3 * (int64_t)n + 2] = a2;
 }
 
-// level-0 SDC smoother (3 scalar components on one node graph), MODE 1 pre: x = D^-1 b, r = b - A D^-1 b;
-// MODE 2 post: xo = x + D^-1 (b - A x); MODE 3 residual (Gauss-Seidel smoother): out1 = b - A x
+// level-0 SDC smoother (3 scalar components on one node graph; pre-smoothing from zero = amg.cu k_dscale +
+// MODE 3), MODE 2 post: xo = x + D^-1 (b - A x); MODE 3 residual (Gauss-Seidel smoother): out1 = b - A x
 template <int ASYM, int MODE, bool D>
 __global__ void __launch_bounds__(256) k_vc_sym(SymGeo g, const double *__restrict__ vs, const double *__restrict__ vf,
                                                 const double *__restrict__ gl, GV dinv, GV b, GV xin, double *__restrict__ out1,
@@ -208,19 +208,14 @@ __global__ void __launch_bounds__(256) k_vc_sym(SymGeo g, const double *__restri
         const int j = sym_xidx(g, n2);
 #pragma unroll
         for (int cc = 0; cc < 3; ++cc) {
-            const double xv = MODE == 1 ? gvld<D>(b, j, cc, 3) * gvld<D>(dinv, j, cc, 3)
-                            : MODE == 4 ? ca.sc * (gvld<D>(dinv, j, cc, 3) * gvld<D>(b, j, cc, 3)) : gvld<D>(xin, j, cc, 3);
+            const double xv = MODE == 4 ? ca.sc * (gvld<D>(dinv, j, cc, 3) * gvld<D>(b, j, cc, 3)) : gvld<D>(xin, j, cc, 3);
             acc[cc] = fma(B[cc], xv, acc[cc]);
         }
     }
 #pragma unroll
     for (int cc = 0; cc < 3; ++cc) {
         const int64_t t = 3 * (int64_t)n + cc;
-        if (MODE == 1) {
-            const double bi = b.own[t];
-            out1[t] = bi * dinv.own[t];
-            out2[t] = bi - acc[cc];
-        } else if (MODE == 3) {
+        if (MODE == 3) {
             out1[t] = b.own[t] - acc[cc];
         } else if (MODE == 4 || MODE == 5) {
             cheb_epi<MODE == 4>(t, acc[cc], b.own[t], dinv.own[t], MODE == 5 ? xin.own[t] : 0.0, ca, out1);
@@ -371,21 +366,6 @@ bool sym_op_node(Ctx &c, const GV &gu, const GV &gf, double *yu, Rows R, int cnt
         else OPS(kAsymZ);
     }
 #undef OPS
-    return true;
-}
-bool sym_vcycle_pre(Ctx &c, int n, const GV &dinv, const GV &b, double *x, double *r)
-{
-    if (!c.sym_sdc.ok || n != c.Nn) return false;
-    const SymGeo g = sym_geo(c);
-    const Sym27 &S = c.sym_sdc;
-#define VCS(A)                                                                                                    \
-    (c.comm ? k_vc_sym<A, 1, true> : k_vc_sym<A, 1, false>)<<<grid_for(c.Nn, 256), 256, 0, c.s>>>(                        \
-        g, S.val_s, S.val_f, S.gl, dinv, b, gv(nullptr, 0), x, r, ChebArgs{})
-    if (n) {
-        if (c.sym_asym == 0) VCS(0u);
-        else VCS(kAsymZ);
-    }
-#undef VCS
     return true;
 }
 bool sym_vcycle_post(Ctx &c, int n, const double *dinv, const double *b, const GV &x, double *xo)

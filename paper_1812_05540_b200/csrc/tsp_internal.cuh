@@ -369,7 +369,6 @@ void sym_build(Ctx &c);           // sym_uu / sym_sdc from the uploaded A_uu (ts
 bool sym_refill_uu(Ctx &c);       // tsp_update_values: sym_uu from the new c.uu.v (false: generic SELL needed)
 void sym_refill_sdc(Ctx &c);      // TSP_SETUP_MECH after an update: sym_sdc from c.uu_sdc
 bool sym_op_node(Ctx &c, const GV &gu, const GV &gf, double *yu, Rows R, int cnt);                      // A_uu x_u + A_uf x_f, if sym_uu.ok
-bool sym_vcycle_pre(Ctx &c, int n, const GV &dinv, const GV &b, double *x, double *r);   // level-0 SDC, if sym_sdc.ok
 bool sym_vcycle_post(Ctx &c, int n, const double *dinv, const double *b, const GV &x, double *xo);
 double sym_bytes(const Ctx &c, int bs);   // bytes of one stream over a Sym27 with bs values per block
 void prec_apply(Ctx &c, const double *v, double *z);
