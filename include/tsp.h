@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define TSP_ABI_VERSION 4
+#define TSP_ABI_VERSION 5
 
 typedef int tsp_status;
 enum {
@@ -247,6 +247,15 @@ tsp_status tsp_apply_operator(tsp_handle h, const double *x, double *y);
  * error (TSP_ERR_NUMERIC on a non-finite Arnoldi coefficient).  Collective over the ranks; synchronises. */
 tsp_status tsp_solve(tsp_handle h, const double *b, double *x, const tsp_solve_opts *o, tsp_solve_info *info);
 void tsp_default_solve_opts(tsp_solve_opts *o);
+
+/* The "sequential" embedding of Algorithm 1 (remark P:640-642; SURVEY NEXT-f4 iii): stationary Richardson iteration
+ * x <- x + M^-1 (b - A x) from x0, stopped when the TRUE residual ||b - A x|| <= rtol ||b|| (TSP_OK), after
+ * o->max_iters preconditioner applications (TSP_NOT_CONVERGED) or on a non-finite residual norm (TSP_ERR_NUMERIC;
+ * the iteration is a contraction only when M^-1 A has its spectrum inside (0, 2), which one SDC V-cycle as the
+ * mechanics stage does not guarantee -- DESIGN.md section 7).  Same arguments, pointer kinds and info fields as
+ * tsp_solve (o->restart is not read; restarts = reorth = 0; est_relres = true_relres); iterations counts the
+ * preconditioner applications.  Collective over the ranks; synchronises. */
+tsp_status tsp_richardson(tsp_handle h, const double *b, double *x, const tsp_solve_opts *o, tsp_solve_info *info);
 
 tsp_status tsp_get_stats(tsp_handle h, tsp_stats *s);
 

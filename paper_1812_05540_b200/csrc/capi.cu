@@ -465,7 +465,21 @@ tsp_status tsp_apply_operator(tsp_handle h, const double *x, double *y)
     API_END
 }
 
+static tsp_status solve_entry(tsp_handle h, const double *b, double *x, const tsp_solve_opts *o, tsp_solve_info *info,
+                              bool richardson);
+
 tsp_status tsp_solve(tsp_handle h, const double *b, double *x, const tsp_solve_opts *o, tsp_solve_info *info)
+{
+    return solve_entry(h, b, x, o, info, false);
+}
+
+tsp_status tsp_richardson(tsp_handle h, const double *b, double *x, const tsp_solve_opts *o, tsp_solve_info *info)
+{
+    return solve_entry(h, b, x, o, info, true);
+}
+
+static tsp_status solve_entry(tsp_handle h, const double *b, double *x, const tsp_solve_opts *o, tsp_solve_info *info,
+                              bool richardson)
 {
     if (!h || !b || !x) { set_error("null argument"); return TSP_ERR_INVALID_ARG; }
     tsp_solve_opts oo;
@@ -483,7 +497,8 @@ tsp_status tsp_solve(tsp_handle h, const double *b, double *x, const tsp_solve_o
         if (!oo.x0_zero) TSP_CUDA(cudaMemcpyAsync(h->kx, x, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->s));
         db = h->kb; dx = h->kx;
     }
-    krylov_solve(*h, db, dx, oo, inf);
+    if (richardson) richardson_solve(*h, db, dx, oo, inf);
+    else krylov_solve(*h, db, dx, oo, inf);
     if (oo.host_ptrs) {
         TSP_CUDA(cudaMemcpyAsync(x, h->kx, sizeof(double) * h->n, cudaMemcpyDeviceToHost, h->s));
         TSP_CUDA(cudaStreamSynchronize(h->s));

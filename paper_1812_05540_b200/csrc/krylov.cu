@@ -595,20 +595,88 @@ static void run_body(Ctx &c, Kr &K, int j, bool use_graph, F &body)
     K.bytes += G.bytes;
 }
 
+// the solver workspace of restart length m: basis V (m + 1 columns), Z (m), residual, scalars, reduction partials
+static void krylov_reserve(Ctx &c, int m)
+{
+    const int64_t n = c.n, ld = (n + 31) & ~(int64_t)31;
+    if (c.kcap == m && c.V.n == (size_t)(m + 1) * ld) return;
+    krylov_graphs_drop(c);
+    c.V.alloc((size_t)(m + 1) * ld);
+    c.Z.alloc((size_t)m * ld);
+    c.kr.alloc(std::max<int64_t>(n, 1));
+    c.kh.alloc(5 * (m + 2) + 16);
+    c.kpart.alloc((size_t)2 * (m + 2) * std::max(c.nchunk_loc, 1) + 64);
+    c.seg_part.alloc((size_t)2 * (m + 2) * std::max(c.nseg_max, 1) + 64);
+    c.kcap = m;
+}
+
+// x += z
+__global__ void k_xpz(int64_t n, const double *__restrict__ z, double *__restrict__ x)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) x[i] = x[i] + z[i];
+}
+
+// The "sequential" embedding of the remark at P:640-642 (SURVEY NEXT-f4 iii): stationary Richardson iteration
+// x <- x + M^-1 (b - A x) with Algorithm 1 as M^-1, from x0 (zero if o.x0_zero), stopped on the TRUE residual
+// ||b - A x|| <= rtol ||b||, after max_iters preconditioner applications, or on a non-finite residual norm
+// (TSP_ERR_NUMERIC, x = the last finite iterate's successor as computed).  Per iteration: the operator, r = b - r,
+// one norm (allgathered over the ranks), Algorithm 1, x += z -- the FGMRES kernels, no basis.
+void richardson_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, tsp_solve_info &info)
+{
+    const int64_t n = c.n;
+    krylov_reserve(c, c.kcap > 0 ? c.kcap : 1);
+    Kr K(c, 4);
+    double *r = c.kr, *z = c.Z, *dh = c.kh;
+    struct Events {
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        ~Events() { if (e0) cudaEventDestroy(e0); if (e1) cudaEventDestroy(e1); }
+    } ev;
+    TSP_CUDA(cudaEventCreate(&ev.e0)); TSP_CUDA(cudaEventCreate(&ev.e1));
+    TSP_CUDA(cudaEventRecord(ev.e0, c.s));
+    double bn;
+    K.norm(b, dh);
+    TSP_CUDA(cudaMemcpyAsync(&bn, dh, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+    TSP_CUDA(cudaStreamSynchronize(c.s));
+    TSP_REQUIRE(std::isfinite(bn), TSP_ERR_NUMERIC, "non-finite ||b||");
+    if (o.x0_zero && n) TSP_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, c.s));
+    int it = 0, status = TSP_NOT_CONVERGED;
+    for (;;) {
+        op_apply(c, x, r);
+        k_bminus<<<K.nblk, KB, 0, c.s>>>(n, b, r);
+        c.launches++;
+        K.norm(r, dh);
+        double rn;
+        TSP_CUDA(cudaMemcpyAsync(&rn, dh, sizeof(double), cudaMemcpyDeviceToHost, c.s));
+        TSP_CUDA(cudaStreamSynchronize(c.s));
+        info.true_relres = bn > 0.0 ? rn / bn : 0.0;
+        info.est_relres = info.true_relres;
+        if (rn <= o.rtol * bn) { status = TSP_OK; break; }
+        if (!std::isfinite(rn)) { status = TSP_ERR_NUMERIC; break; }
+        if (it >= o.max_iters) { status = TSP_NOT_CONVERGED; break; }
+        prec_apply(c, r, z);
+        prof_begin(c, PK_VEC);
+        k_xpz<<<K.nblk, KB, 0, c.s>>>(n, z, x);
+        prof_end(c, PK_VEC, 24.0 * n);
+        K.bytes += 24.0 * n;
+        c.launches++;
+        ++it;
+    }
+    TSP_CUDA(cudaEventRecord(ev.e1, c.s));
+    TSP_CUDA(cudaEventSynchronize(ev.e1));
+    float ms = 0;
+    TSP_CUDA(cudaEventElapsedTime(&ms, ev.e0, ev.e1));
+    info.iterations = it;
+    info.restarts = 0;
+    info.status = status;
+    info.t_solve_s = ms * 1e-3;
+    info.bytes_krylov = K.bytes;
+}
+
 void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, tsp_solve_info &info)
 {
     const int m = std::max(1, std::min(o.restart, 120));
     const int64_t n = c.n, ld = (n + 31) & ~(int64_t)31;
-    if (c.kcap != m || c.V.n != (size_t)(m + 1) * ld) {
-        krylov_graphs_drop(c);
-        c.V.alloc((size_t)(m + 1) * ld);
-        c.Z.alloc((size_t)m * ld);
-        c.kr.alloc(std::max<int64_t>(n, 1));
-        c.kh.alloc(5 * (m + 2) + 16);
-        c.kpart.alloc((size_t)2 * (m + 2) * std::max(c.nchunk_loc, 1) + 64);
-        c.seg_part.alloc((size_t)2 * (m + 2) * std::max(c.nseg_max, 1) + 64);
-        c.kcap = m;
-    }
+    krylov_reserve(c, m);
     Kr K(c, 2 * (m + 2));
     double *V = c.V, *Z = c.Z, *r = c.kr;
     // device scalars: d = pass-1 dots [0, 2(j+1)), then alpha, h_j, rho right behind them

@@ -455,6 +455,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t phase)
 // Krylov (krylov.cu)
 void krylov_graphs_drop(Ctx &c);
 void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, tsp_solve_info &info);
+void richardson_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, tsp_solve_info &info);
 
 }  // namespace tsp
 

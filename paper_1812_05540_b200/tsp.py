@@ -164,6 +164,7 @@ def lib():
         L.tsp_apply_operator.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.tsp_solve.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, _P(tsp_solve_opts), _P(tsp_solve_info)]
         L.tsp_default_solve_opts.argtypes = [_P(tsp_solve_opts)]
+        L.tsp_richardson.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, _P(tsp_solve_opts), _P(tsp_solve_info)]
         L.tsp_default_solve_opts.restype = None
         L.tsp_get_stats.argtypes = [C.c_void_p, _P(tsp_stats)]
         L.tsp_level_sizes.argtypes = [C.c_void_p, C.c_int, C.c_int, _P(C.c_int64)]
@@ -197,14 +198,14 @@ def lib():
         L.tsp_default_newton_opts.restype = None
         L.tsp_newton_step.argtypes = [C.c_void_p, _P(tsp_asm_params), _P(tsp_cell_fields), C.c_double, C.c_void_p, C.c_void_p,
                                       C.c_void_p, _P(tsp_newton_opts), _P(tsp_newton_info)]
-        if L.tsp_abi_version() != 4:
+        if L.tsp_abi_version() != 5:
             raise RuntimeError("libtsp ABI version mismatch")
         _LIB = L
     return _LIB
 
 
 EXPORTED = ["tsp_abi_version", "tsp_last_error", "tsp_default_options", "tsp_create", "tsp_setup", "tsp_update_values",
-            "tsp_apply_preconditioner", "tsp_apply_operator", "tsp_solve", "tsp_default_solve_opts",
+            "tsp_apply_preconditioner", "tsp_apply_operator", "tsp_solve", "tsp_default_solve_opts", "tsp_richardson",
             "tsp_get_stats", "tsp_level_sizes", "tsp_export_level", "tsp_prof_enable", "tsp_prof_read",
             "tsp_prof_classes", "tsp_export_cpr", "tsp_destroy", "tsp_nccl_unique_id", "tsp_local_world_create", "tsp_local_world_destroy",
             "tsp_partition", "tsp_level_dist", "tsp_variant_counts", "tsp_export_colour",
@@ -516,6 +517,16 @@ class Tsp:
         return dict(iterations=info.iterations, restarts=info.restarts, status=STATUS.get(info.status, info.status),
                     est_relres=info.est_relres, true_relres=info.true_relres, t_solve_s=info.t_solve_s,
                     reorth=info.reorth, bytes_krylov=info.bytes_krylov, dcgs_fallbacks=info.dcgs_fallbacks)
+
+    def richardson(self, b, x, rtol=1e-8, max_iters=1000, x0_zero=True):
+        """Sequential embedding x <- x + M^-1 (b - A x); arguments as solve()."""
+        host = isinstance(b, np.ndarray)
+        o = tsp_solve_opts(rtol, 1, max_iters, int(x0_zero), int(host))
+        info = tsp_solve_info()
+        rc = lib().tsp_richardson(self.h, _ptr(b), _ptr(x), C.byref(o), C.byref(info))
+        _check(rc, "tsp_richardson", ok=(0, 1, -8))
+        return dict(iterations=info.iterations, status=STATUS.get(info.status, info.status),
+                    true_relres=info.true_relres, t_solve_s=info.t_solve_s)
 
     def stats(self):
         s = tsp_stats()

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
     from paper_1812_05540_b200 import lib as load, EXPORTED
     L = load()
-    assert L.tsp_abi_version() == 4
+    assert L.tsp_abi_version() == 5
     for n in EXPORTED:
         getattr(L, n)
 
