@@ -1373,6 +1373,7 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
 {
     Level &L = H.L[l];
     const bool mech = NC == 3;
+    const int l0 = l == 0 ? PK_VC_L0 : 0;    // level 0 has profile classes of its own
     if (L.coarsest) {
         prof_begin(c, PK_COARSE);
         if (L.n) k_coarse<NC><<<dim3(grid_for(L.n, 128), NC), 128, 0, c.s>>>(L.n, L.cinv, b, xout);
@@ -1394,7 +1395,7 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     const bool gs = H.smoother == 1;         // Gauss-Seidel (gs.cu, R-gs): single GPU, never distributed
     const bool cheb = H.smoother == 2;       // Chebyshev (R-cheb)
     const int deg = c.o.amg_cheb_degree;
-    prof_begin(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P);
+    prof_begin(c, (mech ? PK_VC_PRE_U : PK_VC_PRE_P) + l0);
     if (gs) {
         gs_sweep<NC>(c, L, false, b, nullptr, L.x2);                      // forward sweep from zero
         level_resid<NC>(c, L, sym0, b, L.x2, L.r);
@@ -1413,17 +1414,17 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
         else (L.dist ? k_sell_resid<NC, true> : k_sell_resid<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
             n, L.sA.off, L.sA.col, L.sA.val, b, gx, L.r);
     }
-    prof_end(c, mech ? PK_VC_PRE_U : PK_VC_PRE_P, gs ? gs_sweep_bytes(L, NC) + bA0 + 3 * vec
+    prof_end(c, (mech ? PK_VC_PRE_U : PK_VC_PRE_P) + l0, gs ? gs_sweep_bytes(L, NC) + bA0 + 3 * vec
                                                   : cheb ? (deg - 1) * (bA0 + 5 * vec) + bA0 + 3 * vec : bA0 + 4 * vec);
     // restriction (local rows of R); a replicated next level is gathered on every rank
     Level &Lc = H.L[l + 1];
     const bool gather = L.dist && !L.next_dist;
     const int nr = L.sR.nrows;
     double *rdst = gather ? L.rep_buf.p + (size_t)c.nranks * 0 : Lc.b.p;
-    prof_begin(c, mech ? PK_VC_RESTR_U : PK_VC_RESTR_P);
+    prof_begin(c, (mech ? PK_VC_RESTR_U : PK_VC_RESTR_P) + l0);
     if (wR) csr_vec<NC, 0, false>(wR, c.s, nr, L.R, gv(nullptr, 0), gv(nullptr, 0), gv(L.r, n), rdst, nullptr, ChebArgs{});
     else if (nr) k_sell_mv<NC><<<grid_for(nr, 256), 256, 0, c.s>>>(nr, L.sR.off, L.sR.col, L.sR.val, L.r, rdst);
-    prof_end(c, mech ? PK_VC_RESTR_U : PK_VC_RESTR_P, bR + vec + 8.0 * NC * nr);
+    prof_end(c, (mech ? PK_VC_RESTR_U : PK_VC_RESTR_P) + l0, bR + vec + 8.0 * NC * nr);
     if (gather) {
         int64_t mx = 1;
         for (auto v : L.rep_counts) mx = std::max(mx, v);
@@ -1433,13 +1434,13 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
         c.launches++;
     }
     vcycle_rec<NC>(c, H, l + 1, Lc.b, Lc.x);
-    prof_begin(c, mech ? PK_VC_PROL_U : PK_VC_PROL_P);
+    prof_begin(c, (mech ? PK_VC_PROL_U : PK_VC_PROL_P) + l0);
     if (n) k_prolong<NC><<<grid_for(n, 256), 256, 0, c.s>>>(n, L.sP.off, L.sP.col, L.sP.val, Lc.x, L.x2);
-    prof_end(c, mech ? PK_VC_PROL_U : PK_VC_PROL_P, sbytes(L.sP) + 2 * vec + 8.0 * NC * Lc.n);
+    prof_end(c, (mech ? PK_VC_PROL_U : PK_VC_PROL_P) + l0, sbytes(L.sP) + 2 * vec + 8.0 * NC * Lc.n);
     // post-smooth (needs x of the ghost rows)
     if (L.dist && !cheb) halo_exchange(c, *L.hp, NC, L.x2, L.gh_x);
     const GV gx = gv(L.x2, n, L.dist ? L.gh_x.p : nullptr);
-    prof_begin(c, mech ? PK_VC_POST_U : PK_VC_POST_P);
+    prof_begin(c, (mech ? PK_VC_POST_U : PK_VC_POST_P) + l0);
     if (gs) gs_sweep<NC>(c, L, true, b, L.x2, xout);                      // backward sweep
     else if (cheb) cheb_run<NC>(c, L, sym0, b, L.x2, xout, L.xc, false);
     else if (p70) p7_launch(c, 2, gv(L.dinv, n), gv(b, n), gx, xout, nullptr, ChebArgs{});
@@ -1447,7 +1448,7 @@ static void vcycle_rec(Ctx &c, Hier &H, int l, const double *b, double *xout)
     else if (wA) (L.dist ? csr_vec<NC, 2, true> : csr_vec<NC, 2, false>)(wA, c.s, n, L.A, gv(L.dinv, n), gv(b, n), gx, xout, nullptr, ChebArgs{});
     else if (n) (L.dist ? k_vc_post<NC, true> : k_vc_post<NC, false>)<<<grid_for(n, 256), 256, 0, c.s>>>(
         n, L.sA.off, L.sA.col, L.sA.val, L.dinv, b, gx, xout);
-    prof_end(c, mech ? PK_VC_POST_U : PK_VC_POST_P, gs ? gs_sweep_bytes(L, NC) : cheb ? deg * (bA0 + 5 * vec) : bA0 + 4 * vec);
+    prof_end(c, (mech ? PK_VC_POST_U : PK_VC_POST_P) + l0, gs ? gs_sweep_bytes(L, NC) : cheb ? deg * (bA0 + 5 * vec) : bA0 + 4 * vec);
     c.launches += 4;
 }
 

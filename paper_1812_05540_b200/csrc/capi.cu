@@ -128,7 +128,9 @@ void *scratch(Ctx &c, size_t bytes)
 
 static const char *kProfNames[PK_COUNT] = {
     "op_node", "op_cell", "step2", "step34", "ilu_steps678", "vc_pre_u", "vc_restr_u", "vc_prol_u", "vc_post_u",
-    "vc_pre_p", "vc_restr_p", "vc_prol_p", "vc_post_p", "coarse", "mdot", "maxpy", "norm", "vec", "setup"};
+    "vc_pre_p", "vc_restr_p", "vc_prol_p", "vc_post_p", "coarse", "mdot", "maxpy", "norm", "vec", "setup",
+    "vc_pre_u_l0", "vc_restr_u_l0", "vc_prol_u_l0", "vc_post_u_l0", "vc_pre_p_l0", "vc_restr_p_l0", "vc_prol_p_l0",
+    "vc_post_p_l0"};
 
 // Every launch of a profiled class is bracketed by two events from a pool that
 // grows on demand (up to 4M events); prof_end only closes a record that the

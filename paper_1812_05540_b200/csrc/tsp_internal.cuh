@@ -262,8 +262,14 @@ struct Hier {
 enum ProfClass {
     PK_OP_NODE, PK_OP_CELL, PK_STEP2, PK_STEP34, PK_ILU, PK_VC_PRE_U, PK_VC_RESTR_U, PK_VC_PROL_U, PK_VC_POST_U,
     PK_VC_PRE_P, PK_VC_RESTR_P, PK_VC_PROL_P, PK_VC_POST_P, PK_COARSE, PK_DOT, PK_AXPY, PK_NORM, PK_VEC, PK_SETUP,
+    // the same eight V-cycle classes on level 0 alone (the bandwidth-bound launches; the classes above then hold
+    // levels >= 1, which are latency-bound): same order, PK_VC_L0 apart
+    PK_VC_PRE_U0, PK_VC_RESTR_U0, PK_VC_PROL_U0, PK_VC_POST_U0, PK_VC_PRE_P0, PK_VC_RESTR_P0, PK_VC_PROL_P0, PK_VC_POST_P0,
     PK_COUNT
 };
+
+constexpr int PK_VC_L0 = PK_VC_PRE_U0 - PK_VC_PRE_U;
+static_assert(PK_COUNT <= TSP_PROF_MAX, "too many profile classes");
 
 struct Prof {
     bool on = false;

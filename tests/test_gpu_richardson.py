@@ -160,3 +160,28 @@ def test_sharded_bitwise_equals_single(dev):
     f = np.concatenate([x[3 * lp.Nn:] for x, _, lp in parts])
     assert np.array_equal(np.concatenate([u, f]), x1)
     assert all(i["true_relres"] == i1["true_relres"] and i["iterations"] == 6 for _, i, _ in parts)
+
+
+def test_profile_classes_cover_the_iteration(dev):
+    """tsp_prof_*: every launch of Algorithm 1 / the operator / DCGS2 lands in a class; level 0 of each V-cycle has
+    classes of its own (the bandwidth-bound launches bench.py's roofline table reads) and profiling does not change
+    the iterates."""
+    pb, o, g = _pair("C1")
+    b = _cuda(pb.b)
+    x0 = torch.zeros(pb.n, dtype=torch.float64, device=dev)
+    i0 = g.solve(b, x0)
+    g.prof_enable(True)
+    x1 = torch.zeros_like(x0)
+    i1 = g.solve(b, x1)
+    p = g.prof_read()
+    g.prof_enable(False)
+    assert i1["iterations"] == i0["iterations"] and torch.equal(x0, x1)
+    it = i1["iterations"]
+    for nm in ("vc_pre_u_l0", "vc_restr_u_l0", "vc_prol_u_l0", "vc_post_u_l0", "vc_pre_p_l0", "vc_restr_p_l0",
+               "vc_prol_p_l0", "vc_post_p_l0", "step2", "step34", "ilu_steps678"):
+        assert p[nm]["launches"] == it and p[nm]["ms"] > 0 and p[nm]["bytes"] > 0, nm
+    lv = g.stats()["levels"]
+    n_of = lambda nm: p.get(nm, dict(launches=0))["launches"]
+    assert n_of("vc_pre_u") == it * (lv[0] - 2) and n_of("vc_pre_p") == it * (lv[1] - 2)      # levels 1 .. coarsest - 1
+    assert p["coarse"]["launches"] == 2 * it
+    assert p["op_node"]["launches"] == p["op_cell"]["launches"] >= it
