@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(KB) k_dcgs_update(int j, const double *__restr
     double nrm = 0.0;
     for (int64_t r = beg + threadIdx.x; r < end; r += KB) {
         double su = 0.0, sa = 0.0;
+        const double ur = u[r], wr = w[r];                 // in flight with the first basis loads
         int t = 0;
         for (; t + UL <= j; t += UL) {
             double vv[UL];
@@ -321,12 +322,16 @@ __global__ void __launch_bounds__(KB) k_dcgs_update(int j, const double *__restr
 #pragma unroll
             for (int q = 0; q < UL; ++q) { su = fma(ss[t + q], vv[q], su); sa = fma(as[t + q], vv[q], sa); }
         }
-        for (; t < j; ++t) {
-            const double vv = __ldcs(V + t * ldv + r);
-            su = fma(ss[t], vv, su); sa = fma(as[t], vv, sa);
+        if (t < j) {                                       // the last j % UL columns: loads issued together, same fma order
+            double vv[UL];
+#pragma unroll
+            for (int q = 0; q < UL; ++q) vv[q] = t + q < j ? __ldcs(V + (t + q) * ldv + r) : 0.0;
+#pragma unroll
+            for (int q = 0; q < UL; ++q)
+                if (t + q < j) { su = fma(ss[t + q], vv[q], su); sa = fma(as[t + q], vv[q], sa); }
         }
-        const double v = (u[r] - su) / alpha;
-        const double wn = (w[r] - sa) - hj * v;
+        const double v = (ur - su) / alpha;
+        const double wn = (wr - sa) - hj * v;
         u[r] = v;
         w[r] = wn;
         nrm = fma(wn, wn, nrm);
