@@ -579,7 +579,13 @@ def main():
                            "apply_gbs": st["bytes_apply"] / (apply_ms * 1e-3) / 1e9},
             "iteration_roofline": {"bytes_per_iter": bytes_iter, "achieved_gbs": iter_gbs, "peak_gbs": hbm,
                                    "frac": iter_gbs / hbm, "mean_krylov_index": mean_j,
-                                   "reorth_fraction": reorth_frac},
+                                   "reorth_fraction": reorth_frac,
+                                   # SURVEY.md section 8(d)'s own count (generic layouts, CGS2 with 4 basis passes):
+                                   # 1.97 kB per DoF per iteration; the library moves fewer bytes (structured
+                                   # symmetric A_uu, two basis passes), so this fraction is the time against
+                                   # the survey's roofline time, not a bandwidth
+                                   "survey_bytes_per_iter": 1970.0 * n_glob,
+                                   "frac_on_survey_bytes": 1970.0 * n_glob / (solve_ms * 1e-3 / max(iters, 1)) / 1e9 / hbm},
             "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": ncu_traffic(dname)[0], "ncu_dram_pct": ncu_traffic(dname)[1],
                          "peak_source": peak_src,
