@@ -18,7 +18,7 @@ def col(name, r):
 # profile class of bench.py's kernel table <- kernel name (first match wins)
 CLASSES = [("op_node", "k_op_node_sym"), ("op_cell", "k_op_cell<0"), ("op_cell_fused", "k_op_cell<2"), ("step2", "k_op_cell<1"),
            ("step34", "k_step34"), ("ilu_steps678", "k_ilu_apply2"), ("mdot", "k_mdot2"), ("maxpy", "k_dcgs_update"),
-           ("vc_resid_u_l0", "k_vc_sym<484, 1"), ("vc_post_u_l0", "k_vc_sym<484, 2"), ("vc_dscale_u_l0", "k_dscale"),
+           ("vc_resid_u_l0", ", 3, 0>(SymGeo"), ("vc_post_u_l0", ", 2, 0>(SymGeo"), ("vc_dscale_u_l0", "k_dscale"),
            ("vc_p7", "k_p7<")]
 out, seen = {}, set()
 print(f"{'kernel':46s} {'ms':>8s} {'rd GB':>8s} {'wr GB':>8s} {'DRAM%':>6s} {'warps%':>6s} {'regs':>4s} {'grid':>8s}")
