@@ -57,6 +57,22 @@ for cfg in cfgs:
     a1.record()
     torch.cuda.synchronize()
     apply_ms = a0.elapsed_time(a1) / 20
+    st = g.stats()
+    last = steps[-1][3]
+    cyc = last["restarts"] + 2
+    bytes_iter = (st["bytes_iter_base"] * it + st["bytes_operator"] * cyc + last["bytes_krylov"]) / max(it, 1)
+    try:
+        hbm = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except Exception:
+        hbm = 6650.0
+    H_g = [g.hierarchy(w) for w in (0, 1)]
+    rng = np.random.default_rng(5)
+    v_par = rng.uniform(-1, 1, pb.n)
+    zt = torch.empty_like(b)
+    g.apply_preconditioner(torch.from_numpy(v_par).to(dev), zt)
+    z_gpu = zt.cpu().numpy()
+    clk = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,clocks.mem,clocks_throttle_reasons.active", "--format=csv,noheader"],
+                         capture_output=True, text=True).stdout.strip()
     g.close()
     # the oracle, full step on the same input
     t0 = time.perf_counter()
@@ -65,6 +81,13 @@ for cfg in cfgs:
     xo, io = o.solve(pb.b, rtol=1e-8, m=64)
     t2 = time.perf_counter()
     fwd_orc = float(np.linalg.norm(xo - pb.x_rand) / np.linalg.norm(pb.x_rand))
+    # parity results of this record: hierarchies bitwise, one application, |delta it|
+    keys = ("A_rp", "A_ci", "A_v", "dl1")
+    hier_ok = all(len(H_g[w]) == o.num_levels(w) and all(
+        all(np.array_equal(lo[k], lg[k]) for k in keys + (() if lo["coarsest"] else ("agg", "P_rp", "P_ci", "P_v")))
+        for lo, lg in zip(o.hierarchy(w), H_g[w])) for w in (0, 1))
+    z_orc = o.apply(v_par)
+    apply_err = float(np.linalg.norm(z_gpu - z_orc) / np.linalg.norm(z_orc))
     nproc = os.cpu_count()
     env = dict(os.environ, ORACLE_OMP="1", OMP_NUM_THREADS=str(nproc))
     out = subprocess.run([sys.executable, os.path.join(os.path.dirname(os.path.abspath(__file__)), "oracle_run.py"), cfg],
@@ -75,7 +98,12 @@ for cfg in cfgs:
                    "step_ms": su + so, "forward_error": fwd_gpu,
                    "iters_per_s": it / ((su + so) * 1e-3), "ms_per_iter": so / max(it, 1),
                    "apply_ms": apply_ms, "apply_gdof_per_s": pb.n / (apply_ms * 1e-3) / 1e9,
-                   "true_relres": steps[-1][3]["true_relres"]},
+                   "true_relres": steps[-1][3]["true_relres"],
+                   "iteration_roofline": {"bytes_per_iter": bytes_iter, "achieved_gbs": bytes_iter / (so / max(it, 1) * 1e-3) / 1e9,
+                                          "peak_gbs": hbm, "frac": bytes_iter / (so / max(it, 1) * 1e-3) / 1e9 / hbm},
+                   "levels": st["levels"], "clocks_sm_mem_reasons": clk},
+           "parity": {"hierarchies_bit_exact": bool(hier_ok), "apply_rel_err": apply_err,
+                      "delta_iterations": int(abs(io["iterations"] - it))},
            "oracle": {"iterations": io["iterations"], "status": io["status"], "setup_s": t1 - t0, "solve_s": t2 - t1,
                       "forward_error": fwd_orc, "true_relres": io["true_relres"], "cpu_model": cpu_model,
                       "host_nproc": os.cpu_count(),
