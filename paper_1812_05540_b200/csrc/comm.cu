@@ -86,6 +86,7 @@ struct NcclComm : Comm {
     {
         TSP_NCCL(nccl().AllGather(send, recv, bytes, ncclChar, comm, s));
     }
+    bool capturable() const override { return true; }      // NCCL >= 2.9 collectives and grouped send/recv capture
 };
 
 // ------------------------------------------------------------------ in-process test world

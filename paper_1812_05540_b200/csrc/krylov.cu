@@ -700,7 +700,11 @@ void krylov_solve(Ctx &c, const double *b, double *x, const tsp_solve_opts &o, t
     if ((int)c.kgraph.size() != m) { krylov_graphs_drop(c); c.kgraph.resize(m); }
     // CUDA graphs for the iteration body: one rank, no profiling (its events are per launch)
     const bool no_graph = getenv("TSP_NO_GRAPH") != nullptr;
-    const bool use_graph = !c.comm && !c.prof.on && !no_graph;
+    // sharded handles: only on request (TSP_NCCL_GRAPH=1) and only over a transport whose calls are pure stream
+    // work (NCCL; the halo overlap's comm stream forks from and rejoins the capturing stream through its two
+    // events).  Off by default: this build had one GPU, so the captured NCCL iteration was never executed.
+    const bool comm_graph = c.comm && c.comm->capturable() && getenv("TSP_NCCL_GRAPH") != nullptr;
+    const bool use_graph = (!c.comm || comm_graph) && !c.prof.on && !no_graph;
     const bool no_fuse = getenv("TSP_NO_OP_FUSE") != nullptr;   // test knob (read per solve): the full operator every iteration
     double bn;
     K.norm(b, dh);

@@ -134,6 +134,8 @@ struct Comm {
                                    const void *send_hi, size_t bytes_send_hi, void *recv_hi, size_t bytes_recv_hi,
                                    cudaStream_t s) = 0;
     virtual void allgather(const void *send, void *recv, size_t bytes, cudaStream_t s) = 0;
+    // true when every call only enqueues stream work (no host-side rendezvous), so a stream capture may hold it
+    virtual bool capturable() const { return false; }
 };
 Comm *make_comm(int kind, void *arg, int rank, int nranks);
 template <class T> std::vector<T> host_allgather(Ctx &c, const std::vector<T> &mine);
