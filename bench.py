@@ -39,9 +39,11 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(kernel_class):
+def ncu_traffic(kernel_class, workload="C5", ws=1):
     """(DRAM bytes per launch, ncu DRAM % of peak) of a kernel class from the committed ncu --set full
-    capture, or (None, None)."""
+    capture, or (None, None).  The capture was taken at C5 on one GPU: any other workload gets null."""
+    if workload != "C5" or ws != 1:
+        return None, None
     try:
         with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
             k = json.load(f)["kernels"][kernel_class]
@@ -587,7 +589,8 @@ def main():
                                    "survey_bytes_per_iter": 1970.0 * n_glob,
                                    "frac_on_survey_bytes": 1970.0 * n_glob / (solve_ms * 1e-3 / max(iters, 1)) / 1e9 / hbm},
             "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": ncu_traffic(dname)[0], "ncu_dram_pct": ncu_traffic(dname)[1],
+                         "frac": achieved / hbm, "traffic": ncu_traffic(dname, args.config, ws)[0],
+                         "ncu_dram_pct": ncu_traffic(dname, args.config, ws)[1],
                          "peak_source": peak_src,
                          "measured": "CUDA events around every launch of this class on the launching stream, in one "
                                      "profiled step right after the timed region (the timed steps run unprofiled)",
