@@ -9,6 +9,12 @@
 //   U_KK = A_KK - sum_{J<K, same tile} A_KJ D_J A_JK
 //   forward   yhat_K = D_K (w_K - sum_{J<K} A_KJ yhat_J)
 //   backward  x_K    = yhat_K - D_K sum_{J>K} A_KJ x_J
+// Steps 6-8 without streaming the in-tile lower blocks twice (Eisenstat's trick for M = (D + L) D^-1 (D + U), D = U_KK,
+// L / U = the in-tile lower / upper blocks, S^FS = L + S_KK + U + C with C the couplings that leave the tile):
+//   M^-1 (y - S z) = (I + D^-1 U)^-1 [ (D + L)^-1 (y - E z - U z - C z) - z ],   E = S_KK - U_KK,
+// so the residual phase reads the diagonal slot (holding E after the factorisation), the upper blocks and the few
+// lower blocks that cross the tile boundary; L is streamed once, by the forward sweep.  The same operator as
+// w = y - S z followed by the two sweeps, in a different association of the sums (TSP_ILU_PLAIN_RESID: the old form).
 // B200 mapping: one CTA per tile; the tile is swept by x-LINES in (j+k)
 // wavefront order (31 levels for 16^3 instead of 46 cell levels), each line
 // held by a W-lane warp segment.  Inside a line the x-recurrence is affine,
@@ -90,9 +96,10 @@ __device__ __forceinline__ void mm2(const double a[4], const double b[4], double
 
 // a5: one thread per x-line, lines in (j+k) order, cells along x sequential
 // plain = 1 (second stage = hybrid block GS): D_K = A_KK^-1 without the ILU Schur updates
+// eis = 1: slot 3 of `ival` (the diagonal block S_KK, read by this cell only) is replaced by E_K = S_KK - U_KK
 __global__ void k_ilu_factor(TileGeo g, const int32_t *__restrict__ lines, const int32_t *__restrict__ lvlptr,
-                             const double *__restrict__ ival, double *__restrict__ dinv, unsigned long long *__restrict__ npert,
-                             int plain)
+                             double *__restrict__ ival, double *__restrict__ dinv, unsigned long long *__restrict__ npert,
+                             int plain, int eis)
 {
     const int64_t t = blockIdx.x;
     const int TI = t % g.ntx, TJ = (t / g.ntx) % g.nty, TK = t / ((int64_t)g.ntx * g.nty);
@@ -102,8 +109,9 @@ __global__ void k_ilu_factor(TileGeo g, const int32_t *__restrict__ lines, const
             if (TJ * g.ty + lj >= g.ny || TK * g.tz + lk >= g.nz) continue;
             const int len = min(g.tx, g.nx - TI * g.tx);
             for (int li = 0; li < len; ++li) {
-                double U[4];
+                double U[4], S0[4];
                 ld2x2(ival, g, t, lk, lj, 3, li, U);
+                for (int e = 0; e < 4; ++e) S0[e] = U[e];
                 for (int s = 0; s < (plain ? 0 : 3); ++s) {
                     int nlk = lk, nlj = lj, nli = li;
                     if (s == 0) nlk--; else if (s == 1) nlj--; else nli--;
@@ -127,6 +135,8 @@ __global__ void k_ilu_factor(TileGeo g, const int32_t *__restrict__ lines, const
                 dinv[didx(g, t, lk, lj, 1, li)] = -U[1] / det;
                 dinv[didx(g, t, lk, lj, 2, li)] = -U[2] / det;
                 dinv[didx(g, t, lk, lj, 3, li)] = U[0] / det;
+                if (eis)
+                    for (int e = 0; e < 4; ++e) ival[vidx(g, t, lk, lj, 3, e, li)] = S0[e] - U[e];
             }
         }
         __syncthreads();
@@ -179,6 +189,7 @@ __device__ __forceinline__ void pf_load_dir(const double *__restrict__ ival, con
         _Pragma("unroll") for (int s = S0; s < S1; ++s) {                                                        \
             const int ni = gi + dxs[s], nj = gj + dys[s], nk = gk + dzs[s];                                      \
             use[s] = ni >= 0 && nj >= 0 && ni < g.nx && nj < g.ny;                                               \
+            if (EIS && ((s == 0 && lk > 0) || (s == 1 && lj > 0) || (s == 2 && li > 0))) use[s] = false;         \
             const double *p0 = zs, *p1 = zp;                                                                     \
             int64_t q = gc + dxs[s] + dys[s] * sy + dzs[s] * sz;                                                 \
             if (dzs[s] < 0 && nk < 0) {                                                                          \
@@ -188,7 +199,9 @@ __device__ __forceinline__ void pf_load_dir(const double *__restrict__ ival, con
             }                                                                                                    \
             if (!use[s]) { p0 = zs; p1 = zp; q = gc; }                                                           \
             Z0[s] = __ldg(p0 + q); Z1[s] = __ldg(p1 + q);                                                        \
-            _Pragma("unroll") for (int e = 0; e < 4; ++e) AA[s][e] = __ldg(ival + vidx(g, t, lk, lj, s, e, li)); \
+            /* a skipped slot re-reads the cell's diagonal slot (needed anyway, a cache hit): no branch */      \
+            const int sl = (EIS && !use[s]) ? 3 : s;                                                             \
+            _Pragma("unroll") for (int e = 0; e < 4; ++e) AA[s][e] = __ldg(ival + vidx(g, t, lk, lj, sl, e, li)); \
         }                                                                                                        \
         _Pragma("unroll") for (int s = S0; s < S1; ++s)                                                          \
             if (use[s]) {                                                                                        \
@@ -213,7 +226,7 @@ __device__ __forceinline__ unsigned long long gtimer() { unsigned long long t; a
 #else
 #define ILU_T(k) do { } while (0)
 #endif
-template <bool BGS>
+template <bool BGS, bool EIS>
 __global__ void __launch_bounds__(256, 3) k_ilu_apply2(TileGeo g, const int32_t *__restrict__ lines, const int32_t *__restrict__ lvlptr,
                                                     const double *__restrict__ ival, const double *__restrict__ dinv,
                                                     const double *__restrict__ yf, const double *__restrict__ zs,
@@ -229,7 +242,7 @@ __global__ void __launch_bounds__(256, 3) k_ilu_apply2(TileGeo g, const int32_t 
     const int li = lseg, gi = TI * g.tx + li;
     const bool xin = li < g.tx && gi < g.nx;
     ILU_T(0);
-    // ---------------- phase 0: w = y - S^FS z (step 6)
+    // ---------------- phase 0: w = y - S^FS z (step 6); EIS: y - E z - U z - C z
     for (int line = slot0; line < g.ty * g.tz; line += nslots) {
         const int lj = line % g.ty, lk = line / g.ty;
         const int gj = TJ * g.ty + lj, gk = TK * g.tz + lk;
@@ -291,8 +304,8 @@ __global__ void __launch_bounds__(256, 3) k_ilu_apply2(TileGeo g, const int32_t 
         if (ok) { sm[sidx(g, lk, lj, li)] = c[0]; sm[sidx(g, lk, lj, li) + 1] = c[1]; }
         if (BGS && ok) {                          // hybrid block GS: the forward sweep is the whole M_L (step 8)
             const int64_t gc = gi + sy * (TJ * g.ty + lj) + sz * (TK * g.tz + lk);
-            zout[2 * gc] = zs[gc] + c[0];
-            zout[2 * gc + 1] = zp[gc] + c[1];
+            zout[2 * gc] = EIS ? c[0] : zs[gc] + c[0];          // EIS: z + ((D + L)^-1 (..) - z)
+            zout[2 * gc + 1] = EIS ? c[1] : zp[gc] + c[1];
         }
         __syncthreads();
     }
@@ -316,8 +329,8 @@ __global__ void __launch_bounds__(256, 3) k_ilu_apply2(TileGeo g, const int32_t 
                 t0 += P[4] * x0 + P[5] * x1; t1 += P[6] * x0 + P[7] * x1;
             }
             const double *D = P + 12;
-            c[0] = sm[sidx(g, lk, lj, li)] - (D[0] * t0 + D[1] * t1);
-            c[1] = sm[sidx(g, lk, lj, li) + 1] - (D[2] * t0 + D[3] * t1);
+            c[0] = (EIS ? sm[sidx(g, lk, lj, li)] - zn0 : sm[sidx(g, lk, lj, li)]) - (D[0] * t0 + D[1] * t1);
+            c[1] = (EIS ? sm[sidx(g, lk, lj, li) + 1] - zn1 : sm[sidx(g, lk, lj, li) + 1]) - (D[2] * t0 + D[3] * t1);
             if (li + 1 < g.tx && gi + 1 < g.nx) {
                 double T[4]; mm2(D, P + 8, T);
                 M[0] = -T[0]; M[1] = -T[1]; M[2] = -T[2]; M[3] = -T[3];
@@ -388,8 +401,11 @@ void ilu_setup(Ctx &c, const double *)
         TSP_CUDA(cudaStreamSynchronize(c.s));
     }
     // per handle (the attribute is per device; tsp_setup runs on the handle's device)
-    TSP_CUDA(cudaFuncSetAttribute(k_ilu_apply2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    TSP_CUDA(cudaFuncSetAttribute(k_ilu_apply2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    TSP_CUDA(cudaFuncSetAttribute(k_ilu_apply2<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    TSP_CUDA(cudaFuncSetAttribute(k_ilu_apply2<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    TSP_CUDA(cudaFuncSetAttribute(k_ilu_apply2<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    TSP_CUDA(cudaFuncSetAttribute(k_ilu_apply2<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    c.ilu_eis = getenv("TSP_ILU_PLAIN_RESID") == nullptr;       // read per setup: slot 3 then holds E = S_KK - U_KK
     c.ntx = g.ntx; c.nty = g.nty; c.ntz = g.ntz;
     c.ntiles = g.ntx * g.nty * g.ntz;
     const size_t per_tile = (size_t)g.tz * g.ty * g.W;
@@ -400,7 +416,7 @@ void ilu_setup(Ctx &c, const double *)
     if (c.Nc) k_ilu_fill<<<grid_for(c.Nc, 256), 256, 0, c.s>>>(g, c.ny, c.ff.rp, c.ff.gci.p ? c.ff.gci.p : c.ff.ci.p, c.ff.v, c.fs_eff,
                                                              c.ilu_val);
     c.dcount.zero(c.s);
-    k_ilu_factor<<<c.ntiles, 32, 0, c.s>>>(g, c.ilu_cells, c.ilu_lvlptr, c.ilu_val, c.ilu_dinv, c.dcount, c.o.second_stage == 1);
+    k_ilu_factor<<<c.ntiles, 32, 0, c.s>>>(g, c.ilu_cells, c.ilu_lvlptr, c.ilu_val, c.ilu_dinv, c.dcount, c.o.second_stage == 1, c.ilu_eis);
     TSP_CUDA(cudaGetLastError());
     unsigned long long np = 0;
     TSP_CUDA(cudaMemcpyAsync(&np, c.dcount, sizeof(np), cudaMemcpyDeviceToHost, c.s));
@@ -417,7 +433,8 @@ void ilu_apply_fused(Ctx &c, const double *yf, const double *zs, const double *z
     const double *zs_gh = c.gh_f2.p, *zp_gh = c.gh_f2.p ? c.gh_f2.p + c.hf.nghost() : nullptr;
     prof_begin(c, PK_ILU);
     if (c.ntiles)
-        (c.o.second_stage == 1 ? k_ilu_apply2<true> : k_ilu_apply2<false>)<<<c.ntiles, 256, smem, c.s>>>(
+        (c.o.second_stage == 1 ? (c.ilu_eis ? k_ilu_apply2<true, true> : k_ilu_apply2<true, false>)
+                               : (c.ilu_eis ? k_ilu_apply2<false, true> : k_ilu_apply2<false, false>))<<<c.ntiles, 256, smem, c.s>>>(
             g, c.ilu_cells, c.ilu_lvlptr, c.ilu_val, c.ilu_dinv, yf, zs, zp, zs_gh, zp_gh, zf_out);
     prof_end(c, PK_ILU, (28.0 * 8 + 32 + 16 + 16 + 16) * c.Nc);
     c.launches += 1;

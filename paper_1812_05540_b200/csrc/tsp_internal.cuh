@@ -330,6 +330,7 @@ struct Ctx {
     Sell s_aps;                   // A_ps values on A_ff's pattern (bs 1)
     DBuf<double> ilu_val;         // tile-level-major S_ff^FS blocks, 7 slots x 4 (R-ilu)
     DBuf<double> ilu_dinv;        // tile-level-major U_KK^-1, 4 per cell
+    bool ilu_eis = true;          // slot 3 of ilu_val holds E = S_KK - U_KK (ilu.cu, Eisenstat form of steps 6-8)
     DBuf<int32_t> ilu_lvlptr;     // level pointers of the full-tile table
     DBuf<int32_t> ilu_cells;      // local (i,j,k) packed per table position
     DBuf<int32_t> ilu_posmap;     // local linear index -> table position

@@ -367,6 +367,35 @@ def test_cuda_graph_iterations_are_bitwise_the_eager_ones(dev):
     assert np.array_equal(xs[0][0], xs[1][0]) and np.array_equal(xs[0][0], xs[2][0])
 
 
+@pytest.mark.parametrize("opts", [{}, {"second_stage": 1}, {"local_sweeps": 2}])
+def test_ilu_eisenstat_form_equals_plain_residual(dev, opts):
+    """ilu.cu computes M_L^-1 (y_f - S^FS z_f) as (I + D^-1 U)^-1 [(D + L)^-1 (y - E z - U z - C z) - z] (the in-tile
+    lower blocks streamed once); TSP_ILU_PLAIN_RESID keeps w = y - S z followed by the two sweeps (P:629-634 as
+    written).  Same operator: one application agrees to rounding on a ragged multi-tile grid, both with the oracle."""
+    import os
+    from paper_1812_05540_b200 import Tsp
+    pb = _problem("R1")
+    v = np.random.default_rng(11).uniform(-1, 1, pb.n)
+    zs = []
+    for plain in (False, True):
+        if plain:
+            os.environ["TSP_ILU_PLAIN_RESID"] = "1"
+        try:
+            g = Tsp(pb, **opts).setup()
+        finally:
+            os.environ.pop("TSP_ILU_PLAIN_RESID", None)
+        z = torch.empty(pb.n, dtype=torch.float64, device=dev)
+        g.apply_preconditioner(_cuda(v), z)
+        torch.cuda.synchronize()
+        zs.append(z.cpu().numpy())
+        g.close()
+    ref = oracle.Oracle(pb, **opts).setup().apply(v)
+    nf = np.linalg.norm(ref[3 * pb.Nn:])
+    assert np.linalg.norm((zs[0] - zs[1])[3 * pb.Nn:]) <= 1e-12 * nf
+    assert np.linalg.norm((zs[0] - ref)[3 * pb.Nn:]) <= 1e-10 * nf
+    assert np.linalg.norm((zs[1] - ref)[3 * pb.Nn:]) <= 1e-10 * nf
+
+
 def test_solve_edge_cases(dev):
     """tsp_solve semantics (include/tsp.h): max_iters = 0 reports x0's true residual; b = 0 gives x = 0 at once;
     a non-zero x0 (x0_zero = False) converges to the same solution; restart > 120 is clamped."""
